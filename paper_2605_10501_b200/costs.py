@@ -1,0 +1,117 @@
+"""Cost model knobs that feed the device 6-tuple kernel (K1).
+
+The reference derives per-sample 6-tuples from a roofline-style estimator
+(``maestro/costs.py:105-200``) and sums them per side in ``derive_batch``
+(``costs.py:230-299``).  Here the same arithmetic runs on the device, one
+thread per sample, from the per-sample token counts of the step
+(``csrc/plan.cu: plan_sample_times_kernel``).  This module holds the host-side
+parameter objects and lowers them to the flat per-submodule cost table the
+kernel reads.  The host only precomputes the per-section constant
+``effective = peak * tp * cp * efficiency`` in exactly the reference's
+left-to-right order, so the device result is bit-identical.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Mapping
+
+import numpy as np
+
+from .errors import InvalidConfig, InvalidDims
+from .workload import SectionConfig, SectionGraph, SectionSpec
+
+
+@dataclass(frozen=True)
+class CostParams:
+    """Time/memory model knobs of one section (costs.py:30-68)."""
+
+    flops_per_token_fwd: float
+    peak_flops_per_gpu: float
+    bwd_fwd_ratio: float = 2.0
+    parallel_efficiency: Mapping[tuple[int, int, int], float] = field(default_factory=dict)
+    mbs_efficiency: Mapping[int, float] = field(default_factory=dict)
+    bytes_per_param_weights: float = 2.0
+    bytes_per_param_optimizer: float = 12.0
+    activation_bytes_per_token: float = 0.0
+    live_microbatch_cap: float = 4.0
+
+    def __post_init__(self) -> None:
+        if self.flops_per_token_fwd <= 0 or self.peak_flops_per_gpu <= 0:
+            raise InvalidDims("flops_per_token_fwd and peak_flops_per_gpu must be positive")
+        if self.bwd_fwd_ratio <= 0:
+            raise InvalidDims("bwd_fwd_ratio must be positive")
+        if self.parallel_efficiency.get((1, 1, 1), 1.0) != 1.0:
+            raise InvalidDims("parallel_efficiency(1,1,1) must be 1")
+        for eff in list(self.parallel_efficiency.values()) + list(self.mbs_efficiency.values()):
+            if not 0 < eff <= 1:
+                raise InvalidDims("efficiencies must lie in (0,1]")
+
+    def efficiency(self, config: SectionConfig) -> float:
+        par = self.parallel_efficiency.get((config.tp, config.pp, config.cp), 1.0)
+        return par * self.mbs_efficiency.get(config.mbs, 1.0)
+
+
+def check_config(section: SectionSpec, config: SectionConfig) -> None:
+    if not config.divides(section.structural):
+        s = section.structural
+        raise InvalidConfig(
+            f"config tp={config.tp} pp={config.pp} cp={config.cp} does not divide section "
+            f"'{section.id}' structural params (heads={s.num_heads}, layers={s.num_layers}, "
+            f"seq={s.max_seq_len})",
+            section=section.id,
+        )
+
+
+def effective_rate(config: SectionConfig, params: CostParams) -> float:
+    """``peak * tp * cp * efficiency`` with the reference's evaluation order (costs.py:121)."""
+    return params.peak_flops_per_gpu * config.tp * config.cp * params.efficiency(config)
+
+
+def per_sample_times(section, config, params, tokens_per_sample, samples_per_rank):
+    """Host twin of the device K1 arithmetic (costs.py:105-123, 182-200)."""
+    if samples_per_rank <= 0:
+        return 0.0, 0.0
+    check_config(section, config)
+    if tokens_per_sample <= 0:
+        raise InvalidDims("tokens_per_sample must be positive")
+    fwd = (config.mbs * tokens_per_sample * params.flops_per_token_fwd) / effective_rate(config, params)
+    bwd = 0.0 if section.forward_only else fwd * params.bwd_fwd_ratio
+    m = math.ceil(samples_per_rank / config.mbs)
+    scale = (m + config.pp - 1) / (m * config.pp * config.mbs)
+    return fwd * scale, bwd * scale
+
+
+# Row layout of the device cost table, one row per submodule bit (float64).
+COST_COLS = ("flops_per_token_fwd", "effective", "bwd_fwd_ratio", "forward_only", "mbs", "pp", "dp", "owner")
+
+
+def cost_table(graph: SectionGraph, configs: Mapping[str, SectionConfig],
+               params_by_section: Mapping[str, CostParams],
+               params_by_submodule: Mapping[str, CostParams] | None = None) -> np.ndarray:
+    """Lower cost knobs to a ``[n_bits, 8]`` float64 table indexed by submodule bit.
+
+    Merged exclusive encoders keep one config but may carry per-submodule
+    ``CostParams`` (``params_by_submodule``), since a sample's time in the
+    merged section is whichever submodule it activates (workload.py:520-523).
+    """
+    tab = graph.tables
+    out = np.zeros((len(tab.sub_names), len(COST_COLS)), dtype=np.float64)
+    for bit, name in enumerate(tab.sub_names):
+        owner = tab.sub_owner[bit]
+        sid = tab.section_ids[owner]
+        spec, cfg = graph.section(sid), configs[sid]
+        params = (params_by_submodule or {}).get(name) or params_by_section[sid]
+        check_config(spec, cfg)
+        out[bit] = (
+            params.flops_per_token_fwd,
+            effective_rate(cfg, params),
+            params.bwd_fwd_ratio,
+            1.0 if spec.forward_only else 0.0,
+            cfg.mbs,
+            cfg.pp,
+            cfg.dp,
+            owner,
+        )
+    return out
