@@ -1,0 +1,141 @@
+/*
+ * maestro_b200.h -- C ABI of the B200-native section-graph executor hot path.
+ *
+ * Plain pointers and sizes only (no torch types).  Every pointer named d_* is
+ * device memory; `stream` is a cudaStream_t passed as void*.  Every call is
+ * stream-ordered, never allocates, never synchronises, and returns 0 or a
+ * CUDA error code (launch failure).  Domain errors found on the device (the
+ * reference's exceptions) are folded into one device error word
+ * `int64 d_err` = min over errors of (priority << 32 | code << 24 | index),
+ * INT64_MAX when clean (maestro_error_reset).  Priority reproduces the
+ * reference's raise order: sample construction (K1, by batch index) before
+ * duplicate ids before activation errors (by LPT position) before fan-out
+ * violations (by merge order).  The host shim decodes the word into the
+ * reference's exception classes (MAESTRO_E_* map 1:1 to maestro/errors.py;
+ * see paper_2605_10501_b200/errors.py DEVICE_CODES).
+ *
+ * The reference has no C/C++ interface: its boundary is a set of Python
+ * functions (/root/reference/pkg/src/maestro/scheduling.py, workload.py,
+ * simulator.py, mq.py).  Each entry point below names the reference function
+ * it replaces; INTEGRATION.md shows the ctypes binding a maintainer would add.
+ */
+#ifndef MAESTRO_B200_H
+#define MAESTRO_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MAESTRO_MAX_SECTIONS 16
+#define MAESTRO_MAX_BITS 32
+#define MAESTRO_MAX_DP 64
+#define MAESTRO_MAX_BATCH 4096      /* per step (partition stages it in smem) */
+#define MAESTRO_MAX_RANK_SAMPLES 1023 /* per critical rank (one thread per insertion slot) */
+
+/* device error codes (errors.py class per code) */
+#define MAESTRO_E_OK 0
+#define MAESTRO_E_NEGATIVE_TIME 1       /* NegativeTime         workload.py:164-177 */
+#define MAESTRO_E_BOTH_ACTIVATED 2      /* BothActivated        workload.py:310-316 */
+#define MAESTRO_E_ACTIVATION 3          /* ActivationError      workload.py:323-328,351-355 */
+#define MAESTRO_E_INVALID_DIMS 4        /* InvalidDims          costs.py:116-117 */
+#define MAESTRO_E_FANOUT_MISMATCH 5     /* FanoutMismatch       scheduling.py:219,275-279 */
+#define MAESTRO_E_EMPTY_BATCH 6         /* EmptyBatch           scheduling.py:217,324 */
+#define MAESTRO_E_INCONSISTENT 7        /* InconsistentSchedule scheduling.py:327 */
+#define MAESTRO_E_FANOUT_VIOLATION 8    /* FanoutViolation      scheduling.py:361-365 */
+
+#define MAESTRO_POLICY_INTERLEAVED 0      /* ExecPolicy.INTERLEAVED      scheduling.py:42 */
+#define MAESTRO_POLICY_ALL_FWD_THEN_BWD 1 /* ExecPolicy.ALL_FWD_THEN_BWD scheduling.py:43 */
+
+/* Lowered section graph (SectionGraph.tables in workload.py mirror). */
+typedef struct {
+  int32_t n_sections;
+  int32_t n_bits;                              /* submodule names, sorted; bit b = name b */
+  int32_t critical;                            /* section index of the critical section */
+  int32_t n_up, n_down;                        /* candidate auxiliaries per side */
+  int32_t n_aux;                               /* auxiliaries in merge order */
+  int32_t sub_owner[MAESTRO_MAX_BITS];         /* bit -> owning section */
+  int32_t side[MAESTRO_MAX_SECTIONS];          /* 0 upstream, 1 critical, 2 downstream */
+  int32_t up_cand[MAESTRO_MAX_SECTIONS];
+  int32_t down_cand[MAESTRO_MAX_SECTIONS];
+  int32_t neighbor[MAESTRO_MAX_SECTIONS];      /* toward-critical hop, -1 for critical */
+  int32_t merge_order[MAESTRO_MAX_SECTIONS];   /* auxiliaries by (hops, id) */
+  int32_t dp[MAESTRO_MAX_SECTIONS];
+  int32_t fanout[MAESTRO_MAX_SECTIONS];
+  int32_t mbs[MAESTRO_MAX_SECTIONS];
+  uint32_t sec_bits[MAESTRO_MAX_SECTIONS];     /* submodule bits owned by each section */
+  int32_t crit_bit;                            /* bit of the critical section's own id */
+} maestro_graph_t;
+
+/* Reset a device error word to "no error" (INT64_MAX). */
+int maestro_error_reset(int64_t* d_err, void* stream);
+
+/* K1 -- per-sample 6-tuples from token counts (costs.py:105-123,182-200 summed per side as
+ * derive_batch does, costs.py:276-286).  d_tokens[n_bits][B] = tokens the sample occupies
+ * in submodule b (0 = not activated; the critical section's id bit carries its length).
+ * d_cost[n_bits][8] rows = (flops_per_token_fwd, effective_rate, bwd_fwd_ratio,
+ * forward_only, mbs, pp, dp, owner).  Outputs phase-major d_times[6][B] and the
+ * activation bitmask d_act[B] (non-critical bits with tokens > 0). */
+int maestro_sample_times(const maestro_graph_t* g, const double* d_cost, const int32_t* d_tokens,
+                         int32_t B, double* d_times, uint32_t* d_act, int64_t* d_err, void* stream);
+
+/* K2 -- activation resolution (workload.py:297-355) + partition_batch (scheduling.py:202-264).
+ * Outputs: d_up/d_down[B] resolved section or -1; d_lpt[B] LPT order; d_part[B] the
+ * per-rank lists in assignment order, rank r at d_part_off[r] .. d_part_off[r+1]. */
+int maestro_partition(const maestro_graph_t* g, const double* d_times, const int32_t* d_ids,
+                      const uint32_t* d_act, int32_t B, int32_t* d_up, int32_t* d_down,
+                      int32_t* d_lpt, int32_t* d_part, int32_t* d_part_off, int64_t* d_err,
+                      void* stream);
+
+/* K3 -- schedule_rank (scheduling.py:162-199) for every critical rank, one CTA per rank.
+ * d_orders[B] receives the per-rank orders at the same offsets as d_part.  d_metrics[3*dp]
+ * = (makespan, critical_busy, critical_span) of each final order (rank_metrics,
+ * scheduling.py:81-152); d_evals[dp] = calculate_makespan evaluations (EvalCounter). */
+int maestro_wavefront(const double* d_times, int32_t B, const int32_t* d_part,
+                      const int32_t* d_part_off, int32_t dp, int32_t policy, int32_t* d_orders,
+                      double* d_metrics, int64_t* d_evals, void* stream);
+
+/* rank_metrics (scheduling.py:81-152) of one given order: d_out[3] = (makespan,
+ * critical_busy, critical_span).  Also serves calculate_makespan (scheduling.py:155-159). */
+int maestro_rank_metrics(const double* d_times, int32_t B, const int32_t* d_order, int32_t n,
+                         int32_t policy, double* d_out, void* stream);
+
+/* K4 -- build_schedule's auxiliary pass (scheduling.py:347-371): for each auxiliary in
+ * merge order, rank q's order = merge_fanout (scheduling.py:267-285) of its neighbour's
+ * ranks [q*f, (q+1)*f) filtered to activating samples.  d_orders[n_sections][B],
+ * d_sec_off[n_sections][MAESTRO_MAX_DP+1]; the critical slots must already hold K3's
+ * output (maestro_build_schedule does that). */
+int maestro_fanout_merge(const maestro_graph_t* g, int32_t B, const int32_t* d_up,
+                         const int32_t* d_down, int32_t* d_orders, int32_t* d_sec_off,
+                         int64_t* d_err, void* stream);
+
+/* K1..K4 in one stream-ordered call: build_schedule (scheduling.py:309-373) from
+ * 6-tuples.  d_work must hold maestro_schedule_workspace(B, dp) bytes. */
+int64_t maestro_schedule_workspace(int32_t B, int32_t dp_critical);
+int maestro_build_schedule(const maestro_graph_t* g, const double* d_times, const int32_t* d_ids,
+                           const uint32_t* d_act, int32_t B, int32_t policy, int32_t* d_orders,
+                           int32_t* d_sec_off, double* d_metrics, int64_t* d_evals, void* d_work,
+                           int64_t* d_err, void* stream);
+
+/* K5 -- varlen pack of one section rank's order (not in the reference):
+ * consecutive groups of `mbs` samples form micro-batches; d_mb[k] = k / mbs,
+ * d_tok_off[k] = token offset of order[k] inside its micro-batch's packed stream,
+ * d_mb_tokens[m] = tokens of micro-batch m, d_cu[m*(mbs+1) + j] = cu_seqlens.
+ * d_len[B] = sequence length per batch index. */
+int maestro_varlen_pack(const int32_t* d_order, int32_t n, const int32_t* d_len, int32_t mbs,
+                        int32_t* d_mb, int32_t* d_tok_off, int32_t* d_mb_tokens, int32_t* d_cu,
+                        void* stream);
+
+/* K6 -- row scatter of encoder outputs into the packed token stream and its backward.
+ * fwd: dst[dst_row[k], :] = src[src_row[k], :]  (bf16, d multiple of 8)
+ * bwd: dsrc[r, :] = sum over k in seg[r]..seg[r+1] of ddst[seg_dst[k], :] (fp32 accumulate). */
+int maestro_scatter_rows_fwd(const void* d_src, void* d_dst, const int32_t* d_src_row,
+                             const int32_t* d_dst_row, int32_t n_rows, int32_t d, void* stream);
+int maestro_gather_rows_bwd(const void* d_ddst, void* d_dsrc, const int32_t* d_seg,
+                            const int32_t* d_seg_dst, int32_t n_src_rows, int32_t d, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,30 @@
+// Shared device helpers for the maestro_b200 kernels (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "maestro_b200.h"
+
+#define MAESTRO_API extern "C" __attribute__((visibility("default")))
+
+namespace mb {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// splitmix64 finaliser; must match paper_2605_10501_b200/synthetic.py
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// Fold one domain error into the device error word (min = earliest in reference raise order).
+__device__ __forceinline__ void report(int64_t* err, uint32_t prio, int code, int index) {
+  if (err == nullptr) return;
+  long long key = ((long long)prio << 32) | ((long long)(code & 0xff) << 24) | (long long)(index & 0xffffff);
+  atomicMin(reinterpret_cast<long long*>(err), key);
+}
+
+inline int launch_status() { return (int)cudaGetLastError(); }
+
+}  // namespace mb

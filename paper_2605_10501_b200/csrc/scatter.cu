@@ -1,0 +1,93 @@
+// K6: encoder outputs -> packed backbone token stream at placeholder rows, and its backward.
+//
+// Not in the reference (4:1 downsampled visual tokens concatenated with
+// text).  HBM-bound row movement: one warp per row, 16-byte vectors, several rows in
+// flight per warp; the backward is a segmented gather-reduce in fp32 (a 1:1 placeholder map
+// degenerates to a copy but the kernel accepts any CSR segment structure).
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+
+namespace mb {
+namespace {
+
+constexpr int kRowsPerWarp = 4;
+
+__global__ void __launch_bounds__(256) scatter_rows_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                                           const int32_t* __restrict__ src_row,
+                                                           const int32_t* __restrict__ dst_row, int n_rows,
+                                                           int vec_per_row) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int r0 = warp * kRowsPerWarp;
+#pragma unroll
+  for (int k = 0; k < kRowsPerWarp; ++k) {
+    const int r = r0 + k;
+    if (r >= n_rows) return;
+    const uint4* s = src + (size_t)src_row[r] * vec_per_row;
+    uint4* d = dst + (size_t)dst_row[r] * vec_per_row;
+    for (int v = lane; v < vec_per_row; v += 32) {
+      uint4 x;
+      asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w)
+                   : "l"(s + v));
+      d[v] = x;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) gather_rows_bwd_kernel(const __nv_bfloat16* __restrict__ ddst,
+                                                              __nv_bfloat16* __restrict__ dsrc,
+                                                              const int32_t* __restrict__ seg,
+                                                              const int32_t* __restrict__ seg_dst, int n_src,
+                                                              int d) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= n_src) return;
+  const int k0 = seg[warp], k1 = seg[warp + 1];
+  __nv_bfloat16* out = dsrc + (size_t)warp * d;
+  for (int c = lane * 8; c < d; c += 32 * 8) {
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int k = k0; k < k1; ++k) {
+      const uint4 v = *reinterpret_cast<const uint4*>(ddst + (size_t)seg_dst[k] * d + c);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(h[j]);
+        acc[2 * j] += f.x;
+        acc[2 * j + 1] += f.y;
+      }
+    }
+    uint4 o;
+    __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) oh[j] = __floats2bfloat162_rn(acc[2 * j], acc[2 * j + 1]);
+    *reinterpret_cast<uint4*>(out + c) = o;
+  }
+}
+
+}  // namespace
+}  // namespace mb
+
+using namespace mb;
+
+MAESTRO_API int maestro_scatter_rows_fwd(const void* d_src, void* d_dst, const int32_t* d_src_row,
+                                         const int32_t* d_dst_row, int32_t n_rows, int32_t d, void* stream) {
+  if (n_rows <= 0) return 0;
+  if (d % 8) return (int)cudaErrorInvalidValue;
+  const int warps = (n_rows + kRowsPerWarp - 1) / kRowsPerWarp;
+  const int blocks = (warps * 32 + 255) / 256;
+  scatter_rows_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>((const uint4*)d_src, (uint4*)d_dst, d_src_row,
+                                                                d_dst_row, n_rows, d / 8);
+  return launch_status();
+}
+
+MAESTRO_API int maestro_gather_rows_bwd(const void* d_ddst, void* d_dsrc, const int32_t* d_seg,
+                                        const int32_t* d_seg_dst, int32_t n_src_rows, int32_t d, void* stream) {
+  if (n_src_rows <= 0) return 0;
+  if (d % 8) return (int)cudaErrorInvalidValue;
+  const int blocks = (n_src_rows * 32 + 255) / 256;
+  gather_rows_bwd_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+      (const __nv_bfloat16*)d_ddst, (__nv_bfloat16*)d_dsrc, d_seg, d_seg_dst, n_src_rows, d);
+  return launch_status();
+}
