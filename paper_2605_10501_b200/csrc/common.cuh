@@ -27,4 +27,16 @@ __device__ __forceinline__ void report(int64_t* err, uint32_t prio, int code, in
 
 inline int launch_status() { return (int)cudaGetLastError(); }
 
+// Raise a kernel's dynamic shared-memory limit to `bytes` if needed (idempotent, cached
+// per kernel).  Returns nonzero on failure (the error stays queued for launch_status()).
+template <auto KERNEL>
+inline int ensure_smem(size_t bytes) {
+  static size_t configured = 0;  // one instance per kernel
+  if (bytes <= 48 * 1024 || bytes <= configured) return 0;
+  cudaError_t e = cudaFuncSetAttribute(KERNEL, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) return (int)e;
+  configured = bytes;
+  return 0;
+}
+
 }  // namespace mb

@@ -739,11 +739,7 @@ MAESTRO_API int maestro_partition(const maestro_graph_t* g, const double* d_time
   const int dp = g->dp[g->critical];
   if (dp < 1 || dp > MAESTRO_MAX_DP) return (int)cudaErrorInvalidValue;
   const size_t smem = partition_smem(B);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(partition_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
+  if (ensure_smem<partition_kernel>(smem)) return launch_status();
   partition_kernel<<<1, 1024, smem, (cudaStream_t)stream>>>(*g, d_times, d_ids, d_act, B, d_up, d_down, d_lpt,
                                                             d_part, d_part_off, d_err);
   return launch_status();
@@ -758,12 +754,7 @@ MAESTRO_API int maestro_wavefront(const double* d_times, int32_t B, const int32_
   if (max_n > MAESTRO_MAX_RANK_SAMPLES) return (int)cudaErrorInvalidValue;
   const int threads = wavefront_threads(max_n);
   const size_t smem = wavefront_smem(threads);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(wavefront_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(wavefront_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
+  if (ensure_smem<wavefront_kernel<0>>(smem) || ensure_smem<wavefront_kernel<1>>(smem)) return launch_status();
   if (policy == MAESTRO_POLICY_INTERLEAVED)
     wavefront_kernel<0><<<dp, threads, smem, (cudaStream_t)stream>>>(d_times, B, d_part, d_part_off, d_orders,
                                                                       d_metrics, d_evals);
