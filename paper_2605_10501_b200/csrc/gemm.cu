@@ -1,0 +1,264 @@
+// K7: persistent warp-specialised tcgen05 GEMM for the dense section compute.
+//
+//   C[m, n] (+)= sum_k A(m, k) * B(n, k)      bf16 operands, fp32 accumulation in TMEM
+//
+// A and B are each K-major (row-major [rows][K]) or MN-major ([K][rows]), which covers the
+// three training GEMMs without transposes:  fwd  Y = X W^T      (A K-major,  B K-major)
+//                                            dgrad dX = dY W     (A K-major,  B MN-major)
+//                                            wgrad dW = dY^T X   (A MN-major, B MN-major)
+// Tile 128 x 256 x 64, 4-stage TMA ring (SWIZZLE_128B), one elected thread issues
+// tcgen05.mma (M=128, N=256, K=16) into a double-buffered TMEM accumulator (2 x 256 of the
+// 512 columns), four epilogue warps drain TMEM (tcgen05.ld) while the next tile's MMAs run.
+// Grid = min(tiles, #SMs); tiles are visited in grouped-M raster order for L2 reuse.
+//
+// Warp roles (192 threads): w0 TMA producer, w1 MMA issuer + TMEM owner, w2..w5 epilogue.
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+#include "sm100.cuh"
+#include "tma_host.cuh"
+
+namespace mb {
+namespace {
+
+using namespace sm100;
+
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;  // 16 KB
+constexpr int B_BYTES = BN * BK * 2;  // 32 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int GROUP_M = 8;
+constexpr int THREADS = 192;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+
+enum Epi { EPI_BF16 = 0, EPI_F32 = 1, EPI_F32_ACC = 2 };
+
+struct TileSched {
+  int num_m, num_n;
+  __device__ __forceinline__ void coords(int t, int& m, int& n) const {
+    const int per_group = GROUP_M * num_n;
+    const int g = t / per_group;
+    const int first_m = g * GROUP_M;
+    const int gsize = min(GROUP_M, num_m - first_m);
+    const int r = t - g * per_group;
+    m = first_m + r % gsize;
+    n = r / gsize;
+  }
+};
+
+template <bool A_MN, bool B_MN, int EPI>
+__global__ void __launch_bounds__(THREADS, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, void* C,
+                int M, int N, int K, int ldc) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 1024-byte alignment for SWIZZLE_128B atoms
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* sA = smem;
+  unsigned char* sB = smem + STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const TileSched sched{(M + BM - 1) / BM, (N + BN - 1) / BN};
+  const int num_tiles = sched.num_m * sched.num_n;
+  const int num_kb = (K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&map_a);
+    tma_prefetch(&map_b);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer
+      int s = 0;
+      uint32_t ph = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int mb_, nb_;
+        sched.coords(t, mb_, nb_);
+        const int m0 = mb_ * BM, n0 = nb_ * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+          const int k0 = kb * BK;
+          unsigned char* a = sA + s * A_BYTES;
+          unsigned char* b = sB + s * B_BYTES;
+          if (!A_MN) {
+            tma_load_2d(a, &map_a, &full[s], k0, m0);
+          } else {
+            tma_load_2d(a, &map_a, &full[s], m0, k0);
+            tma_load_2d(a + 8192, &map_a, &full[s], m0 + 64, k0);
+          }
+          if (!B_MN) {
+            tma_load_2d(b, &map_b, &full[s], k0, n0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) tma_load_2d(b + 8192 * j, &map_b, &full[s], n0 + 64 * j, k0);
+          }
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer
+      constexpr uint32_t idesc = idesc_bf16_f32(BM, BN, A_MN, B_MN);
+      int s = 0;
+      uint32_t ph = 0;
+      int local = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+        const int as = local & 1;
+        const uint32_t aph = (local >> 1) & 1;
+        mbar_wait(&tempty[as], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + as * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(sA + s * A_BYTES);
+          const uint32_t b_base = smem_u32(sB + s * B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            // K-major: +32 B per 16-element K step inside the 128 B swizzle row;
+            // MN-major: +16 K-rows of 128 B.
+            const uint64_t ad = A_MN ? smem_desc_sw128(a_base + k * 2048, 8192, 1024)
+                                     : smem_desc_sw128(a_base + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? smem_desc_sw128(b_base + k * 2048, 8192, 1024)
+                                     : smem_desc_sw128(b_base + k * 32, 16, 1024);
+            umma_bf16(d, ad, bd, idesc, (kb | k) != 0);
+          }
+          umma_commit(&empty[s]);  // smem slot free once these MMAs retire
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        umma_commit(&tfull[as]);  // accumulator ready for the epilogue
+      }
+    }
+  } else {
+    // ---------------- epilogue: TMEM -> registers -> global
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    int local = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+      int mb_, nb_;
+      sched.coords(t, mb_, nb_);
+      const int as = local & 1;
+      const uint32_t aph = (local >> 1) & 1;
+      mbar_wait(&tfull[as], aph);
+      tc_fence_after();
+      const int row = mb_ * BM + q * 32 + lane;
+      const int n0 = nb_ * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + as * BN + c, r);
+        tmem_ld_wait();
+        const int col = n0 + c;
+        if (row >= M || col >= N) continue;
+        const bool full_chunk = col + 32 <= N;
+        if (EPI == EPI_BF16) {
+          __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(C) + (size_t)row * ldc + col;
+          uint32_t p[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) p[j] = pack_bf16(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+          const int nvec = full_chunk ? 4 : (N - col) / 8;
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (j < nvec)
+              reinterpret_cast<uint4*>(out)[j] = make_uint4(p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]);
+        } else {
+          float* out = reinterpret_cast<float*>(C) + (size_t)row * ldc + col;
+          const int nv = full_chunk ? 8 : (N - col) / 4;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (j >= nv) break;
+            float4 v = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                   __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+            if (EPI == EPI_F32_ACC) {
+              const float4 o = reinterpret_cast<const float4*>(out)[j];
+              v.x += o.x;
+              v.y += o.y;
+              v.z += o.z;
+              v.w += o.w;
+            }
+            reinterpret_cast<float4*>(out)[j] = v;
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[as]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+template <bool A_MN, bool B_MN, int EPI>
+int launch(const CUtensorMap& ma, const CUtensorMap& mbm, void* C, int M, int N, int K, int ldc, cudaStream_t st) {
+  auto kern = gemm_kernel<A_MN, B_MN, EPI>;
+  if (ensure_smem<gemm_kernel<A_MN, B_MN, EPI>>(SMEM_BYTES)) return launch_status();
+  const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  kern<<<grid, THREADS, SMEM_BYTES, st>>>(ma, mbm, C, M, N, K, ldc);
+  return launch_status();
+}
+
+}  // namespace
+}  // namespace mb
+
+using namespace mb;
+
+// C[m, n] (+)= sum_k A(m,k) B(n,k).  A(m,k) = A[m*lda + k] (a_mn=0) or A[k*lda + m] (a_mn=1);
+// likewise B.  epi: 0 = store bf16, 1 = store fp32, 2 = accumulate into fp32 C.
+MAESTRO_API int maestro_gemm_bf16(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K,
+                                  int32_t lda, int32_t ldb, int32_t ldc, int32_t a_mn, int32_t b_mn, int32_t epi,
+                                  void* stream) {
+  if (M <= 0 || N <= 0 || K <= 0) return (int)cudaErrorInvalidValue;
+  if ((lda % 8) || (ldb % 8) || (N % 8) || (ldc % 8)) return (int)cudaErrorInvalidValue;
+  CUtensorMap ma, mbm;
+  bool ok = a_mn ? make_map_2d(&ma, A, M, K, lda, 64, 64) : make_map_2d(&ma, A, K, M, lda, 64, 128);
+  ok = ok && (b_mn ? make_map_2d(&mbm, B, N, K, ldb, 64, 64) : make_map_2d(&mbm, B, K, N, ldb, 64, 256));
+  if (!ok) return (int)cudaErrorInvalidValue;
+  cudaStream_t st = (cudaStream_t)stream;
+#define MB_GEMM_CASE(AM, BMN, E) \
+  if (a_mn == AM && b_mn == BMN && epi == E) return launch<AM, BMN, E>(ma, mbm, C, M, N, K, ldc, st);
+  MB_GEMM_CASE(0, 0, 0)
+  MB_GEMM_CASE(0, 0, 1)
+  MB_GEMM_CASE(0, 0, 2)
+  MB_GEMM_CASE(0, 1, 0)
+  MB_GEMM_CASE(0, 1, 1)
+  MB_GEMM_CASE(0, 1, 2)
+  MB_GEMM_CASE(1, 1, 0)
+  MB_GEMM_CASE(1, 1, 1)
+  MB_GEMM_CASE(1, 1, 2)
+  MB_GEMM_CASE(1, 0, 0)
+  MB_GEMM_CASE(1, 0, 1)
+  MB_GEMM_CASE(1, 0, 2)
+#undef MB_GEMM_CASE
+  return (int)cudaErrorInvalidValue;
+}

@@ -1,0 +1,69 @@
+"""Host wrappers of the tcgen05 GEMM (K7, csrc/gemm.cu) for the three training GEMMs.
+
+All tensors are torch CUDA tensors (bf16 operands; fp32 or bf16 outputs).  No
+autograd and no cuBLAS: the section compute calls these directly with explicit
+forward / dgrad / wgrad.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _native as N
+
+EPI_BF16, EPI_F32, EPI_F32_ACC = 0, 1, 2
+
+_bound = False
+
+
+def _lib():
+    global _bound
+    L = N.lib()
+    if not _bound:
+        I32, P = ctypes.c_int32, ctypes.c_void_p
+        N.extra_symbols({"maestro_gemm_bf16": ([P, P, P, I32, I32, I32, I32, I32, I32, I32, I32, I32, P], ctypes.c_int)})
+        _bound = True
+    return L
+
+
+def gemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, M: int, N_: int, K: int, a_mn: bool, b_mn: bool,
+         epi: int, lda: int | None = None, ldb: int | None = None, ldc: int | None = None) -> torch.Tensor:
+    """c[m, n] (+)= sum_k A(m,k) B(n,k); see include/maestro_b200.h (maestro_gemm_bf16)."""
+    if lda is None:
+        lda = a.stride(0)
+    if ldb is None:
+        ldb = b.stride(0)
+    if ldc is None:
+        ldc = c.stride(0)
+    rc = _lib().maestro_gemm_bf16(N.ptr(a), N.ptr(b), N.ptr(c), M, N_, K, lda, ldb, ldc, int(a_mn), int(b_mn),
+                                  epi, N.stream_ptr())
+    N.check(rc, "gemm_bf16")
+    return c
+
+
+def linear_fwd(x: torch.Tensor, w: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """y[T, out] = x[T, in] @ w[out, in]^T."""
+    T, K = x.shape
+    Nn = w.shape[0]
+    if out is None:
+        out = torch.empty(T, Nn, device=x.device, dtype=torch.bfloat16)
+    return gemm(x, w, out, T, Nn, K, False, False, EPI_BF16)
+
+
+def linear_dgrad(dy: torch.Tensor, w: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """dx[T, in] = dy[T, out] @ w[out, in]."""
+    T, Nn = dy.shape
+    K = w.shape[1]
+    if out is None:
+        out = torch.empty(T, K, device=dy.device, dtype=torch.bfloat16)
+    return gemm(dy, w, out, T, K, Nn, False, True, EPI_BF16, ldb=w.stride(0))
+
+
+def linear_wgrad(dy: torch.Tensor, x: torch.Tensor, dw: torch.Tensor, accumulate: bool = True) -> torch.Tensor:
+    """dw[out, in] (+)= dy[T, out]^T @ x[T, in]   (dw fp32)."""
+    T, Nn = dy.shape
+    K = x.shape[1]
+    return gemm(dy, x, dw, Nn, K, T, True, True, EPI_F32_ACC if accumulate else EPI_F32,
+                lda=dy.stride(0), ldb=x.stride(0))

@@ -1,0 +1,74 @@
+"""GPU numerics of the tcgen05 GEMM (K7) against a plain PyTorch fp32 reference.
+
+Tolerance: operands are bf16; accumulation is fp32 in TMEM.  fp32 outputs must match an
+fp32 reference of the same bf16 operands to 1e-4 relative (sum-order differences only);
+bf16 outputs to one bf16 ulp-ish (2^-7 relative of max magnitude).
+"""
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [(128, 256, 64), (300, 264, 200), (1000, 768, 768), (2048, 2048, 2048), (129, 8, 1000), (4096, 5632, 2048)]
+
+
+def _rel(a, b):
+    return ((a.float() - b.float()).abs().max() / b.float().abs().max().clamp_min(1e-6)).item()
+
+
+@pytest.mark.parametrize("M,N,K", SHAPES)
+def test_fwd(M, N, K):
+    from paper_2605_10501_b200 import dense
+
+    torch.manual_seed(M + N + K)
+    x = torch.randn(M, K, device="cuda").bfloat16()
+    w = torch.randn(N, K, device="cuda").bfloat16()
+    ref = x.float() @ w.float().t()
+    y = dense.linear_fwd(x, w)
+    assert _rel(y, ref) < 8e-3
+    y32 = torch.empty(M, N, device="cuda")
+    dense.gemm(x, w, y32, M, N, K, False, False, dense.EPI_F32)
+    assert _rel(y32, ref) < 1e-4
+
+
+@pytest.mark.parametrize("M,N,K", SHAPES)
+def test_dgrad(M, N, K):
+    from paper_2605_10501_b200 import dense
+
+    torch.manual_seed(1 + M)
+    dy = torch.randn(M, N, device="cuda").bfloat16()
+    w = torch.randn(N, K, device="cuda").bfloat16()
+    if K % 8:
+        pytest.skip("K must be a multiple of 8")
+    ref = dy.float() @ w.float()
+    dx = dense.linear_dgrad(dy, w)
+    assert _rel(dx, ref) < 8e-3
+
+
+@pytest.mark.parametrize("M,N,K", SHAPES)
+def test_wgrad_accumulate(M, N, K):
+    from paper_2605_10501_b200 import dense
+
+    torch.manual_seed(2 + N)
+    if M % 8 or K % 8:
+        pytest.skip("alignment")
+    dy = torch.randn(M, N, device="cuda").bfloat16()
+    x = torch.randn(M, K, device="cuda").bfloat16()
+    dw = torch.randn(N, K, device="cuda")
+    ref = dw + dy.float().t() @ x.float()
+    dense.linear_wgrad(dy, x, dw, accumulate=True)
+    assert _rel(dw, ref) < 1e-4
+
+
+def test_strided_views():
+    """Operands that are column slices of wider buffers (fused QKV layouts)."""
+    from paper_2605_10501_b200 import dense
+
+    torch.manual_seed(7)
+    big = torch.randn(512, 3 * 256, device="cuda").bfloat16()
+    x = big[:, 256:512]
+    w = torch.randn(384, 256, device="cuda").bfloat16()
+    out = torch.empty(512, 384, device="cuda", dtype=torch.bfloat16)
+    dense.gemm(x, w, out, 512, 384, 256, False, False, dense.EPI_BF16, lda=big.stride(0))
+    assert _rel(out, x.float() @ w.float().t()) < 8e-3
