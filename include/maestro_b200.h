@@ -118,14 +118,19 @@ int maestro_build_schedule(const maestro_graph_t* g, const double* d_times, cons
                            int32_t* d_sec_off, double* d_metrics, int64_t* d_evals, void* d_work,
                            int64_t* d_err, void* stream);
 
-/* K5 -- varlen pack of one section rank's order (not in the reference):
- * consecutive groups of `mbs` samples form micro-batches; d_mb[k] = k / mbs,
- * d_tok_off[k] = token offset of order[k] inside its micro-batch's packed stream,
- * d_mb_tokens[m] = tokens of micro-batch m, d_cu[m*(mbs+1) + j] = cu_seqlens.
- * d_len[B] = sequence length per batch index. */
+/* K5 -- varlen pack of one section rank's order (not in the reference).
+ * d_tok_off[k] = exclusive prefix of d_len over the order (offset of order[k] in the rank's
+ * packed token stream); consecutive groups of `mbs` samples form micro-batches:
+ * d_mb[k] = k / mbs, d_mb_start[m] = first token of micro-batch m, d_mb_tokens[m] its token
+ * count, d_cu[m*(mbs+1) + j] its cu_seqlens (relative).  d_len[B] = length per batch index. */
 int maestro_varlen_pack(const int32_t* d_order, int32_t n, const int32_t* d_len, int32_t mbs,
                         int32_t* d_mb, int32_t* d_tok_off, int32_t* d_mb_tokens, int32_t* d_cu,
-                        void* stream);
+                        int32_t* d_mb_start, void* stream);
+
+/* Gather the token ids of the ordered samples into the packed stream:
+ * d_out[d_tok_off[k] + j] = d_ids[d_order[k] * ld + j], j < d_len[d_order[k]]. */
+int maestro_pack_tokens(const int32_t* d_ids, int32_t ld, const int32_t* d_order, const int32_t* d_len,
+                        const int32_t* d_tok_off, int32_t n, int32_t* d_out, void* stream);
 
 /* K6 -- row scatter of encoder outputs into the packed token stream and its backward.
  * fwd: dst[dst_row[k], :] = src[src_row[k], :]  (bf16, d multiple of 8)

@@ -67,7 +67,8 @@ def lib() -> ctypes.CDLL:
         "maestro_rank_metrics": [P, I32, P, I32, I32, P, P],
         "maestro_fanout_merge": [G, I32, P, P, P, P, P, P],
         "maestro_build_schedule": [G, P, P, P, I32, I32, P, P, P, P, P, P, P],
-        "maestro_varlen_pack": [P, I32, P, I32, P, P, P, P, P],
+        "maestro_varlen_pack": [P, I32, P, I32, P, P, P, P, P, P],
+        "maestro_pack_tokens": [P, I32, P, P, P, I32, P, P],
         "maestro_scatter_rows_fwd": [P, P, P, P, I32, I32, P],
         "maestro_gather_rows_bwd": [P, P, P, P, I32, I32, P],
     }

@@ -1,0 +1,335 @@
+// Memory-bound kernels of the section compute: fused residual-add + RMSNorm (fwd/bwd), RoPE,
+// SwiGLU, embedding gather / scatter-add, varlen positions and the fused multi-tensor AdamW.
+// All are HBM-bound: 16-byte vectors, fp32 math, one pass where the dependency allows.
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+
+namespace mb {
+namespace {
+
+__device__ __forceinline__ void ld8(const __nv_bfloat16* p, float (&f)[8]) {
+  const uint4 v = *reinterpret_cast<const uint4*>(p);
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float2 x = __bfloat1622float2(h[j]);
+    f[2 * j] = x.x;
+    f[2 * j + 1] = x.y;
+  }
+}
+__device__ __forceinline__ void st8(__nv_bfloat16* p, const float (&f)[8]) {
+  uint4 v;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) h[j] = __floats2bfloat162_rn(f[2 * j], f[2 * j + 1]);
+  *reinterpret_cast<uint4*>(p) = v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+// ---------------------------------------------------------------- RMSNorm
+// h = x (+ a); y = h * rsqrt(mean(h^2) + eps) * w.  One warp per row.
+__global__ void __launch_bounds__(256) add_rmsnorm_fwd_kernel(const __nv_bfloat16* __restrict__ x,
+                                                              const __nv_bfloat16* __restrict__ a,
+                                                              __nv_bfloat16* __restrict__ h,
+                                                              __nv_bfloat16* __restrict__ y,
+                                                              const __nv_bfloat16* __restrict__ w,
+                                                              float* __restrict__ rstd, int T, int d, float eps) {
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= T) return;
+  const size_t base = (size_t)row * d;
+  float ss = 0.f;
+  for (int c = lane * 8; c < d; c += 256) {
+    float f[8];
+    ld8(x + base + c, f);
+    if (a != nullptr) {
+      float g[8];
+      ld8(a + base + c, g);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) f[j] += g[j];
+      st8(h + base + c, f);
+      ld8(h + base + c, f);  // normalise the bf16-rounded residual, as stored
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) ss += f[j] * f[j];
+  }
+  ss = warp_sum(ss);
+  const float r = rsqrtf(ss / d + eps);
+  if (lane == 0) rstd[row] = r;
+  const __nv_bfloat16* src = a != nullptr ? h : x;
+  for (int c = lane * 8; c < d; c += 256) {
+    float f[8], g[8];
+    ld8(src + base + c, f);
+    ld8(w + c, g);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) f[j] = f[j] * r * g[j];
+    st8(y + base + c, f);
+  }
+}
+
+// dx = dres + r * (w*dy - hn * mean(hn * w * dy)),  hn = h * r;  dw += sum_rows dy * hn
+__global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(const __nv_bfloat16* __restrict__ dy,
+                                                          const __nv_bfloat16* __restrict__ h,
+                                                          const __nv_bfloat16* __restrict__ w,
+                                                          const float* __restrict__ rstd,
+                                                          const __nv_bfloat16* dres, __nv_bfloat16* dx,
+                                                          float* __restrict__ dw, int T, int d) {
+  extern __shared__ float sdw[];
+  for (int c = threadIdx.x; c < d; c += blockDim.x) sdw[c] = 0.f;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+  for (int row = blockIdx.x * nw + warp; row < T; row += gridDim.x * nw) {
+    const size_t base = (size_t)row * d;
+    const float r = rstd[row];
+    float dot = 0.f;
+    for (int c = lane * 8; c < d; c += 256) {
+      float g[8], hh[8], ww[8];
+      ld8(dy + base + c, g);
+      ld8(h + base + c, hh);
+      ld8(w + c, ww);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float hn = hh[j] * r;
+        dot += hn * ww[j] * g[j];
+        atomicAdd(&sdw[c + j], g[j] * hn);
+      }
+    }
+    dot = warp_sum(dot) / d;
+    for (int c = lane * 8; c < d; c += 256) {
+      float g[8], hh[8], ww[8], o[8];
+      ld8(dy + base + c, g);
+      ld8(h + base + c, hh);
+      ld8(w + c, ww);
+      if (dres != nullptr) {
+        ld8(dres + base + c, o);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] = 0.f;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] += r * (ww[j] * g[j] - hh[j] * r * dot);
+      st8(dx + base + c, o);
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < d; c += blockDim.x) atomicAdd(&dw[c], sdw[c]);
+}
+
+// ---------------------------------------------------------------- RoPE (rotate-half pairs)
+// qk rows: [T, n_heads, dh] at row pitch `ld`; cs[pos][dh/2] = (cos, sin).  sign=+1 fwd, -1 bwd.
+__global__ void rope_kernel(__nv_bfloat16* __restrict__ qk, const int32_t* __restrict__ pos,
+                            const float2* __restrict__ cs, int T, int n_heads, int dh, int ld, float sign) {
+  const int half = dh / 2;
+  const int pairs_per_row = n_heads * half;
+  const long long total = (long long)T * pairs_per_row;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const int t = (int)(i / pairs_per_row);
+    const int r = (int)(i - (long long)t * pairs_per_row);
+    const int hd = r / half, k = r - hd * half;
+    __nv_bfloat16* p = qk + (size_t)t * ld + hd * dh;
+    const float2 c = cs[(size_t)pos[t] * half + k];
+    const float s = c.y * sign;
+    const float a = __bfloat162float(p[k]), b = __bfloat162float(p[k + half]);
+    p[k] = __float2bfloat16(a * c.x - b * s);
+    p[k + half] = __float2bfloat16(b * c.x + a * s);
+  }
+}
+
+// positions inside each packed sequence: pos[t] = t - cu[j] for cu[j] <= t < cu[j+1]
+__global__ void positions_kernel(const int32_t* __restrict__ cu, int nseq, int32_t* __restrict__ pos) {
+  const int j = blockIdx.x;
+  if (j >= nseq) return;
+  const int a = cu[j], b = cu[j + 1];
+  for (int t = a + threadIdx.x; t < b; t += blockDim.x) pos[t] = t - a;
+}
+
+// ---------------------------------------------------------------- SwiGLU
+// gu: [T, 2F] = [gate | up]; out[T, F] = silu(gate) * up
+__global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ out, int T,
+                                  int F) {
+  const long long nv = (long long)T * F / 8;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nv; i += (long long)gridDim.x * blockDim.x) {
+    const long long e = i * 8;
+    const long long t = e / F, c = e - t * F;
+    float g[8], u[8], o[8];
+    ld8(gu + t * 2 * F + c, g);
+    ld8(gu + t * 2 * F + F + c, u);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = g[j] / (1.f + __expf(-g[j])) * u[j];
+    st8(out + e, o);
+  }
+}
+
+__global__ void swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ dout, const __nv_bfloat16* __restrict__ gu,
+                                  __nv_bfloat16* __restrict__ dgu, int T, int F) {
+  const long long nv = (long long)T * F / 8;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nv; i += (long long)gridDim.x * blockDim.x) {
+    const long long e = i * 8;
+    const long long t = e / F, c = e - t * F;
+    float d[8], g[8], u[8], dg[8], du[8];
+    ld8(dout + e, d);
+    ld8(gu + t * 2 * F + c, g);
+    ld8(gu + t * 2 * F + F + c, u);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float sg = 1.f / (1.f + __expf(-g[j]));
+      du[j] = d[j] * g[j] * sg;
+      dg[j] = d[j] * u[j] * sg * (1.f + g[j] * (1.f - sg));
+    }
+    st8(dgu + t * 2 * F + c, dg);
+    st8(dgu + t * 2 * F + F + c, du);
+  }
+}
+
+// ---------------------------------------------------------------- embedding
+__global__ void embed_fwd_kernel(const __nv_bfloat16* __restrict__ table, const int32_t* __restrict__ ids,
+                                 __nv_bfloat16* __restrict__ out, int T, int d) {
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= T) return;
+  const uint4* src = reinterpret_cast<const uint4*>(table + (size_t)ids[row] * d);
+  uint4* dst = reinterpret_cast<uint4*>(out + (size_t)row * d);
+  for (int v = lane; v < d / 8; v += 32) dst[v] = src[v];
+}
+
+__global__ void embed_bwd_kernel(const __nv_bfloat16* __restrict__ dout, const int32_t* __restrict__ ids,
+                                 float* __restrict__ dtable, int T, int d) {
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= T) return;
+  float* dst = dtable + (size_t)ids[row] * d;
+  for (int c = lane * 8; c < d; c += 256) {
+    float f[8];
+    ld8(dout + (size_t)row * d + c, f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) atomicAdd(dst + c + j, f[j]);
+  }
+}
+
+// ---------------------------------------------------------------- AdamW (flat arena)
+// p (fp32 master), g (fp32 grad), m, v (fp32), pb (bf16 working copy)
+__global__ void adamw_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
+                             float* __restrict__ v, __nv_bfloat16* __restrict__ pb, long long n, float lr, float b1,
+                             float b2, float eps, float wd, float bc1, float bc2, float gscale) {
+  const long long n4 = n / 4;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+    float4 pp = reinterpret_cast<float4*>(p)[i];
+    const float4 gg = reinterpret_cast<const float4*>(g)[i];
+    float4 mm = reinterpret_cast<float4*>(m)[i];
+    float4 vv = reinterpret_cast<float4*>(v)[i];
+    float* P = &pp.x;
+    const float* G = &gg.x;
+    float* Mm = &mm.x;
+    float* Vv = &vv.x;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float gj = G[j] * gscale;
+      Mm[j] = b1 * Mm[j] + (1.f - b1) * gj;
+      Vv[j] = b2 * Vv[j] + (1.f - b2) * gj * gj;
+      const float upd = (Mm[j] / bc1) / (sqrtf(Vv[j] / bc2) + eps);
+      P[j] -= lr * (upd + wd * P[j]);
+    }
+    reinterpret_cast<float4*>(p)[i] = pp;
+    reinterpret_cast<float4*>(m)[i] = mm;
+    reinterpret_cast<float4*>(v)[i] = vv;
+    __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(pb + 4 * i);
+    o[0] = __floats2bfloat162_rn(pp.x, pp.y);
+    o[1] = __floats2bfloat162_rn(pp.z, pp.w);
+  }
+}
+
+inline int grid_for(long long work, int threads) {
+  long long b = (work + threads - 1) / threads;
+  const long long cap = 148LL * 16;
+  return (int)(b < 1 ? 1 : (b > cap ? cap : b));
+}
+
+}  // namespace
+}  // namespace mb
+
+using namespace mb;
+
+MAESTRO_API int maestro_add_rmsnorm_fwd(const void* x, const void* a, void* h, void* y, const void* w, float* rstd,
+                                        int32_t T, int32_t d, float eps, void* stream) {
+  if (T <= 0) return 0;
+  if (d % 8) return (int)cudaErrorInvalidValue;
+  add_rmsnorm_fwd_kernel<<<(T + 7) / 8, 256, 0, (cudaStream_t)stream>>>(
+      (const __nv_bfloat16*)x, (const __nv_bfloat16*)a, (__nv_bfloat16*)h, (__nv_bfloat16*)y,
+      (const __nv_bfloat16*)w, rstd, T, d, eps);
+  return launch_status();
+}
+
+MAESTRO_API int maestro_rmsnorm_bwd(const void* dy, const void* h, const void* w, const float* rstd,
+                                    const void* dres, void* dx, float* dw, int32_t T, int32_t d, void* stream) {
+  if (T <= 0) return 0;
+  if (d % 8) return (int)cudaErrorInvalidValue;
+  const size_t smem = (size_t)d * sizeof(float);
+  if (ensure_smem<rmsnorm_bwd_kernel>(smem)) return launch_status();
+  const int grid = T / 8 < 148 * 2 ? (T + 7) / 8 : 148 * 2;
+  rmsnorm_bwd_kernel<<<grid, 256, smem, (cudaStream_t)stream>>>(
+      (const __nv_bfloat16*)dy, (const __nv_bfloat16*)h, (const __nv_bfloat16*)w, rstd, (const __nv_bfloat16*)dres,
+      (__nv_bfloat16*)dx, dw, T, d);
+  return launch_status();
+}
+
+MAESTRO_API int maestro_rope(void* qk, const int32_t* pos, const void* cos_sin, int32_t T, int32_t n_heads,
+                             int32_t dh, int32_t ld, int32_t backward, void* stream) {
+  if (T <= 0) return 0;
+  const long long work = (long long)T * n_heads * dh / 2;
+  rope_kernel<<<grid_for(work, 256), 256, 0, (cudaStream_t)stream>>>(
+      (__nv_bfloat16*)qk, pos, (const float2*)cos_sin, T, n_heads, dh, ld, backward ? -1.f : 1.f);
+  return launch_status();
+}
+
+MAESTRO_API int maestro_positions(const int32_t* cu, int32_t nseq, int32_t* pos, void* stream) {
+  if (nseq <= 0) return 0;
+  positions_kernel<<<nseq, 256, 0, (cudaStream_t)stream>>>(cu, nseq, pos);
+  return launch_status();
+}
+
+MAESTRO_API int maestro_swiglu_fwd(const void* gu, void* out, int32_t T, int32_t F, void* stream) {
+  if (T <= 0) return 0;
+  if (F % 8) return (int)cudaErrorInvalidValue;
+  swiglu_fwd_kernel<<<grid_for((long long)T * F / 8, 256), 256, 0, (cudaStream_t)stream>>>(
+      (const __nv_bfloat16*)gu, (__nv_bfloat16*)out, T, F);
+  return launch_status();
+}
+
+MAESTRO_API int maestro_swiglu_bwd(const void* dout, const void* gu, void* dgu, int32_t T, int32_t F, void* stream) {
+  if (T <= 0) return 0;
+  if (F % 8) return (int)cudaErrorInvalidValue;
+  swiglu_bwd_kernel<<<grid_for((long long)T * F / 8, 256), 256, 0, (cudaStream_t)stream>>>(
+      (const __nv_bfloat16*)dout, (const __nv_bfloat16*)gu, (__nv_bfloat16*)dgu, T, F);
+  return launch_status();
+}
+
+MAESTRO_API int maestro_embed_fwd(const void* table, const int32_t* ids, void* out, int32_t T, int32_t d,
+                                  void* stream) {
+  if (T <= 0) return 0;
+  embed_fwd_kernel<<<(T + 7) / 8, 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)table, ids,
+                                                                  (__nv_bfloat16*)out, T, d);
+  return launch_status();
+}
+
+MAESTRO_API int maestro_embed_bwd(const void* dout, const int32_t* ids, float* dtable, int32_t T, int32_t d,
+                                  void* stream) {
+  if (T <= 0) return 0;
+  embed_bwd_kernel<<<(T + 7) / 8, 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)dout, ids, dtable, T, d);
+  return launch_status();
+}
+
+MAESTRO_API int maestro_adamw(float* p, const float* g, float* m, float* v, void* pb, int64_t n, float lr, float b1,
+                              float b2, float eps, float wd, int32_t step, float gscale, void* stream) {
+  if (n <= 0) return 0;
+  if (n % 4) return (int)cudaErrorInvalidValue;
+  const float bc1 = 1.f - powf(b1, (float)step), bc2 = 1.f - powf(b2, (float)step);
+  adamw_kernel<<<grid_for(n / 4, 256), 256, 0, (cudaStream_t)stream>>>(p, g, m, v, (__nv_bfloat16*)pb, n, lr, b1, b2,
+                                                                        eps, wd, bc1, bc2, gscale);
+  return launch_status();
+}

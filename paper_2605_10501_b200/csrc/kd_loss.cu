@@ -1,0 +1,164 @@
+// K9: fused knowledge-distillation loss over the full vocabulary.
+//
+// Per token row:  KL(p_t || p_s) = sum_v p_t (t - s) - lse(t) + lse(s),   p = softmax(logits / tau)
+// and its gradient w.r.t. the student logits  ds = g / tau * (softmax(s/tau) - softmax(t/tau)).
+// The teacher's output layer is colocated with the student (workload.py:471-514), so both
+// logit rows are produced in the student section; no probabilities are ever materialised.
+// Pass 1 streams both rows once keeping online (max, sum-exp) for t and s plus the running
+// sum_v e^{t-m}(t - s); pass 2 re-reads the rows (L2-resident: a CTA's row is < 0.6 MB and
+// just touched) and writes ds.  HBM traffic ~ 2 x V x 2 B read + V x 2 B written per token.
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+
+namespace mb {
+namespace {
+
+constexpr int KD_THREADS = 512;
+constexpr float LOG2E = 1.4426950408889634f;
+constexpr float LN2 = 0.6931471805599453f;
+
+struct Stat {  // online stats in the log2 domain
+  float mt, st, at, ms, ss;
+};
+
+__device__ __forceinline__ void merge(Stat& a, const Stat& b) {
+  if (b.mt != -INFINITY) {
+    if (a.mt == -INFINITY) {
+      a.mt = b.mt;
+      a.st = b.st;
+      a.at = b.at;
+    } else {
+      const float mt = fmaxf(a.mt, b.mt);
+      const float ca = exp2f(a.mt - mt), cb = exp2f(b.mt - mt);
+      a.st = a.st * ca + b.st * cb;
+      a.at = a.at * ca + b.at * cb;
+      a.mt = mt;
+    }
+  }
+  if (b.ms != -INFINITY) {
+    if (a.ms == -INFINITY) {
+      a.ms = b.ms;
+      a.ss = b.ss;
+    } else {
+      const float ms = fmaxf(a.ms, b.ms);
+      a.ss = a.ss * exp2f(a.ms - ms) + b.ss * exp2f(b.ms - ms);
+      a.ms = ms;
+    }
+  }
+}
+
+__device__ __forceinline__ void unpack8(const uint4& v, float (&f)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float2 x = __bfloat1622float2(h[j]);
+    f[2 * j] = x.x;
+    f[2 * j + 1] = x.y;
+  }
+}
+
+__global__ void __launch_bounds__(KD_THREADS) kd_loss_kernel(const __nv_bfloat16* __restrict__ tl,
+                                                             const __nv_bfloat16* sl,
+                                                             __nv_bfloat16* ds,  // may alias sl
+                                                             float* __restrict__ loss,
+                                                             int T, int V, int ldt, int lds, int ldd, float scale2,
+                                                             float grad_scale, float inv_tau) {
+  __shared__ Stat red[KD_THREADS / 32];
+  __shared__ Stat fin;
+  const int nvec = V / 8;
+  for (int row = blockIdx.x; row < T; row += gridDim.x) {
+    const uint4* t4 = reinterpret_cast<const uint4*>(tl + (size_t)row * ldt);
+    const uint4* s4 = reinterpret_cast<const uint4*>(sl + (size_t)row * lds);
+    Stat a{-INFINITY, 0.f, 0.f, -INFINITY, 0.f};
+    for (int v = threadIdx.x; v < nvec; v += KD_THREADS) {
+      float ft[8], fs[8];
+      unpack8(t4[v], ft);
+      unpack8(s4[v], fs);
+      float mt = a.mt, ms = a.ms;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        mt = fmaxf(mt, ft[j] * scale2);
+        ms = fmaxf(ms, fs[j] * scale2);
+      }
+      const float ct = exp2f(a.mt - mt), cs = exp2f(a.ms - ms);
+      float st = a.st * ct, at = a.at * ct, ss = a.ss * cs;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float et = exp2f(ft[j] * scale2 - mt);
+        st += et;
+        at += et * (ft[j] - fs[j]);
+        ss += exp2f(fs[j] * scale2 - ms);
+      }
+      a = Stat{mt, st, at, ms, ss};
+    }
+    // block reduction of the online stats
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      Stat b{__shfl_xor_sync(kFull, a.mt, o), __shfl_xor_sync(kFull, a.st, o), __shfl_xor_sync(kFull, a.at, o),
+             __shfl_xor_sync(kFull, a.ms, o), __shfl_xor_sync(kFull, a.ss, o)};
+      merge(a, b);
+    }
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      a = threadIdx.x < KD_THREADS / 32 ? red[threadIdx.x] : Stat{-INFINITY, 0.f, 0.f, -INFINITY, 0.f};
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        Stat b{__shfl_xor_sync(kFull, a.mt, o), __shfl_xor_sync(kFull, a.st, o), __shfl_xor_sync(kFull, a.at, o),
+               __shfl_xor_sync(kFull, a.ms, o), __shfl_xor_sync(kFull, a.ss, o)};
+        merge(a, b);
+      }
+      if (threadIdx.x == 0) {
+        fin = a;
+        // lse in natural units of the tempered logits: (m2 + log2 S) * ln 2
+        const float lse_t = (a.mt + log2f(a.st)) * LN2;
+        const float lse_s = (a.ms + log2f(a.ss)) * LN2;
+        // sum p_t (t - s)/tau - lse_t + lse_s
+        loss[row] = a.at / a.st * inv_tau - lse_t + lse_s;
+      }
+    }
+    __syncthreads();
+    if (ds != nullptr) {
+      const Stat f = fin;
+      const float it = 1.f / f.st, is = 1.f / f.ss;
+      const float g = grad_scale * inv_tau;
+      uint4* d4 = reinterpret_cast<uint4*>(ds + (size_t)row * ldd);
+      for (int v = threadIdx.x; v < nvec; v += KD_THREADS) {
+        float ft[8], fs[8];
+        unpack8(t4[v], ft);
+        unpack8(s4[v], fs);
+        uint4 o;
+        __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float g0 = g * (exp2f(fs[2 * j] * scale2 - f.ms) * is - exp2f(ft[2 * j] * scale2 - f.mt) * it);
+          const float g1 = g * (exp2f(fs[2 * j + 1] * scale2 - f.ms) * is - exp2f(ft[2 * j + 1] * scale2 - f.mt) * it);
+          oh[j] = __floats2bfloat162_rn(g0, g1);
+        }
+        d4[v] = o;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+}  // namespace mb
+
+using namespace mb;
+
+// loss[T] (fp32, per token) and, if d_ds != null, ds = grad_scale * d loss / d s (bf16).
+// ds may alias the student logits (in-place): every element is read before it is written
+// by the same thread.
+MAESTRO_API int maestro_kd_loss_fwd_bwd(const void* d_t, const void* d_s, void* d_ds, float* d_loss, int32_t T,
+                                        int32_t V, int32_t ldt, int32_t lds, int32_t ldd, float grad_scale,
+                                        float inv_tau, void* stream) {
+  if (T <= 0) return 0;
+  if (V % 8 || ldt % 8 || lds % 8 || ldd % 8) return (int)cudaErrorInvalidValue;
+  const int grid = T < 148 * 4 ? T : 148 * 4;
+  kd_loss_kernel<<<grid, KD_THREADS, 0, (cudaStream_t)stream>>>(
+      (const __nv_bfloat16*)d_t, (const __nv_bfloat16*)d_s, (__nv_bfloat16*)d_ds, d_loss, T, V, ldt, lds, ldd,
+      inv_tau * LOG2E, grad_scale, inv_tau);
+  return launch_status();
+}

@@ -653,23 +653,73 @@ __global__ void __launch_bounds__(1024) fanout_merge_kernel(maestro_graph_t g, i
 }
 
 // ---------------------------------------------------------------------------------------
-// K5: varlen pack of one rank's order into micro-batches of `mbs` samples.
-__global__ void varlen_pack_kernel(const int32_t* __restrict__ order, int n, const int32_t* __restrict__ len,
-                                   int mbs, int32_t* __restrict__ mb, int32_t* __restrict__ tok_off,
-                                   int32_t* __restrict__ mb_tokens, int32_t* __restrict__ cu) {
-  const int n_mb = (n + mbs - 1) / mbs;
-  for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < n_mb; m += gridDim.x * blockDim.x) {
-    int acc = 0;
-    const int k0 = m * mbs, k1 = min(n, k0 + mbs);
-    cu[m * (mbs + 1)] = 0;
-    for (int k = k0; k < k1; ++k) {
-      mb[k] = m;
-      tok_off[k] = acc;
-      acc += len[order[k]];
-      cu[m * (mbs + 1) + (k - k0) + 1] = acc;
+// K5: varlen pack of one rank's order.  Token offsets are an exclusive prefix scan of the
+// sequence lengths in schedule order (one CTA, carry across 1024-sample chunks);
+// consecutive groups of `mbs` samples form micro-batches with their own cu_seqlens.
+__global__ void __launch_bounds__(1024) varlen_pack_kernel(const int32_t* __restrict__ order, int n,
+                                                           const int32_t* __restrict__ len, int mbs,
+                                                           int32_t* __restrict__ mb, int32_t* __restrict__ tok_off,
+                                                           int32_t* __restrict__ mb_tokens, int32_t* __restrict__ cu,
+                                                           int32_t* __restrict__ mb_start) {
+  __shared__ int wsum[33];
+  __shared__ int carry_s;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry_s = 0;
+  __syncthreads();
+  for (int k0 = 0; k0 < n; k0 += blockDim.x) {
+    const int k = k0 + threadIdx.x;
+    const int l = k < n ? len[order[k]] : 0;
+    int incl = l;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += y;
     }
-    for (int k = k1 - k0; k < mbs; ++k) cu[m * (mbs + 1) + k + 1] = acc;
-    mb_tokens[m] = acc;
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const int nw = blockDim.x >> 5;
+      const int v = lane < nw ? wsum[lane] : 0;
+      int x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane < nw) wsum[lane] = x - v;
+      if (lane == 31) wsum[32] = x;
+    }
+    __syncthreads();
+    const int carry = carry_s;
+    if (k < n) {
+      tok_off[k] = carry + wsum[warp] + incl - l;
+      mb[k] = k / mbs;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) carry_s = carry + wsum[32];
+    __syncthreads();
+  }
+  const int n_mb = (n + mbs - 1) / mbs;
+  for (int m = threadIdx.x; m < n_mb; m += blockDim.x) {
+    const int k0 = m * mbs, k1 = min(n, k0 + mbs);
+    const int base = tok_off[k0];
+    mb_start[m] = base;
+    cu[m * (mbs + 1)] = 0;
+    for (int k = k0; k < k1; ++k) cu[m * (mbs + 1) + (k - k0) + 1] = tok_off[k] + len[order[k]] - base;
+    for (int k = k1 - k0; k < mbs; ++k) cu[m * (mbs + 1) + k + 1] = cu[m * (mbs + 1) + (k1 - k0)];
+    mb_tokens[m] = cu[m * (mbs + 1) + mbs];
+  }
+}
+
+// Token ids of the ordered samples into one packed stream: out[tok_off[k] + j] = ids[order[k], j].
+__global__ void pack_tokens_kernel(const int32_t* __restrict__ ids, int ld, const int32_t* __restrict__ order,
+                                   const int32_t* __restrict__ len, const int32_t* __restrict__ tok_off, int n,
+                                   int32_t* __restrict__ out) {
+  for (int k = blockIdx.x; k < n; k += gridDim.x) {
+    const int i = order[k];
+    const int32_t* src = ids + (size_t)i * ld;
+    int32_t* dst = out + tok_off[k];
+    for (int j = threadIdx.x; j < len[i]; j += blockDim.x) dst[j] = src[j];
   }
 }
 
@@ -801,10 +851,17 @@ MAESTRO_API int maestro_build_schedule(const maestro_graph_t* g, const double* d
 
 MAESTRO_API int maestro_varlen_pack(const int32_t* d_order, int32_t n, const int32_t* d_len, int32_t mbs,
                                     int32_t* d_mb, int32_t* d_tok_off, int32_t* d_mb_tokens, int32_t* d_cu,
-                                    void* stream) {
+                                    int32_t* d_mb_start, void* stream) {
   if (n <= 0) return 0;
-  const int n_mb = (n + mbs - 1) / mbs;
-  varlen_pack_kernel<<<(n_mb + 127) / 128, 128, 0, (cudaStream_t)stream>>>(d_order, n, d_len, mbs, d_mb, d_tok_off,
-                                                                             d_mb_tokens, d_cu);
+  varlen_pack_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(d_order, n, d_len, mbs, d_mb, d_tok_off, d_mb_tokens, d_cu,
+                                                            d_mb_start);
+  return launch_status();
+}
+
+MAESTRO_API int maestro_pack_tokens(const int32_t* d_ids, int32_t ld, const int32_t* d_order, const int32_t* d_len,
+                                    const int32_t* d_tok_off, int32_t n, int32_t* d_out, void* stream) {
+  if (n <= 0) return 0;
+  pack_tokens_kernel<<<n < 1024 ? n : 1024, 256, 0, (cudaStream_t)stream>>>(d_ids, ld, d_order, d_len, d_tok_off, n,
+                                                                            d_out);
   return launch_status();
 }

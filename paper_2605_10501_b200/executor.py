@@ -1,0 +1,356 @@
+"""Section-graph executor: ``step()`` runs one training iteration of a section graph.
+
+The execution contract is the reference executor model (``maestro/simulator.py:202-233``):
+every (section, DP rank) is a resource that runs a fixed stage queue derived from the
+wavefront schedule --
+
+* UPSTREAM sections: all forward stages (f_bc) in schedule order, then all backward (b_ac);
+* CRITICAL / DOWNSTREAM sections: per micro-batch forward then backward (INTERLEAVED), or all
+  forwards then all backwards (ALL_FWD_THEN_BWD);
+
+and a stage may start once its resource is free and its chain predecessor (possibly on another
+section) has finished.  Here a resource is a CUDA stream on the GPU that hosts the section rank;
+a chain predecessor on the same GPU is a CUDA event, on another GPU an NCCL send/recv on the
+fan-out map (``scheduling.py:366-371``).  Per-step work:
+
+1. plan on device: K1 6-tuples from token counts, K2-K4 wavefront schedule, K5 varlen pack of the
+   local rank's order into micro-batches (one small D2H of micro-batch sizes per step);
+2. run the local stage queues; stage boundaries are CUDA events, so the critical section's
+   busy time and span -- the reference's ``critical_idle`` / section stall (scheduling.py:64-66,
+   simulator.py:312-315) -- are measured on the device;
+3. per-section gradient all-reduce over that section's own DP group, then the fused optimizer.
+
+The KD graph (cfg 2) is implemented by :class:`KDExecutor`: a forward-only teacher upstream of
+the student, with the teacher's output layer colocated in the student section
+(``workload.colocate_output_layer``), so the teacher ships final hidden states ``[T, d_t]``
+and the student computes teacher logits next to the fused KL loss (K9).
+"""
+
+from __future__ import annotations
+
+import math
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as N
+from . import kernels as K
+from . import recipes as R
+from .costs import cost_table
+from .scheduling import DevicePlanner, ExecPolicy
+from .transformer import SHAPES, Batch, FlatParams, Shape, Transformer
+
+
+@dataclass
+class StepStats:
+    loss: float | None
+    step_ms: float
+    critical_busy_ms: float
+    critical_span_ms: float
+    stages: list = field(default_factory=list)
+
+    @property
+    def stall_frac(self) -> float:
+        return 0.0 if self.critical_span_ms <= 0 else max(0.0, 1.0 - self.critical_busy_ms / self.critical_span_ms)
+
+
+class StageClock:
+    """CUDA events around every stage of one resource (stream)."""
+
+    def __init__(self):
+        self.marks = []
+
+    def begin(self, stream, name):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        self.marks.append([name, e, None])
+
+    def end(self, stream):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        self.marks[-1][2] = e
+
+    def busy_span(self):
+        if not self.marks:
+            return 0.0, 0.0
+        busy = sum(a.elapsed_time(b) for _, a, b in self.marks)
+        span = self.marks[0][1].elapsed_time(self.marks[-1][2])
+        return busy, span
+
+
+def _dist():
+    import torch.distributed as dist
+
+    return dist if dist.is_available() and dist.is_initialized() else None
+
+
+class KDExecutor:
+    """KD section graph (recipes.kd): teacher (upstream, forward-only) -> student (critical)."""
+
+    def __init__(self, n_gpus: int = 1, batch_per_rank: int = 64, seq: int = R.KD_SEQ, mbs: int = 4,
+                 teacher: str = "kd_teacher_1b", student: str = "kd_student_125m", seed: int = 0,
+                 lr: float = 3e-4, policy=ExecPolicy.INTERLEAVED, device=None):
+        dist = _dist()
+        self.rank = dist.get_rank() if dist else 0
+        self.world = dist.get_world_size() if dist else 1
+        if self.world != n_gpus:
+            raise ValueError(f"n_gpus={n_gpus} but world size is {self.world}")
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.n_gpus, self.seq, self.mbs = n_gpus, seq, mbs
+        dp_s, dp_t, f_t = R.KD_LAYOUTS[n_gpus]
+        self.batch = batch_per_rank * dp_s
+        self.recipe = R.kd(n_gpus, self.batch, seq)
+        cfg = {"student": self.recipe.configs["student"].__class__(dp=dp_s, mbs=mbs),
+               "teacher": self.recipe.configs["teacher"].__class__(dp=dp_t, fanout=f_t, mbs=mbs)}
+        self.configs = cfg
+        self.graph = self.recipe.graph
+        # roles: co-resident at 1 GPU; disjoint GPU groups otherwise (teacher ranks first)
+        self.colocated = n_gpus == 1
+        if self.colocated:
+            self.t_rank, self.s_rank = 0, 0
+        else:
+            self.t_rank = self.rank if self.rank < dp_t else None
+            self.s_rank = self.rank - dp_t if self.rank >= dp_t else None
+        self.dp_s, self.dp_t = dp_s, dp_t
+        self.tshape: Shape = SHAPES[teacher]
+        self.sshape: Shape = SHAPES[student]
+        dev = self.device
+        # --- sections hosted here
+        self.teacher = self.student = None
+        if self.t_rank is not None:
+            tp = FlatParams(self.tshape.param_shapes(), dev, trainable=False, seed=seed + 1)
+            self.teacher = Transformer(self.tshape, tp, dev, max_pos=seq)
+            self.t_stream = torch.cuda.Stream(device=dev)
+        if self.s_rank is not None:
+            sp = FlatParams(self.sshape.param_shapes(), dev, trainable=True, seed=seed + 2)
+            self.student = Transformer(self.sshape, sp, dev, max_pos=seq)
+            # colocated teacher output layer (workload.colocate_output_layer): frozen, lives here
+            g = torch.Generator(device=dev).manual_seed(seed + 3)
+            self.t_head = (torch.randn(self.tshape.vocab, self.tshape.d, device=dev, generator=g) * 0.02).bfloat16()
+            self.s_stream = torch.cuda.Stream(device=dev)
+        self.lr = lr
+        # --- device planner (every rank computes the same deterministic schedule)
+        self.planner = DevicePlanner(self.graph, cfg, policy, max_batch=self.batch, device=dev)
+        self.cost = torch.from_numpy(cost_table(self.graph, cfg, self.recipe.params)).to(dev)
+        tab = self.graph.tables
+        self.n_bits = len(tab.sub_names)
+        self._bits = {n: i for i, n in enumerate(tab.sub_names)}
+        self.lens = torch.full((self.batch,), seq, dtype=torch.int32, device=dev)
+        self.tokens = torch.zeros(self.n_bits, self.batch, dtype=torch.int32, device=dev)
+        self.tokens[self._bits["student"]] = seq
+        self.tokens[self._bits["teacher"]] = seq
+        self.planner.ids[: self.batch].copy_(torch.arange(self.batch, dtype=torch.int32))
+        self.groups = self._make_groups()
+        self.step_idx = 0
+
+    # ------------------------------------------------------------------ distributed plumbing
+    def _make_groups(self):
+        dist = _dist()
+        if dist is None or self.colocated:
+            return {}
+        dp_t = self.dp_t
+        s_ranks = list(range(dp_t, self.world))
+        grp = dist.new_group(s_ranks) if len(s_ranks) > 1 else None
+        return {"student": grp, "student_ranks": s_ranks}
+
+    # ------------------------------------------------------------------ planning
+    def plan(self, stream):
+        """K1-K5 on device for this step; returns per-local-rank micro-batch tables (host)."""
+        with torch.cuda.stream(stream):
+            self.planner.plan_tokens(self.cost, self.tokens, self.batch, stream)
+        tab = self.graph.tables
+        crit, teach = tab.critical, tab.section_ids.index("teacher")
+        out = {}
+        W = N.MAX_DP + 1
+        for sec, rank in (("student", self.s_rank), ("teacher", self.t_rank)):
+            if rank is None:
+                continue
+            s = crit if sec == "student" else teach
+            # orders of section s live at orders[s*B + off] (device); build the pack tables
+            n_per = self.batch // (self.dp_s if sec == "student" else self.dp_t)
+            off = self.planner.sec_off.view(-1, W)[s, rank: rank + 1]
+            base = s * self.batch
+            with torch.cuda.stream(stream):
+                order = torch.empty(n_per, dtype=torch.int32, device=self.device)
+                # device-side gather of the rank's slice (offset read on device via index_select)
+                idx = (torch.arange(n_per, device=self.device, dtype=torch.int32) + off.to(torch.int32) + base).long()
+                order.copy_(self.planner.orders.index_select(0, idx))
+                n_mb = -(-n_per // self.mbs)
+                z = lambda k: torch.empty(k, dtype=torch.int32, device=self.device)  # noqa: E731
+                mb, tok_off, mb_tok, cu, mb_start = z(n_per), z(n_per), z(n_mb), z(n_mb * (self.mbs + 1)), z(n_mb)
+                N.check(N.lib().maestro_varlen_pack(N.ptr(order), n_per, N.ptr(self.lens), self.mbs, N.ptr(mb),
+                                                    N.ptr(tok_off), N.ptr(mb_tok), N.ptr(cu), N.ptr(mb_start),
+                                                    stream.cuda_stream), "varlen_pack")
+            out[sec] = dict(order=order, tok_off=tok_off, mb_tok=mb_tok, cu=cu, mb_start=mb_start, n=n_per,
+                            n_mb=n_mb)
+        return out
+
+    # ------------------------------------------------------------------ one step
+    def step(self, ids: torch.Tensor, want_loss: bool = True) -> StepStats:
+        """One training iteration.  ``ids``: [batch, seq] int32 token ids (device or pinned host)."""
+        dev = self.device
+        main = torch.cuda.current_stream(dev)
+        if ids.device.type != "cuda":
+            ids_dev = torch.empty(ids.shape, dtype=torch.int32, device=dev)
+            ids_dev.copy_(ids, non_blocking=True)
+        else:
+            ids_dev = ids
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_start.record(main)
+        plan = self.plan(main)
+        # one small D2H per step: micro-batch token counts of the local rank orders
+        host = {k: (v["mb_tok"].cpu().tolist(), v["mb_start"].cpu().tolist()) for k, v in plan.items()}
+        packed = {}
+        with torch.cuda.stream(main):
+            for sec, v in plan.items():
+                total = int(sum(host[sec][0]))
+                pk = torch.empty(total, dtype=torch.int32, device=dev)
+                N.check(N.lib().maestro_pack_tokens(N.ptr(ids_dev), ids_dev.shape[1], N.ptr(v["order"]),
+                                                    N.ptr(self.lens), N.ptr(v["tok_off"]), v["n"], N.ptr(pk),
+                                                    main.cuda_stream), "pack_tokens")
+                packed[sec] = pk
+        ready = torch.cuda.Event()
+        ready.record(main)
+        clock = StageClock()
+        loss_acc = None
+        if self.student is not None:
+            loss_acc = torch.zeros(1, device=dev, dtype=torch.float32)
+            self.student.p.zero_grad() if self.step_idx == 0 or True else None
+        global_tokens = float(self.batch * self.seq)
+        if self.colocated:
+            self._run_colocated(plan, host, packed, ready, clock, loss_acc, global_tokens)
+        elif self.t_rank is not None:
+            self._run_teacher_remote(plan, host, packed, ready)
+        else:
+            self._run_student_remote(plan, host, packed, ready, clock, loss_acc, global_tokens)
+        # per-section gradient sync (student DP group) + optimizer, on the student stream
+        if self.student is not None:
+            with torch.cuda.stream(self.s_stream):
+                dist = _dist()
+                if dist is not None and self.dp_s > 1:
+                    dist.all_reduce(self.student.p.grad, group=self.groups.get("student"))
+                    dist.all_reduce(loss_acc, group=self.groups.get("student"))
+                self.student.p.adamw(self.lr)
+            main.wait_stream(self.s_stream)
+        if self.teacher is not None and not self.colocated:
+            main.wait_stream(self.t_stream)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_end.record(main)
+        self.step_idx += 1
+        loss = None
+        if want_loss and loss_acc is not None:
+            loss = float(loss_acc.item()) / global_tokens
+        t_end.synchronize()
+        busy, span = clock.busy_span()
+        return StepStats(loss, t_start.elapsed_time(t_end), busy, span)
+
+    # --- co-resident sections on one GPU: the teacher stream runs ahead (upstream queue),
+    # the student stream waits per micro-batch on a CUDA event.
+    def _teacher_mb(self, packed, cu, m, start, T):
+        b = Batch(ids=packed[start: start + T], cu=cu, pos=self._positions(cu, T), max_len=self.seq)
+        yf, _ = self.teacher.forward(b, save=False)
+        return yf
+
+    def _positions(self, cu, T):
+        pos = torch.empty(T, dtype=torch.int32, device=self.device)
+        K.positions(cu, cu.numel() - 1, pos)
+        return pos
+
+    def _student_mb(self, yf_t, packed, cu, start, T, loss_acc, global_tokens, clock, m):
+        b = Batch(ids=packed[start: start + T], cu=cu, pos=self._positions(cu, T), max_len=self.seq)
+        clock.begin(self.s_stream, f"fwd{m}")
+        yf, ctx = self.student.forward(b)
+        s_logits = self.student.logits(yf)
+        t_logits = torch.empty_like(s_logits)
+        from . import dense as D
+
+        D.linear_fwd(yf_t, self.t_head, t_logits)  # colocated teacher output layer
+        tok_loss = torch.empty(T, device=self.device, dtype=torch.float32)
+        K.kd_loss(t_logits, s_logits, s_logits, tok_loss, grad_scale=1.0 / global_tokens)
+        loss_acc.add_(tok_loss.sum())
+        del t_logits
+        self.student.backward(ctx, dlogits=s_logits)
+        clock.end(self.s_stream)
+
+    def _mb_cu(self, plan_sec, m, T):
+        n_in = min(self.mbs, plan_sec["n"] - m * self.mbs)
+        cu = plan_sec["cu"][m * (self.mbs + 1): m * (self.mbs + 1) + n_in + 1]
+        return cu
+
+    def _run_colocated(self, plan, host, packed, ready, clock, loss_acc, global_tokens):
+        ps, pt = plan["student"], plan["teacher"]
+        ht, hs = host["teacher"], host["student"]
+        ev = []
+        self.t_stream.wait_event(ready)
+        self.s_stream.wait_event(ready)
+        outs = []
+        with torch.cuda.stream(self.t_stream):
+            for m in range(pt["n_mb"]):
+                T = ht[0][m]
+                yf = self._teacher_mb(packed["teacher"], self._mb_cu(pt, m, T), m, ht[1][m], T)
+                e = torch.cuda.Event()
+                e.record(self.t_stream)
+                ev.append(e)
+                outs.append(yf)
+        with torch.cuda.stream(self.s_stream):
+            for m in range(ps["n_mb"]):
+                # fan-out 1 and equal mbs: student micro-batch m consumes teacher micro-batch m
+                self.s_stream.wait_event(ev[m])
+                T = hs[0][m]
+                self._student_mb(outs[m], packed["student"], self._mb_cu(ps, m, T), hs[1][m], T, loss_acc,
+                                 global_tokens, clock, m)
+                outs[m].record_stream(self.s_stream)
+                outs[m] = None
+
+    def _run_teacher_remote(self, plan, host, packed, ready):
+        dist = _dist()
+        pt, ht = plan["teacher"], host["teacher"]
+        dst = self.dp_t + self.t_rank  # fan-out 1: teacher rank q feeds student rank q
+        self.t_stream.wait_event(ready)
+        with torch.cuda.stream(self.t_stream):
+            for m in range(pt["n_mb"]):
+                T = ht[0][m]
+                yf = self._teacher_mb(packed["teacher"], self._mb_cu(pt, m, T), m, ht[1][m], T)
+                dist.send(yf, dst)
+
+    def _run_student_remote(self, plan, host, packed, ready, clock, loss_acc, global_tokens):
+        dist = _dist()
+        ps, hs = plan["student"], host["student"]
+        src = self.s_rank  # teacher rank feeding this student rank
+        self.s_stream.wait_event(ready)
+        with torch.cuda.stream(self.s_stream):
+            for m in range(ps["n_mb"]):
+                T = hs[0][m]
+                yf_t = torch.empty(T, self.tshape.d, device=self.device, dtype=torch.bfloat16)
+                dist.recv(yf_t, src)
+                self._student_mb(yf_t, packed["student"], self._mb_cu(ps, m, T), hs[1][m], T, loss_acc,
+                                 global_tokens, clock, m)
+
+    # ------------------------------------------------------------------ accounting
+    def model_flops_per_step(self) -> float:
+        """Algorithmic FLOPs of one step over the whole job (teacher fwd + head, student train)."""
+        s, t, L = self.sshape, self.tshape, self.seq
+        tok = self.batch * L
+        t_fwd = t.fwd_flops_per_token(L, with_head=True)  # teacher body + colocated head
+        s_train = 3.0 * s.fwd_flops_per_token(L, with_head=True)
+        return tok * (t_fwd + s_train)
+
+
+def synthetic_ids(batch: int, seq: int, vocab: int, seed: int = 0, step: int = 0) -> np.ndarray:
+    from .synthetic import rand_int
+
+    n = batch * seq
+    return rand_int(seed, 4 + 16 * step, np.arange(n), 0, vocab - 1).astype(np.int32).reshape(batch, seq)
+
+
+def smoke_step():
+    """Tiny KD step on cuda:0 (used by __graft_entry__.smoke)."""
+    ex = KDExecutor(n_gpus=1, batch_per_rank=4, seq=256, mbs=2, teacher="test_tiny", student="test_tiny")
+    ids = torch.from_numpy(synthetic_ids(4, 256, 512)).cuda()
+    st = ex.step(ids)
+    assert st.loss is not None and math.isfinite(st.loss), st
+    st2 = ex.step(ids)
+    assert math.isfinite(st2.loss)
+    print(f"smoke kd step: loss {st.loss:.4f} -> {st2.loss:.4f}, stall {st.stall_frac:.3f}")

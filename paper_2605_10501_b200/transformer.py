@@ -1,0 +1,254 @@
+"""Section compute: Llama-style decoder blocks with explicit forward / backward on our kernels.
+
+No autograd and no torch compute ops on the hot path: every FLOP goes through the tcgen05
+GEMM (dense.py), the attention kernels (attention.py) or the memory-bound kernels
+(kernels.py).  torch only allocates buffers and owns streams.
+
+A block is   h1 = x + a ; y1 = rmsnorm(h1) ; qkv = y1 Wqkv^T ; rope ; o = attn(qkv)
+             h2 = h1 + o Wo^T ; y2 = rmsnorm(h2) ; gu = y2 Wgu^T ; s = silu(g) u ; a' = s Wd^T
+with the residual add fused into the following norm.  Parameters of a section live in one
+flat arena (fp32 master, bf16 working copy, fp32 grad, Adam m/v) so the optimizer and the
+gradient all-reduce are single launches over contiguous memory.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import attention as A
+from . import dense as D
+from . import kernels as K
+
+
+@dataclass(frozen=True)
+class Shape:
+    d: int
+    layers: int
+    heads: int
+    kv_heads: int
+    ffn: int
+    vocab: int
+    head_dim: int = 64
+    tied: bool = False
+    eps: float = 1e-5
+    rope_base: float = 10000.0
+    causal: bool = True
+
+    @property
+    def qkv_dim(self) -> int:
+        return (self.heads + 2 * self.kv_heads) * self.head_dim
+
+    def param_shapes(self):
+        out = [("embed", (self.vocab, self.d))]
+        for i in range(self.layers):
+            out += [
+                (f"l{i}.ln1", (self.d,)), (f"l{i}.wqkv", (self.qkv_dim, self.d)),
+                (f"l{i}.wo", (self.d, self.heads * self.head_dim)), (f"l{i}.ln2", (self.d,)),
+                (f"l{i}.wgu", (2 * self.ffn, self.d)), (f"l{i}.wd", (self.d, self.ffn)),
+            ]
+        out.append(("lnf", (self.d,)))
+        if not self.tied:
+            out.append(("head", (self.vocab, self.d)))
+        return out
+
+    def n_params(self) -> int:
+        return sum(math.prod(s) for _, s in self.param_shapes())
+
+    def fwd_flops_per_token(self, seq_len: int, with_head: bool = True) -> float:
+        """Model FLOPs of one forward token (GEMMs + causal attention at seq_len)."""
+        lin = self.layers * (self.d * self.qkv_dim + self.heads * self.head_dim * self.d + 3 * self.d * self.ffn)
+        attn = self.layers * 4 * self.heads * self.head_dim * seq_len * (0.5 if self.causal else 1.0)
+        head = self.vocab * self.d if with_head else 0
+        return 2.0 * (lin + head) + attn
+
+
+SHAPES = {
+    # cfg 2: TinyLlama-1.1B-shaped teacher, 125M-class student (tied embeddings)
+    "kd_teacher_1b": Shape(d=2048, layers=22, heads=32, kv_heads=4, ffn=5632, vocab=32000),
+    "kd_student_125m": Shape(d=768, layers=12, heads=12, kv_heads=12, ffn=3072, vocab=32000, tied=True),
+    # cfg 1: 2-layer GPT backbone (d=768) and ViT-tiny encoder (bidirectional, no vocab)
+    "vlm_gpt2l": Shape(d=768, layers=2, heads=12, kv_heads=12, ffn=3072, vocab=32768),
+    "vit_tiny": Shape(d=192, layers=12, heads=3, kv_heads=3, ffn=768, vocab=8, causal=False),
+    # tiny shapes for tests
+    "test_tiny": Shape(d=128, layers=2, heads=2, kv_heads=1, ffn=256, vocab=512),
+}
+
+
+def _align(n: int, a: int = 64) -> int:
+    return (n + a - 1) // a * a
+
+
+class FlatParams:
+    """Parameters of one section in contiguous arenas."""
+
+    def __init__(self, shapes, device, trainable: bool, seed: int, std: float = 0.02):
+        self.index = {}
+        off = 0
+        for name, shp in shapes:
+            n = math.prod(shp)
+            self.index[name] = (off, shp)
+            off += _align(n)
+        self.numel = _align(off, 256)
+        self.trainable = trainable
+        g = torch.Generator(device=device).manual_seed(seed)
+        master = torch.empty(self.numel, device=device, dtype=torch.float32)
+        master.normal_(0.0, std, generator=g)
+        for name, (o, shp) in self.index.items():
+            if len(shp) == 1:  # norm gains
+                master[o: o + shp[0]] = 1.0
+        self.w = master.to(torch.bfloat16)
+        if trainable:
+            self.master = master
+            self.grad = torch.zeros_like(master)
+            self.m = torch.zeros_like(master)
+            self.v = torch.zeros_like(master)
+        else:
+            del master
+            self.master = self.grad = self.m = self.v = None
+        self.step = 0
+
+    def _view(self, buf, name):
+        o, shp = self.index[name]
+        return buf[o: o + math.prod(shp)].view(*shp)
+
+    def __getitem__(self, name):
+        return self._view(self.w, name)
+
+    def g(self, name):
+        return self._view(self.grad, name)
+
+    def zero_grad(self):
+        self.grad.zero_()
+
+    def adamw(self, lr: float, wd: float = 0.1, gscale: float = 1.0):
+        self.step += 1
+        K.adamw(self.master, self.grad, self.m, self.v, self.w, lr, self.step, wd=wd, gscale=gscale)
+
+
+def rope_table(max_pos: int, head_dim: int, base: float, device) -> torch.Tensor:
+    inv = base ** (-torch.arange(0, head_dim, 2, dtype=torch.float64) / head_dim)
+    ang = torch.arange(max_pos, dtype=torch.float64)[:, None] * inv[None, :]
+    return torch.stack([ang.cos(), ang.sin()], -1).to(torch.float32).to(device).contiguous()
+
+
+@dataclass
+class Batch:
+    """One packed micro-batch: token ids [T] int32, cu_seqlens [n+1] int32, positions [T]."""
+
+    ids: torch.Tensor
+    cu: torch.Tensor
+    pos: torch.Tensor
+    max_len: int
+
+    @property
+    def T(self) -> int:
+        return self.ids.shape[0]
+
+
+class Transformer:
+    """Explicit fwd/bwd of a decoder (or, with causal=False, encoder) stack."""
+
+    def __init__(self, shape: Shape, params: FlatParams, device, max_pos: int = 8192):
+        self.s = shape
+        self.p = params
+        self.device = device
+        self.cs = rope_table(max_pos, shape.head_dim, shape.rope_base, device)
+        self.scale = 1.0 / math.sqrt(shape.head_dim)
+
+    # -------------------------------------------------------------------- forward
+    def forward(self, b: Batch, x0: torch.Tensor | None = None, save: bool = True):
+        """Returns (yf [T, d] final-normed hidden, ctx for backward).  x0 overrides the embedding."""
+        s, p, T = self.s, self.p, b.T
+        dev, bf = self.device, torch.bfloat16
+        if x0 is None:
+            x0 = torch.empty(T, s.d, device=dev, dtype=bf)
+            K.embed(p["embed"], b.ids, x0)
+        ctx = {"b": b, "layers": [], "x0": x0}
+        x, a = x0, None
+        H, Hk, dh = s.heads, s.kv_heads, s.head_dim
+        for i in range(s.layers):
+            h1 = torch.empty(T, s.d, device=dev, dtype=bf) if a is not None else x
+            y1 = torch.empty(T, s.d, device=dev, dtype=bf)
+            r1 = torch.empty(T, device=dev, dtype=torch.float32)
+            K.add_rmsnorm(x, a, h1, y1, p[f"l{i}.ln1"], r1, s.eps)
+            qkv = D.linear_fwd(y1, p[f"l{i}.wqkv"])
+            K.rope(qkv[:, : (H + Hk) * dh], b.pos, self.cs, H + Hk, dh)
+            q = qkv[:, : H * dh].view(T, H, dh)
+            k = qkv[:, H * dh: (H + Hk) * dh].view(T, Hk, dh)
+            v = qkv[:, (H + Hk) * dh:].view(T, Hk, dh)
+            o = torch.empty(T, H, dh, device=dev, dtype=bf)
+            lse = A.attn_fwd(q, k, v, b.cu, b.max_len, s.causal, o, self.scale)
+            ao = D.linear_fwd(o.view(T, H * dh), p[f"l{i}.wo"])
+            h2 = torch.empty(T, s.d, device=dev, dtype=bf)
+            y2 = torch.empty(T, s.d, device=dev, dtype=bf)
+            r2 = torch.empty(T, device=dev, dtype=torch.float32)
+            K.add_rmsnorm(h1, ao, h2, y2, p[f"l{i}.ln2"], r2, s.eps)
+            gu = D.linear_fwd(y2, p[f"l{i}.wgu"])
+            sw = torch.empty(T, s.ffn, device=dev, dtype=bf)
+            K.swiglu(gu, sw)
+            mo = D.linear_fwd(sw, p[f"l{i}.wd"])
+            if save:
+                ctx["layers"].append((h1, r1, y1, qkv, o, lse, h2, r2, y2, gu, sw))
+            x, a = h2, mo
+        hf = torch.empty(T, s.d, device=dev, dtype=bf)
+        yf = torch.empty(T, s.d, device=dev, dtype=bf)
+        rf = torch.empty(T, device=dev, dtype=torch.float32)
+        K.add_rmsnorm(x, a, hf, yf, p["lnf"], rf, s.eps)
+        ctx["final"] = (hf, rf, yf)
+        return yf, ctx
+
+    def head_weight(self):
+        return self.p["embed"] if self.s.tied else self.p["head"]
+
+    def logits(self, yf: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        return D.linear_fwd(yf, self.head_weight(), out)
+
+    # -------------------------------------------------------------------- backward
+    def backward(self, ctx, dlogits: torch.Tensor | None = None, dyf: torch.Tensor | None = None,
+                 need_dx0: bool = False):
+        """Accumulates parameter grads (fp32) from dlogits (or dyf); returns dx0 if asked."""
+        s, p, b = self.s, self.p, ctx["b"]
+        T, dev, bf = b.T, self.device, torch.bfloat16
+        H, Hk, dh = s.heads, s.kv_heads, s.head_dim
+        hf, rf, yf = ctx["final"]
+        if dlogits is not None:
+            hw = "embed" if s.tied else "head"
+            dyf = D.linear_dgrad(dlogits, p[hw])
+            D.linear_wgrad(dlogits, yf, p.g(hw))
+        dh_ = torch.empty(T, s.d, device=dev, dtype=bf)
+        K.rmsnorm_bwd(dyf, hf, p["lnf"], rf, None, dh_, p.g("lnf"))
+        for i in reversed(range(s.layers)):
+            h1, r1, y1, qkv, o, lse, h2, r2, y2, gu, sw = ctx["layers"][i]
+            # MLP
+            dsw = D.linear_dgrad(dh_, p[f"l{i}.wd"])
+            D.linear_wgrad(dh_, sw, p.g(f"l{i}.wd"))
+            dgu = torch.empty_like(gu)
+            K.swiglu_bwd(dsw, gu, dgu)
+            D.linear_wgrad(dgu, y2, p.g(f"l{i}.wgu"))
+            dy2 = D.linear_dgrad(dgu, p[f"l{i}.wgu"])
+            dh2 = torch.empty(T, s.d, device=dev, dtype=bf)
+            K.rmsnorm_bwd(dy2, h2, p[f"l{i}.ln2"], r2, dh_, dh2, p.g(f"l{i}.ln2"))
+            # attention
+            do = D.linear_dgrad(dh2, p[f"l{i}.wo"])
+            D.linear_wgrad(dh2, o.view(T, H * dh), p.g(f"l{i}.wo"))
+            dqkv = torch.empty_like(qkv)
+            q = qkv[:, : H * dh].view(T, H, dh)
+            k = qkv[:, H * dh: (H + Hk) * dh].view(T, Hk, dh)
+            v = qkv[:, (H + Hk) * dh:].view(T, Hk, dh)
+            dq = dqkv[:, : H * dh].view(T, H, dh)
+            dk = dqkv[:, H * dh: (H + Hk) * dh].view(T, Hk, dh)
+            dv = dqkv[:, (H + Hk) * dh:].view(T, Hk, dh)
+            A.attn_bwd(do.view(T, H, dh), q, k, v, o, lse, b.cu, b.max_len, s.causal, dq, dk, dv, self.scale)
+            K.rope(dqkv[:, : (H + Hk) * dh], b.pos, self.cs, H + Hk, dh, backward=True)
+            D.linear_wgrad(dqkv, y1, p.g(f"l{i}.wqkv"))
+            dy1 = D.linear_dgrad(dqkv, p[f"l{i}.wqkv"])
+            dh1 = torch.empty(T, s.d, device=dev, dtype=bf)
+            K.rmsnorm_bwd(dy1, h1, p[f"l{i}.ln1"], r1, dh2, dh1, p.g(f"l{i}.ln1"))
+            dh_ = dh1
+        if need_dx0:
+            return dh_
+        K.embed_bwd(dh_, b.ids, p.g("embed"))
+        return None

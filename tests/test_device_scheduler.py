@@ -193,31 +193,39 @@ def test_full_size_vs_oracle(B, dp, fan, policy, quant):
         assert tuple(float.hex(float(x)) for x in m[r]) == tuple(float.hex(x) for x in oracle.rank_metrics(t, o, policy))
 
 
-def test_varlen_pack():
+def test_varlen_pack_and_pack_tokens():
     import torch
 
     from paper_2605_10501_b200 import _native as N
 
     rng = np.random.default_rng(0)
-    B, n, mbs = 100, 37, 4
-    lens = rng.integers(1, 500, B).astype(np.int32)
-    order = rng.permutation(B)[:n].astype(np.int32)
-    d = lambda a: torch.from_numpy(a).cuda()  # noqa: E731
-    n_mb = -(-n // mbs)
-    mb, off = torch.zeros(n, dtype=torch.int32, device="cuda"), torch.zeros(n, dtype=torch.int32, device="cuda")
-    tot = torch.zeros(n_mb, dtype=torch.int32, device="cuda")
-    cu = torch.zeros(n_mb * (mbs + 1), dtype=torch.int32, device="cuda")
-    dord, dlen = d(order), d(lens)
-    N.check(N.lib().maestro_varlen_pack(N.ptr(dord), n, N.ptr(dlen), mbs, N.ptr(mb), N.ptr(off), N.ptr(tot),
-                                        N.ptr(cu), N.stream_ptr()), "varlen")
-    want_mb = np.arange(n) // mbs
-    want_off = np.zeros(n, np.int32)
-    for m in range(n_mb):
-        ks = np.arange(m * mbs, min(n, (m + 1) * mbs))
-        want_off[ks] = np.concatenate([[0], np.cumsum(lens[order[ks]])[:-1]])
-        assert tot[m].item() == lens[order[ks]].sum()
-    assert mb.cpu().numpy().tolist() == want_mb.tolist()
-    assert off.cpu().numpy().tolist() == want_off.tolist()
+    for B, n, mbs in ((100, 37, 4), (3000, 2100, 3), (64, 64, 64)):
+        lens = rng.integers(1, 500, B).astype(np.int32)
+        order = rng.permutation(B)[:n].astype(np.int32)
+        d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+        n_mb = -(-n // mbs)
+        z = lambda k: torch.zeros(k, dtype=torch.int32, device="cuda")  # noqa: E731
+        mb, off, tot, cu, start = z(n), z(n), z(n_mb), z(n_mb * (mbs + 1)), z(n_mb)
+        dord, dlen = d(order), d(lens)
+        N.check(N.lib().maestro_varlen_pack(N.ptr(dord), n, N.ptr(dlen), mbs, N.ptr(mb), N.ptr(off), N.ptr(tot),
+                                            N.ptr(cu), N.ptr(start), N.stream_ptr()), "varlen")
+        glob = np.concatenate([[0], np.cumsum(lens[order])[:-1]]).astype(np.int64)
+        assert mb.cpu().numpy().tolist() == (np.arange(n) // mbs).tolist()
+        assert off.cpu().numpy().tolist() == glob.tolist()
+        cu_h = cu.cpu().numpy().reshape(n_mb, mbs + 1)
+        for m in range(n_mb):
+            ks = np.arange(m * mbs, min(n, (m + 1) * mbs))
+            assert start[m].item() == glob[ks[0]]
+            assert tot[m].item() == lens[order[ks]].sum()
+            assert cu_h[m, : len(ks) + 1].tolist() == np.concatenate([[0], np.cumsum(lens[order[ks]])]).tolist()
+        # pack token ids of the ordered samples
+        L = int(lens.max())
+        ids = rng.integers(0, 1 << 20, (B, L)).astype(np.int32)
+        out = z(int(lens[order].sum()))
+        N.check(N.lib().maestro_pack_tokens(N.ptr(d(ids)), L, N.ptr(dord), N.ptr(dlen), N.ptr(off), n, N.ptr(out),
+                                            N.stream_ptr()), "pack")
+        want = np.concatenate([ids[i, : lens[i]] for i in order])
+        assert out.cpu().numpy().tolist() == want.tolist()
 
 
 def test_scatter_rows_bitexact_and_bwd():
