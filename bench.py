@@ -1,0 +1,302 @@
+"""Benchmark: training samples/s of the section-graph executor step (BASELINE.json metric).
+
+Workload (configs[1] of BASELINE.json): knowledge distillation, forward-only 1.1B teacher
+(TinyLlama shape) -> 125M student, fused KL over the 32k vocabulary, seq 2048, 64 samples per
+student DP rank, synthetic token ids, random-init weights.  At 1 GPU both sections are
+co-resident; at N GPUs the teacher and student run on disjoint GPU groups with an NCCL handoff
+of teacher hidden states (recipes.KD_LAYOUTS).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints one JSON line (rank 0).  `value` is device-timed (CUDA events, max over ranks) with
+inputs resident in HBM; `e2e` is the same metric through the public API (KDExecutor.step) with
+token ids in pinned host memory copied in and the loss read back every step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "training samples/sec (device-timed, max over ranks) at 1/2/4/8 B200; section-stall %"
+UNIT = "samples/s"
+SEQ = 2048
+BATCH_PER_RANK = 64
+MBS = 4
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = []
+        for line in Path(self.path).read_text().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8:
+                rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[4:8]) if v.lower().startswith("active")})
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+
+        sm = [num(r[0]) for r in rows if num(r[0]) is not None]
+        pw = [num(r[2]) for r in rows if num(r[2]) is not None]
+        loaded = [s for s, p in zip(sm, pw) if p is not None and p > 300] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": num(rows[0][1]), "reasons": reasons, "samples": len(rows),
+                "power_w_max": max(pw) if pw else None}
+
+
+# ---------------------------------------------------------------------------------------------- CPU leg
+def cpu_kd_step_sample(seq: int = SEQ, reps: int = 1):
+    """The oracle's fp32 CPU restatement of one KD training step on ONE sample (all host threads)."""
+    import torch
+
+    from oracle import torch_ref as R
+    from paper_2605_10501_b200.transformer import SHAPES
+
+    torch.set_num_threads(os.cpu_count() or 1)
+    t_shape, s_shape = SHAPES["kd_teacher_1b"], SHAPES["kd_student_125m"]
+    g = torch.Generator().manual_seed(0)
+
+    def flat(shape):
+        n = sum(((__import__("math").prod(s) + 63) // 64 * 64) for _, s in shape.param_shapes())
+        return torch.randn(n, generator=g) * 0.02
+
+    t_flat, s_flat = flat(t_shape), flat(s_shape)
+    t_head = torch.randn(t_shape.vocab, t_shape.d, generator=g) * 0.02
+    ids = torch.randint(0, 32000, (seq,), generator=g, dtype=torch.int32)
+    cu = torch.tensor([0, seq], dtype=torch.int32)
+    m, v = torch.zeros_like(s_flat), torch.zeros_like(s_flat)
+    times = []
+    for i in range(reps):
+        t0 = time.perf_counter()
+        _, grad = R.kd_step_reference(t_shape, s_shape, t_flat, s_flat, t_head, ids, cu, global_tokens=seq)
+        R.adamw_reference(s_flat, grad, m, v, 3e-4, i + 1)
+        times.append(time.perf_counter() - t0)
+    return min(times), torch.get_num_threads()
+
+
+def run_reference(args):
+    """--impl reference: the CPU implementation of the path (oracle port; the reference itself is
+    a planning/simulation toolkit with no training step), rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    secs = []
+    threads = 1
+    for _ in range(args.warmup + args.steps):
+        t, threads = cpu_kd_step_sample()
+        secs.append(t)
+    sec = statistics.mean(secs[args.warmup:]) if args.steps else secs[-1]
+    value = 1.0 / sec
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "kd_cfg2 (1.1B teacher fwd -> 125M student train, KL over 32k vocab, seq 2048)",
+                   "global_batch": 1, "seq_len": SEQ, "parallelism": "cpu"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": "1 sample of 2048 tokens per step: oracle/torch_ref.py fp32 KD step "
+                                   "(teacher fwd + colocated head, student fwd/bwd, KL, AdamW)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------------------- GPU leg
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--batch-per-rank", type=int, default=BATCH_PER_RANK)
+    ap.add_argument("--mbs", type=int, default=MBS)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
+
+    from paper_2605_10501_b200 import instrument
+    from paper_2605_10501_b200.executor import KDExecutor, synthetic_ids
+
+    ex = KDExecutor(n_gpus=args.gpus, batch_per_rank=args.batch_per_rank, seq=SEQ, mbs=args.mbs)
+    B = ex.batch
+    ids_host = torch.from_numpy(synthetic_ids(B, SEQ, 32000)).pin_memory()
+    ids_dev = ids_host.cuda()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        ex.step(ids_dev, want_loss=False)
+    barrier()
+    # ---- device-timed region (inputs resident in HBM)
+    clocks = ClockSampler(local)
+    clocks.start()
+    instrument.start_gemm_timing()
+    launches0 = instrument.launches
+    main_stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stalls, busy, span = [], 0.0, 0.0
+    e0.record(main_stream)
+    for _ in range(args.steps):
+        st = ex.step(ids_dev, want_loss=False)
+        stalls.append(st.stall_frac)
+        busy += st.critical_busy_ms
+        span += st.critical_span_ms
+    e1.record(main_stream)
+    barrier()
+    launches = instrument.launches - launches0
+    gemm_flops, gemm_ms, gemm_n = instrument.stop_gemm_timing()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], device="cuda")
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    ms_per_step = ms / max(args.steps, 1)
+    value = B * args.steps / (ms / 1e3)
+    # ---- end-to-end through the public API: ids from pinned host memory, loss read back
+    barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record()
+    losses = []
+    for _ in range(args.steps):
+        st = ex.step(ids_host, want_loss=True)
+        losses.append(st.loss)
+    f1.record()
+    barrier()
+    ems = f0.elapsed_time(f1)
+    t = torch.tensor([ems], device="cuda")
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_value = B * args.steps / (float(t.item()) / 1e3)
+    # ---- stall: max over critical ranks
+    stall = torch.tensor([max(stalls) if stalls and ex.student is not None else 0.0,
+                          (1 - busy / span) if span > 0 else 0.0], device="cuda")
+    if dist is not None:
+        dist.all_reduce(stall, op=dist.ReduceOp.MAX)
+    peaks, peak_kind = load_peaks()
+    gemm_tflops = (gemm_flops / (gemm_ms / 1e3) / 1e12) if gemm_ms > 0 else None
+    peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+    traffic = None
+    prof = ROOT / "profiles" / "gemm_traffic.json"
+    if prof.exists():
+        traffic = json.loads(prof.read_text()).get("traffic_bytes_per_launch")
+    cpu = None
+    if rank == 0 and args.gpus == 1 and not args.no_cpu_baseline:
+        try:
+            sec, threads = cpu_kd_step_sample()
+            cpu = {"value": 1.0 / sec, "unit": UNIT, "cores": threads, "kind": "port",
+                   "sample": "1 sample of 2048 tokens: oracle/torch_ref.py fp32 KD step on the host CPU "
+                             "(teacher fwd + colocated head, student fwd/bwd, KL, AdamW)"}
+        except Exception as exc:  # noqa: BLE001
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {exc}"}
+    if rank == 0:
+        dp_s, dp_t, _ = __import__("paper_2605_10501_b200.recipes", fromlist=["KD_LAYOUTS"]).KD_LAYOUTS[args.gpus]
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {
+                "workload": "kd_cfg2: fwd-only 1.1B teacher (TinyLlama shape) -> 125M student, fused KL over "
+                            "32k vocab, seq 2048, teacher head colocated with the student",
+                "global_batch": B, "seq_len": SEQ, "micro_batch": args.mbs,
+                "parallelism": ("colocated teacher+student" if args.gpus == 1
+                                else f"teacher dp{dp_t} -> student dp{dp_s} (fanout 1, NCCL handoff)"),
+                "l2": "inputs larger than L2 (teacher weights 2.2 GB, logits 1 GB per micro-batch)",
+            },
+            "section_stall_pct": 100.0 * float(stall[0].item()),
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(B * SEQ * 4),
+                    "d2h_bytes_per_step": 4 + 8 * 64},
+            "gpu_launches": launches // max(args.steps, 1),
+            "roofline": {"bound": "tensor", "kernel": "maestro tcgen05 GEMM (csrc/gemm.cu)",
+                         "achieved": gemm_tflops, "peak": peak, "unit": "TFLOP/s",
+                         "frac": (gemm_tflops / peak) if gemm_tflops else None, "traffic": traffic,
+                         "peak_kind": f"{peak_kind} bf16_tflops_sustained",
+                         "launches_timed": gemm_n, "share_of_step": gemm_ms / ms if ms > 0 else None},
+            "model_tflops": ex.model_flops_per_step() * args.steps / (ms / 1e3) / 1e12,
+            "clocks": clk,
+            "cpu_baseline": cpu,
+            "loss": losses[-1] if losses else None,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -95,6 +95,9 @@ def extra_symbols(names):
 def check(rc: int, what: str) -> None:
     if rc != 0:
         raise E.NativeError(f"{what} failed with CUDA error {rc}")
+    from . import instrument
+
+    instrument.count(what)
 
 
 def ptr(t) -> int:

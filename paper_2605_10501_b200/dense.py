@@ -12,6 +12,7 @@ import ctypes
 import torch
 
 from . import _native as N
+from . import instrument
 
 EPI_BF16, EPI_F32, EPI_F32_ACC = 0, 1, 2
 
@@ -37,9 +38,16 @@ def gemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, M: int, N_: int, K: 
         ldb = b.stride(0)
     if ldc is None:
         ldc = c.stride(0)
+    rec = instrument.gemm_timing
+    if rec is not None:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
     rc = _lib().maestro_gemm_bf16(N.ptr(a), N.ptr(b), N.ptr(c), M, N_, K, lda, ldb, ldc, int(a_mn), int(b_mn),
                                   epi, N.stream_ptr())
     N.check(rc, "gemm_bf16")
+    if rec is not None:
+        e1.record()
+        rec.append((2.0 * M * N_ * K, e0, e1))
     return c
 
 
