@@ -1,44 +1,63 @@
-"""Varlen (packed, cu_seqlens) causal / bidirectional attention with GQA: forward + backward.
+"""Varlen (packed, cu_seqlens) attention with GQA on tcgen05/TMEM (K8, csrc/attention.cu).
 
 Layout: q [T, H, dh], k/v [T, Hkv, dh] (row-pitched views into the fused QKV buffer),
-o [T, H, dh] bf16, lse [H, T] fp32 (natural log of the softmax denominator of the scaled
-scores).  Backward writes dq/dk/dv into the fused dQKV buffer views.
-
-Round-1 status: the forward/backward are served by the flash-attn 2 library kernels
-(sm_100 build shipped in the image), wrapped behind this interface; the hand-written
-tcgen05/TMEM replacement (csrc/attention.cu) is the next kernel in DESIGN.md and plugs in
-here without touching the callers.
+o [T, H, dh] bf16, lse [H, T] fp32 (natural log-sum-exp of the scaled scores).  The backward
+writes dq/dk/dv straight into the fused dQKV buffer views.  head_dim 64.
 """
 
 from __future__ import annotations
 
+import ctypes
+
 import torch
 
-_fa = None
+from . import _native as N
+
+_P, _I32, _F = ctypes.c_void_p, ctypes.c_int32, ctypes.c_float
+_bound = None
 
 
 def _lib():
-    global _fa
-    if _fa is None:
-        from flash_attn import flash_attn_interface as fa
+    global _bound
+    if _bound is None:
+        _bound = N.extra_symbols({
+            "maestro_attn_workspace": ([_I32, _I32], ctypes.c_int64),
+            "maestro_attn_bwd_workspace": ([_I32, _I32, _I32], ctypes.c_int64),
+            "maestro_attn_fwd": ([_P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P, _I32, _P, _F,
+                                  _I32, _P, _P], ctypes.c_int),
+            "maestro_attn_bwd": ([_P, _I32, _P, _P, _P, _P, _I32, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _I32,
+                                  _I32, _P, _I32, _P, _I32, _P, _I32, _F, _I32, _P, _P], ctypes.c_int),
+        })
+    return _bound
 
-        _fa = fa
-    return _fa
+
+def _ws(nbytes: int, device) -> torch.Tensor:
+    return torch.empty((nbytes + 255) // 256 * 256, dtype=torch.uint8, device=device)
 
 
 def attn_fwd(q, k, v, cu, max_len: int, causal: bool, out, scale: float):
-    """Returns lse [H, T] fp32; writes out."""
-    fa = _lib()
-    o, lse, _, _ = fa._flash_attn_varlen_forward(q, k, v, cu, cu, max_len, max_len, 0.0, scale, causal)
-    out.copy_(o)
+    """Writes out [T, H, dh]; returns lse [H, T] fp32."""
+    L = _lib()
+    T, H, dh = q.shape
+    Hk = k.shape[1]
+    nseq = cu.numel() - 1
+    lse = torch.empty(H, T, dtype=torch.float32, device=q.device)
+    ws = _ws(L.maestro_attn_workspace(T, nseq), q.device)
+    rc = L.maestro_attn_fwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), cu.data_ptr(), nseq, T, H, Hk, dh,
+                            q.stride(0), k.stride(0), v.stride(0), out.data_ptr(), out.stride(0), lse.data_ptr(),
+                            scale, int(causal), ws.data_ptr(), N.stream_ptr())
+    N.check(rc, "attn_fwd")
     return lse
 
 
 def attn_bwd(do, q, k, v, o, lse, cu, max_len: int, causal: bool, dq, dk, dv, scale: float):
-    fa = _lib()
-    dq_, dk_, dv_ = (torch.empty(t.shape, device=t.device, dtype=t.dtype) for t in (dq, dk, dv))
-    fa._flash_attn_varlen_backward(do.contiguous(), q, k, v, o, lse, dq_, dk_, dv_, cu, cu, max_len, max_len, 0.0,
-                                   scale, causal, -1, -1, 0.0, None, False)
-    dq.copy_(dq_)
-    dk.copy_(dk_)
-    dv.copy_(dv_)
+    L = _lib()
+    T, H, dh = q.shape
+    Hk = k.shape[1]
+    nseq = cu.numel() - 1
+    ws = _ws(L.maestro_attn_bwd_workspace(T, nseq, H), q.device)
+    rc = L.maestro_attn_bwd(do.data_ptr(), do.stride(0), q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
+                            o.stride(0), lse.data_ptr(), cu.data_ptr(), nseq, T, H, Hk, dh, q.stride(0), k.stride(0),
+                            v.stride(0), dq.data_ptr(), dq.stride(0), dk.data_ptr(), dk.stride(0), dv.data_ptr(),
+                            dv.stride(0), scale, int(causal), ws.data_ptr(), N.stream_ptr())
+    N.check(rc, "attn_bwd")

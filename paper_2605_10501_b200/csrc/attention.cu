@@ -1,0 +1,720 @@
+// K8: varlen (cu_seqlens) attention with GQA on tcgen05/TMEM, head_dim 64, causal or not.
+//
+// Forward, one CTA per (128-row query tile, head), warp-specialised:
+//   w0     TMA producer: Q tile once, then K/V tiles through a 3-stage ring (SWIZZLE_128B)
+//   w1     MMA issuer:   S_i = Q K_i^T into one of two TMEM score buffers (M=128, N=128, K=64),
+//                        then O += P_{i-1} V_{i-1} (M=128, N=64, K=128; P from smem, V MN-major),
+//                        so the tensor core computes S_i while the softmax warps work on S_{i-1}
+//   w2..w5 softmax:      one thread per query row: tcgen05.ld its 128 scores, mask, online
+//                        softmax in the log2 domain with lazy rescaling (O in TMEM is rescaled
+//                        only when the row max grows by more than 2^8), write P (bf16) into the
+//                        swizzled smem operand, and finally O / l -> bf16 rows + LSE.
+// TMEM: S0 cols [0,128), S1 [128,256), O [256,320).
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+#include "sm100.cuh"
+#include "tma_host.cuh"
+
+namespace mb {
+namespace {
+
+using namespace sm100;
+
+constexpr int DH = 64;
+constexpr int BQ = 128, BKV = 128, KV_STAGES = 3;
+constexpr int TILE_BYTES = 128 * DH * 2;  // 16 KB (128 rows x 128 B)
+constexpr int P_BYTES = BQ * BKV * 2;     // 32 KB (two 64-col chunks)
+constexpr int FWD_THREADS = 192;
+constexpr float LOG2E_F = 1.4426950408889634f;
+constexpr float LN2_F = 0.6931471805599453f;
+
+struct FwdSmem {
+  static constexpr int Q = 0;
+  static constexpr int K = Q + TILE_BYTES;
+  static constexpr int V = K + KV_STAGES * TILE_BYTES;
+  static constexpr int P = V + KV_STAGES * TILE_BYTES;
+  static constexpr int BAR = P + 2 * P_BYTES;
+  static constexpr int TOTAL = BAR + 256;
+};
+
+// Query-tile list, heaviest (largest causal row count) first: tiles[i] = (seq, q0)
+__global__ void attn_tiles_kernel(const int32_t* __restrict__ cu, int nseq, int2* __restrict__ tiles,
+                                  int* __restrict__ count) {
+  __shared__ int s_max, s_n;
+  if (threadIdx.x == 0) {
+    s_max = 0;
+    s_n = 0;
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < nseq; j += blockDim.x) atomicMax(&s_max, (cu[j + 1] - cu[j] + BQ - 1) / BQ);
+  __syncthreads();
+  for (int qb = s_max - 1; qb >= 0; --qb) {
+    for (int j0 = 0; j0 < nseq; j0 += blockDim.x) {
+      const int j = j0 + threadIdx.x;
+      const bool has = j < nseq && (cu[j + 1] - cu[j] + BQ - 1) / BQ > qb;
+      const unsigned bal = __ballot_sync(kFull, has);
+      // warp-aggregated append (order inside a qb level is irrelevant)
+      int base = 0;
+      if ((threadIdx.x & 31) == 0 && bal) base = atomicAdd(&s_n, __popc(bal));
+      base = __shfl_sync(kFull, base, 0);
+      if (has) tiles[base + __popc(bal & ((1u << (threadIdx.x & 31)) - 1u))] = make_int2(j, qb * BQ);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *count = s_n;
+}
+
+__device__ __forceinline__ uint32_t p_offset(int r, int c) {
+  // (row r, col c) of a 128 x 128 bf16 operand stored as two K-major SWIZZLE_128B chunks
+  const int chunk = c >> 6, cc = c & 63;
+  return (uint32_t)(chunk * 16384 + r * 128 + ((((cc >> 3) ^ (r & 7)) << 4)) + ((cc & 7) << 1));
+}
+
+template <bool CAUSAL>
+__global__ void __launch_bounds__(FWD_THREADS, 1)
+    attn_fwd_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
+                    const __grid_constant__ CUtensorMap map_v, const int32_t* __restrict__ cu,
+                    const int2* __restrict__ tiles, const int* __restrict__ n_tiles, __nv_bfloat16* __restrict__ out,
+                    int ldo, float* __restrict__ lse, int T, int H, int Hk, float scale2) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + FwdSmem::BAR);
+  uint64_t* q_full = bar;
+  uint64_t* k_full = bar + 1;
+  uint64_t* k_empty = k_full + KV_STAGES;
+  uint64_t* v_full = k_empty + KV_STAGES;
+  uint64_t* v_empty = v_full + KV_STAGES;
+  uint64_t* s_full = v_empty + KV_STAGES;
+  uint64_t* s_empty = s_full + 2;
+  uint64_t* p_full = s_empty + 2;
+  uint64_t* p_empty = p_full + 2;
+  uint64_t* o_full = p_empty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 1);
+
+  const int tile = blockIdx.x;
+  if (tile >= *n_tiles) return;
+  const int2 tq = tiles[tile];
+  const int seq = tq.x, q0 = tq.y;
+  const int h = blockIdx.y, hk = h / (H / Hk);
+  const int s0 = cu[seq], L = cu[seq + 1] - s0;
+  const int n_kv_all = (L + BKV - 1) / BKV;
+  const int n_kv = CAUSAL ? min(n_kv_all, q0 / BKV + 1) : n_kv_all;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&map_q);
+    tma_prefetch(&map_k);
+    tma_prefetch(&map_v);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < KV_STAGES; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&s_full[b], 1);
+      mbar_init(&s_empty[b], 128);
+      mbar_init(&p_full[b], 128);
+      mbar_init(&p_empty[b], 1);
+    }
+    mbar_init(o_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(q_full, TILE_BYTES);
+      tma_load_2d(sm + FwdSmem::Q, &map_q, q_full, h * DH, s0 + q0);
+      for (int i = 0; i < n_kv; ++i) {
+        const int st = i % KV_STAGES;
+        const uint32_t ph = (i / KV_STAGES) & 1;
+        mbar_wait(&k_empty[st], ph ^ 1);
+        mbar_arrive_expect_tx(&k_full[st], TILE_BYTES);
+        tma_load_2d(sm + FwdSmem::K + st * TILE_BYTES, &map_k, &k_full[st], hk * DH, s0 + i * BKV);
+        mbar_wait(&v_empty[st], ph ^ 1);
+        mbar_arrive_expect_tx(&v_full[st], TILE_BYTES);
+        tma_load_2d(sm + FwdSmem::V + st * TILE_BYTES, &map_v, &v_full[st], hk * DH, s0 + i * BKV);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = idesc_bf16_f32(BQ, BKV, false, false);
+      constexpr uint32_t idesc_o = idesc_bf16_f32(BQ, DH, false, true);
+      const uint32_t q_base = smem_u32(sm + FwdSmem::Q);
+      auto issue_pv = [&](int j) {
+        const int pb = j & 1;
+        mbar_wait(&p_full[pb], (j >> 1) & 1);
+        mbar_wait(&v_full[j % KV_STAGES], (j / KV_STAGES) & 1);
+        tc_fence_after();
+        const uint32_t p_base = smem_u32(sm + FwdSmem::P + pb * P_BYTES);
+        const uint32_t v_base = smem_u32(sm + FwdSmem::V + (j % KV_STAGES) * TILE_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < BKV / 16; ++kk) {
+          const uint64_t ad = smem_desc_sw128(p_base + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024);
+          const uint64_t bd = smem_desc_sw128(v_base + kk * 2048, 8192, 1024);
+          umma_bf16(tmem + 256, ad, bd, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        umma_commit(&v_empty[j % KV_STAGES]);
+        umma_commit(&p_empty[pb]);
+      };
+      mbar_wait(q_full, 0);
+      for (int i = 0; i < n_kv; ++i) {
+        const int b = i & 1;
+        const int st = i % KV_STAGES;
+        mbar_wait(&k_full[st], (i / KV_STAGES) & 1);
+        mbar_wait(&s_empty[b], ((i >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t k_base = smem_u32(sm + FwdSmem::K + st * TILE_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          const uint64_t ad = smem_desc_sw128(q_base + kk * 32, 16, 1024);
+          const uint64_t bd = smem_desc_sw128(k_base + kk * 32, 16, 1024);
+          umma_bf16(tmem + b * BKV, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
+        }
+        umma_commit(&k_empty[st]);
+        umma_commit(&s_full[b]);
+        if (i >= 1) issue_pv(i - 1);
+      }
+      issue_pv(n_kv - 1);
+      umma_commit(o_full);
+    }
+  } else {
+    // ---------------- softmax / correction / epilogue: thread = query row
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const int qpos = q0 + r;
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    float m = -INFINITY, l = 0.f;
+    unsigned char* pbuf = sm + FwdSmem::P;
+    for (int i = 0; i < n_kv; ++i) {
+      const int b = i & 1;
+      mbar_wait(&s_full[b], (i >> 1) & 1);
+      tc_fence_after();
+      float s[BKV];
+#pragma unroll
+      for (int c = 0; c < BKV / 32; ++c) {
+        uint32_t rr[32];
+        tmem_ld_32x32b_x32(tmem + lane_base + b * BKV + c * 32, rr);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) s[c * 32 + j] = __uint_as_float(rr[j]);
+      }
+      tc_fence_before();
+      mbar_arrive(&s_empty[b]);
+      const int kv0 = i * BKV;
+      const bool need_mask = (CAUSAL && kv0 + BKV - 1 > q0) || (kv0 + BKV > L);
+      float mx = -INFINITY;
+      if (need_mask) {
+#pragma unroll
+        for (int c = 0; c < BKV; ++c) {
+          const int kv = kv0 + c;
+          if ((CAUSAL && kv > qpos) || kv >= L) s[c] = -INFINITY;
+          mx = fmaxf(mx, s[c]);
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < BKV; ++c) mx = fmaxf(mx, s[c]);
+      }
+      const float m_new = mx * scale2;
+      bool rescale = false;
+      float alpha = 1.f;
+      if (m_new > m + 8.0f) {  // lazy rescale: keep a stale max unless it grew by > 2^8
+        alpha = exp2f(m - m_new);
+        m = m_new;
+        rescale = i > 0;
+      }
+      float rowsum = 0.f;
+#pragma unroll
+      for (int c = 0; c < BKV; ++c) {
+        s[c] = exp2f(s[c] * scale2 - m);
+        rowsum += s[c];
+      }
+      l = l * alpha + rowsum;
+      // P buffer b was last read by PV_{i-2}
+      if (i >= 2) mbar_wait(&p_empty[b], ((i >> 1) + 1) & 1);
+      if (rescale) {
+        mbar_wait(&p_empty[(i - 1) & 1], ((i - 1) >> 1) & 1);  // PV_{i-1} retired: O is final
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < DH / 32; ++c) {
+          uint32_t rr[32];
+          tmem_ld_32x32b_x32(tmem + lane_base + 256 + c * 32, rr);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) rr[j] = __float_as_uint(__uint_as_float(rr[j]) * alpha);
+          tmem_st_32x32b_x32(tmem + lane_base + 256 + c * 32, rr);
+        }
+        tmem_st_wait();
+      }
+      unsigned char* pb = pbuf + b * P_BYTES;
+#pragma unroll
+      for (int u = 0; u < BKV / 8; ++u) {
+        uint4 v;
+        v.x = pack_bf16(s[8 * u + 0], s[8 * u + 1]);
+        v.y = pack_bf16(s[8 * u + 2], s[8 * u + 3]);
+        v.z = pack_bf16(s[8 * u + 4], s[8 * u + 5]);
+        v.w = pack_bf16(s[8 * u + 6], s[8 * u + 7]);
+        *reinterpret_cast<uint4*>(pb + p_offset(r, 8 * u)) = v;
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(&p_full[b]);
+    }
+    mbar_wait(o_full, 0);
+    tc_fence_after();
+    const float inv_l = 1.f / l;
+    uint32_t o[DH / 2];
+#pragma unroll
+    for (int c = 0; c < DH / 32; ++c) {
+      uint32_t rr[32];
+      tmem_ld_32x32b_x32(tmem + lane_base + 256 + c * 32, rr);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        o[c * 16 + j] = pack_bf16(__uint_as_float(rr[2 * j]) * inv_l, __uint_as_float(rr[2 * j + 1]) * inv_l);
+    }
+    if (qpos < L) {
+      uint4* dst = reinterpret_cast<uint4*>(out + (size_t)(s0 + qpos) * ldo + h * DH);
+#pragma unroll
+      for (int u = 0; u < DH / 8; ++u) dst[u] = make_uint4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);
+      lse[(size_t)h * T + s0 + qpos] = (m + log2f(l)) * LN2_F;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+
+// ==========================================================================================
+// Backward, one CTA per (128-row KV tile, KV head); loops over the query heads of the GQA group
+// and the query tiles the tile can see.  Thread r of the 4 "softmax" warps owns KV row r:
+//   S^T = K Q^T, dP^T = V dO^T                      (TMEM, M = kv, N = q)
+//   P^T = exp2(S^T * scale2 - lse2[q]),  dS^T = P^T (dP^T - D[q])   -> bf16 smem operands
+//   dV += P^T dO, dK += dS^T Q                      (TMEM accumulators across all tiles)
+//   dQ_tile = dS K                                  (TMEM, drained with red.global.add.v4.f32)
+// TMEM: S^T [0,128), dP^T [128,256), dV [256,320), dK [320,384), dQ [384,448).
+constexpr int BWD_THREADS = 192;
+
+struct BwdSmem {
+  static constexpr int K = 0;
+  static constexpr int V = K + TILE_BYTES;
+  static constexpr int QD = V + TILE_BYTES;                 // 2 stages x (Q tile, dO tile)
+  static constexpr int PT = QD + 2 * 2 * TILE_BYTES;        // P^T  [kv][q] bf16, 2 chunks
+  static constexpr int DST = PT + P_BYTES;                  // dS^T [kv][q] bf16, 2 chunks
+  static constexpr int LSE = DST + P_BYTES;                 // 2 x 128 fp32 (double-buffered by tile)
+  static constexpr int DD = LSE + 1024;                     // 2 x 128 fp32
+  static constexpr int BAR = DD + 1024;
+  static constexpr int TOTAL = BAR + 256;
+};
+
+__device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
+
+template <bool CAUSAL>
+__global__ void __launch_bounds__(BWD_THREADS, 1)
+    attn_bwd_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
+                    const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_do,
+                    const int32_t* __restrict__ cu, const int2* __restrict__ tiles, const int* __restrict__ n_tiles,
+                    const float* __restrict__ lse, const float* __restrict__ Dvec, float* __restrict__ dq_acc,
+                    __nv_bfloat16* __restrict__ dk, int lddk, __nv_bfloat16* __restrict__ dv, int lddv, int T, int H,
+                    int Hk, float scale2, float scale) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + BwdSmem::BAR);
+  uint64_t* kv_full = bar;
+  uint64_t* qd_full = bar + 1;      // [2]
+  uint64_t* qd_empty = bar + 3;     // [2]
+  uint64_t* sp_full = bar + 5;
+  uint64_t* sp_empty = bar + 6;
+  uint64_t* ds_full = bar + 7;
+  uint64_t* ds_empty = bar + 8;
+  uint64_t* dq_full = bar + 9;
+  uint64_t* dq_empty = bar + 10;
+  uint64_t* dkv_full = bar + 11;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+  float* s_lse = reinterpret_cast<float*>(sm + BwdSmem::LSE);
+  float* s_D = reinterpret_cast<float*>(sm + BwdSmem::DD);
+
+  const int tile = blockIdx.x;
+  if (tile >= *n_tiles) return;
+  const int2 tk = tiles[tile];
+  const int seq = tk.x, kv0 = tk.y;
+  const int hk = blockIdx.y, G = H / Hk;
+  const int s0 = cu[seq], L = cu[seq + 1] - s0;
+  const int n_q_all = (L + BQ - 1) / BQ;
+  const int qt_first = CAUSAL ? kv0 / BQ : 0;
+  const int n_q = n_q_all - qt_first;
+  const int n_it = G * n_q;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&map_q);
+    tma_prefetch(&map_k);
+    tma_prefetch(&map_v);
+    tma_prefetch(&map_do);
+    mbar_init(kv_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&qd_full[b], 1);
+      mbar_init(&qd_empty[b], 1);
+    }
+    mbar_init(sp_full, 1);
+    mbar_init(sp_empty, 128);
+    mbar_init(ds_full, 128);
+    mbar_init(ds_empty, 1);
+    mbar_init(dq_full, 1);
+    mbar_init(dq_empty, 128);
+    mbar_init(dkv_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  constexpr uint32_t T_ST = 0, T_DPT = 128, T_DV = 256, T_DK = 320, T_DQ = 384;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(kv_full, 2 * TILE_BYTES);
+      tma_load_2d(sm + BwdSmem::K, &map_k, kv_full, hk * DH, s0 + kv0);
+      tma_load_2d(sm + BwdSmem::V, &map_v, kv_full, hk * DH, s0 + kv0);
+      for (int it = 0; it < n_it; ++it) {
+        const int g = it / n_q, qt = qt_first + it % n_q;
+        const int h = hk * G + g;
+        const int st = it & 1;
+        mbar_wait(&qd_empty[st], ((it >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&qd_full[st], 2 * TILE_BYTES);
+        unsigned char* dst = sm + BwdSmem::QD + st * 2 * TILE_BYTES;
+        tma_load_2d(dst, &map_q, &qd_full[st], h * DH, s0 + qt * BQ);
+        tma_load_2d(dst + TILE_BYTES, &map_do, &qd_full[st], h * DH, s0 + qt * BQ);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t id_sp = idesc_bf16_f32(BKV, BQ, false, false);  // M = kv, N = q
+      constexpr uint32_t id_kv = idesc_bf16_f32(BKV, DH, false, true);   // dV, dK: A K-major, B MN-major
+      constexpr uint32_t id_dq = idesc_bf16_f32(BQ, DH, true, true);     // dQ: A = dS (MN-major view of dS^T)
+      const uint32_t k_base = smem_u32(sm + BwdSmem::K), v_base = smem_u32(sm + BwdSmem::V);
+      const uint32_t pt_base = smem_u32(sm + BwdSmem::PT), ds_base = smem_u32(sm + BwdSmem::DST);
+      mbar_wait(kv_full, 0);
+      for (int it = 0; it < n_it; ++it) {
+        const int st = it & 1;
+        const uint32_t q_base = smem_u32(sm + BwdSmem::QD + st * 2 * TILE_BYTES);
+        const uint32_t do_base = q_base + TILE_BYTES;
+        mbar_wait(&qd_full[st], (it >> 1) & 1);
+        mbar_wait(sp_empty, (it & 1) ^ 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          umma_bf16(tmem + T_ST, smem_desc_sw128(k_base + kk * 32, 16, 1024), smem_desc_sw128(q_base + kk * 32, 16, 1024),
+                    id_sp, kk > 0);
+          umma_bf16(tmem + T_DPT, smem_desc_sw128(v_base + kk * 32, 16, 1024),
+                    smem_desc_sw128(do_base + kk * 32, 16, 1024), id_sp, kk > 0);
+        }
+        umma_commit(sp_full);
+        mbar_wait(ds_full, it & 1);
+        mbar_wait(dq_empty, (it & 1) ^ 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < BQ / 16; ++kk) {  // reduction over the 128 queries
+          const uint32_t chunk = (kk >> 2) * 16384 + (kk & 3) * 32;
+          umma_bf16(tmem + T_DV, smem_desc_sw128(pt_base + chunk, 16, 1024),
+                    smem_desc_sw128(do_base + kk * 2048, 8192, 1024), id_kv, (it > 0 || kk > 0) ? 1u : 0u);
+          umma_bf16(tmem + T_DK, smem_desc_sw128(ds_base + chunk, 16, 1024),
+                    smem_desc_sw128(q_base + kk * 2048, 8192, 1024), id_kv, (it > 0 || kk > 0) ? 1u : 0u);
+        }
+#pragma unroll
+        for (int kk = 0; kk < BKV / 16; ++kk) {  // reduction over the 128 keys
+          umma_bf16(tmem + T_DQ, smem_desc_sw128(ds_base + kk * 2048, 16384, 1024),
+                    smem_desc_sw128(k_base + kk * 2048, 8192, 1024), id_dq, kk > 0 ? 1u : 0u);
+        }
+        umma_commit(&qd_empty[st]);
+        umma_commit(ds_empty);
+        umma_commit(dq_full);
+      }
+      umma_commit(dkv_full);
+    }
+  } else {
+    const int q4 = warp & 3;
+    const int r = q4 * 32 + lane;  // kv row (S^T, dP^T, dK, dV) and q row (dQ)
+    const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
+    const int kvpos = kv0 + r;
+    const int tid = threadIdx.x - 64;
+    unsigned char* pt = sm + BwdSmem::PT;
+    unsigned char* dst = sm + BwdSmem::DST;
+    for (int it = 0; it < n_it; ++it) {
+      const int g = it / n_q, qt = qt_first + it % n_q;
+      const int h = hk * G + g;
+      const int q0 = qt * BQ;
+      float* lse_t = s_lse + (it & 1) * 128;  // double-buffered: one barrier per tile suffices
+      float* D_t = s_D + (it & 1) * 128;
+      {
+        const int qi = q0 + tid;
+        const bool ok = qi < L;
+        lse_t[tid] = ok ? lse[(size_t)h * T + s0 + qi] * LOG2E_F : INFINITY;
+        D_t[tid] = ok ? Dvec[(size_t)h * T + s0 + qi] : 0.f;
+      }
+      named_bar(1, 128);
+      mbar_wait(sp_full, it & 1);
+      mbar_wait(ds_empty, (it & 1) ^ 1);
+      tc_fence_after();
+      const bool need_mask = (CAUSAL && q0 < kv0 + BKV - 1) || (q0 + BQ > L) || (kv0 + BKV > L);
+#pragma unroll 1
+      for (int c0 = 0; c0 < BQ; c0 += 32) {
+        uint32_t sr[32], pr[32];
+        tmem_ld_32x32b_x32(tmem + lane_base + T_ST + c0, sr);
+        tmem_ld_32x32b_x32(tmem + lane_base + T_DPT + c0, pr);
+        tmem_ld_wait();
+        float p[32], ds[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int c = c0 + j;
+          float pv = exp2f(__uint_as_float(sr[j]) * scale2 - lse_t[c]);
+          if (need_mask) {
+            const int qpos = q0 + c;
+            if ((CAUSAL && qpos < kvpos) || qpos >= L || kvpos >= L) pv = 0.f;
+          }
+          p[j] = pv;
+          ds[j] = pv * (__uint_as_float(pr[j]) - D_t[c]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          uint4 a, b;
+          a.x = pack_bf16(p[8 * u + 0], p[8 * u + 1]);
+          a.y = pack_bf16(p[8 * u + 2], p[8 * u + 3]);
+          a.z = pack_bf16(p[8 * u + 4], p[8 * u + 5]);
+          a.w = pack_bf16(p[8 * u + 6], p[8 * u + 7]);
+          b.x = pack_bf16(ds[8 * u + 0], ds[8 * u + 1]);
+          b.y = pack_bf16(ds[8 * u + 2], ds[8 * u + 3]);
+          b.z = pack_bf16(ds[8 * u + 4], ds[8 * u + 5]);
+          b.w = pack_bf16(ds[8 * u + 6], ds[8 * u + 7]);
+          const uint32_t off = p_offset(r, c0 + 8 * u);
+          *reinterpret_cast<uint4*>(pt + off) = a;
+          *reinterpret_cast<uint4*>(dst + off) = b;
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(sp_empty);
+      fence_proxy_async_smem();
+      mbar_arrive(ds_full);
+      // drain this tile's dQ (overlaps the next tile's S^T / dP^T MMAs)
+      mbar_wait(dq_full, it & 1);
+      tc_fence_after();
+      const int qrow = q0 + r;
+#pragma unroll
+      for (int c0 = 0; c0 < DH; c0 += 32) {
+        uint32_t qr[32];
+        tmem_ld_32x32b_x32(tmem + lane_base + T_DQ + c0, qr);
+        tmem_ld_wait();
+        if (qrow < L) {
+          float* dst_row = dq_acc + ((size_t)(s0 + qrow) * H + h) * DH + c0;
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            red_add_v4(dst_row + j, __uint_as_float(qr[j]), __uint_as_float(qr[j + 1]), __uint_as_float(qr[j + 2]),
+                       __uint_as_float(qr[j + 3]));
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(dq_empty);
+    }
+    // dK (scaled), dV -> bf16
+    mbar_wait(dkv_full, 0);
+    tc_fence_after();
+#pragma unroll
+    for (int which = 0; which < 2; ++which) {
+      uint32_t o[DH / 2];
+      const float f = which == 0 ? scale : 1.f;
+#pragma unroll
+      for (int c = 0; c < DH / 32; ++c) {
+        uint32_t rr[32];
+        tmem_ld_32x32b_x32(tmem + lane_base + (which == 0 ? T_DK : T_DV) + c * 32, rr);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          o[c * 16 + j] = pack_bf16(__uint_as_float(rr[2 * j]) * f, __uint_as_float(rr[2 * j + 1]) * f);
+      }
+      if (kvpos < L) {
+        __nv_bfloat16* base = which == 0 ? dk + (size_t)(s0 + kvpos) * lddk : dv + (size_t)(s0 + kvpos) * lddv;
+        uint4* d4 = reinterpret_cast<uint4*>(base + hk * DH);
+#pragma unroll
+        for (int u = 0; u < DH / 8; ++u) d4[u] = make_uint4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// D[h][t] = sum_d dO[t,h,d] * O[t,h,d]; zero the fp32 dQ accumulator row.  One warp per (t, h).
+__global__ void attn_bwd_pre_kernel(const __nv_bfloat16* __restrict__ o, int ldo, const __nv_bfloat16* __restrict__ dout,
+                                    int lddo, float* __restrict__ Dvec, float* __restrict__ dq_acc, int T, int H) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= T * H) return;
+  const int t = w / H, h = w - t * H;
+  const __nv_bfloat162 a = reinterpret_cast<const __nv_bfloat162*>(o + (size_t)t * ldo + h * DH)[lane];
+  const __nv_bfloat162 b = reinterpret_cast<const __nv_bfloat162*>(dout + (size_t)t * lddo + h * DH)[lane];
+  const float2 fa = __bfloat1622float2(a), fb = __bfloat1622float2(b);
+  float v = fa.x * fb.x + fa.y * fb.y;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
+  if (lane == 0) Dvec[(size_t)h * T + t] = v;
+  reinterpret_cast<float2*>(dq_acc + ((size_t)t * H + h) * DH)[lane] = make_float2(0.f, 0.f);
+}
+
+// dq[t, h, :] (bf16, pitched) = scale * dq_acc[t, h, :]
+__global__ void attn_bwd_post_kernel(const float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dq, int lddq, int T,
+                                     int H, float scale) {
+  const long long n = (long long)T * H * DH / 8;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long e = i * 8;
+    const long long t = e / (H * DH), rem = e - t * H * DH;
+    const float4 a = reinterpret_cast<const float4*>(dq_acc + e)[0];
+    const float4 b = reinterpret_cast<const float4*>(dq_acc + e)[1];
+    uint4 v;
+    v.x = pack_bf16(a.x * scale, a.y * scale);
+    v.y = pack_bf16(a.z * scale, a.w * scale);
+    v.z = pack_bf16(b.x * scale, b.y * scale);
+    v.w = pack_bf16(b.z * scale, b.w * scale);
+    *reinterpret_cast<uint4*>(dq + t * lddq + rem) = v;
+  }
+}
+
+// KV-tile list for the backward, lightest-first inversion of the query list: causal work of
+// a KV tile shrinks with kv0, so ascending kv0 puts the heaviest tiles first.
+__global__ void attn_kv_tiles_kernel(const int32_t* __restrict__ cu, int nseq, int2* __restrict__ tiles,
+                                     int* __restrict__ count) {
+  __shared__ int s_max, s_n;
+  if (threadIdx.x == 0) {
+    s_max = 0;
+    s_n = 0;
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < nseq; j += blockDim.x) atomicMax(&s_max, (cu[j + 1] - cu[j] + BKV - 1) / BKV);
+  __syncthreads();
+  for (int kb = 0; kb < s_max; ++kb) {
+    for (int j0 = 0; j0 < nseq; j0 += blockDim.x) {
+      const int j = j0 + threadIdx.x;
+      const bool has = j < nseq && (cu[j + 1] - cu[j] + BKV - 1) / BKV > kb;
+      const unsigned bal = __ballot_sync(kFull, has);
+      int base = 0;
+      if ((threadIdx.x & 31) == 0 && bal) base = atomicAdd(&s_n, __popc(bal));
+      base = __shfl_sync(kFull, base, 0);
+      if (has) tiles[base + __popc(bal & ((1u << (threadIdx.x & 31)) - 1u))] = make_int2(j, kb * BKV);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *count = s_n;
+}
+
+}  // namespace
+}  // namespace mb
+
+using namespace mb;
+
+// Workspace for the tile list: (ceil(T/128) + nseq) int2 + one int.
+MAESTRO_API int64_t maestro_attn_workspace(int32_t T, int32_t nseq) {
+  return (int64_t)sizeof(int2) * ((T + BQ - 1) / BQ + nseq) + 16;
+}
+
+// q [T, H, 64] (row pitch ldq elements), k/v [T, Hk, 64] (pitch ldk/ldv), cu [nseq+1];
+// out [T, H, 64] (pitch ldo), lse [H, T] fp32 (natural log-sum-exp of the scaled scores).
+MAESTRO_API int maestro_attn_fwd(const void* q, const void* k, const void* v, const int32_t* cu, int32_t nseq,
+                                 int32_t T, int32_t H, int32_t Hk, int32_t head_dim, int32_t ldq, int32_t ldk,
+                                 int32_t ldv, void* out, int32_t ldo, float* lse, float softmax_scale, int32_t causal,
+                                 void* workspace, void* stream) {
+  if (T <= 0) return 0;
+  if (head_dim != DH || H % Hk) return (int)cudaErrorInvalidValue;
+  cudaStream_t st = (cudaStream_t)stream;
+  int2* tiles = reinterpret_cast<int2*>(workspace);
+  const int max_tiles = (T + BQ - 1) / BQ + nseq;
+  int* count = reinterpret_cast<int*>(tiles + max_tiles);
+  attn_tiles_kernel<<<1, 1024, 0, st>>>(cu, nseq, tiles, count);
+  CUtensorMap mq, mk, mv;
+  bool ok = make_map_2d(&mq, q, (uint64_t)H * DH, T, ldq, 64, 128);
+  ok = ok && make_map_2d(&mk, k, (uint64_t)Hk * DH, T, ldk, 64, 128);
+  ok = ok && make_map_2d(&mv, v, (uint64_t)Hk * DH, T, ldv, 64, 128);
+  if (!ok) return (int)cudaErrorInvalidValue;
+  const int smem = FwdSmem::TOTAL + 1024;
+  dim3 grid(max_tiles, H);
+  const float scale2 = softmax_scale * LOG2E_F;
+  if (causal) {
+    if (ensure_smem<attn_fwd_kernel<true>>(smem)) return launch_status();
+    attn_fwd_kernel<true><<<grid, FWD_THREADS, smem, st>>>(mq, mk, mv, cu, tiles, count, (__nv_bfloat16*)out, ldo,
+                                                          lse, T, H, Hk, scale2);
+  } else {
+    if (ensure_smem<attn_fwd_kernel<false>>(smem)) return launch_status();
+    attn_fwd_kernel<false><<<grid, FWD_THREADS, smem, st>>>(mq, mk, mv, cu, tiles, count, (__nv_bfloat16*)out, ldo,
+                                                           lse, T, H, Hk, scale2);
+  }
+  return launch_status();
+}
+
+// Backward workspace: tile list + D [H, T] fp32 + dQ accumulator [T, H, 64] fp32.
+MAESTRO_API int64_t maestro_attn_bwd_workspace(int32_t T, int32_t nseq, int32_t H) {
+  return maestro_attn_workspace(T, nseq) + 256 + (int64_t)4 * H * T + (int64_t)4 * T * H * DH + 256;
+}
+
+MAESTRO_API int maestro_attn_bwd(const void* dout, int32_t lddo, const void* q, const void* k, const void* v,
+                                 const void* o, int32_t ldo, const float* lse, const int32_t* cu, int32_t nseq,
+                                 int32_t T, int32_t H, int32_t Hk, int32_t head_dim, int32_t ldq, int32_t ldk,
+                                 int32_t ldv, void* dq, int32_t lddq, void* dk, int32_t lddk, void* dv, int32_t lddv,
+                                 float softmax_scale, int32_t causal, void* workspace, void* stream) {
+  if (T <= 0) return 0;
+  if (head_dim != DH || H % Hk) return (int)cudaErrorInvalidValue;
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned char* w = reinterpret_cast<unsigned char*>(workspace);
+  int2* tiles = reinterpret_cast<int2*>(w);
+  const int max_tiles = (T + BKV - 1) / BKV + nseq;
+  int* count = reinterpret_cast<int*>(tiles + max_tiles);
+  const size_t off_d = ((size_t)maestro_attn_workspace(T, nseq) + 255) / 256 * 256;
+  float* Dvec = reinterpret_cast<float*>(w + off_d);
+  const size_t off_acc = (off_d + (size_t)4 * H * T + 255) / 256 * 256;
+  float* dq_acc = reinterpret_cast<float*>(w + off_acc);
+  attn_kv_tiles_kernel<<<1, 1024, 0, st>>>(cu, nseq, tiles, count);
+  const long long warps = (long long)T * H;
+  attn_bwd_pre_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(
+      (const __nv_bfloat16*)o, ldo, (const __nv_bfloat16*)dout, lddo, Dvec, dq_acc, T, H);
+  CUtensorMap mq, mk, mv, mdo;
+  bool ok = make_map_2d(&mq, q, (uint64_t)H * DH, T, ldq, 64, 128);
+  ok = ok && make_map_2d(&mk, k, (uint64_t)Hk * DH, T, ldk, 64, 128);
+  ok = ok && make_map_2d(&mv, v, (uint64_t)Hk * DH, T, ldv, 64, 128);
+  ok = ok && make_map_2d(&mdo, dout, (uint64_t)H * DH, T, lddo, 64, 128);
+  if (!ok) return (int)cudaErrorInvalidValue;
+  const int smem = BwdSmem::TOTAL + 1024;
+  dim3 grid(max_tiles, Hk);
+  const float scale2 = softmax_scale * LOG2E_F;
+  if (causal) {
+    if (ensure_smem<attn_bwd_kernel<true>>(smem)) return launch_status();
+    attn_bwd_kernel<true><<<grid, BWD_THREADS, smem, st>>>(mq, mk, mv, mdo, cu, tiles, count, lse, Dvec, dq_acc,
+                                                          (__nv_bfloat16*)dk, lddk, (__nv_bfloat16*)dv, lddv, T, H, Hk,
+                                                          scale2, softmax_scale);
+  } else {
+    if (ensure_smem<attn_bwd_kernel<false>>(smem)) return launch_status();
+    attn_bwd_kernel<false><<<grid, BWD_THREADS, smem, st>>>(mq, mk, mv, mdo, cu, tiles, count, lse, Dvec, dq_acc,
+                                                           (__nv_bfloat16*)dk, lddk, (__nv_bfloat16*)dv, lddv, T, H,
+                                                           Hk, scale2, softmax_scale);
+  }
+  const long long n8 = (long long)T * H * DH / 8;
+  attn_bwd_post_kernel<<<(unsigned)((n8 + 255) / 256 < 148 * 16 ? (n8 + 255) / 256 : 148 * 16), 256, 0, st>>>(
+      dq_acc, (__nv_bfloat16*)dq, lddq, T, H, softmax_scale);
+  return launch_status();
+}

@@ -1,0 +1,71 @@
+"""GPU numerics of the tcgen05 varlen attention (K8) against the fp32 PyTorch restatement.
+
+Tolerance: bf16 inputs/outputs, fp32 softmax statistics -> outputs and gradients within
+2e-2 relative to the max magnitude; lse within 1e-3 absolute.
+"""
+
+import math
+
+import pytest
+import torch
+
+from oracle import torch_ref as R
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return ((a.float() - b.float()).abs().max() / b.float().abs().max().clamp_min(1e-6)).item()
+
+
+def ref_lse(q, k, cu, causal, scale):
+    T, H, dh = q.shape
+    rep = H // k.shape[1]
+    out = torch.empty(H, T, device=q.device)
+    c = cu.tolist()
+    for a, b in zip(c[:-1], c[1:]):
+        s = (q[a:b].float().transpose(0, 1) @ k[a:b].float().repeat_interleave(rep, 1).permute(1, 2, 0)) * scale
+        if causal:
+            s = s.masked_fill(torch.ones(b - a, b - a, dtype=torch.bool, device=q.device).triu(1), float("-inf"))
+        out[:, a:b] = torch.logsumexp(s, -1)
+    return out
+
+
+CASES = [
+    ([128], 2, 2, True), ([1, 127, 128, 129, 300], 4, 2, True), ([2048, 2048], 2, 1, True),
+    ([196] * 5, 3, 3, False), ([64, 500, 1000], 4, 4, False), ([4096], 1, 1, True),
+]
+
+
+@pytest.mark.parametrize("lens,H,Hk,causal", CASES)
+def test_attention_fwd_bwd(lens, H, Hk, causal):
+    from paper_2605_10501_b200 import attention as A
+
+    torch.manual_seed(sum(lens) + H)
+    dh = 64
+    T = sum(lens)
+    cu = torch.tensor([0] + list(torch.tensor(lens).cumsum(0)), dtype=torch.int32, device="cuda")
+    # fused-QKV-like pitched layout
+    W = (H + 2 * Hk) * dh + 64
+    qkv = torch.randn(T, W, device="cuda").bfloat16()
+    q = qkv[:, : H * dh].view(T, H, dh)
+    k = qkv[:, H * dh: (H + Hk) * dh].view(T, Hk, dh)
+    v = qkv[:, (H + Hk) * dh: (H + 2 * Hk) * dh].view(T, Hk, dh)
+    scale = 1.0 / math.sqrt(dh)
+    o = torch.empty(T, H, dh, device="cuda", dtype=torch.bfloat16)
+    lse = A.attn_fwd(q, k, v, cu, max(lens), causal, o, scale)
+    qf, kf, vf = (x.float().clone().requires_grad_(True) for x in (q, k, v))
+    ref = R.varlen_attention(qf, kf, vf, cu, causal, scale)
+    assert rel(o, ref) < 2e-2
+    assert (lse - ref_lse(q, k, cu, causal, scale)).abs().max().item() < 1e-3
+    do = torch.randn(T, H, dh, device="cuda").bfloat16()
+    ref.backward(do.float())
+    dqkv = torch.zeros_like(qkv)
+    dq = dqkv[:, : H * dh].view(T, H, dh)
+    dk = dqkv[:, H * dh: (H + Hk) * dh].view(T, Hk, dh)
+    dv = dqkv[:, (H + Hk) * dh: (H + 2 * Hk) * dh].view(T, Hk, dh)
+    A.attn_bwd(do, q, k, v, o, lse, cu, max(lens), causal, dq, dk, dv, scale)
+    assert rel(dv, vf.grad) < 2e-2
+    assert rel(dk, kf.grad) < 3e-2
+    assert rel(dq, qf.grad) < 3e-2
+    assert torch.all(dqkv[:, (H + 2 * Hk) * dh:] == 0)  # pitch padding untouched
