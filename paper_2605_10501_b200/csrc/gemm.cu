@@ -6,10 +6,12 @@
 // three training GEMMs without transposes:  fwd  Y = X W^T      (A K-major,  B K-major)
 //                                            dgrad dX = dY W     (A K-major,  B MN-major)
 //                                            wgrad dW = dY^T X   (A MN-major, B MN-major)
-// Tile 128 x 256 x 64, 4-stage TMA ring (SWIZZLE_128B), one elected thread issues
-// tcgen05.mma (M=128, N=256, K=16) into a double-buffered TMEM accumulator (2 x 256 of the
-// 512 columns), four epilogue warps drain TMEM (tcgen05.ld) while the next tile's MMAs run.
-// Grid = min(tiles, #SMs); tiles are visited in grouped-M raster order for L2 reuse.
+// Tile 128 x BN x 64 (BN = 256 or 128, picked per shape against wave quantisation over the
+// 148 SMs), 4/6-stage TMA ring (SWIZZLE_128B), one elected thread issues tcgen05.mma
+// (M=128, N=BN, K=16) into a double-buffered TMEM accumulator, four epilogue warps drain TMEM
+// (tcgen05.ld) while the next tile's MMAs run.  Grid = min(work units, #SMs); tiles are
+// visited in grouped-M raster order for L2 reuse.  Small-output, long-K GEMMs (weight
+// gradients) split K across CTAs and accumulate with red.global.add.v4.f32 into fp32 C.
 //
 // Warp roles (192 threads): w0 TMA producer, w1 MMA issuer + TMEM owner, w2..w5 epilogue.
 #include <cuda_bf16.h>
@@ -23,15 +25,25 @@ namespace {
 
 using namespace sm100;
 
-constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int BM = 128, BK = 64;
 constexpr int A_BYTES = BM * BK * 2;  // 16 KB
-constexpr int B_BYTES = BN * BK * 2;  // 32 KB
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int GROUP_M = 8;
 constexpr int THREADS = 192;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 
-enum Epi { EPI_BF16 = 0, EPI_F32 = 1, EPI_F32_ACC = 2 };
+template <int BN>
+struct Cfg {
+  static constexpr int STAGES = BN == 256 ? 4 : 6;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+enum Epi { EPI_BF16 = 0, EPI_F32 = 1, EPI_F32_ACC = 2, EPI_F32_ATOMIC = 3 };
+
+__device__ __forceinline__ void red_add_v4f(float* addr, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
 
 struct TileSched {
   int num_m, num_n;
@@ -46,10 +58,11 @@ struct TileSched {
   }
 };
 
-template <bool A_MN, bool B_MN, int EPI>
+template <int BN, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, void* C,
-                int M, int N, int K, int ldc) {
+                int M, int N, int K, int ldc, int splits) {
+  constexpr int STAGES = Cfg<BN>::STAGES, B_BYTES = Cfg<BN>::B_BYTES, STAGE_BYTES = Cfg<BN>::STAGE_BYTES;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-byte alignment for SWIZZLE_128B atoms
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -63,8 +76,17 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const TileSched sched{(M + BM - 1) / BM, (N + BN - 1) / BN};
-  const int num_tiles = sched.num_m * sched.num_n;
-  const int num_kb = (K + BK - 1) / BK;
+  const int num_units = sched.num_m * sched.num_n * splits;
+  const int kb_total = (K + BK - 1) / BK;
+  const int kb_per = (kb_total + splits - 1) / splits;
+  // work unit u -> (tile u / splits, K slice u % splits); the host derives splits from
+  // kb_per so that no K slice is empty.
+  auto unit = [&](int u, int& mb_, int& nb_, int& kb0, int& kb1) {
+    sched.coords(u / splits, mb_, nb_);
+    const int ks = u % splits;
+    kb0 = ks * kb_per;
+    kb1 = min(kb_total, kb0 + kb_per);
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&map_a);
@@ -90,11 +112,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       // ---------------- TMA producer
       int s = 0;
       uint32_t ph = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        int mb_, nb_;
-        sched.coords(t, mb_, nb_);
+      for (int t = blockIdx.x; t < num_units; t += gridDim.x) {
+        int mb_, nb_, kb0, kb1;
+        unit(t, mb_, nb_, kb0, kb1);
         const int m0 = mb_ * BM, n0 = nb_ * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
           mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
           const int k0 = kb * BK;
@@ -110,7 +132,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             tma_load_2d(b, &map_b, &full[s], k0, n0);
           } else {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) tma_load_2d(b + 8192 * j, &map_b, &full[s], n0 + 64 * j, k0);
+            for (int j = 0; j < BN / 64; ++j) tma_load_2d(b + 8192 * j, &map_b, &full[s], n0 + 64 * j, k0);
           }
           if (++s == STAGES) {
             s = 0;
@@ -126,13 +148,15 @@ __global__ void __launch_bounds__(THREADS, 1)
       int s = 0;
       uint32_t ph = 0;
       int local = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+      for (int t = blockIdx.x; t < num_units; t += gridDim.x, ++local) {
+        int mb_, nb_, kb0, kb1;
+        unit(t, mb_, nb_, kb0, kb1);
         const int as = local & 1;
         const uint32_t aph = (local >> 1) & 1;
         mbar_wait(&tempty[as], aph ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + as * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
           const uint32_t a_base = smem_u32(sA + s * A_BYTES);
@@ -145,7 +169,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                                      : smem_desc_sw128(a_base + k * 32, 16, 1024);
             const uint64_t bd = B_MN ? smem_desc_sw128(b_base + k * 2048, 8192, 1024)
                                      : smem_desc_sw128(b_base + k * 32, 16, 1024);
-            umma_bf16(d, ad, bd, idesc, (kb | k) != 0);
+            umma_bf16(d, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           }
           umma_commit(&empty[s]);  // smem slot free once these MMAs retire
           if (++s == STAGES) {
@@ -160,9 +184,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ---------------- epilogue: TMEM -> registers -> global
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
     int local = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
-      int mb_, nb_;
-      sched.coords(t, mb_, nb_);
+    for (int t = blockIdx.x; t < num_units; t += gridDim.x, ++local) {
+      int mb_, nb_, kb0, kb1;
+      unit(t, mb_, nb_, kb0, kb1);
       const int as = local & 1;
       const uint32_t aph = (local >> 1) & 1;
       mbar_wait(&tfull[as], aph);
@@ -190,6 +214,14 @@ __global__ void __launch_bounds__(THREADS, 1)
         } else {
           float* out = reinterpret_cast<float*>(C) + (size_t)row * ldc + col;
           const int nv = full_chunk ? 8 : (N - col) / 4;
+          if (EPI == EPI_F32_ATOMIC) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (j < nv)
+                red_add_v4f(out + 4 * j, __uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                            __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+            continue;
+          }
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             if (j >= nv) break;
@@ -218,14 +250,37 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
-template <bool A_MN, bool B_MN, int EPI>
-int launch(const CUtensorMap& ma, const CUtensorMap& mbm, void* C, int M, int N, int K, int ldc, cudaStream_t st) {
-  auto kern = gemm_kernel<A_MN, B_MN, EPI>;
-  if (ensure_smem<gemm_kernel<A_MN, B_MN, EPI>>(SMEM_BYTES)) return launch_status();
-  const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
-  const int grid = tiles < num_sms() ? tiles : num_sms();
-  kern<<<grid, THREADS, SMEM_BYTES, st>>>(ma, mbm, C, M, N, K, ldc);
+template <int BN, bool A_MN, bool B_MN, int EPI>
+int launch(const CUtensorMap& ma, const CUtensorMap& mbm, void* C, int M, int N, int K, int ldc, int splits,
+           cudaStream_t st) {
+  constexpr int SMEM = Cfg<BN>::SMEM;
+  if (ensure_smem<gemm_kernel<BN, A_MN, B_MN, EPI>>(SMEM)) return launch_status();
+  const int units = ((M + BM - 1) / BM) * ((N + BN - 1) / BN) * splits;
+  const int grid = units < num_sms() ? units : num_sms();
+  gemm_kernel<BN, A_MN, B_MN, EPI><<<grid, THREADS, SMEM, st>>>(ma, mbm, C, M, N, K, ldc, splits);
   return launch_status();
+}
+
+// Pick BN in {256, 128} minimising ceil(tiles / SMs) * BN (work of the slowest CTA), and a
+// split-K factor for accumulate-into-fp32 GEMMs whose tile count cannot fill the machine.
+inline void plan_shape(int M, int N, int K, int epi, int& bn, int& splits) {
+  const int sms = num_sms();
+  const long long t256 = (long long)((M + BM - 1) / BM) * ((N + 255) / 256);
+  const long long t128 = (long long)((M + BM - 1) / BM) * ((N + 127) / 128);
+  const long long c256 = (t256 + sms - 1) / sms * 2, c128 = (t128 + sms - 1) / sms;
+  bn = 4 * c128 < 3 * c256 ? 128 : 256;  // BN=128 only when it cuts quantisation by > 25%
+  splits = 1;
+  const long long tiles = bn == 256 ? t256 : t128;
+  const int kb = (K + BK - 1) / BK;
+  if (epi == EPI_F32_ACC && tiles < sms && kb >= 8) {
+    bn = 256;
+    const long long t = t256;
+    int s = (int)((2 * sms + t - 1) / t);
+    s = s < kb / 4 ? s : kb / 4;
+    s = s < 1 ? 1 : s;
+    const int per = (kb + s - 1) / s;  // re-derive so that no K slice is empty
+    splits = (kb + per - 1) / per;
+  }
 }
 
 }  // namespace
@@ -240,13 +295,18 @@ MAESTRO_API int maestro_gemm_bf16(const void* A, const void* B, void* C, int32_t
                                   void* stream) {
   if (M <= 0 || N <= 0 || K <= 0) return (int)cudaErrorInvalidValue;
   if ((lda % 8) || (ldb % 8) || (N % 8) || (ldc % 8)) return (int)cudaErrorInvalidValue;
+  int bn, splits;
+  plan_shape(M, N, K, epi, bn, splits);
+  const int epi_k = splits > 1 ? EPI_F32_ATOMIC : epi;
   CUtensorMap ma, mbm;
   bool ok = a_mn ? make_map_2d(&ma, A, M, K, lda, 64, 64) : make_map_2d(&ma, A, K, M, lda, 64, 128);
-  ok = ok && (b_mn ? make_map_2d(&mbm, B, N, K, ldb, 64, 64) : make_map_2d(&mbm, B, K, N, ldb, 64, 256));
+  ok = ok && (b_mn ? make_map_2d(&mbm, B, N, K, ldb, 64, 64) : make_map_2d(&mbm, B, K, N, ldb, 64, bn));
   if (!ok) return (int)cudaErrorInvalidValue;
   cudaStream_t st = (cudaStream_t)stream;
-#define MB_GEMM_CASE(AM, BMN, E) \
-  if (a_mn == AM && b_mn == BMN && epi == E) return launch<AM, BMN, E>(ma, mbm, C, M, N, K, ldc, st);
+#define MB_GEMM_CASE(AM, BMN, E)                                                                   \
+  if (a_mn == AM && b_mn == BMN && epi_k == E)                                                     \
+    return bn == 256 ? launch<256, AM, BMN, E>(ma, mbm, C, M, N, K, ldc, splits, st)               \
+                     : launch<128, AM, BMN, E>(ma, mbm, C, M, N, K, ldc, splits, st);
   MB_GEMM_CASE(0, 0, 0)
   MB_GEMM_CASE(0, 0, 1)
   MB_GEMM_CASE(0, 0, 2)
@@ -256,9 +316,7 @@ MAESTRO_API int maestro_gemm_bf16(const void* A, const void* B, void* C, int32_t
   MB_GEMM_CASE(1, 1, 0)
   MB_GEMM_CASE(1, 1, 1)
   MB_GEMM_CASE(1, 1, 2)
-  MB_GEMM_CASE(1, 0, 0)
-  MB_GEMM_CASE(1, 0, 1)
-  MB_GEMM_CASE(1, 0, 2)
+  MB_GEMM_CASE(1, 1, 3)
 #undef MB_GEMM_CASE
   return (int)cudaErrorInvalidValue;
 }

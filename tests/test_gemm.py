@@ -72,3 +72,20 @@ def test_strided_views():
     out = torch.empty(512, 384, device="cuda", dtype=torch.bfloat16)
     dense.gemm(x, w, out, 512, 384, 256, False, False, dense.EPI_BF16, lda=big.stride(0))
     assert _rel(out, x.float() @ w.float().t()) < 8e-3
+
+
+@pytest.mark.parametrize("M,N,K", [(8192, 768, 768), (8192, 2304, 768), (8192, 768, 3072), (8192, 6144, 768)])
+def test_training_shapes_all_paths(M, N, K):
+    """Student-layer shapes: BN=128 wave-quantisation path (fwd) and split-K atomic wgrad."""
+    from paper_2605_10501_b200 import dense
+
+    torch.manual_seed(M + N)
+    x = torch.randn(M, K, device="cuda").bfloat16()
+    w = torch.randn(N, K, device="cuda").bfloat16()
+    assert _rel(dense.linear_fwd(x, w), x.float() @ w.float().t()) < 8e-3
+    dy = torch.randn(M, N, device="cuda").bfloat16()
+    assert _rel(dense.linear_dgrad(dy, w), dy.float() @ w.float()) < 8e-3
+    dw = torch.randn(N, K, device="cuda")
+    ref = dw + dy.float().t() @ x.float()
+    dense.linear_wgrad(dy, x, dw)
+    assert _rel(dw, ref) < 1e-4
