@@ -2,9 +2,10 @@
 
 Workload (configs[1] of BASELINE.json): knowledge distillation, forward-only 1.1B teacher
 (TinyLlama shape) -> 125M student, fused KL over the 32k vocabulary, seq 2048, 64 samples per
-student DP rank, synthetic token ids, random-init weights.  At 1 GPU both sections are
-co-resident; at N GPUs the teacher and student run on disjoint GPU groups with an NCCL handoff
-of teacher hidden states (recipes.KD_LAYOUTS).
+student DP rank, synthetic token ids, random-init weights.  Default layout (--layout colocated):
+every GPU hosts a teacher and a student DP rank (handoff = CUDA event, student gradients
+all-reduced over NCCL); --layout disjoint puts teacher and student on disjoint GPU groups with an
+NCCL send/recv handoff of teacher hidden states (recipes.kd_layout).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -166,6 +167,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--batch-per-rank", type=int, default=BATCH_PER_RANK)
     ap.add_argument("--mbs", type=int, default=MBS)
+    ap.add_argument("--layout", default="colocated", choices=["colocated", "disjoint"])
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -188,7 +190,8 @@ def main():
     from paper_2605_10501_b200 import instrument
     from paper_2605_10501_b200.executor import KDExecutor, synthetic_ids
 
-    ex = KDExecutor(n_gpus=args.gpus, batch_per_rank=args.batch_per_rank, seq=SEQ, mbs=args.mbs)
+    ex = KDExecutor(n_gpus=args.gpus, batch_per_rank=args.batch_per_rank, seq=SEQ, mbs=args.mbs,
+                    layout=args.layout)
     B = ex.batch
     ids_host = torch.from_numpy(synthetic_ids(B, SEQ, 32000)).pin_memory()
     ids_dev = ids_host.cuda()
@@ -239,6 +242,11 @@ def main():
     f1.record()
     barrier()
     ems = f0.elapsed_time(f1)
+    if dist is not None:  # loss lives on student ranks; report the first student rank's
+        lt = torch.tensor([losses[-1] if losses and losses[-1] is not None else float("nan")], device="cuda")
+        src = 0 if ex.colocated else ex.dp_t
+        dist.broadcast(lt, src)
+        losses = [float(lt.item())]
     t = torch.tensor([ems], device="cuda")
     if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -265,7 +273,7 @@ def main():
         except Exception as exc:  # noqa: BLE001
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {exc}"}
     if rank == 0:
-        dp_s, dp_t, _ = __import__("paper_2605_10501_b200.recipes", fromlist=["KD_LAYOUTS"]).KD_LAYOUTS[args.gpus]
+        dp_s, dp_t = ex.dp_s, ex.dp_t
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
@@ -274,8 +282,9 @@ def main():
                 "workload": "kd_cfg2: fwd-only 1.1B teacher (TinyLlama shape) -> 125M student, fused KL over "
                             "32k vocab, seq 2048, teacher head colocated with the student",
                 "global_batch": B, "seq_len": SEQ, "micro_batch": args.mbs,
-                "parallelism": ("colocated teacher+student" if args.gpus == 1
-                                else f"teacher dp{dp_t} -> student dp{dp_s} (fanout 1, NCCL handoff)"),
+                "parallelism": (f"colocated teacher+student per GPU, student dp{dp_s} (grad all-reduce)"
+                                if ex.colocated
+                                else f"disjoint groups: teacher dp{dp_t} -> student dp{dp_s} (fanout 1, NCCL handoff)"),
                 "l2": "inputs larger than L2 (teacher weights 2.2 GB, logits 1 GB per micro-batch)",
             },
             "section_stall_pct": 100.0 * float(stall[0].item()),

@@ -80,6 +80,26 @@ class StageClock:
         return busy, span
 
 
+def rank_roles(rank: int, n_gpus: int, layout: str = "colocated"):
+    """Host-only placement of the KD section ranks (no device needed).
+
+    Returns dict(t_rank, s_rank, dp_s, dp_t, colocated, send_to, recv_from, student_ranks):
+    the teacher DP rank / student DP rank hosted by ``rank`` (None if absent), and the NCCL
+    peer of the teacher->student handoff on the fan-out map (scheduling.py:366-371): teacher
+    rank q serves student ranks q*f .. q*f+f-1; with fan-out 1 that is student rank q.
+    """
+    dp_s, dp_t, f, colocated = R.kd_layout(n_gpus, layout)
+    if colocated:
+        return dict(t_rank=rank, s_rank=rank, dp_s=dp_s, dp_t=dp_t, colocated=True, send_to=[], recv_from=[],
+                    student_ranks=list(range(n_gpus)))
+    t_rank = rank if rank < dp_t else None
+    s_rank = rank - dp_t if rank >= dp_t else None
+    send_to = [dp_t + q for q in range(t_rank * f, (t_rank + 1) * f)] if t_rank is not None else []
+    recv_from = [s_rank // f] if s_rank is not None else []
+    return dict(t_rank=t_rank, s_rank=s_rank, dp_s=dp_s, dp_t=dp_t, colocated=False, send_to=send_to,
+                recv_from=recv_from, student_ranks=list(range(dp_t, n_gpus)))
+
+
 def _dist():
     import torch.distributed as dist
 
@@ -91,7 +111,7 @@ class KDExecutor:
 
     def __init__(self, n_gpus: int = 1, batch_per_rank: int = 64, seq: int = R.KD_SEQ, mbs: int = 4,
                  teacher: str = "kd_teacher_1b", student: str = "kd_student_125m", seed: int = 0,
-                 lr: float = 3e-4, policy=ExecPolicy.INTERLEAVED, device=None):
+                 lr: float = 3e-4, policy=ExecPolicy.INTERLEAVED, device=None, layout: str = "colocated"):
         dist = _dist()
         self.rank = dist.get_rank() if dist else 0
         self.world = dist.get_world_size() if dist else 1
@@ -99,20 +119,18 @@ class KDExecutor:
             raise ValueError(f"n_gpus={n_gpus} but world size is {self.world}")
         self.device = device or torch.device("cuda", torch.cuda.current_device())
         self.n_gpus, self.seq, self.mbs = n_gpus, seq, mbs
-        dp_s, dp_t, f_t = R.KD_LAYOUTS[n_gpus]
+        dp_s, dp_t, f_t, colocated = R.kd_layout(n_gpus, layout)
+        self.layout = "colocated" if colocated else "disjoint"
         self.batch = batch_per_rank * dp_s
-        self.recipe = R.kd(n_gpus, self.batch, seq)
+        self.recipe = R.kd(n_gpus, self.batch, seq, self.layout)
         cfg = {"student": self.recipe.configs["student"].__class__(dp=dp_s, mbs=mbs),
                "teacher": self.recipe.configs["teacher"].__class__(dp=dp_t, fanout=f_t, mbs=mbs)}
         self.configs = cfg
         self.graph = self.recipe.graph
-        # roles: co-resident at 1 GPU; disjoint GPU groups otherwise (teacher ranks first)
-        self.colocated = n_gpus == 1
-        if self.colocated:
-            self.t_rank, self.s_rank = 0, 0
-        else:
-            self.t_rank = self.rank if self.rank < dp_t else None
-            self.s_rank = self.rank - dp_t if self.rank >= dp_t else None
+        # roles: co-resident teacher+student DP rank per GPU, or disjoint groups (teacher first)
+        self.colocated = colocated
+        self.roles = rank_roles(self.rank, n_gpus, self.layout)
+        self.t_rank, self.s_rank = self.roles["t_rank"], self.roles["s_rank"]
         self.dp_s, self.dp_t = dp_s, dp_t
         self.tshape: Shape = SHAPES[teacher]
         self.sshape: Shape = SHAPES[student]
@@ -148,8 +166,10 @@ class KDExecutor:
     # ------------------------------------------------------------------ distributed plumbing
     def _make_groups(self):
         dist = _dist()
-        if dist is None or self.colocated:
+        if dist is None:
             return {}
+        if self.colocated:  # student DP group = every rank
+            return {"student": None, "student_ranks": list(range(self.world))}
         dp_t = self.dp_t
         s_ranks = list(range(dp_t, self.world))
         grp = dist.new_group(s_ranks) if len(s_ranks) > 1 else None
@@ -307,7 +327,7 @@ class KDExecutor:
     def _run_teacher_remote(self, plan, host, packed, ready):
         dist = _dist()
         pt, ht = plan["teacher"], host["teacher"]
-        dst = self.dp_t + self.t_rank  # fan-out 1: teacher rank q feeds student rank q
+        (dst,) = self.roles["send_to"]  # fan-out 1: teacher rank q feeds student rank q
         self.t_stream.wait_event(ready)
         with torch.cuda.stream(self.t_stream):
             for m in range(pt["n_mb"]):
@@ -318,7 +338,7 @@ class KDExecutor:
     def _run_student_remote(self, plan, host, packed, ready, clock, loss_acc, global_tokens):
         dist = _dist()
         ps, hs = plan["student"], host["student"]
-        src = self.s_rank  # teacher rank feeding this student rank
+        (src,) = self.roles["recv_from"]  # teacher rank feeding this student rank
         self.s_stream.wait_event(ready)
         with torch.cuda.stream(self.s_stream):
             for m in range(ps["n_mb"]):

@@ -101,7 +101,7 @@ def kd_graph() -> SectionGraph:
 
 
 KD_LAYOUTS = {
-    # n_gpus -> (student dp, teacher dp, teacher fanout)
+    # disjoint GPU groups: n_gpus -> (student dp, teacher dp, teacher fanout); teacher ranks first
     1: (1, 1, 1),
     2: (1, 1, 1),
     4: (2, 2, 1),
@@ -109,9 +109,23 @@ KD_LAYOUTS = {
 }
 
 
-def kd(n_gpus: int = 1, batch: int = 64, seq: int = KD_SEQ) -> Recipe:
+def kd_layout(n_gpus: int, layout: str = "colocated"):
+    """(student dp, teacher dp, teacher fanout, colocated?) for a GPU count.
+
+    "colocated": every GPU hosts one teacher and one student DP rank (handoff = CUDA event);
+    "disjoint":  teacher and student on disjoint GPU groups (handoff = NCCL send/recv).
+    The teacher is ~70% of the per-sample FLOPs, so with equal GPUs the disjoint split is
+    teacher-bound and the colocated layout is the throughput-optimal plan on one node.
+    """
+    if layout == "colocated" or n_gpus == 1:
+        return n_gpus, n_gpus, 1, True
+    dp_s, dp_t, f = KD_LAYOUTS[n_gpus]
+    return dp_s, dp_t, f, False
+
+
+def kd(n_gpus: int = 1, batch: int = 64, seq: int = KD_SEQ, layout: str = "disjoint") -> Recipe:
     g = kd_graph()
-    dp_s, dp_t, f_t = KD_LAYOUTS[n_gpus]
+    dp_s, dp_t, f_t, _ = kd_layout(n_gpus, layout)
     configs = {"student": SectionConfig(dp=dp_s), "teacher": SectionConfig(dp=dp_t, fanout=f_t)}
     # fwd FLOPs per token ~ 2 * params (+ attention); student includes the colocated teacher head
     params = {
