@@ -140,6 +140,50 @@ int maestro_scatter_rows_fwd(const void* d_src, void* d_dst, const int32_t* d_sr
 int maestro_gather_rows_bwd(const void* d_ddst, void* d_dsrc, const int32_t* d_seg,
                             const int32_t* d_seg_dst, int32_t n_src_rows, int32_t d, void* stream);
 
+
+/* ---------------------------------------------------------------- section compute
+ * Not in the reference (paper prose only: PAPER.md:56,88,93,250,270-271).  bf16 operands,
+ * fp32 accumulation.  All pointers are device memory; row pitches are in elements. */
+
+/* K7 -- C[m,n] (+)= sum_k A(m,k) B(n,k) on tcgen05/TMEM.  A(m,k) = A[m*lda+k] (a_mn = 0) or
+ * A[k*lda+m] (a_mn = 1); likewise B.  epi: 0 store bf16, 1 store fp32, 2 accumulate into fp32
+ * (small-output shapes split K and use fp32 reductions).  N, lda, ldb, ldc multiples of 8. */
+int maestro_gemm_bf16(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K, int32_t lda,
+                      int32_t ldb, int32_t ldc, int32_t a_mn, int32_t b_mn, int32_t epi, void* stream);
+
+/* K8 -- varlen GQA attention, head_dim 64: q [T,H,64], k/v [T,Hk,64] (pitched), cu [nseq+1];
+ * out [T,H,64] bf16, lse [H,T] fp32 (natural LSE of the scaled scores). */
+int64_t maestro_attn_workspace(int32_t T, int32_t nseq);
+int maestro_attn_fwd(const void* q, const void* k, const void* v, const int32_t* cu, int32_t nseq, int32_t T,
+                     int32_t H, int32_t Hk, int32_t head_dim, int32_t ldq, int32_t ldk, int32_t ldv, void* out,
+                     int32_t ldo, float* lse, float softmax_scale, int32_t causal, void* workspace, void* stream);
+int64_t maestro_attn_bwd_workspace(int32_t T, int32_t nseq, int32_t H);
+int maestro_attn_bwd(const void* dout, int32_t lddo, const void* q, const void* k, const void* v, const void* o,
+                     int32_t ldo, const float* lse, const int32_t* cu, int32_t nseq, int32_t T, int32_t H,
+                     int32_t Hk, int32_t head_dim, int32_t ldq, int32_t ldk, int32_t ldv, void* dq, int32_t lddq,
+                     void* dk, int32_t lddk, void* dv, int32_t lddv, float softmax_scale, int32_t causal,
+                     void* workspace, void* stream);
+
+/* K9 -- fused full-vocab KL(softmax(t/tau) || softmax(s/tau)) per token (d_loss[T]) and
+ * ds = grad_scale * dKL/ds (bf16, may alias s).  Teacher head colocated per workload.py:471-514. */
+int maestro_kd_loss_fwd_bwd(const void* d_t, const void* d_s, void* d_ds, float* d_loss, int32_t T, int32_t V,
+                            int32_t ldt, int32_t lds, int32_t ldd, float grad_scale, float inv_tau, void* stream);
+
+/* Memory-bound block kernels. */
+int maestro_add_rmsnorm_fwd(const void* x, const void* a, void* h, void* y, const void* w, float* rstd, int32_t T,
+                            int32_t d, float eps, void* stream);
+int maestro_rmsnorm_bwd(const void* dy, const void* h, const void* w, const float* rstd, const void* dres,
+                        void* dx, float* dw, int32_t T, int32_t d, void* stream);
+int maestro_rope(void* qk, const int32_t* pos, const void* cos_sin, int32_t T, int32_t n_heads, int32_t dh,
+                 int32_t ld, int32_t backward, void* stream);
+int maestro_positions(const int32_t* cu, int32_t nseq, int32_t* pos, void* stream);
+int maestro_swiglu_fwd(const void* gu, void* out, int32_t T, int32_t F, void* stream);
+int maestro_swiglu_bwd(const void* dout, const void* gu, void* dgu, int32_t T, int32_t F, void* stream);
+int maestro_embed_fwd(const void* table, const int32_t* ids, void* out, int32_t T, int32_t d, void* stream);
+int maestro_embed_bwd(const void* dout, const int32_t* ids, float* dtable, int32_t T, int32_t d, void* stream);
+int maestro_adamw(float* p, const float* g, float* m, float* v, void* pb, int64_t n, float lr, float b1, float b2,
+                  float eps, float wd, int32_t step, float gscale, void* stream);
+
 #ifdef __cplusplus
 }
 #endif
