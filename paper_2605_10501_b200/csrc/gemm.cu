@@ -15,6 +15,7 @@
 //
 // Warp roles (192 threads): w0 TMA producer, w1 MMA issuer + TMEM owner, w2..w5 epilogue.
 #include <cuda_bf16.h>
+#include <string.h>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -261,6 +262,254 @@ int launch(const CUtensorMap& ma, const CUtensorMap& mbm, void* C, int M, int N,
   return launch_status();
 }
 
+
+// ==========================================================================================
+// CTA-pair variant (cta_group::2): a cluster of 2 CTAs computes a 256 x BN2 tile.  Each CTA
+// TMA-loads its 128 rows of A and BN2/2 rows of B; completion of both halves is counted on the
+// leader's mbarrier; the leader alone issues tcgen05.mma (M=256, N=BN2), whose accumulator
+// rows 0-127 land in the leader's TMEM and 128-255 in the peer's.  Commits are multicast to
+// both CTAs (smem slot free / accumulator ready); both epilogues drain their own TMEM and
+// arrive on the leader's TMEM-empty barrier.  Per SM this halves B traffic and smem operand
+// bandwidth relative to the 1-CTA 128 x 256 tile.
+template <int BN2>
+struct Cfg2 {
+  static constexpr int B_ROWS = BN2 / 2;  // B rows per CTA
+  static constexpr int B_BYTES = B_ROWS * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = BN2 == 256 ? 6 : 8;
+  static constexpr int EPI_BUF = 128 * 64 * 2;  // one 128 x 64 bf16 SWIZZLE_128B staging tile
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 2 * EPI_BUF + 1024 + 256;
+};
+
+template <int BN2, bool A_MN, bool B_MN, int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+    gemm2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                 const __grid_constant__ CUtensorMap map_c, void* C, int M, int N, int K, int ldc, int splits) {
+  using CF = Cfg2<BN2>;
+  constexpr int STAGES = CF::STAGES, B_BYTES = CF::B_BYTES, STAGE_BYTES = CF::STAGE_BYTES, B_ROWS = CF::B_ROWS;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* sA = smem;
+  unsigned char* sB = smem + STAGES * A_BYTES;
+  unsigned char* sC = smem + STAGES * STAGE_BYTES;  // 2 x 16 KB epilogue staging (bf16 path)
+  uint64_t* full = reinterpret_cast<uint64_t*>(sC + 2 * CF::EPI_BUF);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const TileSched sched{(M + 255) / 256, (N + BN2 - 1) / BN2};
+  const int num_units = sched.num_m * sched.num_n * splits;
+  const int kb_total = (K + BK - 1) / BK;
+  const int kb_per = (kb_total + splits - 1) / splits;
+  auto unit = [&](int u, int& mb_, int& nb_, int& kb0, int& kb1) {
+    sched.coords(u / splits, mb_, nb_);
+    const int ks = u % splits;
+    kb0 = ks * kb_per;
+    kb1 = min(kb_total, kb0 + kb_per);
+  };
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&map_a);
+    tma_prefetch(&map_b);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 256);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_2sm(tmem_slot, 512);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int t = pair; t < num_units; t += npairs) {
+        int mb_, nb_, kb0, kb1;
+        unit(t, mb_, nb_, kb0, kb1);
+        const int m0 = mb_ * 256 + (int)rank * 128, n0 = nb_ * BN2 + (int)rank * B_ROWS;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          if (leader) mbar_arrive_expect_tx(&full[s], 2 * STAGE_BYTES);
+          const uint32_t fb = mapa_shared(smem_u32(&full[s]), 0);
+          const int k0 = kb * BK;
+          unsigned char* a = sA + s * A_BYTES;
+          unsigned char* b = sB + s * B_BYTES;
+          if (!A_MN) {
+            tma_load_2d_2sm(a, &map_a, fb, k0, m0);
+          } else {
+            tma_load_2d_2sm(a, &map_a, fb, m0, k0);
+            tma_load_2d_2sm(a + 8192, &map_a, fb, m0 + 64, k0);
+          }
+          if (!B_MN) {
+            tma_load_2d_2sm(b, &map_b, fb, k0, n0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < B_ROWS / 64; ++j) tma_load_2d_2sm(b + 8192 * j, &map_b, fb, n0 + 64 * j, k0);
+          }
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      constexpr uint32_t idesc = idesc_bf16_f32(256, BN2, A_MN, B_MN);
+      int s = 0;
+      uint32_t ph = 0;
+      int local = 0;
+      for (int t = pair; t < num_units; t += npairs, ++local) {
+        int mb_, nb_, kb0, kb1;
+        unit(t, mb_, nb_, kb0, kb1);
+        const int as = local & 1;
+        const uint32_t aph = (local >> 1) & 1;
+        mbar_wait(&tempty[as], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + as * BN2;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(sA + s * A_BYTES);
+          const uint32_t b_base = smem_u32(sB + s * B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = A_MN ? smem_desc_sw128(a_base + k * 2048, 8192, 1024)
+                                     : smem_desc_sw128(a_base + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? smem_desc_sw128(b_base + k * 2048, 8192, 1024)
+                                     : smem_desc_sw128(b_base + k * 32, 16, 1024);
+            umma_bf16_2sm(d, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          }
+          umma_commit_2sm(&empty[s], 0x3);
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        umma_commit_2sm(&tfull[as], 0x3);
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
+    const int et = threadIdx.x - 64;  // 0..127 over the four epilogue warps
+    int local = 0, chunk_ctr = 0;
+    for (int t = pair; t < num_units; t += npairs, ++local) {
+      int mb_, nb_, kb0, kb1;
+      unit(t, mb_, nb_, kb0, kb1);
+      const int as = local & 1;
+      const uint32_t aph = (local >> 1) & 1;
+      mbar_wait(&tfull[as], aph);
+      tc_fence_after();
+      const int row0 = mb_ * 256 + (int)rank * 128;
+      const int row = row0 + q * 32 + lane;
+      const int n0 = nb_ * BN2;
+      if (EPI == EPI_BF16) {
+        // TMEM -> regs -> bf16 -> swizzled smem tile (128 rows x 64 cols) -> TMA bulk store;
+        // two staging buffers alternate, the store of one overlaps filling the other.
+        const int r_in = q * 32 + lane;
+#pragma unroll 1
+        for (int c = 0; c < BN2; c += 64, ++chunk_ctr) {
+          unsigned char* buf = sC + (chunk_ctr & 1) * CF::EPI_BUF;
+          uint32_t r0[32], r1[32];
+          tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + as * BN2 + c, r0);
+          tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + as * BN2 + c + 32, r1);
+          tmem_ld_wait();
+          if (chunk_ctr >= 2) {
+            if (et == 0) bulk_wait_read<1>();  // the store issued from this buffer has read it
+            named_barrier_sync(1, 128);
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const uint32_t* src = u < 4 ? &r0[8 * u] : &r1[8 * (u - 4)];
+            uint4 v;
+            v.x = pack_bf16(__uint_as_float(src[0]), __uint_as_float(src[1]));
+            v.y = pack_bf16(__uint_as_float(src[2]), __uint_as_float(src[3]));
+            v.z = pack_bf16(__uint_as_float(src[4]), __uint_as_float(src[5]));
+            v.w = pack_bf16(__uint_as_float(src[6]), __uint_as_float(src[7]));
+            *reinterpret_cast<uint4*>(buf + r_in * 128 + ((u ^ (r_in & 7)) << 4)) = v;
+          }
+          fence_proxy_async_smem();
+          named_barrier_sync(1, 128);
+          if (et == 0 && n0 + c < N && row0 < M) {
+            tma_store_2d(&map_c, buf, n0 + c, row0);
+            bulk_commit();
+          }
+        }
+      } else {
+#pragma unroll 1
+      for (int c = 0; c < BN2; c += 32) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + as * BN2 + c, r);
+        tmem_ld_wait();
+        const int col = n0 + c;
+        if (row >= M || col >= N) continue;
+        const bool full_chunk = col + 32 <= N;
+        {
+          float* out = reinterpret_cast<float*>(C) + (size_t)row * ldc + col;
+          const int nv = full_chunk ? 8 : (N - col) / 4;
+          if (EPI == EPI_F32_ATOMIC) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (j < nv)
+                red_add_v4f(out + 4 * j, __uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                            __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+            continue;
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (j >= nv) break;
+            float4 v = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                   __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+            if (EPI == EPI_F32_ACC) {
+              const float4 o = reinterpret_cast<const float4*>(out)[j];
+              v.x += o.x;
+              v.y += o.y;
+              v.z += o.z;
+              v.w += o.w;
+            }
+            reinterpret_cast<float4*>(out)[j] = v;
+          }
+        }
+      }
+      }
+      tc_fence_before();
+      mbar_arrive_cluster(tempty_leader0 + (uint32_t)(as * sizeof(uint64_t)));
+    }
+    if (EPI == EPI_BF16 && et == 0) bulk_wait<0>();
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_2sm(tmem, 512);
+  }
+}
+
+template <int BN2, bool A_MN, bool B_MN, int EPI>
+int launch2(const CUtensorMap& ma, const CUtensorMap& mbm, const CUtensorMap& mc, void* C, int M, int N, int K,
+            int ldc, int splits, cudaStream_t st) {
+  constexpr int SMEM = Cfg2<BN2>::SMEM;
+  if (ensure_smem<gemm2_kernel<BN2, A_MN, B_MN, EPI>>(SMEM)) return launch_status();
+  const int units = ((M + 255) / 256) * ((N + BN2 - 1) / BN2) * splits;
+  const int pairs = units < num_sms() / 2 ? units : num_sms() / 2;
+  gemm2_kernel<BN2, A_MN, B_MN, EPI><<<2 * pairs, THREADS, SMEM, st>>>(ma, mbm, mc, C, M, N, K, ldc, splits);
+  return launch_status();
+}
+
 // Pick BN in {256, 128} minimising ceil(tiles / SMs) * BN (work of the slowest CTA), and a
 // split-K factor for accumulate-into-fp32 GEMMs whose tile count cannot fill the machine.
 inline void plan_shape(int M, int N, int K, int epi, int& bn, int& splits) {
@@ -295,28 +544,49 @@ MAESTRO_API int maestro_gemm_bf16(const void* A, const void* B, void* C, int32_t
                                   void* stream) {
   if (M <= 0 || N <= 0 || K <= 0) return (int)cudaErrorInvalidValue;
   if ((lda % 8) || (ldb % 8) || (N % 8) || (ldc % 8)) return (int)cudaErrorInvalidValue;
-  int bn, splits;
-  plan_shape(M, N, K, epi, bn, splits);
-  const int epi_k = splits > 1 ? EPI_F32_ATOMIC : epi;
-  CUtensorMap ma, mbm;
-  bool ok = a_mn ? make_map_2d(&ma, A, M, K, lda, 64, 64) : make_map_2d(&ma, A, K, M, lda, 64, 128);
-  ok = ok && (b_mn ? make_map_2d(&mbm, B, N, K, ldb, 64, 64) : make_map_2d(&mbm, B, K, N, ldb, 64, bn));
-  if (!ok) return (int)cudaErrorInvalidValue;
+  const int sms = num_sms();
   cudaStream_t st = (cudaStream_t)stream;
-#define MB_GEMM_CASE(AM, BMN, E)                                                                   \
+  // CTA-pair path: 256 x BN2 tiles over sms/2 clusters, BN2 in {256, 128} by quantisation;
+  // accumulate-into-fp32 GEMMs that cannot fill the pairs split K.
+  {
+    const int pairs = sms / 2;
+    const long long tm = (M + 255) / 256;
+    const long long t256 = tm * ((N + 255) / 256), t128 = tm * ((N + 127) / 128);
+    const long long c256 = (t256 + pairs - 1) / pairs * 2, c128 = (t128 + pairs - 1) / pairs;
+    int bn2 = 4 * c128 < 3 * c256 ? 128 : 256;
+    int splits = 1;
+    const int kb = (K + BK - 1) / BK;
+    if (epi == EPI_F32_ACC && t256 < pairs && kb >= 8) {
+      bn2 = 256;
+      int sp = (int)((2 * pairs + t256 - 1) / t256);
+      sp = sp < kb / 4 ? sp : kb / 4;
+      sp = sp < 1 ? 1 : sp;
+      const int per = (kb + sp - 1) / sp;
+      splits = (kb + per - 1) / per;
+    }
+    const int epi_k = splits > 1 ? EPI_F32_ATOMIC : epi;
+    CUtensorMap ma, mbm, mc;
+    const int brows = bn2 / 2;
+    memset(&mc, 0, sizeof(mc));
+    if (epi_k == EPI_BF16 && !make_map_2d(&mc, C, N, M, ldc, 64, 128)) return (int)cudaErrorInvalidValue;
+    bool ok = a_mn ? make_map_2d(&ma, A, M, K, lda, 64, 64) : make_map_2d(&ma, A, K, M, lda, 64, 128);
+    ok = ok && (b_mn ? make_map_2d(&mbm, B, N, K, ldb, 64, 64) : make_map_2d(&mbm, B, K, N, ldb, 64, brows));
+    if (!ok) return (int)cudaErrorInvalidValue;
+#define MB_GEMM2_CASE(AM, BMN, E)                                                                  \
   if (a_mn == AM && b_mn == BMN && epi_k == E)                                                     \
-    return bn == 256 ? launch<256, AM, BMN, E>(ma, mbm, C, M, N, K, ldc, splits, st)               \
-                     : launch<128, AM, BMN, E>(ma, mbm, C, M, N, K, ldc, splits, st);
-  MB_GEMM_CASE(0, 0, 0)
-  MB_GEMM_CASE(0, 0, 1)
-  MB_GEMM_CASE(0, 0, 2)
-  MB_GEMM_CASE(0, 1, 0)
-  MB_GEMM_CASE(0, 1, 1)
-  MB_GEMM_CASE(0, 1, 2)
-  MB_GEMM_CASE(1, 1, 0)
-  MB_GEMM_CASE(1, 1, 1)
-  MB_GEMM_CASE(1, 1, 2)
-  MB_GEMM_CASE(1, 1, 3)
-#undef MB_GEMM_CASE
+    return bn2 == 256 ? launch2<256, AM, BMN, E>(ma, mbm, mc, C, M, N, K, ldc, splits, st)         \
+                      : launch2<128, AM, BMN, E>(ma, mbm, mc, C, M, N, K, ldc, splits, st);
+    MB_GEMM2_CASE(0, 0, 0)
+    MB_GEMM2_CASE(0, 0, 1)
+    MB_GEMM2_CASE(0, 0, 2)
+    MB_GEMM2_CASE(0, 1, 0)
+    MB_GEMM2_CASE(0, 1, 1)
+    MB_GEMM2_CASE(0, 1, 2)
+    MB_GEMM2_CASE(1, 1, 0)
+    MB_GEMM2_CASE(1, 1, 1)
+    MB_GEMM2_CASE(1, 1, 2)
+    MB_GEMM2_CASE(1, 1, 3)
+#undef MB_GEMM2_CASE
+  }
   return (int)cudaErrorInvalidValue;
 }
