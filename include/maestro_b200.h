@@ -169,6 +169,10 @@ int maestro_attn_bwd(const void* dout, int32_t lddo, const void* q, const void* 
 int maestro_kd_loss_fwd_bwd(const void* d_t, const void* d_s, void* d_ds, float* d_loss, int32_t T, int32_t V,
                             int32_t ldt, int32_t lds, int32_t ldd, float grad_scale, float inv_tau, void* stream);
 
+/* Next-token cross entropy (VLM backbone loss) with ignore index label < 0. */
+int maestro_ce_loss_fwd_bwd(const void* d_s, const int32_t* d_labels, void* d_ds, float* d_loss, int32_t T,
+                            int32_t V, int32_t lds, int32_t ldd, float grad_scale, void* stream);
+
 /* Memory-bound block kernels. */
 int maestro_add_rmsnorm_fwd(const void* x, const void* a, void* h, void* y, const void* w, float* rstd, int32_t T,
                             int32_t d, float eps, void* stream);

@@ -117,3 +117,54 @@ def adamw_reference(p, g, m, v, lr, step, b1=0.9, b2=0.95, eps=1e-8, wd=0.1):
     upd = (m / (1 - b1 ** step)) / ((v / (1 - b2 ** step)).sqrt() + eps)
     p.sub_(lr * (upd + wd * p))
     return p
+
+
+def vlm_step_reference(llm_shape, vit_shape, llm_flat, vit_flat, hb, merge_idx, patch_dim=768):
+    """fp32 autograd restatement of one VLM step (ViT -> 2x2 merge -> projector -> scatter into the
+    LLM sequence at the placeholder offset -> LLM -> next-token CE).  Returns (loss, llm grad, vit grad)."""
+    dev = llm_flat.device
+    lf = llm_flat.detach().clone().requires_grad_(True)
+    vf = vit_flat.detach().clone().requires_grad_(True)
+    Pl = param_views(llm_shape, lf)
+    extra = [("patch_w", (vit_shape.d, patch_dim)), ("proj_w", (llm_shape.d, 4 * vit_shape.d))]
+
+    class _S:  # vit shape + extra params
+        pass
+
+    Pv = {}
+    off = 0
+    for name, shp in vit_shape.param_shapes() + extra:
+        n = math.prod(shp)
+        Pv[name] = vf[off: off + n].view(*shp)
+        off += (n + 63) // 64 * 64
+    n_img = hb["pixels"].shape[0]
+    emb = None
+    if n_img:
+        px = torch.from_numpy(hb["pixels"]).to(dev).to(torch.bfloat16).float().view(-1, patch_dim)
+        x0 = px @ Pv["patch_w"].t()
+        cu = torch.arange(0, n_img * 196 + 1, 196, dtype=torch.int32, device=dev)
+        yf = forward(vit_shape, Pv, torch.zeros(n_img * 196, dtype=torch.int32, device=dev), cu, x0=x0)
+        src = (torch.from_numpy(merge_idx).to(dev)[None, :].long() + 196 * torch.arange(n_img, device=dev)[:, None]).reshape(-1)
+        merged = yf[src].view(n_img * 49, 4 * vit_shape.d)
+        emb = merged @ Pv["proj_w"].t()
+    total, nlab = 0.0, 0
+    loss_sum = torch.zeros((), device=dev)
+    for i in range(hb["ids"].shape[0]):
+        L = int(hb["lens"][i])
+        ids = torch.from_numpy(hb["ids"][i, :L]).to(dev)
+        lab = torch.from_numpy(hb["labels"][i, :L]).to(dev).long()
+        x = Pl["embed"][ids.clamp_min(0).long()] * (ids >= 0).float()[:, None]
+        if hb["has_img"][i]:
+            o = int(hb["img_offset"][i])
+            k = int(hb["img_ordinal"][i])
+            x = torch.cat([x[:o], emb[49 * k: 49 * k + 49], x[o + 49:]], 0)
+        cu = torch.tensor([0, L], dtype=torch.int32, device=dev)
+        y = forward(llm_shape, Pl, ids, cu, x0=x)
+        logits = y @ head_weight(llm_shape, Pl).t()
+        valid = lab >= 0
+        if valid.any():
+            loss_sum = loss_sum + F.cross_entropy(logits[valid], lab[valid], reduction="sum")
+            nlab += int(valid.sum())
+    loss = loss_sum / max(nlab, 1)
+    loss.backward()
+    return loss.item(), lf.grad, vf.grad

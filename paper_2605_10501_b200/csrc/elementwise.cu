@@ -192,7 +192,7 @@ __global__ void embed_fwd_kernel(const __nv_bfloat16* __restrict__ table, const 
                                  __nv_bfloat16* __restrict__ out, int T, int d) {
   const int lane = threadIdx.x & 31;
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (row >= T) return;
+  if (row >= T || ids[row] < 0) return;  // negative id = placeholder row filled by a scatter
   const uint4* src = reinterpret_cast<const uint4*>(table + (size_t)ids[row] * d);
   uint4* dst = reinterpret_cast<uint4*>(out + (size_t)row * d);
   for (int v = lane; v < d / 8; v += 32) dst[v] = src[v];
@@ -202,7 +202,7 @@ __global__ void embed_bwd_kernel(const __nv_bfloat16* __restrict__ dout, const i
                                  float* __restrict__ dtable, int T, int d) {
   const int lane = threadIdx.x & 31;
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (row >= T) return;
+  if (row >= T || ids[row] < 0) return;
   float* dst = dtable + (size_t)ids[row] * d;
   for (int c = lane * 8; c < d; c += 256) {
     float f[8];

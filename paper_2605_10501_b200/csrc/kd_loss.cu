@@ -143,6 +143,86 @@ __global__ void __launch_bounds__(KD_THREADS) kd_loss_kernel(const __nv_bfloat16
   }
 }
 
+
+// Next-token cross entropy over the full vocabulary with ignore index (label < 0):
+// loss[row] = lse(s) - s[label];  ds = grad_scale * (softmax(s) - onehot(label)).  Same
+// single-pass online max/sum-exp + L2-resident second pass as the KL kernel.
+__global__ void __launch_bounds__(KD_THREADS) ce_loss_kernel(const __nv_bfloat16* sl, const int32_t* __restrict__ labels,
+                                                             __nv_bfloat16* ds, float* __restrict__ loss, int T, int V,
+                                                             int lds, int ldd, float grad_scale) {
+  __shared__ float red_m[KD_THREADS / 32], red_s[KD_THREADS / 32];
+  __shared__ float fin_m, fin_s;
+  const int nvec = V / 8;
+  for (int row = blockIdx.x; row < T; row += gridDim.x) {
+    const int lab = labels[row];
+    const uint4* s4 = reinterpret_cast<const uint4*>(sl + (size_t)row * lds);
+    uint4* d4 = reinterpret_cast<uint4*>(ds + (size_t)row * ldd);
+    if (lab < 0) {  // ignored position: zero loss and gradient
+      for (int v = threadIdx.x; v < nvec; v += KD_THREADS) d4[v] = make_uint4(0, 0, 0, 0);
+      if (threadIdx.x == 0) loss[row] = 0.f;
+      continue;
+    }
+    float m = -INFINITY, ss = 0.f;
+    for (int v = threadIdx.x; v < nvec; v += KD_THREADS) {
+      float f[8];
+      unpack8(s4[v], f);
+      float mx = m;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) mx = fmaxf(mx, f[j] * LOG2E);
+      ss *= exp2f(m - mx);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) ss += exp2f(f[j] * LOG2E - mx);
+      m = mx;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float om = __shfl_xor_sync(kFull, m, o), os = __shfl_xor_sync(kFull, ss, o);
+      const float mx = fmaxf(m, om);
+      ss = (m == -INFINITY ? 0.f : ss * exp2f(m - mx)) + (om == -INFINITY ? 0.f : os * exp2f(om - mx));
+      m = mx;
+    }
+    if ((threadIdx.x & 31) == 0) {
+      red_m[threadIdx.x >> 5] = m;
+      red_s[threadIdx.x >> 5] = ss;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      m = threadIdx.x < KD_THREADS / 32 ? red_m[threadIdx.x] : -INFINITY;
+      ss = threadIdx.x < KD_THREADS / 32 ? red_s[threadIdx.x] : 0.f;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float om = __shfl_xor_sync(kFull, m, o), os = __shfl_xor_sync(kFull, ss, o);
+        const float mx = fmaxf(m, om);
+        ss = (m == -INFINITY ? 0.f : ss * exp2f(m - mx)) + (om == -INFINITY ? 0.f : os * exp2f(om - mx));
+        m = mx;
+      }
+      if (threadIdx.x == 0) {
+        fin_m = m;
+        fin_s = ss;
+        const float lse = (m + log2f(ss)) * LN2;
+        loss[row] = lse - __bfloat162float(sl[(size_t)row * lds + lab]);
+      }
+    }
+    __syncthreads();
+    const float fm = fin_m, inv = 1.f / fin_s;
+    for (int v = threadIdx.x; v < nvec; v += KD_THREADS) {
+      float f[8];
+      unpack8(s4[v], f);
+      uint4 o;
+      __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float g0 = exp2f(f[2 * j] * LOG2E - fm) * inv, g1 = exp2f(f[2 * j + 1] * LOG2E - fm) * inv;
+        if (8 * v + 2 * j == lab) g0 -= 1.f;
+        if (8 * v + 2 * j + 1 == lab) g1 -= 1.f;
+        oh[j] = __floats2bfloat162_rn(g0 * grad_scale, g1 * grad_scale);
+      }
+      d4[v] = o;
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace
 }  // namespace mb
 
@@ -160,5 +240,18 @@ MAESTRO_API int maestro_kd_loss_fwd_bwd(const void* d_t, const void* d_s, void* 
   kd_loss_kernel<<<grid, KD_THREADS, 0, (cudaStream_t)stream>>>(
       (const __nv_bfloat16*)d_t, (const __nv_bfloat16*)d_s, (__nv_bfloat16*)d_ds, d_loss, T, V, ldt, lds, ldd,
       inv_tau * LOG2E, grad_scale, inv_tau);
+  return launch_status();
+}
+
+// Cross entropy with ignore index (label < 0): loss[T], ds = grad_scale * dCE/ds (bf16, may alias s).
+MAESTRO_API int maestro_ce_loss_fwd_bwd(const void* d_s, const int32_t* d_labels, void* d_ds, float* d_loss,
+                                        int32_t T, int32_t V, int32_t lds, int32_t ldd, float grad_scale,
+                                        void* stream) {
+  if (T <= 0) return 0;
+  if (V % 8 || lds % 8 || ldd % 8) return (int)cudaErrorInvalidValue;
+  const int grid = T < 148 * 4 ? T : 148 * 4;
+  ce_loss_kernel<<<grid, KD_THREADS, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)d_s, d_labels,
+                                                                 (__nv_bfloat16*)d_ds, d_loss, T, V, lds, ldd,
+                                                                 grad_scale);
   return launch_status();
 }

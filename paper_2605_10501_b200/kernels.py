@@ -24,6 +24,9 @@ _SIGS = {
     "maestro_embed_bwd": [_P, _P, _P, _I32, _I32, _P],
     "maestro_adamw": [_P, _P, _P, _P, _P, _I64, _F, _F, _F, _F, _F, _I32, _F, _P],
     "maestro_kd_loss_fwd_bwd": [_P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32, _F, _F, _P],
+    "maestro_ce_loss_fwd_bwd": [_P, _P, _P, _P, _I32, _I32, _I32, _I32, _F, _P],
+    "maestro_scatter_rows_fwd": [_P, _P, _P, _P, _I32, _I32, _P],
+    "maestro_gather_rows_bwd": [_P, _P, _P, _P, _I32, _I32, _P],
 }
 _L = None
 
@@ -98,3 +101,23 @@ def kd_loss(t_logits, s_logits, ds, loss, grad_scale, tau=1.0):
     N.check(L().maestro_kd_loss_fwd_bwd(_p(t_logits), _p(s_logits), _p(ds), _p(loss), T, V, t_logits.stride(0),
                                         s_logits.stride(0), ds.stride(0) if ds is not None else 8, grad_scale,
                                         1.0 / tau, _s()), "kd_loss")
+
+
+def ce_loss(logits, labels, ds, loss, grad_scale):
+    """Fused full-vocab next-token cross entropy (+ d/dlogits); labels < 0 are ignored."""
+    T, V = logits.shape
+    N.check(L().maestro_ce_loss_fwd_bwd(_p(logits), _p(labels), _p(ds), _p(loss), T, V, logits.stride(0),
+                                        ds.stride(0), grad_scale, _s()), "ce_loss")
+
+
+def scatter_rows(src, dst, src_rows, dst_rows):
+    """K6: dst[dst_rows[k]] = src[src_rows[k]] (bf16 rows, 16-byte vectors)."""
+    n = src_rows.numel()
+    N.check(L().maestro_scatter_rows_fwd(_p(src), _p(dst), _p(src_rows), _p(dst_rows), n, src.shape[-1], _s()),
+            "scatter_rows")
+
+
+def gather_rows_bwd(ddst, dsrc, seg, seg_dst):
+    """K6 backward: dsrc[r] = sum_{k in seg[r]..seg[r+1]} ddst[seg_dst[k]] (fp32 accumulate)."""
+    N.check(L().maestro_gather_rows_bwd(_p(ddst), _p(dsrc), _p(seg), _p(seg_dst), dsrc.shape[0], dsrc.shape[-1],
+                                        _s()), "gather_rows_bwd")

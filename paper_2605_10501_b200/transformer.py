@@ -145,7 +145,7 @@ class Batch:
 
     @property
     def T(self) -> int:
-        return self.ids.shape[0]
+        return self.pos.shape[0]
 
 
 class Transformer:

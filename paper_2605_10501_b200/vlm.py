@@ -1,0 +1,291 @@
+"""VLM section graph (BASELINE cfg 1): ViT encoder (upstream) -> GPT backbone (critical).
+
+The executor follows the reference stage-queue contract (simulator.py:202-233) with the
+device wavefront schedule deciding both orders:
+
+* the critical (LLM) rank runs its micro-batches (mbs consecutive samples of its K3 order)
+  forward+backward, interleaved;
+* the upstream (ViT) rank runs all forward micro-batches of its K4 fan-out-merged order, then
+  all backward micro-batches in the same order;
+* an LLM micro-batch forward waits only for the ViT micro-batches that produced its images
+  (CUDA events; the wavefront order puts text-only samples first so the LLM starts at t=0),
+  and a ViT backward micro-batch waits for the LLM backwards that produced its gradients.
+
+Handoff (co-resident): ViT final hidden -> 2x2 patch merge (K6 row gather) -> projector GEMM ->
+image-token rows scattered into the LLM's packed embedding stream at placeholder positions
+(K6 scatter); the backward gathers the placeholder-row gradients back (K6) and runs the ViT
+backward.  Loss: next-token cross entropy over text targets (fused full-vocab CE kernel).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import _native as N
+from . import dense as D
+from . import kernels as K
+from . import recipes as R
+from .costs import cost_table
+from .executor import StageClock, StepStats
+from .scheduling import DevicePlanner, ExecPolicy
+from .synthetic import rand_int
+from .transformer import SHAPES, Batch, FlatParams, Transformer
+
+PATCH_DIM = 3 * 16 * 16  # pixels per 16x16 RGB patch
+GRID = 14                 # 224 / 16
+
+
+def merge_index() -> np.ndarray:
+    """Row gather for the 2x2 merge: merged row (i*7+j), part k <- patch (2i+k//2)*14 + 2j+k%2."""
+    out = np.empty(49 * 4, dtype=np.int32)
+    for i in range(7):
+        for j in range(7):
+            for k in range(4):
+                out[(i * 7 + j) * 4 + k] = (2 * i + k // 2) * GRID + 2 * j + k % 2
+    return out
+
+
+def vlm_host_batch(B: int, seed: int = 0, vocab: int = 32768, step: int = 0):
+    """Synthetic inputs of one step: padded ids/labels [B, Lmax], lengths, image flags, pixels."""
+    meta = R.vlm_tiny(1, B, seed).extra
+    has_img, tl, off = meta["has_image"], meta["text_len"], meta["img_offset"]
+    lens = tl + np.where(has_img, R.VIT_MERGED, 0)
+    Lmax = int(lens.max())
+    ids = np.full((B, Lmax), -1, dtype=np.int32)
+    labels = np.full((B, Lmax), -1, dtype=np.int32)
+    toks = rand_int(seed + 977 * step, 4, np.arange(B * 512), 0, vocab - 1).astype(np.int32).reshape(B, 512)
+    for i in range(B):
+        t = toks[i, : tl[i]]
+        if has_img[i]:
+            o = off[i]
+            seq = np.concatenate([t[:o], np.full(R.VIT_MERGED, -1, np.int32), t[o:]])
+        else:
+            seq = t
+        ids[i, : lens[i]] = seq
+        nxt = np.concatenate([seq[1:], [-1]])
+        lab = np.where((seq >= 0) & (nxt >= 0), nxt, -1)
+        labels[i, : lens[i]] = lab
+    n_img = int(has_img.sum())
+    g = np.random.default_rng(seed + step)
+    pixels = (g.standard_normal((n_img, 196, PATCH_DIM)) * 0.5).astype(np.float32)
+    img_ordinal = np.full(B, -1, dtype=np.int32)
+    img_ordinal[np.nonzero(has_img)[0]] = np.arange(n_img, dtype=np.int32)
+    return dict(ids=ids, labels=labels, lens=lens.astype(np.int32), has_img=has_img, img_offset=off,
+                pixels=pixels, img_ordinal=img_ordinal, n_labels=int((labels >= 0).sum()))
+
+
+class ViTSection:
+    """Patch embed -> bidirectional encoder -> final norm -> 2x2 merge -> projector."""
+
+    def __init__(self, shape, llm_d: int, device, seed: int):
+        self.s = shape
+        extra = [("patch_w", (shape.d, PATCH_DIM)), ("proj_w", (llm_d, 4 * shape.d))]
+        self.p = FlatParams(shape.param_shapes() + extra, device, trainable=True, seed=seed)
+        self.model = Transformer(shape, self.p, device, max_pos=256)
+        self.device = device
+        self.merge = torch.from_numpy(merge_index()).to(device)
+        self.llm_d = llm_d
+
+    def forward(self, pixels_bf16: torch.Tensor, n_img: int):
+        """pixels [n_img*196, 768] -> (image token embeddings [n_img*49, llm_d], ctx)."""
+        dev, s = self.device, self.s
+        T = n_img * 196
+        x0 = D.linear_fwd(pixels_bf16, self.p["patch_w"])
+        cu = torch.arange(0, T + 1, 196, dtype=torch.int32, device=dev)
+        pos = torch.empty(T, dtype=torch.int32, device=dev)
+        K.positions(cu, n_img, pos)
+        yf, ctx = self.model.forward(Batch(ids=None, cu=cu, pos=pos, max_len=196), x0=x0)
+        src = (self.merge[None, :] + 196 * torch.arange(n_img, device=dev, dtype=torch.int32)[:, None]).reshape(-1)
+        merged = torch.empty(n_img * 196, s.d, device=dev, dtype=torch.bfloat16)
+        K.scatter_rows(yf, merged, src, torch.arange(src.numel(), device=dev, dtype=torch.int32))
+        merged = merged.view(n_img * 49, 4 * s.d)
+        emb = D.linear_fwd(merged, self.p["proj_w"])
+        return emb, dict(ctx=ctx, merged=merged, src=src, pixels=pixels_bf16, n_img=n_img)
+
+    def backward(self, demb: torch.Tensor, st) -> None:
+        dev, s = self.device, self.s
+        D.linear_wgrad(demb, st["merged"], self.p.g("proj_w"))
+        dmerged = D.linear_dgrad(demb, self.p["proj_w"]).view(-1, s.d)
+        dyf = torch.empty_like(dmerged)
+        # un-merge: a permutation, so the scatter with swapped indices is its own inverse
+        K.scatter_rows(dmerged, dyf, torch.arange(st["src"].numel(), device=dev, dtype=torch.int32), st["src"])
+        dx0 = self.model.backward(st["ctx"], dyf=dyf, need_dx0=True)
+        D.linear_wgrad(dx0, st["pixels"], self.p.g("patch_w"))
+
+
+class VLMExecutor:
+    """Co-resident VLM step on one GPU (cfg 1 layout "1 GPU")."""
+
+    def __init__(self, batch: int = 64, mbs_llm: int = 8, mbs_vit: int = 8, seed: int = 0, lr: float = 3e-4,
+                 policy=ExecPolicy.INTERLEAVED, device=None):
+        self.device = dev = device or torch.device("cuda", torch.cuda.current_device())
+        self.batch, self.mbs_llm, self.mbs_vit = batch, mbs_llm, mbs_vit
+        self.rec = R.vlm_tiny(1, batch, seed)
+        from .workload import SectionConfig
+
+        self.configs = {"llm": SectionConfig(dp=1, mbs=mbs_llm), "vit": SectionConfig(dp=1, mbs=mbs_vit)}
+        self.graph = self.rec.graph
+        self.llm_shape = SHAPES["vlm_gpt2l"]
+        self.vit_shape = SHAPES["vit_tiny"]
+        self.llm = Transformer(self.llm_shape, FlatParams(self.llm_shape.param_shapes(), dev, True, seed + 10), dev,
+                               max_pos=1024)
+        self.vit = ViTSection(self.vit_shape, self.llm_shape.d, dev, seed + 11)
+        self.planner = DevicePlanner(self.graph, self.configs, policy, max_batch=batch, device=dev)
+        self.cost = torch.from_numpy(cost_table(self.graph, self.configs, self.rec.params)).to(dev)
+        self.lr = lr
+        self.s_llm = torch.cuda.Stream(device=dev)
+        self.s_vit = torch.cuda.Stream(device=dev)
+        self.step_idx = 0
+        tab = self.graph.tables
+        self.bits = {n: i for i, n in enumerate(tab.sub_names)}
+
+    def step(self, hb: dict, want_loss: bool = True) -> StepStats:
+        """One iteration from a host batch (vlm_host_batch); inputs are copied in per step."""
+        dev, B = self.device, self.batch
+        main = torch.cuda.current_stream(dev)
+        t0 = torch.cuda.Event(enable_timing=True)
+        t0.record(main)
+        ids = torch.from_numpy(hb["ids"]).to(dev, non_blocking=True)
+        labels = torch.from_numpy(hb["labels"]).to(dev, non_blocking=True)
+        lens = torch.from_numpy(hb["lens"]).to(dev, non_blocking=True)
+        pixels = torch.from_numpy(hb["pixels"]).to(dev, non_blocking=True).to(torch.bfloat16)
+        tok = np.zeros((len(self.bits), B), dtype=np.int32)
+        tok[self.bits["llm"]] = hb["lens"]
+        tok[self.bits["vit"]] = np.where(hb["has_img"], R.VIT_PATCHES, 0)
+        tokens = torch.from_numpy(tok).to(dev, non_blocking=True)
+        # ---- device plan: K1 6-tuples -> K2-K4 schedule
+        self.planner.ids[:B].copy_(torch.arange(B, dtype=torch.int32))
+        self.planner.plan_tokens(self.cost, tokens, B)
+        tab = self.graph.tables
+        ci, vi = tab.critical, tab.section_ids.index("vit")
+        W = N.MAX_DP + 1
+        off = self.planner.sec_off.view(-1, W)
+        # one small readback: both rank orders (<= 2 x 64 ints) define the micro-batch plan
+        orders = self.planner.orders.view(-1, B)
+        o_llm = orders[ci, :B].cpu().numpy()
+        n_vit = int(off[vi, 1].item())
+        o_vit = orders[vi, :n_vit].cpu().numpy()
+        # ---- K5 pack of the LLM order; token ids + labels in schedule order
+        o_llm_d = torch.from_numpy(o_llm).to(dev)
+        n_mb = -(-B // self.mbs_llm)
+        z = lambda k: torch.empty(k, dtype=torch.int32, device=dev)  # noqa: E731
+        mb, tok_off, mb_tok, cu, mb_start = z(B), z(B), z(n_mb), z(n_mb * (self.mbs_llm + 1)), z(n_mb)
+        s = main.cuda_stream
+        N.check(N.lib().maestro_varlen_pack(N.ptr(o_llm_d), B, N.ptr(lens), self.mbs_llm, N.ptr(mb), N.ptr(tok_off),
+                                            N.ptr(mb_tok), N.ptr(cu), N.ptr(mb_start), s), "varlen_pack")
+        lens_h = hb["lens"]
+        total = int(lens_h.sum())
+        p_ids, p_lab = z(total), z(total)
+        for src, dst in ((ids, p_ids), (labels, p_lab)):
+            N.check(N.lib().maestro_pack_tokens(N.ptr(src), src.shape[1], N.ptr(o_llm_d), N.ptr(lens), N.ptr(tok_off),
+                                                B, N.ptr(dst), s), "pack_tokens")
+        # host mirrors of the per-sample offsets (the orders are already on the host)
+        toff_h = np.concatenate([[0], np.cumsum(lens_h[o_llm])[:-1]]).astype(np.int64)
+        ordinal = hb["img_ordinal"]
+        vit_pos = {int(i): k for k, i in enumerate(o_vit)}  # sample -> slot in ViT order
+        n_vmb = -(-n_vit // self.mbs_vit)
+        ready = torch.cuda.Event()
+        ready.record(main)
+        clock = StageClock()
+        loss_acc = torch.zeros(1, device=dev)
+        grad_scale = 1.0 / max(hb["n_labels"], 1)
+        self.llm.p.zero_grad()
+        self.vit.p.zero_grad()
+        emb_buf = torch.empty(max(n_vit, 1) * 49, self.llm_shape.d, device=dev, dtype=torch.bfloat16)
+        demb_buf = torch.zeros_like(emb_buf)
+        # ---- ViT forward queue (upstream f_bc in merged order)
+        vit_fwd_ev, vit_ctx = [], []
+        self.s_vit.wait_event(ready)
+        with torch.cuda.stream(self.s_vit):
+            for k in range(n_vmb):
+                samples = o_vit[k * self.mbs_vit: (k + 1) * self.mbs_vit]
+                idx = torch.from_numpy(ordinal[samples].astype(np.int64)).to(dev)
+                px = pixels.index_select(0, idx).view(-1, PATCH_DIM)
+                emb, st = self.vit.forward(px, len(samples))
+                emb_buf[k * self.mbs_vit * 49: k * self.mbs_vit * 49 + emb.shape[0]].copy_(emb)
+                vit_ctx.append(st)
+                e = torch.cuda.Event()
+                e.record(self.s_vit)
+                vit_fwd_ev.append(e)
+        # ---- LLM queue: per micro-batch fwd + bwd (critical, interleaved)
+        llm_bwd_ev = []
+        d = self.llm_shape.d
+        self.s_llm.wait_event(ready)
+        with torch.cuda.stream(self.s_llm):
+            for m in range(n_mb):
+                ks = list(range(m * self.mbs_llm, min(B, (m + 1) * self.mbs_llm)))
+                samples = o_llm[ks]
+                start = int(toff_h[ks[0]])
+                T = int(lens_h[samples].sum())
+                cu_m = cu[m * (self.mbs_llm + 1): m * (self.mbs_llm + 1) + len(ks) + 1]
+                # dependencies: ViT micro-batches holding this micro-batch's images
+                slots = [vit_pos[int(i)] for i in samples if hb["has_img"][i]]
+                if slots:
+                    self.s_llm.wait_event(vit_fwd_ev[max(slots) // self.mbs_vit])
+                clock.begin(self.s_llm, f"llm{m}")
+                pos = torch.empty(T, dtype=torch.int32, device=dev)
+                K.positions(cu_m, len(ks), pos)
+                b = Batch(ids=p_ids[start: start + T], cu=cu_m, pos=pos, max_len=int(lens_h[samples].max()))
+                x0 = torch.empty(T, d, device=dev, dtype=torch.bfloat16)
+                K.embed(self.llm.p["embed"], b.ids, x0)
+                src_rows, dst_rows = [], []
+                for k, i in zip(ks, samples):
+                    if hb["has_img"][i]:
+                        base = int(toff_h[k]) - start + int(hb["img_offset"][i])
+                        src_rows.append(np.arange(49) + 49 * vit_pos[int(i)])
+                        dst_rows.append(np.arange(49) + base)
+                if src_rows:
+                    sr = torch.from_numpy(np.concatenate(src_rows).astype(np.int32)).to(dev)
+                    dr = torch.from_numpy(np.concatenate(dst_rows).astype(np.int32)).to(dev)
+                    K.scatter_rows(emb_buf, x0, sr, dr)
+                yf, ctx = self.llm.forward(b, x0=x0)
+                logits = self.llm.logits(yf)
+                tl = torch.empty(T, device=dev)
+                K.ce_loss(logits, p_lab[start: start + T], logits, tl, grad_scale)
+                loss_acc.add_(tl.sum())
+                dx0 = self.llm.backward(ctx, dlogits=logits, need_dx0=True)
+                K.embed_bwd(dx0, b.ids, self.llm.p.g("embed"))
+                if src_rows:
+                    # gradients of the placeholder rows back to the image-token slots (1:1 -> gather)
+                    seg = torch.arange(0, dr.numel() + 1, dtype=torch.int32, device=dev)
+                    tmp = torch.empty(dr.numel(), d, device=dev, dtype=torch.bfloat16)
+                    K.gather_rows_bwd(dx0, tmp, seg, dr)
+                    K.scatter_rows(tmp, demb_buf, torch.arange(sr.numel(), dtype=torch.int32, device=dev), sr)
+                clock.end(self.s_llm)
+                e = torch.cuda.Event()
+                e.record(self.s_llm)
+                llm_bwd_ev.append(e)
+        # ---- ViT backward queue (upstream b_ac, same order), after the LLM grads it needs
+        llm_mb_of = {int(o_llm[k]): k // self.mbs_llm for k in range(B)}
+        with torch.cuda.stream(self.s_vit):
+            for k in range(n_vmb):
+                samples = o_vit[k * self.mbs_vit: (k + 1) * self.mbs_vit]
+                self.s_vit.wait_event(llm_bwd_ev[max(llm_mb_of[int(i)] for i in samples)])
+                a = k * self.mbs_vit * 49
+                self.vit.backward(demb_buf[a: a + len(samples) * 49], vit_ctx[k])
+            self.vit.p.adamw(self.lr)
+        with torch.cuda.stream(self.s_llm):
+            self.llm.p.adamw(self.lr)
+        main.wait_stream(self.s_llm)
+        main.wait_stream(self.s_vit)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t1.record(main)
+        self.step_idx += 1
+        loss = float(loss_acc.item()) * grad_scale if want_loss else None
+        t1.synchronize()
+        busy, span = clock.busy_span()
+        return StepStats(loss, t0.elapsed_time(t1), busy, span)
+
+    def model_flops_per_step(self, hb) -> float:
+        L = self.llm_shape
+        toks = int(hb["lens"].sum())
+        avg = float(np.mean(hb["lens"]))
+        llm = 3.0 * toks * L.fwd_flops_per_token(int(avg), with_head=True)
+        V = self.vit_shape
+        n_img = int(hb["has_img"].sum())
+        vit = 3.0 * n_img * (196 * (V.fwd_flops_per_token(196, with_head=False) + 2 * PATCH_DIM * V.d)
+                             + 49 * 2 * 4 * V.d * L.d)
+        return llm + vit

@@ -1,0 +1,39 @@
+"""GPU: VLM (cfg 1) executor step vs the fp32 autograd restatement (loss + gradients of both sections)."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import torch_ref as R
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return ((a.float() - b.float()).abs().max() / b.float().abs().max().clamp_min(1e-6)).item()
+
+
+def test_vlm_step_matches_reference():
+    from paper_2605_10501_b200 import vlm
+
+    ex = vlm.VLMExecutor(batch=12, mbs_llm=4, mbs_vit=3, lr=0.0)
+    hb = vlm.vlm_host_batch(12, seed=3)
+    lf, vf = ex.llm.p.w.float().clone(), ex.vit.p.w.float().clone()
+    st = ex.step(hb)
+    loss, gl, gv = R.vlm_step_reference(ex.llm_shape, ex.vit_shape, lf, vf, hb, vlm.merge_index())
+    assert abs(st.loss - loss) / loss < 2e-2
+    Pg = R.param_views(ex.llm_shape, ex.llm.p.grad)
+    Pr = R.param_views(ex.llm_shape, gl)
+    for name in ("embed", "head", "l0.wqkv", "l1.wd", "lnf"):
+        assert rel(Pg[name], Pr[name]) < 6e-2, name
+    # ViT section gradients (flat arena incl. patch / projector weights)
+    assert rel(ex.vit.p.grad[: gv.numel()], gv) < 8e-2
+
+
+def test_vlm_loss_decreases():
+    from paper_2605_10501_b200 import vlm
+
+    ex = vlm.VLMExecutor(batch=16, mbs_llm=8, mbs_vit=4, lr=1e-3)
+    hb = vlm.vlm_host_batch(16, seed=1)
+    losses = [ex.step(hb).loss for _ in range(4)]
+    assert all(np.isfinite(losses)) and losses[-1] < losses[0]
