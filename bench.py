@@ -157,6 +157,46 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------------------------------------- VLM leg
+def run_vlm(args):
+    """configs[0] (tiny VLM: ViT-tiny encoder -> 2-layer GPT, 50/50 text/image) on one GPU."""
+    import torch
+
+    from paper_2605_10501_b200 import instrument
+    from paper_2605_10501_b200.vlm import VLMExecutor, vlm_host_batch
+
+    if args.gpus != 1:
+        raise SystemExit("the VLM workload is wired for 1 GPU (co-resident sections)")
+    B = args.batch_per_rank
+    ex = VLMExecutor(batch=B, mbs_llm=8, mbs_vit=8)
+    hb = vlm_host_batch(B, seed=0)
+    for _ in range(args.warmup):
+        ex.step(hb, want_loss=False)
+    torch.cuda.synchronize()
+    launches0 = instrument.launches
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stalls = []
+    e0.record()
+    for _ in range(args.steps):
+        st = ex.step(hb, want_loss=True)
+        stalls.append(st.stall_frac)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    value = B * args.steps / (ms / 1e3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": "vlm_cfg1: ViT-tiny (d192 L12) -> 2-layer GPT (d768), 50/50 text/image, "
+                               "wavefront schedule on device", "global_batch": B, "seq_len": "64..497",
+                   "parallelism": "colocated vit+llm", "note": "end-to-end: inputs copied from host every step"},
+        "section_stall_pct": 100.0 * max(stalls), "gpu_launches": (instrument.launches - launches0) // args.steps,
+        "model_tflops": ex.model_flops_per_step(hb) * args.steps / (ms / 1e3) / 1e12, "loss": st.loss,
+    }
+    print(json.dumps(line), flush=True)
+
+
 # ---------------------------------------------------------------------------------------------- GPU leg
 def main():
     ap = argparse.ArgumentParser()
@@ -168,7 +208,12 @@ def main():
     ap.add_argument("--batch-per-rank", type=int, default=BATCH_PER_RANK)
     ap.add_argument("--mbs", type=int, default=MBS)
     ap.add_argument("--layout", default="colocated", choices=["colocated", "disjoint"])
+    ap.add_argument("--workload", default="kd", choices=["kd", "vlm"],
+                    help="kd = BASELINE configs[1] (default); vlm = configs[0] tiny VLM, 1 GPU")
     args = ap.parse_args()
+    if args.workload == "vlm":
+        run_vlm(args)
+        return
     if args.impl == "reference":
         run_reference(args)
         return

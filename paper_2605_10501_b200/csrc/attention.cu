@@ -65,6 +65,12 @@ __global__ void attn_tiles_kernel(const int32_t* __restrict__ cu, int nseq, int2
   if (threadIdx.x == 0) *count = s_n;
 }
 
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ uint32_t p_offset(int r, int c) {
   // (row r, col c) of a 128 x 128 bf16 operand stored as two K-major SWIZZLE_128B chunks
   const int chunk = c >> 6, cc = c & 63;
@@ -210,33 +216,34 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       mbar_arrive(&s_empty[b]);
       const int kv0 = i * BKV;
       const bool need_mask = (CAUSAL && kv0 + BKV - 1 > q0) || (kv0 + BKV > L);
-      float mx = -INFINITY;
+      float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};  // 4 chains: ILP
       if (need_mask) {
 #pragma unroll
         for (int c = 0; c < BKV; ++c) {
           const int kv = kv0 + c;
           if ((CAUSAL && kv > qpos) || kv >= L) s[c] = -INFINITY;
-          mx = fmaxf(mx, s[c]);
+          mx4[c & 3] = fmaxf(mx4[c & 3], s[c]);
         }
       } else {
 #pragma unroll
-        for (int c = 0; c < BKV; ++c) mx = fmaxf(mx, s[c]);
+        for (int c = 0; c < BKV; ++c) mx4[c & 3] = fmaxf(mx4[c & 3], s[c]);
       }
-      const float m_new = mx * scale2;
+      const float m_new = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * scale2;
       bool rescale = false;
       float alpha = 1.f;
       if (m_new > m + 8.0f) {  // lazy rescale: keep a stale max unless it grew by > 2^8
-        alpha = exp2f(m - m_new);
+        alpha = ex2(m - m_new);
         m = m_new;
         rescale = i > 0;
       }
-      float rowsum = 0.f;
+      float sum4[4] = {0.f, 0.f, 0.f, 0.f};
+      const float neg_m = -m;
 #pragma unroll
       for (int c = 0; c < BKV; ++c) {
-        s[c] = exp2f(s[c] * scale2 - m);
-        rowsum += s[c];
+        s[c] = ex2(fmaf(s[c], scale2, neg_m));
+        sum4[c & 3] += s[c];
       }
-      l = l * alpha + rowsum;
+      l = l * alpha + ((sum4[0] + sum4[1]) + (sum4[2] + sum4[3]));
       // P buffer b was last read by PV_{i-2}
       if (i >= 2) mbar_wait(&p_empty[b], ((i >> 1) + 1) & 1);
       if (rescale) {
@@ -484,7 +491,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const int c = c0 + j;
-          float pv = exp2f(__uint_as_float(sr[j]) * scale2 - lse_t[c]);
+          float pv = ex2(fmaf(__uint_as_float(sr[j]), scale2, -lse_t[c]));
           if (need_mask) {
             const int qpos = q0 + c;
             if ((CAUSAL && qpos < kvpos) || qpos >= L || kvpos >= L) pv = 0.f;
