@@ -151,6 +151,12 @@ int maestro_gather_rows_bwd(const void* d_ddst, void* d_dsrc, const int32_t* d_s
 int maestro_gemm_bf16(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K, int32_t lda,
                       int32_t ldb, int32_t ldc, int32_t a_mn, int32_t b_mn, int32_t epi, void* stream);
 
+/* K7 + fused RoPE epilogue: C = A B^T (bf16, K-major A/B); every 64-column head in columns
+ * [0, rope_cols) is rotated (rotate-half) at position pos[row]; cos_sin[p][32] = (cos, sin). */
+int maestro_gemm_bf16_rope(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K, int32_t lda,
+                           int32_t ldb, int32_t ldc, const int32_t* pos, const void* cos_sin, int32_t rope_cols,
+                           void* stream);
+
 /* K8 -- varlen GQA attention, head_dim 64: q [T,H,64], k/v [T,Hk,64] (pitched), cu [nseq+1];
  * out [T,H,64] bf16, lse [H,T] fp32 (natural LSE of the scaled scores). */
 int64_t maestro_attn_workspace(int32_t T, int32_t nseq);
@@ -162,7 +168,9 @@ int maestro_attn_bwd(const void* dout, int32_t lddo, const void* q, const void* 
                      int32_t ldo, const float* lse, const int32_t* cu, int32_t nseq, int32_t T, int32_t H,
                      int32_t Hk, int32_t head_dim, int32_t ldq, int32_t ldk, int32_t ldv, void* dq, int32_t lddq,
                      void* dk, int32_t lddk, void* dv, int32_t lddv, float softmax_scale, int32_t causal,
-                     void* workspace, void* stream);
+                     const int32_t* rope_pos, const void* rope_cos_sin, void* workspace, void* stream);
+/* (rope_pos/rope_cos_sin non-null: dQ and dK are returned through the inverse RoPE rotation,
+ * i.e. w.r.t. the pre-rotation projections.) */
 
 /* K9 -- fused full-vocab KL(softmax(t/tau) || softmax(s/tau)) per token (d_loss[T]) and
  * ds = grad_scale * dKL/ds (bf16, may alias s).  Teacher head colocated per workload.py:471-514. */

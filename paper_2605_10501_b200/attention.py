@@ -26,7 +26,7 @@ def _lib():
             "maestro_attn_fwd": ([_P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P, _I32, _P, _F,
                                   _I32, _P, _P], ctypes.c_int),
             "maestro_attn_bwd": ([_P, _I32, _P, _P, _P, _P, _I32, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _I32,
-                                  _I32, _P, _I32, _P, _I32, _P, _I32, _F, _I32, _P, _P], ctypes.c_int),
+                                  _I32, _P, _I32, _P, _I32, _P, _I32, _F, _I32, _P, _P, _P, _P], ctypes.c_int),
         })
     return _bound
 
@@ -50,7 +50,8 @@ def attn_fwd(q, k, v, cu, max_len: int, causal: bool, out, scale: float):
     return lse
 
 
-def attn_bwd(do, q, k, v, o, lse, cu, max_len: int, causal: bool, dq, dk, dv, scale: float):
+def attn_bwd(do, q, k, v, o, lse, cu, max_len: int, causal: bool, dq, dk, dv, scale: float, rope=None):
+    """rope=(pos, cos_sin): dq/dk come back through the inverse RoPE rotation (fused)."""
     L = _lib()
     T, H, dh = q.shape
     Hk = k.shape[1]
@@ -59,5 +60,6 @@ def attn_bwd(do, q, k, v, o, lse, cu, max_len: int, causal: bool, dq, dk, dv, sc
     rc = L.maestro_attn_bwd(do.data_ptr(), do.stride(0), q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
                             o.stride(0), lse.data_ptr(), cu.data_ptr(), nseq, T, H, Hk, dh, q.stride(0), k.stride(0),
                             v.stride(0), dq.data_ptr(), dq.stride(0), dk.data_ptr(), dk.stride(0), dv.data_ptr(),
-                            dv.stride(0), scale, int(causal), ws.data_ptr(), N.stream_ptr())
+                            dv.stride(0), scale, int(causal), rope[0].data_ptr() if rope else None,
+                            rope[1].data_ptr() if rope else None, ws.data_ptr(), N.stream_ptr())
     N.check(rc, "attn_bwd")

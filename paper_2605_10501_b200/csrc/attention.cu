@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
                     const int32_t* __restrict__ cu, const int2* __restrict__ tiles, const int* __restrict__ n_tiles,
                     const float* __restrict__ lse, const float* __restrict__ Dvec, float* __restrict__ dq_acc,
                     __nv_bfloat16* __restrict__ dk, int lddk, __nv_bfloat16* __restrict__ dv, int lddv, int T, int H,
-                    int Hk, float scale2, float scale) {
+                    int Hk, float scale2, float scale, const float2* __restrict__ rope_cs) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + BwdSmem::BAR);
@@ -546,14 +546,25 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     for (int which = 0; which < 2; ++which) {
       uint32_t o[DH / 2];
       const float f = which == 0 ? scale : 1.f;
+      uint32_t lo[32], hi[32];
+      tmem_ld_32x32b_x32(tmem + lane_base + (which == 0 ? T_DK : T_DV), lo);
+      tmem_ld_32x32b_x32(tmem + lane_base + (which == 0 ? T_DK : T_DV) + 32, hi);
+      tmem_ld_wait();
+      if (which == 0 && rope_cs != nullptr && kvpos < L) {
+        // K was rotated by RoPE in the forward: dK_pre = R(pos)^T dK  (rotate by -theta)
+        const float2* csr = rope_cs + (size_t)kvpos * 32;
 #pragma unroll
-      for (int c = 0; c < DH / 32; ++c) {
-        uint32_t rr[32];
-        tmem_ld_32x32b_x32(tmem + lane_base + (which == 0 ? T_DK : T_DV) + c * 32, rr);
-        tmem_ld_wait();
+        for (int k = 0; k < 32; ++k) {
+          const float2 cs = csr[k];
+          const float a = __uint_as_float(lo[k]), b = __uint_as_float(hi[k]);
+          lo[k] = __float_as_uint(a * cs.x + b * cs.y);
+          hi[k] = __float_as_uint(b * cs.x - a * cs.y);
+        }
+      }
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-          o[c * 16 + j] = pack_bf16(__uint_as_float(rr[2 * j]) * f, __uint_as_float(rr[2 * j + 1]) * f);
+      for (int j = 0; j < 16; ++j) {
+        o[j] = pack_bf16(__uint_as_float(lo[2 * j]) * f, __uint_as_float(lo[2 * j + 1]) * f);
+        o[16 + j] = pack_bf16(__uint_as_float(hi[2 * j]) * f, __uint_as_float(hi[2 * j + 1]) * f);
       }
       if (kvpos < L) {
         __nv_bfloat16* base = which == 0 ? dk + (size_t)(s0 + kvpos) * lddk : dv + (size_t)(s0 + kvpos) * lddv;
@@ -587,21 +598,45 @@ __global__ void attn_bwd_pre_kernel(const __nv_bfloat16* __restrict__ o, int ldo
   reinterpret_cast<float2*>(dq_acc + ((size_t)t * H + h) * DH)[lane] = make_float2(0.f, 0.f);
 }
 
-// dq[t, h, :] (bf16, pitched) = scale * dq_acc[t, h, :]
+// dq[t, h, :] (bf16, pitched) = scale * dq_acc[t, h, :], then the inverse RoPE rotation at
+// the token's sequence position (cs == null: no rotation).  Thread per (t, h, 8 pair-groups).
 __global__ void attn_bwd_post_kernel(const float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dq, int lddq, int T,
-                                     int H, float scale) {
-  const long long n = (long long)T * H * DH / 8;
+                                     int H, float scale, const int32_t* __restrict__ pos,
+                                     const float2* __restrict__ cs) {
+  const long long n = (long long)T * H * 4;  // 4 groups of 8 rotation pairs per head
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const long long e = i * 8;
-    const long long t = e / (H * DH), rem = e - t * H * DH;
-    const float4 a = reinterpret_cast<const float4*>(dq_acc + e)[0];
-    const float4 b = reinterpret_cast<const float4*>(dq_acc + e)[1];
-    uint4 v;
-    v.x = pack_bf16(a.x * scale, a.y * scale);
-    v.y = pack_bf16(a.z * scale, a.w * scale);
-    v.z = pack_bf16(b.x * scale, b.y * scale);
-    v.w = pack_bf16(b.z * scale, b.w * scale);
-    *reinterpret_cast<uint4*>(dq + t * lddq + rem) = v;
+    const long long th = i >> 2;
+    const int g = (int)(i & 3);
+    const long long t = th / H;
+    const int h = (int)(th - t * H);
+    const float* src = dq_acc + th * DH + 8 * g;
+    float a[8], b[8];
+    *reinterpret_cast<float4*>(a) = reinterpret_cast<const float4*>(src)[0];
+    *reinterpret_cast<float4*>(a + 4) = reinterpret_cast<const float4*>(src)[1];
+    *reinterpret_cast<float4*>(b) = reinterpret_cast<const float4*>(src + 32)[0];
+    *reinterpret_cast<float4*>(b + 4) = reinterpret_cast<const float4*>(src + 32)[1];
+    if (cs != nullptr) {
+      const float2* c = cs + (size_t)pos[t] * 32 + 8 * g;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float2 v = c[k];
+        const float x = a[k], y = b[k];
+        a[k] = x * v.x + y * v.y;
+        b[k] = y * v.x - x * v.y;
+      }
+    }
+    uint4 va, vb;
+    va.x = pack_bf16(a[0] * scale, a[1] * scale);
+    va.y = pack_bf16(a[2] * scale, a[3] * scale);
+    va.z = pack_bf16(a[4] * scale, a[5] * scale);
+    va.w = pack_bf16(a[6] * scale, a[7] * scale);
+    vb.x = pack_bf16(b[0] * scale, b[1] * scale);
+    vb.y = pack_bf16(b[2] * scale, b[3] * scale);
+    vb.z = pack_bf16(b[4] * scale, b[5] * scale);
+    vb.w = pack_bf16(b[6] * scale, b[7] * scale);
+    __nv_bfloat16* d = dq + t * lddq + h * DH + 8 * g;
+    *reinterpret_cast<uint4*>(d) = va;
+    *reinterpret_cast<uint4*>(d + 32) = vb;
   }
 }
 
@@ -684,7 +719,8 @@ MAESTRO_API int maestro_attn_bwd(const void* dout, int32_t lddo, const void* q, 
                                  const void* o, int32_t ldo, const float* lse, const int32_t* cu, int32_t nseq,
                                  int32_t T, int32_t H, int32_t Hk, int32_t head_dim, int32_t ldq, int32_t ldk,
                                  int32_t ldv, void* dq, int32_t lddq, void* dk, int32_t lddk, void* dv, int32_t lddv,
-                                 float softmax_scale, int32_t causal, void* workspace, void* stream) {
+                                 float softmax_scale, int32_t causal, const int32_t* rope_pos, const void* rope_cs,
+                                 void* workspace, void* stream) {
   if (T <= 0) return 0;
   if (head_dim != DH || H % Hk) return (int)cudaErrorInvalidValue;
   cudaStream_t st = (cudaStream_t)stream;
@@ -713,15 +749,15 @@ MAESTRO_API int maestro_attn_bwd(const void* dout, int32_t lddo, const void* q, 
     if (ensure_smem<attn_bwd_kernel<true>>(smem)) return launch_status();
     attn_bwd_kernel<true><<<grid, BWD_THREADS, smem, st>>>(mq, mk, mv, mdo, cu, tiles, count, lse, Dvec, dq_acc,
                                                           (__nv_bfloat16*)dk, lddk, (__nv_bfloat16*)dv, lddv, T, H, Hk,
-                                                          scale2, softmax_scale);
+                                                          scale2, softmax_scale, (const float2*)rope_cs);
   } else {
     if (ensure_smem<attn_bwd_kernel<false>>(smem)) return launch_status();
     attn_bwd_kernel<false><<<grid, BWD_THREADS, smem, st>>>(mq, mk, mv, mdo, cu, tiles, count, lse, Dvec, dq_acc,
                                                            (__nv_bfloat16*)dk, lddk, (__nv_bfloat16*)dv, lddv, T, H,
-                                                           Hk, scale2, softmax_scale);
+                                                           Hk, scale2, softmax_scale, (const float2*)rope_cs);
   }
-  const long long n8 = (long long)T * H * DH / 8;
-  attn_bwd_post_kernel<<<(unsigned)((n8 + 255) / 256 < 148 * 16 ? (n8 + 255) / 256 : 148 * 16), 256, 0, st>>>(
-      dq_acc, (__nv_bfloat16*)dq, lddq, T, H, softmax_scale);
+  const long long n4 = (long long)T * H * 4;
+  attn_bwd_post_kernel<<<(unsigned)((n4 + 255) / 256 < 148 * 16 ? (n4 + 255) / 256 : 148 * 16), 256, 0, st>>>(
+      dq_acc, (__nv_bfloat16*)dq, lddq, T, H, softmax_scale, rope_pos, (const float2*)rope_cs);
   return launch_status();
 }

@@ -32,8 +32,127 @@ __device__ __forceinline__ float warp_sum(float v) {
 }
 
 // ---------------------------------------------------------------- RMSNorm
-// h = x (+ a); y = h * rsqrt(mean(h^2) + eps) * w.  One warp per row.
+// h = x (+ a); y = h * rsqrt(mean(h^2) + eps) * w.  One warp per row, the row held in
+// registers (NV 16-byte vectors per lane, d = 256 * NV): one HBM read of x (and a), one write
+// of h and y.
+template <int NV>
 __global__ void __launch_bounds__(256) add_rmsnorm_fwd_kernel(const __nv_bfloat16* __restrict__ x,
+                                                              const __nv_bfloat16* __restrict__ a,
+                                                              __nv_bfloat16* __restrict__ h,
+                                                              __nv_bfloat16* __restrict__ y,
+                                                              const __nv_bfloat16* __restrict__ w,
+                                                              float* __restrict__ rstd, int T, int d, float eps) {
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= T) return;
+  const size_t base = (size_t)row * d;
+  float f[NV][8];
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int c = (k * 32 + lane) * 8;
+    ld8(x + base + c, f[k]);
+    if (a != nullptr) {
+      float g[8];
+      ld8(a + base + c, g);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) f[k][j] += g[j];
+      // normalise the bf16-rounded residual exactly as stored
+      uint4 v;
+      __nv_bfloat162* hv = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        hv[j] = __floats2bfloat162_rn(f[k][2 * j], f[k][2 * j + 1]);
+        const float2 back = __bfloat1622float2(hv[j]);
+        f[k][2 * j] = back.x;
+        f[k][2 * j + 1] = back.y;
+      }
+      *reinterpret_cast<uint4*>(h + base + c) = v;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) ss += f[k][j] * f[k][j];
+  }
+  ss = warp_sum(ss);
+  const float r = rsqrtf(ss / d + eps);
+  if (lane == 0) rstd[row] = r;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int c = (k * 32 + lane) * 8;
+    float g[8];
+    ld8(w + c, g);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) f[k][j] = f[k][j] * r * g[j];
+    st8(y + base + c, f[k]);
+  }
+}
+
+// dx = dres + r * (w*dy - hn * mean(hn * w * dy)),  hn = h * r;  dw += sum_rows dy * hn.
+// Warp per row, rows in registers; each lane owns fixed columns, so its dw partials stay in
+// registers across all rows the warp visits and are reduced through smem once per CTA.
+template <int NV>
+__global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(const __nv_bfloat16* __restrict__ dy,
+                                                          const __nv_bfloat16* __restrict__ h,
+                                                          const __nv_bfloat16* __restrict__ w,
+                                                          const float* __restrict__ rstd,
+                                                          const __nv_bfloat16* dres, __nv_bfloat16* dx,
+                                                          float* __restrict__ dw, int T, int d) {
+  extern __shared__ float sdw[];
+  for (int c = threadIdx.x; c < d; c += blockDim.x) sdw[c] = 0.f;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+  float acc[NV][8];
+  float wv[NV][8];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    ld8(w + (k * 32 + lane) * 8, wv[k]);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[k][j] = 0.f;
+  }
+  for (int row = blockIdx.x * nw + warp; row < T; row += gridDim.x * nw) {
+    const size_t base = (size_t)row * d;
+    const float r = rstd[row];
+    float g[NV][8], hn[NV][8];
+    float dot = 0.f;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const int c = (k * 32 + lane) * 8;
+      ld8(dy + base + c, g[k]);
+      ld8(h + base + c, hn[k]);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        hn[k][j] *= r;
+        dot += hn[k][j] * wv[k][j] * g[k][j];
+        acc[k][j] += g[k][j] * hn[k][j];
+      }
+    }
+    dot = warp_sum(dot) / d;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const int c = (k * 32 + lane) * 8;
+      float o[8];
+      if (dres != nullptr) {
+        ld8(dres + base + c, o);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] = 0.f;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] += r * (wv[k][j] * g[k][j] - hn[k][j] * dot);
+      st8(dx + base + c, o);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) atomicAdd(&sdw[(k * 32 + lane) * 8 + j], acc[k][j]);
+  __syncthreads();
+  for (int c = threadIdx.x; c < d; c += blockDim.x) atomicAdd(&dw[c], sdw[c]);
+}
+
+// ---------------------------------------------------------------- RMSNorm, any d (multiple of 8)
+// h = x (+ a); y = h * rsqrt(mean(h^2) + eps) * w.  One warp per row.
+__global__ void __launch_bounds__(256) rmsnorm_generic_fwd_kernel(const __nv_bfloat16* __restrict__ x,
                                                               const __nv_bfloat16* __restrict__ a,
                                                               __nv_bfloat16* __restrict__ h,
                                                               __nv_bfloat16* __restrict__ y,
@@ -73,7 +192,7 @@ __global__ void __launch_bounds__(256) add_rmsnorm_fwd_kernel(const __nv_bfloat1
 }
 
 // dx = dres + r * (w*dy - hn * mean(hn * w * dy)),  hn = h * r;  dw += sum_rows dy * hn
-__global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(const __nv_bfloat16* __restrict__ dy,
+__global__ void __launch_bounds__(256) rmsnorm_generic_bwd_kernel(const __nv_bfloat16* __restrict__ dy,
                                                           const __nv_bfloat16* __restrict__ h,
                                                           const __nv_bfloat16* __restrict__ w,
                                                           const float* __restrict__ rstd,
@@ -255,27 +374,79 @@ inline int grid_for(long long work, int threads) {
 
 using namespace mb;
 
+static int rmsnorm_generic_fwd(const void* x, const void* a, void* h, void* y, const void* w, float* rstd, int T,
+                               int d, float eps, cudaStream_t st) {
+  rmsnorm_generic_fwd_kernel<<<(T + 7) / 8, 256, 0, st>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)a,
+                                                          (__nv_bfloat16*)h, (__nv_bfloat16*)y,
+                                                          (const __nv_bfloat16*)w, rstd, T, d, eps);
+  return launch_status();
+}
+
+static int rmsnorm_generic_bwd(const void* dy, const void* h, const void* w, const float* rstd, const void* dres,
+                               void* dx, float* dw, int T, int d, cudaStream_t st) {
+  const size_t smem = (size_t)d * sizeof(float);
+  if (ensure_smem<rmsnorm_generic_bwd_kernel>(smem)) return launch_status();
+  const int grid = T / 8 < 148 * 2 ? (T + 7) / 8 : 148 * 2;
+  rmsnorm_generic_bwd_kernel<<<grid, 256, smem, st>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)h,
+                                                      (const __nv_bfloat16*)w, rstd, (const __nv_bfloat16*)dres,
+                                                      (__nv_bfloat16*)dx, dw, T, d);
+  return launch_status();
+}
+
+template <int NV>
+static int rmsnorm_fwd_launch(const void* x, const void* a, void* h, void* y, const void* w, float* rstd, int T, int d,
+                              float eps, cudaStream_t st) {
+  add_rmsnorm_fwd_kernel<NV><<<(T + 7) / 8, 256, 0, st>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)a,
+                                                          (__nv_bfloat16*)h, (__nv_bfloat16*)y,
+                                                          (const __nv_bfloat16*)w, rstd, T, d, eps);
+  return launch_status();
+}
+
+template <int NV>
+static int rmsnorm_bwd_launch(const void* dy, const void* h, const void* w, const float* rstd, const void* dres,
+                              void* dx, float* dw, int T, int d, cudaStream_t st) {
+  const size_t smem = (size_t)d * sizeof(float);
+  if (ensure_smem<rmsnorm_bwd_kernel<NV>>(smem)) return launch_status();
+  const int grid = T / 8 < 148 * 2 ? (T + 7) / 8 : 148 * 2;
+  rmsnorm_bwd_kernel<NV><<<grid, 256, smem, st>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)h,
+                                                  (const __nv_bfloat16*)w, rstd, (const __nv_bfloat16*)dres,
+                                                  (__nv_bfloat16*)dx, dw, T, d);
+  return launch_status();
+}
+
+// register-resident fast path for d in {256 .. 4096} multiples of 256; generic path otherwise
 MAESTRO_API int maestro_add_rmsnorm_fwd(const void* x, const void* a, void* h, void* y, const void* w, float* rstd,
                                         int32_t T, int32_t d, float eps, void* stream) {
   if (T <= 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (d) {
+    case 256: return rmsnorm_fwd_launch<1>(x, a, h, y, w, rstd, T, d, eps, st);
+    case 512: return rmsnorm_fwd_launch<2>(x, a, h, y, w, rstd, T, d, eps, st);
+    case 768: return rmsnorm_fwd_launch<3>(x, a, h, y, w, rstd, T, d, eps, st);
+    case 1024: return rmsnorm_fwd_launch<4>(x, a, h, y, w, rstd, T, d, eps, st);
+    case 2048: return rmsnorm_fwd_launch<8>(x, a, h, y, w, rstd, T, d, eps, st);
+    case 3584: return rmsnorm_fwd_launch<14>(x, a, h, y, w, rstd, T, d, eps, st);
+    case 4096: return rmsnorm_fwd_launch<16>(x, a, h, y, w, rstd, T, d, eps, st);
+    default: break;
+  }
   if (d % 8) return (int)cudaErrorInvalidValue;
-  add_rmsnorm_fwd_kernel<<<(T + 7) / 8, 256, 0, (cudaStream_t)stream>>>(
-      (const __nv_bfloat16*)x, (const __nv_bfloat16*)a, (__nv_bfloat16*)h, (__nv_bfloat16*)y,
-      (const __nv_bfloat16*)w, rstd, T, d, eps);
-  return launch_status();
+  return rmsnorm_generic_fwd(x, a, h, y, w, rstd, T, d, eps, st);
 }
 
 MAESTRO_API int maestro_rmsnorm_bwd(const void* dy, const void* h, const void* w, const float* rstd,
                                     const void* dres, void* dx, float* dw, int32_t T, int32_t d, void* stream) {
   if (T <= 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (d) {
+    case 256: return rmsnorm_bwd_launch<1>(dy, h, w, rstd, dres, dx, dw, T, d, st);
+    case 512: return rmsnorm_bwd_launch<2>(dy, h, w, rstd, dres, dx, dw, T, d, st);
+    case 768: return rmsnorm_bwd_launch<3>(dy, h, w, rstd, dres, dx, dw, T, d, st);
+    case 1024: return rmsnorm_bwd_launch<4>(dy, h, w, rstd, dres, dx, dw, T, d, st);
+    case 2048: return rmsnorm_bwd_launch<8>(dy, h, w, rstd, dres, dx, dw, T, d, st);
+    default: break;
+  }
   if (d % 8) return (int)cudaErrorInvalidValue;
-  const size_t smem = (size_t)d * sizeof(float);
-  if (ensure_smem<rmsnorm_bwd_kernel>(smem)) return launch_status();
-  const int grid = T / 8 < 148 * 2 ? (T + 7) / 8 : 148 * 2;
-  rmsnorm_bwd_kernel<<<grid, 256, smem, (cudaStream_t)stream>>>(
-      (const __nv_bfloat16*)dy, (const __nv_bfloat16*)h, (const __nv_bfloat16*)w, rstd, (const __nv_bfloat16*)dres,
-      (__nv_bfloat16*)dx, dw, T, d);
-  return launch_status();
+  return rmsnorm_generic_bwd(dy, h, w, rstd, dres, dx, dw, T, d, st);
 }
 
 MAESTRO_API int maestro_rope(void* qk, const int32_t* pos, const void* cos_sin, int32_t T, int32_t n_heads,

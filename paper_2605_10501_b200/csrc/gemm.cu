@@ -284,7 +284,8 @@ struct Cfg2 {
 template <int BN2, bool A_MN, bool B_MN, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                 const __grid_constant__ CUtensorMap map_c, void* C, int M, int N, int K, int ldc, int splits) {
+                 const __grid_constant__ CUtensorMap map_c, void* C, int M, int N, int K, int ldc, int splits,
+                 const int32_t* __restrict__ rope_pos, const float2* __restrict__ rope_cs, int rope_cols) {
   using CF = Cfg2<BN2>;
   constexpr int STAGES = CF::STAGES, B_BYTES = CF::B_BYTES, STAGE_BYTES = CF::STAGE_BYTES, B_ROWS = CF::B_ROWS;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -428,6 +429,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + as * BN2 + c, r0);
           tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + as * BN2 + c + 32, r1);
           tmem_ld_wait();
+          if (rope_cols > 0 && n0 + c < rope_cols && row < M) {
+            // fused RoPE (rotate-half): this 64-column chunk is exactly one head of Q or K;
+            // r0 holds dims [0,32), r1 dims [32,64) of the row
+            const float2* csr = rope_cs + (size_t)rope_pos[row] * 32;
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+              const float2 cs = csr[k];
+              const float a = __uint_as_float(r0[k]), b = __uint_as_float(r1[k]);
+              r0[k] = __float_as_uint(a * cs.x - b * cs.y);
+              r1[k] = __float_as_uint(b * cs.x + a * cs.y);
+            }
+          }
           if (chunk_ctr >= 2) {
             if (et == 0) bulk_wait_read<1>();  // the store issued from this buffer has read it
             named_barrier_sync(1, 128);
@@ -501,12 +514,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 
 template <int BN2, bool A_MN, bool B_MN, int EPI>
 int launch2(const CUtensorMap& ma, const CUtensorMap& mbm, const CUtensorMap& mc, void* C, int M, int N, int K,
-            int ldc, int splits, cudaStream_t st) {
+            int ldc, int splits, cudaStream_t st, const int32_t* rope_pos = nullptr, const float2* rope_cs = nullptr,
+            int rope_cols = 0) {
   constexpr int SMEM = Cfg2<BN2>::SMEM;
   if (ensure_smem<gemm2_kernel<BN2, A_MN, B_MN, EPI>>(SMEM)) return launch_status();
   const int units = ((M + 255) / 256) * ((N + BN2 - 1) / BN2) * splits;
   const int pairs = units < num_sms() / 2 ? units : num_sms() / 2;
-  gemm2_kernel<BN2, A_MN, B_MN, EPI><<<2 * pairs, THREADS, SMEM, st>>>(ma, mbm, mc, C, M, N, K, ldc, splits);
+  gemm2_kernel<BN2, A_MN, B_MN, EPI><<<2 * pairs, THREADS, SMEM, st>>>(ma, mbm, mc, C, M, N, K, ldc, splits,
+                                                                        rope_pos, rope_cs, rope_cols);
   return launch_status();
 }
 
@@ -539,9 +554,28 @@ using namespace mb;
 
 // C[m, n] (+)= sum_k A(m,k) B(n,k).  A(m,k) = A[m*lda + k] (a_mn=0) or A[k*lda + m] (a_mn=1);
 // likewise B.  epi: 0 = store bf16, 1 = store fp32, 2 = accumulate into fp32 C.
+static int gemm_impl(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K, int32_t lda,
+                     int32_t ldb, int32_t ldc, int32_t a_mn, int32_t b_mn, int32_t epi, void* stream,
+                     const int32_t* rope_pos, const float2* rope_cs, int rope_cols);
+
 MAESTRO_API int maestro_gemm_bf16(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K,
                                   int32_t lda, int32_t ldb, int32_t ldc, int32_t a_mn, int32_t b_mn, int32_t epi,
                                   void* stream) {
+  return gemm_impl(A, B, C, M, N, K, lda, ldb, ldc, a_mn, b_mn, epi, stream, nullptr, nullptr, 0);
+}
+
+// Forward projection with RoPE fused into the epilogue: C = A B^T (bf16), then every
+// 64-column head in columns [0, rope_cols) is rotated (rotate-half) at position pos[row];
+// cos_sin[p][32] = (cos, sin).  Replaces the separate RoPE pass on the fused QKV output.
+MAESTRO_API int maestro_gemm_bf16_rope(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K,
+                                       int32_t lda, int32_t ldb, int32_t ldc, const int32_t* pos,
+                                       const void* cos_sin, int32_t rope_cols, void* stream) {
+  return gemm_impl(A, B, C, M, N, K, lda, ldb, ldc, 0, 0, 0, stream, pos, (const float2*)cos_sin, rope_cols);
+}
+
+static int gemm_impl(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K, int32_t lda,
+                     int32_t ldb, int32_t ldc, int32_t a_mn, int32_t b_mn, int32_t epi, void* stream,
+                     const int32_t* rope_pos, const float2* rope_cs, int rope_cols) {
   if (M <= 0 || N <= 0 || K <= 0) return (int)cudaErrorInvalidValue;
   if ((lda % 8) || (ldb % 8) || (N % 8) || (ldc % 8)) return (int)cudaErrorInvalidValue;
   const int sms = num_sms();
@@ -574,8 +608,10 @@ MAESTRO_API int maestro_gemm_bf16(const void* A, const void* B, void* C, int32_t
     if (!ok) return (int)cudaErrorInvalidValue;
 #define MB_GEMM2_CASE(AM, BMN, E)                                                                  \
   if (a_mn == AM && b_mn == BMN && epi_k == E)                                                     \
-    return bn2 == 256 ? launch2<256, AM, BMN, E>(ma, mbm, mc, C, M, N, K, ldc, splits, st)         \
-                      : launch2<128, AM, BMN, E>(ma, mbm, mc, C, M, N, K, ldc, splits, st);
+    return bn2 == 256 ? launch2<256, AM, BMN, E>(ma, mbm, mc, C, M, N, K, ldc, splits, st, rope_pos, rope_cs,  \
+                                                 rope_cols)                                                     \
+                      : launch2<128, AM, BMN, E>(ma, mbm, mc, C, M, N, K, ldc, splits, st, rope_pos, rope_cs,  \
+                                                 rope_cols);
     MB_GEMM2_CASE(0, 0, 0)
     MB_GEMM2_CASE(0, 0, 1)
     MB_GEMM2_CASE(0, 0, 2)

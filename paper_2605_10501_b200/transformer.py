@@ -174,8 +174,8 @@ class Transformer:
             y1 = torch.empty(T, s.d, device=dev, dtype=bf)
             r1 = torch.empty(T, device=dev, dtype=torch.float32)
             K.add_rmsnorm(x, a, h1, y1, p[f"l{i}.ln1"], r1, s.eps)
-            qkv = D.linear_fwd(y1, p[f"l{i}.wqkv"])
-            K.rope(qkv[:, : (H + Hk) * dh], b.pos, self.cs, H + Hk, dh)
+            # QKV projection with RoPE fused into the GEMM epilogue (one head per 64-col chunk)
+            qkv = D.linear_fwd_rope(y1, p[f"l{i}.wqkv"], b.pos, self.cs, (H + Hk) * dh)
             q = qkv[:, : H * dh].view(T, H, dh)
             k = qkv[:, H * dh: (H + Hk) * dh].view(T, Hk, dh)
             v = qkv[:, (H + Hk) * dh:].view(T, Hk, dh)
@@ -241,8 +241,9 @@ class Transformer:
             dq = dqkv[:, : H * dh].view(T, H, dh)
             dk = dqkv[:, H * dh: (H + Hk) * dh].view(T, Hk, dh)
             dv = dqkv[:, (H + Hk) * dh:].view(T, Hk, dh)
-            A.attn_bwd(do.view(T, H, dh), q, k, v, o, lse, b.cu, b.max_len, s.causal, dq, dk, dv, self.scale)
-            K.rope(dqkv[:, : (H + Hk) * dh], b.pos, self.cs, H + Hk, dh, backward=True)
+            # inverse RoPE fused into the attention backward's dQ / dK stores
+            A.attn_bwd(do.view(T, H, dh), q, k, v, o, lse, b.cu, b.max_len, s.causal, dq, dk, dv, self.scale,
+                       rope=(b.pos, self.cs))
             D.linear_wgrad(dqkv, y1, p.g(f"l{i}.wqkv"))
             dy1 = D.linear_dgrad(dqkv, p[f"l{i}.wqkv"])
             dh1 = torch.empty(T, s.d, device=dev, dtype=bf)

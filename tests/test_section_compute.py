@@ -186,3 +186,28 @@ def test_kd_executor_step_matches_reference():
     for name in ("embed", "lnf", "l0.wqkv", "l1.wd"):
         assert rel(got[name], want[name]) < 6e-2, name
     assert 0.0 <= st.stall_frac <= 1.0
+
+
+@pytest.mark.parametrize("d", [192, 768, 2048, 4096])
+def test_rmsnorm_all_widths(d):
+    """Register-resident fast path (multiples of 256) and the generic path agree with fp32."""
+    from paper_2605_10501_b200 import kernels as K
+
+    torch.manual_seed(d)
+    T = 333
+    x = torch.randn(T, d, device="cuda").bfloat16()
+    a = torch.randn(T, d, device="cuda").bfloat16()
+    w = (1 + 0.1 * torch.randn(d, device="cuda")).bfloat16()
+    h, y = torch.empty_like(x), torch.empty_like(x)
+    r = torch.empty(T, device="cuda")
+    K.add_rmsnorm(x, a, h, y, w, r, 1e-5)
+    href = (x.float() + a.float()).bfloat16().float()
+    assert torch.equal(h, href.bfloat16())
+    assert rel(y, R.rms_norm(href, w.float(), 1e-5)) < 1e-2
+    hh = href.clone().requires_grad_(True)
+    ww = w.float().clone().requires_grad_(True)
+    dy = torch.randn(T, d, device="cuda").bfloat16()
+    R.rms_norm(hh, ww, 1e-5).backward(dy.float())
+    dx, dw = torch.empty_like(x), torch.zeros(d, device="cuda")
+    K.rmsnorm_bwd(dy, h, w, r, None, dx, dw)
+    assert rel(dx, hh.grad) < 1e-2 and rel(dw, ww.grad) < 1e-3
