@@ -157,6 +157,11 @@ int maestro_gemm_bf16_rope(const void* A, const void* B, void* C, int32_t M, int
                            int32_t ldb, int32_t ldc, const int32_t* pos, const void* cos_sin, int32_t rope_cols,
                            void* stream);
 
+/* K7 + fused SwiGLU epilogue: C = A B^T is the gate/up activation with gate/up rows of B
+ * interleaved in 32-row blocks ([g_0..g_31, u_0..u_31, g_32..]); S[m, f] = silu(g_f) * u_f. */
+int maestro_gemm_bf16_swiglu(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K, int32_t lda,
+                             int32_t ldb, int32_t ldc, void* S, int32_t lds, void* stream);
+
 /* K8 -- varlen GQA attention, head_dim 64: q [T,H,64], k/v [T,Hk,64] (pitched), cu [nseq+1];
  * out [T,H,64] bf16, lse [H,T] fp32 (natural LSE of the scaled scores). */
 int64_t maestro_attn_workspace(int32_t T, int32_t nseq);
@@ -189,6 +194,7 @@ int maestro_rmsnorm_bwd(const void* dy, const void* h, const void* w, const floa
 int maestro_rope(void* qk, const int32_t* pos, const void* cos_sin, int32_t T, int32_t n_heads, int32_t dh,
                  int32_t ld, int32_t backward, void* stream);
 int maestro_positions(const int32_t* cu, int32_t nseq, int32_t* pos, void* stream);
+/* gu layout: gate/up interleaved in 32-column blocks (see maestro_gemm_bf16_swiglu) */
 int maestro_swiglu_fwd(const void* gu, void* out, int32_t T, int32_t F, void* stream);
 int maestro_swiglu_bwd(const void* dout, const void* gu, void* dgu, int32_t T, int32_t F, void* stream);
 int maestro_embed_fwd(const void* table, const int32_t* ids, void* out, int32_t T, int32_t d, void* stream);

@@ -82,9 +82,15 @@ def forward(shape, P, ids, cu, x0=None):
         x = x + o.reshape(T, H * dh) @ P[f"l{i}.wo"].t()
         y = rms_norm(x, P[f"l{i}.ln2"], shape.eps)
         gu = y @ P[f"l{i}.wgu"].t()
-        g, u = gu[:, : shape.ffn], gu[:, shape.ffn:]
+        g, u = gu[:, gate_index(shape.ffn, gu.device)], gu[:, gate_index(shape.ffn, gu.device) + 32]
         x = x + (F.silu(g) * u) @ P[f"l{i}.wd"].t()
     return rms_norm(x, P["lnf"], shape.eps)
+
+
+def gate_index(F, device):
+    """Columns of the gate features in the interleaved [g(32) | u(32)] gate/up layout."""
+    f = torch.arange(F, device=device)
+    return (f // 32) * 64 + f % 32
 
 
 def head_weight(shape, P):

@@ -269,16 +269,20 @@ __global__ void positions_kernel(const int32_t* __restrict__ cu, int nseq, int32
 }
 
 // ---------------------------------------------------------------- SwiGLU
-// gu: [T, 2F] = [gate | up]; out[T, F] = silu(gate) * up
+// gu: [T, 2F] with gate/up interleaved in 32-column blocks: block j = [g_{32j..32j+31} |
+// u_{32j..32j+31}] (the layout the fused gate/up GEMM epilogue consumes); out[T, F] = silu(g)*u.
+__device__ __forceinline__ long long gate_col(long long f) { return (f >> 5) * 64 + (f & 31); }
+
 __global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ out, int T,
                                   int F) {
   const long long nv = (long long)T * F / 8;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nv; i += (long long)gridDim.x * blockDim.x) {
     const long long e = i * 8;
-    const long long t = e / F, c = e - t * F;
+    const long long t = e / F, f = e - t * F;
+    const __nv_bfloat16* rowp = gu + t * 2 * F + gate_col(f);
     float g[8], u[8], o[8];
-    ld8(gu + t * 2 * F + c, g);
-    ld8(gu + t * 2 * F + F + c, u);
+    ld8(rowp, g);
+    ld8(rowp + 32, u);
 #pragma unroll
     for (int j = 0; j < 8; ++j) o[j] = g[j] / (1.f + __expf(-g[j])) * u[j];
     st8(out + e, o);
@@ -290,19 +294,20 @@ __global__ void swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ dout, const 
   const long long nv = (long long)T * F / 8;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nv; i += (long long)gridDim.x * blockDim.x) {
     const long long e = i * 8;
-    const long long t = e / F, c = e - t * F;
+    const long long t = e / F, f = e - t * F;
+    const long long gc = t * 2 * F + gate_col(f);
     float d[8], g[8], u[8], dg[8], du[8];
     ld8(dout + e, d);
-    ld8(gu + t * 2 * F + c, g);
-    ld8(gu + t * 2 * F + F + c, u);
+    ld8(gu + gc, g);
+    ld8(gu + gc + 32, u);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const float sg = 1.f / (1.f + __expf(-g[j]));
       du[j] = d[j] * g[j] * sg;
       dg[j] = d[j] * u[j] * sg * (1.f + g[j] * (1.f - sg));
     }
-    st8(dgu + t * 2 * F + c, dg);
-    st8(dgu + t * 2 * F + F + c, du);
+    st8(dgu + gc, dg);
+    st8(dgu + gc + 32, du);
   }
 }
 
@@ -466,7 +471,7 @@ MAESTRO_API int maestro_positions(const int32_t* cu, int32_t nseq, int32_t* pos,
 
 MAESTRO_API int maestro_swiglu_fwd(const void* gu, void* out, int32_t T, int32_t F, void* stream) {
   if (T <= 0) return 0;
-  if (F % 8) return (int)cudaErrorInvalidValue;
+  if (F % 32) return (int)cudaErrorInvalidValue;
   swiglu_fwd_kernel<<<grid_for((long long)T * F / 8, 256), 256, 0, (cudaStream_t)stream>>>(
       (const __nv_bfloat16*)gu, (__nv_bfloat16*)out, T, F);
   return launch_status();
@@ -474,7 +479,7 @@ MAESTRO_API int maestro_swiglu_fwd(const void* gu, void* out, int32_t T, int32_t
 
 MAESTRO_API int maestro_swiglu_bwd(const void* dout, const void* gu, void* dgu, int32_t T, int32_t F, void* stream) {
   if (T <= 0) return 0;
-  if (F % 8) return (int)cudaErrorInvalidValue;
+  if (F % 32) return (int)cudaErrorInvalidValue;
   swiglu_bwd_kernel<<<grid_for((long long)T * F / 8, 256), 256, 0, (cudaStream_t)stream>>>(
       (const __nv_bfloat16*)dout, (const __nv_bfloat16*)gu, (__nv_bfloat16*)dgu, T, F);
   return launch_status();

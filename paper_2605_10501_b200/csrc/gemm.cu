@@ -285,7 +285,8 @@ template <int BN2, bool A_MN, bool B_MN, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                  const __grid_constant__ CUtensorMap map_c, void* C, int M, int N, int K, int ldc, int splits,
-                 const int32_t* __restrict__ rope_pos, const float2* __restrict__ rope_cs, int rope_cols) {
+                 const int32_t* __restrict__ rope_pos, const float2* __restrict__ rope_cs, int rope_cols,
+                 __nv_bfloat16* __restrict__ swiglu_out, int ld_swiglu) {
   using CF = Cfg2<BN2>;
   constexpr int STAGES = CF::STAGES, B_BYTES = CF::B_BYTES, STAGE_BYTES = CF::STAGE_BYTES, B_ROWS = CF::B_ROWS;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -441,6 +442,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               r1[k] = __float_as_uint(b * cs.x + a * cs.y);
             }
           }
+          if (swiglu_out != nullptr && row < M && n0 + c < N) {
+            // fused SwiGLU: gate/up rows are interleaved in 32-row blocks, so this chunk holds
+            // gate (r0) and up (r1) of the same 32 features: s = silu(g) * u
+            uint32_t sv[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+              const float g0 = __uint_as_float(r0[2 * k]), g1 = __uint_as_float(r0[2 * k + 1]);
+              const float u0 = __uint_as_float(r1[2 * k]), u1 = __uint_as_float(r1[2 * k + 1]);
+              sv[k] = pack_bf16(g0 / (1.f + __expf(-g0)) * u0, g1 / (1.f + __expf(-g1)) * u1);
+            }
+            uint4* dst = reinterpret_cast<uint4*>(swiglu_out + (size_t)row * ld_swiglu + (n0 + c) / 2);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) dst[k] = make_uint4(sv[4 * k], sv[4 * k + 1], sv[4 * k + 2], sv[4 * k + 3]);
+          }
           if (chunk_ctr >= 2) {
             if (et == 0) bulk_wait_read<1>();  // the store issued from this buffer has read it
             named_barrier_sync(1, 128);
@@ -515,13 +530,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 template <int BN2, bool A_MN, bool B_MN, int EPI>
 int launch2(const CUtensorMap& ma, const CUtensorMap& mbm, const CUtensorMap& mc, void* C, int M, int N, int K,
             int ldc, int splits, cudaStream_t st, const int32_t* rope_pos = nullptr, const float2* rope_cs = nullptr,
-            int rope_cols = 0) {
+            int rope_cols = 0, __nv_bfloat16* swiglu_out = nullptr, int ld_swiglu = 0) {
   constexpr int SMEM = Cfg2<BN2>::SMEM;
   if (ensure_smem<gemm2_kernel<BN2, A_MN, B_MN, EPI>>(SMEM)) return launch_status();
   const int units = ((M + 255) / 256) * ((N + BN2 - 1) / BN2) * splits;
   const int pairs = units < num_sms() / 2 ? units : num_sms() / 2;
   gemm2_kernel<BN2, A_MN, B_MN, EPI><<<2 * pairs, THREADS, SMEM, st>>>(ma, mbm, mc, C, M, N, K, ldc, splits,
-                                                                        rope_pos, rope_cs, rope_cols);
+                                                                        rope_pos, rope_cs, rope_cols, swiglu_out,
+                                                                        ld_swiglu);
   return launch_status();
 }
 
@@ -556,7 +572,8 @@ using namespace mb;
 // likewise B.  epi: 0 = store bf16, 1 = store fp32, 2 = accumulate into fp32 C.
 static int gemm_impl(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K, int32_t lda,
                      int32_t ldb, int32_t ldc, int32_t a_mn, int32_t b_mn, int32_t epi, void* stream,
-                     const int32_t* rope_pos, const float2* rope_cs, int rope_cols);
+                     const int32_t* rope_pos, const float2* rope_cs, int rope_cols, void* swiglu_out = nullptr,
+                     int ld_swiglu = 0);
 
 MAESTRO_API int maestro_gemm_bf16(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K,
                                   int32_t lda, int32_t ldb, int32_t ldc, int32_t a_mn, int32_t b_mn, int32_t epi,
@@ -573,9 +590,18 @@ MAESTRO_API int maestro_gemm_bf16_rope(const void* A, const void* B, void* C, in
   return gemm_impl(A, B, C, M, N, K, lda, ldb, ldc, 0, 0, 0, stream, pos, (const float2*)cos_sin, rope_cols);
 }
 
+// Gate/up projection with SwiGLU fused into the epilogue: C = A B^T is the interleaved [g|u]
+// activation (gate/up rows of B interleaved in 32-row blocks), S[m, f] = silu(g) * u.
+MAESTRO_API int maestro_gemm_bf16_swiglu(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K,
+                                         int32_t lda, int32_t ldb, int32_t ldc, void* S, int32_t lds, void* stream) {
+  if (N % 64) return (int)cudaErrorInvalidValue;
+  return gemm_impl(A, B, C, M, N, K, lda, ldb, ldc, 0, 0, 0, stream, nullptr, nullptr, 0, S, lds);
+}
+
 static int gemm_impl(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K, int32_t lda,
                      int32_t ldb, int32_t ldc, int32_t a_mn, int32_t b_mn, int32_t epi, void* stream,
-                     const int32_t* rope_pos, const float2* rope_cs, int rope_cols) {
+                     const int32_t* rope_pos, const float2* rope_cs, int rope_cols, void* swiglu_out,
+                     int ld_swiglu) {
   if (M <= 0 || N <= 0 || K <= 0) return (int)cudaErrorInvalidValue;
   if ((lda % 8) || (ldb % 8) || (N % 8) || (ldc % 8)) return (int)cudaErrorInvalidValue;
   const int sms = num_sms();
@@ -609,9 +635,9 @@ static int gemm_impl(const void* A, const void* B, void* C, int32_t M, int32_t N
 #define MB_GEMM2_CASE(AM, BMN, E)                                                                  \
   if (a_mn == AM && b_mn == BMN && epi_k == E)                                                     \
     return bn2 == 256 ? launch2<256, AM, BMN, E>(ma, mbm, mc, C, M, N, K, ldc, splits, st, rope_pos, rope_cs,  \
-                                                 rope_cols)                                                     \
+                                                 rope_cols, (__nv_bfloat16*)swiglu_out, ld_swiglu)              \
                       : launch2<128, AM, BMN, E>(ma, mbm, mc, C, M, N, K, ldc, splits, st, rope_pos, rope_cs,  \
-                                                 rope_cols);
+                                                 rope_cols, (__nv_bfloat16*)swiglu_out, ld_swiglu);
     MB_GEMM2_CASE(0, 0, 0)
     MB_GEMM2_CASE(0, 0, 1)
     MB_GEMM2_CASE(0, 0, 2)

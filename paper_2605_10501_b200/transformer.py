@@ -6,6 +6,8 @@ GEMM (dense.py), the attention kernels (attention.py) or the memory-bound kernel
 
 A block is   h1 = x + a ; y1 = rmsnorm(h1) ; qkv = y1 Wqkv^T ; rope ; o = attn(qkv)
              h2 = h1 + o Wo^T ; y2 = rmsnorm(h2) ; gu = y2 Wgu^T ; s = silu(g) u ; a' = s Wd^T
+(Wgu stores gate/up rows interleaved in 32-row blocks so SwiGLU runs in the GEMM epilogue;
+RoPE likewise runs in the QKV GEMM epilogue.)
 with the residual add fused into the following norm.  Parameters of a section live in one
 flat arena (fp32 master, bf16 working copy, fp32 grad, Adam m/v) so the optimizer and the
 gradient all-reduce are single launches over contiguous memory.
@@ -186,9 +188,10 @@ class Transformer:
             y2 = torch.empty(T, s.d, device=dev, dtype=bf)
             r2 = torch.empty(T, device=dev, dtype=torch.float32)
             K.add_rmsnorm(h1, ao, h2, y2, p[f"l{i}.ln2"], r2, s.eps)
-            gu = D.linear_fwd(y2, p[f"l{i}.wgu"])
+            # gate/up projection with SwiGLU fused into the epilogue (gate/up rows interleaved
+            # in 32-row blocks in wgu)
             sw = torch.empty(T, s.ffn, device=dev, dtype=bf)
-            K.swiglu(gu, sw)
+            gu = D.linear_fwd_swiglu(y2, p[f"l{i}.wgu"], sw)
             mo = D.linear_fwd(sw, p[f"l{i}.wd"])
             if save:
                 ctx["layers"].append((h1, r1, y1, qkv, o, lse, h2, r2, y2, gu, sw))

@@ -89,3 +89,30 @@ def test_training_shapes_all_paths(M, N, K):
     ref = dw + dy.float().t() @ x.float()
     dense.linear_wgrad(dy, x, dw)
     assert _rel(dw, ref) < 1e-4
+
+
+def test_fused_epilogues_rope_swiglu():
+    """RoPE and SwiGLU fused into the 2-CTA GEMM epilogue == unfused fp32 formulas."""
+    from oracle import torch_ref as R
+    from paper_2605_10501_b200 import dense
+    from paper_2605_10501_b200.transformer import rope_table
+
+    torch.manual_seed(11)
+    T, K, H = 1000, 512, 6
+    x = torch.randn(T, K, device="cuda").bfloat16()
+    w = torch.randn(H * 64 + 128, K, device="cuda").bfloat16()  # 6 rotated heads + 2 plain
+    pos = torch.randint(0, 1024, (T,), device="cuda", dtype=torch.int32)
+    cs = rope_table(1024, 64, 10000.0, "cuda")
+    y = dense.linear_fwd_rope(x, w, pos, cs, H * 64)
+    ref = x.float() @ w.float().t()
+    rot = R.rope(ref[:, : H * 64].view(T, H, 64), pos, 10000.0).view(T, H * 64)
+    assert _rel(y[:, : H * 64], rot) < 1e-2 and _rel(y[:, H * 64:], ref[:, H * 64:]) < 8e-3
+    F = 384
+    wgu = torch.randn(2 * F, K, device="cuda").bfloat16()
+    s = torch.empty(T, F, device="cuda", dtype=torch.bfloat16)
+    gu = dense.linear_fwd_swiglu(x, wgu, s)
+    gref = x.float() @ wgu.float().t()
+    assert _rel(gu, gref) < 8e-3
+    gi = R.gate_index(F, "cuda")
+    sref = torch.nn.functional.silu(gref[:, gi]) * gref[:, gi + 32]
+    assert _rel(s, sref) < 2e-2

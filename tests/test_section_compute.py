@@ -56,14 +56,15 @@ def test_swiglu_rope_embed():
     gu = torch.randn(T, 2 * F, device="cuda").bfloat16()
     out = torch.empty(T, F, device="cuda", dtype=torch.bfloat16)
     K.swiglu(gu, out)
-    g, u = gu.float()[:, :F].requires_grad_(True), gu.float()[:, F:].requires_grad_(True)
+    gi = R.gate_index(F, "cuda")  # interleaved [g(32) | u(32)] blocks
+    g, u = gu.float()[:, gi].requires_grad_(True), gu.float()[:, gi + 32].requires_grad_(True)
     ref = torch.nn.functional.silu(g) * u
     assert rel(out, ref) < 1e-2
     dout = torch.randn(T, F, device="cuda").bfloat16()
     ref.backward(dout.float())
     dgu = torch.empty_like(gu)
     K.swiglu_bwd(dout, gu, dgu)
-    assert rel(dgu[:, :F], g.grad) < 2e-2 and rel(dgu[:, F:], u.grad) < 2e-2
+    assert rel(dgu[:, gi], g.grad) < 2e-2 and rel(dgu[:, gi + 32], u.grad) < 2e-2
     # RoPE fwd then bwd is the identity (orthogonal rotation), and matches the fp32 formula
     H, dh = 6, 64
     x = torch.randn(T, H * dh + 32, device="cuda").bfloat16()  # row pitch > H*dh
