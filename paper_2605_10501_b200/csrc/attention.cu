@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
 //   dV += P^T dO, dK += dS^T Q                      (TMEM accumulators across all tiles)
 //   dQ_tile = dS K                                  (TMEM, drained with red.global.add.v4.f32)
 // TMEM: S^T [0,128), dP^T [128,256), dV [256,320), dK [320,384), dQ [384,448).
-constexpr int BWD_THREADS = 192;
+constexpr int BWD_THREADS = 320;  // w0 TMA, w1 MMA, w2-5 softmax, w6-9 dQ drain
 
 struct BwdSmem {
   static constexpr int K = 0;
@@ -456,9 +456,38 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       }
       umma_commit(dkv_full);
     }
+  } else if (warp >= 6) {
+    // ---------------- dQ drain: TMEM -> fp32 reductions into dq_acc, overlapping the softmax
+    // warps' next tile (they no longer wait on these ~2k vector reductions per tile)
+    const int q4 = warp & 3;
+    const int r = q4 * 32 + lane;  // query row of the dQ tile
+    const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
+    for (int it = 0; it < n_it; ++it) {
+      const int g = it / n_q, qt = qt_first + it % n_q;
+      const int h = hk * G + g;
+      const int qrow = qt * BQ + r;
+      mbar_wait(dq_full, it & 1);
+      tc_fence_after();
+      uint32_t qa[32], qb[32];
+      tmem_ld_32x32b_x32(tmem + lane_base + T_DQ, qa);
+      tmem_ld_32x32b_x32(tmem + lane_base + T_DQ + 32, qb);
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(dq_empty);  // TMEM free as soon as it is in registers
+      if (qrow < L) {
+        float* dst_row = dq_acc + ((size_t)(s0 + qrow) * H + h) * DH;
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          red_add_v4(dst_row + j, __uint_as_float(qa[j]), __uint_as_float(qa[j + 1]), __uint_as_float(qa[j + 2]),
+                     __uint_as_float(qa[j + 3]));
+          red_add_v4(dst_row + 32 + j, __uint_as_float(qb[j]), __uint_as_float(qb[j + 1]),
+                     __uint_as_float(qb[j + 2]), __uint_as_float(qb[j + 3]));
+        }
+      }
+    }
   } else {
     const int q4 = warp & 3;
-    const int r = q4 * 32 + lane;  // kv row (S^T, dP^T, dK, dV) and q row (dQ)
+    const int r = q4 * 32 + lane;  // kv row (S^T, dP^T, dK, dV)
     const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
     const int kvpos = kv0 + r;
     const int tid = threadIdx.x - 64;
@@ -519,25 +548,6 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       mbar_arrive(sp_empty);
       fence_proxy_async_smem();
       mbar_arrive(ds_full);
-      // drain this tile's dQ (overlaps the next tile's S^T / dP^T MMAs)
-      mbar_wait(dq_full, it & 1);
-      tc_fence_after();
-      const int qrow = q0 + r;
-#pragma unroll
-      for (int c0 = 0; c0 < DH; c0 += 32) {
-        uint32_t qr[32];
-        tmem_ld_32x32b_x32(tmem + lane_base + T_DQ + c0, qr);
-        tmem_ld_wait();
-        if (qrow < L) {
-          float* dst_row = dq_acc + ((size_t)(s0 + qrow) * H + h) * DH + c0;
-#pragma unroll
-          for (int j = 0; j < 32; j += 4)
-            red_add_v4(dst_row + j, __uint_as_float(qr[j]), __uint_as_float(qr[j + 1]), __uint_as_float(qr[j + 2]),
-                       __uint_as_float(qr[j + 3]));
-        }
-      }
-      tc_fence_before();
-      mbar_arrive(dq_empty);
     }
     // dK (scaled), dV -> bf16
     mbar_wait(dkv_full, 0);
