@@ -208,6 +208,7 @@ def main():
     ap.add_argument("--batch-per-rank", type=int, default=BATCH_PER_RANK)
     ap.add_argument("--mbs", type=int, default=MBS)
     ap.add_argument("--layout", default="colocated", choices=["colocated", "disjoint"])
+    ap.add_argument("--trace", default=None, help="write the measured chrome trace of the last step here")
     ap.add_argument("--workload", default="kd", choices=["kd", "vlm"],
                     help="kd = BASELINE configs[1] (default); vlm = configs[0] tiny VLM, 1 GPU")
     args = ap.parse_args()
@@ -317,6 +318,18 @@ def main():
                              "(teacher fwd + colocated head, student fwd/bwd, KL, AdamW)"}
         except Exception as exc:  # noqa: BLE001
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {exc}"}
+    xcheck = None
+    if ex.colocated or ex.student is not None:
+        try:
+            mk, cidle, span, midle = ex.crosscheck()
+            xcheck = {"model_makespan_ms": mk * 1e3, "model_critical_idle_ms": cidle * 1e3,
+                      "measured_critical_span_ms": span * 1e3, "measured_critical_idle_ms": midle * 1e3}
+        except Exception as exc:  # noqa: BLE001
+            xcheck = {"error": repr(exc)}
+    if args.trace and rank == 0:
+        from paper_2605_10501_b200.simulator import export_trace
+
+        export_trace(ex.measured_events(), args.trace)
     if rank == 0:
         dp_s, dp_t = ex.dp_s, ex.dp_t
         line = {
@@ -342,6 +355,7 @@ def main():
                          "peak_kind": f"{peak_kind} bf16_tflops_sustained",
                          "launches_timed": gemm_n, "share_of_step": gemm_ms / ms if ms > 0 else None},
             "model_tflops": ex.model_flops_per_step() * args.steps / (ms / 1e3) / 1e12,
+            "simulator_crosscheck": xcheck,
             "clocks": clk,
             "cpu_baseline": cpu,
             "loss": losses[-1] if losses else None,

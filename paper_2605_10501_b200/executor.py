@@ -234,6 +234,8 @@ class KDExecutor:
         ready = torch.cuda.Event()
         ready.record(main)
         clock = StageClock()
+        self.t_clock = StageClock()
+        self.s_clock, self.t_origin = clock, t_start
         loss_acc = None
         if self.student is not None:
             loss_acc = torch.zeros(1, device=dev, dtype=torch.float32)
@@ -280,7 +282,7 @@ class KDExecutor:
 
     def _student_mb(self, yf_t, packed, cu, start, T, loss_acc, global_tokens, clock, m):
         b = Batch(ids=packed[start: start + T], cu=cu, pos=self._positions(cu, T), max_len=self.seq)
-        clock.begin(self.s_stream, f"fwd{m}")
+        clock.begin(self.s_stream, f"f_c{m}")
         yf, ctx = self.student.forward(b)
         s_logits = self.student.logits(yf)
         t_logits = torch.empty_like(s_logits)
@@ -291,6 +293,8 @@ class KDExecutor:
         K.kd_loss(t_logits, s_logits, s_logits, tok_loss, grad_scale=1.0 / global_tokens)
         loss_acc.add_(tok_loss.sum())
         del t_logits
+        clock.end(self.s_stream)
+        clock.begin(self.s_stream, f"b_c{m}")
         self.student.backward(ctx, dlogits=s_logits)
         clock.end(self.s_stream)
 
@@ -309,7 +313,9 @@ class KDExecutor:
         with torch.cuda.stream(self.t_stream):
             for m in range(pt["n_mb"]):
                 T = ht[0][m]
+                self.t_clock.begin(self.t_stream, f"f_bc{m}")
                 yf = self._teacher_mb(packed["teacher"], self._mb_cu(pt, m, T), m, ht[1][m], T)
+                self.t_clock.end(self.t_stream)
                 e = torch.cuda.Event()
                 e.record(self.t_stream)
                 ev.append(e)
@@ -347,6 +353,45 @@ class KDExecutor:
                 dist.recv(yf_t, src)
                 self._student_mb(yf_t, packed["student"], self._mb_cu(ps, m, T), hs[1][m], T, loss_acc,
                                  global_tokens, clock, m)
+
+    # ------------------------------------------------------------------ measured timeline
+    def measured_events(self):
+        """Device stage timestamps of the last step as simulator StageEvents (sample id = micro-batch)."""
+        from .simulator import measured_events
+
+        ev = []
+        if self.teacher is not None and getattr(self, "t_clock", None) is not None:
+            ev += measured_events(self.t_clock.marks, self.t_origin, "teacher", self.t_rank, lambda n: "f_bc")
+        if self.student is not None:
+            ev += measured_events(self.s_clock.marks, self.t_origin, "student", self.s_rank,
+                                  lambda n: "f_c" if n.startswith("f_c") else "b_c")
+        return sorted(ev, key=lambda e: (e.start, e.section, e.dp_rank, e.sample_id, e.phase))
+
+    def crosscheck(self):
+        """Re-run the executor model (simulator.simulate) with the measured per-micro-batch stage
+        durations; returns (modelled makespan s, modelled critical idle s, measured span s, measured
+        critical idle s).  Co-resident sections share one GPU, so the model (one resource per
+        section) bounds what a disjoint placement of the same stages would achieve."""
+        from .scheduling import Schedule
+        from .simulator import simulate
+        from .workload import SampleTiming
+
+        ev = self.measured_events()
+        dur: dict = {}
+        for e in ev:
+            dur.setdefault(e.sample_id, {})[e.phase] = e.end - e.start
+        batch = [SampleTiming(m, t_f_bc=d.get("f_bc", 0.0), t_f_c=max(d.get("f_c", 0.0), 1e-12),
+                              t_b_c=d.get("b_c", 0.0), activated_sections=frozenset({"teacher"}))
+                 for m, d in sorted(dur.items())]
+        order = tuple(m for m, _ in sorted(dur.items()))
+        from .workload import SectionConfig
+
+        sched = Schedule(per_rank_orders={("student", 0): order, ("teacher", 0): order}, batch=tuple(batch))
+        rep, _ = simulate(self.graph, {"student": SectionConfig(), "teacher": SectionConfig()}, sched)
+        crit = [e for e in ev if e.section == "student"]
+        span = crit[-1].end - crit[0].start if crit else 0.0
+        busy = sum(e.end - e.start for e in crit)
+        return rep.makespan, rep.critical_idle, span, span - busy
 
     # ------------------------------------------------------------------ accounting
     def model_flops_per_step(self) -> float:

@@ -138,4 +138,124 @@ def kd(n_gpus: int = 1, batch: int = 64, seq: int = KD_SEQ, layout: str = "disjo
     return Recipe("kd", g, configs, params, tokens, batch, {})
 
 
-RECIPES = {"vlm_tiny": vlm_tiny, "kd": kd}
+# ----------------------------------------------------------------------------- cfg 3
+QWEN_VIT_PARAMS = 630_000_000
+QWEN_LLM_PARAMS = 7_600_000_000
+
+
+def vlm_7b_graph() -> SectionGraph:
+    vit = SectionSpec("vit", Role.AUXILIARY, ExecMode.FORWARD_BACKWARD,
+                      StructuralParams(1280, 16, 32, 1, 16384, QWEN_VIT_PARAMS))
+    llm = SectionSpec("llm", Role.CRITICAL, ExecMode.FORWARD_BACKWARD,
+                      StructuralParams(3584, 28, 28, 152064, 8192, QWEN_LLM_PARAMS))
+    return build_graph([vit, llm], [Edge("vit", "llm", 1024 * 3584 * 2.0)])
+
+
+VLM7B_LAYOUTS = {1: (1, 1, 1), 2: (1, 1, 1), 4: (3, 1, 3), 8: (7, 1, 7)}
+
+
+def vlm_7b(n_gpus: int = 8, batch: int = 64, seed: int = 0) -> Recipe:
+    """cfg 3: Qwen2.5-VL-7B-shaped VLM; 50 % images with U{256..4096} patches (2x2 merge -> /4)."""
+    from .synthetic import rand_int
+
+    g = vlm_7b_graph()
+    dp_llm, dp_vit, f_vit = VLM7B_LAYOUTS[n_gpus]
+    configs = {"llm": SectionConfig(dp=dp_llm), "vit": SectionConfig(dp=dp_vit, fanout=f_vit)}
+    params = {
+        "vit": CostParams(flops_per_token_fwd=2.0 * QWEN_VIT_PARAMS, peak_flops_per_gpu=B200_PEAK_FLOPS),
+        "llm": CostParams(flops_per_token_fwd=2.0 * QWEN_LLM_PARAMS, peak_flops_per_gpu=B200_PEAK_FLOPS),
+    }
+    b = vlm_batch(seed, batch, text_lo=256, text_hi=2048)
+    patches = rand_int(seed, 7, np.arange(batch), 256, 4096).astype(np.int32) // 4 * 4
+    vit_tokens = np.where(b["has_image"], patches, 0)
+    llm_tokens = b["text_len"] + vit_tokens // 4
+    return Recipe("vlm_7b", g, configs, params,
+                  {"llm": llm_tokens.astype(np.int32), "vit": vit_tokens.astype(np.int32)}, batch, dict(b))
+
+
+# ----------------------------------------------------------------------------- cfg 4
+def omni_graph() -> SectionGraph:
+    img = SectionSpec("image_enc", Role.AUXILIARY, ExecMode.FORWARD_BACKWARD,
+                      StructuralParams(1280, 16, 32, 1, 16384, QWEN_VIT_PARAMS))
+    aud = SectionSpec("audio_enc", Role.AUXILIARY, ExecMode.FORWARD_BACKWARD,
+                      StructuralParams(1280, 20, 32, 1, 1500, 640_000_000))
+    llm = SectionSpec("llm", Role.CRITICAL, ExecMode.FORWARD_BACKWARD,
+                      StructuralParams(3584, 28, 28, 152064, 8192, QWEN_LLM_PARAMS))
+    dec = SectionSpec("audio_dec", Role.AUXILIARY, ExecMode.FORWARD_BACKWARD,
+                      StructuralParams(1024, 16, 12, 4096, 4096, 300_000_000))
+    return build_graph([img, aud, llm, dec], [Edge("image_enc", "llm", 1024 * 3584 * 2.0),
+                                             Edge("audio_enc", "llm", 375 * 3584 * 2.0),
+                                             Edge("llm", "audio_dec", 512 * 3584 * 2.0)])
+
+
+OMNI_LAYOUTS = {1: (1, 1, 1), 2: (2, 1, 2), 4: (4, 2, 2), 8: (8, 2, 4)}
+
+
+def omni(n_gpus: int = 8, batch: int = 64, seed: int = 0, mix: str = "4way") -> Recipe:
+    """cfg 4: image + audio encoders (upstream), 7B backbone, audio decoder (downstream).
+
+    mix "4way" = text / img / audio / img+audio in equal shares.  The img+audio class activates
+    two upstream sections; the reference's 6-tuple model rejects it (ActivationError,
+    workload.py:323-328) and so does the device resolver -- that is the parity-pinned behaviour.
+    mix "3way" drops that class (text / img / audio) and schedules.  Audio samples also run the
+    downstream audio decoder on 512 generated tokens.
+    """
+    from .synthetic import permutation
+
+    g = omni_graph()
+    dp_llm, dp_enc, f_enc = OMNI_LAYOUTS[n_gpus]
+    configs = {"llm": SectionConfig(dp=dp_llm), "image_enc": SectionConfig(dp=dp_enc, fanout=f_enc),
+               "audio_enc": SectionConfig(dp=dp_enc, fanout=f_enc), "audio_dec": SectionConfig(dp=dp_llm)}
+    params = {
+        "image_enc": CostParams(flops_per_token_fwd=2.0 * QWEN_VIT_PARAMS, peak_flops_per_gpu=B200_PEAK_FLOPS),
+        "audio_enc": CostParams(flops_per_token_fwd=2.0 * 640_000_000, peak_flops_per_gpu=B200_PEAK_FLOPS),
+        "llm": CostParams(flops_per_token_fwd=2.0 * QWEN_LLM_PARAMS, peak_flops_per_gpu=B200_PEAK_FLOPS),
+        "audio_dec": CostParams(flops_per_token_fwd=2.0 * 300_000_000, peak_flops_per_gpu=B200_PEAK_FLOPS),
+    }
+    classes = 4 if mix == "4way" else 3
+    perm = permutation(seed, 9, batch)
+    cls = np.empty(batch, dtype=np.int64)
+    cls[perm] = np.arange(batch) % classes  # 0 text, 1 img, 2 audio, 3 img+audio
+    b = vlm_batch(seed, batch, text_lo=256, text_hi=2048)
+    img = (cls == 1) | (cls == 3)
+    aud = (cls == 2) | (cls == 3)
+    img_tok = np.where(img, 4096, 0)
+    aud_tok = np.where(aud, 1500, 0)
+    llm_tok = b["text_len"] + img_tok // 4 + aud_tok // 4
+    dec_tok = np.where(aud, 512, 0)
+    return Recipe("omni", g, configs, params,
+                  {"llm": llm_tok.astype(np.int32), "image_enc": img_tok.astype(np.int32),
+                   "audio_enc": aud_tok.astype(np.int32), "audio_dec": dec_tok.astype(np.int32)},
+                  batch, {"class": cls})
+
+
+# ----------------------------------------------------------------------------- cfg 5
+def kd_8b_graph() -> SectionGraph:
+    teacher = SectionSpec("teacher", Role.AUXILIARY, ExecMode.FORWARD_ONLY,
+                          StructuralParams(4096, 32, 32, 128256, 8192, 8_000_000_000),
+                          submodules=("teacher", "output_layer"))
+    student = SectionSpec("student", Role.CRITICAL, ExecMode.FORWARD_BACKWARD,
+                          StructuralParams(2048, 32, 16, 128256, 8192, 1_240_000_000))
+    g = build_graph([teacher, student], [Edge("teacher", "student", 8192 * 128256 * 2.0)])
+    return colocate_output_layer(g, "teacher", "student", 4096, 128256)
+
+
+KD8B_LAYOUTS = {1: (1, 1, 1), 2: (1, 1, 1), 4: (2, 2, 1), 8: (4, 4, 1)}
+
+
+def kd_8b(n_gpus: int = 8, batch: int = 32, seq: int = 8192) -> Recipe:
+    """cfg 5: Llama-3-8B teacher -> Llama-3.2-1B student, 8k seq, disjoint GPU groups."""
+    g = kd_8b_graph()
+    dp_s, dp_t, f_t = KD8B_LAYOUTS[n_gpus]
+    configs = {"student": SectionConfig(dp=dp_s), "teacher": SectionConfig(dp=dp_t, fanout=f_t)}
+    params = {
+        "teacher": CostParams(flops_per_token_fwd=2.0 * 7.5e9 + 4 * 32 * 4096 * seq / 2,
+                              peak_flops_per_gpu=B200_PEAK_FLOPS),
+        "student": CostParams(flops_per_token_fwd=2.0 * (0.97e9 + 4096 * 128256) + 4 * 16 * 2048 * seq / 2,
+                              peak_flops_per_gpu=B200_PEAK_FLOPS),
+    }
+    tokens = {"student": np.full(batch, seq, np.int32), "teacher": np.full(batch, seq, np.int32)}
+    return Recipe("kd_8b", g, configs, params, tokens, batch, {})
+
+
+RECIPES = {"vlm_tiny": vlm_tiny, "kd": kd, "vlm_7b": vlm_7b, "omni": omni, "kd_8b": kd_8b}

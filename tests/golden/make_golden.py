@@ -326,6 +326,13 @@ def main():
                              rs.ExecPolicy.ALL_FWD_THEN_BWD, with_sim=False))
     for n in (1, 4, 8):
         cases.append(recipe_case(recipes.kd(n, 32), f"recipe:kd:{n}gpu:B32"))
+    for n in (1, 4, 8):  # cfg 3 Qwen2.5-VL-7B shape
+        cases.append(recipe_case(recipes.vlm_7b(n, 64), f"recipe:vlm_7b:{n}gpu:B64", with_sim=n > 1))
+    for n in (2, 8):  # cfg 4 omni, 3-way mix schedules; 4-way (img+audio) is rejected by the reference
+        cases.append(recipe_case(recipes.omni(n, 48, mix="3way"), f"recipe:omni3:{n}gpu:B48"))
+    cases.append(recipe_case(recipes.omni(8, 48, mix="4way"), "recipe:omni4:8gpu:B48"))
+    for n in (4, 8):  # cfg 5 Llama-3-8B -> 3.2-1B
+        cases.append(recipe_case(recipes.kd_8b(n, 32), f"recipe:kd_8b:{n}gpu:B32"))
     # --- evaluation-count bound ---------------------------------------------
     evals = {}
     g = g3()

@@ -212,3 +212,19 @@ def test_rmsnorm_all_widths(d):
     dx, dw = torch.empty_like(x), torch.zeros(d, device="cuda")
     K.rmsnorm_bwd(dy, h, w, r, None, dx, dw)
     assert rel(dx, hh.grad) < 1e-2 and rel(dw, ww.grad) < 1e-3
+
+
+def test_measured_trace_and_model_crosscheck(tmp_path):
+    """Device stage timestamps -> simulator StageEvents -> chrome trace; model re-run."""
+    from paper_2605_10501_b200.executor import KDExecutor, synthetic_ids
+    from paper_2605_10501_b200.simulator import export_trace
+
+    ex = KDExecutor(n_gpus=1, batch_per_rank=8, seq=128, mbs=2, teacher="test_tiny", student="test_tiny")
+    ids = torch.from_numpy(synthetic_ids(8, 128, 512, seed=6)).cuda()
+    ex.step(ids)
+    ev = ex.measured_events()
+    assert {e.phase for e in ev} == {"f_bc", "f_c", "b_c"} and len(ev) == 3 * 4
+    assert all(e.end >= e.start >= 0 for e in ev)
+    export_trace(ev, str(tmp_path / "trace.json"))
+    mk, cidle, span, midle = ex.crosscheck()
+    assert mk > 0 and cidle >= 0 and span > 0 and midle >= -1e-9
