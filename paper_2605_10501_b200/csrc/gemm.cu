@@ -618,7 +618,7 @@ static int gemm_impl(const void* A, const void* B, void* C, int32_t M, int32_t N
     const int kb = (K + BK - 1) / BK;
     if (epi == EPI_F32_ACC && t256 < pairs && kb >= 8) {
       bn2 = 256;
-      int sp = (int)((2 * pairs + t256 - 1) / t256);
+      int sp = (int)((pairs + t256 - 1) / t256);  // one wave of pairs: atomics, not MMAs, dominate beyond
       sp = sp < kb / 4 ? sp : kb / 4;
       sp = sp < 1 ? 1 : sp;
       const int per = (kb + sp - 1) / sp;
