@@ -204,13 +204,15 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       mbar_wait(&s_full[b], (i >> 1) & 1);
       tc_fence_after();
       float s[BKV];
+      {
+        uint32_t raw[BKV / 32][32];  // all four TMEM loads in flight, one wait
 #pragma unroll
-      for (int c = 0; c < BKV / 32; ++c) {
-        uint32_t rr[32];
-        tmem_ld_32x32b_x32(tmem + lane_base + b * BKV + c * 32, rr);
+        for (int c = 0; c < BKV / 32; ++c) tmem_ld_32x32b_x32(tmem + lane_base + b * BKV + c * 32, raw[c]);
         tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) s[c * 32 + j] = __uint_as_float(rr[j]);
+        for (int c = 0; c < BKV / 32; ++c)
+#pragma unroll
+          for (int j = 0; j < 32; ++j) s[c * 32 + j] = __uint_as_float(raw[c][j]);
       }
       tc_fence_before();
       mbar_arrive(&s_empty[b]);
