@@ -15,6 +15,7 @@
 //
 // Warp roles (192 threads): w0 TMA producer, w1 MMA issuer + TMEM owner, w2..w5 epilogue.
 #include <cuda_bf16.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "common.cuh"
@@ -613,15 +614,28 @@ static int gemm_impl(const void* A, const void* B, void* C, int32_t M, int32_t N
     const long long tm = (M + 255) / 256;
     const long long t256 = tm * ((N + 255) / 256), t128 = tm * ((N + 127) / 128);
     const long long c256 = (t256 + pairs - 1) / pairs * 2, c128 = (t128 + pairs - 1) / pairs;
-    int bn2 = 4 * c128 < 3 * c256 ? 128 : 256;
+    // per-pair work: ceil(tiles / pairs) * tile cost; a 256x128 tile costs ~0.6 of a 256x256 tile
+    // (measured on the step shapes: more operand traffic and epilogue per FLOP), not 0.5
+    // (c256 counts 256-wide tiles twice); only short-K, epilogue-bound shapes gain from 128
+    int bn2 = (K <= 1024 && 6 * c128 < 5 * c256) ? 128 : 256;
+    if (const char* e = getenv("MAESTRO_GEMM_BN")) bn2 = atoi(e) == 128 ? 128 : 256;  // experiments
     int splits = 1;
     const int kb = (K + BK - 1) / BK;
     if (epi == EPI_F32_ACC && t256 < pairs && kb >= 8) {
+      // split K to fill the pairs; per-pair cost = ceil(tiles*s/pairs) * (k-blocks per slice +
+      // epilogue), where a split slice's epilogue (a 256x256 fp32 tile of red.global.add) costs
+      // ~4 k-blocks of MMA and the unsplit read-modify-write ~1
       bn2 = 256;
-      int sp = (int)((pairs + t256 - 1) / t256);  // one wave of pairs: atomics, not MMAs, dominate beyond
-      sp = sp < kb / 4 ? sp : kb / 4;
-      sp = sp < 1 ? 1 : sp;
-      const int per = (kb + sp - 1) / sp;
+      long long best = -1;
+      for (int sp = 1; sp <= kb / 2; ++sp) {
+        const long long waves = (t256 * sp + pairs - 1) / pairs;
+        const long long cost = waves * ((kb + sp - 1) / sp + (sp > 1 ? 4 : 1));
+        if (best < 0 || cost < best) {
+          best = cost;
+          splits = sp;
+        }
+      }
+      const int per = (kb + splits - 1) / splits;
       splits = (kb + per - 1) / per;
     }
     const int epi_k = splits > 1 ? EPI_F32_ATOMIC : epi;

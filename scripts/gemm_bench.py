@@ -24,8 +24,14 @@ def timeit(fn, iters=20, warm=5):
 
 
 def main():
-    shapes = [(8192, 8192, 8192), (16384, 2048, 2048), (16384, 5632, 2048), (16384, 2048, 5632),
-              (16384, 768, 768), (16384, 3072, 768), (16384, 32000, 2048), (16384, 32000, 768)]
+    shapes = [(8192, 8192, 8192)]
+    if "--step" in sys.argv:  # the exact per-micro-batch GEMMs of the KD step (T = 4 x 2048)
+        shapes += [(8192, 2560, 2048), (8192, 2048, 2048), (8192, 11264, 2048), (8192, 2048, 5632),
+                   (8192, 32000, 2048), (8192, 2304, 768), (8192, 768, 768), (8192, 6144, 768),
+                   (8192, 768, 3072), (8192, 32000, 768)]
+    else:
+        shapes += [(16384, 2048, 2048), (16384, 5632, 2048), (16384, 2048, 5632), (16384, 768, 768),
+                   (16384, 3072, 768), (16384, 32000, 2048), (16384, 32000, 768)]
     out = []
     for M, N, K in shapes:
         a = torch.randn(M, K, device="cuda").bfloat16()
