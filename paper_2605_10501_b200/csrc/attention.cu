@@ -77,6 +77,45 @@ __device__ __forceinline__ uint32_t p_offset(int r, int c) {
   return (uint32_t)(chunk * 16384 + r * 128 + ((((cc >> 3) ^ (r & 7)) << 4)) + ((cc & 7) << 1));
 }
 
+// Persistent forward: one CTA per SM loops over work items (query tile, head) in heavy-first
+// order.  All pipeline counters run across items: K/V stream through the ring, S alternates
+// between two TMEM buffers by global tile index, Q and O are double-buffered by item index,
+// so the next item's Q load, first S MMAs and softmax overlap the current item's epilogue.
+// TMEM: S0 [0,128) S1 [128,256) O0 [256,320) O1 [320,384).
+struct FwdSmemP {
+  static constexpr int Q = 0;                                  // 2 x 16 KB (by item parity)
+  static constexpr int K = Q + 2 * TILE_BYTES;
+  static constexpr int V = K + KV_STAGES * TILE_BYTES;
+  static constexpr int P = V + KV_STAGES * TILE_BYTES;         // 2 x 32 KB (by tile parity)
+  static constexpr int BAR = P + 2 * P_BYTES;
+  static constexpr int TOTAL = BAR + 256;
+};
+
+struct FwdItem {
+  int seq, q0, h, hk, s0, L, n_kv;
+};
+
+template <bool CAUSAL>
+__device__ __forceinline__ FwdItem fwd_item(int w, int H, int Hk, const int32_t* cu, const int2* tiles) {
+  FwdItem it;
+  const int2 tq = tiles[w / H];
+  it.seq = tq.x;
+  it.q0 = tq.y;
+  it.h = w % H;
+  it.hk = it.h / (H / Hk);
+  it.s0 = cu[it.seq];
+  it.L = cu[it.seq + 1] - it.s0;
+  const int n_all = (it.L + BKV - 1) / BKV;
+  it.n_kv = CAUSAL ? min(n_all, it.q0 / BKV + 1) : n_all;
+  return it;
+}
+
+// Item of round r for this CTA; rounds alternate direction so the heavy-first item list is
+// dealt like LPT (the CTA that got the heaviest item of one round gets the lightest of the next).
+__device__ __forceinline__ int snake_item(int r) {
+  return r * (int)gridDim.x + ((r & 1) ? (int)gridDim.x - 1 - (int)blockIdx.x : (int)blockIdx.x);
+}
+
 template <bool CAUSAL>
 __global__ void __launch_bounds__(FWD_THREADS, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
@@ -85,47 +124,43 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
                     int ldo, float* __restrict__ lse, int T, int H, int Hk, float scale2) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + FwdSmem::BAR);
-  uint64_t* q_full = bar;
-  uint64_t* k_full = bar + 1;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + FwdSmemP::BAR);
+  uint64_t* q_full = bar;                  // [2]
+  uint64_t* q_empty = bar + 2;             // [2]
+  uint64_t* k_full = bar + 4;              // [KV_STAGES]
   uint64_t* k_empty = k_full + KV_STAGES;
   uint64_t* v_full = k_empty + KV_STAGES;
   uint64_t* v_empty = v_full + KV_STAGES;
-  uint64_t* s_full = v_empty + KV_STAGES;
+  uint64_t* s_full = v_empty + KV_STAGES;  // [2]
   uint64_t* s_empty = s_full + 2;
   uint64_t* p_full = s_empty + 2;
   uint64_t* p_empty = p_full + 2;
-  uint64_t* o_full = p_empty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 1);
+  uint64_t* o_full = p_empty + 2;          // [2]
+  uint64_t* o_empty = o_full + 2;          // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
 
-  const int tile = blockIdx.x;
-  if (tile >= *n_tiles) return;
-  const int2 tq = tiles[tile];
-  const int seq = tq.x, q0 = tq.y;
-  const int h = blockIdx.y, hk = h / (H / Hk);
-  const int s0 = cu[seq], L = cu[seq + 1] - s0;
-  const int n_kv_all = (L + BKV - 1) / BKV;
-  const int n_kv = CAUSAL ? min(n_kv_all, q0 / BKV + 1) : n_kv_all;
+  const int n_items = *n_tiles * H;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
   if (warp == 0 && lane == 0) {
     tma_prefetch(&map_q);
     tma_prefetch(&map_k);
     tma_prefetch(&map_v);
-    mbar_init(q_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&q_full[b], 1);
+      mbar_init(&q_empty[b], 1);
+      mbar_init(&s_full[b], 1);
+      mbar_init(&s_empty[b], 128);
+      mbar_init(&p_full[b], 128);
+      mbar_init(&p_empty[b], 1);
+      mbar_init(&o_full[b], 1);
+      mbar_init(&o_empty[b], 128);
+    }
     for (int s = 0; s < KV_STAGES; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
       mbar_init(&v_full[s], 1);
       mbar_init(&v_empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&s_full[b], 1);
-      mbar_init(&s_empty[b], 128);
-      mbar_init(&p_full[b], 128);
-      mbar_init(&p_empty[b], 1);
-    }
-    mbar_init(o_full, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -136,164 +171,194 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(q_full, TILE_BYTES);
-      tma_load_2d(sm + FwdSmem::Q, &map_q, q_full, h * DH, s0 + q0);
-      for (int i = 0; i < n_kv; ++i) {
-        const int st = i % KV_STAGES;
-        const uint32_t ph = (i / KV_STAGES) & 1;
-        mbar_wait(&k_empty[st], ph ^ 1);
-        mbar_arrive_expect_tx(&k_full[st], TILE_BYTES);
-        tma_load_2d(sm + FwdSmem::K + st * TILE_BYTES, &map_k, &k_full[st], hk * DH, s0 + i * BKV);
-        mbar_wait(&v_empty[st], ph ^ 1);
-        mbar_arrive_expect_tx(&v_full[st], TILE_BYTES);
-        tma_load_2d(sm + FwdSmem::V + st * TILE_BYTES, &map_v, &v_full[st], hk * DH, s0 + i * BKV);
+      int g = 0;  // global KV tile counter (ring position)
+      int j = 0;  // local item counter
+      for (int w = snake_item(0); w < n_items; w = snake_item(j + 1), ++j) {
+        const FwdItem it = fwd_item<CAUSAL>(w, H, Hk, cu, tiles);
+        const int qb = j & 1;
+        mbar_wait(&q_empty[qb], ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&q_full[qb], TILE_BYTES);
+        tma_load_2d(sm + FwdSmemP::Q + qb * TILE_BYTES, &map_q, &q_full[qb], it.h * DH, it.s0 + it.q0);
+        for (int i = 0; i < it.n_kv; ++i, ++g) {
+          const int st = g % KV_STAGES;
+          const uint32_t ph = (g / KV_STAGES) & 1;
+          mbar_wait(&k_empty[st], ph ^ 1);
+          mbar_arrive_expect_tx(&k_full[st], TILE_BYTES);
+          tma_load_2d(sm + FwdSmemP::K + st * TILE_BYTES, &map_k, &k_full[st], it.hk * DH, it.s0 + i * BKV);
+          mbar_wait(&v_empty[st], ph ^ 1);
+          mbar_arrive_expect_tx(&v_full[st], TILE_BYTES);
+          tma_load_2d(sm + FwdSmemP::V + st * TILE_BYTES, &map_v, &v_full[st], it.hk * DH, it.s0 + i * BKV);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc_s = idesc_bf16_f32(BQ, BKV, false, false);
       constexpr uint32_t idesc_o = idesc_bf16_f32(BQ, DH, false, true);
-      const uint32_t q_base = smem_u32(sm + FwdSmem::Q);
-      auto issue_pv = [&](int j) {
-        const int pb = j & 1;
-        mbar_wait(&p_full[pb], (j >> 1) & 1);
-        mbar_wait(&v_full[j % KV_STAGES], (j / KV_STAGES) & 1);
+      // PV of global tile gp (item-local index ip) into O buffer ob
+      auto issue_pv = [&](int gp, int ip, int ob) {
+        const int pb = gp & 1;
+        mbar_wait(&p_full[pb], (gp >> 1) & 1);
+        mbar_wait(&v_full[gp % KV_STAGES], (gp / KV_STAGES) & 1);
         tc_fence_after();
-        const uint32_t p_base = smem_u32(sm + FwdSmem::P + pb * P_BYTES);
-        const uint32_t v_base = smem_u32(sm + FwdSmem::V + (j % KV_STAGES) * TILE_BYTES);
+        const uint32_t p_base = smem_u32(sm + FwdSmemP::P + pb * P_BYTES);
+        const uint32_t v_base = smem_u32(sm + FwdSmemP::V + (gp % KV_STAGES) * TILE_BYTES);
 #pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk) {
-          const uint64_t ad = smem_desc_sw128(p_base + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024);
-          const uint64_t bd = smem_desc_sw128(v_base + kk * 2048, 8192, 1024);
-          umma_bf16(tmem + 256, ad, bd, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
-        }
-        umma_commit(&v_empty[j % KV_STAGES]);
+        for (int kk = 0; kk < BKV / 16; ++kk)
+          umma_bf16(tmem + 256 + ob * DH, smem_desc_sw128(p_base + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                    smem_desc_sw128(v_base + kk * 2048, 8192, 1024), idesc_o, (ip > 0 || kk > 0) ? 1u : 0u);
+        umma_commit(&v_empty[gp % KV_STAGES]);
         umma_commit(&p_empty[pb]);
       };
-      mbar_wait(q_full, 0);
-      for (int i = 0; i < n_kv; ++i) {
-        const int b = i & 1;
-        const int st = i % KV_STAGES;
-        mbar_wait(&k_full[st], (i / KV_STAGES) & 1);
-        mbar_wait(&s_empty[b], ((i >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t k_base = smem_u32(sm + FwdSmem::K + st * TILE_BYTES);
+      int g = 0, j = 0;
+      // the PV of each tile is issued after the NEXT tile's S (also across item boundaries), so
+      // the tensor core computes S while the softmax warps work on the previous tile
+      int pend_g = -1, pend_i = 0, pend_o = 0;
+      bool pend_last = false;
+      auto flush = [&]() {
+        if (pend_g < 0) return;
+        issue_pv(pend_g, pend_i, pend_o);
+        if (pend_last) umma_commit(&o_full[pend_o]);
+        pend_g = -1;
+      };
+      for (int w = snake_item(0); w < n_items; w = snake_item(j + 1), ++j) {
+        const FwdItem it = fwd_item<CAUSAL>(w, H, Hk, cu, tiles);
+        const int qb = j & 1, ob = j & 1;
+        mbar_wait(&q_full[qb], (j >> 1) & 1);
+        const uint32_t q_base = smem_u32(sm + FwdSmemP::Q + qb * TILE_BYTES);
+        for (int i = 0; i < it.n_kv; ++i, ++g) {
+          const int b = g & 1;
+          const int st = g % KV_STAGES;
+          mbar_wait(&k_full[st], (g / KV_STAGES) & 1);
+          mbar_wait(&s_empty[b], ((g >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t k_base = smem_u32(sm + FwdSmemP::K + st * TILE_BYTES);
 #pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk) {
-          const uint64_t ad = smem_desc_sw128(q_base + kk * 32, 16, 1024);
-          const uint64_t bd = smem_desc_sw128(k_base + kk * 32, 16, 1024);
-          umma_bf16(tmem + b * BKV, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
+          for (int kk = 0; kk < DH / 16; ++kk)
+            umma_bf16(tmem + b * BKV, smem_desc_sw128(q_base + kk * 32, 16, 1024),
+                      smem_desc_sw128(k_base + kk * 32, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+          umma_commit(&k_empty[st]);
+          umma_commit(&s_full[b]);
+          if (i == it.n_kv - 1) umma_commit(&q_empty[qb]);  // last S of the item: Q buffer free
+          flush();
+          if (i == 0) mbar_wait(&o_empty[ob], ((j >> 1) & 1) ^ 1);  // epilogue of item j-2 read O[ob]
+          pend_g = g;
+          pend_i = i;
+          pend_o = ob;
+          pend_last = i == it.n_kv - 1;
         }
-        umma_commit(&k_empty[st]);
-        umma_commit(&s_full[b]);
-        if (i >= 1) issue_pv(i - 1);
       }
-      issue_pv(n_kv - 1);
-      umma_commit(o_full);
+      flush();
     }
   } else {
-    // ---------------- softmax / correction / epilogue: thread = query row
     const int q = warp & 3;
     const int r = q * 32 + lane;
-    const int qpos = q0 + r;
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
-    float m = -INFINITY, l = 0.f;
-    unsigned char* pbuf = sm + FwdSmem::P;
-    for (int i = 0; i < n_kv; ++i) {
-      const int b = i & 1;
-      mbar_wait(&s_full[b], (i >> 1) & 1);
-      tc_fence_after();
-      float s[BKV];
-      {
-        uint32_t raw[BKV / 32][32];  // all four TMEM loads in flight, one wait
-#pragma unroll
-        for (int c = 0; c < BKV / 32; ++c) tmem_ld_32x32b_x32(tmem + lane_base + b * BKV + c * 32, raw[c]);
-        tmem_ld_wait();
-#pragma unroll
-        for (int c = 0; c < BKV / 32; ++c)
-#pragma unroll
-          for (int j = 0; j < 32; ++j) s[c * 32 + j] = __uint_as_float(raw[c][j]);
-      }
-      tc_fence_before();
-      mbar_arrive(&s_empty[b]);
-      const int kv0 = i * BKV;
-      const bool need_mask = (CAUSAL && kv0 + BKV - 1 > q0) || (kv0 + BKV > L);
-      float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};  // 4 chains: ILP
-      if (need_mask) {
-#pragma unroll
-        for (int c = 0; c < BKV; ++c) {
-          const int kv = kv0 + c;
-          if ((CAUSAL && kv > qpos) || kv >= L) s[c] = -INFINITY;
-          mx4[c & 3] = fmaxf(mx4[c & 3], s[c]);
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < BKV; ++c) mx4[c & 3] = fmaxf(mx4[c & 3], s[c]);
-      }
-      const float m_new = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * scale2;
-      bool rescale = false;
-      float alpha = 1.f;
-      if (m_new > m + 8.0f) {  // lazy rescale: keep a stale max unless it grew by > 2^8
-        alpha = ex2(m - m_new);
-        m = m_new;
-        rescale = i > 0;
-      }
-      float sum4[4] = {0.f, 0.f, 0.f, 0.f};
-      const float neg_m = -m;
-#pragma unroll
-      for (int c = 0; c < BKV; ++c) {
-        s[c] = ex2(fmaf(s[c], scale2, neg_m));
-        sum4[c & 3] += s[c];
-      }
-      l = l * alpha + ((sum4[0] + sum4[1]) + (sum4[2] + sum4[3]));
-      // P buffer b was last read by PV_{i-2}
-      if (i >= 2) mbar_wait(&p_empty[b], ((i >> 1) + 1) & 1);
-      if (rescale) {
-        mbar_wait(&p_empty[(i - 1) & 1], ((i - 1) >> 1) & 1);  // PV_{i-1} retired: O is final
+    unsigned char* pbuf = sm + FwdSmemP::P;
+    int g = 0, j = 0;
+    for (int w = snake_item(0); w < n_items; w = snake_item(j + 1), ++j) {
+      const FwdItem it = fwd_item<CAUSAL>(w, H, Hk, cu, tiles);
+      const int ob = j & 1;
+      const int qpos = it.q0 + r;
+      float m = -INFINITY, l = 0.f;
+      for (int i = 0; i < it.n_kv; ++i, ++g) {
+        const int b = g & 1;
+        mbar_wait(&s_full[b], (g >> 1) & 1);
         tc_fence_after();
+        float s[BKV];
+        {
+          uint32_t raw[BKV / 32][32];
 #pragma unroll
-        for (int c = 0; c < DH / 32; ++c) {
-          uint32_t rr[32];
-          tmem_ld_32x32b_x32(tmem + lane_base + 256 + c * 32, rr);
+          for (int c = 0; c < BKV / 32; ++c) tmem_ld_32x32b_x32(tmem + lane_base + b * BKV + c * 32, raw[c]);
           tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 32; ++j) rr[j] = __float_as_uint(__uint_as_float(rr[j]) * alpha);
-          tmem_st_32x32b_x32(tmem + lane_base + 256 + c * 32, rr);
+          for (int c = 0; c < BKV / 32; ++c)
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) s[c * 32 + jj] = __uint_as_float(raw[c][jj]);
         }
-        tmem_st_wait();
-      }
-      unsigned char* pb = pbuf + b * P_BYTES;
+        tc_fence_before();
+        mbar_arrive(&s_empty[b]);
+        const int kv0 = i * BKV;
+        const bool need_mask = (CAUSAL && kv0 + BKV - 1 > it.q0) || (kv0 + BKV > it.L);
+        float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        if (need_mask) {
 #pragma unroll
-      for (int u = 0; u < BKV / 8; ++u) {
-        uint4 v;
-        v.x = pack_bf16(s[8 * u + 0], s[8 * u + 1]);
-        v.y = pack_bf16(s[8 * u + 2], s[8 * u + 3]);
-        v.z = pack_bf16(s[8 * u + 4], s[8 * u + 5]);
-        v.w = pack_bf16(s[8 * u + 6], s[8 * u + 7]);
-        *reinterpret_cast<uint4*>(pb + p_offset(r, 8 * u)) = v;
-      }
-      fence_proxy_async_smem();
-      tc_fence_before();
-      mbar_arrive(&p_full[b]);
-    }
-    mbar_wait(o_full, 0);
-    tc_fence_after();
-    const float inv_l = 1.f / l;
-    uint32_t o[DH / 2];
+          for (int c = 0; c < BKV; ++c) {
+            const int kv = kv0 + c;
+            if ((CAUSAL && kv > qpos) || kv >= it.L) s[c] = -INFINITY;
+            mx4[c & 3] = fmaxf(mx4[c & 3], s[c]);
+          }
+        } else {
 #pragma unroll
-    for (int c = 0; c < DH / 32; ++c) {
-      uint32_t rr[32];
-      tmem_ld_32x32b_x32(tmem + lane_base + 256 + c * 32, rr);
+          for (int c = 0; c < BKV; ++c) mx4[c & 3] = fmaxf(mx4[c & 3], s[c]);
+        }
+        const float m_new = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * scale2;
+        bool rescale = false;
+        float alpha = 1.f;
+        if (m_new > m + 8.0f) {
+          alpha = ex2(m - m_new);
+          m = m_new;
+          rescale = i > 0;
+        }
+        float sum4[4] = {0.f, 0.f, 0.f, 0.f};
+        const float neg_m = -m;
+#pragma unroll
+        for (int c = 0; c < BKV; ++c) {
+          s[c] = ex2(fmaf(s[c], scale2, neg_m));
+          sum4[c & 3] += s[c];
+        }
+        l = l * alpha + ((sum4[0] + sum4[1]) + (sum4[2] + sum4[3]));
+        if (g >= 2) mbar_wait(&p_empty[b], ((g >> 1) + 1) & 1);  // PV_{g-2} read P buffer b
+        if (rescale) {
+          mbar_wait(&p_empty[(g - 1) & 1], ((g - 1) >> 1) & 1);  // PV_{g-1} retired: O is final
+          tc_fence_after();
+#pragma unroll
+          for (int c = 0; c < DH / 32; ++c) {
+            uint32_t rr[32];
+            tmem_ld_32x32b_x32(tmem + lane_base + 256 + ob * DH + c * 32, rr);
+            tmem_ld_wait();
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) rr[jj] = __float_as_uint(__uint_as_float(rr[jj]) * alpha);
+            tmem_st_32x32b_x32(tmem + lane_base + 256 + ob * DH + c * 32, rr);
+          }
+          tmem_st_wait();
+        }
+        unsigned char* pb = pbuf + b * P_BYTES;
+#pragma unroll
+        for (int u = 0; u < BKV / 8; ++u) {
+          uint4 v;
+          v.x = pack_bf16(s[8 * u + 0], s[8 * u + 1]);
+          v.y = pack_bf16(s[8 * u + 2], s[8 * u + 3]);
+          v.z = pack_bf16(s[8 * u + 4], s[8 * u + 5]);
+          v.w = pack_bf16(s[8 * u + 6], s[8 * u + 7]);
+          *reinterpret_cast<uint4*>(pb + p_offset(r, 8 * u)) = v;
+        }
+        fence_proxy_async_smem();
+        tc_fence_before();
+        mbar_arrive(&p_full[b]);
+      }
+      // epilogue of item j (overlaps the MMA warp starting item j+1)
+      mbar_wait(&o_full[ob], (j >> 1) & 1);
+      tc_fence_after();
+      const float inv_l = 1.f / l;
+      uint32_t raw[DH / 32][32];
+#pragma unroll
+      for (int c = 0; c < DH / 32; ++c) tmem_ld_32x32b_x32(tmem + lane_base + 256 + ob * DH + c * 32, raw[c]);
       tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(&o_empty[ob]);
+      if (qpos < it.L) {
+        uint32_t o[DH / 2];
 #pragma unroll
-      for (int j = 0; j < 16; ++j)
-        o[c * 16 + j] = pack_bf16(__uint_as_float(rr[2 * j]) * inv_l, __uint_as_float(rr[2 * j + 1]) * inv_l);
-    }
-    if (qpos < L) {
-      uint4* dst = reinterpret_cast<uint4*>(out + (size_t)(s0 + qpos) * ldo + h * DH);
+        for (int c = 0; c < DH / 32; ++c)
 #pragma unroll
-      for (int u = 0; u < DH / 8; ++u) dst[u] = make_uint4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);
-      lse[(size_t)h * T + s0 + qpos] = (m + log2f(l)) * LN2_F;
+          for (int jj = 0; jj < 16; ++jj)
+            o[c * 16 + jj] = pack_bf16(__uint_as_float(raw[c][2 * jj]) * inv_l, __uint_as_float(raw[c][2 * jj + 1]) * inv_l);
+        uint4* dst = reinterpret_cast<uint4*>(out + (size_t)(it.s0 + qpos) * ldo + it.h * DH);
+#pragma unroll
+        for (int u = 0; u < DH / 8; ++u) dst[u] = make_uint4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);
+        lse[(size_t)it.h * T + it.s0 + qpos] = (m + log2f(l)) * LN2_F;
+      }
     }
   }
   tc_fence_before();
@@ -303,7 +368,6 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     tmem_dealloc(tmem, 512);
   }
 }
-
 
 // ==========================================================================================
 // Backward, one CTA per (128-row KV tile, KV head); loops over the query heads of the GQA group
@@ -707,8 +771,9 @@ MAESTRO_API int maestro_attn_fwd(const void* q, const void* k, const void* v, co
   ok = ok && make_map_2d(&mk, k, (uint64_t)Hk * DH, T, ldk, 64, 128);
   ok = ok && make_map_2d(&mv, v, (uint64_t)Hk * DH, T, ldv, 64, 128);
   if (!ok) return (int)cudaErrorInvalidValue;
-  const int smem = FwdSmem::TOTAL + 1024;
-  dim3 grid(max_tiles, H);
+  const int smem = FwdSmemP::TOTAL + 1024;
+  const int items = max_tiles * H;  // upper bound; the kernel reads the true count
+  dim3 grid(items < num_sms() ? items : num_sms());
   const float scale2 = softmax_scale * LOG2E_F;
   if (causal) {
     if (ensure_smem<attn_fwd_kernel<true>>(smem)) return launch_status();
