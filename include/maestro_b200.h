@@ -199,6 +199,10 @@ int maestro_swiglu_fwd(const void* gu, void* out, int32_t T, int32_t F, void* st
 int maestro_swiglu_bwd(const void* dout, const void* gu, void* dgu, int32_t T, int32_t F, void* stream);
 int maestro_embed_fwd(const void* table, const int32_t* ids, void* out, int32_t T, int32_t d, void* stream);
 int maestro_embed_bwd(const void* dout, const int32_t* ids, float* dtable, int32_t T, int32_t d, void* stream);
+/* dst[c * ld_dst + r] = src[r * ld_src + c] (bf16; rows, cols, pitches multiples of 8).  Keeps the
+   K-major weight copies the dgrad GEMM reads (see FlatParams.refresh_transposed). */
+int maestro_transpose_bf16(const void* src, void* dst, int32_t rows, int32_t cols, int32_t ld_src, int32_t ld_dst,
+                           void* stream);
 int maestro_adamw(float* p, const float* g, float* m, float* v, void* pb, int64_t n, float lr, float b1, float b2,
                   float eps, float wd, int32_t step, float gscale, void* stream);
 

@@ -29,15 +29,6 @@ constexpr int FWD_THREADS = 192;
 constexpr float LOG2E_F = 1.4426950408889634f;
 constexpr float LN2_F = 0.6931471805599453f;
 
-struct FwdSmem {
-  static constexpr int Q = 0;
-  static constexpr int K = Q + TILE_BYTES;
-  static constexpr int V = K + KV_STAGES * TILE_BYTES;
-  static constexpr int P = V + KV_STAGES * TILE_BYTES;
-  static constexpr int BAR = P + 2 * P_BYTES;
-  static constexpr int TOTAL = BAR + 256;
-};
-
 // Query-tile list, heaviest (largest causal row count) first: tiles[i] = (seq, q0)
 __global__ void attn_tiles_kernel(const int32_t* __restrict__ cu, int nseq, int2* __restrict__ tiles,
                                   int* __restrict__ count) {
@@ -123,7 +114,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
                     const int2* __restrict__ tiles, const int* __restrict__ n_tiles, __nv_bfloat16* __restrict__ out,
                     int ldo, float* __restrict__ lse, int T, int H, int Hk, float scale2) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* sm = align_smem_1024(smem_raw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + FwdSmemP::BAR);
   uint64_t* q_full = bar;                  // [2]
   uint64_t* q_empty = bar + 2;             // [2]
@@ -370,19 +361,24 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
 }
 
 // ==========================================================================================
-// Backward, one CTA per (128-row KV tile, KV head); loops over the query heads of the GQA group
-// and the query tiles the tile can see.  Thread r of the 4 "softmax" warps owns KV row r:
+// Backward, persistent: one CTA per SM loops over items (128-row KV tile, KV head) in
+// heavy-first order; an item loops over the query heads of its GQA group and the query tiles
+// its keys can see.  Thread r of the 4 softmax warps owns KV row r:
 //   S^T = K Q^T, dP^T = V dO^T                      (TMEM, M = kv, N = q)
-//   P^T = exp2(S^T * scale2 - lse2[q]),  dS^T = P^T (dP^T - D[q])   -> bf16 smem operands
-//   dV += P^T dO, dK += dS^T Q                      (TMEM accumulators across all tiles)
+//   P1: P^T = exp2(S^T * scale2 - lse2[q])            -> bf16 smem operand     (p_ready)
+//   P2: dS^T = P^T (dP^T - D[q])                      -> bf16 smem operand     (ds_ready)
+//   dV += P^T dO, dK += dS^T Q                      (TMEM accumulators across the item)
 //   dQ_tile = dS K                                  (TMEM, drained with red.global.add.v4.f32)
+// The MMA warp issues dV(i), S(i+1) during P2(i) and dK(i), dQ(i), dP(i+1) during P1(i+1), also
+// across item boundaries (K/V are double-buffered by item), so softmax and tensor core overlap.
+// Two softmax warps share each TMEM lane quadrant and split the 128 query columns (the backward
+// needs no row reductions), so every SM sub-partition interleaves two softmax warps.
 // TMEM: S^T [0,128), dP^T [128,256), dV [256,320), dK [320,384), dQ [384,448).
-constexpr int BWD_THREADS = 320;  // w0 TMA, w1 MMA, w2-5 softmax, w6-9 dQ drain
+constexpr int BWD_THREADS = 448;  // w0 TMA, w1 MMA, w2-9 softmax (2 per lane quadrant), w10-13 dQ drain
 
 struct BwdSmem {
-  static constexpr int K = 0;
-  static constexpr int V = K + TILE_BYTES;
-  static constexpr int QD = V + TILE_BYTES;                 // 2 stages x (Q tile, dO tile)
+  static constexpr int KV = 0;                              // 2 items x (K tile, V tile)
+  static constexpr int QD = KV + 2 * 2 * TILE_BYTES;        // 2 stages x (Q tile, dO tile)
   static constexpr int PT = QD + 2 * 2 * TILE_BYTES;        // P^T  [kv][q] bf16, 2 chunks
   static constexpr int DST = PT + P_BYTES;                  // dS^T [kv][q] bf16, 2 chunks
   static constexpr int LSE = DST + P_BYTES;                 // 2 x 128 fp32 (double-buffered by tile)
@@ -398,6 +394,45 @@ __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float 
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
 
+struct BwdItem {
+  int kv0, hk, s0, L, qt_first, n_q, n_it;
+};
+
+template <bool CAUSAL>
+__device__ __forceinline__ BwdItem bwd_item(int w, int Hk, int G, const int32_t* cu, const int2* tiles) {
+  BwdItem it;
+  const int2 tk = tiles[w / Hk];
+  it.kv0 = tk.y;
+  it.hk = w % Hk;
+  it.s0 = cu[tk.x];
+  it.L = cu[tk.x + 1] - it.s0;
+  const int n_q_all = (it.L + BQ - 1) / BQ;
+  it.qt_first = CAUSAL ? it.kv0 / BQ : 0;
+  it.n_q = n_q_all - it.qt_first;
+  it.n_it = G * it.n_q;
+  return it;
+}
+
+// Flat cursor over (item, iteration) for the MMA warp's one-iteration lookahead.
+template <bool CAUSAL>
+struct BwdCursor {
+  int j, w, it;
+  bool valid;
+  BwdItem item;
+  __device__ __forceinline__ void load(int n_items, int Hk, int G, const int32_t* cu, const int2* tiles) {
+    w = snake_item(j);
+    valid = w < n_items;
+    if (valid) item = bwd_item<CAUSAL>(w, Hk, G, cu, tiles);
+  }
+  __device__ __forceinline__ void next(int n_items, int Hk, int G, const int32_t* cu, const int2* tiles) {
+    if (++it == item.n_it) {
+      ++j;
+      it = 0;
+      load(n_items, Hk, G, cu, tiles);
+    }
+  }
+};
+
 template <bool CAUSAL>
 __global__ void __launch_bounds__(BWD_THREADS, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
@@ -407,32 +442,28 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
                     __nv_bfloat16* __restrict__ dk, int lddk, __nv_bfloat16* __restrict__ dv, int lddv, int T, int H,
                     int Hk, float scale2, float scale, const float2* __restrict__ rope_cs) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* sm = align_smem_1024(smem_raw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + BwdSmem::BAR);
-  uint64_t* kv_full = bar;
-  uint64_t* qd_full = bar + 1;      // [2]
-  uint64_t* qd_empty = bar + 3;     // [2]
-  uint64_t* sp_full = bar + 5;
-  uint64_t* sp_empty = bar + 6;
-  uint64_t* ds_full = bar + 7;
-  uint64_t* ds_empty = bar + 8;
-  uint64_t* dq_full = bar + 9;
-  uint64_t* dq_empty = bar + 10;
-  uint64_t* dkv_full = bar + 11;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+  uint64_t* kv_full = bar;          // [2]
+  uint64_t* kv_empty = bar + 2;     // [2]
+  uint64_t* qd_full = bar + 4;      // [2]
+  uint64_t* qd_empty = bar + 6;     // [2]
+  uint64_t* s_full = bar + 8;
+  uint64_t* dp_full = bar + 9;
+  uint64_t* p_ready = bar + 10;
+  uint64_t* p_free = bar + 11;
+  uint64_t* ds_ready = bar + 12;
+  uint64_t* ds_free = bar + 13;
+  uint64_t* dq_full = bar + 14;
+  uint64_t* dq_empty = bar + 15;
+  uint64_t* dkv_full = bar + 16;
+  uint64_t* dkv_empty = bar + 17;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 18);
   float* s_lse = reinterpret_cast<float*>(sm + BwdSmem::LSE);
   float* s_D = reinterpret_cast<float*>(sm + BwdSmem::DD);
 
-  const int tile = blockIdx.x;
-  if (tile >= *n_tiles) return;
-  const int2 tk = tiles[tile];
-  const int seq = tk.x, kv0 = tk.y;
-  const int hk = blockIdx.y, G = H / Hk;
-  const int s0 = cu[seq], L = cu[seq + 1] - s0;
-  const int n_q_all = (L + BQ - 1) / BQ;
-  const int qt_first = CAUSAL ? kv0 / BQ : 0;
-  const int n_q = n_q_all - qt_first;
-  const int n_it = G * n_q;
+  const int G = H / Hk;
+  const int n_items = *n_tiles * Hk;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
@@ -440,18 +471,22 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     tma_prefetch(&map_k);
     tma_prefetch(&map_v);
     tma_prefetch(&map_do);
-    mbar_init(kv_full, 1);
     for (int b = 0; b < 2; ++b) {
+      mbar_init(&kv_full[b], 1);
+      mbar_init(&kv_empty[b], 1);
       mbar_init(&qd_full[b], 1);
       mbar_init(&qd_empty[b], 1);
     }
-    mbar_init(sp_full, 1);
-    mbar_init(sp_empty, 128);
-    mbar_init(ds_full, 128);
-    mbar_init(ds_empty, 1);
+    mbar_init(s_full, 1);
+    mbar_init(dp_full, 1);
+    mbar_init(p_ready, 256);
+    mbar_init(p_free, 1);
+    mbar_init(ds_ready, 256);
+    mbar_init(ds_free, 1);
     mbar_init(dq_full, 1);
     mbar_init(dq_empty, 128);
     mbar_init(dkv_full, 1);
+    mbar_init(dkv_empty, 256);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -463,18 +498,25 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(kv_full, 2 * TILE_BYTES);
-      tma_load_2d(sm + BwdSmem::K, &map_k, kv_full, hk * DH, s0 + kv0);
-      tma_load_2d(sm + BwdSmem::V, &map_v, kv_full, hk * DH, s0 + kv0);
-      for (int it = 0; it < n_it; ++it) {
-        const int g = it / n_q, qt = qt_first + it % n_q;
-        const int h = hk * G + g;
-        const int st = it & 1;
-        mbar_wait(&qd_empty[st], ((it >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(&qd_full[st], 2 * TILE_BYTES);
-        unsigned char* dst = sm + BwdSmem::QD + st * 2 * TILE_BYTES;
-        tma_load_2d(dst, &map_q, &qd_full[st], h * DH, s0 + qt * BQ);
-        tma_load_2d(dst + TILE_BYTES, &map_do, &qd_full[st], h * DH, s0 + qt * BQ);
+      int gi = 0, j = 0;
+      for (int w = snake_item(0); w < n_items; w = snake_item(j + 1), ++j) {
+        const BwdItem itm = bwd_item<CAUSAL>(w, Hk, G, cu, tiles);
+        const int kb = j & 1;
+        mbar_wait(&kv_empty[kb], ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&kv_full[kb], 2 * TILE_BYTES);
+        unsigned char* kvd = sm + BwdSmem::KV + kb * 2 * TILE_BYTES;
+        tma_load_2d(kvd, &map_k, &kv_full[kb], itm.hk * DH, itm.s0 + itm.kv0);
+        tma_load_2d(kvd + TILE_BYTES, &map_v, &kv_full[kb], itm.hk * DH, itm.s0 + itm.kv0);
+        for (int it = 0; it < itm.n_it; ++it, ++gi) {
+          const int g = it / itm.n_q, qt = itm.qt_first + it % itm.n_q;
+          const int h = itm.hk * G + g;
+          const int st = gi & 1;
+          mbar_wait(&qd_empty[st], ((gi >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(&qd_full[st], 2 * TILE_BYTES);
+          unsigned char* dst = sm + BwdSmem::QD + st * 2 * TILE_BYTES;
+          tma_load_2d(dst, &map_q, &qd_full[st], h * DH, itm.s0 + qt * BQ);
+          tma_load_2d(dst + TILE_BYTES, &map_do, &qd_full[st], h * DH, itm.s0 + qt * BQ);
+        }
       }
     }
   } else if (warp == 1) {
@@ -482,171 +524,245 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       constexpr uint32_t id_sp = idesc_bf16_f32(BKV, BQ, false, false);  // M = kv, N = q
       constexpr uint32_t id_kv = idesc_bf16_f32(BKV, DH, false, true);   // dV, dK: A K-major, B MN-major
       constexpr uint32_t id_dq = idesc_bf16_f32(BQ, DH, true, true);     // dQ: A = dS (MN-major view of dS^T)
-      const uint32_t k_base = smem_u32(sm + BwdSmem::K), v_base = smem_u32(sm + BwdSmem::V);
       const uint32_t pt_base = smem_u32(sm + BwdSmem::PT), ds_base = smem_u32(sm + BwdSmem::DST);
-      mbar_wait(kv_full, 0);
-      for (int it = 0; it < n_it; ++it) {
-        const int st = it & 1;
-        const uint32_t q_base = smem_u32(sm + BwdSmem::QD + st * 2 * TILE_BYTES);
-        const uint32_t do_base = q_base + TILE_BYTES;
-        mbar_wait(&qd_full[st], (it >> 1) & 1);
-        mbar_wait(sp_empty, (it & 1) ^ 1);
+      auto kv_base = [&](int j) { return smem_u32(sm + BwdSmem::KV + (j & 1) * 2 * TILE_BYTES); };
+      auto qd_base = [&](int gi) { return smem_u32(sm + BwdSmem::QD + (gi & 1) * 2 * TILE_BYTES); };
+      // S^T(gi) = K Q^T and dP^T(gi) = V dO^T of the cursor's iteration
+      auto issue_s = [&](const BwdCursor<CAUSAL>& c, int gi) {
+        mbar_wait(&qd_full[gi & 1], (gi >> 1) & 1);
+        if (c.it == 0) mbar_wait(&kv_full[c.j & 1], (c.j >> 1) & 1);
         tc_fence_after();
+        const uint32_t kb = kv_base(c.j), qb = qd_base(gi);
 #pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk) {
-          umma_bf16(tmem + T_ST, smem_desc_sw128(k_base + kk * 32, 16, 1024), smem_desc_sw128(q_base + kk * 32, 16, 1024),
+        for (int kk = 0; kk < DH / 16; ++kk)
+          umma_bf16(tmem + T_ST, smem_desc_sw128(kb + kk * 32, 16, 1024), smem_desc_sw128(qb + kk * 32, 16, 1024),
                     id_sp, kk > 0);
-          umma_bf16(tmem + T_DPT, smem_desc_sw128(v_base + kk * 32, 16, 1024),
-                    smem_desc_sw128(do_base + kk * 32, 16, 1024), id_sp, kk > 0);
-        }
-        umma_commit(sp_full);
-        mbar_wait(ds_full, it & 1);
-        mbar_wait(dq_empty, (it & 1) ^ 1);
+        umma_commit(s_full);
+      };
+      auto issue_dp = [&](const BwdCursor<CAUSAL>& c, int gi) {
+        const uint32_t vb = kv_base(c.j) + TILE_BYTES, db = qd_base(gi) + TILE_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk)
+          umma_bf16(tmem + T_DPT, smem_desc_sw128(vb + kk * 32, 16, 1024), smem_desc_sw128(db + kk * 32, 16, 1024),
+                    id_sp, kk > 0);
+        umma_commit(dp_full);
+      };
+      BwdCursor<CAUSAL> cur;
+      cur.j = 0;
+      cur.it = 0;
+      cur.load(n_items, Hk, G, cu, tiles);
+      int gi = 0;
+      if (cur.valid) {
+        issue_s(cur, 0);
+        issue_dp(cur, 0);
+      }
+      while (cur.valid) {
+        BwdCursor<CAUSAL> nxt = cur;
+        nxt.next(n_items, Hk, G, cu, tiles);
+        const uint32_t qb = qd_base(gi), kb = kv_base(cur.j);
+        // dV += P^T dO
+        mbar_wait(p_ready, gi & 1);
+        if (cur.it == 0) mbar_wait(dkv_empty, (cur.j & 1) ^ 1);  // previous item's epilogue read dK/dV
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < BQ / 16; ++kk) {  // reduction over the 128 queries
           const uint32_t chunk = (kk >> 2) * 16384 + (kk & 3) * 32;
           umma_bf16(tmem + T_DV, smem_desc_sw128(pt_base + chunk, 16, 1024),
-                    smem_desc_sw128(do_base + kk * 2048, 8192, 1024), id_kv, (it > 0 || kk > 0) ? 1u : 0u);
+                    smem_desc_sw128(qb + TILE_BYTES + kk * 2048, 8192, 1024), id_kv,
+                    (cur.it > 0 || kk > 0) ? 1u : 0u);
+        }
+        umma_commit(p_free);
+        if (nxt.valid) issue_s(nxt, gi + 1);  // S TMEM was read before p_ready
+        // dK += dS^T Q ; dQ = dS K
+        mbar_wait(ds_ready, gi & 1);
+        mbar_wait(dq_empty, (gi & 1) ^ 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < BQ / 16; ++kk) {
+          const uint32_t chunk = (kk >> 2) * 16384 + (kk & 3) * 32;
           umma_bf16(tmem + T_DK, smem_desc_sw128(ds_base + chunk, 16, 1024),
-                    smem_desc_sw128(q_base + kk * 2048, 8192, 1024), id_kv, (it > 0 || kk > 0) ? 1u : 0u);
+                    smem_desc_sw128(qb + kk * 2048, 8192, 1024), id_kv, (cur.it > 0 || kk > 0) ? 1u : 0u);
         }
 #pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk) {  // reduction over the 128 keys
+        for (int kk = 0; kk < BKV / 16; ++kk)  // reduction over the 128 keys
           umma_bf16(tmem + T_DQ, smem_desc_sw128(ds_base + kk * 2048, 16384, 1024),
-                    smem_desc_sw128(k_base + kk * 2048, 8192, 1024), id_dq, kk > 0 ? 1u : 0u);
-        }
-        umma_commit(&qd_empty[st]);
-        umma_commit(ds_empty);
+                    smem_desc_sw128(kb + kk * 2048, 8192, 1024), id_dq, kk > 0 ? 1u : 0u);
         umma_commit(dq_full);
+        umma_commit(&qd_empty[gi & 1]);
+        umma_commit(ds_free);
+        if (cur.it == cur.item.n_it - 1) {
+          umma_commit(dkv_full);
+          umma_commit(&kv_empty[cur.j & 1]);
+        }
+        if (nxt.valid) issue_dp(nxt, gi + 1);  // dP TMEM was read before ds_ready
+        cur = nxt;
+        ++gi;
       }
-      umma_commit(dkv_full);
     }
-  } else if (warp >= 6) {
-    // ---------------- dQ drain: TMEM -> fp32 reductions into dq_acc, overlapping the softmax
-    // warps' next tile (they no longer wait on these ~2k vector reductions per tile)
+  } else if (warp >= 10) {
+    // ---------------- dQ drain: TMEM -> fp32 reductions into dq_acc
     const int q4 = warp & 3;
     const int r = q4 * 32 + lane;  // query row of the dQ tile
     const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
-    for (int it = 0; it < n_it; ++it) {
-      const int g = it / n_q, qt = qt_first + it % n_q;
-      const int h = hk * G + g;
-      const int qrow = qt * BQ + r;
-      mbar_wait(dq_full, it & 1);
-      tc_fence_after();
-      uint32_t qa[32], qb[32];
-      tmem_ld_32x32b_x32(tmem + lane_base + T_DQ, qa);
-      tmem_ld_32x32b_x32(tmem + lane_base + T_DQ + 32, qb);
-      tmem_ld_wait();
-      tc_fence_before();
-      mbar_arrive(dq_empty);  // TMEM free as soon as it is in registers
-      if (qrow < L) {
-        float* dst_row = dq_acc + ((size_t)(s0 + qrow) * H + h) * DH;
+    int gi = 0, j = 0;
+    for (int w = snake_item(0); w < n_items; w = snake_item(j + 1), ++j) {
+      const BwdItem itm = bwd_item<CAUSAL>(w, Hk, G, cu, tiles);
+      for (int it = 0; it < itm.n_it; ++it, ++gi) {
+        const int g = it / itm.n_q, qt = itm.qt_first + it % itm.n_q;
+        const int h = itm.hk * G + g;
+        const int qrow = qt * BQ + r;
+        mbar_wait(dq_full, gi & 1);
+        tc_fence_after();
+        uint32_t qa[32], qb[32];
+        tmem_ld_32x32b_x32(tmem + lane_base + T_DQ, qa);
+        tmem_ld_32x32b_x32(tmem + lane_base + T_DQ + 32, qb);
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(dq_empty);  // TMEM free as soon as it is in registers
+        if (qrow < itm.L) {
+          float* dst_row = dq_acc + ((size_t)(itm.s0 + qrow) * H + h) * DH;
 #pragma unroll
-        for (int j = 0; j < 32; j += 4) {
-          red_add_v4(dst_row + j, __uint_as_float(qa[j]), __uint_as_float(qa[j + 1]), __uint_as_float(qa[j + 2]),
-                     __uint_as_float(qa[j + 3]));
-          red_add_v4(dst_row + 32 + j, __uint_as_float(qb[j]), __uint_as_float(qb[j + 1]),
-                     __uint_as_float(qb[j + 2]), __uint_as_float(qb[j + 3]));
+          for (int k = 0; k < 32; k += 4) {
+            red_add_v4(dst_row + k, __uint_as_float(qa[k]), __uint_as_float(qa[k + 1]), __uint_as_float(qa[k + 2]),
+                       __uint_as_float(qa[k + 3]));
+            red_add_v4(dst_row + 32 + k, __uint_as_float(qb[k]), __uint_as_float(qb[k + 1]),
+                       __uint_as_float(qb[k + 2]), __uint_as_float(qb[k + 3]));
+          }
         }
       }
     }
   } else {
     const int q4 = warp & 3;
-    const int r = q4 * 32 + lane;  // kv row (S^T, dP^T, dK, dV)
+    const int half = (warp - 2) >> 2;  // query columns [64 * half, 64 * half + 64)
+    const int r = q4 * 32 + lane;      // kv row (S^T, dP^T, dK, dV)
     const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
-    const int kvpos = kv0 + r;
-    const int tid = threadIdx.x - 64;
+    const int tid = threadIdx.x - 64;  // 0..255
     unsigned char* pt = sm + BwdSmem::PT;
     unsigned char* dst = sm + BwdSmem::DST;
-    for (int it = 0; it < n_it; ++it) {
-      const int g = it / n_q, qt = qt_first + it % n_q;
-      const int h = hk * G + g;
-      const int q0 = qt * BQ;
-      float* lse_t = s_lse + (it & 1) * 128;  // double-buffered: one barrier per tile suffices
-      float* D_t = s_D + (it & 1) * 128;
-      {
-        const int qi = q0 + tid;
-        const bool ok = qi < L;
-        lse_t[tid] = ok ? lse[(size_t)h * T + s0 + qi] * LOG2E_F : INFINITY;
-        D_t[tid] = ok ? Dvec[(size_t)h * T + s0 + qi] : 0.f;
-      }
-      named_bar(1, 128);
-      mbar_wait(sp_full, it & 1);
-      mbar_wait(ds_empty, (it & 1) ^ 1);
-      tc_fence_after();
-      const bool need_mask = (CAUSAL && q0 < kv0 + BKV - 1) || (q0 + BQ > L) || (kv0 + BKV > L);
-#pragma unroll 1
-      for (int c0 = 0; c0 < BQ; c0 += 32) {
-        uint32_t sr[32], pr[32];
-        tmem_ld_32x32b_x32(tmem + lane_base + T_ST + c0, sr);
-        tmem_ld_32x32b_x32(tmem + lane_base + T_DPT + c0, pr);
-        tmem_ld_wait();
-        float p[32], ds[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int c = c0 + j;
-          float pv = ex2(fmaf(__uint_as_float(sr[j]), scale2, -lse_t[c]));
-          if (need_mask) {
-            const int qpos = q0 + c;
-            if ((CAUSAL && qpos < kvpos) || qpos >= L || kvpos >= L) pv = 0.f;
-          }
-          p[j] = pv;
-          ds[j] = pv * (__uint_as_float(pr[j]) - D_t[c]);
+    int gi = 0, j = 0;
+    for (int w = snake_item(0); w < n_items; w = snake_item(j + 1), ++j) {
+      const BwdItem itm = bwd_item<CAUSAL>(w, Hk, G, cu, tiles);
+      const int kvpos = itm.kv0 + r;
+      for (int it = 0; it < itm.n_it; ++it, ++gi) {
+        const int g = it / itm.n_q, qt = itm.qt_first + it % itm.n_q;
+        const int h = itm.hk * G + g;
+        const int q0 = qt * BQ;
+        float* lse_t = s_lse + (gi & 1) * 128;  // double-buffered: one barrier per tile suffices
+        float* D_t = s_D + (gi & 1) * 128;
+        {
+          const int qi = q0 + (tid & 127);
+          const bool ok = qi < itm.L;
+          if (tid < 128)
+            lse_t[tid] = ok ? lse[(size_t)h * T + itm.s0 + qi] * LOG2E_F : INFINITY;
+          else
+            D_t[tid - 128] = ok ? Dvec[(size_t)h * T + itm.s0 + qi] : 0.f;
         }
+        named_bar(1, 256);
+        const bool need_mask =
+            (CAUSAL && q0 < itm.kv0 + BKV - 1) || (q0 + BQ > itm.L) || (itm.kv0 + BKV > itm.L);
+        // ---- P1: S^T -> P^T
+        mbar_wait(s_full, gi & 1);
+        tc_fence_after();
+        if (gi >= 1) mbar_wait(p_free, (gi - 1) & 1);  // dV(gi-1) has read P^T
+#pragma unroll
+        for (int cc = 0; cc < 64; cc += 32) {
+          const int c0 = half * 64 + cc;
+          uint32_t sr[32];
+          tmem_ld_32x32b_x32(tmem + lane_base + T_ST + c0, sr);
+          tmem_ld_wait();
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            float pv[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int c = c0 + 8 * u + e;
+              pv[e] = ex2(fmaf(__uint_as_float(sr[8 * u + e]), scale2, -lse_t[c]));
+              if (need_mask) {
+                const int qpos = q0 + c;
+                if ((CAUSAL && qpos < kvpos) || qpos >= itm.L || kvpos >= itm.L) pv[e] = 0.f;
+              }
+            }
+            *reinterpret_cast<uint4*>(pt + p_offset(r, c0 + 8 * u)) =
+                make_uint4(pack_bf16(pv[0], pv[1]), pack_bf16(pv[2], pv[3]), pack_bf16(pv[4], pv[5]),
+                           pack_bf16(pv[6], pv[7]));
+          }
+        }
+        fence_proxy_async_smem();
+        tc_fence_before();
+        mbar_arrive(p_ready);
+        // ---- P2: dP^T -> dS^T
+        mbar_wait(dp_full, gi & 1);
+        tc_fence_after();
+        if (gi >= 1) mbar_wait(ds_free, (gi - 1) & 1);  // dK/dQ(gi-1) have read dS^T
+#pragma unroll
+        for (int cc = 0; cc < 64; cc += 32) {
+          const int c0 = half * 64 + cc;
+          uint32_t pr[32];
+          tmem_ld_32x32b_x32(tmem + lane_base + T_DPT + c0, pr);
+          tmem_ld_wait();
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            // P (bf16, as the dV MMA uses it) re-read from this thread's row of the P^T operand
+            const uint4 pp4 = *reinterpret_cast<const uint4*>(pt + p_offset(r, c0 + 8 * u));
+            const uint32_t pw[4] = {pp4.x, pp4.y, pp4.z, pp4.w};
+            float ds[8];
+#pragma unroll
+            for (int k = 0; k < 8; k += 2) {
+              const int c = c0 + 8 * u + k;
+              const float2 pp = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pw[k >> 1]));
+              ds[k] = pp.x * (__uint_as_float(pr[8 * u + k]) - D_t[c]);
+              ds[k + 1] = pp.y * (__uint_as_float(pr[8 * u + k + 1]) - D_t[c + 1]);
+            }
+            *reinterpret_cast<uint4*>(dst + p_offset(r, c0 + 8 * u)) =
+                make_uint4(pack_bf16(ds[0], ds[1]), pack_bf16(ds[2], ds[3]), pack_bf16(ds[4], ds[5]),
+                           pack_bf16(ds[6], ds[7]));
+          }
+        }
+        fence_proxy_async_smem();
+        tc_fence_before();
+        mbar_arrive(ds_ready);
+      }
+      // ---- item epilogue: dK (scaled, inverse RoPE), then dV -> bf16; TMEM is released after
+      // the dV load so the next item's first dV MMA can start while the stores drain
+      mbar_wait(dkv_full, j & 1);
+      tc_fence_after();
+      {
+        const int which = half;  // half 0 drains dK, half 1 dV
+        uint32_t lo[32], hi[32];
+        tmem_ld_32x32b_x32(tmem + lane_base + (which == 0 ? T_DK : T_DV), lo);
+        tmem_ld_32x32b_x32(tmem + lane_base + (which == 0 ? T_DK : T_DV) + 32, hi);
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(dkv_empty);
+        if (kvpos < itm.L) {
+        const float f = which == 0 ? scale : 1.f;
+        if (which == 0 && rope_cs != nullptr) {
+          // K was rotated by RoPE in the forward: dK_pre = R(pos)^T dK  (rotate by -theta)
+          const float2* csr = rope_cs + (size_t)kvpos * 32;
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            const float2 cs = csr[k];
+            const float a = __uint_as_float(lo[k]), b = __uint_as_float(hi[k]);
+            lo[k] = __float_as_uint(a * cs.x + b * cs.y);
+            hi[k] = __float_as_uint(b * cs.x - a * cs.y);
+          }
+        }
+        __nv_bfloat16* base = which == 0 ? dk + (size_t)(itm.s0 + kvpos) * lddk : dv + (size_t)(itm.s0 + kvpos) * lddv;
+        uint4* d4 = reinterpret_cast<uint4*>(base + itm.hk * DH);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          uint4 a, b;
-          a.x = pack_bf16(p[8 * u + 0], p[8 * u + 1]);
-          a.y = pack_bf16(p[8 * u + 2], p[8 * u + 3]);
-          a.z = pack_bf16(p[8 * u + 4], p[8 * u + 5]);
-          a.w = pack_bf16(p[8 * u + 6], p[8 * u + 7]);
-          b.x = pack_bf16(ds[8 * u + 0], ds[8 * u + 1]);
-          b.y = pack_bf16(ds[8 * u + 2], ds[8 * u + 3]);
-          b.z = pack_bf16(ds[8 * u + 4], ds[8 * u + 5]);
-          b.w = pack_bf16(ds[8 * u + 6], ds[8 * u + 7]);
-          const uint32_t off = p_offset(r, c0 + 8 * u);
-          *reinterpret_cast<uint4*>(pt + off) = a;
-          *reinterpret_cast<uint4*>(dst + off) = b;
+          const uint32_t* x = lo + 8 * u;
+          const uint32_t* y = hi + 8 * u;
+          d4[u] = make_uint4(pack_bf16(__uint_as_float(x[0]) * f, __uint_as_float(x[1]) * f),
+                             pack_bf16(__uint_as_float(x[2]) * f, __uint_as_float(x[3]) * f),
+                             pack_bf16(__uint_as_float(x[4]) * f, __uint_as_float(x[5]) * f),
+                             pack_bf16(__uint_as_float(x[6]) * f, __uint_as_float(x[7]) * f));
+          d4[4 + u] = make_uint4(pack_bf16(__uint_as_float(y[0]) * f, __uint_as_float(y[1]) * f),
+                                 pack_bf16(__uint_as_float(y[2]) * f, __uint_as_float(y[3]) * f),
+                                 pack_bf16(__uint_as_float(y[4]) * f, __uint_as_float(y[5]) * f),
+                                 pack_bf16(__uint_as_float(y[6]) * f, __uint_as_float(y[7]) * f));
         }
-      }
-      tc_fence_before();
-      mbar_arrive(sp_empty);
-      fence_proxy_async_smem();
-      mbar_arrive(ds_full);
-    }
-    // dK (scaled), dV -> bf16
-    mbar_wait(dkv_full, 0);
-    tc_fence_after();
-#pragma unroll
-    for (int which = 0; which < 2; ++which) {
-      uint32_t o[DH / 2];
-      const float f = which == 0 ? scale : 1.f;
-      uint32_t lo[32], hi[32];
-      tmem_ld_32x32b_x32(tmem + lane_base + (which == 0 ? T_DK : T_DV), lo);
-      tmem_ld_32x32b_x32(tmem + lane_base + (which == 0 ? T_DK : T_DV) + 32, hi);
-      tmem_ld_wait();
-      if (which == 0 && rope_cs != nullptr && kvpos < L) {
-        // K was rotated by RoPE in the forward: dK_pre = R(pos)^T dK  (rotate by -theta)
-        const float2* csr = rope_cs + (size_t)kvpos * 32;
-#pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          const float2 cs = csr[k];
-          const float a = __uint_as_float(lo[k]), b = __uint_as_float(hi[k]);
-          lo[k] = __float_as_uint(a * cs.x + b * cs.y);
-          hi[k] = __float_as_uint(b * cs.x - a * cs.y);
         }
-      }
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        o[j] = pack_bf16(__uint_as_float(lo[2 * j]) * f, __uint_as_float(lo[2 * j + 1]) * f);
-        o[16 + j] = pack_bf16(__uint_as_float(hi[2 * j]) * f, __uint_as_float(hi[2 * j + 1]) * f);
-      }
-      if (kvpos < L) {
-        __nv_bfloat16* base = which == 0 ? dk + (size_t)(s0 + kvpos) * lddk : dv + (size_t)(s0 + kvpos) * lddv;
-        uint4* d4 = reinterpret_cast<uint4*>(base + hk * DH);
-#pragma unroll
-        for (int u = 0; u < DH / 8; ++u) d4[u] = make_uint4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);
       }
     }
   }
@@ -820,7 +936,8 @@ MAESTRO_API int maestro_attn_bwd(const void* dout, int32_t lddo, const void* q, 
   ok = ok && make_map_2d(&mdo, dout, (uint64_t)H * DH, T, lddo, 64, 128);
   if (!ok) return (int)cudaErrorInvalidValue;
   const int smem = BwdSmem::TOTAL + 1024;
-  dim3 grid(max_tiles, Hk);
+  const int items = max_tiles * Hk;  // upper bound; the kernel reads the true count
+  dim3 grid(items < num_sms() ? items : num_sms());
   const float scale2 = softmax_scale * LOG2E_F;
   if (causal) {
     if (ensure_smem<attn_bwd_kernel<true>>(smem)) return launch_status();

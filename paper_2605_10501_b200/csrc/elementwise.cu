@@ -500,6 +500,39 @@ MAESTRO_API int maestro_embed_bwd(const void* dout, const int32_t* ids, float* d
   return launch_status();
 }
 
+// dst[c][r] = src[r][c] (bf16), 64 x 64 tiles through padded shared memory: 16-byte row loads,
+// 16-byte column-gathered stores.  Used to keep K-major copies of weights for the dgrad GEMM.
+__global__ void transpose_bf16_kernel(const __nv_bfloat16* __restrict__ src, __nv_bfloat16* __restrict__ dst,
+                                      int rows, int cols, int ld_src, int ld_dst) {
+  __shared__ __nv_bfloat16 tile[64][64 + 8];
+  const int r0 = blockIdx.y * 64, c0 = blockIdx.x * 64;
+  for (int i = threadIdx.x; i < 64 * 8; i += blockDim.x) {
+    const int r = i >> 3, cv = (i & 7) * 8;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (r0 + r < rows && c0 + cv < cols) v = *reinterpret_cast<const uint4*>(src + (size_t)(r0 + r) * ld_src + c0 + cv);
+    *reinterpret_cast<uint4*>(&tile[r][cv]) = v;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 64 * 8; i += blockDim.x) {
+    const int c = i >> 3, rv = (i & 7) * 8;
+    if (c0 + c >= cols || r0 + rv >= rows) continue;
+    __align__(16) __nv_bfloat16 o[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) o[k] = tile[rv + k][c];
+    *reinterpret_cast<uint4*>(dst + (size_t)(c0 + c) * ld_dst + r0 + rv) = *reinterpret_cast<uint4*>(o);
+  }
+}
+
+MAESTRO_API int maestro_transpose_bf16(const void* src, void* dst, int32_t rows, int32_t cols, int32_t ld_src,
+                                       int32_t ld_dst, void* stream) {
+  if (rows <= 0 || cols <= 0) return 0;
+  if ((rows % 8) || (cols % 8) || (ld_src % 8) || (ld_dst % 8)) return (int)cudaErrorInvalidValue;
+  dim3 grid((cols + 63) / 64, (rows + 63) / 64);
+  transpose_bf16_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)src, (__nv_bfloat16*)dst, rows,
+                                                                 cols, ld_src, ld_dst);
+  return launch_status();
+}
+
 MAESTRO_API int maestro_adamw(float* p, const float* g, float* m, float* v, void* pb, int64_t n, float lr, float b1,
                               float b2, float eps, float wd, int32_t step, float gscale, void* stream) {
   if (n <= 0) return 0;

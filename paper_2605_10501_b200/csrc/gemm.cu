@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   constexpr int STAGES = Cfg<BN>::STAGES, B_BYTES = Cfg<BN>::B_BYTES, STAGE_BYTES = Cfg<BN>::STAGE_BYTES;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-byte alignment for SWIZZLE_128B atoms
-  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* smem = align_smem_1024(smem_raw);
   unsigned char* sA = smem;
   unsigned char* sB = smem + STAGES * A_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
@@ -277,7 +277,7 @@ struct Cfg2 {
   static constexpr int B_ROWS = BN2 / 2;  // B rows per CTA
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = BN2 == 256 ? 6 : 8;
+  static constexpr int STAGES = BN2 == 128 ? 8 : 6;
   static constexpr int EPI_BUF = 128 * 64 * 2;  // one 128 x 64 bf16 SWIZZLE_128B staging tile
   static constexpr int SMEM = STAGES * STAGE_BYTES + 2 * EPI_BUF + 1024 + 256;
 };
@@ -291,7 +291,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   using CF = Cfg2<BN2>;
   constexpr int STAGES = CF::STAGES, B_BYTES = CF::B_BYTES, STAGE_BYTES = CF::STAGE_BYTES, B_ROWS = CF::B_ROWS;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* smem = align_smem_1024(smem_raw);
   unsigned char* sA = smem;
   unsigned char* sB = smem + STAGES * A_BYTES;
   unsigned char* sC = smem + STAGES * STAGE_BYTES;  // 2 x 16 KB epilogue staging (bf16 path)
@@ -618,7 +618,18 @@ static int gemm_impl(const void* A, const void* B, void* C, int32_t M, int32_t N
     // (measured on the step shapes: more operand traffic and epilogue per FLOP), not 0.5
     // (c256 counts 256-wide tiles twice); only short-K, epilogue-bound shapes gain from 128
     int bn2 = (K <= 1024 && 6 * c128 < 5 * c256) ? 128 : 256;
-    if (const char* e = getenv("MAESTRO_GEMM_BN")) bn2 = atoi(e) == 128 ? 128 : 256;  // experiments
+    if (!b_mn) {
+      // 256 x 192 tiles (K-major B only: 96 rows per CTA is not a whole SWIZZLE_128B MN atom)
+      // fix the quantisation of 768-wide outputs (96 -> 128 tiles on 74 pairs: 2 rounds of 0.75)
+      const long long t192 = tm * ((N + 191) / 192);
+      const long long c192 = (t192 + pairs - 1) / pairs;  // x 0.8 of a 256-wide tile
+      const long long cur = bn2 == 256 ? 10 * c256 / 2 : 6 * c128;  // in tenths of a 256 tile
+      if (8 * c192 < cur) bn2 = 192;
+    }
+    if (const char* e = getenv("MAESTRO_GEMM_BN")) {  // experiments
+      const int v = atoi(e);
+      bn2 = v == 128 ? 128 : (v == 192 && !b_mn) ? 192 : 256;
+    }
     int splits = 1;
     const int kb = (K + BK - 1) / BK;
     if (epi == EPI_F32_ACC && t256 < pairs && kb >= 8) {
@@ -646,15 +657,21 @@ static int gemm_impl(const void* A, const void* B, void* C, int32_t M, int32_t N
     bool ok = a_mn ? make_map_2d(&ma, A, M, K, lda, 64, 64) : make_map_2d(&ma, A, K, M, lda, 64, 128);
     ok = ok && (b_mn ? make_map_2d(&mbm, B, N, K, ldb, 64, 64) : make_map_2d(&mbm, B, K, N, ldb, 64, brows));
     if (!ok) return (int)cudaErrorInvalidValue;
-#define MB_GEMM2_CASE(AM, BMN, E)                                                                  \
-  if (a_mn == AM && b_mn == BMN && epi_k == E)                                                     \
-    return bn2 == 256 ? launch2<256, AM, BMN, E>(ma, mbm, mc, C, M, N, K, ldc, splits, st, rope_pos, rope_cs,  \
-                                                 rope_cols, (__nv_bfloat16*)swiglu_out, ld_swiglu)              \
-                      : launch2<128, AM, BMN, E>(ma, mbm, mc, C, M, N, K, ldc, splits, st, rope_pos, rope_cs,  \
-                                                 rope_cols, (__nv_bfloat16*)swiglu_out, ld_swiglu);
-    MB_GEMM2_CASE(0, 0, 0)
-    MB_GEMM2_CASE(0, 0, 1)
-    MB_GEMM2_CASE(0, 0, 2)
+#define MB_GEMM2_LAUNCH(W, AM, BMN, E)                                                                  \
+  launch2<W, AM, BMN, E>(ma, mbm, mc, C, M, N, K, ldc, splits, st, rope_pos, rope_cs, rope_cols,         \
+                         (__nv_bfloat16*)swiglu_out, ld_swiglu)
+#define MB_GEMM2_CASE(AM, BMN, E)                                                                    \
+  if (a_mn == AM && b_mn == BMN && epi_k == E)                                                       \
+    return bn2 == 256 ? MB_GEMM2_LAUNCH(256, AM, BMN, E) : MB_GEMM2_LAUNCH(128, AM, BMN, E);
+#define MB_GEMM2_CASE_K(AM, E)                                                                      \
+  if (a_mn == AM && b_mn == 0 && epi_k == E)                                                        \
+    return bn2 == 256 ? MB_GEMM2_LAUNCH(256, AM, 0, E)                                              \
+                      : bn2 == 192 ? MB_GEMM2_LAUNCH(192, AM, 0, E) : MB_GEMM2_LAUNCH(128, AM, 0, E);
+    MB_GEMM2_CASE_K(0, 0)
+    MB_GEMM2_CASE_K(0, 1)
+    MB_GEMM2_CASE_K(0, 2)
+    MB_GEMM2_CASE(0, 0, 3)
+    MB_GEMM2_CASE(0, 1, 3)
     MB_GEMM2_CASE(0, 1, 0)
     MB_GEMM2_CASE(0, 1, 1)
     MB_GEMM2_CASE(0, 1, 2)
@@ -663,6 +680,8 @@ static int gemm_impl(const void* A, const void* B, void* C, int32_t M, int32_t N
     MB_GEMM2_CASE(1, 1, 2)
     MB_GEMM2_CASE(1, 1, 3)
 #undef MB_GEMM2_CASE
+#undef MB_GEMM2_CASE_K
+#undef MB_GEMM2_LAUNCH
   }
   return (int)cudaErrorInvalidValue;
 }

@@ -148,6 +148,12 @@ __device__ __forceinline__ void umma_commit_2sm(uint64_t* bar, uint16_t mask) {
       : "memory");
 }
 
+// 1024-byte-aligned base inside the dynamic smem array, derived by pointer offset so the
+// compiler keeps the shared address space (STS/LDS instead of generic ST/LD through it).
+__device__ __forceinline__ unsigned char* align_smem_1024(unsigned char* raw) {
+  return raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);
+}
+
 // D[tmem] (+)= A[smem] * B[smem]^T, kind::f16 (bf16 in, fp32 accumulate), single CTA
 __device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                           uint32_t accumulate) {

@@ -104,12 +104,15 @@ def linear_fwd_swiglu(x: torch.Tensor, w: torch.Tensor, s_out: torch.Tensor,
     return out
 
 
-def linear_dgrad(dy: torch.Tensor, w: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
-    """dx[T, in] = dy[T, out] @ w[out, in]."""
+def linear_dgrad(dy: torch.Tensor, w: torch.Tensor, out: torch.Tensor | None = None,
+                 wt: torch.Tensor | None = None) -> torch.Tensor:
+    """dx[T, in] = dy[T, out] @ w[out, in].  ``wt`` = w^T [in, out] (bf16) makes B K-major."""
     T, Nn = dy.shape
     K = w.shape[1]
     if out is None:
         out = torch.empty(T, K, device=dy.device, dtype=torch.bfloat16)
+    if wt is not None:
+        return gemm(dy, wt, out, T, K, Nn, False, False, EPI_BF16, ldb=wt.stride(0))
     return gemm(dy, w, out, T, K, Nn, False, True, EPI_BF16, ldb=w.stride(0))
 
 

@@ -22,6 +22,7 @@ _SIGS = {
     "maestro_swiglu_bwd": [_P, _P, _P, _I32, _I32, _P],
     "maestro_embed_fwd": [_P, _P, _P, _I32, _I32, _P],
     "maestro_embed_bwd": [_P, _P, _P, _I32, _I32, _P],
+    "maestro_transpose_bf16": [_P, _P, _I32, _I32, _I32, _I32, _P],
     "maestro_adamw": [_P, _P, _P, _P, _P, _I64, _F, _F, _F, _F, _F, _I32, _F, _P],
     "maestro_kd_loss_fwd_bwd": [_P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32, _F, _F, _P],
     "maestro_ce_loss_fwd_bwd": [_P, _P, _P, _P, _I32, _I32, _I32, _I32, _F, _P],
@@ -88,6 +89,12 @@ def embed(table, ids, out):
 def embed_bwd(dout, ids, dtable):
     T, d = dout.shape
     N.check(L().maestro_embed_bwd(_p(dout), _p(ids), _p(dtable), T, d, _s()), "embed_bwd")
+
+
+def transpose(src, dst):
+    """dst[c, r] = src[r, c] (bf16, 2-D, row pitch from the tensors)."""
+    R, C = src.shape
+    N.check(L().maestro_transpose_bf16(_p(src), _p(dst), R, C, src.stride(0), dst.stride(0), _s()), "transpose_bf16")
 
 
 def adamw(p, g, m, v, pb, lr, step, b1=0.9, b2=0.95, eps=1e-8, wd=0.1, gscale=1.0):

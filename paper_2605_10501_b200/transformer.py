@@ -111,6 +111,14 @@ class FlatParams:
             del master
             self.master = self.grad = self.m = self.v = None
         self.step = 0
+        # K-major (transposed) bf16 copies of the trainable matrices: the dgrad GEMM then reads
+        # its B operand K-major, which admits the 256 x 192 tile that fits 768-wide outputs
+        self.wt = {}
+        if trainable:
+            for name, (o, shp) in self.index.items():
+                if len(shp) == 2:
+                    self.wt[name] = torch.empty(shp[1], shp[0], device=device, dtype=torch.bfloat16)
+            self.refresh_transposed()
 
     def _view(self, buf, name):
         o, shp = self.index[name]
@@ -122,12 +130,21 @@ class FlatParams:
     def g(self, name):
         return self._view(self.grad, name)
 
+    def t(self, name):
+        """Transposed bf16 copy [in, out] of a trainable matrix (None when not kept)."""
+        return self.wt.get(name)
+
+    def refresh_transposed(self):
+        for name, wt in self.wt.items():
+            K.transpose(self[name], wt)
+
     def zero_grad(self):
         self.grad.zero_()
 
     def adamw(self, lr: float, wd: float = 0.1, gscale: float = 1.0):
         self.step += 1
         K.adamw(self.master, self.grad, self.m, self.v, self.w, lr, self.step, wd=wd, gscale=gscale)
+        self.refresh_transposed()
 
 
 def rope_table(max_pos: int, head_dim: int, base: float, device) -> torch.Tensor:
@@ -219,23 +236,23 @@ class Transformer:
         hf, rf, yf = ctx["final"]
         if dlogits is not None:
             hw = "embed" if s.tied else "head"
-            dyf = D.linear_dgrad(dlogits, p[hw])
+            dyf = D.linear_dgrad(dlogits, p[hw], wt=p.t(hw))
             D.linear_wgrad(dlogits, yf, p.g(hw))
         dh_ = torch.empty(T, s.d, device=dev, dtype=bf)
         K.rmsnorm_bwd(dyf, hf, p["lnf"], rf, None, dh_, p.g("lnf"))
         for i in reversed(range(s.layers)):
             h1, r1, y1, qkv, o, lse, h2, r2, y2, gu, sw = ctx["layers"][i]
             # MLP
-            dsw = D.linear_dgrad(dh_, p[f"l{i}.wd"])
+            dsw = D.linear_dgrad(dh_, p[f"l{i}.wd"], wt=p.t(f"l{i}.wd"))
             D.linear_wgrad(dh_, sw, p.g(f"l{i}.wd"))
             dgu = torch.empty_like(gu)
             K.swiglu_bwd(dsw, gu, dgu)
             D.linear_wgrad(dgu, y2, p.g(f"l{i}.wgu"))
-            dy2 = D.linear_dgrad(dgu, p[f"l{i}.wgu"])
+            dy2 = D.linear_dgrad(dgu, p[f"l{i}.wgu"], wt=p.t(f"l{i}.wgu"))
             dh2 = torch.empty(T, s.d, device=dev, dtype=bf)
             K.rmsnorm_bwd(dy2, h2, p[f"l{i}.ln2"], r2, dh_, dh2, p.g(f"l{i}.ln2"))
             # attention
-            do = D.linear_dgrad(dh2, p[f"l{i}.wo"])
+            do = D.linear_dgrad(dh2, p[f"l{i}.wo"], wt=p.t(f"l{i}.wo"))
             D.linear_wgrad(dh2, o.view(T, H * dh), p.g(f"l{i}.wo"))
             dqkv = torch.empty_like(qkv)
             q = qkv[:, : H * dh].view(T, H, dh)
@@ -248,7 +265,7 @@ class Transformer:
             A.attn_bwd(do.view(T, H, dh), q, k, v, o, lse, b.cu, b.max_len, s.causal, dq, dk, dv, self.scale,
                        rope=(b.pos, self.cs))
             D.linear_wgrad(dqkv, y1, p.g(f"l{i}.wqkv"))
-            dy1 = D.linear_dgrad(dqkv, p[f"l{i}.wqkv"])
+            dy1 = D.linear_dgrad(dqkv, p[f"l{i}.wqkv"], wt=p.t(f"l{i}.wqkv"))
             dh1 = torch.empty(T, s.d, device=dev, dtype=bf)
             K.rmsnorm_bwd(dy1, h1, p[f"l{i}.ln1"], r1, dh2, dh1, p.g(f"l{i}.ln1"))
             dh_ = dh1

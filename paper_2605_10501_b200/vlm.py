@@ -108,7 +108,7 @@ class ViTSection:
     def backward(self, demb: torch.Tensor, st) -> None:
         dev, s = self.device, self.s
         D.linear_wgrad(demb, st["merged"], self.p.g("proj_w"))
-        dmerged = D.linear_dgrad(demb, self.p["proj_w"]).view(-1, s.d)
+        dmerged = D.linear_dgrad(demb, self.p["proj_w"], wt=self.p.t("proj_w")).view(-1, s.d)
         dyf = torch.empty_like(dmerged)
         # un-merge: a permutation, so the scatter with swapped indices is its own inverse
         K.scatter_rows(dmerged, dyf, torch.arange(st["src"].numel(), device=dev, dtype=torch.int32), st["src"])

@@ -8,7 +8,7 @@ import torch
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2605_10501_b200 import attention as A  # noqa: E402
 
-nseq, L, H, Hk, dh = 4, 2048, 32, 4, 64
+nseq, L, H, Hk, dh = 4, 2048, int(sys.argv[1]) if len(sys.argv) > 1 else 32, int(sys.argv[2]) if len(sys.argv) > 2 else 4, 64
 T = nseq * L
 cu = torch.arange(0, T + 1, L, dtype=torch.int32, device="cuda")
 q = torch.randn(T, H, dh, device="cuda").bfloat16()

@@ -116,3 +116,39 @@ def test_fused_epilogues_rope_swiglu():
     gi = R.gate_index(F, "cuda")
     sref = torch.nn.functional.silu(gref[:, gi]) * gref[:, gi + 32]
     assert _rel(s, sref) < 2e-2
+
+
+@pytest.mark.parametrize("M,N,K", [(8192, 768, 768), (8192, 768, 3072), (1000, 768, 2304), (520, 200, 96)])
+@pytest.mark.parametrize("bn", ["auto", "192"])
+def test_k_major_dgrad_and_192_tiles(M, N, K, bn, monkeypatch):
+    """dgrad through the transposed (K-major) weight copy; 256 x 192 CTA-pair tiles (auto choice
+    for 768-wide outputs, forced for the other shapes incl. ragged M/N)."""
+    from paper_2605_10501_b200 import dense, kernels
+
+    if bn != "auto":
+        monkeypatch.setenv("MAESTRO_GEMM_BN", bn)
+    torch.manual_seed(M + 3 * N + K)
+    w = torch.randn(K, N, device="cuda").bfloat16()  # layer weight [out=K, in=N]
+    wt = torch.empty(N, K, device="cuda", dtype=torch.bfloat16)
+    kernels.transpose(w, wt)
+    torch.cuda.synchronize()
+    assert torch.equal(wt, w.t())
+    dy = torch.randn(M, K, device="cuda").bfloat16()
+    ref = dy.float() @ w.float()
+    assert _rel(dense.linear_dgrad(dy, w, wt=wt), ref) < 8e-3
+    x = torch.randn(M, K, device="cuda").bfloat16()
+    assert _rel(dense.linear_fwd(x, wt), x.float() @ w.float()) < 8e-3
+    acc = torch.randn(M, N, device="cuda")
+    ref2 = acc + x.float() @ w.float()
+    dense.gemm(x, wt, acc, M, N, K, False, False, dense.EPI_F32_ACC)
+    assert _rel(acc, ref2) < 1e-4
+
+
+def test_transpose_ragged():
+    from paper_2605_10501_b200 import kernels
+
+    src = torch.randn(200, 72, device="cuda").bfloat16()
+    dst = torch.zeros(72, 200, device="cuda", dtype=torch.bfloat16)
+    kernels.transpose(src, dst)
+    torch.cuda.synchronize()
+    assert torch.equal(dst, src.t())
