@@ -25,7 +25,7 @@ constexpr int DH = 64;
 constexpr int BQ = 128, BKV = 128, KV_STAGES = 3;
 constexpr int TILE_BYTES = 128 * DH * 2;  // 16 KB (128 rows x 128 B)
 constexpr int P_BYTES = BQ * BKV * 2;     // 32 KB (two 64-col chunks)
-constexpr int FWD_THREADS = 192;
+constexpr int FWD_THREADS = 320;  // w0 TMA, w1 MMA, w2-9 softmax (2 per lane quadrant)
 constexpr float LOG2E_F = 1.4426950408889634f;
 constexpr float LN2_F = 0.6931471805599453f;
 
@@ -56,6 +56,8 @@ __global__ void attn_tiles_kernel(const int32_t* __restrict__ cu, int nseq, int2
   if (threadIdx.x == 0) *count = s_n;
 }
 
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
+
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -72,13 +74,16 @@ __device__ __forceinline__ uint32_t p_offset(int r, int c) {
 // order.  All pipeline counters run across items: K/V stream through the ring, S alternates
 // between two TMEM buffers by global tile index, Q and O are double-buffered by item index,
 // so the next item's Q load, first S MMAs and softmax overlap the current item's epilogue.
-// TMEM: S0 [0,128) S1 [128,256) O0 [256,320) O1 [320,384).
+// TMEM: S0 [0,128) S1 [128,256), O (item parity 0) [256,384), O (parity 1) [384,512); each O is
+// two 64-column accumulators O_a (keys 0-63 of every tile) and O_b (keys 64-127).
 struct FwdSmemP {
   static constexpr int Q = 0;                                  // 2 x 16 KB (by item parity)
   static constexpr int K = Q + 2 * TILE_BYTES;
   static constexpr int V = K + KV_STAGES * TILE_BYTES;
   static constexpr int P = V + KV_STAGES * TILE_BYTES;         // 2 x 32 KB (by tile parity)
-  static constexpr int BAR = P + 2 * P_BYTES;
+  static constexpr int XMAX = P + 2 * P_BYTES;                 // [2 items][2 halves][128] row maxima
+  static constexpr int XSUM = XMAX + 2 * 2 * 128 * 4;          // [2 items][2 halves][128] row sums
+  static constexpr int BAR = XSUM + 2 * 2 * 128 * 4;
   static constexpr int TOTAL = BAR + 256;
 };
 
@@ -140,11 +145,11 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       mbar_init(&q_full[b], 1);
       mbar_init(&q_empty[b], 1);
       mbar_init(&s_full[b], 1);
-      mbar_init(&s_empty[b], 128);
-      mbar_init(&p_full[b], 128);
+      mbar_init(&s_empty[b], 256);
+      mbar_init(&p_full[b], 256);
       mbar_init(&p_empty[b], 1);
       mbar_init(&o_full[b], 1);
-      mbar_init(&o_empty[b], 128);
+      mbar_init(&o_empty[b], 256);
     }
     for (int s = 0; s < KV_STAGES; ++s) {
       mbar_init(&k_full[s], 1);
@@ -194,10 +199,13 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
         tc_fence_after();
         const uint32_t p_base = smem_u32(sm + FwdSmemP::P + pb * P_BYTES);
         const uint32_t v_base = smem_u32(sm + FwdSmemP::V + (gp % KV_STAGES) * TILE_BYTES);
+        // keys [0,64) accumulate into O_a, keys [64,128) into O_b: each softmax half keeps its own
+        // running max, so the halves never synchronise inside the KV loop
 #pragma unroll
         for (int kk = 0; kk < BKV / 16; ++kk)
-          umma_bf16(tmem + 256 + ob * DH, smem_desc_sw128(p_base + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
-                    smem_desc_sw128(v_base + kk * 2048, 8192, 1024), idesc_o, (ip > 0 || kk > 0) ? 1u : 0u);
+          umma_bf16(tmem + 256 + ob * 2 * DH + (kk >> 2) * DH,
+                    smem_desc_sw128(p_base + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                    smem_desc_sw128(v_base + kk * 2048, 8192, 1024), idesc_o, (ip > 0 || (kk & 3) > 0) ? 1u : 0u);
         umma_commit(&v_empty[gp % KV_STAGES]);
         umma_commit(&p_empty[pb]);
       };
@@ -242,10 +250,18 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       flush();
     }
   } else {
+    // Two warps per TMEM lane quadrant split the 128 key columns of a tile (half 0: [0,64),
+    // half 1: [64,128)).  Each half runs its own online softmax (max, sum, lazy rescale) into its
+    // own O accumulator; the halves combine once per item in the epilogue (named barrier per
+    // quadrant pair), each normalising and storing 32 of the 64 output columns.
     const int q = warp & 3;
+    const int half = (warp - 2) >> 2;
     const int r = q * 32 + lane;
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    const int pair_bar = 2 + q;
     unsigned char* pbuf = sm + FwdSmemP::P;
+    float* xmax = reinterpret_cast<float*>(sm + FwdSmemP::XMAX);
+    float* xsum = reinterpret_cast<float*>(sm + FwdSmemP::XSUM);
     int g = 0, j = 0;
     for (int w = snake_item(0); w < n_items; w = snake_item(j + 1), ++j) {
       const FwdItem it = fwd_item<CAUSAL>(w, H, Hk, cu, tiles);
@@ -256,32 +272,32 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
         const int b = g & 1;
         mbar_wait(&s_full[b], (g >> 1) & 1);
         tc_fence_after();
-        float s[BKV];
+        float s[64];
         {
-          uint32_t raw[BKV / 32][32];
-#pragma unroll
-          for (int c = 0; c < BKV / 32; ++c) tmem_ld_32x32b_x32(tmem + lane_base + b * BKV + c * 32, raw[c]);
+          uint32_t raw[2][32];
+          tmem_ld_32x32b_x32(tmem + lane_base + b * BKV + half * 64, raw[0]);
+          tmem_ld_32x32b_x32(tmem + lane_base + b * BKV + half * 64 + 32, raw[1]);
           tmem_ld_wait();
 #pragma unroll
-          for (int c = 0; c < BKV / 32; ++c)
+          for (int c = 0; c < 2; ++c)
 #pragma unroll
             for (int jj = 0; jj < 32; ++jj) s[c * 32 + jj] = __uint_as_float(raw[c][jj]);
         }
         tc_fence_before();
         mbar_arrive(&s_empty[b]);
-        const int kv0 = i * BKV;
-        const bool need_mask = (CAUSAL && kv0 + BKV - 1 > it.q0) || (kv0 + BKV > it.L);
+        const int kv0 = i * BKV + half * 64;
+        const bool need_mask = (CAUSAL && kv0 + 63 > it.q0) || (kv0 + 64 > it.L);
         float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
         if (need_mask) {
 #pragma unroll
-          for (int c = 0; c < BKV; ++c) {
+          for (int c = 0; c < 64; ++c) {
             const int kv = kv0 + c;
             if ((CAUSAL && kv > qpos) || kv >= it.L) s[c] = -INFINITY;
             mx4[c & 3] = fmaxf(mx4[c & 3], s[c]);
           }
         } else {
 #pragma unroll
-          for (int c = 0; c < BKV; ++c) mx4[c & 3] = fmaxf(mx4[c & 3], s[c]);
+          for (int c = 0; c < 64; ++c) mx4[c & 3] = fmaxf(mx4[c & 3], s[c]);
         }
         const float m_new = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * scale2;
         bool rescale = false;
@@ -292,9 +308,9 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
           rescale = i > 0;
         }
         float sum4[4] = {0.f, 0.f, 0.f, 0.f};
-        const float neg_m = -m;
+        const float neg_m = m == -INFINITY ? 0.f : -m;  // half fully masked so far: P = 0
 #pragma unroll
-        for (int c = 0; c < BKV; ++c) {
+        for (int c = 0; c < 64; ++c) {
           s[c] = ex2(fmaf(s[c], scale2, neg_m));
           sum4[c & 3] += s[c];
         }
@@ -304,51 +320,62 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
           mbar_wait(&p_empty[(g - 1) & 1], ((g - 1) >> 1) & 1);  // PV_{g-1} retired: O is final
           tc_fence_after();
 #pragma unroll
-          for (int c = 0; c < DH / 32; ++c) {
+          for (int c = 0; c < 2; ++c) {
             uint32_t rr[32];
-            tmem_ld_32x32b_x32(tmem + lane_base + 256 + ob * DH + c * 32, rr);
+            tmem_ld_32x32b_x32(tmem + lane_base + 256 + ob * 2 * DH + half * DH + c * 32, rr);
             tmem_ld_wait();
 #pragma unroll
             for (int jj = 0; jj < 32; ++jj) rr[jj] = __float_as_uint(__uint_as_float(rr[jj]) * alpha);
-            tmem_st_32x32b_x32(tmem + lane_base + 256 + ob * DH + c * 32, rr);
+            tmem_st_32x32b_x32(tmem + lane_base + 256 + ob * 2 * DH + half * DH + c * 32, rr);
           }
           tmem_st_wait();
         }
         unsigned char* pb = pbuf + b * P_BYTES;
 #pragma unroll
-        for (int u = 0; u < BKV / 8; ++u) {
+        for (int u = 0; u < 8; ++u) {
           uint4 v;
           v.x = pack_bf16(s[8 * u + 0], s[8 * u + 1]);
           v.y = pack_bf16(s[8 * u + 2], s[8 * u + 3]);
           v.z = pack_bf16(s[8 * u + 4], s[8 * u + 5]);
           v.w = pack_bf16(s[8 * u + 6], s[8 * u + 7]);
-          *reinterpret_cast<uint4*>(pb + p_offset(r, 8 * u)) = v;
+          *reinterpret_cast<uint4*>(pb + p_offset(r, half * 64 + 8 * u)) = v;
         }
         fence_proxy_async_smem();
         tc_fence_before();
         mbar_arrive(&p_full[b]);
       }
-      // epilogue of item j (overlaps the MMA warp starting item j+1)
+      // epilogue of item j (overlaps the MMA warp starting item j+1): exchange (m, l) with the
+      // partner half, O = (O_a 2^(m_a - M) + O_b 2^(m_b - M)) / l for this half's 32 columns
+      float* xm = xmax + ob * 256;  // by item parity: the partner reads it before the next item's barrier
+      float* xs = xsum + ob * 256;
+      xm[half * 128 + r] = m;
+      xs[half * 128 + r] = l;
       mbar_wait(&o_full[ob], (j >> 1) & 1);
       tc_fence_after();
-      const float inv_l = 1.f / l;
-      uint32_t raw[DH / 32][32];
-#pragma unroll
-      for (int c = 0; c < DH / 32; ++c) tmem_ld_32x32b_x32(tmem + lane_base + 256 + ob * DH + c * 32, raw[c]);
+      uint32_t ra[32], rb[32];
+      tmem_ld_32x32b_x32(tmem + lane_base + 256 + ob * 2 * DH + half * 32, ra);
+      tmem_ld_32x32b_x32(tmem + lane_base + 256 + ob * 2 * DH + DH + half * 32, rb);
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(&o_empty[ob]);
+      named_bar(pair_bar, 64);
+      const float m_o = xm[(half ^ 1) * 128 + r], l_o = xs[(half ^ 1) * 128 + r];
+      const float ma = half == 0 ? m : m_o, mb = half == 0 ? m_o : m;
+      const float la = half == 0 ? l : l_o, lb = half == 0 ? l_o : l;
+      const float M = fmaxf(ma, mb);
+      const float sa = ma == -INFINITY ? 0.f : ex2(ma - M), sb = mb == -INFINITY ? 0.f : ex2(mb - M);
+      const float l_all = la * sa + lb * sb;
       if (qpos < it.L) {
-        uint32_t o[DH / 2];
+        const float fa = sa / l_all, fb = sb / l_all;
+        uint32_t o[16];
 #pragma unroll
-        for (int c = 0; c < DH / 32; ++c)
+        for (int jj = 0; jj < 16; ++jj)
+          o[jj] = pack_bf16(__uint_as_float(ra[2 * jj]) * fa + __uint_as_float(rb[2 * jj]) * fb,
+                            __uint_as_float(ra[2 * jj + 1]) * fa + __uint_as_float(rb[2 * jj + 1]) * fb);
+        uint4* dst = reinterpret_cast<uint4*>(out + (size_t)(it.s0 + qpos) * ldo + it.h * DH + half * 32);
 #pragma unroll
-          for (int jj = 0; jj < 16; ++jj)
-            o[c * 16 + jj] = pack_bf16(__uint_as_float(raw[c][2 * jj]) * inv_l, __uint_as_float(raw[c][2 * jj + 1]) * inv_l);
-        uint4* dst = reinterpret_cast<uint4*>(out + (size_t)(it.s0 + qpos) * ldo + it.h * DH);
-#pragma unroll
-        for (int u = 0; u < DH / 8; ++u) dst[u] = make_uint4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);
-        lse[(size_t)it.h * T + it.s0 + qpos] = (m + log2f(l)) * LN2_F;
+        for (int u = 0; u < 4; ++u) dst[u] = make_uint4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);
+        if (half == 0) lse[(size_t)it.h * T + it.s0 + qpos] = (M + log2f(l_all)) * LN2_F;
       }
     }
   }
@@ -392,7 +419,6 @@ __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float 
                : "memory");
 }
 
-__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
 
 struct BwdItem {
   int kv0, hk, s0, L, qt_first, n_q, n_it;
