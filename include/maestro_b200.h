@@ -165,15 +165,21 @@ int maestro_gemm_bf16_swiglu(const void* A, const void* B, void* C, int32_t M, i
 /* K8 -- varlen GQA attention, head_dim 64: q [T,H,64], k/v [T,Hk,64] (pitched), cu [nseq+1];
  * out [T,H,64] bf16, lse [H,T] fp32 (natural LSE of the scaled scores). */
 int64_t maestro_attn_workspace(int32_t T, int32_t nseq);
+/* Per-micro-batch work plan (query-tile and KV-tile lists, heavy-first) built once from cu and
+ * passed to every layer's attn_fwd / attn_bwd; plan == NULL builds it per call in the workspace. */
+int64_t maestro_attn_plan_size(int32_t T, int32_t nseq);
+int maestro_attn_plan(const int32_t* cu, int32_t nseq, int32_t T, void* plan, void* stream);
 int maestro_attn_fwd(const void* q, const void* k, const void* v, const int32_t* cu, int32_t nseq, int32_t T,
                      int32_t H, int32_t Hk, int32_t head_dim, int32_t ldq, int32_t ldk, int32_t ldv, void* out,
-                     int32_t ldo, float* lse, float softmax_scale, int32_t causal, void* workspace, void* stream);
+                     int32_t ldo, float* lse, float softmax_scale, int32_t causal, const void* plan, void* workspace,
+                     void* stream);
 int64_t maestro_attn_bwd_workspace(int32_t T, int32_t nseq, int32_t H);
 int maestro_attn_bwd(const void* dout, int32_t lddo, const void* q, const void* k, const void* v, const void* o,
                      int32_t ldo, const float* lse, const int32_t* cu, int32_t nseq, int32_t T, int32_t H,
                      int32_t Hk, int32_t head_dim, int32_t ldq, int32_t ldk, int32_t ldv, void* dq, int32_t lddq,
                      void* dk, int32_t lddk, void* dv, int32_t lddv, float softmax_scale, int32_t causal,
-                     const int32_t* rope_pos, const void* rope_cos_sin, void* workspace, void* stream);
+                     const int32_t* rope_pos, const void* rope_cos_sin, const void* plan, void* workspace,
+                     void* stream);
 /* (rope_pos/rope_cos_sin non-null: dQ and dK are returned through the inverse RoPE rotation,
  * i.e. w.r.t. the pre-rotation projections.) */
 

@@ -897,17 +897,31 @@ MAESTRO_API int64_t maestro_attn_workspace(int32_t T, int32_t nseq) {
 
 // q [T, H, 64] (row pitch ldq elements), k/v [T, Hk, 64] (pitch ldk/ldv), cu [nseq+1];
 // out [T, H, 64] (pitch ldo), lse [H, T] fp32 (natural log-sum-exp of the scaled scores).
+// Plan = [query-tile list | count] [KV-tile list | count], each maestro_attn_workspace bytes.
+MAESTRO_API int64_t maestro_attn_plan_size(int32_t T, int32_t nseq) { return 2 * maestro_attn_workspace(T, nseq); }
+
+MAESTRO_API int maestro_attn_plan(const int32_t* cu, int32_t nseq, int32_t T, void* plan, void* stream) {
+  if (T <= 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int max_tiles = (T + BQ - 1) / BQ + nseq;
+  int2* fw = reinterpret_cast<int2*>(plan);
+  int2* bw = reinterpret_cast<int2*>(reinterpret_cast<unsigned char*>(plan) + maestro_attn_workspace(T, nseq));
+  attn_tiles_kernel<<<1, 1024, 0, st>>>(cu, nseq, fw, reinterpret_cast<int*>(fw + max_tiles));
+  attn_kv_tiles_kernel<<<1, 1024, 0, st>>>(cu, nseq, bw, reinterpret_cast<int*>(bw + max_tiles));
+  return launch_status();
+}
+
 MAESTRO_API int maestro_attn_fwd(const void* q, const void* k, const void* v, const int32_t* cu, int32_t nseq,
                                  int32_t T, int32_t H, int32_t Hk, int32_t head_dim, int32_t ldq, int32_t ldk,
                                  int32_t ldv, void* out, int32_t ldo, float* lse, float softmax_scale, int32_t causal,
-                                 void* workspace, void* stream) {
+                                 const void* plan, void* workspace, void* stream) {
   if (T <= 0) return 0;
   if (head_dim != DH || H % Hk) return (int)cudaErrorInvalidValue;
   cudaStream_t st = (cudaStream_t)stream;
-  int2* tiles = reinterpret_cast<int2*>(workspace);
   const int max_tiles = (T + BQ - 1) / BQ + nseq;
+  int2* tiles = reinterpret_cast<int2*>(plan != nullptr ? const_cast<void*>(plan) : workspace);
   int* count = reinterpret_cast<int*>(tiles + max_tiles);
-  attn_tiles_kernel<<<1, 1024, 0, st>>>(cu, nseq, tiles, count);
+  if (plan == nullptr) attn_tiles_kernel<<<1, 1024, 0, st>>>(cu, nseq, tiles, count);
   CUtensorMap mq, mk, mv;
   bool ok = make_map_2d(&mq, q, (uint64_t)H * DH, T, ldq, 64, 128);
   ok = ok && make_map_2d(&mk, k, (uint64_t)Hk * DH, T, ldk, 64, 128);
@@ -939,19 +953,22 @@ MAESTRO_API int maestro_attn_bwd(const void* dout, int32_t lddo, const void* q, 
                                  int32_t T, int32_t H, int32_t Hk, int32_t head_dim, int32_t ldq, int32_t ldk,
                                  int32_t ldv, void* dq, int32_t lddq, void* dk, int32_t lddk, void* dv, int32_t lddv,
                                  float softmax_scale, int32_t causal, const int32_t* rope_pos, const void* rope_cs,
-                                 void* workspace, void* stream) {
+                                 const void* plan, void* workspace, void* stream) {
   if (T <= 0) return 0;
   if (head_dim != DH || H % Hk) return (int)cudaErrorInvalidValue;
   cudaStream_t st = (cudaStream_t)stream;
   unsigned char* w = reinterpret_cast<unsigned char*>(workspace);
-  int2* tiles = reinterpret_cast<int2*>(w);
   const int max_tiles = (T + BKV - 1) / BKV + nseq;
+  int2* tiles = plan != nullptr
+                    ? reinterpret_cast<int2*>(const_cast<unsigned char*>(reinterpret_cast<const unsigned char*>(plan)) +
+                                              maestro_attn_workspace(T, nseq))
+                    : reinterpret_cast<int2*>(w);
   int* count = reinterpret_cast<int*>(tiles + max_tiles);
   const size_t off_d = ((size_t)maestro_attn_workspace(T, nseq) + 255) / 256 * 256;
   float* Dvec = reinterpret_cast<float*>(w + off_d);
   const size_t off_acc = (off_d + (size_t)4 * H * T + 255) / 256 * 256;
   float* dq_acc = reinterpret_cast<float*>(w + off_acc);
-  attn_kv_tiles_kernel<<<1, 1024, 0, st>>>(cu, nseq, tiles, count);
+  if (plan == nullptr) attn_kv_tiles_kernel<<<1, 1024, 0, st>>>(cu, nseq, tiles, count);
   const long long warps = (long long)T * H;
   attn_bwd_pre_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(
       (const __nv_bfloat16*)o, ldo, (const __nv_bfloat16*)dout, lddo, Dvec, dq_acc, T, H);

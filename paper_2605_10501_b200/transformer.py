@@ -185,7 +185,7 @@ class Transformer:
         if x0 is None:
             x0 = torch.empty(T, s.d, device=dev, dtype=bf)
             K.embed(p["embed"], b.ids, x0)
-        ctx = {"b": b, "layers": [], "x0": x0}
+        ctx = {"b": b, "layers": [], "x0": x0, "plan": A.plan(b.cu, T)}  # tile lists, once per micro-batch
         x, a = x0, None
         H, Hk, dh = s.heads, s.kv_heads, s.head_dim
         for i in range(s.layers):
@@ -199,7 +199,7 @@ class Transformer:
             k = qkv[:, H * dh: (H + Hk) * dh].view(T, Hk, dh)
             v = qkv[:, (H + Hk) * dh:].view(T, Hk, dh)
             o = torch.empty(T, H, dh, device=dev, dtype=bf)
-            lse = A.attn_fwd(q, k, v, b.cu, b.max_len, s.causal, o, self.scale)
+            lse = A.attn_fwd(q, k, v, b.cu, b.max_len, s.causal, o, self.scale, plan=ctx["plan"])
             ao = D.linear_fwd(o.view(T, H * dh), p[f"l{i}.wo"])
             h2 = torch.empty(T, s.d, device=dev, dtype=bf)
             y2 = torch.empty(T, s.d, device=dev, dtype=bf)
@@ -263,7 +263,7 @@ class Transformer:
             dv = dqkv[:, (H + Hk) * dh:].view(T, Hk, dh)
             # inverse RoPE fused into the attention backward's dQ / dK stores
             A.attn_bwd(do.view(T, H, dh), q, k, v, o, lse, b.cu, b.max_len, s.causal, dq, dk, dv, self.scale,
-                       rope=(b.pos, self.cs))
+                       rope=(b.pos, self.cs), plan=ctx["plan"])
             D.linear_wgrad(dqkv, y1, p.g(f"l{i}.wqkv"))
             dy1 = D.linear_dgrad(dqkv, p[f"l{i}.wqkv"], wt=p.t(f"l{i}.wqkv"))
             dh1 = torch.empty(T, s.d, device=dev, dtype=bf)

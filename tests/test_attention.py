@@ -37,8 +37,9 @@ CASES = [
 ]
 
 
+@pytest.mark.parametrize("use_plan", [False, True])
 @pytest.mark.parametrize("lens,H,Hk,causal", CASES)
-def test_attention_fwd_bwd(lens, H, Hk, causal):
+def test_attention_fwd_bwd(lens, H, Hk, causal, use_plan):
     from paper_2605_10501_b200 import attention as A
 
     torch.manual_seed(sum(lens) + H)
@@ -53,7 +54,8 @@ def test_attention_fwd_bwd(lens, H, Hk, causal):
     v = qkv[:, (H + Hk) * dh: (H + 2 * Hk) * dh].view(T, Hk, dh)
     scale = 1.0 / math.sqrt(dh)
     o = torch.empty(T, H, dh, device="cuda", dtype=torch.bfloat16)
-    lse = A.attn_fwd(q, k, v, cu, max(lens), causal, o, scale)
+    plan = A.plan(cu, T) if use_plan else None  # per-micro-batch tile lists vs built per call
+    lse = A.attn_fwd(q, k, v, cu, max(lens), causal, o, scale, plan=plan)
     qf, kf, vf = (x.float().clone().requires_grad_(True) for x in (q, k, v))
     ref = R.varlen_attention(qf, kf, vf, cu, causal, scale)
     assert rel(o, ref) < 2e-2
@@ -64,7 +66,7 @@ def test_attention_fwd_bwd(lens, H, Hk, causal):
     dq = dqkv[:, : H * dh].view(T, H, dh)
     dk = dqkv[:, H * dh: (H + Hk) * dh].view(T, Hk, dh)
     dv = dqkv[:, (H + Hk) * dh: (H + 2 * Hk) * dh].view(T, Hk, dh)
-    A.attn_bwd(do, q, k, v, o, lse, cu, max(lens), causal, dq, dk, dv, scale)
+    A.attn_bwd(do, q, k, v, o, lse, cu, max(lens), causal, dq, dk, dv, scale, plan=plan)
     assert rel(dv, vf.grad) < 2e-2
     assert rel(dk, kf.grad) < 3e-2
     assert rel(dq, qf.grad) < 3e-2
