@@ -157,6 +157,10 @@ int maestro_gemm_bf16_rope(const void* A, const void* B, void* C, int32_t M, int
                            int32_t ldb, int32_t ldc, const int32_t* pos, const void* cos_sin, int32_t rope_cols,
                            void* stream);
 
+/* K7 + fused residual epilogue: C = R + A B^T (bf16; the sum is formed in fp32 and rounded
+ * once).  Used by the attention-output and down projections to write the residual stream. */
+int maestro_gemm_bf16_residual(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K, int32_t lda,
+                               int32_t ldb, int32_t ldc, const void* R, int32_t ldr, void* stream);
 /* K7 + fused SwiGLU epilogue: C = A B^T is the gate/up activation with gate/up rows of B
  * interleaved in 32-row blocks ([g_0..g_31, u_0..u_31, g_32..]); S[m, f] = silu(g_f) * u_f. */
 int maestro_gemm_bf16_swiglu(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K, int32_t lda,

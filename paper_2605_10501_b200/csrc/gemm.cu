@@ -287,7 +287,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                  const __grid_constant__ CUtensorMap map_c, void* C, int M, int N, int K, int ldc, int splits,
                  const int32_t* __restrict__ rope_pos, const float2* __restrict__ rope_cs, int rope_cols,
-                 __nv_bfloat16* __restrict__ swiglu_out, int ld_swiglu) {
+                 __nv_bfloat16* __restrict__ swiglu_out, int ld_swiglu, const __nv_bfloat16* __restrict__ resid,
+                 int ldr) {
   using CF = Cfg2<BN2>;
   constexpr int STAGES = CF::STAGES, B_BYTES = CF::B_BYTES, STAGE_BYTES = CF::STAGE_BYTES, B_ROWS = CF::B_ROWS;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -428,9 +429,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         for (int c = 0; c < BN2; c += 64, ++chunk_ctr) {
           unsigned char* buf = sC + (chunk_ctr & 1) * CF::EPI_BUF;
           uint32_t r0[32], r1[32];
+          uint4 res[8];
+          const bool has_res = resid != nullptr && row < M;
+          if (has_res) {
+            // fused residual add (h = x + A B^T): this row's 64 residual values, loaded before the
+            // TMEM read so their latency overlaps it
+            const __nv_bfloat16* rp = resid + (size_t)row * ldr + n0 + c;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              res[u] = n0 + c + 8 * u < N ? *reinterpret_cast<const uint4*>(rp + 8 * u) : make_uint4(0, 0, 0, 0);
+          }
           tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + as * BN2 + c, r0);
           tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + as * BN2 + c + 32, r1);
           tmem_ld_wait();
+          if (has_res) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              uint32_t* dst = u < 4 ? &r0[8 * u] : &r1[8 * (u - 4)];
+              const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&res[u]);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 f = __bfloat1622float2(hv[e]);
+                dst[2 * e] = __float_as_uint(__uint_as_float(dst[2 * e]) + f.x);
+                dst[2 * e + 1] = __float_as_uint(__uint_as_float(dst[2 * e + 1]) + f.y);
+              }
+            }
+          }
           if (rope_cols > 0 && n0 + c < rope_cols && row < M) {
             // fused RoPE (rotate-half): this 64-column chunk is exactly one head of Q or K;
             // r0 holds dims [0,32), r1 dims [32,64) of the row
@@ -531,14 +555,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 template <int BN2, bool A_MN, bool B_MN, int EPI>
 int launch2(const CUtensorMap& ma, const CUtensorMap& mbm, const CUtensorMap& mc, void* C, int M, int N, int K,
             int ldc, int splits, cudaStream_t st, const int32_t* rope_pos = nullptr, const float2* rope_cs = nullptr,
-            int rope_cols = 0, __nv_bfloat16* swiglu_out = nullptr, int ld_swiglu = 0) {
+            int rope_cols = 0, __nv_bfloat16* swiglu_out = nullptr, int ld_swiglu = 0,
+            const __nv_bfloat16* resid = nullptr, int ldr = 0) {
   constexpr int SMEM = Cfg2<BN2>::SMEM;
   if (ensure_smem<gemm2_kernel<BN2, A_MN, B_MN, EPI>>(SMEM)) return launch_status();
   const int units = ((M + 255) / 256) * ((N + BN2 - 1) / BN2) * splits;
   const int pairs = units < num_sms() / 2 ? units : num_sms() / 2;
   gemm2_kernel<BN2, A_MN, B_MN, EPI><<<2 * pairs, THREADS, SMEM, st>>>(ma, mbm, mc, C, M, N, K, ldc, splits,
                                                                         rope_pos, rope_cs, rope_cols, swiglu_out,
-                                                                        ld_swiglu);
+                                                                        ld_swiglu, resid, ldr);
   return launch_status();
 }
 
@@ -574,7 +599,7 @@ using namespace mb;
 static int gemm_impl(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K, int32_t lda,
                      int32_t ldb, int32_t ldc, int32_t a_mn, int32_t b_mn, int32_t epi, void* stream,
                      const int32_t* rope_pos, const float2* rope_cs, int rope_cols, void* swiglu_out = nullptr,
-                     int ld_swiglu = 0);
+                     int ld_swiglu = 0, const void* resid = nullptr, int ldr = 0);
 
 MAESTRO_API int maestro_gemm_bf16(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K,
                                   int32_t lda, int32_t ldb, int32_t ldc, int32_t a_mn, int32_t b_mn, int32_t epi,
@@ -593,6 +618,16 @@ MAESTRO_API int maestro_gemm_bf16_rope(const void* A, const void* B, void* C, in
 
 // Gate/up projection with SwiGLU fused into the epilogue: C = A B^T is the interleaved [g|u]
 // activation (gate/up rows of B interleaved in 32-row blocks), S[m, f] = silu(g) * u.
+// Output projection with the residual add fused into the epilogue: C = R + A B^T (bf16, fp32
+// sum rounded once).  Produces the block's residual stream h directly, so the following norm
+// reads h instead of re-reading x and the projection output.
+MAESTRO_API int maestro_gemm_bf16_residual(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K,
+                                           int32_t lda, int32_t ldb, int32_t ldc, const void* R, int32_t ldr,
+                                           void* stream) {
+  if (R == nullptr || (ldr % 8)) return (int)cudaErrorInvalidValue;
+  return gemm_impl(A, B, C, M, N, K, lda, ldb, ldc, 0, 0, 0, stream, nullptr, nullptr, 0, nullptr, 0, R, ldr);
+}
+
 MAESTRO_API int maestro_gemm_bf16_swiglu(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K,
                                          int32_t lda, int32_t ldb, int32_t ldc, void* S, int32_t lds, void* stream) {
   if (N % 64) return (int)cudaErrorInvalidValue;
@@ -602,7 +637,7 @@ MAESTRO_API int maestro_gemm_bf16_swiglu(const void* A, const void* B, void* C, 
 static int gemm_impl(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K, int32_t lda,
                      int32_t ldb, int32_t ldc, int32_t a_mn, int32_t b_mn, int32_t epi, void* stream,
                      const int32_t* rope_pos, const float2* rope_cs, int rope_cols, void* swiglu_out,
-                     int ld_swiglu) {
+                     int ld_swiglu, const void* resid, int ldr) {
   if (M <= 0 || N <= 0 || K <= 0) return (int)cudaErrorInvalidValue;
   if ((lda % 8) || (ldb % 8) || (N % 8) || (ldc % 8)) return (int)cudaErrorInvalidValue;
   const int sms = num_sms();
@@ -659,7 +694,7 @@ static int gemm_impl(const void* A, const void* B, void* C, int32_t M, int32_t N
     if (!ok) return (int)cudaErrorInvalidValue;
 #define MB_GEMM2_LAUNCH(W, AM, BMN, E)                                                                  \
   launch2<W, AM, BMN, E>(ma, mbm, mc, C, M, N, K, ldc, splits, st, rope_pos, rope_cs, rope_cols,         \
-                         (__nv_bfloat16*)swiglu_out, ld_swiglu)
+                         (__nv_bfloat16*)swiglu_out, ld_swiglu, (const __nv_bfloat16*)resid, ldr)
 #define MB_GEMM2_CASE(AM, BMN, E)                                                                    \
   if (a_mn == AM && b_mn == BMN && epi_k == E)                                                       \
     return bn2 == 256 ? MB_GEMM2_LAUNCH(256, AM, BMN, E) : MB_GEMM2_LAUNCH(128, AM, BMN, E);

@@ -28,6 +28,7 @@ def _lib():
             "maestro_gemm_bf16": ([P, P, P, I32, I32, I32, I32, I32, I32, I32, I32, I32, P], ctypes.c_int),
             "maestro_gemm_bf16_rope": ([P, P, P, I32, I32, I32, I32, I32, I32, P, P, I32, P], ctypes.c_int),
             "maestro_gemm_bf16_swiglu": ([P, P, P, I32, I32, I32, I32, I32, I32, P, I32, P], ctypes.c_int),
+            "maestro_gemm_bf16_residual": ([P, P, P, I32, I32, I32, I32, I32, I32, P, I32, P], ctypes.c_int),
         })
         _bound = True
     return L
@@ -78,6 +79,26 @@ def linear_fwd_rope(x: torch.Tensor, w: torch.Tensor, pos: torch.Tensor, cos_sin
     rc = _lib().maestro_gemm_bf16_rope(N.ptr(x), N.ptr(w), N.ptr(out), T, Nn, K, x.stride(0), w.stride(0),
                                        out.stride(0), N.ptr(pos), N.ptr(cos_sin), rope_cols, N.stream_ptr())
     N.check(rc, "gemm_bf16_rope")
+    if rec is not None:
+        e1.record()
+        rec.append((2.0 * T * Nn * K, e0, e1))
+    return out
+
+
+def linear_fwd_residual(x: torch.Tensor, w: torch.Tensor, resid: torch.Tensor,
+                        out: torch.Tensor | None = None) -> torch.Tensor:
+    """h[T, out] = resid + x @ w^T (residual add fused into the GEMM epilogue)."""
+    T, K = x.shape
+    Nn = w.shape[0]
+    if out is None:
+        out = torch.empty(T, Nn, device=x.device, dtype=torch.bfloat16)
+    rec = instrument.gemm_timing
+    if rec is not None:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+    rc = _lib().maestro_gemm_bf16_residual(N.ptr(x), N.ptr(w), N.ptr(out), T, Nn, K, x.stride(0), w.stride(0),
+                                           out.stride(0), N.ptr(resid), resid.stride(0), N.stream_ptr())
+    N.check(rc, "gemm_bf16_residual")
     if rec is not None:
         e1.record()
         rec.append((2.0 * T * Nn * K, e0, e1))

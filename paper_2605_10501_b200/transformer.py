@@ -4,11 +4,11 @@ No autograd and no torch compute ops on the hot path: every FLOP goes through th
 GEMM (dense.py), the attention kernels (attention.py) or the memory-bound kernels
 (kernels.py).  torch only allocates buffers and owns streams.
 
-A block is   h1 = x + a ; y1 = rmsnorm(h1) ; qkv = y1 Wqkv^T ; rope ; o = attn(qkv)
-             h2 = h1 + o Wo^T ; y2 = rmsnorm(h2) ; gu = y2 Wgu^T ; s = silu(g) u ; a' = s Wd^T
+A block is   y1 = rmsnorm(h1) ; qkv = y1 Wqkv^T ; rope ; o = attn(qkv)
+             h2 = h1 + o Wo^T ; y2 = rmsnorm(h2) ; gu = y2 Wgu^T ; s = silu(g) u ; h1' = h2 + s Wd^T
 (Wgu stores gate/up rows interleaved in 32-row blocks so SwiGLU runs in the GEMM epilogue;
-RoPE likewise runs in the QKV GEMM epilogue.)
-with the residual add fused into the following norm.  Parameters of a section live in one
+RoPE likewise runs in the QKV GEMM epilogue, and both residual adds in the epilogues of the
+Wo / Wd projections, so the norms read the residual stream once.)  Parameters of a section live in one
 flat arena (fp32 master, bf16 working copy, fp32 grad, Adam m/v) so the optimizer and the
 gradient all-reduce are single launches over contiguous memory.
 """
@@ -186,13 +186,13 @@ class Transformer:
             x0 = torch.empty(T, s.d, device=dev, dtype=bf)
             K.embed(p["embed"], b.ids, x0)
         ctx = {"b": b, "layers": [], "x0": x0, "plan": A.plan(b.cu, T)}  # tile lists, once per micro-batch
-        x, a = x0, None
+        x = x0  # residual stream entering the block (h1); the residual adds run in GEMM epilogues
         H, Hk, dh = s.heads, s.kv_heads, s.head_dim
         for i in range(s.layers):
-            h1 = torch.empty(T, s.d, device=dev, dtype=bf) if a is not None else x
+            h1 = x
             y1 = torch.empty(T, s.d, device=dev, dtype=bf)
             r1 = torch.empty(T, device=dev, dtype=torch.float32)
-            K.add_rmsnorm(x, a, h1, y1, p[f"l{i}.ln1"], r1, s.eps)
+            K.add_rmsnorm(h1, None, h1, y1, p[f"l{i}.ln1"], r1, s.eps)
             # QKV projection with RoPE fused into the GEMM epilogue (one head per 64-col chunk)
             qkv = D.linear_fwd_rope(y1, p[f"l{i}.wqkv"], b.pos, self.cs, (H + Hk) * dh)
             q = qkv[:, : H * dh].view(T, H, dh)
@@ -200,23 +200,23 @@ class Transformer:
             v = qkv[:, (H + Hk) * dh:].view(T, Hk, dh)
             o = torch.empty(T, H, dh, device=dev, dtype=bf)
             lse = A.attn_fwd(q, k, v, b.cu, b.max_len, s.causal, o, self.scale, plan=ctx["plan"])
-            ao = D.linear_fwd(o.view(T, H * dh), p[f"l{i}.wo"])
-            h2 = torch.empty(T, s.d, device=dev, dtype=bf)
+            # h2 = h1 + o Wo^T (residual add in the epilogue)
+            h2 = D.linear_fwd_residual(o.view(T, H * dh), p[f"l{i}.wo"], h1)
             y2 = torch.empty(T, s.d, device=dev, dtype=bf)
             r2 = torch.empty(T, device=dev, dtype=torch.float32)
-            K.add_rmsnorm(h1, ao, h2, y2, p[f"l{i}.ln2"], r2, s.eps)
+            K.add_rmsnorm(h2, None, h2, y2, p[f"l{i}.ln2"], r2, s.eps)
             # gate/up projection with SwiGLU fused into the epilogue (gate/up rows interleaved
             # in 32-row blocks in wgu)
             sw = torch.empty(T, s.ffn, device=dev, dtype=bf)
             gu = D.linear_fwd_swiglu(y2, p[f"l{i}.wgu"], sw)
-            mo = D.linear_fwd(sw, p[f"l{i}.wd"])
             if save:
                 ctx["layers"].append((h1, r1, y1, qkv, o, lse, h2, r2, y2, gu, sw))
-            x, a = h2, mo
-        hf = torch.empty(T, s.d, device=dev, dtype=bf)
+            # next block's residual stream: h2 + sw Wd^T
+            x = D.linear_fwd_residual(sw, p[f"l{i}.wd"], h2)
+        hf = x
         yf = torch.empty(T, s.d, device=dev, dtype=bf)
         rf = torch.empty(T, device=dev, dtype=torch.float32)
-        K.add_rmsnorm(x, a, hf, yf, p["lnf"], rf, s.eps)
+        K.add_rmsnorm(hf, None, hf, yf, p["lnf"], rf, s.eps)
         ctx["final"] = (hf, rf, yf)
         return yf, ctx
 

@@ -152,3 +152,18 @@ def test_transpose_ragged():
     kernels.transpose(src, dst)
     torch.cuda.synchronize()
     assert torch.equal(dst, src.t())
+
+
+@pytest.mark.parametrize("M,N,K", [(8192, 2048, 2048), (8192, 768, 3072), (1000, 200, 96), (300, 2048, 5632)])
+def test_residual_epilogue(M, N, K):
+    """h = R + A B^T with the add in the epilogue: fp32 sum rounded once (vs fp32 reference)."""
+    from paper_2605_10501_b200 import dense
+
+    torch.manual_seed(M + N + 5)
+    x = torch.randn(M, K, device="cuda").bfloat16()
+    w = (torch.randn(N, K, device="cuda") * 0.05).bfloat16()
+    big = torch.randn(M, N + 64, device="cuda").bfloat16()  # residual as a strided view
+    r = big[:, 32: 32 + N]
+    h = dense.linear_fwd_residual(x, w, r)
+    ref = r.float() + x.float() @ w.float().t()
+    assert _rel(h, ref) < 8e-3
