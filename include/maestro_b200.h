@@ -187,6 +187,12 @@ int maestro_attn_bwd(const void* dout, int32_t lddo, const void* q, const void* 
 /* (rope_pos/rope_cos_sin non-null: dQ and dK are returned through the inverse RoPE rotation,
  * i.e. w.r.t. the pre-rotation projections.) */
 
+/* Reshard data mover (mq.py:163-174, 460-469): dst[box] = src[box] for an N-d box (ndim <= 6,
+ * strides in elements, elem_bytes 1/2/4/8).  Used by apply_plan and Endpoint.pull to gather
+ * fragments into a receiver's shard and by push_tensor to slice a sender's shard. */
+int maestro_box_copy(const void* src, const int64_t* src_strides, void* dst, const int64_t* dst_strides,
+                     const int64_t* shape, int32_t ndim, int32_t elem_bytes, void* stream);
+
 /* K9 -- fused full-vocab KL(softmax(t/tau) || softmax(s/tau)) per token (d_loss[T]) and
  * ds = grad_scale * dKL/ds (bf16, may alias s).  Teacher head colocated per workload.py:471-514. */
 int maestro_kd_loss_fwd_bwd(const void* d_t, const void* d_s, void* d_ds, float* d_loss, int32_t T, int32_t V,

@@ -265,6 +265,12 @@ class KDExecutor:
         if want_loss and loss_acc is not None:
             loss = float(loss_acc.item()) / global_tokens
         t_end.synchronize()
+        if self.student is not None and not self.colocated:
+            got = sorted(self.verify_handoff())  # control headers of this step's pulls
+            if got != list(range(plan["student"]["n_mb"])):
+                from .errors import InconsistentSchedule
+
+                raise InconsistentSchedule("handoff delivered unexpected micro-batches", got=got)
         busy, span = clock.busy_span()
         return StepStats(loss, t_start.elapsed_time(t_end), busy, span)
 
@@ -330,29 +336,59 @@ class KDExecutor:
                 outs[m].record_stream(self.s_stream)
                 outs[m] = None
 
+    # --- disjoint groups: the handoff (C1) is the reshard message queue (mq.py) over NCCL
+    # point-to-point: the teacher rank pushes each micro-batch's final hidden state [T, d_t]
+    # (identity layout: DP-only build, so plan_reshard yields one transfer per pair), the student
+    # rank pulls it on its stream; headers are verified once per step (Endpoint.verify).
+    def _handoff_channel(self, peer: int) -> "mq.Channel":
+        from . import mq
+
+        ch = getattr(self, "_h_chan", None)
+        if ch is None:
+            ch = self._h_chan = mq.Channel((0, 0), (0, 0), mq.DistTransport(peer=peer))
+        return ch
+
+    def _handoff_endpoint(self, peer: int, T: int):
+        from . import mq
+
+        eps = self.__dict__.setdefault("_h_eps", {})
+        if T not in eps:
+            lay = mq.ShardLayout((T, self.tshape.d))
+            eps[T] = mq.Endpoint((0, 0), mq.plan_reshard(lay, lay), {(0, 0): self._handoff_channel(peer)},
+                                 torch.bfloat16)
+        return eps[T]
+
     def _run_teacher_remote(self, plan, host, packed, ready):
-        dist = _dist()
+        from . import mq
+
         pt, ht = plan["teacher"], host["teacher"]
         (dst,) = self.roles["send_to"]  # fan-out 1: teacher rank q feeds student rank q
+        ch = self._handoff_channel(dst)
         self.t_stream.wait_event(ready)
         with torch.cuda.stream(self.t_stream):
             for m in range(pt["n_mb"]):
                 T = ht[0][m]
                 yf = self._teacher_mb(packed["teacher"], self._mb_cu(pt, m, T), m, ht[1][m], T)
-                dist.send(yf, dst)
+                meta = mq.MessageMeta((T, self.tshape.d), 2, "teacher", (0, 0), m)
+                ch.push(yf, meta, donate=True)  # fresh buffer per micro-batch: no staging copy
 
     def _run_student_remote(self, plan, host, packed, ready, clock, loss_acc, global_tokens):
-        dist = _dist()
         ps, hs = plan["student"], host["student"]
         (src,) = self.roles["recv_from"]  # teacher rank feeding this student rank
         self.s_stream.wait_event(ready)
         with torch.cuda.stream(self.s_stream):
             for m in range(ps["n_mb"]):
                 T = hs[0][m]
-                yf_t = torch.empty(T, self.tshape.d, device=self.device, dtype=torch.bfloat16)
-                dist.recv(yf_t, src)
+                yf_t, _ = self._handoff_endpoint(src, T).pull(validate=False)
                 self._student_mb(yf_t, packed["student"], self._mb_cu(ps, m, T), hs[1][m], T, loss_acc,
                                  global_tokens, clock, m)
+
+    def verify_handoff(self):
+        """Check the deferred control headers of this step's pulls (sample ids in schedule order)."""
+        got = []
+        for ep in getattr(self, "_h_eps", {}).values():
+            got += [m.sample_id for m in ep.verify()]
+        return got
 
     # ------------------------------------------------------------------ measured timeline
     def measured_events(self):
