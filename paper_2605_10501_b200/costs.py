@@ -115,3 +115,78 @@ def cost_table(graph: SectionGraph, configs: Mapping[str, SectionConfig],
             owner,
         )
     return out
+
+
+# --- batch synthesis (host; costs.py:206-299) ----------------------------------------------------
+
+
+@dataclass(frozen=True)
+class BatchProfile:
+    """Statistical description of a global batch (costs.py:206-227): ``shares`` = fraction of
+    samples activating each auxiliary, ``tokens`` = tokens per sample per section (default:
+    the section's max_seq_len)."""
+
+    global_batch_size: int
+    shares: Mapping[str, float] = field(default_factory=dict)
+    tokens: Mapping[str, int] = field(default_factory=dict)
+
+    def __post_init__(self) -> None:
+        from .errors import EmptyBatch
+
+        if self.global_batch_size < 1:
+            raise EmptyBatch("global_batch_size must be positive")
+        for sid, share in self.shares.items():
+            if not 0 <= share <= 1:
+                raise InvalidDims(f"share for '{sid}' must lie in [0,1]", section=sid)
+
+    def tokens_for(self, section: SectionSpec) -> int:
+        return int(self.tokens.get(section.id, section.structural.max_seq_len))
+
+
+def derive_batch(graph: SectionGraph, configs: Mapping[str, SectionConfig],
+                 params_by_section: Mapping[str, CostParams], profile: BatchProfile, seed: int = 0):
+    """Synthesise a global batch of 6-tuples from the cost model (costs.py:230-299).
+
+    Host-side planning input, identical to the reference: membership of each auxiliary is the
+    rounded share of the batch chosen by ``random.Random(seed)`` shuffles (the reference's own
+    generator, so a given seed yields the same batch); per-sample times come from
+    :func:`per_sample_times` at the rank's sample count, summed per side.  The device step path
+    never uses this generator (its batches come from the token counts, csrc/plan.cu K1)."""
+    import random
+
+    from .workload import SampleTiming, Side
+
+    crit = graph.critical
+    b = profile.global_batch_size
+    rng = random.Random(seed)
+    member = {}
+    for aux in graph.auxiliaries:
+        count = min(b, round(profile.shares.get(aux.id, 0.0) * b))
+        ids = list(range(b))
+        rng.shuffle(ids)
+        member[aux.id] = set(ids[:count])
+    times = {crit.id: per_sample_times(crit, configs[crit.id], params_by_section[crit.id], profile.tokens_for(crit),
+                                       math.ceil(b / configs[crit.id].dp))}
+    for aux in graph.auxiliaries:
+        n = len(member[aux.id])
+        times[aux.id] = per_sample_times(aux, configs[aux.id], params_by_section[aux.id], profile.tokens_for(aux),
+                                         math.ceil(n / configs[aux.id].dp) if n else 0)
+    out = []
+    fwd_c, bwd_c = times[crit.id]
+    for i in range(b):
+        up_f = up_b = down_f = down_b = 0.0
+        act = set()
+        for aux in graph.auxiliaries:
+            if i not in member[aux.id]:
+                continue
+            f, bw = times[aux.id]
+            if graph.side(aux.id) is Side.UPSTREAM:
+                up_f += f
+                up_b += bw
+            else:
+                down_f += f
+                down_b += bw
+            act.add(aux.id)
+        out.append(SampleTiming(sample_id=i, t_f_bc=up_f, t_f_c=fwd_c, t_f_ac=down_f, t_b_bc=down_b, t_b_c=bwd_c,
+                                t_b_ac=up_b, activated_sections=frozenset(act)))
+    return out
