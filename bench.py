@@ -197,6 +197,31 @@ def run_vlm(args):
     print(json.dumps(line), flush=True)
 
 
+def p2p_bandwidth(ex, dist, nbytes=64 << 20, reps=4):
+    """Measured NCCL point-to-point bandwidth on the handoff pairs (teacher rank -> student rank),
+    GB/s on the receiver; the peak the handoff (C1) is reported against.  Disjoint layout only."""
+    import torch
+
+    buf = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    out = None
+    for it in range(2):  # first pass warms the NCCL point-to-point channel
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        dist.barrier()
+        e0.record()
+        for _ in range(reps):
+            for dst in ex.roles["send_to"]:
+                dist.send(buf, dst)
+            for src in ex.roles["recv_from"]:
+                dist.recv(buf, src)
+        e1.record()
+        torch.cuda.synchronize()
+        if ex.roles["recv_from"] and it == 1:
+            out = reps * nbytes / (e0.elapsed_time(e1) / 1e3) / 1e9
+    t = torch.tensor([out or 0.0], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 # ---------------------------------------------------------------------------------------------- GPU leg
 def main():
     ap = argparse.ArgumentParser()
@@ -248,6 +273,7 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    p2p = p2p_bandwidth(ex, dist) if (dist is not None and not ex.colocated) else None
     for _ in range(args.warmup):
         ex.step(ids_dev, want_loss=False)
     barrier()
@@ -258,13 +284,14 @@ def main():
     launches0 = instrument.launches
     main_stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    stalls, busy, span = [], 0.0, 0.0
+    stalls, busy, span, stats = [], 0.0, 0.0, []
     e0.record(main_stream)
     for _ in range(args.steps):
         st = ex.step(ids_dev, want_loss=False)
         stalls.append(st.stall_frac)
         busy += st.critical_busy_ms
         span += st.critical_span_ms
+        stats.append(st)
     e1.record(main_stream)
     barrier()
     launches = instrument.launches - launches0
@@ -297,11 +324,23 @@ def main():
     if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_value = B * args.steps / (float(t.item()) / 1e3)
-    # ---- stall: max over critical ranks
+    # ---- stall: max and mean over critical ranks; per-section idle; scheduler; C2 all-reduce
     stall = torch.tensor([max(stalls) if stalls and ex.student is not None else 0.0,
                           (1 - busy / span) if span > 0 else 0.0], device="cuda")
+    mean_stall = torch.tensor([sum(stalls) / len(stalls) if stalls and ex.student is not None else 0.0,
+                               1.0 if ex.student is not None else 0.0], device="cuda")
+    avg = lambda f: sum(f(x) for x in stats) / max(len(stats), 1)  # noqa: E731
+    per_rank = torch.tensor([avg(lambda x: x.plan_ms), avg(lambda x: x.allreduce_ms),
+                             avg(lambda x: x.step_ms - x.critical_busy_ms) if ex.student is not None else 0.0,
+                             avg(lambda x: x.step_ms - x.teacher_busy_ms) if ex.teacher is not None else 0.0],
+                            device="cuda")
     if dist is not None:
         dist.all_reduce(stall, op=dist.ReduceOp.MAX)
+        dist.all_reduce(mean_stall, op=dist.ReduceOp.SUM)
+        dist.all_reduce(per_rank, op=dist.ReduceOp.MAX)
+    plan_ms, ar_ms, idle_s, idle_t = (float(x) for x in per_rank.tolist())
+    n_sched = [ex.batch // ex.dp_s] * ex.dp_s + ([ex.batch // ex.dp_t] * ex.dp_t if ex.dp_t else [])
+    grad_bytes = ex.student.p.grad.numel() * 4 if ex.student is not None else 0
     peaks, peak_kind = load_peaks()
     gemm_tflops = (gemm_flops / (gemm_ms / 1e3) / 1e12) if gemm_ms > 0 else None
     peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
@@ -346,6 +385,20 @@ def main():
                 "l2": "inputs larger than L2 (teacher weights 2.2 GB, logits 1 GB per micro-batch)",
             },
             "section_stall_pct": 100.0 * float(stall[0].item()),
+            "section_stall": {"max_pct": 100.0 * float(stall[0].item()),
+                              "mean_pct": 100.0 * float(mean_stall[0].item()) / max(float(mean_stall[1].item()), 1.0),
+                              "definition": "(critical span - critical busy) / critical span per student rank"},
+            "section_idle_ms": {"student": idle_s, "teacher": idle_t,
+                                "definition": "step time - section busy time, max over ranks"},
+            "scheduler": {"device_us_per_step": plan_ms * 1e3, "share_of_step_pct": 100.0 * plan_ms / ms_per_step,
+                          "makespan_evals_per_step": sum(n * (n + 1) // 2 for n in n_sched),
+                          "placement": "K1-K5 on the main stream at step start (not overlapped)"},
+            "grad_allreduce": ({"ms": ar_ms, "bytes": grad_bytes,
+                                "bus_GBps": 2 * (dp_s - 1) / dp_s * grad_bytes / (ar_ms / 1e3) / 1e9 if ar_ms else None}
+                               if dp_s > 1 else None),
+            "handoff": (None if ex.colocated else
+                        {"bytes_per_step": int(B // max(dp_s, 1) * SEQ * ex.tshape.d * 2),
+                         "p2p_GBps_measured": p2p, "transport": "mq.DistTransport over NCCL point-to-point"}),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(B * SEQ * 4),
                     "d2h_bytes_per_step": 4 + 8 * 64},
             "gpu_launches": launches // max(args.steps, 1),

@@ -50,6 +50,9 @@ class StepStats:
     critical_busy_ms: float
     critical_span_ms: float
     stages: list = field(default_factory=list)
+    plan_ms: float = 0.0          # device time of the step's schedule build (K1-K5 + pack tables)
+    allreduce_ms: float = 0.0     # student gradient all-reduce (C2), 0 at dp1
+    teacher_busy_ms: float = 0.0  # summed teacher stage time on this rank (0 if not hosted)
 
     @property
     def stall_frac(self) -> float:
@@ -220,6 +223,8 @@ class KDExecutor:
         t_start = torch.cuda.Event(enable_timing=True)
         t_start.record(main)
         plan = self.plan(main)
+        t_plan = torch.cuda.Event(enable_timing=True)
+        t_plan.record(main)
         # one small D2H per step: micro-batch token counts of the local rank orders
         host = {k: (v["mb_tok"].cpu().tolist(), v["mb_start"].cpu().tolist()) for k, v in plan.items()}
         packed = {}
@@ -251,9 +256,13 @@ class KDExecutor:
         if self.student is not None:
             with torch.cuda.stream(self.s_stream):
                 dist = _dist()
+                ar = None
                 if dist is not None and self.dp_s > 1:
+                    ar = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                    ar[0].record(self.s_stream)
                     dist.all_reduce(self.student.p.grad, group=self.groups.get("student"))
                     dist.all_reduce(loss_acc, group=self.groups.get("student"))
+                    ar[1].record(self.s_stream)
                 self.student.p.adamw(self.lr)
             main.wait_stream(self.s_stream)
         if self.teacher is not None and not self.colocated:
@@ -272,7 +281,11 @@ class KDExecutor:
 
                 raise InconsistentSchedule("handoff delivered unexpected micro-batches", got=got)
         busy, span = clock.busy_span()
-        return StepStats(loss, t_start.elapsed_time(t_end), busy, span)
+        extra = {"plan_ms": t_start.elapsed_time(t_plan),
+                 "teacher_busy_ms": self.t_clock.busy_span()[0] if self.teacher is not None else 0.0}
+        if self.student is not None and ar is not None:
+            extra["allreduce_ms"] = ar[0].elapsed_time(ar[1])
+        return StepStats(loss, t_start.elapsed_time(t_end), busy, span, **extra)
 
     # --- co-resident sections on one GPU: the teacher stream runs ahead (upstream queue),
     # the student stream waits per micro-batch on a CUDA event.
@@ -368,7 +381,9 @@ class KDExecutor:
         with torch.cuda.stream(self.t_stream):
             for m in range(pt["n_mb"]):
                 T = ht[0][m]
+                self.t_clock.begin(self.t_stream, f"f_bc{m}")
                 yf = self._teacher_mb(packed["teacher"], self._mb_cu(pt, m, T), m, ht[1][m], T)
+                self.t_clock.end(self.t_stream)
                 meta = mq.MessageMeta((T, self.tshape.d), 2, "teacher", (0, 0), m)
                 ch.push(yf, meta, donate=True)  # fresh buffer per micro-batch: no staging copy
 
