@@ -152,7 +152,8 @@ int maestro_gemm_bf16(const void* A, const void* B, void* C, int32_t M, int32_t 
                       int32_t ldb, int32_t ldc, int32_t a_mn, int32_t b_mn, int32_t epi, void* stream);
 
 /* K7 + fused RoPE epilogue: C = A B^T (bf16, K-major A/B); every 64-column head in columns
- * [0, rope_cols) is rotated (rotate-half) at position pos[row]; cos_sin[p][32] = (cos, sin). */
+ * [0, rope_cols) is rotated (rotate-half) at position pos[row].  cos_sin is position-tiled:
+ * [ceil(P/32)][32 freqs][32 positions] of (cos, sin) fp32 pairs (transformer.rope_table). */
 int maestro_gemm_bf16_rope(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K, int32_t lda,
                            int32_t ldb, int32_t ldc, const int32_t* pos, const void* cos_sin, int32_t rope_cols,
                            void* stream);
@@ -162,7 +163,8 @@ int maestro_gemm_bf16_rope(const void* A, const void* B, void* C, int32_t M, int
 int maestro_gemm_bf16_residual(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K, int32_t lda,
                                int32_t ldb, int32_t ldc, const void* R, int32_t ldr, void* stream);
 /* K7 + fused SwiGLU epilogue: C = A B^T is the gate/up activation with gate/up rows of B
- * interleaved in 32-row blocks ([g_0..g_31, u_0..u_31, g_32..]); S[m, f] = silu(g_f) * u_f. */
+ * interleaved in 32-row blocks ([g_0..g_31, u_0..u_31, g_32..]); S[m, f] = silu(g_f) * u_f.
+ * C may be NULL (forward-only sections): then only S is written. */
 int maestro_gemm_bf16_swiglu(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K, int32_t lda,
                              int32_t ldb, int32_t ldc, void* S, int32_t lds, void* stream);
 
@@ -184,7 +186,7 @@ int maestro_attn_bwd(const void* dout, int32_t lddo, const void* q, const void* 
                      void* dk, int32_t lddk, void* dv, int32_t lddv, float softmax_scale, int32_t causal,
                      const int32_t* rope_pos, const void* rope_cos_sin, const void* plan, void* workspace,
                      void* stream);
-/* (rope_pos/rope_cos_sin non-null: dQ and dK are returned through the inverse RoPE rotation,
+/* (rope_pos/rope_cos_sin (position-tiled table, as above) non-null: dQ and dK are returned through the inverse RoPE rotation,
  * i.e. w.r.t. the pre-rotation projections.) */
 
 /* Reshard data mover (mq.py:163-174, 460-469): dst[box] = src[box] for an N-d box (ndim <= 6,
@@ -207,6 +209,8 @@ int maestro_add_rmsnorm_fwd(const void* x, const void* a, void* h, void* y, cons
                             int32_t d, float eps, void* stream);
 int maestro_rmsnorm_bwd(const void* dy, const void* h, const void* w, const float* rstd, const void* dres,
                         void* dx, float* dw, int32_t T, int32_t d, void* stream);
+/* In-place rotate-half RoPE; cos_sin position-tiled [ceil(P/32)][dh/2][32][2] (see maestro_gemm_bf16_rope);
+ * dh a multiple of 16, row pitch ld a multiple of 8 elements. */
 int maestro_rope(void* qk, const int32_t* pos, const void* cos_sin, int32_t T, int32_t n_heads, int32_t dh,
                  int32_t ld, int32_t backward, void* stream);
 int maestro_positions(const int32_t* cu, int32_t nseq, int32_t* pos, void* stream);

@@ -764,10 +764,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         const float f = which == 0 ? scale : 1.f;
         if (which == 0 && rope_cs != nullptr) {
           // K was rotated by RoPE in the forward: dK_pre = R(pos)^T dK  (rotate by -theta)
-          const float2* csr = rope_cs + (size_t)kvpos * 32;
 #pragma unroll
           for (int k = 0; k < 32; ++k) {
-            const float2 cs = csr[k];
+            const float2 cs = rope_cs_at(rope_cs, kvpos, k, 32);
             const float a = __uint_as_float(lo[k]), b = __uint_as_float(hi[k]);
             lo[k] = __float_as_uint(a * cs.x + b * cs.y);
             hi[k] = __float_as_uint(b * cs.x - a * cs.y);
@@ -834,10 +833,10 @@ __global__ void attn_bwd_post_kernel(const float* __restrict__ dq_acc, __nv_bflo
     *reinterpret_cast<float4*>(b) = reinterpret_cast<const float4*>(src + 32)[0];
     *reinterpret_cast<float4*>(b + 4) = reinterpret_cast<const float4*>(src + 32)[1];
     if (cs != nullptr) {
-      const float2* c = cs + (size_t)pos[t] * 32 + 8 * g;
+      const int pt = pos[t];
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        const float2 v = c[k];
+        const float2 v = rope_cs_at(cs, pt, 8 * g + k, 32);
         const float x = a[k], y = b[k];
         a[k] = x * v.x + y * v.y;
         b[k] = y * v.x - x * v.y;

@@ -39,4 +39,11 @@ inline int ensure_smem(size_t bytes) {
   return 0;
 }
 
+// RoPE (cos, sin) table, position-tiled: [ceil(P/32)][half][32][2] fp32 -- for a fixed
+// frequency k, 32 consecutive positions are contiguous, so a warp whose lanes own consecutive
+// rows reads one 256-byte segment per frequency (transformer.rope_table builds it).
+__device__ __forceinline__ float2 rope_cs_at(const float2* __restrict__ cs, int pos, int k, int half) {
+  return cs[((size_t)(pos >> 5) * half + k) * 32 + (pos & 31)];
+}
+
 }  // namespace mb

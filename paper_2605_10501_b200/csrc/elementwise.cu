@@ -242,21 +242,31 @@ __global__ void __launch_bounds__(256) rmsnorm_generic_bwd_kernel(const __nv_bfl
 
 // ---------------------------------------------------------------- RoPE (rotate-half pairs)
 // qk rows: [T, n_heads, dh] at row pitch `ld`; cs[pos][dh/2] = (cos, sin).  sign=+1 fwd, -1 bwd.
+// Thread per (token, head), consecutive threads = consecutive tokens of one head: the token's
+// head row moves as 16-byte vectors and the position-tiled (cos, sin) table is read coalesced.
 __global__ void rope_kernel(__nv_bfloat16* __restrict__ qk, const int32_t* __restrict__ pos,
                             const float2* __restrict__ cs, int T, int n_heads, int dh, int ld, float sign) {
   const int half = dh / 2;
-  const int pairs_per_row = n_heads * half;
-  const long long total = (long long)T * pairs_per_row;
+  const long long total = (long long)T * n_heads;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
-    const int t = (int)(i / pairs_per_row);
-    const int r = (int)(i - (long long)t * pairs_per_row);
-    const int hd = r / half, k = r - hd * half;
+    const int hd = (int)(i / T), t = (int)(i - (long long)hd * T);
     __nv_bfloat16* p = qk + (size_t)t * ld + hd * dh;
-    const float2 c = cs[(size_t)pos[t] * half + k];
-    const float s = c.y * sign;
-    const float a = __bfloat162float(p[k]), b = __bfloat162float(p[k + half]);
-    p[k] = __float2bfloat16(a * c.x - b * s);
-    p[k + half] = __float2bfloat16(b * c.x + a * s);
+    const int pt = pos[t];
+    for (int k0 = 0; k0 < half; k0 += 8) {
+      uint4 va = *reinterpret_cast<const uint4*>(p + k0), vb = *reinterpret_cast<const uint4*>(p + k0 + half);
+      __nv_bfloat162* a2 = reinterpret_cast<__nv_bfloat162*>(&va);
+      __nv_bfloat162* b2 = reinterpret_cast<__nv_bfloat162*>(&vb);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 c0 = rope_cs_at(cs, pt, k0 + 2 * j, half), c1 = rope_cs_at(cs, pt, k0 + 2 * j + 1, half);
+        const float2 a = __bfloat1622float2(a2[j]), b = __bfloat1622float2(b2[j]);
+        const float s0 = c0.y * sign, s1 = c1.y * sign;
+        a2[j] = __floats2bfloat162_rn(a.x * c0.x - b.x * s0, a.y * c1.x - b.y * s1);
+        b2[j] = __floats2bfloat162_rn(b.x * c0.x + a.x * s0, b.y * c1.x + a.y * s1);
+      }
+      *reinterpret_cast<uint4*>(p + k0) = va;
+      *reinterpret_cast<uint4*>(p + k0 + half) = vb;
+    }
   }
 }
 
@@ -457,7 +467,8 @@ MAESTRO_API int maestro_rmsnorm_bwd(const void* dy, const void* h, const void* w
 MAESTRO_API int maestro_rope(void* qk, const int32_t* pos, const void* cos_sin, int32_t T, int32_t n_heads,
                              int32_t dh, int32_t ld, int32_t backward, void* stream) {
   if (T <= 0) return 0;
-  const long long work = (long long)T * n_heads * dh / 2;
+  if ((dh % 16) || (ld % 8)) return (int)cudaErrorInvalidValue;  // 16-byte row vectors
+  const long long work = (long long)T * n_heads;
   rope_kernel<<<grid_for(work, 256), 256, 0, (cudaStream_t)stream>>>(
       (__nv_bfloat16*)qk, pos, (const float2*)cos_sin, T, n_heads, dh, ld, backward ? -1.f : 1.f);
   return launch_status();

@@ -458,10 +458,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           if (rope_cols > 0 && n0 + c < rope_cols && row < M) {
             // fused RoPE (rotate-half): this 64-column chunk is exactly one head of Q or K;
             // r0 holds dims [0,32), r1 dims [32,64) of the row
-            const float2* csr = rope_cs + (size_t)rope_pos[row] * 32;
+            const int pr = rope_pos[row];
 #pragma unroll
             for (int k = 0; k < 32; ++k) {
-              const float2 cs = csr[k];
+              const float2 cs = rope_cs_at(rope_cs, pr, k, 32);
               const float a = __uint_as_float(r0[k]), b = __uint_as_float(r1[k]);
               r0[k] = __float_as_uint(a * cs.x - b * cs.y);
               r1[k] = __float_as_uint(b * cs.x + a * cs.y);
@@ -475,12 +475,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             for (int k = 0; k < 16; ++k) {
               const float g0 = __uint_as_float(r0[2 * k]), g1 = __uint_as_float(r0[2 * k + 1]);
               const float u0 = __uint_as_float(r1[2 * k]), u1 = __uint_as_float(r1[2 * k + 1]);
-              sv[k] = pack_bf16(g0 / (1.f + __expf(-g0)) * u0, g1 / (1.f + __expf(-g1)) * u1);
+              sv[k] = pack_bf16(__fdividef(g0, 1.f + __expf(-g0)) * u0, __fdividef(g1, 1.f + __expf(-g1)) * u1);
             }
             uint4* dst = reinterpret_cast<uint4*>(swiglu_out + (size_t)row * ld_swiglu + (n0 + c) / 2);
 #pragma unroll
             for (int k = 0; k < 4; ++k) dst[k] = make_uint4(sv[4 * k], sv[4 * k + 1], sv[4 * k + 2], sv[4 * k + 3]);
           }
+          if (C == nullptr) continue;  // SwiGLU-only output (forward-only sections): gu is not stored
           if (chunk_ctr >= 2) {
             if (et == 0) bulk_wait_read<1>();  // the store issued from this buffer has read it
             named_barrier_sync(1, 128);
@@ -630,8 +631,8 @@ MAESTRO_API int maestro_gemm_bf16_residual(const void* A, const void* B, void* C
 
 MAESTRO_API int maestro_gemm_bf16_swiglu(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K,
                                          int32_t lda, int32_t ldb, int32_t ldc, void* S, int32_t lds, void* stream) {
-  if (N % 64) return (int)cudaErrorInvalidValue;
-  return gemm_impl(A, B, C, M, N, K, lda, ldb, ldc, 0, 0, 0, stream, nullptr, nullptr, 0, S, lds);
+  if (N % 64 || S == nullptr) return (int)cudaErrorInvalidValue;
+  return gemm_impl(A, B, C, M, N, K, lda, ldb, C ? ldc : N, 0, 0, 0, stream, nullptr, nullptr, 0, S, lds);
 }
 
 static int gemm_impl(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K, int32_t lda,
@@ -688,7 +689,9 @@ static int gemm_impl(const void* A, const void* B, void* C, int32_t M, int32_t N
     CUtensorMap ma, mbm, mc;
     const int brows = bn2 / 2;
     memset(&mc, 0, sizeof(mc));
-    if (epi_k == EPI_BF16 && !make_map_2d(&mc, C, N, M, ldc, 64, 128)) return (int)cudaErrorInvalidValue;
+    if (epi_k == EPI_BF16 && C != nullptr && !make_map_2d(&mc, C, N, M, ldc, 64, 128))
+      return (int)cudaErrorInvalidValue;
+    if (C == nullptr && swiglu_out == nullptr) return (int)cudaErrorInvalidValue;
     bool ok = a_mn ? make_map_2d(&ma, A, M, K, lda, 64, 64) : make_map_2d(&ma, A, K, M, lda, 64, 128);
     ok = ok && (b_mn ? make_map_2d(&mbm, B, N, K, ldb, 64, 64) : make_map_2d(&mbm, B, K, N, ldb, 64, brows));
     if (!ok) return (int)cudaErrorInvalidValue;

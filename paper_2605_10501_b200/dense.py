@@ -106,18 +106,20 @@ def linear_fwd_residual(x: torch.Tensor, w: torch.Tensor, resid: torch.Tensor,
 
 
 def linear_fwd_swiglu(x: torch.Tensor, w: torch.Tensor, s_out: torch.Tensor,
-                      out: torch.Tensor | None = None) -> torch.Tensor:
-    """gu = x @ w^T (gate/up interleaved in 32-row blocks) and s_out = silu(g) * u from the epilogue."""
+                      out: torch.Tensor | None = None, store_gu: bool = True) -> torch.Tensor | None:
+    """gu = x @ w^T (gate/up interleaved in 32-row blocks) and s_out = silu(g) * u from the epilogue.
+    ``store_gu=False`` (forward-only sections) writes only s_out and returns None."""
     T, K = x.shape
     Nn = w.shape[0]
-    if out is None:
+    if out is None and store_gu:
         out = torch.empty(T, Nn, device=x.device, dtype=torch.bfloat16)
     rec = instrument.gemm_timing
     if rec is not None:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-    rc = _lib().maestro_gemm_bf16_swiglu(N.ptr(x), N.ptr(w), N.ptr(out), T, Nn, K, x.stride(0), w.stride(0),
-                                         out.stride(0), N.ptr(s_out), s_out.stride(0), N.stream_ptr())
+    rc = _lib().maestro_gemm_bf16_swiglu(N.ptr(x), N.ptr(w), N.ptr(out) if out is not None else None, T, Nn, K,
+                                         x.stride(0), w.stride(0), out.stride(0) if out is not None else Nn,
+                                         N.ptr(s_out), s_out.stride(0), N.stream_ptr())
     N.check(rc, "gemm_bf16_swiglu")
     if rec is not None:
         e1.record()

@@ -148,9 +148,15 @@ class FlatParams:
 
 
 def rope_table(max_pos: int, head_dim: int, base: float, device) -> torch.Tensor:
+    """(cos, sin) of every (position, frequency) in the position-tiled layout the kernels read:
+    [ceil(P/32)][head_dim/2][32 positions][2] fp32 (include/maestro_b200.h).  A warp's 32 rows
+    are 32 consecutive positions, so each per-frequency read is one contiguous 256-byte segment."""
+    half = head_dim // 2
+    P = (max_pos + 31) // 32 * 32
     inv = base ** (-torch.arange(0, head_dim, 2, dtype=torch.float64) / head_dim)
-    ang = torch.arange(max_pos, dtype=torch.float64)[:, None] * inv[None, :]
-    return torch.stack([ang.cos(), ang.sin()], -1).to(torch.float32).to(device).contiguous()
+    ang = torch.arange(P, dtype=torch.float64)[:, None] * inv[None, :]  # [P, half]
+    cs = torch.stack([ang.cos(), ang.sin()], -1).to(torch.float32)      # [P, half, 2]
+    return cs.view(P // 32, 32, half, 2).transpose(1, 2).contiguous().to(device)
 
 
 @dataclass
@@ -208,7 +214,7 @@ class Transformer:
             # gate/up projection with SwiGLU fused into the epilogue (gate/up rows interleaved
             # in 32-row blocks in wgu)
             sw = torch.empty(T, s.ffn, device=dev, dtype=bf)
-            gu = D.linear_fwd_swiglu(y2, p[f"l{i}.wgu"], sw)
+            gu = D.linear_fwd_swiglu(y2, p[f"l{i}.wgu"], sw, store_gu=save)  # gu only kept for backward
             if save:
                 ctx["layers"].append((h1, r1, y1, qkv, o, lse, h2, r2, y2, gu, sw))
             # next block's residual stream: h2 + sw Wd^T

@@ -167,3 +167,20 @@ def test_residual_epilogue(M, N, K):
     h = dense.linear_fwd_residual(x, w, r)
     ref = r.float() + x.float() @ w.float().t()
     assert _rel(h, ref) < 8e-3
+
+
+@pytest.mark.parametrize("T,F,K", [(1000, 384, 512), (8192, 2816, 2048)])
+def test_swiglu_without_gu_store(T, F, K):
+    """Forward-only sections: the gate/up GEMM writes only silu(g) * u (C = NULL)."""
+    from oracle import torch_ref as R
+    from paper_2605_10501_b200 import dense
+
+    torch.manual_seed(T + F)
+    x = torch.randn(T, K, device="cuda").bfloat16()
+    wgu = (torch.randn(2 * F, K, device="cuda") * 0.05).bfloat16()
+    s = torch.empty(T, F, device="cuda", dtype=torch.bfloat16)
+    assert dense.linear_fwd_swiglu(x, wgu, s, store_gu=False) is None
+    gref = x.float() @ wgu.float().t()
+    gi = R.gate_index(F, "cuda")
+    sref = torch.nn.functional.silu(gref[:, gi]) * gref[:, gi + 32]
+    assert _rel(s, sref) < 2e-2
