@@ -285,7 +285,8 @@ struct Cfg2 {
 template <int BN2, bool A_MN, bool B_MN, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                 const __grid_constant__ CUtensorMap map_c, void* C, int M, int N, int K, int ldc, int splits,
+                 const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_r, void* C, int M,
+                 int N, int K, int ldc, int splits,
                  const int32_t* __restrict__ rope_pos, const float2* __restrict__ rope_cs, int rope_cols,
                  __nv_bfloat16* __restrict__ swiglu_out, int ld_swiglu, const __nv_bfloat16* __restrict__ resid,
                  int ldr) {
@@ -300,7 +301,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* rbar = tempty + 2;  // [2] residual chunk landed in staging buffer b
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
@@ -327,6 +329,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], 256);
+      mbar_init(&rbar[s], 1);
     }
     fence_barrier_init();
   }
@@ -429,24 +432,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         for (int c = 0; c < BN2; c += 64, ++chunk_ctr) {
           unsigned char* buf = sC + (chunk_ctr & 1) * CF::EPI_BUF;
           uint32_t r0[32], r1[32];
-          uint4 res[8];
-          const bool has_res = resid != nullptr && row < M;
-          if (has_res) {
-            // fused residual add (h = x + A B^T): this row's 64 residual values, loaded before the
-            // TMEM read so their latency overlaps it
-            const __nv_bfloat16* rp = resid + (size_t)row * ldr + n0 + c;
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-              res[u] = n0 + c + 8 * u < N ? *reinterpret_cast<const uint4*>(rp + 8 * u) : make_uint4(0, 0, 0, 0);
+          const bool use_r = resid != nullptr;
+          if (use_r) {
+            // fused residual add (h = x + A B^T): the residual chunk is TMA-loaded into this
+            // chunk's staging buffer (same swizzled 128 x 64 layout the store uses) while the
+            // accumulator is read from TMEM; each thread then adds its row in place
+            if (chunk_ctr >= 2) {
+              if (et == 0) bulk_wait_read<1>();  // the store issued from this buffer has read it
+              named_barrier_sync(1, 128);
+            }
+            if (et == 0) {
+              mbar_arrive_expect_tx(&rbar[chunk_ctr & 1], CF::EPI_BUF);
+              tma_load_2d(buf, &map_r, &rbar[chunk_ctr & 1], n0 + c, row0);
+            }
           }
           tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + as * BN2 + c, r0);
           tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + as * BN2 + c + 32, r1);
           tmem_ld_wait();
-          if (has_res) {
+          if (use_r) {
+            mbar_wait(&rbar[chunk_ctr & 1], (chunk_ctr >> 1) & 1);
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
               uint32_t* dst = u < 4 ? &r0[8 * u] : &r1[8 * (u - 4)];
-              const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&res[u]);
+              const uint4 rv = *reinterpret_cast<const uint4*>(buf + r_in * 128 + ((u ^ (r_in & 7)) << 4));
+              const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&rv);
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
                 const float2 f = __bfloat1622float2(hv[e]);
@@ -482,7 +491,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             for (int k = 0; k < 4; ++k) dst[k] = make_uint4(sv[4 * k], sv[4 * k + 1], sv[4 * k + 2], sv[4 * k + 3]);
           }
           if (C == nullptr) continue;  // SwiGLU-only output (forward-only sections): gu is not stored
-          if (chunk_ctr >= 2) {
+          if (!use_r && chunk_ctr >= 2) {
             if (et == 0) bulk_wait_read<1>();  // the store issued from this buffer has read it
             named_barrier_sync(1, 128);
           }
@@ -554,7 +563,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 }
 
 template <int BN2, bool A_MN, bool B_MN, int EPI>
-int launch2(const CUtensorMap& ma, const CUtensorMap& mbm, const CUtensorMap& mc, void* C, int M, int N, int K,
+int launch2(const CUtensorMap& ma, const CUtensorMap& mbm, const CUtensorMap& mc, const CUtensorMap& mr, void* C,
+            int M, int N, int K,
             int ldc, int splits, cudaStream_t st, const int32_t* rope_pos = nullptr, const float2* rope_cs = nullptr,
             int rope_cols = 0, __nv_bfloat16* swiglu_out = nullptr, int ld_swiglu = 0,
             const __nv_bfloat16* resid = nullptr, int ldr = 0) {
@@ -562,7 +572,7 @@ int launch2(const CUtensorMap& ma, const CUtensorMap& mbm, const CUtensorMap& mc
   if (ensure_smem<gemm2_kernel<BN2, A_MN, B_MN, EPI>>(SMEM)) return launch_status();
   const int units = ((M + 255) / 256) * ((N + BN2 - 1) / BN2) * splits;
   const int pairs = units < num_sms() / 2 ? units : num_sms() / 2;
-  gemm2_kernel<BN2, A_MN, B_MN, EPI><<<2 * pairs, THREADS, SMEM, st>>>(ma, mbm, mc, C, M, N, K, ldc, splits,
+  gemm2_kernel<BN2, A_MN, B_MN, EPI><<<2 * pairs, THREADS, SMEM, st>>>(ma, mbm, mc, mr, C, M, N, K, ldc, splits,
                                                                         rope_pos, rope_cs, rope_cols, swiglu_out,
                                                                         ld_swiglu, resid, ldr);
   return launch_status();
@@ -686,9 +696,12 @@ static int gemm_impl(const void* A, const void* B, void* C, int32_t M, int32_t N
       splits = (kb + per - 1) / per;
     }
     const int epi_k = splits > 1 ? EPI_F32_ATOMIC : epi;
-    CUtensorMap ma, mbm, mc;
+    CUtensorMap ma, mbm, mc, mr;
     const int brows = bn2 / 2;
     memset(&mc, 0, sizeof(mc));
+    memset(&mr, 0, sizeof(mr));
+    if (resid != nullptr && (epi_k != EPI_BF16 || !make_map_2d(&mr, resid, N, M, ldr, 64, 128)))
+      return (int)cudaErrorInvalidValue;
     if (epi_k == EPI_BF16 && C != nullptr && !make_map_2d(&mc, C, N, M, ldc, 64, 128))
       return (int)cudaErrorInvalidValue;
     if (C == nullptr && swiglu_out == nullptr) return (int)cudaErrorInvalidValue;
@@ -696,7 +709,7 @@ static int gemm_impl(const void* A, const void* B, void* C, int32_t M, int32_t N
     ok = ok && (b_mn ? make_map_2d(&mbm, B, N, K, ldb, 64, 64) : make_map_2d(&mbm, B, K, N, ldb, 64, brows));
     if (!ok) return (int)cudaErrorInvalidValue;
 #define MB_GEMM2_LAUNCH(W, AM, BMN, E)                                                                  \
-  launch2<W, AM, BMN, E>(ma, mbm, mc, C, M, N, K, ldc, splits, st, rope_pos, rope_cs, rope_cols,         \
+  launch2<W, AM, BMN, E>(ma, mbm, mc, mr, C, M, N, K, ldc, splits, st, rope_pos, rope_cs, rope_cols,     \
                          (__nv_bfloat16*)swiglu_out, ld_swiglu, (const __nv_bfloat16*)resid, ldr)
 #define MB_GEMM2_CASE(AM, BMN, E)                                                                    \
   if (a_mn == AM && b_mn == BMN && epi_k == E)                                                       \
