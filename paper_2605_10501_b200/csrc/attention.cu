@@ -169,8 +169,11 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     if (lane == 0) {
       int g = 0;  // global KV tile counter (ring position)
       int j = 0;  // local item counter
-      for (int w = snake_item(0); w < n_items; w = snake_item(j + 1), ++j) {
-        const FwdItem it = fwd_item<CAUSAL>(w, H, Hk, cu, tiles);
+      FwdItem it_n{};
+        if (snake_item(0) < n_items) it_n = fwd_item<CAUSAL>(snake_item(0), H, Hk, cu, tiles);
+        for (int w = snake_item(0); w < n_items; w = snake_item(j + 1), ++j) {
+        const FwdItem it = it_n;
+        if (snake_item(j + 1) < n_items) it_n = fwd_item<CAUSAL>(snake_item(j + 1), H, Hk, cu, tiles);  // prefetch
         const int qb = j & 1;
         mbar_wait(&q_empty[qb], ((j >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(&q_full[qb], TILE_BYTES);
@@ -220,8 +223,11 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
         if (pend_last) umma_commit(&o_full[pend_o]);
         pend_g = -1;
       };
-      for (int w = snake_item(0); w < n_items; w = snake_item(j + 1), ++j) {
-        const FwdItem it = fwd_item<CAUSAL>(w, H, Hk, cu, tiles);
+      FwdItem it_n{};
+        if (snake_item(0) < n_items) it_n = fwd_item<CAUSAL>(snake_item(0), H, Hk, cu, tiles);
+        for (int w = snake_item(0); w < n_items; w = snake_item(j + 1), ++j) {
+        const FwdItem it = it_n;
+        if (snake_item(j + 1) < n_items) it_n = fwd_item<CAUSAL>(snake_item(j + 1), H, Hk, cu, tiles);  // prefetch
         const int qb = j & 1, ob = j & 1;
         mbar_wait(&q_full[qb], (j >> 1) & 1);
         const uint32_t q_base = smem_u32(sm + FwdSmemP::Q + qb * TILE_BYTES);
@@ -262,9 +268,57 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     unsigned char* pbuf = sm + FwdSmemP::P;
     float* xmax = reinterpret_cast<float*>(sm + FwdSmemP::XMAX);
     float* xsum = reinterpret_cast<float*>(sm + FwdSmemP::XSUM);
+    // Epilogue of item jj (O buffer ob, final m / l), deferred until after the next item's first
+    // tile: by then the item's last PV has completed, so O is read without waiting on it.
+    auto epilogue = [&](const FwdItem& it, int jj, float m, float l) {
+      const int ob = jj & 1;
+      const int qpos = it.q0 + r;
+      // epilogue of item jj: exchange (m, l) with the
+      // partner half, O = (O_a 2^(m_a - M) + O_b 2^(m_b - M)) / l for this half's 32 columns
+      float* xm = xmax + ob * 256;  // by item parity: the partner reads it before the next item's barrier
+      float* xs = xsum + ob * 256;
+      xm[half * 128 + r] = m;
+      xs[half * 128 + r] = l;
+      mbar_wait(&o_full[ob], (jj >> 1) & 1);
+      tc_fence_after();
+      uint32_t ra[32], rb[32];
+      tmem_ld_32x32b_x32(tmem + lane_base + 256 + ob * 2 * DH + half * 32, ra);
+      tmem_ld_32x32b_x32(tmem + lane_base + 256 + ob * 2 * DH + DH + half * 32, rb);
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(&o_empty[ob]);
+      named_bar(pair_bar, 64);
+      const float m_o = xm[(half ^ 1) * 128 + r], l_o = xs[(half ^ 1) * 128 + r];
+      const float ma = half == 0 ? m : m_o, mb = half == 0 ? m_o : m;
+      const float la = half == 0 ? l : l_o, lb = half == 0 ? l_o : l;
+      const float M = fmaxf(ma, mb);
+      const float sa = ma == -INFINITY ? 0.f : ex2(ma - M), sb = mb == -INFINITY ? 0.f : ex2(mb - M);
+      const float l_all = la * sa + lb * sb;
+      if (qpos < it.L) {
+        const float fa = sa / l_all, fb = sb / l_all;
+        uint32_t o[16];
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj)
+          o[jj] = pack_bf16(__uint_as_float(ra[2 * jj]) * fa + __uint_as_float(rb[2 * jj]) * fb,
+                            __uint_as_float(ra[2 * jj + 1]) * fa + __uint_as_float(rb[2 * jj + 1]) * fb);
+        uint4* dst = reinterpret_cast<uint4*>(out + (size_t)(it.s0 + qpos) * ldo + it.h * DH + half * 32);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) dst[u] = make_uint4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);
+        if (half == 0) lse[(size_t)it.h * T + it.s0 + qpos] = (M + log2f(l_all)) * LN2_F;
+      }
+    };
     int g = 0, j = 0;
-    for (int w = snake_item(0); w < n_items; w = snake_item(j + 1), ++j) {
-      const FwdItem it = fwd_item<CAUSAL>(w, H, Hk, cu, tiles);
+    bool pend = false;
+    FwdItem pit{};
+    int pj = 0;
+    float pm = 0.f, pl = 0.f;
+    int w = snake_item(0);
+    FwdItem it{};
+    if (w < n_items) it = fwd_item<CAUSAL>(w, H, Hk, cu, tiles);
+    for (; w < n_items; ++j) {
+      const int w_next = snake_item(j + 1);
+      FwdItem nxt{};
+      if (w_next < n_items) nxt = fwd_item<CAUSAL>(w_next, H, Hk, cu, tiles);  // prefetch the next item
       const int ob = j & 1;
       const int qpos = it.q0 + r;
       float m = -INFINITY, l = 0.f;
@@ -343,41 +397,20 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
         fence_proxy_async_smem();
         tc_fence_before();
         mbar_arrive(&p_full[b]);
+        if (i == 0 && pend) {
+          epilogue(pit, pj, pm, pl);
+          pend = false;
+        }
       }
-      // epilogue of item j (overlaps the MMA warp starting item j+1): exchange (m, l) with the
-      // partner half, O = (O_a 2^(m_a - M) + O_b 2^(m_b - M)) / l for this half's 32 columns
-      float* xm = xmax + ob * 256;  // by item parity: the partner reads it before the next item's barrier
-      float* xs = xsum + ob * 256;
-      xm[half * 128 + r] = m;
-      xs[half * 128 + r] = l;
-      mbar_wait(&o_full[ob], (j >> 1) & 1);
-      tc_fence_after();
-      uint32_t ra[32], rb[32];
-      tmem_ld_32x32b_x32(tmem + lane_base + 256 + ob * 2 * DH + half * 32, ra);
-      tmem_ld_32x32b_x32(tmem + lane_base + 256 + ob * 2 * DH + DH + half * 32, rb);
-      tmem_ld_wait();
-      tc_fence_before();
-      mbar_arrive(&o_empty[ob]);
-      named_bar(pair_bar, 64);
-      const float m_o = xm[(half ^ 1) * 128 + r], l_o = xs[(half ^ 1) * 128 + r];
-      const float ma = half == 0 ? m : m_o, mb = half == 0 ? m_o : m;
-      const float la = half == 0 ? l : l_o, lb = half == 0 ? l_o : l;
-      const float M = fmaxf(ma, mb);
-      const float sa = ma == -INFINITY ? 0.f : ex2(ma - M), sb = mb == -INFINITY ? 0.f : ex2(mb - M);
-      const float l_all = la * sa + lb * sb;
-      if (qpos < it.L) {
-        const float fa = sa / l_all, fb = sb / l_all;
-        uint32_t o[16];
-#pragma unroll
-        for (int jj = 0; jj < 16; ++jj)
-          o[jj] = pack_bf16(__uint_as_float(ra[2 * jj]) * fa + __uint_as_float(rb[2 * jj]) * fb,
-                            __uint_as_float(ra[2 * jj + 1]) * fa + __uint_as_float(rb[2 * jj + 1]) * fb);
-        uint4* dst = reinterpret_cast<uint4*>(out + (size_t)(it.s0 + qpos) * ldo + it.h * DH + half * 32);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) dst[u] = make_uint4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);
-        if (half == 0) lse[(size_t)it.h * T + it.s0 + qpos] = (M + log2f(l_all)) * LN2_F;
-      }
+      pend = true;
+      pit = it;
+      pj = j;
+      pm = m;
+      pl = l;
+      it = nxt;
+      w = w_next;
     }
+    if (pend) epilogue(pit, pj, pm, pl);
   }
   tc_fence_before();
   __syncthreads();
@@ -525,8 +558,11 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   if (warp == 0) {
     if (lane == 0) {
       int gi = 0, j = 0;
+      BwdItem itm_n{};
+      if (snake_item(0) < n_items) itm_n = bwd_item<CAUSAL>(snake_item(0), Hk, G, cu, tiles);
       for (int w = snake_item(0); w < n_items; w = snake_item(j + 1), ++j) {
-        const BwdItem itm = bwd_item<CAUSAL>(w, Hk, G, cu, tiles);
+        const BwdItem itm = itm_n;
+        if (snake_item(j + 1) < n_items) itm_n = bwd_item<CAUSAL>(snake_item(j + 1), Hk, G, cu, tiles);  // prefetch
         const int kb = j & 1;
         mbar_wait(&kv_empty[kb], ((j >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(&kv_full[kb], 2 * TILE_BYTES);
@@ -631,8 +667,11 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     const int r = q4 * 32 + lane;  // query row of the dQ tile
     const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
     int gi = 0, j = 0;
+    BwdItem itm_n{};
+    if (snake_item(0) < n_items) itm_n = bwd_item<CAUSAL>(snake_item(0), Hk, G, cu, tiles);
     for (int w = snake_item(0); w < n_items; w = snake_item(j + 1), ++j) {
-      const BwdItem itm = bwd_item<CAUSAL>(w, Hk, G, cu, tiles);
+      const BwdItem itm = itm_n;
+      if (snake_item(j + 1) < n_items) itm_n = bwd_item<CAUSAL>(snake_item(j + 1), Hk, G, cu, tiles);  // prefetch
       for (int it = 0; it < itm.n_it; ++it, ++gi) {
         const int g = it / itm.n_q, qt = itm.qt_first + it % itm.n_q;
         const int h = itm.hk * G + g;
@@ -666,8 +705,11 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     unsigned char* pt = sm + BwdSmem::PT;
     unsigned char* dst = sm + BwdSmem::DST;
     int gi = 0, j = 0;
+    BwdItem itm_n{};
+    if (snake_item(0) < n_items) itm_n = bwd_item<CAUSAL>(snake_item(0), Hk, G, cu, tiles);
     for (int w = snake_item(0); w < n_items; w = snake_item(j + 1), ++j) {
-      const BwdItem itm = bwd_item<CAUSAL>(w, Hk, G, cu, tiles);
+      const BwdItem itm = itm_n;
+      if (snake_item(j + 1) < n_items) itm_n = bwd_item<CAUSAL>(snake_item(j + 1), Hk, G, cu, tiles);  // prefetch
       const int kvpos = itm.kv0 + r;
       for (int it = 0; it < itm.n_it; ++it, ++gi) {
         const int g = it / itm.n_q, qt = itm.qt_first + it % itm.n_q;
