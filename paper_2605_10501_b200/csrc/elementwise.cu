@@ -18,6 +18,15 @@ __device__ __forceinline__ void ld8(const __nv_bfloat16* p, float (&f)[8]) {
     f[2 * j + 1] = x.y;
   }
 }
+__device__ __forceinline__ void unpack8(const uint4& v, float (&f)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float2 x = __bfloat1622float2(h[j]);
+    f[2 * j] = x.x;
+    f[2 * j + 1] = x.y;
+  }
+}
 __device__ __forceinline__ void st8(__nv_bfloat16* p, const float (&f)[8]) {
   uint4 v;
   __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
@@ -109,6 +118,54 @@ __global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(const __nv_bfloat16* _
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[k][j] = 0.f;
   }
+  if constexpr (NV <= 4) {
+  // raw 16-byte vectors of the next row (dy, h, dres) are prefetched while the current row is
+  // reduced, so every warp keeps 3 x NV x 16 B per lane in flight across its rows
+  const int step = gridDim.x * nw;
+  int row = blockIdx.x * nw + warp;
+  uint4 ndy[NV], nh[NV], nres[NV];
+  auto fetch = [&](int rw) {
+    const size_t base = (size_t)rw * d;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const int c = (k * 32 + lane) * 8;
+      ndy[k] = *reinterpret_cast<const uint4*>(dy + base + c);
+      nh[k] = *reinterpret_cast<const uint4*>(h + base + c);
+      nres[k] = dres != nullptr ? *reinterpret_cast<const uint4*>(dres + base + c) : make_uint4(0, 0, 0, 0);
+    }
+  };
+  if (row < T) fetch(row);
+  for (; row < T; row += step) {
+    const size_t base = (size_t)row * d;
+    const float r = rstd[row];
+    float g[NV][8], hn[NV][8], o[NV][8];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      unpack8(ndy[k], g[k]);
+      unpack8(nh[k], hn[k]);
+      unpack8(nres[k], o[k]);
+    }
+    if (row + step < T) fetch(row + step);
+    float dot = 0.f;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        hn[k][j] *= r;
+        dot += hn[k][j] * wv[k][j] * g[k][j];
+        acc[k][j] += g[k][j] * hn[k][j];
+      }
+    }
+    dot = warp_sum(dot) / d;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const int c = (k * 32 + lane) * 8;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[k][j] += r * (wv[k][j] * g[k][j] - hn[k][j] * dot);
+      st8(dx + base + c, o[k]);
+    }
+  }
+  } else {  // wide rows: registers cannot hold a prefetched row as well
   for (int row = blockIdx.x * nw + warp; row < T; row += gridDim.x * nw) {
     const size_t base = (size_t)row * d;
     const float r = rstd[row];
@@ -141,6 +198,7 @@ __global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(const __nv_bfloat16* _
       for (int j = 0; j < 8; ++j) o[j] += r * (wv[k][j] * g[k][j] - hn[k][j] * dot);
       st8(dx + base + c, o);
     }
+  }
   }
 #pragma unroll
   for (int k = 0; k < NV; ++k)
@@ -401,7 +459,7 @@ static int rmsnorm_generic_bwd(const void* dy, const void* h, const void* w, con
                                void* dx, float* dw, int T, int d, cudaStream_t st) {
   const size_t smem = (size_t)d * sizeof(float);
   if (ensure_smem<rmsnorm_generic_bwd_kernel>(smem)) return launch_status();
-  const int grid = T / 8 < 148 * 2 ? (T + 7) / 8 : 148 * 2;
+  const int grid = T / 8 < 148 * 3 ? (T + 7) / 8 : 148 * 3;
   rmsnorm_generic_bwd_kernel<<<grid, 256, smem, st>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)h,
                                                       (const __nv_bfloat16*)w, rstd, (const __nv_bfloat16*)dres,
                                                       (__nv_bfloat16*)dx, dw, T, d);
@@ -422,7 +480,7 @@ static int rmsnorm_bwd_launch(const void* dy, const void* h, const void* w, cons
                               void* dx, float* dw, int T, int d, cudaStream_t st) {
   const size_t smem = (size_t)d * sizeof(float);
   if (ensure_smem<rmsnorm_bwd_kernel<NV>>(smem)) return launch_status();
-  const int grid = T / 8 < 148 * 2 ? (T + 7) / 8 : 148 * 2;
+  const int grid = T / 8 < 148 * 3 ? (T + 7) / 8 : 148 * 3;
   rmsnorm_bwd_kernel<NV><<<grid, 256, smem, st>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)h,
                                                   (const __nv_bfloat16*)w, rstd, (const __nv_bfloat16*)dres,
                                                   (__nv_bfloat16*)dx, dw, T, d);

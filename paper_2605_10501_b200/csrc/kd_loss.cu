@@ -18,6 +18,13 @@ constexpr int KD_THREADS = 512;
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float LN2 = 0.6931471805599453f;
 
+// 2^x on the MUFU unit without exp2f's range fix-ups (arguments here are <= 0 or bounded)
+__device__ __forceinline__ float ex2a(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 struct Stat {  // online stats in the log2 domain
   float mt, st, at, ms, ss;
 };
@@ -71,26 +78,49 @@ __global__ void __launch_bounds__(KD_THREADS) kd_loss_kernel(const __nv_bfloat16
     const uint4* t4 = reinterpret_cast<const uint4*>(tl + (size_t)row * ldt);
     const uint4* s4 = reinterpret_cast<const uint4*>(sl + (size_t)row * lds);
     Stat a{-INFINITY, 0.f, 0.f, -INFINITY, 0.f};
-    for (int v = threadIdx.x; v < nvec; v += KD_THREADS) {
-      float ft[8], fs[8];
-      unpack8(t4[v], ft);
-      unpack8(s4[v], fs);
-      float mt = a.mt, ms = a.ms;
+    // four vectors per step (their loads are independent of the running stats, so they are all
+    // in flight together); the running max is only rescaled when it grows, which after the first
+    // few vectors of a row is rare -- the exponentials are what bounds this kernel next to HBM
+    for (int v0 = threadIdx.x; v0 < nvec; v0 += 4 * KD_THREADS) {
+      uint4 rt[4], rs[4];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        mt = fmaxf(mt, ft[j] * scale2);
-        ms = fmaxf(ms, fs[j] * scale2);
+      for (int u = 0; u < 4; ++u) {
+        const int v = v0 + u * KD_THREADS;
+        if (v < nvec) {
+          rt[u] = t4[v];
+          rs[u] = s4[v];
+        }
       }
-      const float ct = exp2f(a.mt - mt), cs = exp2f(a.ms - ms);
-      float st = a.st * ct, at = a.at * ct, ss = a.ss * cs;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float et = exp2f(ft[j] * scale2 - mt);
-        st += et;
-        at += et * (ft[j] - fs[j]);
-        ss += exp2f(fs[j] * scale2 - ms);
+      for (int u = 0; u < 4; ++u) {
+        if (v0 + u * KD_THREADS >= nvec) break;
+        float ft[8], fs[8];
+        unpack8(rt[u], ft);
+        unpack8(rs[u], fs);
+        float mt = a.mt, ms = a.ms;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          mt = fmaxf(mt, ft[j] * scale2);
+          ms = fmaxf(ms, fs[j] * scale2);
+        }
+        if (mt > a.mt) {  // a.mt == -inf: st = at = 0, any finite factor is fine
+          const float ct = a.mt == -INFINITY ? 0.f : ex2a(a.mt - mt);
+          a.st *= ct;
+          a.at *= ct;
+          a.mt = mt;
+        }
+        if (ms > a.ms) {
+          a.ss *= a.ms == -INFINITY ? 0.f : ex2a(a.ms - ms);
+          a.ms = ms;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float et = ex2a(fmaf(ft[j], scale2, -mt));
+          a.st += et;
+          a.at += et * (ft[j] - fs[j]);
+          a.ss += ex2a(fmaf(fs[j], scale2, -ms));
+        }
       }
-      a = Stat{mt, st, at, ms, ss};
     }
     // block reduction of the online stats
 #pragma unroll
@@ -132,8 +162,9 @@ __global__ void __launch_bounds__(KD_THREADS) kd_loss_kernel(const __nv_bfloat16
         __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&o);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const float g0 = g * (exp2f(fs[2 * j] * scale2 - f.ms) * is - exp2f(ft[2 * j] * scale2 - f.mt) * it);
-          const float g1 = g * (exp2f(fs[2 * j + 1] * scale2 - f.ms) * is - exp2f(ft[2 * j + 1] * scale2 - f.mt) * it);
+          const float g0 = g * (ex2a(fmaf(fs[2 * j], scale2, -f.ms)) * is - ex2a(fmaf(ft[2 * j], scale2, -f.mt)) * it);
+          const float g1 =
+              g * (ex2a(fmaf(fs[2 * j + 1], scale2, -f.ms)) * is - ex2a(fmaf(ft[2 * j + 1], scale2, -f.mt)) * it);
           oh[j] = __floats2bfloat162_rn(g0, g1);
         }
         d4[v] = o;
