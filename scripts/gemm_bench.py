@@ -25,7 +25,9 @@ def timeit(fn, iters=20, warm=5):
 
 def main():
     shapes = [(8192, 8192, 8192)]
-    if "--step" in sys.argv:  # the exact per-micro-batch GEMMs of the KD step (T = 4 x 2048)
+    if "--student" in sys.argv:  # the student's per-micro-batch GEMMs (T = 4 x 2048)
+        shapes = [(8192, 2304, 768), (8192, 768, 768), (8192, 6144, 768), (8192, 768, 3072), (8192, 32000, 768)]
+    elif "--step" in sys.argv:  # the exact per-micro-batch GEMMs of the KD step (T = 4 x 2048)
         shapes += [(8192, 2560, 2048), (8192, 2048, 2048), (8192, 11264, 2048), (8192, 2048, 5632),
                    (8192, 32000, 2048), (8192, 2304, 768), (8192, 768, 768), (8192, 6144, 768),
                    (8192, 768, 3072), (8192, 32000, 768)]
@@ -42,7 +44,8 @@ def main():
         t_cub = timeit(lambda: torch.matmul(a, b.t(), out=c))
         dy = torch.randn(M, N, device="cuda").bfloat16()
         dx = torch.empty(M, K, device="cuda", dtype=torch.bfloat16)
-        t_dg = timeit(lambda: dense.linear_dgrad(dy, b, dx))
+        bt = b.t().contiguous()  # the training path keeps a K-major (transposed) weight copy
+        t_dg = timeit(lambda: dense.linear_dgrad(dy, b, dx, wt=bt))
         dw = torch.zeros(N, K, device="cuda")
         t_wg = timeit(lambda: dense.linear_wgrad(dy, a, dw))
         t_cub_wg = timeit(lambda: torch.matmul(dy.t(), a))
