@@ -159,20 +159,44 @@ def run_reference(args):
 
 # ---------------------------------------------------------------------------------------------- VLM leg
 def run_vlm(args):
-    """configs[0] (tiny VLM: ViT-tiny encoder -> 2-layer GPT, 50/50 text/image) on one GPU."""
+    """configs[0] (tiny VLM: ViT-tiny encoder -> 2-layer GPT, 50/50 text/image).  N=1: sections
+    co-resident on one GPU; N=2/4/8: disjoint ViT / LLM groups (recipes.VLM_LAYOUTS) with the
+    activation and gradient handoff through the reshard message queue; 64 samples per LLM rank."""
     import torch
 
     from paper_2605_10501_b200 import instrument
-    from paper_2605_10501_b200.vlm import VLMExecutor, vlm_host_batch
+    from paper_2605_10501_b200.vlm import VLMExecutor, VLMGroupExecutor, vlm_host_batch
 
-    if args.gpus != 1:
-        raise SystemExit("the VLM workload is wired for 1 GPU (co-resident sections)")
-    B = args.batch_per_rank
-    ex = VLMExecutor(batch=B, mbs_llm=8, mbs_vit=8)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        ex = VLMGroupExecutor(world, batch_per_llm_rank=args.batch_per_rank, mbs_llm=8, mbs_vit=8)
+        layout = f"disjoint: vit dp{ex.dp_vit} (fanout {ex.f}) -> llm dp{ex.dp_llm}, NCCL handoff (mq)"
+    else:
+        ex = VLMExecutor(batch=args.batch_per_rank, mbs_llm=8, mbs_vit=8)
+        layout = "colocated vit+llm"
+    B = ex.batch
     hb = vlm_host_batch(B, seed=0)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
     for _ in range(args.warmup):
         ex.step(hb, want_loss=False)
-    torch.cuda.synchronize()
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
     launches0 = instrument.launches
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     stalls = []
@@ -181,20 +205,31 @@ def run_vlm(args):
         st = ex.step(hb, want_loss=True)
         stalls.append(st.stall_frac)
     e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
+    barrier()
+    clk = clocks.stop()
+    t = torch.tensor([e0.elapsed_time(e1), max(stalls) if getattr(ex, "role", "llm") == "llm" else 0.0],
+                     device="cuda")
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t[0].item())
     value = B * args.steps / (ms / 1e3)
-    line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": "vlm_cfg1: ViT-tiny (d192 L12) -> 2-layer GPT (d768), 50/50 text/image, "
-                               "wavefront schedule on device", "global_batch": B, "seq_len": "64..497",
-                   "parallelism": "colocated vit+llm", "note": "end-to-end: inputs copied from host every step"},
-        "section_stall_pct": 100.0 * max(stalls), "gpu_launches": (instrument.launches - launches0) // args.steps,
-        "model_tflops": ex.model_flops_per_step(hb) * args.steps / (ms / 1e3) / 1e12, "loss": st.loss,
-    }
-    print(json.dumps(line), flush=True)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": "vlm_cfg1: ViT-tiny (d192 L12) -> 2-layer GPT (d768), 50/50 text/image, "
+                                   "wavefront schedule on device", "global_batch": B, "seq_len": "64..497",
+                       "parallelism": layout, "note": "end-to-end: inputs copied from host every step"},
+            "section_stall_pct": 100.0 * float(t[1].item()),
+            "gpu_launches": (instrument.launches - launches0) // args.steps,
+            "model_tflops": ex.model_flops_per_step(hb) * args.steps / (ms / 1e3) / 1e12, "loss": st.loss,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 def p2p_bandwidth(ex, dist, nbytes=64 << 20, reps=4):

@@ -189,6 +189,11 @@ int maestro_attn_bwd(const void* dout, int32_t lddo, const void* q, const void* 
 /* (rope_pos/rope_cos_sin (position-tiled table, as above) non-null: dQ and dK are returned through the inverse RoPE rotation,
  * i.e. w.r.t. the pre-rotation projections.) */
 
+/* Upper bound on the SMs the persistent kernels (GEMM, attention) size their grids to; 0 = all.
+ * Executors whose NCCL point-to-point kernels run concurrently with compute reserve a few SMs so
+ * that a static persistent tile schedule never waits on a CTA that cannot become resident. */
+int maestro_set_sm_budget(int32_t n_sms);
+
 /* Reshard data mover (mq.py:163-174, 460-469): dst[box] = src[box] for an N-d box (ndim <= 6,
  * strides in elements, elem_bytes 1/2/4/8).  Used by apply_plan and Endpoint.pull to gather
  * fragments into a receiver's shard and by push_tensor to slice a sender's shard. */

@@ -92,6 +92,22 @@ def extra_symbols(names):
     return L
 
 
+def reserve_sms_for_comm(default: int = 16) -> int:
+    """Cap the persistent kernels' grids below the SM count so NCCL point-to-point kernels that
+    spin while waiting on another GPU never hold an SM a persistent CTA needs
+    (maestro_set_sm_budget).  MAESTRO_NCCL_RESERVED_SMS overrides the reserve; returns the budget."""
+    import os
+
+    import torch
+
+    reserve = int(os.environ.get("MAESTRO_NCCL_RESERVED_SMS", default))
+    n = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    budget = max(2, n - reserve) if reserve > 0 else 0
+    L = extra_symbols({"maestro_set_sm_budget": ([ctypes.c_int32], ctypes.c_int)})
+    check(L.maestro_set_sm_budget(budget), "set_sm_budget")
+    return budget
+
+
 def check(rc: int, what: str) -> None:
     if rc != 0:
         raise E.NativeError(f"{what} failed with CUDA error {rc}")

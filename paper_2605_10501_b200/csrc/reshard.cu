@@ -105,3 +105,10 @@ MAESTRO_API int maestro_box_copy(const void* src, const int64_t* src_strides, vo
   }
   return launch_status();
 }
+
+// Upper bound on the SMs persistent grids (GEMM, attention, box copy) may use; 0 = all.
+MAESTRO_API int maestro_set_sm_budget(int32_t n_sms) {
+  if (n_sms < 0) return (int)cudaErrorInvalidValue;
+  sm_budget() = n_sms;
+  return 0;
+}

@@ -34,6 +34,14 @@ inline bool make_map_2d(CUtensorMap* map, const void* base, uint64_t inner, uint
   return r == CUDA_SUCCESS;
 }
 
+// SMs a persistent grid may occupy: all of them, unless an executor reserved some for kernels
+// that run concurrently and wait on another GPU (NCCL point-to-point).  A static persistent
+// schedule stalls on every CTA that cannot become resident, so the budget keeps the grid inside
+// the SMs that are actually free (maestro_set_sm_budget).
+inline int& sm_budget() {
+  static int b = 0;  // 0 = no limit
+  return b;
+}
 inline int num_sms() {
   static int n = 0;
   if (!n) {
@@ -41,7 +49,8 @@ inline int num_sms() {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
   }
-  return n;
+  const int b = sm_budget();
+  return (b > 0 && b < n) ? (b & ~1) : n;  // even: CTA pairs
 }
 
 }  // namespace mb

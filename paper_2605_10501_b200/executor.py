@@ -164,6 +164,8 @@ class KDExecutor:
         self.tokens[self._bits["teacher"]] = seq
         self.planner.ids[: self.batch].copy_(torch.arange(self.batch, dtype=torch.int32))
         self.groups = self._make_groups()
+        if not colocated:
+            N.reserve_sms_for_comm()  # NCCL handoff kernels run concurrently with the section compute
         self.step_idx = 0
 
     # ------------------------------------------------------------------ distributed plumbing

@@ -289,3 +289,309 @@ class VLMExecutor:
         vit = 3.0 * n_img * (196 * (V.fwd_flops_per_token(196, with_head=False) + 2 * PATCH_DIM * V.d)
                              + 49 * 2 * 4 * V.d * L.d)
         return llm + vit
+
+
+def _h2d(a: np.ndarray, dev) -> torch.Tensor:
+    """Host array -> device through pinned staging (a pageable upload would block the host on the
+    stream and serialise enqueue with execution)."""
+    return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().to(dev, non_blocking=True)
+
+
+def _dist():
+    import torch.distributed as dist
+
+    return dist if dist.is_available() and dist.is_initialized() else None
+
+
+class VLMGroupExecutor:
+    """VLM step with the sections on disjoint GPU groups (cfg 1 layouts 2 / 4 / 8 GPUs).
+
+    Global ranks [0, dp_vit) host ViT ranks, [dp_vit, dp_vit + dp_llm) host LLM (critical)
+    ranks; ViT rank q serves LLM ranks q*f .. q*f+f-1 (the fan-out map, scheduling.py:366-371).
+    Every rank builds the same device schedule (K1-K4) from the same batch, so both ends of every
+    handoff know its contents:
+
+    * forward: after ViT micro-batch k, ViT rank q pushes to each LLM rank r the merged image
+      tokens of the samples of k owned by r ([n*49, d_llm] bf16, mq.Channel over NCCL);
+    * backward: after LLM micro-batch m, rank r pushes the placeholder-row gradients of m's image
+      samples back to q; q runs all forwards, then all backwards in the same order (the upstream
+      stage order of simulator.py:202-233), each backward once its gradients have arrived.
+
+    Activations and gradients of a pair travel on two separate NCCL groups so that neither
+    direction's point-to-point queue can block the other.  Per-section gradient all-reduce runs
+    over each section's own DP group.  The batch is ``batch_per_llm_rank * dp_llm`` samples.
+    """
+
+    def __init__(self, n_gpus: int, batch_per_llm_rank: int = 64, mbs_llm: int = 8, mbs_vit: int = 8,
+                 seed: int = 0, lr: float = 3e-4, policy=ExecPolicy.INTERLEAVED, device=None):
+        from . import mq
+        from .workload import SectionConfig
+
+        dist = _dist()
+        if dist is None or dist.get_world_size() != n_gpus or n_gpus < 2:
+            raise ValueError("VLMGroupExecutor needs torch.distributed with world size == n_gpus >= 2")
+        self.rank, self.world = dist.get_rank(), n_gpus
+        self.device = dev = device or torch.device("cuda", torch.cuda.current_device())
+        self.dp_llm, self.dp_vit, self.f = R.VLM_LAYOUTS[n_gpus]
+        if self.dp_llm + self.dp_vit != n_gpus:
+            raise ValueError(f"layout {R.VLM_LAYOUTS[n_gpus]} does not fill {n_gpus} GPUs")
+        self.batch = batch_per_llm_rank * self.dp_llm
+        # a ViT rank serves f LLM ranks: its micro-batches grow with the fan-out so its launch count
+        # per step stays that of one LLM rank's images (ViT-tiny micro-batches are launch-bound;
+        # with pp = 1 the per-sample 6-tuple, hence the schedule, does not depend on mbs)
+        self.mbs_llm, self.mbs_vit = mbs_llm, mbs_vit * self.f
+        self.rec = R.vlm_tiny(n_gpus, self.batch, seed)
+        self.configs = {"llm": SectionConfig(dp=self.dp_llm, mbs=mbs_llm),
+                        "vit": SectionConfig(dp=self.dp_vit, fanout=self.f, mbs=mbs_vit)}
+        self.graph = self.rec.graph
+        self.llm_shape, self.vit_shape = SHAPES["vlm_gpt2l"], SHAPES["vit_tiny"]
+        self.role = "vit" if self.rank < self.dp_vit else "llm"
+        self.q = self.rank if self.role == "vit" else None           # ViT section rank
+        self.r = self.rank - self.dp_vit if self.role == "llm" else None  # LLM section rank
+        self.seed, self.lr = seed, lr
+        if self.role == "llm":
+            self.llm = Transformer(self.llm_shape, FlatParams(self.llm_shape.param_shapes(), dev, True, seed + 10),
+                                   dev, max_pos=1024)
+        else:
+            self.vit = ViTSection(self.vit_shape, self.llm_shape.d, dev, seed + 11)
+        self.stream = torch.cuda.Stream(device=dev)
+        N.reserve_sms_for_comm()  # handoff kernels run concurrently with the section compute
+        self.planner = DevicePlanner(self.graph, self.configs, policy, max_batch=self.batch, device=dev)
+        self.cost = torch.from_numpy(cost_table(self.graph, self.configs, self.rec.params)).to(dev)
+        self.bits = {n: i for i, n in enumerate(self.graph.tables.sub_names)}
+        # process groups (created collectively, same order on every rank)
+        g_llm = dist.new_group(list(range(self.dp_vit, n_gpus)))
+        g_vit = dist.new_group(list(range(self.dp_vit)))
+        self.sec_group = g_llm if self.role == "llm" else g_vit
+        self.chan_fwd, self.chan_bwd = {}, {}
+        for r in range(self.dp_llm):
+            q = r // self.f
+            a, b = q, self.dp_vit + r
+            gf, gb = dist.new_group([a, b]), dist.new_group([a, b])
+            if self.rank == a:
+                self.chan_fwd[r] = mq.Channel((0, 0), (0, 0), mq.DistTransport(peer=b, group=gf))
+                self.chan_bwd[r] = mq.Channel((0, 0), (0, 0), mq.DistTransport(peer=b, group=gb))
+            elif self.rank == b:
+                self.chan_fwd[q] = mq.Channel((0, 0), (0, 0), mq.DistTransport(peer=a, group=gf))
+                self.chan_bwd[q] = mq.Channel((0, 0), (0, 0), mq.DistTransport(peer=a, group=gb))
+        self._eps = {}
+        self.step_idx = 0
+
+    # ------------------------------------------------------------------ plan (host view)
+    def _orders(self, hb):
+        dev, B = self.device, self.batch
+        tok = np.zeros((len(self.bits), B), dtype=np.int32)
+        tok[self.bits["llm"]] = hb["lens"]
+        tok[self.bits["vit"]] = np.where(hb["has_img"], R.VIT_PATCHES, 0)
+        tokens = _h2d(tok, dev)
+        self.planner.ids[:B].copy_(torch.arange(B, dtype=torch.int32))
+        self.planner.plan_tokens(self.cost, tokens, B)
+        tab = self.graph.tables
+        ci, vi = tab.critical, tab.section_ids.index("vit")
+        W = N.MAX_DP + 1
+        off = self.planner.sec_off.view(-1, W).cpu().numpy()
+        orders = self.planner.orders.view(-1, B).cpu().numpy()
+        llm = [orders[ci, off[ci, r]: off[ci, r + 1]] for r in range(self.dp_llm)]
+        vit = [orders[vi, off[vi, q]: off[vi, q + 1]] for q in range(self.dp_vit)]
+        return llm, vit
+
+    def _endpoint(self, peer, direction, rows):
+        from . import mq
+
+        key = (peer, direction, rows)
+        if key not in self._eps:
+            lay = mq.ShardLayout((rows, self.llm_shape.d))
+            ch = (self.chan_fwd if direction == "fwd" else self.chan_bwd)[peer]
+            self._eps[key] = mq.Endpoint((0, 0), mq.plan_reshard(lay, lay), {(0, 0): ch}, torch.bfloat16)
+        return self._eps[key]
+
+    # ------------------------------------------------------------------ one step
+    def step(self, hb: dict, want_loss: bool = True) -> StepStats:
+        dist = _dist()
+        dev = self.device
+        main = torch.cuda.current_stream(dev)
+        t0 = torch.cuda.Event(enable_timing=True)
+        t0.record(main)
+        llm_orders, vit_orders = self._orders(hb)
+        owner = np.full(self.batch, -1, dtype=np.int64)
+        for r, o in enumerate(llm_orders):
+            owner[o] = r
+        has_img = hb["has_img"]
+        grad_scale = 1.0 / max(hb["n_labels"], 1)
+        ready = torch.cuda.Event()
+        ready.record(main)
+        self.stream.wait_event(ready)
+        clock = StageClock()
+        loss_acc = torch.zeros(1, device=dev)
+        (self.vit.p if self.role == "vit" else self.llm.p).zero_grad()
+        with torch.cuda.stream(self.stream):
+            if self.role == "vit":
+                self._vit_step(hb, vit_orders[self.q], llm_orders, owner, clock)
+            else:
+                self._llm_step(hb, llm_orders[self.r], vit_orders[self.r // self.f], owner, clock, loss_acc,
+                               grad_scale)
+            p = self.vit.p if self.role == "vit" else self.llm.p
+            if dist.get_world_size(self.sec_group) > 1:
+                dist.all_reduce(p.grad, group=self.sec_group)
+            p.adamw(self.lr)
+        main.wait_stream(self.stream)
+        # loss: sum over the LLM ranks (the ViT ranks contribute 0), after the compute stream
+        dist.all_reduce(loss_acc)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t1.record(main)
+        self.step_idx += 1
+        loss = float(loss_acc.item()) * grad_scale if want_loss else None
+        t1.synchronize()
+        for ep in self._eps.values():
+            ep.verify()
+        busy, span = clock.busy_span()
+        self._last = (t0, clock)
+        return StepStats(loss, t0.elapsed_time(t1), busy, span)
+
+    def timeline(self):
+        """Stage (name, start ms, end ms) of the last step on this rank, relative to its start."""
+        t0, clock = self._last
+        return [(n, t0.elapsed_time(a), t0.elapsed_time(b)) for n, a, b in clock.marks]
+
+    def _vit_step(self, hb, order, llm_orders, owner, clock):
+        from . import mq
+
+        dev, d = self.device, self.llm_shape.d
+        mbs = self.mbs_vit
+        peers = [r for r in range(self.dp_llm) if r // self.f == self.q]
+        pixels_all = hb["pixels"]
+        ordinal = hb["img_ordinal"]
+        n_mb = -(-len(order) // mbs)
+        ctxs = []
+        for k in range(n_mb):
+            samples = order[k * mbs: (k + 1) * mbs]
+            px = _h2d(pixels_all[ordinal[samples]], dev).to(torch.bfloat16)
+            clock.begin(self.stream, f"f_bc{k}")
+            emb, st = self.vit.forward(px.view(-1, PATCH_DIM), len(samples))
+            clock.end(self.stream)
+            ctxs.append(st)
+            emb = emb.view(len(samples), 49, d)
+            for r in peers:  # this micro-batch's tokens for each LLM rank it serves
+                sel = [j for j, s in enumerate(samples) if owner[s] == r]
+                if not sel:
+                    continue
+                part = torch.empty(len(sel) * 49, d, device=dev, dtype=torch.bfloat16)
+                src = np.concatenate([np.arange(49) + 49 * j for j in sel]).astype(np.int32)
+                K.scatter_rows(emb.view(-1, d), part, _h2d(src, dev),
+                               torch.arange(part.shape[0], dtype=torch.int32, device=dev))
+                meta = mq.MessageMeta(tuple(part.shape), 2, "vit", (0, 0), int(samples[sel[0]]))
+                self.chan_fwd[r].push(part, meta, donate=True)
+        # gradient messages per LLM peer, in that rank's micro-batch order
+        expect = {}
+        for r in peers:
+            o = llm_orders[r]
+            for m in range(-(-len(o) // self.mbs_llm)):
+                mb_s = [int(s) for s in o[m * self.mbs_llm: (m + 1) * self.mbs_llm] if hb["has_img"][s]]
+                if mb_s:
+                    expect.setdefault(r, []).append(mb_s)
+        got = {}  # sample -> (tensor, row offset)
+        pulled = {r: 0 for r in expect}
+        for k in range(n_mb):
+            samples = [int(s) for s in order[k * mbs: (k + 1) * mbs]]
+            for s in samples:  # pull (in per-peer order) until every sample's rows are here
+                r = int(owner[s])
+                while s not in got:
+                    mb_s = expect[r][pulled[r]]
+                    t, _ = self._endpoint(r, "bwd", len(mb_s) * 49).pull(validate=False)
+                    for j, x in enumerate(mb_s):
+                        got[x] = (t, j * 49)
+                    pulled[r] += 1
+            demb = torch.empty(len(samples) * 49, d, device=dev, dtype=torch.bfloat16)
+            by_msg = {}
+            for j, s in enumerate(samples):
+                t, o = got.pop(s)
+                by_msg.setdefault(id(t), (t, [], []))
+                by_msg[id(t)][1].append(np.arange(49) + o)
+                by_msg[id(t)][2].append(np.arange(49) + 49 * j)
+            for t, sr, dr in by_msg.values():  # K6 row scatter from each gradient message
+                K.scatter_rows(t, demb, _h2d(np.concatenate(sr).astype(np.int32), dev),
+                               _h2d(np.concatenate(dr).astype(np.int32), dev))
+            clock.begin(self.stream, f"b_ac{k}")
+            self.vit.backward(demb, ctxs[k])
+            clock.end(self.stream)
+
+    def _llm_step(self, hb, order, vit_order, owner, clock, loss_acc, grad_scale):
+        from . import mq
+
+        dev, d = self.device, self.llm_shape.d
+        B = len(order)
+        mbs = self.mbs_llm
+        s = self.stream.cuda_stream
+        lens_h = hb["lens"]
+        o_d = _h2d(order.astype(np.int32), dev)
+        lens = _h2d(lens_h, dev)
+        ids = _h2d(hb["ids"], dev)
+        labels = _h2d(hb["labels"], dev)
+        n_mb = -(-B // mbs)
+        z = lambda k: torch.empty(k, dtype=torch.int32, device=dev)  # noqa: E731
+        mb, tok_off, mb_tok, cu, mb_start = z(B), z(B), z(n_mb), z(n_mb * (mbs + 1)), z(n_mb)
+        N.check(N.lib().maestro_varlen_pack(N.ptr(o_d), B, N.ptr(lens), mbs, N.ptr(mb), N.ptr(tok_off),
+                                            N.ptr(mb_tok), N.ptr(cu), N.ptr(mb_start), s), "varlen_pack")
+        total = int(lens_h[order].sum())
+        p_ids, p_lab = z(total), z(total)
+        for src, dst in ((ids, p_ids), (labels, p_lab)):
+            N.check(N.lib().maestro_pack_tokens(N.ptr(src), src.shape[1], N.ptr(o_d), N.ptr(lens), N.ptr(tok_off),
+                                                B, N.ptr(dst), s), "pack_tokens")
+        toff_h = np.concatenate([[0], np.cumsum(lens_h[order])[:-1]]).astype(np.int64)
+        # forward messages from the ViT rank: one per ViT micro-batch holding our images
+        msgs = []
+        for k in range(-(-len(vit_order) // self.mbs_vit)):
+            mine = [int(x) for x in vit_order[k * self.mbs_vit: (k + 1) * self.mbs_vit] if owner[x] == self.r]
+            if mine:
+                msgs.append(mine)
+        q = self.r // self.f
+        got, pulled = {}, 0
+        for m in range(n_mb):
+            ks = list(range(m * mbs, min(B, (m + 1) * mbs)))
+            samples = order[ks]
+            img = [int(x) for x in samples if hb["has_img"][x]]
+            for x in img:
+                while x not in got:
+                    mine = msgs[pulled]
+                    t, _ = self._endpoint(q, "fwd", len(mine) * 49).pull(validate=False)
+                    for j, y in enumerate(mine):
+                        got[y] = (t, j * 49)
+                    pulled += 1
+            start, T = int(toff_h[ks[0]]), int(lens_h[samples].sum())
+            cu_m = cu[m * (mbs + 1): m * (mbs + 1) + len(ks) + 1]
+            clock.begin(self.stream, f"c{m}")
+            pos = torch.empty(T, dtype=torch.int32, device=dev)
+            K.positions(cu_m, len(ks), pos)
+            b = Batch(ids=p_ids[start: start + T], cu=cu_m, pos=pos, max_len=int(lens_h[samples].max()))
+            x0 = torch.empty(T, d, device=dev, dtype=torch.bfloat16)
+            K.embed(self.llm.p["embed"], b.ids, x0)
+            dst_rows, by_msg = [], {}
+            for k, i in zip(ks, samples):
+                if hb["has_img"][i]:
+                    t, o = got.pop(int(i))
+                    base = int(toff_h[k]) - start + int(hb["img_offset"][i])
+                    dst_rows.append(base)
+                    by_msg.setdefault(id(t), (t, [], []))
+                    by_msg[id(t)][1].append(np.arange(49) + o)
+                    by_msg[id(t)][2].append(np.arange(49) + base)
+            for t, sr, dr in by_msg.values():  # K6 scatter into the packed stream at the placeholders
+                K.scatter_rows(t, x0, _h2d(np.concatenate(sr).astype(np.int32), dev),
+                               _h2d(np.concatenate(dr).astype(np.int32), dev))
+            yf, ctx = self.llm.forward(b, x0=x0)
+            logits = self.llm.logits(yf)
+            tl = torch.empty(T, device=dev)
+            K.ce_loss(logits, p_lab[start: start + T], logits, tl, grad_scale)
+            loss_acc.add_(tl.sum())
+            dx0 = self.llm.backward(ctx, dlogits=logits, need_dx0=True)
+            K.embed_bwd(dx0, b.ids, self.llm.p.g("embed"))
+            if dst_rows:  # placeholder-row gradients back to the ViT rank, in micro-batch order
+                g = torch.empty(len(dst_rows) * 49, d, device=dev, dtype=torch.bfloat16)
+                src = np.concatenate([np.arange(49) + b0 for b0 in dst_rows]).astype(np.int32)
+                K.scatter_rows(dx0, g, _h2d(src, dev),
+                               torch.arange(g.shape[0], dtype=torch.int32, device=dev))
+                meta = mq.MessageMeta(tuple(g.shape), 2, "llm", (0, 0), int(img[0]))
+                self.chan_bwd[q].push(g, meta, donate=True)
+            clock.end(self.stream)
+
+    def model_flops_per_step(self, hb) -> float:
+        return VLMExecutor.model_flops_per_step(self, hb)
