@@ -433,7 +433,10 @@ def main():
                                if dp_s > 1 else None),
             "handoff": (None if ex.colocated else
                         {"bytes_per_step": int(B // max(dp_s, 1) * SEQ * ex.tshape.d * 2),
-                         "p2p_GBps_measured": p2p, "transport": "mq.DistTransport over NCCL point-to-point"}),
+                         "p2p_GBps_measured": p2p,
+                         "transport": ("mq.PeerTransport: copy-engine puts over NVLink + stream memory-op signals"
+                                       if os.environ.get("MAESTRO_HANDOFF", "nvlink") == "nvlink"
+                                       else "mq.DistTransport over NCCL point-to-point")}),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(B * SEQ * 4),
                     "d2h_bytes_per_step": 4 + 8 * 64},
             "gpu_launches": launches // max(args.steps, 1),

@@ -194,6 +194,18 @@ int maestro_attn_bwd(const void* dout, int32_t lddo, const void* q, const void* 
  * that a static persistent tile schedule never waits on a CTA that cannot become resident. */
 int maestro_set_sm_budget(int32_t n_sms);
 
+/* One-sided NVLink handoff (mq.PeerTransport): receiver-owned slot ring + per-slot flags exported
+ * by CUDA IPC; sends are copy-engine copies into the peer slot followed by a stream memory write of
+ * the slot flag, receives are stream waits on the flag -- no kernel spins on another GPU. */
+int maestro_device_alloc(int64_t bytes, void** dev_ptr_out);
+int maestro_device_free(void* dev_ptr);
+int maestro_ipc_get_handle(const void* dev_ptr, void* handle_out /* 64 bytes */);
+int maestro_ipc_open_handle(const void* handle /* 64 bytes */, void** dev_ptr_out);
+int maestro_ipc_close(void* dev_ptr);
+int maestro_stream_wait_geq(void* stream, const void* dev_addr, uint32_t value);
+int maestro_stream_write(void* stream, void* dev_addr, uint32_t value);
+int maestro_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
+
 /* Reshard data mover (mq.py:163-174, 460-469): dst[box] = src[box] for an N-d box (ndim <= 6,
  * strides in elements, elem_bytes 1/2/4/8).  Used by apply_plan and Endpoint.pull to gather
  * fragments into a receiver's shard and by push_tensor to slice a sender's shard. */

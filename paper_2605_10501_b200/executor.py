@@ -103,6 +103,17 @@ def rank_roles(rank: int, n_gpus: int, layout: str = "colocated"):
                 recv_from=recv_from, student_ranks=list(range(dp_t, n_gpus)))
 
 
+def handoff_mode() -> str:
+    """Cross-GPU handoff transport: "nvlink" (default; mq.PeerTransport, copy-engine puts and
+    stream memory ops, no SMs) or "nccl" (mq.DistTransport, NCCL point-to-point)."""
+    import os
+
+    mode = os.environ.get("MAESTRO_HANDOFF", "nvlink")
+    if mode not in ("nvlink", "nccl"):
+        raise ValueError(f"MAESTRO_HANDOFF must be nvlink or nccl, got {mode!r}")
+    return mode
+
+
 def _dist():
     import torch.distributed as dist
 
@@ -164,7 +175,7 @@ class KDExecutor:
         self.tokens[self._bits["teacher"]] = seq
         self.planner.ids[: self.batch].copy_(torch.arange(self.batch, dtype=torch.int32))
         self.groups = self._make_groups()
-        if not colocated:
+        if not colocated and handoff_mode() == "nccl":
             N.reserve_sms_for_comm()  # NCCL handoff kernels run concurrently with the section compute
         self.step_idx = 0
 
@@ -360,7 +371,13 @@ class KDExecutor:
 
         ch = getattr(self, "_h_chan", None)
         if ch is None:
-            ch = self._h_chan = mq.Channel((0, 0), (0, 0), mq.DistTransport(peer=peer))
+            if handoff_mode() == "nvlink":  # one-sided copy-engine puts into the student's slot ring
+                role = "send" if self.teacher is not None else "recv"
+                slot = self.mbs * self.seq * self.tshape.d * 2 + (1 << 20)
+                tr = mq.PeerTransport(peer=peer, role=role, slot_bytes=slot, slots=8)
+            else:
+                tr = mq.DistTransport(peer=peer)
+            ch = self._h_chan = mq.Channel((0, 0), (0, 0), tr)
         return ch
 
     def _handoff_endpoint(self, peer: int, T: int):

@@ -396,6 +396,150 @@ class DistTransport(Transport):
         self.flush()
 
 
+_p2p = None
+
+
+def _p2p_lib():
+    global _p2p
+    if _p2p is None:
+        P, I64, U32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint32
+        _p2p = N.extra_symbols({
+            "maestro_device_alloc": ([I64, ctypes.POINTER(P)], ctypes.c_int),
+            "maestro_device_free": ([P], ctypes.c_int),
+            "maestro_ipc_get_handle": ([P, P], ctypes.c_int),
+            "maestro_ipc_open_handle": ([P, ctypes.POINTER(P)], ctypes.c_int),
+            "maestro_ipc_close": ([P], ctypes.c_int),
+            "maestro_stream_wait_geq": ([P, P, U32], ctypes.c_int),
+            "maestro_stream_write": ([P, P, U32], ctypes.c_int),
+            "maestro_copy_async": ([P, P, I64, P], ctypes.c_int),
+        })
+    return _p2p
+
+
+class PeerTransport(Transport):
+    """One-sided NVLink transport between two processes of one node (csrc/p2p.cu).
+
+    The receiver owns a ring of ``slots`` slots (a 256-byte control header + ``slot_bytes`` of
+    payload each) and one flag word per slot; the sender owns one credit word.  Both are exported
+    once through CUDA IPC.  Message i goes to slot i % slots.  Send, on the sender's stream:
+    stream-wait credit >= i - slots + 1, copy header + payload into the peer slot (copy engine),
+    stream-write the peer flag = i + 1.  Receive, on the receiver's stream: stream-wait flag >=
+    i + 1, copy the payload out, stream-write the sender's credit = i + 1.  Nothing blocks the
+    host and no kernel spins on the other GPU, so compute keeps every SM (compare DistTransport,
+    whose NCCL kernels hold SMs while they wait for the peer).  The constructor is collective
+    over the pair: both processes call it in the same order with the same sizes."""
+
+    HEADER = 256
+
+    def __init__(self, peer: int = -1, role: str = "send", slot_bytes: int = 64 << 20, slots: int = 4,
+                 group=None, _local=None) -> None:
+        L = _p2p_lib()
+        self.role, self.slots = role, slots
+        self.stride = self.HEADER + (slot_bytes + 255) // 256 * 256
+        self.slot_bytes = slot_bytes
+        self.seq = 0
+        self._owned = []
+        self._opened = []
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
+
+        def alloc(nbytes):
+            ptr = ctypes.c_void_p()
+            N.check(L.maestro_device_alloc(nbytes, ctypes.byref(ptr)), "device_alloc")
+            self._owned.append(ptr.value)
+            return ptr.value
+
+        if _local is not None:  # in-process pair (tests): share the receiver's buffers directly
+            self.flags, self.arena, self.credit = _local
+            self.peer_flags, self.peer_arena, self.peer_credit = _local
+            return
+        import torch.distributed as dist
+
+        def send_handle(ptr):
+            h = (ctypes.c_ubyte * 64)()
+            N.check(L.maestro_ipc_get_handle(ptr, h), "ipc_get_handle")
+            dist.send(torch.tensor(list(h), dtype=torch.uint8, device=dev), peer, group=group)
+
+        def recv_handle():
+            t = torch.empty(64, dtype=torch.uint8, device=dev)
+            dist.recv(t, peer, group=group)
+            h = (ctypes.c_ubyte * 64)(*t.cpu().tolist())
+            ptr = ctypes.c_void_p()
+            N.check(L.maestro_ipc_open_handle(h, ctypes.byref(ptr)), "ipc_open_handle")
+            self._opened.append(ptr.value)
+            return ptr.value
+
+        if role == "recv":
+            base = alloc(256 + slots * self.stride)  # flags (slots x u32, padded) then the slot ring
+            self.flags, self.arena = base, base + 256
+            send_handle(base)
+            self.peer_credit = recv_handle()
+        else:
+            self.credit = alloc(256)
+            base = recv_handle()
+            self.peer_flags, self.peer_arena = base, base + 256
+            send_handle(self.credit)
+
+    @classmethod
+    def local_pair(cls, slot_bytes: int = 1 << 20, slots: int = 4):
+        """(sender, receiver) in one process sharing one ring (single-GPU protocol tests)."""
+        L = _p2p_lib()
+        stride = cls.HEADER + (slot_bytes + 255) // 256 * 256
+        ptr, cred = ctypes.c_void_p(), ctypes.c_void_p()
+        N.check(L.maestro_device_alloc(256 + slots * stride, ctypes.byref(ptr)), "device_alloc")
+        N.check(L.maestro_device_alloc(256, ctypes.byref(cred)), "device_alloc")
+        bufs = (ptr.value, ptr.value + 256, cred.value)
+        tx = cls(role="send", slot_bytes=slot_bytes, slots=slots, _local=bufs)
+        rx = cls(role="recv", slot_bytes=slot_bytes, slots=slots, _local=bufs)
+        rx._owned = [ptr.value, cred.value]
+        return tx, rx
+
+    def send(self, meta: MessageMeta, payload: torch.Tensor) -> None:
+        L, st = _p2p_lib(), N.stream_ptr()
+        nbytes = payload.numel() * payload.element_size()
+        if nbytes > self.slot_bytes:
+            raise SlotExhausted(f"fragment of {nbytes} B exceeds the {self.slot_bytes} B transport slot",
+                                request=nbytes, reserved=self.slot_bytes)
+        i, slot = self.seq, self.seq % self.slots
+        if i >= self.slots:  # the receiver released this slot's previous message
+            N.check(L.maestro_stream_wait_geq(st, self.credit, i - self.slots + 1), "stream_wait")
+        hdr = _encode_header(meta).pin_memory().to(payload.device, non_blocking=True)
+        dst = self.peer_arena + slot * self.stride
+        N.check(L.maestro_copy_async(dst, hdr.data_ptr(), hdr.numel() * 8, st), "copy_async")
+        N.check(L.maestro_copy_async(dst + self.HEADER, payload.data_ptr(), nbytes, st), "copy_async")
+        N.check(L.maestro_stream_write(st, self.peer_flags + 4 * slot, i + 1), "stream_write")
+        payload.record_stream(torch.cuda.current_stream(payload.device))
+        hdr.record_stream(torch.cuda.current_stream(payload.device))
+        self.last_works = ()
+        self.seq += 1
+
+    def recv(self, shape, dtype, timeout: Optional[float] = None) -> Fragment:
+        L, st = _p2p_lib(), N.stream_ptr()
+        i, slot = self.seq, self.seq % self.slots
+        out = torch.empty(tuple(shape), dtype=_torch_dtype(dtype), device=self.device)
+        nbytes = out.numel() * out.element_size()
+        if nbytes > self.slot_bytes:
+            raise SlotExhausted(f"fragment of {nbytes} B exceeds the {self.slot_bytes} B transport slot",
+                                request=nbytes, reserved=self.slot_bytes)
+        src = self.arena + slot * self.stride
+        N.check(L.maestro_stream_wait_geq(st, self.flags + 4 * slot, i + 1), "stream_wait")
+        hdr = torch.empty(_HDR, dtype=torch.int64, device=self.device)
+        N.check(L.maestro_copy_async(hdr.data_ptr(), src, _HDR * 8, st), "copy_async")
+        N.check(L.maestro_copy_async(out.data_ptr(), src + self.HEADER, nbytes, st), "copy_async")
+        N.check(L.maestro_stream_write(st, self.peer_credit, i + 1), "stream_write")  # slot released
+        self.seq += 1
+        return Fragment(payload=out, header=hdr)
+
+    def close(self) -> None:
+        L = _p2p_lib()
+        torch.cuda.synchronize()
+        for p in self._opened:
+            L.maestro_ipc_close(p)
+        for p in self._owned:
+            L.maestro_device_free(p)
+        self._opened, self._owned = [], []
+
+
 # --- slot accounting ---------------------------------------------------------------------------
 
 
@@ -453,7 +597,7 @@ class Channel:
             raise IncompatibleShapes(f"fragment element size {fragment.element_size()} != declared "
                                      f"{meta.element_size_bytes}")
         nbytes = fragment.numel() * fragment.element_size()
-        remote = isinstance(self.transport, DistTransport)
+        remote = isinstance(self.transport, (DistTransport, PeerTransport))
         if remote:  # the receiver's slots live in another process: count bytes in flight here
             self._reap()
         self.budget.reserve(nbytes)
@@ -539,7 +683,7 @@ class Endpoint:
             for t in transfers:
                 box_copy(frags[t.sender].payload, buf[_slices(t.receiver_slice)])
         for s in self._expected:
-            if not isinstance(self.channels[s].transport, DistTransport):  # in-process slots
+            if isinstance(self.channels[s].transport, DeviceTransport):  # in-process slots
                 p = frags[s].payload
                 self.channels[s].budget.release(p.numel() * p.element_size())
         self.pulled_tensors += 1

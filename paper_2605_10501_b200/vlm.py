@@ -29,7 +29,7 @@ from . import dense as D
 from . import kernels as K
 from . import recipes as R
 from .costs import cost_table
-from .executor import StageClock, StepStats
+from .executor import StageClock, StepStats, handoff_mode
 from .scheduling import DevicePlanner, ExecPolicy
 from .synthetic import rand_int
 from .transformer import SHAPES, Batch, FlatParams, Transformer
@@ -355,7 +355,8 @@ class VLMGroupExecutor:
         else:
             self.vit = ViTSection(self.vit_shape, self.llm_shape.d, dev, seed + 11)
         self.stream = torch.cuda.Stream(device=dev)
-        N.reserve_sms_for_comm()  # handoff kernels run concurrently with the section compute
+        if handoff_mode() == "nccl":
+            N.reserve_sms_for_comm()  # NCCL handoff kernels run concurrently with the section compute
         self.planner = DevicePlanner(self.graph, self.configs, policy, max_batch=self.batch, device=dev)
         self.cost = torch.from_numpy(cost_table(self.graph, self.configs, self.rec.params)).to(dev)
         self.bits = {n: i for i, n in enumerate(self.graph.tables.sub_names)}
@@ -364,16 +365,24 @@ class VLMGroupExecutor:
         g_vit = dist.new_group(list(range(self.dp_vit)))
         self.sec_group = g_llm if self.role == "llm" else g_vit
         self.chan_fwd, self.chan_bwd = {}, {}
+        nvlink = handoff_mode() == "nvlink"
+        slot = self.mbs_vit * 49 * self.llm_shape.d * 2 + (1 << 16)  # largest fragment of a pair
+
+        def transport(peer, group, role):
+            if nvlink:  # one-sided copy-engine puts into the receiver's slot ring (csrc/p2p.cu)
+                return mq.PeerTransport(peer=peer, role=role, slot_bytes=slot, slots=16, group=group)
+            return mq.DistTransport(peer=peer, group=group)
+
         for r in range(self.dp_llm):
             q = r // self.f
             a, b = q, self.dp_vit + r
             gf, gb = dist.new_group([a, b]), dist.new_group([a, b])
             if self.rank == a:
-                self.chan_fwd[r] = mq.Channel((0, 0), (0, 0), mq.DistTransport(peer=b, group=gf))
-                self.chan_bwd[r] = mq.Channel((0, 0), (0, 0), mq.DistTransport(peer=b, group=gb))
+                self.chan_fwd[r] = mq.Channel((0, 0), (0, 0), transport(b, gf, "send"))
+                self.chan_bwd[r] = mq.Channel((0, 0), (0, 0), transport(b, gb, "recv"))
             elif self.rank == b:
-                self.chan_fwd[q] = mq.Channel((0, 0), (0, 0), mq.DistTransport(peer=a, group=gf))
-                self.chan_bwd[q] = mq.Channel((0, 0), (0, 0), mq.DistTransport(peer=a, group=gb))
+                self.chan_fwd[q] = mq.Channel((0, 0), (0, 0), transport(a, gf, "recv"))
+                self.chan_bwd[q] = mq.Channel((0, 0), (0, 0), transport(a, gb, "send"))
         self._eps = {}
         self.step_idx = 0
 

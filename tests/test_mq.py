@@ -277,3 +277,33 @@ def test_identity_plan_is_zero_copy_and_box_copy_strided():
     mq.box_copy(a.permute(0, 2, 1, 3, 4)[:, 1:4, :, ::2], b[1:4, 2:5, 3:7, 0:3, 5:12])
     torch.cuda.synchronize()
     assert torch.equal(b[1:4, 2:5, 3:7, 0:3, 5:12], a.permute(0, 2, 1, 3, 4)[:, 1:4, :, ::2])
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(60)
+def test_peer_transport_ring_protocol_on_one_gpu():
+    """PeerTransport's slot ring (flags, credits, copy-engine puts, stream memory ops) through an
+    in-process pair: six messages through two slots, pushed on one stream and pulled on another,
+    so later pushes wait (in-stream) for the receiver to release slots."""
+    src = mq.ShardLayout((64, 256))
+    plan = mq.plan_reshard(src, src)
+    tx, rx = mq.PeerTransport.local_pair(slot_bytes=64 * 256 * 2, slots=2)
+    ch_tx = mq.Channel((0, 0), (0, 0), tx)
+    ch_rx = mq.Channel((0, 0), (0, 0), rx)
+    ep = mq.Endpoint((0, 0), plan, {(0, 0): ch_rx}, torch.bfloat16)
+    s_push, s_pull = torch.cuda.Stream(), torch.cuda.Stream()
+    xs = [torch.randn(64, 256, device="cuda").bfloat16() for _ in range(6)]
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s_push):
+        for i, x in enumerate(xs):
+            ch_tx.push(x, mq.MessageMeta((64, 256), 2, "teacher", (0, 0), 100 + i))
+    got = []
+    with torch.cuda.stream(s_pull):
+        for _ in xs:
+            got.append(ep.pull(validate=False)[0])
+    torch.cuda.synchronize()
+    assert all(torch.equal(a, b) for a, b in zip(got, xs))
+    assert [m.sample_id for m in ep.verify()] == [100 + i for i in range(6)]
+    with pytest.raises(E.SlotExhausted):
+        ch_tx.push(torch.zeros(65, 256, device="cuda").bfloat16(), mq.MessageMeta((65, 256), 2, "t", (0, 0), 0))
+    rx.close()
