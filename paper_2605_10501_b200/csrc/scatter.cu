@@ -12,7 +12,6 @@ namespace mb {
 namespace {
 
 constexpr int kRowsPerWarp = 4;
-
 __global__ void __launch_bounds__(256) scatter_rows_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
                                                            const int32_t* __restrict__ src_row,
                                                            const int32_t* __restrict__ dst_row, int n_rows,
@@ -26,12 +25,19 @@ __global__ void __launch_bounds__(256) scatter_rows_kernel(const uint4* __restri
     if (r >= n_rows) return;
     const uint4* s = src + (size_t)src_row[r] * vec_per_row;
     uint4* d = dst + (size_t)dst_row[r] * vec_per_row;
-    for (int v = lane; v < vec_per_row; v += 32) {
-      uint4 x;
-      asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                   : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w)
-                   : "l"(s + v));
-      d[v] = x;
+    for (int v0 = lane; v0 < vec_per_row; v0 += 4 * 32) {  // four 16-byte loads in flight per lane
+      uint4 x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int v = v0 + u * 32;
+        if (v < vec_per_row)
+          asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(x[u].x), "=r"(x[u].y), "=r"(x[u].z), "=r"(x[u].w)
+                       : "l"(s + v));
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (v0 + u * 32 < vec_per_row) d[v0 + u * 32] = x[u];
     }
   }
 }
@@ -46,23 +52,36 @@ __global__ void __launch_bounds__(256) gather_rows_bwd_kernel(const __nv_bfloat1
   if (warp >= n_src) return;
   const int k0 = seg[warp], k1 = seg[warp + 1];
   __nv_bfloat16* out = dsrc + (size_t)warp * d;
-  for (int c = lane * 8; c < d; c += 32 * 8) {
-    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  // four 16-byte column chunks per step: their loads are independent, so they are in flight together
+  for (int c0 = lane * 8; c0 < d; c0 += 4 * 32 * 8) {
+    float acc[4][8] = {};
     for (int k = k0; k < k1; ++k) {
-      const uint4 v = *reinterpret_cast<const uint4*>(ddst + (size_t)seg_dst[k] * d + c);
-      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+      const __nv_bfloat16* row = ddst + (size_t)seg_dst[k] * d;
+      uint4 v[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float2 f = __bfloat1622float2(h[j]);
-        acc[2 * j] += f.x;
-        acc[2 * j + 1] += f.y;
+      for (int u = 0; u < 4; ++u)
+        if (c0 + u * 256 < d) v[u] = *reinterpret_cast<const uint4*>(row + c0 + u * 256);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (c0 + u * 256 >= d) break;
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v[u]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 f = __bfloat1622float2(h[j]);
+          acc[u][2 * j] += f.x;
+          acc[u][2 * j + 1] += f.y;
+        }
       }
     }
-    uint4 o;
-    __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&o);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) oh[j] = __floats2bfloat162_rn(acc[2 * j], acc[2 * j + 1]);
-    *reinterpret_cast<uint4*>(out + c) = o;
+    for (int u = 0; u < 4; ++u) {
+      if (c0 + u * 256 >= d) break;
+      uint4 o;
+      __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) oh[j] = __floats2bfloat162_rn(acc[u][2 * j], acc[u][2 * j + 1]);
+      *reinterpret_cast<uint4*>(out + c0 + u * 256) = o;
+    }
   }
 }
 
