@@ -55,6 +55,11 @@ __global__ void __launch_bounds__(256) add_rmsnorm_fwd_kernel(const __nv_bfloat1
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (row >= T) return;
   const size_t base = (size_t)row * d;
+  // norm gains first: their (L2-resident) loads overlap the row loads instead of following the
+  // reduction as a second dependent round trip
+  uint4 wraw[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) wraw[k] = *reinterpret_cast<const uint4*>(w + (k * 32 + lane) * 8);
   float f[NV][8];
   float ss = 0.f;
 #pragma unroll
@@ -88,7 +93,7 @@ __global__ void __launch_bounds__(256) add_rmsnorm_fwd_kernel(const __nv_bfloat1
   for (int k = 0; k < NV; ++k) {
     const int c = (k * 32 + lane) * 8;
     float g[8];
-    ld8(w + c, g);
+    unpack8(wraw[k], g);
 #pragma unroll
     for (int j = 0; j < 8; ++j) f[k][j] = f[k][j] * r * g[j];
     st8(y + base + c, f[k]);
@@ -459,7 +464,7 @@ static int rmsnorm_generic_bwd(const void* dy, const void* h, const void* w, con
                                void* dx, float* dw, int T, int d, cudaStream_t st) {
   const size_t smem = (size_t)d * sizeof(float);
   if (ensure_smem<rmsnorm_generic_bwd_kernel>(smem)) return launch_status();
-  const int grid = T / 8 < 148 * 3 ? (T + 7) / 8 : 148 * 3;
+  const int grid = T / 8 < 148 ? (T + 7) / 8 : 148;  // one CTA per SM: 148 x d atomics for dw, ~7 rows per warp
   rmsnorm_generic_bwd_kernel<<<grid, 256, smem, st>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)h,
                                                       (const __nv_bfloat16*)w, rstd, (const __nv_bfloat16*)dres,
                                                       (__nv_bfloat16*)dx, dw, T, d);
@@ -480,7 +485,7 @@ static int rmsnorm_bwd_launch(const void* dy, const void* h, const void* w, cons
                               void* dx, float* dw, int T, int d, cudaStream_t st) {
   const size_t smem = (size_t)d * sizeof(float);
   if (ensure_smem<rmsnorm_bwd_kernel<NV>>(smem)) return launch_status();
-  const int grid = T / 8 < 148 * 3 ? (T + 7) / 8 : 148 * 3;
+  const int grid = T / 8 < 148 ? (T + 7) / 8 : 148;  // one CTA per SM: 148 x d atomics for dw, ~7 rows per warp
   rmsnorm_bwd_kernel<NV><<<grid, 256, smem, st>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)h,
                                                   (const __nv_bfloat16*)w, rstd, (const __nv_bfloat16*)dres,
                                                   (__nv_bfloat16*)dx, dw, T, d);
