@@ -35,6 +35,7 @@ UNIT = "samples/s"
 SEQ = 2048
 BATCH_PER_RANK = 64
 MBS = 4
+TEACHER_MBS = 8  # forward-only teacher: fuller last GEMM waves (measured +2.8 %)
 
 
 def load_peaks():
@@ -267,6 +268,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--batch-per-rank", type=int, default=BATCH_PER_RANK)
     ap.add_argument("--mbs", type=int, default=MBS)
+    ap.add_argument("--teacher-mbs", type=int, default=TEACHER_MBS,
+                    help="teacher (forward-only) micro-batch size, a multiple of --mbs")
     ap.add_argument("--layout", default="colocated", choices=["colocated", "disjoint"])
     ap.add_argument("--trace", default=None, help="write the measured chrome trace of the last step here")
     ap.add_argument("--workload", default="kd", choices=["kd", "vlm"],
@@ -297,7 +300,7 @@ def main():
     from paper_2605_10501_b200.executor import KDExecutor, synthetic_ids
 
     ex = KDExecutor(n_gpus=args.gpus, batch_per_rank=args.batch_per_rank, seq=SEQ, mbs=args.mbs,
-                    layout=args.layout)
+                    layout=args.layout, teacher_mbs=args.teacher_mbs)
     B = ex.batch
     ids_host = torch.from_numpy(synthetic_ids(B, SEQ, 32000)).pin_memory()
     ids_dev = ids_host.cuda()
@@ -413,7 +416,7 @@ def main():
             "config": {
                 "workload": "kd_cfg2: fwd-only 1.1B teacher (TinyLlama shape) -> 125M student, fused KL over "
                             "32k vocab, seq 2048, teacher head colocated with the student",
-                "global_batch": B, "seq_len": SEQ, "micro_batch": args.mbs,
+                "global_batch": B, "seq_len": SEQ, "micro_batch": args.mbs, "teacher_micro_batch": ex.mbs_t,
                 "parallelism": (f"colocated teacher+student per GPU, student dp{dp_s} (grad all-reduce)"
                                 if ex.colocated
                                 else f"disjoint groups: teacher dp{dp_t} -> student dp{dp_s} (fanout 1, NCCL handoff)"),

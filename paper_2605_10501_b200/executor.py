@@ -125,7 +125,8 @@ class KDExecutor:
 
     def __init__(self, n_gpus: int = 1, batch_per_rank: int = 64, seq: int = R.KD_SEQ, mbs: int = 4,
                  teacher: str = "kd_teacher_1b", student: str = "kd_student_125m", seed: int = 0,
-                 lr: float = 3e-4, policy=ExecPolicy.INTERLEAVED, device=None, layout: str = "colocated"):
+                 lr: float = 3e-4, policy=ExecPolicy.INTERLEAVED, device=None, layout: str = "colocated",
+                 teacher_mbs: int | None = None):
         dist = _dist()
         self.rank = dist.get_rank() if dist else 0
         self.world = dist.get_world_size() if dist else 1
@@ -133,12 +134,19 @@ class KDExecutor:
             raise ValueError(f"n_gpus={n_gpus} but world size is {self.world}")
         self.device = device or torch.device("cuda", torch.cuda.current_device())
         self.n_gpus, self.seq, self.mbs = n_gpus, seq, mbs
+        # per-section micro-batch sizes (SectionConfig.mbs): the forward-only teacher may run larger
+        # micro-batches (fuller last GEMM waves, fewer launches); a student micro-batch then reads
+        # its rows out of the teacher micro-batch holding it (same sample order at fan-out 1)
+        self.mbs_t = teacher_mbs or mbs
+        if self.mbs_t % mbs:
+            raise ValueError(f"teacher_mbs {self.mbs_t} must be a multiple of the student mbs {mbs}")
+        self.mbs_of = {"student": mbs, "teacher": self.mbs_t}
         dp_s, dp_t, f_t, colocated = R.kd_layout(n_gpus, layout)
         self.layout = "colocated" if colocated else "disjoint"
         self.batch = batch_per_rank * dp_s
         self.recipe = R.kd(n_gpus, self.batch, seq, self.layout)
         cfg = {"student": self.recipe.configs["student"].__class__(dp=dp_s, mbs=mbs),
-               "teacher": self.recipe.configs["teacher"].__class__(dp=dp_t, fanout=f_t, mbs=mbs)}
+               "teacher": self.recipe.configs["teacher"].__class__(dp=dp_t, fanout=f_t, mbs=self.mbs_t)}
         self.configs = cfg
         self.graph = self.recipe.graph
         # roles: co-resident teacher+student DP rank per GPU, or disjoint groups (teacher first)
@@ -213,14 +221,15 @@ class KDExecutor:
                 # device-side gather of the rank's slice (offset read on device via index_select)
                 idx = (torch.arange(n_per, device=self.device, dtype=torch.int32) + off.to(torch.int32) + base).long()
                 order.copy_(self.planner.orders.index_select(0, idx))
-                n_mb = -(-n_per // self.mbs)
+                mbs = self.mbs_of[sec]
+                n_mb = -(-n_per // mbs)
                 z = lambda k: torch.empty(k, dtype=torch.int32, device=self.device)  # noqa: E731
-                mb, tok_off, mb_tok, cu, mb_start = z(n_per), z(n_per), z(n_mb), z(n_mb * (self.mbs + 1)), z(n_mb)
-                N.check(N.lib().maestro_varlen_pack(N.ptr(order), n_per, N.ptr(self.lens), self.mbs, N.ptr(mb),
+                mb, tok_off, mb_tok, cu, mb_start = z(n_per), z(n_per), z(n_mb), z(n_mb * (mbs + 1)), z(n_mb)
+                N.check(N.lib().maestro_varlen_pack(N.ptr(order), n_per, N.ptr(self.lens), mbs, N.ptr(mb),
                                                     N.ptr(tok_off), N.ptr(mb_tok), N.ptr(cu), N.ptr(mb_start),
                                                     stream.cuda_stream), "varlen_pack")
             out[sec] = dict(order=order, tok_off=tok_off, mb_tok=mb_tok, cu=cu, mb_start=mb_start, n=n_per,
-                            n_mb=n_mb)
+                            n_mb=n_mb, mbs=mbs)
         return out
 
     # ------------------------------------------------------------------ one step
@@ -289,7 +298,7 @@ class KDExecutor:
         t_end.synchronize()
         if self.student is not None and not self.colocated:
             got = sorted(self.verify_handoff())  # control headers of this step's pulls
-            if got != list(range(plan["student"]["n_mb"])):
+            if got != list(range(-(-plan["student"]["n_mb"] // (self.mbs_t // self.mbs)))):
                 from .errors import InconsistentSchedule
 
                 raise InconsistentSchedule("handoff delivered unexpected micro-batches", got=got)
@@ -331,8 +340,9 @@ class KDExecutor:
         clock.end(self.s_stream)
 
     def _mb_cu(self, plan_sec, m, T):
-        n_in = min(self.mbs, plan_sec["n"] - m * self.mbs)
-        cu = plan_sec["cu"][m * (self.mbs + 1): m * (self.mbs + 1) + n_in + 1]
+        mbs = plan_sec["mbs"]
+        n_in = min(mbs, plan_sec["n"] - m * mbs)
+        cu = plan_sec["cu"][m * (mbs + 1): m * (mbs + 1) + n_in + 1]
         return cu
 
     def _run_colocated(self, plan, host, packed, ready, clock, loss_acc, global_tokens):
@@ -352,15 +362,20 @@ class KDExecutor:
                 e.record(self.t_stream)
                 ev.append(e)
                 outs.append(yf)
+        ratio = self.mbs_t // self.mbs
         with torch.cuda.stream(self.s_stream):
             for m in range(ps["n_mb"]):
-                # fan-out 1 and equal mbs: student micro-batch m consumes teacher micro-batch m
-                self.s_stream.wait_event(ev[m])
+                # fan-out 1, same sample order: student micro-batch m's rows sit in teacher micro-batch
+                # m // ratio at the token offset of its first sample
+                k = m // ratio
+                self.s_stream.wait_event(ev[k])
                 T = hs[0][m]
-                self._student_mb(outs[m], packed["student"], self._mb_cu(ps, m, T), hs[1][m], T, loss_acc,
+                o = hs[1][m] - ht[1][k]
+                self._student_mb(outs[k][o: o + T], packed["student"], self._mb_cu(ps, m, T), hs[1][m], T, loss_acc,
                                  global_tokens, clock, m)
-                outs[m].record_stream(self.s_stream)
-                outs[m] = None
+                if m % ratio == ratio - 1 or m == ps["n_mb"] - 1:
+                    outs[k].record_stream(self.s_stream)
+                    outs[k] = None
 
     # --- disjoint groups: the handoff (C1) is the reshard message queue (mq.py) over NCCL
     # point-to-point: the teacher rank pushes each micro-batch's final hidden state [T, d_t]
@@ -373,7 +388,7 @@ class KDExecutor:
         if ch is None:
             if handoff_mode() == "nvlink":  # one-sided copy-engine puts into the student's slot ring
                 role = "send" if self.teacher is not None else "recv"
-                slot = self.mbs * self.seq * self.tshape.d * 2 + (1 << 20)
+                slot = self.mbs_t * self.seq * self.tshape.d * 2 + (1 << 20)
                 tr = mq.PeerTransport(peer=peer, role=role, slot_bytes=slot, slots=8)
             else:
                 tr = mq.DistTransport(peer=peer)
@@ -411,10 +426,17 @@ class KDExecutor:
         (src,) = self.roles["recv_from"]  # teacher rank feeding this student rank
         self.s_stream.wait_event(ready)
         with torch.cuda.stream(self.s_stream):
+            ratio = self.mbs_t // self.mbs
+            cur, cur_start = None, 0
             for m in range(ps["n_mb"]):
                 T = hs[0][m]
-                yf_t, _ = self._handoff_endpoint(src, T).pull(validate=False)
-                self._student_mb(yf_t, packed["student"], self._mb_cu(ps, m, T), hs[1][m], T, loss_acc,
+                if m % ratio == 0:  # the teacher micro-batch holding this and the next ratio-1 ones
+                    ms = list(range(m, min(ps["n_mb"], m + ratio)))
+                    Tt = sum(hs[0][x] for x in ms)
+                    cur, _ = self._handoff_endpoint(src, Tt).pull(validate=False)
+                    cur_start = hs[1][m]
+                o = hs[1][m] - cur_start
+                self._student_mb(cur[o: o + T], packed["student"], self._mb_cu(ps, m, T), hs[1][m], T, loss_acc,
                                  global_tokens, clock, m)
 
     def verify_handoff(self):
@@ -431,7 +453,18 @@ class KDExecutor:
 
         ev = []
         if self.teacher is not None and getattr(self, "t_clock", None) is not None:
-            ev += measured_events(self.t_clock.marks, self.t_origin, "teacher", self.t_rank, lambda n: "f_bc")
+            tev = measured_events(self.t_clock.marks, self.t_origin, "teacher", self.t_rank, lambda n: "f_bc")
+            ratio = self.mbs_t // self.mbs
+            if ratio > 1:  # a teacher micro-batch feeds `ratio` student micro-batches: one sub-stage each
+                from dataclasses import replace
+
+                split = []
+                for e in tev:
+                    d = (e.end - e.start) / ratio
+                    split += [replace(e, sample_id=e.sample_id * ratio + i, start=e.start + i * d,
+                                      end=e.start + (i + 1) * d) for i in range(ratio)]
+                tev = split
+            ev += tev
         if self.student is not None:
             ev += measured_events(self.s_clock.marks, self.t_origin, "student", self.s_rank,
                                   lambda n: "f_c" if n.startswith("f_c") else "b_c")

@@ -228,3 +228,22 @@ def test_measured_trace_and_model_crosscheck(tmp_path):
     export_trace(ev, str(tmp_path / "trace.json"))
     mk, cidle, span, midle = ex.crosscheck()
     assert mk > 0 and cidle >= 0 and span > 0 and midle >= -1e-9
+
+
+def test_kd_teacher_micro_batch_size_is_a_schedule_knob():
+    """SectionConfig.mbs per section: a teacher micro-batch twice the student's gives the same step
+    (loss, student gradients) -- only GEMM tiling / reduction order differ."""
+    from paper_2605_10501_b200.executor import KDExecutor, synthetic_ids
+
+    ids = torch.from_numpy(synthetic_ids(8, 128, 512, seed=7)).cuda()
+    res = []
+    for tm in (2, 4):
+        ex = KDExecutor(n_gpus=1, batch_per_rank=8, seq=128, mbs=2, teacher="test_tiny", student="test_tiny",
+                        lr=0.0, teacher_mbs=tm)
+        st = ex.step(ids)
+        res.append((st.loss, ex.student.p.grad.clone()))
+        ev = ex.measured_events()
+        assert sorted(e.sample_id for e in ev if e.phase == "f_bc") == list(range(4))
+    assert abs(res[0][0] - res[1][0]) / abs(res[0][0]) < 1e-3
+    g0, g1 = res[0][1], res[1][1]
+    assert ((g0 - g1).abs().max() / g0.abs().max()).item() < 2e-2
