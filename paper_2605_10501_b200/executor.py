@@ -389,7 +389,7 @@ class KDExecutor:
             if handoff_mode() == "nvlink":  # one-sided copy-engine puts into the student's slot ring
                 role = "send" if self.teacher is not None else "recv"
                 slot = self.mbs_t * self.seq * self.tshape.d * 2 + (1 << 20)
-                tr = mq.PeerTransport(peer=peer, role=role, slot_bytes=slot, slots=8)
+                tr = mq.PeerTransport(peer=peer, role=role, slot_bytes=slot, slots=4 if slot > (64 << 20) else 8)
             else:
                 tr = mq.DistTransport(peer=peer)
             ch = self._h_chan = mq.Channel((0, 0), (0, 0), tr)
