@@ -1,15 +1,25 @@
 // K8: varlen (cu_seqlens) attention with GQA on tcgen05/TMEM, head_dim 64, causal or not.
 //
-// Forward, one CTA per (128-row query tile, head), warp-specialised:
-//   w0     TMA producer: Q tile once, then K/V tiles through a 3-stage ring (SWIZZLE_128B)
-//   w1     MMA issuer:   S_i = Q K_i^T into one of two TMEM score buffers (M=128, N=128, K=64),
-//                        then O += P_{i-1} V_{i-1} (M=128, N=64, K=128; P from smem, V MN-major),
-//                        so the tensor core computes S_i while the softmax warps work on S_{i-1}
-//   w2..w5 softmax:      one thread per query row: tcgen05.ld its 128 scores, mask, online
-//                        softmax in the log2 domain with lazy rescaling (O in TMEM is rescaled
-//                        only when the row max grows by more than 2^8), write P (bf16) into the
-//                        swizzled smem operand, and finally O / l -> bf16 rows + LSE.
-// TMEM: S0 cols [0,128), S1 [128,256), O [256,320).
+// Both directions are persistent: one CTA per SM loops over heavy-first work items dealt in
+// snake order; items come from a per-micro-batch plan (query-tile / KV-tile lists) built once by
+// maestro_attn_plan and shared by every layer.
+//
+// Forward item = (128 queries, head), warp-specialised (320 threads):
+//   w0     TMA producer: Q (double-buffered by item), K/V tiles through a 3-stage ring
+//   w1     MMA issuer:   S_i = Q K_i^T into one of two TMEM score buffers (M=128, N=128, K=64);
+//                        O += P_{i-1} V_{i-1} issued after S_i, keys 0-63 into O_a and 64-127
+//                        into O_b (V as an MN-major operand), O double-buffered by item
+//   w2..w9 softmax:      two warps per TMEM lane quadrant, each owning 64 key columns of a row
+//                        with its own online softmax (max, sum, lazy rescale of its O half when
+//                        the max grows by > 2^8); P written as a swizzled bf16 smem operand.
+//                        The item epilogue (combine the halves, normalise, store O and LSE) runs
+//                        after the next item's first tile, when the last PV has long completed.
+// TMEM: S0 [0,128) S1 [128,256), O(item parity 0) [256,384), O(parity 1) [384,512).
+//
+// Backward item = (128 keys, KV head) over its GQA heads and visible query tiles: softmax work in
+// two phases (P^T from S^T, then dS^T from dP^T) that overlap the MMAs of the neighbouring
+// phases; dV/dK accumulate in TMEM across the item; dQ tiles are drained by a dedicated
+// warpgroup with red.global.add.v4.f32; inverse RoPE fused into the dQ/dK stores.
 #include <cuda_bf16.h>
 
 #include "common.cuh"

@@ -6,14 +6,17 @@
 // three training GEMMs without transposes:  fwd  Y = X W^T      (A K-major,  B K-major)
 //                                            dgrad dX = dY W     (A K-major,  B MN-major)
 //                                            wgrad dW = dY^T X   (A MN-major, B MN-major)
-// Tile 128 x BN x 64 (BN = 256 or 128, picked per shape against wave quantisation over the
-// 148 SMs), 4/6-stage TMA ring (SWIZZLE_128B), one elected thread issues tcgen05.mma
-// (M=128, N=BN, K=16) into a double-buffered TMEM accumulator, four epilogue warps drain TMEM
-// (tcgen05.ld) while the next tile's MMAs run.  Grid = min(work units, #SMs); tiles are
-// visited in grouped-M raster order for L2 reuse.  Small-output, long-K GEMMs (weight
-// gradients) split K across CTAs and accumulate with red.global.add.v4.f32 into fp32 C.
+// A cluster of two CTAs (cta_group::2) computes a 256 x BN tile, BN in {256, 192, 128} picked
+// per shape from the per-pair cost ceil(tiles / 74) x tile cost; each CTA TMA-loads its 128 rows
+// of A and BN/2 rows of B into a 6-8-stage SWIZZLE_128B ring, one elected thread of the leader
+// issues tcgen05.mma (M=256, N=BN, K=16) into a double-buffered TMEM accumulator, and four
+// epilogue warps per CTA drain TMEM (tcgen05.ld) while the next tile's MMAs run.  The grid is
+// min(work units, SM budget); tiles are visited in grouped-M raster order for L2 reuse.  Epilogues:
+// bf16 through swizzled smem staging + TMA store, with fused RoPE / SwiGLU / residual add; fp32
+// store or accumulate; split-K (weight gradients whose tile count cannot fill the pairs) with
+// red.global.add.v4.f32.
 //
-// Warp roles (192 threads): w0 TMA producer, w1 MMA issuer + TMEM owner, w2..w5 epilogue.
+// Warp roles (192 threads per CTA): w0 TMA producer, w1 MMA issuer + TMEM owner, w2..w5 epilogue.
 #include <cuda_bf16.h>
 #include <stdlib.h>
 #include <string.h>
@@ -31,14 +34,6 @@ constexpr int BM = 128, BK = 64;
 constexpr int A_BYTES = BM * BK * 2;  // 16 KB
 constexpr int GROUP_M = 8;
 constexpr int THREADS = 192;
-
-template <int BN>
-struct Cfg {
-  static constexpr int STAGES = BN == 256 ? 4 : 6;
-  static constexpr int B_BYTES = BN * BK * 2;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-};
 
 enum Epi { EPI_BF16 = 0, EPI_F32 = 1, EPI_F32_ACC = 2, EPI_F32_ATOMIC = 3 };
 
@@ -60,211 +55,6 @@ struct TileSched {
   }
 };
 
-template <int BN, bool A_MN, bool B_MN, int EPI>
-__global__ void __launch_bounds__(THREADS, 1)
-    gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, void* C,
-                int M, int N, int K, int ldc, int splits) {
-  constexpr int STAGES = Cfg<BN>::STAGES, B_BYTES = Cfg<BN>::B_BYTES, STAGE_BYTES = Cfg<BN>::STAGE_BYTES;
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
-  // 1024-byte alignment for SWIZZLE_128B atoms
-  unsigned char* smem = align_smem_1024(smem_raw);
-  unsigned char* sA = smem;
-  unsigned char* sB = smem + STAGES * A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const TileSched sched{(M + BM - 1) / BM, (N + BN - 1) / BN};
-  const int num_units = sched.num_m * sched.num_n * splits;
-  const int kb_total = (K + BK - 1) / BK;
-  const int kb_per = (kb_total + splits - 1) / splits;
-  // work unit u -> (tile u / splits, K slice u % splits); the host derives splits from
-  // kb_per so that no K slice is empty.
-  auto unit = [&](int u, int& mb_, int& nb_, int& kb0, int& kb1) {
-    sched.coords(u / splits, mb_, nb_);
-    const int ks = u % splits;
-    kb0 = ks * kb_per;
-    kb1 = min(kb_total, kb0 + kb_per);
-  };
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&map_a);
-    tma_prefetch(&map_b);
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 128);
-    }
-    fence_barrier_init();
-  }
-  if (warp == 1) tmem_alloc(tmem_slot, 512);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      // ---------------- TMA producer
-      int s = 0;
-      uint32_t ph = 0;
-      for (int t = blockIdx.x; t < num_units; t += gridDim.x) {
-        int mb_, nb_, kb0, kb1;
-        unit(t, mb_, nb_, kb0, kb1);
-        const int m0 = mb_ * BM, n0 = nb_ * BN;
-        for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&empty[s], ph ^ 1);
-          mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
-          const int k0 = kb * BK;
-          unsigned char* a = sA + s * A_BYTES;
-          unsigned char* b = sB + s * B_BYTES;
-          if (!A_MN) {
-            tma_load_2d(a, &map_a, &full[s], k0, m0);
-          } else {
-            tma_load_2d(a, &map_a, &full[s], m0, k0);
-            tma_load_2d(a + 8192, &map_a, &full[s], m0 + 64, k0);
-          }
-          if (!B_MN) {
-            tma_load_2d(b, &map_b, &full[s], k0, n0);
-          } else {
-#pragma unroll
-            for (int j = 0; j < BN / 64; ++j) tma_load_2d(b + 8192 * j, &map_b, &full[s], n0 + 64 * j, k0);
-          }
-          if (++s == STAGES) {
-            s = 0;
-            ph ^= 1;
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer
-      constexpr uint32_t idesc = idesc_bf16_f32(BM, BN, A_MN, B_MN);
-      int s = 0;
-      uint32_t ph = 0;
-      int local = 0;
-      for (int t = blockIdx.x; t < num_units; t += gridDim.x, ++local) {
-        int mb_, nb_, kb0, kb1;
-        unit(t, mb_, nb_, kb0, kb1);
-        const int as = local & 1;
-        const uint32_t aph = (local >> 1) & 1;
-        mbar_wait(&tempty[as], aph ^ 1);
-        tc_fence_after();
-        const uint32_t d = tmem + as * BN;
-        for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&full[s], ph);
-          tc_fence_after();
-          const uint32_t a_base = smem_u32(sA + s * A_BYTES);
-          const uint32_t b_base = smem_u32(sB + s * B_BYTES);
-#pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            // K-major: +32 B per 16-element K step inside the 128 B swizzle row;
-            // MN-major: +16 K-rows of 128 B.
-            const uint64_t ad = A_MN ? smem_desc_sw128(a_base + k * 2048, 8192, 1024)
-                                     : smem_desc_sw128(a_base + k * 32, 16, 1024);
-            const uint64_t bd = B_MN ? smem_desc_sw128(b_base + k * 2048, 8192, 1024)
-                                     : smem_desc_sw128(b_base + k * 32, 16, 1024);
-            umma_bf16(d, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
-          }
-          umma_commit(&empty[s]);  // smem slot free once these MMAs retire
-          if (++s == STAGES) {
-            s = 0;
-            ph ^= 1;
-          }
-        }
-        umma_commit(&tfull[as]);  // accumulator ready for the epilogue
-      }
-    }
-  } else {
-    // ---------------- epilogue: TMEM -> registers -> global
-    const int q = warp & 3;  // TMEM lane quadrant this warp may access
-    int local = 0;
-    for (int t = blockIdx.x; t < num_units; t += gridDim.x, ++local) {
-      int mb_, nb_, kb0, kb1;
-      unit(t, mb_, nb_, kb0, kb1);
-      const int as = local & 1;
-      const uint32_t aph = (local >> 1) & 1;
-      mbar_wait(&tfull[as], aph);
-      tc_fence_after();
-      const int row = mb_ * BM + q * 32 + lane;
-      const int n0 = nb_ * BN;
-#pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + as * BN + c, r);
-        tmem_ld_wait();
-        const int col = n0 + c;
-        if (row >= M || col >= N) continue;
-        const bool full_chunk = col + 32 <= N;
-        if (EPI == EPI_BF16) {
-          __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(C) + (size_t)row * ldc + col;
-          uint32_t p[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j) p[j] = pack_bf16(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
-          const int nvec = full_chunk ? 4 : (N - col) / 8;
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (j < nvec)
-              reinterpret_cast<uint4*>(out)[j] = make_uint4(p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]);
-        } else {
-          float* out = reinterpret_cast<float*>(C) + (size_t)row * ldc + col;
-          const int nv = full_chunk ? 8 : (N - col) / 4;
-          if (EPI == EPI_F32_ATOMIC) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-              if (j < nv)
-                red_add_v4f(out + 4 * j, __uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
-                            __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
-            continue;
-          }
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            if (j >= nv) break;
-            float4 v = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
-                                   __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
-            if (EPI == EPI_F32_ACC) {
-              const float4 o = reinterpret_cast<const float4*>(out)[j];
-              v.x += o.x;
-              v.y += o.y;
-              v.z += o.z;
-              v.w += o.w;
-            }
-            reinterpret_cast<float4*>(out)[j] = v;
-          }
-        }
-      }
-      tc_fence_before();
-      mbar_arrive(&tempty[as]);
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc(tmem, 512);
-  }
-}
-
-template <int BN, bool A_MN, bool B_MN, int EPI>
-int launch(const CUtensorMap& ma, const CUtensorMap& mbm, void* C, int M, int N, int K, int ldc, int splits,
-           cudaStream_t st) {
-  constexpr int SMEM = Cfg<BN>::SMEM;
-  if (ensure_smem<gemm_kernel<BN, A_MN, B_MN, EPI>>(SMEM)) return launch_status();
-  const int units = ((M + BM - 1) / BM) * ((N + BN - 1) / BN) * splits;
-  const int grid = units < num_sms() ? units : num_sms();
-  gemm_kernel<BN, A_MN, B_MN, EPI><<<grid, THREADS, SMEM, st>>>(ma, mbm, C, M, N, K, ldc, splits);
-  return launch_status();
-}
-
-
-// ==========================================================================================
 // CTA-pair variant (cta_group::2): a cluster of 2 CTAs computes a 256 x BN2 tile.  Each CTA
 // TMA-loads its 128 rows of A and BN2/2 rows of B; completion of both halves is counted on the
 // leader's mbarrier; the leader alone issues tcgen05.mma (M=256, N=BN2), whose accumulator
@@ -576,28 +366,6 @@ int launch2(const CUtensorMap& ma, const CUtensorMap& mbm, const CUtensorMap& mc
                                                                         rope_pos, rope_cs, rope_cols, swiglu_out,
                                                                         ld_swiglu, resid, ldr);
   return launch_status();
-}
-
-// Pick BN in {256, 128} minimising ceil(tiles / SMs) * BN (work of the slowest CTA), and a
-// split-K factor for accumulate-into-fp32 GEMMs whose tile count cannot fill the machine.
-inline void plan_shape(int M, int N, int K, int epi, int& bn, int& splits) {
-  const int sms = num_sms();
-  const long long t256 = (long long)((M + BM - 1) / BM) * ((N + 255) / 256);
-  const long long t128 = (long long)((M + BM - 1) / BM) * ((N + 127) / 128);
-  const long long c256 = (t256 + sms - 1) / sms * 2, c128 = (t128 + sms - 1) / sms;
-  bn = 4 * c128 < 3 * c256 ? 128 : 256;  // BN=128 only when it cuts quantisation by > 25%
-  splits = 1;
-  const long long tiles = bn == 256 ? t256 : t128;
-  const int kb = (K + BK - 1) / BK;
-  if (epi == EPI_F32_ACC && tiles < sms && kb >= 8) {
-    bn = 256;
-    const long long t = t256;
-    int s = (int)((2 * sms + t - 1) / t);
-    s = s < kb / 4 ? s : kb / 4;
-    s = s < 1 ? 1 : s;
-    const int per = (kb + s - 1) / s;  // re-derive so that no K slice is empty
-    splits = (kb + per - 1) / per;
-  }
 }
 
 }  // namespace
