@@ -35,6 +35,8 @@ UNIT = "samples/s"
 SEQ = 2048
 BATCH_PER_RANK = 64
 MBS = 8  # student micro-batch (samples); measured: 4 -> 8 +4.8 %
+KD_WORKLOAD = ("kd_cfg2: fwd-only 1.1B teacher (TinyLlama shape) -> 125M student, fused KL over 32k vocab, "
+               "seq 2048, teacher head colocated with the student")
 TEACHER_MBS = 16  # forward-only teacher: fuller GEMM waves, fewer launches (8 -> 16 +1.5 %)
 
 
@@ -148,8 +150,8 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "kd_cfg2 (1.1B teacher fwd -> 125M student train, KL over 32k vocab, seq 2048)",
-                   "global_batch": 1, "seq_len": SEQ, "parallelism": "cpu"},
+        "config": {"workload": KD_WORKLOAD, "global_batch": args.batch_per_rank * args.gpus, "seq_len": SEQ,
+                   "parallelism": f"host CPU ({threads} threads); each step times a bounded sample of 1 sequence"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": "1 sample of 2048 tokens per step: oracle/torch_ref.py fp32 KD step "
                                    "(teacher fwd + colocated head, student fwd/bwd, KL, AdamW)"},
@@ -420,8 +422,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {
-                "workload": "kd_cfg2: fwd-only 1.1B teacher (TinyLlama shape) -> 125M student, fused KL over "
-                            "32k vocab, seq 2048, teacher head colocated with the student",
+                "workload": KD_WORKLOAD,
                 "global_batch": B, "seq_len": SEQ, "micro_batch": args.mbs, "teacher_micro_batch": ex.mbs_t,
                 "parallelism": (f"colocated teacher+student per GPU, student dp{dp_s} (grad all-reduce)"
                                 if ex.colocated
