@@ -236,6 +236,47 @@ def run_vlm(args):
         dist.destroy_process_group()
 
 
+def fp64_probe():
+    """Measured fp64 CUDA-core add throughput (adds/s) and dependent-add latency (s): the
+    denominators of the scheduler kernels' roofline (maestro_fp64_probe)."""
+    import ctypes
+
+    import torch
+
+    from paper_2605_10501_b200 import _native as N
+
+    L = N.extra_symbols({"maestro_fp64_probe": ([ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                                 ctypes.c_void_p], ctypes.c_int)})
+    out = torch.zeros(4096, dtype=torch.float64, device="cuda")
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    res = []
+    for mode, iters, blocks in ((0, 4096, sms * 8), (1, 1 << 16, 1)):
+        for rep in range(2):  # first launch warms up
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            N.check(L.maestro_fp64_probe(out.data_ptr(), mode, iters, blocks, N.stream_ptr()), "fp64_probe")
+            e1.record()
+            torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / 1e3
+        res.append(blocks * 256 * 8 * iters / t if mode == 0 else t / iters)
+    return res[0], res[1]
+
+
+def scheduler_roofline(n_per_rank, plan_ms, ops_per_sample=8):
+    """K3 (wavefront) work and critical path for ranks of n samples: insertion step k evaluates
+    k+1 candidate orders of k+1 samples (one thread each), ~8 dependent fp64 ops per sample update."""
+    add_rate, lat = fp64_probe()
+    work = sum(ops_per_sample * sum((k + 1) ** 2 for k in range(1, n)) for n in n_per_rank)
+    chain = max(ops_per_sample * sum(k + 1 for k in range(1, n)) for n in n_per_rank) * lat
+    t = plan_ms / 1e3
+    return {"fp64_add_rate_measured_Gps": add_rate / 1e9, "fp64_dep_add_latency_ns": lat * 1e9,
+            "k3_fp64_ops": work, "achieved_fp64_Gops": work / t / 1e9 if t > 0 else None,
+            "frac_of_fp64_throughput": (work / t) / add_rate if t > 0 else None,
+            "critical_path_bound_us": chain * 1e6,
+            "frac_of_latency_bound": chain / t if t > 0 else None,
+            "note": "latency-bound: the wavefront recurrence is a dependent chain per candidate order"}
+
+
 def p2p_bandwidth(ex, dist, nbytes=64 << 20, reps=4):
     """Measured NCCL point-to-point bandwidth on the handoff pairs (teacher rank -> student rank),
     GB/s on the receiver; the peak the handoff (C1) is reported against.  Disjoint layout only."""
@@ -415,6 +456,12 @@ def main():
         from paper_2605_10501_b200.simulator import export_trace
 
         export_trace(ex.measured_events(), args.trace)
+    sched_roof = None
+    if rank == 0:
+        try:
+            sched_roof = scheduler_roofline(n_sched, plan_ms)
+        except Exception as exc:  # noqa: BLE001
+            sched_roof = {"error": repr(exc)}
     if rank == 0:
         dp_s, dp_t = ex.dp_s, ex.dp_t
         line = {
@@ -437,7 +484,8 @@ def main():
                                 "definition": "step time - section busy time, max over ranks"},
             "scheduler": {"device_us_per_step": plan_ms * 1e3, "share_of_step_pct": 100.0 * plan_ms / ms_per_step,
                           "makespan_evals_per_step": sum(n * (n + 1) // 2 for n in n_sched),
-                          "placement": "K1-K5 on the main stream at step start (not overlapped)"},
+                          "placement": "K1-K5 on the main stream at step start (not overlapped)",
+                          "roofline": sched_roof},
             "grad_allreduce": ({"ms": ar_ms, "bytes": grad_bytes,
                                 "bus_GBps": 2 * (dp_s - 1) / dp_s * grad_bytes / (ar_ms / 1e3) / 1e9 if ar_ms else None}
                                if dp_s > 1 else None),

@@ -189,6 +189,10 @@ int maestro_attn_bwd(const void* dout, int32_t lddo, const void* q, const void* 
 /* (rope_pos/rope_cos_sin (position-tiled table, as above) non-null: dQ and dK are returned through the inverse RoPE rotation,
  * i.e. w.r.t. the pre-rotation projections.) */
 
+/* fp64 CUDA-core probe (scheduler roofline denominators): mode 0 = add throughput over
+ * blocks x 256 threads x 8 independent chains x iters adds; mode 1 = one dependent chain of iters adds. */
+int maestro_fp64_probe(double* out, int32_t mode, int32_t iters, int32_t blocks, void* stream);
+
 /* Upper bound on the SMs the persistent kernels (GEMM, attention) size their grids to; 0 = all.
  * Executors whose NCCL point-to-point kernels run concurrently with compute reserve a few SMs so
  * that a static persistent tile schedule never waits on a CTA that cannot become resident. */
