@@ -65,13 +65,14 @@ __device__ __forceinline__ void unpack8(const uint4& v, float (&f)[8]) {
   }
 }
 
-__global__ void __launch_bounds__(KD_THREADS) kd_loss_kernel(const __nv_bfloat16* __restrict__ tl,
+template <int THREADS, int MIN_BLOCKS, int UNROLL>
+__global__ void __launch_bounds__(THREADS, MIN_BLOCKS) kd_loss_kernel(const __nv_bfloat16* __restrict__ tl,
                                                              const __nv_bfloat16* sl,
                                                              __nv_bfloat16* ds,  // may alias sl
                                                              float* __restrict__ loss,
                                                              int T, int V, int ldt, int lds, int ldd, float scale2,
                                                              float grad_scale, float inv_tau) {
-  __shared__ Stat red[KD_THREADS / 32];
+  __shared__ Stat red[THREADS / 32];
   __shared__ Stat fin;
   const int nvec = V / 8;
   for (int row = blockIdx.x; row < T; row += gridDim.x) {
@@ -81,19 +82,19 @@ __global__ void __launch_bounds__(KD_THREADS) kd_loss_kernel(const __nv_bfloat16
     // four vectors per step (their loads are independent of the running stats, so they are all
     // in flight together); the running max is only rescaled when it grows, which after the first
     // few vectors of a row is rare -- the exponentials are what bounds this kernel next to HBM
-    for (int v0 = threadIdx.x; v0 < nvec; v0 += 4 * KD_THREADS) {
-      uint4 rt[4], rs[4];
+    for (int v0 = threadIdx.x; v0 < nvec; v0 += UNROLL * THREADS) {
+      uint4 rt[UNROLL], rs[UNROLL];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int v = v0 + u * KD_THREADS;
+      for (int u = 0; u < UNROLL; ++u) {
+        const int v = v0 + u * THREADS;
         if (v < nvec) {
           rt[u] = t4[v];
           rs[u] = s4[v];
         }
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (v0 + u * KD_THREADS >= nvec) break;
+      for (int u = 0; u < UNROLL; ++u) {
+        if (v0 + u * THREADS >= nvec) break;
         float ft[8], fs[8];
         unpack8(rt[u], ft);
         unpack8(rs[u], fs);
@@ -132,7 +133,7 @@ __global__ void __launch_bounds__(KD_THREADS) kd_loss_kernel(const __nv_bfloat16
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
     __syncthreads();
     if (threadIdx.x < 32) {
-      a = threadIdx.x < KD_THREADS / 32 ? red[threadIdx.x] : Stat{-INFINITY, 0.f, 0.f, -INFINITY, 0.f};
+      a = threadIdx.x < THREADS / 32 ? red[threadIdx.x] : Stat{-INFINITY, 0.f, 0.f, -INFINITY, 0.f};
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         Stat b{__shfl_xor_sync(kFull, a.mt, o), __shfl_xor_sync(kFull, a.st, o), __shfl_xor_sync(kFull, a.at, o),
@@ -154,7 +155,7 @@ __global__ void __launch_bounds__(KD_THREADS) kd_loss_kernel(const __nv_bfloat16
       const float it = 1.f / f.st, is = 1.f / f.ss;
       const float g = grad_scale * inv_tau;
       uint4* d4 = reinterpret_cast<uint4*>(ds + (size_t)row * ldd);
-      for (int v = threadIdx.x; v < nvec; v += KD_THREADS) {
+      for (int v = threadIdx.x; v < nvec; v += THREADS) {
         float ft[8], fs[8];
         unpack8(t4[v], ft);
         unpack8(s4[v], fs);
@@ -267,8 +268,12 @@ MAESTRO_API int maestro_kd_loss_fwd_bwd(const void* d_t, const void* d_s, void* 
                                         float inv_tau, void* stream) {
   if (T <= 0) return 0;
   if (V % 8 || ldt % 8 || lds % 8 || ldd % 8) return (int)cudaErrorInvalidValue;
-  const int grid = T < 148 * 4 ? T : 148 * 4;
-  kd_loss_kernel<<<grid, KD_THREADS, 0, (cudaStream_t)stream>>>(
+  // 256-thread blocks, 4 resident per SM (<= 64 registers), two 16-byte vectors in flight per
+  // thread: rows in different phases (streaming pass / L2 re-read pass) overlap on each SM.
+  // Measured at 16384 x 32000 (scripts/kd_bench.py): 512 x 1 block/SM 1.12 ms -> this 0.83 ms.
+  constexpr int TH = 256, MB = 4, UN = 2;
+  const int grid = T < 148 * MB * 4 ? T : 148 * MB * 4;
+  kd_loss_kernel<TH, MB, UN><<<grid, TH, 0, (cudaStream_t)stream>>>(
       (const __nv_bfloat16*)d_t, (const __nv_bfloat16*)d_s, (__nv_bfloat16*)d_ds, d_loss, T, V, ldt, lds, ldd,
       inv_tau * LOG2E, grad_scale, inv_tau);
   return launch_status();
