@@ -69,15 +69,73 @@ def effective_rate(config: SectionConfig, params: CostParams) -> float:
     return params.peak_flops_per_gpu * config.tp * config.cp * params.efficiency(config)
 
 
-def per_sample_times(section, config, params, tokens_per_sample, samples_per_rank):
-    """Host twin of the device K1 arithmetic (costs.py:105-123, 182-200)."""
-    if samples_per_rank <= 0:
-        return 0.0, 0.0
+def estimate_step_time(section: SectionSpec, config: SectionConfig, params: CostParams,
+                       tokens_per_sample: int) -> tuple[float, float]:
+    """(forward, backward) time of one micro-batch of ``config.mbs`` samples (costs.py:105-123):
+    mbs * tokens * flops_per_token / (peak * tp * cp * efficiency); backward = ratio x forward,
+    or 0 for forward-only sections."""
     check_config(section, config)
     if tokens_per_sample <= 0:
         raise InvalidDims("tokens_per_sample must be positive")
     fwd = (config.mbs * tokens_per_sample * params.flops_per_token_fwd) / effective_rate(config, params)
-    bwd = 0.0 if section.forward_only else fwd * params.bwd_fwd_ratio
+    return fwd, (0.0 if section.forward_only else fwd * params.bwd_fwd_ratio)
+
+
+def section_iteration_time(section: SectionSpec, config: SectionConfig, params: CostParams,
+                           tokens_per_sample: int, samples_per_rank: int) -> float:
+    """One DP rank's share of an iteration through a pp-deep pipeline (costs.py:159-179):
+    (m + pp - 1) * (fwd + bwd) / pp with m = ceil(samples / mbs) micro-batches."""
+    if samples_per_rank <= 0:
+        return 0.0
+    fwd, bwd = estimate_step_time(section, config, params, tokens_per_sample)
+    m = math.ceil(samples_per_rank / config.mbs)
+    return (m + config.pp - 1) * (fwd + bwd) / config.pp
+
+
+@dataclass(frozen=True)
+class MemoryEstimate:
+    """Per-GPU bytes by component (costs.py:71-92)."""
+
+    weights: float
+    optimizer_state: float
+    gradients: float
+    activations: float
+
+    @property
+    def total(self) -> float:
+        return self.weights + self.optimizer_state + self.gradients + self.activations
+
+    def as_dict(self) -> dict[str, float]:
+        return {"weights": self.weights, "optimizer_state": self.optimizer_state, "gradients": self.gradients,
+                "activations": self.activations, "total": self.total}
+
+
+def estimate_memory(section: SectionSpec, config: SectionConfig, params: CostParams,
+                    tokens_per_sample: int) -> MemoryEstimate:
+    """Per-GPU memory of one section under one config (costs.py:126-156): weights and optimizer
+    state shard over tp*pp, activations over tp*cp; forward-only sections keep no optimizer state
+    or gradients and at most ``live_microbatch_cap`` micro-batches of activations."""
+    check_config(section, config)
+    if tokens_per_sample <= 0:
+        raise InvalidDims("tokens_per_sample must be positive")
+    shard = config.tp * config.pp
+    weights = section.structural.param_count * params.bytes_per_param_weights / shard
+    if section.forward_only:
+        opt = grads = 0.0
+        live = min(config.mbs, params.live_microbatch_cap)
+    else:
+        opt = section.structural.param_count * params.bytes_per_param_optimizer / shard
+        grads = weights
+        live = float(config.mbs)
+    act = live * tokens_per_sample * params.activation_bytes_per_token / (config.tp * config.cp)
+    return MemoryEstimate(weights=weights, optimizer_state=opt, gradients=grads, activations=act)
+
+
+def per_sample_times(section, config, params, tokens_per_sample, samples_per_rank):
+    """Host twin of the device K1 arithmetic (costs.py:105-123, 182-200)."""
+    if samples_per_rank <= 0:
+        return 0.0, 0.0
+    fwd, bwd = estimate_step_time(section, config, params, tokens_per_sample)
     m = math.ceil(samples_per_rank / config.mbs)
     scale = (m + config.pp - 1) / (m * config.pp * config.mbs)
     return fwd * scale, bwd * scale
