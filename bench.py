@@ -402,6 +402,14 @@ def main():
     f1.record()
     barrier()
     ems = f0.elapsed_time(f1)
+    # one extra step with the sections serialised on one stream: per-launch GEMM throughput without
+    # the other section's kernels time-sharing the GPU (not part of the timed region)
+    instrument.start_gemm_timing()
+    with ex.serialized():
+        ex.step(ids_dev, want_loss=False)
+    torch.cuda.synchronize()
+    s_flops, s_ms, _ = instrument.stop_gemm_timing()
+    serial_tflops = s_flops / (s_ms / 1e3) / 1e12 if s_ms > 0 else None
     if dist is not None:  # loss lives on student ranks; report the first student rank's
         lt = torch.tensor([losses[-1] if losses and losses[-1] is not None else float("nan")], device="cuda")
         src = 0 if ex.colocated else ex.dp_t
@@ -502,7 +510,11 @@ def main():
                          "achieved": gemm_tflops, "peak": peak, "unit": "TFLOP/s",
                          "frac": (gemm_tflops / peak) if gemm_tflops else None, "traffic": traffic,
                          "peak_kind": f"{peak_kind} bf16_tflops_sustained",
-                         "launches_timed": gemm_n, "share_of_step": gemm_ms / ms if ms > 0 else None},
+                         "launches_timed": gemm_n, "share_of_step": gemm_ms / ms if ms > 0 else None,
+                         "achieved_serialized": serial_tflops,
+                         "note": "achieved = per-launch CUDA-event durations in the timed step, where the "
+                                 "co-resident teacher and student streams time-share the GPU; "
+                                 "achieved_serialized = the same with the sections on one stream"},
             "model_tflops": ex.model_flops_per_step() * args.steps / (ms / 1e3) / 1e12,
             "simulator_crosscheck": xcheck,
             "clocks": clk,

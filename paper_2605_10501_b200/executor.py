@@ -232,6 +232,23 @@ class KDExecutor:
                             n_mb=n_mb, mbs=mbs)
         return out
 
+    def serialized(self):
+        """Context: co-resident sections share one stream (teacher micro-batches, then student
+        ones) -- used to time each kernel without the other section's kernels sharing the GPU."""
+        from contextlib import contextmanager
+
+        @contextmanager
+        def ctx():
+            saved = self.s_stream
+            if self.colocated and self.teacher is not None:
+                self.s_stream = self.t_stream
+            try:
+                yield self
+            finally:
+                self.s_stream = saved
+
+        return ctx()
+
     # ------------------------------------------------------------------ one step
     def step(self, ids: torch.Tensor, want_loss: bool = True) -> StepStats:
         """One training iteration.  ``ids``: [batch, seq] int32 token ids (device or pinned host)."""
