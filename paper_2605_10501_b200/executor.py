@@ -239,9 +239,11 @@ class KDExecutor:
 
         @contextmanager
         def ctx():
+            if not (self.colocated and self.teacher is not None and self.student is not None):
+                yield self  # one section per rank: nothing to serialise
+                return
             saved = self.s_stream
-            if self.colocated and self.teacher is not None:
-                self.s_stream = self.t_stream
+            self.s_stream = self.t_stream
             try:
                 yield self
             finally:

@@ -247,3 +247,21 @@ def test_kd_teacher_micro_batch_size_is_a_schedule_knob():
     assert abs(res[0][0] - res[1][0]) / abs(res[0][0]) < 1e-3
     g0, g1 = res[0][1], res[1][1]
     assert ((g0 - g1).abs().max() / g0.abs().max()).item() < 2e-2
+
+
+def test_kd_uneven_batch_and_micro_batch_ratio():
+    """10 samples, student micro-batches of 4 and teacher micro-batches of 8: partial last micro-
+    batches on both sides, and a partial teacher micro-batch feeding a partial student one -- same
+    step as equal micro-batches."""
+    from paper_2605_10501_b200.executor import KDExecutor, synthetic_ids
+
+    ids = torch.from_numpy(synthetic_ids(10, 128, 512, seed=9)).cuda()
+    res = []
+    for tm in (4, 8):
+        ex = KDExecutor(n_gpus=1, batch_per_rank=10, seq=128, mbs=4, teacher="test_tiny", student="test_tiny",
+                        lr=0.0, teacher_mbs=tm)
+        st = ex.step(ids)
+        assert math.isfinite(st.loss)
+        res.append((st.loss, ex.student.p.grad.clone()))
+    assert abs(res[0][0] - res[1][0]) / abs(res[0][0]) < 1e-3
+    assert ((res[0][1] - res[1][1]).abs().max() / res[0][1].abs().max()).item() < 2e-2
