@@ -19,7 +19,6 @@ backward.  Loss: next-token cross entropy over text targets (fused full-vocab CE
 
 from __future__ import annotations
 
-import math
 
 import numpy as np
 import torch
