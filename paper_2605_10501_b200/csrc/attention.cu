@@ -19,7 +19,7 @@
 // Backward item = (128 keys, KV head) over its GQA heads and visible query tiles: softmax work in
 // two phases (P^T from S^T, then dS^T from dP^T) that overlap the MMAs of the neighbouring
 // phases; dV/dK accumulate in TMEM across the item; dQ tiles are drained by a dedicated
-// warpgroup with red.global.add.v4.f32; inverse RoPE fused into the dQ/dK stores.
+// warpgroup through swizzled smem boxes and TMA reduce-add; inverse RoPE fused into the dQ/dK stores.
 #include <cuda_bf16.h>
 
 #include "common.cuh"
@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {
       constexpr uint32_t idesc_s = idesc_bf16_f32(BQ, BKV, false, false);
       constexpr uint32_t idesc_o = idesc_bf16_f32(BQ, DH, false, true);
       // PV of global tile gp (item-local index ip) into O buffer ob
@@ -214,13 +214,16 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
         const uint32_t v_base = smem_u32(sm + FwdSmemP::V + (gp % KV_STAGES) * TILE_BYTES);
         // keys [0,64) accumulate into O_a, keys [64,128) into O_b: each softmax half keeps its own
         // running max, so the halves never synchronise inside the KV loop
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk)
-          umma_bf16(tmem + 256 + ob * 2 * DH + (kk >> 2) * DH,
-                    smem_desc_sw128(p_base + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
-                    smem_desc_sw128(v_base + kk * 2048, 8192, 1024), idesc_o, (ip > 0 || (kk & 3) > 0) ? 1u : 0u);
-        umma_commit(&v_empty[gp % KV_STAGES]);
-        umma_commit(&p_empty[pb]);
+          for (int kk = 0; kk < BKV / 16; ++kk)
+            umma_bf16(tmem + 256 + ob * 2 * DH + (kk >> 2) * DH,
+                      smem_desc_sw128(p_base + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                      smem_desc_sw128(v_base + kk * 2048, 8192, 1024), idesc_o, (ip > 0 || (kk & 3) > 0) ? 1u : 0u);
+          umma_commit(&v_empty[gp % KV_STAGES]);
+          umma_commit(&p_empty[pb]);
+        }
+        __syncwarp();
       };
       int g = 0, j = 0;
       // the PV of each tile is issued after the NEXT tile's S (also across item boundaries), so
@@ -230,7 +233,10 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       auto flush = [&]() {
         if (pend_g < 0) return;
         issue_pv(pend_g, pend_i, pend_o);
-        if (pend_last) umma_commit(&o_full[pend_o]);
+        if (pend_last) {
+          if (elect_one()) umma_commit(&o_full[pend_o]);
+          __syncwarp();
+        }
         pend_g = -1;
       };
       FwdItem it_n{};
@@ -248,13 +254,16 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
           mbar_wait(&s_empty[b], ((g >> 1) & 1) ^ 1);
           tc_fence_after();
           const uint32_t k_base = smem_u32(sm + FwdSmemP::K + st * TILE_BYTES);
+          if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < DH / 16; ++kk)
-            umma_bf16(tmem + b * BKV, smem_desc_sw128(q_base + kk * 32, 16, 1024),
-                      smem_desc_sw128(k_base + kk * 32, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
-          umma_commit(&k_empty[st]);
-          umma_commit(&s_full[b]);
-          if (i == it.n_kv - 1) umma_commit(&q_empty[qb]);  // last S of the item: Q buffer free
+            for (int kk = 0; kk < DH / 16; ++kk)
+              umma_bf16(tmem + b * BKV, smem_desc_sw128(q_base + kk * 32, 16, 1024),
+                        smem_desc_sw128(k_base + kk * 32, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+            umma_commit(&k_empty[st]);
+            umma_commit(&s_full[b]);
+            if (i == it.n_kv - 1) umma_commit(&q_empty[qb]);  // last S of the item: Q buffer free
+          }
+          __syncwarp();
           flush();
           if (i == 0) mbar_wait(&o_empty[ob], ((j >> 1) & 1) ^ 1);  // epilogue of item j-2 read O[ob]
           pend_g = g;
@@ -438,7 +447,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
 //   P1: P^T = exp2(S^T * scale2 - lse2[q])            -> bf16 smem operand     (p_ready)
 //   P2: dS^T = P^T (dP^T - D[q])                      -> bf16 smem operand     (ds_ready)
 //   dV += P^T dO, dK += dS^T Q                      (TMEM accumulators across the item)
-//   dQ_tile = dS K                                  (TMEM, drained with red.global.add.v4.f32)
+//   dQ_tile = dS K                                  (TMEM, drained by TMA reduce-add)
 // The MMA warp issues dV(i), S(i+1) during P2(i) and dK(i), dQ(i), dP(i+1) during P1(i+1), also
 // across item boundaries (K/V are double-buffered by item), so softmax and tensor core overlap.
 // Two softmax warps share each TMEM lane quadrant and split the 128 query columns (the backward
@@ -453,14 +462,11 @@ struct BwdSmem {
   static constexpr int DST = PT + P_BYTES;                  // dS^T [kv][q] bf16, 2 chunks
   static constexpr int LSE = DST + P_BYTES;                 // 2 x 128 fp32 (double-buffered by tile)
   static constexpr int DD = LSE + 1024;                     // 2 x 128 fp32
-  static constexpr int BAR = DD + 1024;
+  static constexpr int DQS = DD + 1024;                     // dQ staging: 4 drain warps x 32 rows x 32 fp32
+  static constexpr int BAR = DQS + 4 * 4096;
   static constexpr int TOTAL = BAR + 256;
 };
 
-__device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
-  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
-               : "memory");
-}
 
 
 struct BwdItem {
@@ -506,8 +512,9 @@ template <bool CAUSAL>
 __global__ void __launch_bounds__(BWD_THREADS, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                     const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_do,
-                    const int32_t* __restrict__ cu, const int2* __restrict__ tiles, const int* __restrict__ n_tiles,
-                    const float* __restrict__ lse, const float* __restrict__ Dvec, float* __restrict__ dq_acc,
+                    const __grid_constant__ CUtensorMap map_dq, const int32_t* __restrict__ cu,
+                    const int2* __restrict__ tiles, const int* __restrict__ n_tiles,
+                    const float* __restrict__ lse, const float* __restrict__ Dvec,
                     __nv_bfloat16* __restrict__ dk, int lddk, __nv_bfloat16* __restrict__ dv, int lddv, int T, int H,
                     int Hk, float scale2, float scale, const float2* __restrict__ rope_cs) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -672,10 +679,13 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       }
     }
   } else if (warp >= 10) {
-    // ---------------- dQ drain: TMEM -> fp32 reductions into dq_acc
+    // ---------------- dQ drain: TMEM -> smem (SWIZZLE_128B, 32 rows x 32 fp32 per warp) -> TMA
+    // reduce-add into the fp32 accumulator.  Rows past the sequence end are exact zeros (their
+    // dS columns were masked), so whole boxes are added; the map clips rows past T.
     const int q4 = warp & 3;
-    const int r = q4 * 32 + lane;  // query row of the dQ tile
     const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
+    unsigned char* stage = sm + BwdSmem::DQS + q4 * 4096;
+    bool staged = false;
     int gi = 0, j = 0;
     BwdItem itm_n{};
     if (snake_item(0) < n_items) itm_n = bwd_item<CAUSAL>(snake_item(0), Hk, G, cu, tiles);
@@ -685,7 +695,6 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       for (int it = 0; it < itm.n_it; ++it, ++gi) {
         const int g = it / itm.n_q, qt = itm.qt_first + it % itm.n_q;
         const int h = itm.hk * G + g;
-        const int qrow = qt * BQ + r;
         mbar_wait(dq_full, gi & 1);
         tc_fence_after();
         uint32_t qa[32], qb[32];
@@ -694,18 +703,28 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         tmem_ld_wait();
         tc_fence_before();
         mbar_arrive(dq_empty);  // TMEM free as soon as it is in registers
-        if (qrow < itm.L) {
-          float* dst_row = dq_acc + ((size_t)(itm.s0 + qrow) * H + h) * DH;
 #pragma unroll
-          for (int k = 0; k < 32; k += 4) {
-            red_add_v4(dst_row + k, __uint_as_float(qa[k]), __uint_as_float(qa[k + 1]), __uint_as_float(qa[k + 2]),
-                       __uint_as_float(qa[k + 3]));
-            red_add_v4(dst_row + 32 + k, __uint_as_float(qb[k]), __uint_as_float(qb[k + 1]),
-                       __uint_as_float(qb[k + 2]), __uint_as_float(qb[k + 3]));
+        for (int hc = 0; hc < 2; ++hc) {
+          const uint32_t* x = hc == 0 ? qa : qb;
+          if (staged) {  // the previous box has been read out of the staging buffer
+            if (lane == 0) bulk_wait_read<0>();
+            __syncwarp();
           }
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            *reinterpret_cast<uint4*>(stage + lane * 128 + ((c ^ (lane & 7)) << 4)) =
+                make_uint4(x[4 * c], x[4 * c + 1], x[4 * c + 2], x[4 * c + 3]);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_reduce_add_2d(&map_dq, stage, h * DH + hc * 32, itm.s0 + qt * BQ + q4 * 32);
+            bulk_commit();
+          }
+          staged = true;
         }
       }
     }
+    if (lane == 0) bulk_wait<0>();
   } else {
     const int q4 = warp & 3;
     const int half = (warp - 2) >> 2;  // query columns [64 * half, 64 * half + 64)
@@ -1028,6 +1047,8 @@ MAESTRO_API int maestro_attn_bwd(const void* dout, int32_t lddo, const void* q, 
   ok = ok && make_map_2d(&mk, k, (uint64_t)Hk * DH, T, ldk, 64, 128);
   ok = ok && make_map_2d(&mv, v, (uint64_t)Hk * DH, T, ldv, 64, 128);
   ok = ok && make_map_2d(&mdo, dout, (uint64_t)H * DH, T, lddo, 64, 128);
+  CUtensorMap mdq;
+  ok = ok && make_map_2d(&mdq, dq_acc, (uint64_t)H * DH, T, (uint64_t)H * DH, 32, 32, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4);
   if (!ok) return (int)cudaErrorInvalidValue;
   const int smem = BwdSmem::TOTAL + 1024;
   const int items = max_tiles * Hk;  // upper bound; the kernel reads the true count
@@ -1035,12 +1056,12 @@ MAESTRO_API int maestro_attn_bwd(const void* dout, int32_t lddo, const void* q, 
   const float scale2 = softmax_scale * LOG2E_F;
   if (causal) {
     if (ensure_smem<attn_bwd_kernel<true>>(smem)) return launch_status();
-    attn_bwd_kernel<true><<<grid, BWD_THREADS, smem, st>>>(mq, mk, mv, mdo, cu, tiles, count, lse, Dvec, dq_acc,
+    attn_bwd_kernel<true><<<grid, BWD_THREADS, smem, st>>>(mq, mk, mv, mdo, mdq, cu, tiles, count, lse, Dvec,
                                                           (__nv_bfloat16*)dk, lddk, (__nv_bfloat16*)dv, lddv, T, H, Hk,
                                                           scale2, softmax_scale, (const float2*)rope_cs);
   } else {
     if (ensure_smem<attn_bwd_kernel<false>>(smem)) return launch_status();
-    attn_bwd_kernel<false><<<grid, BWD_THREADS, smem, st>>>(mq, mk, mv, mdo, cu, tiles, count, lse, Dvec, dq_acc,
+    attn_bwd_kernel<false><<<grid, BWD_THREADS, smem, st>>>(mq, mk, mv, mdo, mdq, cu, tiles, count, lse, Dvec,
                                                            (__nv_bfloat16*)dk, lddk, (__nv_bfloat16*)dv, lddv, T, H,
                                                            Hk, scale2, softmax_scale, (const float2*)rope_cs);
   }
