@@ -21,6 +21,8 @@
 // phases; dV/dK accumulate in TMEM across the item; dQ tiles are drained by a dedicated
 // warpgroup through swizzled smem boxes and TMA reduce-add; inverse RoPE fused into the dQ/dK stores.
 #include <cuda_bf16.h>
+#include <climits>
+#include <type_traits>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -448,8 +450,11 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
 //   P2: dS^T = P^T (dP^T - D[q])                      -> bf16 smem operand     (ds_ready)
 //   dV += P^T dO, dK += dS^T Q                      (TMEM accumulators across the item)
 //   dQ_tile = dS K                                  (TMEM, drained by TMA reduce-add)
-// The MMA warp issues dV(i), S(i+1) during P2(i) and dK(i), dQ(i), dP(i+1) during P1(i+1), also
-// across item boundaries (K/V are double-buffered by item), so softmax and tensor core overlap.
+// P^T and dS^T go back to TMEM as bf16 pairs (thread = kv row = TMEM lane), so dV and dK are
+// TS-MMAs with A from TMEM (no shared-memory operand traffic; dS^T also goes to smem as the dQ
+// operand).  P1 pulls S^T into registers first and releases it (s_empty), so S(i+1) runs while
+// P1/P2(i) compute; dS^T reuses the dP^T columns, so dP(i+1) is issued after dK(i).  The order
+// also spans item boundaries (K/V are double-buffered by item).
 // Two softmax warps share each TMEM lane quadrant and split the 128 query columns (the backward
 // needs no row reductions), so every SM sub-partition interleaves two softmax warps.
 // TMEM: S^T [0,128), dP^T [128,256), dV [256,320), dK [320,384), dQ [384,448).
@@ -458,8 +463,7 @@ constexpr int BWD_THREADS = 448;  // w0 TMA, w1 MMA, w2-9 softmax (2 per lane qu
 struct BwdSmem {
   static constexpr int KV = 0;                              // 2 items x (K tile, V tile)
   static constexpr int QD = KV + 2 * 2 * TILE_BYTES;        // 2 stages x (Q tile, dO tile)
-  static constexpr int PT = QD + 2 * 2 * TILE_BYTES;        // P^T  [kv][q] bf16, 2 chunks
-  static constexpr int DST = PT + P_BYTES;                  // dS^T [kv][q] bf16, 2 chunks
+  static constexpr int DST = QD + 2 * 2 * TILE_BYTES;       // dS^T [kv][q] bf16, 2 chunks (dQ operand)
   static constexpr int LSE = DST + P_BYTES;                 // 2 x 128 fp32 (double-buffered by tile)
   static constexpr int DD = LSE + 1024;                     // 2 x 128 fp32
   static constexpr int DQS = DD + 1024;                     // dQ staging: 4 drain warps x 32 rows x 32 fp32
@@ -534,7 +538,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   uint64_t* dq_empty = bar + 15;
   uint64_t* dkv_full = bar + 16;
   uint64_t* dkv_empty = bar + 17;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 18);
+  uint64_t* s_empty = bar + 18;   // S^T TMEM loaded by the softmax warps (the next S may overwrite it)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 20);
   float* s_lse = reinterpret_cast<float*>(sm + BwdSmem::LSE);
   float* s_D = reinterpret_cast<float*>(sm + BwdSmem::DD);
 
@@ -563,6 +568,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     mbar_init(dq_empty, 128);
     mbar_init(dkv_full, 1);
     mbar_init(dkv_empty, 256);
+    mbar_init(s_empty, 256);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -570,7 +576,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  constexpr uint32_t T_ST = 0, T_DPT = 128, T_DV = 256, T_DK = 320, T_DQ = 384;
+  // P^T (bf16 pairs) lives in [448, 512): half h at 448 + 32h.  dS^T (bf16 pairs) overwrites the
+  // first 32 of each half's 64 dP^T columns once that half holds dP^T in registers.
+  constexpr uint32_t T_ST = 0, T_DPT = 128, T_DV = 256, T_DK = 320, T_DQ = 384, T_PT = 448;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -603,13 +611,14 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       constexpr uint32_t id_sp = idesc_bf16_f32(BKV, BQ, false, false);  // M = kv, N = q
       constexpr uint32_t id_kv = idesc_bf16_f32(BKV, DH, false, true);   // dV, dK: A K-major, B MN-major
       constexpr uint32_t id_dq = idesc_bf16_f32(BQ, DH, true, true);     // dQ: A = dS (MN-major view of dS^T)
-      const uint32_t pt_base = smem_u32(sm + BwdSmem::PT), ds_base = smem_u32(sm + BwdSmem::DST);
+      const uint32_t ds_base = smem_u32(sm + BwdSmem::DST);
       auto kv_base = [&](int j) { return smem_u32(sm + BwdSmem::KV + (j & 1) * 2 * TILE_BYTES); };
       auto qd_base = [&](int gi) { return smem_u32(sm + BwdSmem::QD + (gi & 1) * 2 * TILE_BYTES); };
       // S^T(gi) = K Q^T and dP^T(gi) = V dO^T of the cursor's iteration
       auto issue_s = [&](const BwdCursor<CAUSAL>& c, int gi) {
         mbar_wait(&qd_full[gi & 1], (gi >> 1) & 1);
         if (c.it == 0) mbar_wait(&kv_full[c.j & 1], (c.j >> 1) & 1);
+        if (gi >= 1) mbar_wait(s_empty, (gi - 1) & 1);  // S^T(gi-1) is in the softmax registers
         tc_fence_after();
         const uint32_t kb = kv_base(c.j), qb = qd_base(gi);
 #pragma unroll
@@ -639,29 +648,25 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         BwdCursor<CAUSAL> nxt = cur;
         nxt.next(n_items, Hk, G, cu, tiles);
         const uint32_t qb = qd_base(gi), kb = kv_base(cur.j);
+        // S^T(gi+1) as soon as P1(gi) has pulled S^T(gi) into registers: it runs while P1/P2(gi) compute
+        if (nxt.valid) issue_s(nxt, gi + 1);
         // dV += P^T dO
         mbar_wait(p_ready, gi & 1);
         if (cur.it == 0) mbar_wait(dkv_empty, (cur.j & 1) ^ 1);  // previous item's epilogue read dK/dV
         tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < BQ / 16; ++kk) {  // reduction over the 128 queries
-          const uint32_t chunk = (kk >> 2) * 16384 + (kk & 3) * 32;
-          umma_bf16(tmem + T_DV, smem_desc_sw128(pt_base + chunk, 16, 1024),
-                    smem_desc_sw128(qb + TILE_BYTES + kk * 2048, 8192, 1024), id_kv,
-                    (cur.it > 0 || kk > 0) ? 1u : 0u);
-        }
+        for (int kk = 0; kk < BQ / 16; ++kk)  // reduction over the 128 queries; A = P^T from TMEM
+          umma_bf16_ts(tmem + T_DV, tmem + T_PT + kk * 8, smem_desc_sw128(qb + TILE_BYTES + kk * 2048, 8192, 1024),
+                       id_kv, (cur.it > 0 || kk > 0) ? 1u : 0u);
         umma_commit(p_free);
-        if (nxt.valid) issue_s(nxt, gi + 1);  // S TMEM was read before p_ready
-        // dK += dS^T Q ; dQ = dS K
+        // dK += dS^T Q (A = dS^T from TMEM) ; dQ = dS K (A = dS^T smem, MN-major view)
         mbar_wait(ds_ready, gi & 1);
         mbar_wait(dq_empty, (gi & 1) ^ 1);
         tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < BQ / 16; ++kk) {
-          const uint32_t chunk = (kk >> 2) * 16384 + (kk & 3) * 32;
-          umma_bf16(tmem + T_DK, smem_desc_sw128(ds_base + chunk, 16, 1024),
-                    smem_desc_sw128(qb + kk * 2048, 8192, 1024), id_kv, (cur.it > 0 || kk > 0) ? 1u : 0u);
-        }
+        for (int kk = 0; kk < BQ / 16; ++kk)
+          umma_bf16_ts(tmem + T_DK, tmem + T_DPT + (kk >> 2) * 64 + (kk & 3) * 8,
+                       smem_desc_sw128(qb + kk * 2048, 8192, 1024), id_kv, (cur.it > 0 || kk > 0) ? 1u : 0u);
 #pragma unroll
         for (int kk = 0; kk < BKV / 16; ++kk)  // reduction over the 128 keys
           umma_bf16(tmem + T_DQ, smem_desc_sw128(ds_base + kk * 2048, 16384, 1024),
@@ -673,7 +678,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
           umma_commit(dkv_full);
           umma_commit(&kv_empty[cur.j & 1]);
         }
-        if (nxt.valid) issue_dp(nxt, gi + 1);  // dP TMEM was read before ds_ready
+        // dP^T(gi+1) after dK(gi) (in issue order) has read dS^T out of the dP^T columns
+        if (nxt.valid) issue_dp(nxt, gi + 1);
         cur = nxt;
         ++gi;
       }
@@ -731,14 +737,26 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     const int r = q4 * 32 + lane;      // kv row (S^T, dP^T, dK, dV)
     const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
     const int tid = threadIdx.x - 64;  // 0..255
-    unsigned char* pt = sm + BwdSmem::PT;
     unsigned char* dst = sm + BwdSmem::DST;
+    // This thread's lse2 (tid < 128) or D (tid >= 128) entry of iteration `it` of item `im`; loaded
+    // one iteration ahead so the global-load latency stays off the per-tile path.
+    auto fetch_row = [&](const BwdItem& im, int it) -> float {
+      const int hh = im.hk * G + it / im.n_q;
+      const int qi = (im.qt_first + it % im.n_q) * BQ + (tid & 127);
+      if (qi >= im.L) return tid < 128 ? INFINITY : 0.f;
+      return tid < 128 ? lse[(size_t)hh * T + im.s0 + qi] * LOG2E_F : Dvec[(size_t)hh * T + im.s0 + qi];
+    };
     int gi = 0, j = 0;
     BwdItem itm_n{};
-    if (snake_item(0) < n_items) itm_n = bwd_item<CAUSAL>(snake_item(0), Hk, G, cu, tiles);
+    float row_next = 0.f;
+    if (snake_item(0) < n_items) {
+      itm_n = bwd_item<CAUSAL>(snake_item(0), Hk, G, cu, tiles);
+      row_next = fetch_row(itm_n, 0);
+    }
     for (int w = snake_item(0); w < n_items; w = snake_item(j + 1), ++j) {
       const BwdItem itm = itm_n;
-      if (snake_item(j + 1) < n_items) itm_n = bwd_item<CAUSAL>(snake_item(j + 1), Hk, G, cu, tiles);  // prefetch
+      const bool has_next = snake_item(j + 1) < n_items;
+      if (has_next) itm_n = bwd_item<CAUSAL>(snake_item(j + 1), Hk, G, cu, tiles);  // prefetch
       const int kvpos = itm.kv0 + r;
       for (int it = 0; it < itm.n_it; ++it, ++gi) {
         const int g = it / itm.n_q, qt = itm.qt_first + it % itm.n_q;
@@ -746,51 +764,67 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         const int q0 = qt * BQ;
         float* lse_t = s_lse + (gi & 1) * 128;  // double-buffered: one barrier per tile suffices
         float* D_t = s_D + (gi & 1) * 128;
-        {
-          const int qi = q0 + (tid & 127);
-          const bool ok = qi < itm.L;
-          if (tid < 128)
-            lse_t[tid] = ok ? lse[(size_t)h * T + itm.s0 + qi] * LOG2E_F : INFINITY;
-          else
-            D_t[tid - 128] = ok ? Dvec[(size_t)h * T + itm.s0 + qi] : 0.f;
-        }
+        (tid < 128 ? lse_t : D_t)[tid & 127] = row_next;
+        if (it + 1 < itm.n_it)
+          row_next = fetch_row(itm, it + 1);
+        else if (has_next)
+          row_next = fetch_row(itm_n, 0);
         named_bar(1, 256);
         const bool need_mask =
             (CAUSAL && q0 < itm.kv0 + BKV - 1) || (q0 + BQ > itm.L) || (itm.kv0 + BKV > itm.L);
         // ---- P1: S^T -> P^T
         mbar_wait(s_full, gi & 1);
         tc_fence_after();
+        uint32_t sr2[2][32];
+        tmem_ld_32x32b_x32(tmem + lane_base + T_ST + half * 64, sr2[0]);
+        tmem_ld_32x32b_x32(tmem + lane_base + T_ST + half * 64 + 32, sr2[1]);
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(s_empty);
         if (gi >= 1) mbar_wait(p_free, (gi - 1) & 1);  // dV(gi-1) has read P^T
+        uint32_t pk[32];  // this row's P^T as bf16 pairs: the dV operand, and P for phase 2
+        // Two instantiations so that interior tiles carry no per-element mask code (if-converted
+        // compares and selects otherwise cost more issue slots than the exponentials).
+        auto phase1 = [&](auto masked) {
 #pragma unroll
-        for (int cc = 0; cc < 64; cc += 32) {
-          const int c0 = half * 64 + cc;
-          uint32_t sr[32];
-          tmem_ld_32x32b_x32(tmem + lane_base + T_ST + c0, sr);
-          tmem_ld_wait();
+          for (int cc = 0; cc < 64; cc += 32) {
+            const int c0 = half * 64 + cc;
+            const uint32_t* sr = sr2[cc >> 5];
+            // valid columns c0 + i: i >= lo (causal: query not before the key), i < hi (inside the sequence)
+            const int lo = CAUSAL ? kvpos - (q0 + c0) : INT_MIN;
+            const int hi = kvpos >= itm.L ? INT_MIN : itm.L - (q0 + c0);
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            float pv[8];
+            for (int u = 0; u < 4; ++u) {
+              const float4 la = *reinterpret_cast<const float4*>(lse_t + c0 + 8 * u);
+              const float4 lb = *reinterpret_cast<const float4*>(lse_t + c0 + 8 * u + 4);
+              const float lv[8] = {la.x, la.y, la.z, la.w, lb.x, lb.y, lb.z, lb.w};
+              float pv[8];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const int c = c0 + 8 * u + e;
-              pv[e] = ex2(fmaf(__uint_as_float(sr[8 * u + e]), scale2, -lse_t[c]));
-              if (need_mask) {
-                const int qpos = q0 + c;
-                if ((CAUSAL && qpos < kvpos) || qpos >= itm.L || kvpos >= itm.L) pv[e] = 0.f;
+              for (int e = 0; e < 8; ++e) {
+                pv[e] = ex2(fmaf(__uint_as_float(sr[8 * u + e]), scale2, -lv[e]));
+                if constexpr (decltype(masked)::value) {
+                  const int i = 8 * u + e;
+                  if (i < lo || i >= hi) pv[e] = 0.f;
+                }
               }
+#pragma unroll
+              for (int e = 0; e < 4; ++e) pk[cc / 2 + 4 * u + e] = pack_bf16(pv[2 * e], pv[2 * e + 1]);
             }
-            *reinterpret_cast<uint4*>(pt + p_offset(r, c0 + 8 * u)) =
-                make_uint4(pack_bf16(pv[0], pv[1]), pack_bf16(pv[2], pv[3]), pack_bf16(pv[4], pv[5]),
-                           pack_bf16(pv[6], pv[7]));
           }
-        }
-        fence_proxy_async_smem();
+        };
+        if (need_mask)
+          phase1(std::true_type{});
+        else
+          phase1(std::false_type{});
+        tmem_st_32x32b_x32(tmem + lane_base + T_PT + half * 32, pk);
+        tmem_st_wait();
         tc_fence_before();
         mbar_arrive(p_ready);
         // ---- P2: dP^T -> dS^T
         mbar_wait(dp_full, gi & 1);
         tc_fence_after();
-        if (gi >= 1) mbar_wait(ds_free, (gi - 1) & 1);  // dK/dQ(gi-1) have read dS^T
+        if (gi >= 1) mbar_wait(ds_free, (gi - 1) & 1);  // dQ(gi-1) has read the dS^T smem operand
+        uint32_t dk2[32];  // dS^T as bf16 pairs
 #pragma unroll
         for (int cc = 0; cc < 64; cc += 32) {
           const int c0 = half * 64 + cc;
@@ -799,22 +833,22 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
           tmem_ld_wait();
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            // P (bf16, as the dV MMA uses it) re-read from this thread's row of the P^T operand
-            const uint4 pp4 = *reinterpret_cast<const uint4*>(pt + p_offset(r, c0 + 8 * u));
-            const uint32_t pw[4] = {pp4.x, pp4.y, pp4.z, pp4.w};
-            float ds[8];
+            const float4 da = *reinterpret_cast<const float4*>(D_t + c0 + 8 * u);
+            const float4 db = *reinterpret_cast<const float4*>(D_t + c0 + 8 * u + 4);
+            const float dv8[8] = {da.x, da.y, da.z, da.w, db.x, db.y, db.z, db.w};
 #pragma unroll
             for (int k = 0; k < 8; k += 2) {
-              const int c = c0 + 8 * u + k;
-              const float2 pp = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pw[k >> 1]));
-              ds[k] = pp.x * (__uint_as_float(pr[8 * u + k]) - D_t[c]);
-              ds[k + 1] = pp.y * (__uint_as_float(pr[8 * u + k + 1]) - D_t[c + 1]);
+              const float2 pp = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pk[cc / 2 + 4 * u + k / 2]));
+              dk2[cc / 2 + 4 * u + k / 2] = pack_bf16(pp.x * (__uint_as_float(pr[8 * u + k]) - dv8[k]),
+                                                      pp.y * (__uint_as_float(pr[8 * u + k + 1]) - dv8[k + 1]));
             }
             *reinterpret_cast<uint4*>(dst + p_offset(r, c0 + 8 * u)) =
-                make_uint4(pack_bf16(ds[0], ds[1]), pack_bf16(ds[2], ds[3]), pack_bf16(ds[4], ds[5]),
-                           pack_bf16(ds[6], ds[7]));
+                make_uint4(dk2[cc / 2 + 4 * u], dk2[cc / 2 + 4 * u + 1], dk2[cc / 2 + 4 * u + 2], dk2[cc / 2 + 4 * u + 3]);
           }
         }
+        // dS^T into the first 32 of this half's dP^T columns (already in registers)
+        tmem_st_32x32b_x32(tmem + lane_base + T_DPT + half * 64, dk2);
+        tmem_st_wait();
         fence_proxy_async_smem();
         tc_fence_before();
         mbar_arrive(ds_ready);
