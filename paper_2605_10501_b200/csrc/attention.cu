@@ -92,8 +92,7 @@ struct FwdSmemP {
   static constexpr int Q = 0;                                  // 2 x 16 KB (by item parity)
   static constexpr int K = Q + 2 * TILE_BYTES;
   static constexpr int V = K + KV_STAGES * TILE_BYTES;
-  static constexpr int P = V + KV_STAGES * TILE_BYTES;         // 2 x 32 KB (by tile parity)
-  static constexpr int XMAX = P + 2 * P_BYTES;                 // [2 items][2 halves][128] row maxima
+  static constexpr int XMAX = V + KV_STAGES * TILE_BYTES;      // [2 items][2 halves][128] row maxima
   static constexpr int XSUM = XMAX + 2 * 2 * 128 * 4;          // [2 items][2 halves][128] row sums
   static constexpr int BAR = XSUM + 2 * 2 * 128 * 4;
   static constexpr int TOTAL = BAR + 256;
@@ -212,16 +211,15 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
         mbar_wait(&p_full[pb], (gp >> 1) & 1);
         mbar_wait(&v_full[gp % KV_STAGES], (gp / KV_STAGES) & 1);
         tc_fence_after();
-        const uint32_t p_base = smem_u32(sm + FwdSmemP::P + pb * P_BYTES);
         const uint32_t v_base = smem_u32(sm + FwdSmemP::V + (gp % KV_STAGES) * TILE_BYTES);
         // keys [0,64) accumulate into O_a, keys [64,128) into O_b: each softmax half keeps its own
-        // running max, so the halves never synchronise inside the KV loop
+        // running max, so the halves never synchronise inside the KV loop.  A = P from TMEM: half
+        // h's bf16 pairs sit in the first 32 columns of its 64 score columns of S buffer pb.
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < BKV / 16; ++kk)
-            umma_bf16(tmem + 256 + ob * 2 * DH + (kk >> 2) * DH,
-                      smem_desc_sw128(p_base + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
-                      smem_desc_sw128(v_base + kk * 2048, 8192, 1024), idesc_o, (ip > 0 || (kk & 3) > 0) ? 1u : 0u);
+            umma_bf16_ts(tmem + 256 + ob * 2 * DH + (kk >> 2) * DH, tmem + pb * BKV + (kk >> 2) * 64 + (kk & 3) * 8,
+                         smem_desc_sw128(v_base + kk * 2048, 8192, 1024), idesc_o, (ip > 0 || (kk & 3) > 0) ? 1u : 0u);
           umma_commit(&v_empty[gp % KV_STAGES]);
           umma_commit(&p_empty[pb]);
         }
@@ -286,7 +284,6 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     const int r = q * 32 + lane;
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     const int pair_bar = 2 + q;
-    unsigned char* pbuf = sm + FwdSmemP::P;
     float* xmax = reinterpret_cast<float*>(sm + FwdSmemP::XMAX);
     float* xsum = reinterpret_cast<float*>(sm + FwdSmemP::XSUM);
     // Epilogue of item jj (O buffer ob, final m / l), deferred until after the next item's first
@@ -390,7 +387,6 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
           sum4[c & 3] += s[c];
         }
         l = l * alpha + ((sum4[0] + sum4[1]) + (sum4[2] + sum4[3]));
-        if (g >= 2) mbar_wait(&p_empty[b], ((g >> 1) + 1) & 1);  // PV_{g-2} read P buffer b
         if (rescale) {
           mbar_wait(&p_empty[(g - 1) & 1], ((g - 1) >> 1) & 1);  // PV_{g-1} retired: O is final
           tc_fence_after();
@@ -405,17 +401,15 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
           }
           tmem_st_wait();
         }
-        unsigned char* pb = pbuf + b * P_BYTES;
+        // P (bf16 pairs) over the first 32 of this half's score columns: S_{g+2} is issued after
+        // PV_g, so the buffer is not rewritten before the tensor core has read P
+        {
+          uint32_t pk[32];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          uint4 v;
-          v.x = pack_bf16(s[8 * u + 0], s[8 * u + 1]);
-          v.y = pack_bf16(s[8 * u + 2], s[8 * u + 3]);
-          v.z = pack_bf16(s[8 * u + 4], s[8 * u + 5]);
-          v.w = pack_bf16(s[8 * u + 6], s[8 * u + 7]);
-          *reinterpret_cast<uint4*>(pb + p_offset(r, half * 64 + 8 * u)) = v;
+          for (int e = 0; e < 32; ++e) pk[e] = pack_bf16(s[2 * e], s[2 * e + 1]);
+          tmem_st_32x32b_x32(tmem + lane_base + b * BKV + half * 64, pk);
         }
-        fence_proxy_async_smem();
+        tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&p_full[b]);
         if (i == 0 && pend) {
