@@ -379,14 +379,20 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
           m = m_new;
           rescale = i > 0;
         }
-        float sum4[4] = {0.f, 0.f, 0.f, 0.f};
         const float neg_m = m == -INFINITY ? 0.f : -m;  // half fully masked so far: P = 0
+        // paired fp32 FMA/add (FFMA2/FADD2): half the issue slots of the scalar forms
+        const float2 sc2 = make_float2(scale2, scale2), nm2 = make_float2(neg_m, neg_m);
+        float2 sum2[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
 #pragma unroll
-        for (int c = 0; c < 64; ++c) {
-          s[c] = ex2(fmaf(s[c], scale2, neg_m));
-          sum4[c & 3] += s[c];
+        for (int c = 0; c < 64; c += 2) {
+          const float2 x = __ffma2_rn(make_float2(s[c], s[c + 1]), sc2, nm2);
+          s[c] = ex2(x.x);
+          s[c + 1] = ex2(x.y);
+          sum2[(c >> 1) & 3] = __fadd2_rn(sum2[(c >> 1) & 3], make_float2(s[c], s[c + 1]));
         }
-        l = l * alpha + ((sum4[0] + sum4[1]) + (sum4[2] + sum4[3]));
+        const float2 t01 = __fadd2_rn(sum2[0], sum2[1]), t23 = __fadd2_rn(sum2[2], sum2[3]);
+        const float2 t = __fadd2_rn(t01, t23);
+        l = l * alpha + (t.x + t.y);
         if (rescale) {
           mbar_wait(&p_empty[(g - 1) & 1], ((g - 1) >> 1) & 1);  // PV_{g-1} retired: O is final
           tc_fence_after();
