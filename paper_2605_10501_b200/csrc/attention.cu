@@ -86,6 +86,9 @@ __device__ __forceinline__ float2 ex2_fma2(float2 x) {
   return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(j.x) << 23)),
                      __int_as_float(__float_as_int(p.y) + (__float_as_int(j.y) << 23)));
 }
+#ifndef BWD_EMU_BITS
+#define BWD_EMU_BITS 0x00  // backward P^T = exp2(S^T scale2 - lse2): not MUFU-bound, all on MUFU
+#endif
 #ifndef FWD_EMU_BITS
 #define FWD_EMU_BITS 0x92  // pair p of a row's 32 goes to the FMA pipe if bit (p & 7) is set (3/8)
 #endif
@@ -763,13 +766,13 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
     const int tid = threadIdx.x - 64;  // 0..255
     unsigned char* dst = sm + BwdSmem::DST;
-    // This thread's lse2 (tid < 128) or D (tid >= 128) entry of iteration `it` of item `im`; loaded
+    // This thread's -lse2 (tid < 128) or -D (tid >= 128) entry of iteration `it` of item `im`; loaded
     // one iteration ahead so the global-load latency stays off the per-tile path.
     auto fetch_row = [&](const BwdItem& im, int it) -> float {
       const int hh = im.hk * G + it / im.n_q;
       const int qi = (im.qt_first + it % im.n_q) * BQ + (tid & 127);
-      if (qi >= im.L) return tid < 128 ? INFINITY : 0.f;
-      return tid < 128 ? lse[(size_t)hh * T + im.s0 + qi] * LOG2E_F : Dvec[(size_t)hh * T + im.s0 + qi];
+      if (qi >= im.L) return tid < 128 ? -INFINITY : 0.f;  // stored negated: -lse2, -D
+      return tid < 128 ? -lse[(size_t)hh * T + im.s0 + qi] * LOG2E_F : -Dvec[(size_t)hh * T + im.s0 + qi];
     };
     int gi = 0, j = 0;
     BwdItem itm_n{};
@@ -825,8 +828,20 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
               const float lv[8] = {la.x, la.y, la.z, la.w, lb.x, lb.y, lb.z, lb.w};
               float pv[8];
 #pragma unroll
+              for (int e = 0; e < 8; e += 2) {
+                const float2 x = __ffma2_rn(make_float2(__uint_as_float(sr[8 * u + e]), __uint_as_float(sr[8 * u + e + 1])),
+                                            make_float2(scale2, scale2), make_float2(lv[e], lv[e + 1]));
+                if ((BWD_EMU_BITS >> (((cc + 8 * u + e) >> 1) & 7)) & 1) {
+                  const float2 y = ex2_fma2(x);
+                  pv[e] = y.x;
+                  pv[e + 1] = y.y;
+                } else {
+                  pv[e] = ex2(x.x);
+                  pv[e + 1] = ex2(x.y);
+                }
+              }
+#pragma unroll
               for (int e = 0; e < 8; ++e) {
-                pv[e] = ex2(fmaf(__uint_as_float(sr[8 * u + e]), scale2, -lv[e]));
                 if constexpr (decltype(masked)::value) {
                   const int i = 8 * u + e;
                   if (i < lo || i >= hi) pv[e] = 0.f;
@@ -864,8 +879,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
 #pragma unroll
             for (int k = 0; k < 8; k += 2) {
               const float2 pp = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pk[cc / 2 + 4 * u + k / 2]));
-              dk2[cc / 2 + 4 * u + k / 2] = pack_bf16(pp.x * (__uint_as_float(pr[8 * u + k]) - dv8[k]),
-                                                      pp.y * (__uint_as_float(pr[8 * u + k + 1]) - dv8[k + 1]));
+              const float2 d = __fmul2_rn(pp, __fadd2_rn(make_float2(__uint_as_float(pr[8 * u + k]),
+                                                                     __uint_as_float(pr[8 * u + k + 1])),
+                                                         make_float2(dv8[k], dv8[k + 1])));
+              dk2[cc / 2 + 4 * u + k / 2] = pack_bf16(d.x, d.y);
             }
             *reinterpret_cast<uint4*>(dst + p_offset(r, c0 + 8 * u)) =
                 make_uint4(dk2[cc / 2 + 4 * u], dk2[cc / 2 + 4 * u + 1], dk2[cc / 2 + 4 * u + 2], dk2[cc / 2 + 4 * u + 3]);
