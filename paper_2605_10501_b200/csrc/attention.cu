@@ -488,10 +488,13 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
 // TMEM: S^T [0,128), dP^T [128,256), dV [256,320), dK [320,384), dQ [384,448).
 constexpr int BWD_THREADS = 448;  // w0 TMA, w1 MMA, w2-9 softmax (2 per lane quadrant), w10-13 dQ drain
 
+// Q/dO ring depth: stage i+1's load can only start once dK/dQ(i-1) have read their stage, so two
+// stages expose the TMA latency in front of S(i+1); three hide it.
+constexpr int QD_STAGES = 3;
 struct BwdSmem {
   static constexpr int KV = 0;                              // 2 items x (K tile, V tile)
-  static constexpr int QD = KV + 2 * 2 * TILE_BYTES;        // 2 stages x (Q tile, dO tile)
-  static constexpr int DST = QD + 2 * 2 * TILE_BYTES;       // dS^T [kv][q] bf16, 2 chunks (dQ operand)
+  static constexpr int QD = KV + 2 * 2 * TILE_BYTES;        // QD_STAGES x (Q tile, dO tile)
+  static constexpr int DST = QD + QD_STAGES * 2 * TILE_BYTES;  // dS^T [kv][q] bf16, 2 chunks (dQ operand)
   static constexpr int LSE = DST + P_BYTES;                 // 2 x 128 fp32 (double-buffered by tile)
   static constexpr int DD = LSE + 1024;                     // 2 x 128 fp32
   static constexpr int DQS = DD + 1024;                     // dQ staging: 4 drain warps x 32 rows x 32 fp32
@@ -554,20 +557,20 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + BwdSmem::BAR);
   uint64_t* kv_full = bar;          // [2]
   uint64_t* kv_empty = bar + 2;     // [2]
-  uint64_t* qd_full = bar + 4;      // [2]
-  uint64_t* qd_empty = bar + 6;     // [2]
-  uint64_t* s_full = bar + 8;
-  uint64_t* dp_full = bar + 9;
-  uint64_t* p_ready = bar + 10;
-  uint64_t* p_free = bar + 11;
-  uint64_t* ds_ready = bar + 12;
-  uint64_t* ds_free = bar + 13;
-  uint64_t* dq_full = bar + 14;
-  uint64_t* dq_empty = bar + 15;
-  uint64_t* dkv_full = bar + 16;
-  uint64_t* dkv_empty = bar + 17;
-  uint64_t* s_empty = bar + 18;   // S^T TMEM loaded by the softmax warps (the next S may overwrite it)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 20);
+  uint64_t* qd_full = bar + 4;      // [QD_STAGES]
+  uint64_t* qd_empty = bar + 7;     // [QD_STAGES]
+  uint64_t* s_full = bar + 10;
+  uint64_t* dp_full = bar + 11;
+  uint64_t* p_ready = bar + 12;
+  uint64_t* p_free = bar + 13;
+  uint64_t* ds_ready = bar + 14;
+  uint64_t* ds_free = bar + 15;
+  uint64_t* dq_full = bar + 16;
+  uint64_t* dq_empty = bar + 17;
+  uint64_t* dkv_full = bar + 18;
+  uint64_t* dkv_empty = bar + 19;
+  uint64_t* s_empty = bar + 20;   // S^T TMEM loaded by the softmax warps (the next S may overwrite it)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 21);
   float* s_lse = reinterpret_cast<float*>(sm + BwdSmem::LSE);
   float* s_D = reinterpret_cast<float*>(sm + BwdSmem::DD);
 
@@ -583,6 +586,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     for (int b = 0; b < 2; ++b) {
       mbar_init(&kv_full[b], 1);
       mbar_init(&kv_empty[b], 1);
+    }
+    for (int b = 0; b < QD_STAGES; ++b) {
       mbar_init(&qd_full[b], 1);
       mbar_init(&qd_empty[b], 1);
     }
@@ -625,8 +630,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         for (int it = 0; it < itm.n_it; ++it, ++gi) {
           const int g = it / itm.n_q, qt = itm.qt_first + it % itm.n_q;
           const int h = itm.hk * G + g;
-          const int st = gi & 1;
-          mbar_wait(&qd_empty[st], ((gi >> 1) & 1) ^ 1);
+          const int st = gi % QD_STAGES;
+          mbar_wait(&qd_empty[st], ((gi / QD_STAGES) & 1) ^ 1);
           mbar_arrive_expect_tx(&qd_full[st], 2 * TILE_BYTES);
           unsigned char* dst = sm + BwdSmem::QD + st * 2 * TILE_BYTES;
           tma_load_2d(dst, &map_q, &qd_full[st], h * DH, itm.s0 + qt * BQ);
@@ -635,33 +640,39 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // the whole warp runs the loop; MMAs and commits are issued by one elected lane
       constexpr uint32_t id_sp = idesc_bf16_f32(BKV, BQ, false, false);  // M = kv, N = q
       constexpr uint32_t id_kv = idesc_bf16_f32(BKV, DH, false, true);   // dV, dK: A K-major, B MN-major
       constexpr uint32_t id_dq = idesc_bf16_f32(BQ, DH, true, true);     // dQ: A = dS (MN-major view of dS^T)
       const uint32_t ds_base = smem_u32(sm + BwdSmem::DST);
       auto kv_base = [&](int j) { return smem_u32(sm + BwdSmem::KV + (j & 1) * 2 * TILE_BYTES); };
-      auto qd_base = [&](int gi) { return smem_u32(sm + BwdSmem::QD + (gi & 1) * 2 * TILE_BYTES); };
+      auto qd_base = [&](int gi) { return smem_u32(sm + BwdSmem::QD + (gi % QD_STAGES) * 2 * TILE_BYTES); };
       // S^T(gi) = K Q^T and dP^T(gi) = V dO^T of the cursor's iteration
       auto issue_s = [&](const BwdCursor<CAUSAL>& c, int gi) {
-        mbar_wait(&qd_full[gi & 1], (gi >> 1) & 1);
+        mbar_wait(&qd_full[gi % QD_STAGES], (gi / QD_STAGES) & 1);
         if (c.it == 0) mbar_wait(&kv_full[c.j & 1], (c.j >> 1) & 1);
         if (gi >= 1) mbar_wait(s_empty, (gi - 1) & 1);  // S^T(gi-1) is in the softmax registers
         tc_fence_after();
         const uint32_t kb = kv_base(c.j), qb = qd_base(gi);
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk)
-          umma_bf16(tmem + T_ST, smem_desc_sw128(kb + kk * 32, 16, 1024), smem_desc_sw128(qb + kk * 32, 16, 1024),
-                    id_sp, kk > 0);
-        umma_commit(s_full);
+          for (int kk = 0; kk < DH / 16; ++kk)
+            umma_bf16(tmem + T_ST, smem_desc_sw128(kb + kk * 32, 16, 1024), smem_desc_sw128(qb + kk * 32, 16, 1024),
+                      id_sp, kk > 0);
+          umma_commit(s_full);
+        }
+        __syncwarp();
       };
       auto issue_dp = [&](const BwdCursor<CAUSAL>& c, int gi) {
         const uint32_t vb = kv_base(c.j) + TILE_BYTES, db = qd_base(gi) + TILE_BYTES;
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk)
-          umma_bf16(tmem + T_DPT, smem_desc_sw128(vb + kk * 32, 16, 1024), smem_desc_sw128(db + kk * 32, 16, 1024),
-                    id_sp, kk > 0);
-        umma_commit(dp_full);
+          for (int kk = 0; kk < DH / 16; ++kk)
+            umma_bf16(tmem + T_DPT, smem_desc_sw128(vb + kk * 32, 16, 1024), smem_desc_sw128(db + kk * 32, 16, 1024),
+                      id_sp, kk > 0);
+          umma_commit(dp_full);
+        }
+        __syncwarp();
       };
       BwdCursor<CAUSAL> cur;
       cur.j = 0;
@@ -682,30 +693,36 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         mbar_wait(p_ready, gi & 1);
         if (cur.it == 0) mbar_wait(dkv_empty, (cur.j & 1) ^ 1);  // previous item's epilogue read dK/dV
         tc_fence_after();
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < BQ / 16; ++kk)  // reduction over the 128 queries; A = P^T from TMEM
-          umma_bf16_ts(tmem + T_DV, tmem + T_PT + kk * 8, smem_desc_sw128(qb + TILE_BYTES + kk * 2048, 8192, 1024),
-                       id_kv, (cur.it > 0 || kk > 0) ? 1u : 0u);
-        umma_commit(p_free);
+          for (int kk = 0; kk < BQ / 16; ++kk)  // reduction over the 128 queries; A = P^T from TMEM
+            umma_bf16_ts(tmem + T_DV, tmem + T_PT + kk * 8, smem_desc_sw128(qb + TILE_BYTES + kk * 2048, 8192, 1024),
+                         id_kv, (cur.it > 0 || kk > 0) ? 1u : 0u);
+          umma_commit(p_free);
+        }
+        __syncwarp();
         // dK += dS^T Q (A = dS^T from TMEM) ; dQ = dS K (A = dS^T smem, MN-major view)
         mbar_wait(ds_ready, gi & 1);
         mbar_wait(dq_empty, (gi & 1) ^ 1);
         tc_fence_after();
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < BQ / 16; ++kk)
-          umma_bf16_ts(tmem + T_DK, tmem + T_DPT + (kk >> 2) * 64 + (kk & 3) * 8,
-                       smem_desc_sw128(qb + kk * 2048, 8192, 1024), id_kv, (cur.it > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < BQ / 16; ++kk)
+            umma_bf16_ts(tmem + T_DK, tmem + T_DPT + (kk >> 2) * 64 + (kk & 3) * 8,
+                         smem_desc_sw128(qb + kk * 2048, 8192, 1024), id_kv, (cur.it > 0 || kk > 0) ? 1u : 0u);
 #pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk)  // reduction over the 128 keys
-          umma_bf16(tmem + T_DQ, smem_desc_sw128(ds_base + kk * 2048, 16384, 1024),
-                    smem_desc_sw128(kb + kk * 2048, 8192, 1024), id_dq, kk > 0 ? 1u : 0u);
-        umma_commit(dq_full);
-        umma_commit(&qd_empty[gi & 1]);
-        umma_commit(ds_free);
-        if (cur.it == cur.item.n_it - 1) {
-          umma_commit(dkv_full);
-          umma_commit(&kv_empty[cur.j & 1]);
+          for (int kk = 0; kk < BKV / 16; ++kk)  // reduction over the 128 keys
+            umma_bf16(tmem + T_DQ, smem_desc_sw128(ds_base + kk * 2048, 16384, 1024),
+                      smem_desc_sw128(kb + kk * 2048, 8192, 1024), id_dq, kk > 0 ? 1u : 0u);
+          umma_commit(dq_full);
+          umma_commit(&qd_empty[gi % QD_STAGES]);
+          umma_commit(ds_free);
+          if (cur.it == cur.item.n_it - 1) {
+            umma_commit(dkv_full);
+            umma_commit(&kv_empty[cur.j & 1]);
+          }
         }
+        __syncwarp();
         // dP^T(gi+1) after dK(gi) (in issue order) has read dS^T out of the dP^T columns
         if (nxt.valid) issue_dp(nxt, gi + 1);
         cur = nxt;

@@ -40,6 +40,9 @@ for a, b in zip(order, order[1:]):
     print(f"{names[a]:>12s} -> {names[b]:<12s} median {np.median(buf[b][5:n-5] - buf[a][5:n-5]):8.0f}")
 for a, b in [(2, 0), (0, 1), (1, 3), (3, 4), (4, 5), (5, 6), (9, 0), (12, 3), (13, 14), (7, 2)]:
     print(f"{names[a]:>12s} -> {names[b]:<12s} median {np.median(buf[b][5:n-5] - buf[a][5:n-5]):8.0f}")
+for a, b in [(4, 19), (19, 5), (18, 15), (15, 16), (16, 17)]:
+    print(f"issue_s {a}->{b} median {np.median(buf[b][5:n-5] - buf[a][5:n-5]):8.0f}")
+print("issue_s start -> s_full seen", np.median(buf[7][5:n-5] - buf[18][5:n-5]))
 x = buf[0][6:n-4] - buf[6][5:n-5]
 print(f"{'M:dP+1_iss':>12s} -> next p_ready median {np.median(x):8.0f}")
 x = buf[7][6:n-4] - buf[12][5:n-5]
