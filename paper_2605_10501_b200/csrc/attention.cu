@@ -92,6 +92,12 @@ __device__ __forceinline__ float2 ex2_fma2(float2 x) {
 #ifndef FWD_EMU_BITS
 #define FWD_EMU_BITS 0x92  // pair p of a row's 32 goes to the FMA pipe if bit (p & 7) is set (3/8)
 #endif
+// SWIZZLE_128B smem descriptor from a 16-byte-unit address (addr >> 4; the CTA window is below
+// 256 KB so it fits the 14-bit field unmasked): callers shift a stage base once and add per-K-step
+// constants, so issuing an MMA costs one add per operand instead of a shift/mask/or chain.
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr16, uint32_t lbo, uint32_t sbo) {
+  return ((uint64_t)((sbo >> 4) | (1u << 14) | (2u << 29)) << 32) | (uint64_t)(addr16 + ((lbo >> 4) << 16));
+}
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -241,7 +247,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
 #pragma unroll
           for (int kk = 0; kk < BKV / 16; ++kk)
             umma_bf16_ts(tmem + 256 + ob * 2 * DH + (kk >> 2) * DH, tmem + pb * BKV + (kk >> 2) * 64 + (kk & 3) * 8,
-                         smem_desc_sw128(v_base + kk * 2048, 8192, 1024), idesc_o, (ip > 0 || (kk & 3) > 0) ? 1u : 0u);
+                         sdesc((v_base >> 4) + kk * 128, 8192, 1024), idesc_o, (ip > 0 || (kk & 3) > 0) ? 1u : 0u);
           umma_commit(&v_empty[gp % KV_STAGES]);
           umma_commit(&p_empty[pb]);
         }
@@ -279,8 +285,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
           if (elect_one()) {
 #pragma unroll
             for (int kk = 0; kk < DH / 16; ++kk)
-              umma_bf16(tmem + b * BKV, smem_desc_sw128(q_base + kk * 32, 16, 1024),
-                        smem_desc_sw128(k_base + kk * 32, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+              umma_bf16(tmem + b * BKV, sdesc((q_base >> 4) + kk * 2, 16, 1024),
+                        sdesc((k_base >> 4) + kk * 2, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
             umma_commit(&k_empty[st]);
             umma_commit(&s_full[b]);
             if (i == it.n_kv - 1) umma_commit(&q_empty[qb]);  // last S of the item: Q buffer free
@@ -657,7 +663,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < DH / 16; ++kk)
-            umma_bf16(tmem + T_ST, smem_desc_sw128(kb + kk * 32, 16, 1024), smem_desc_sw128(qb + kk * 32, 16, 1024),
+            umma_bf16(tmem + T_ST, sdesc((kb >> 4) + kk * 2, 16, 1024), sdesc((qb >> 4) + kk * 2, 16, 1024),
                       id_sp, kk > 0);
           umma_commit(s_full);
         }
@@ -668,7 +674,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < DH / 16; ++kk)
-            umma_bf16(tmem + T_DPT, smem_desc_sw128(vb + kk * 32, 16, 1024), smem_desc_sw128(db + kk * 32, 16, 1024),
+            umma_bf16(tmem + T_DPT, sdesc((vb >> 4) + kk * 2, 16, 1024), sdesc((db >> 4) + kk * 2, 16, 1024),
                       id_sp, kk > 0);
           umma_commit(dp_full);
         }
@@ -696,7 +702,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < BQ / 16; ++kk)  // reduction over the 128 queries; A = P^T from TMEM
-            umma_bf16_ts(tmem + T_DV, tmem + T_PT + kk * 8, smem_desc_sw128(qb + TILE_BYTES + kk * 2048, 8192, 1024),
+            umma_bf16_ts(tmem + T_DV, tmem + T_PT + kk * 8, sdesc(((qb + TILE_BYTES) >> 4) + kk * 128, 8192, 1024),
                          id_kv, (cur.it > 0 || kk > 0) ? 1u : 0u);
           umma_commit(p_free);
         }
@@ -709,11 +715,11 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
 #pragma unroll
           for (int kk = 0; kk < BQ / 16; ++kk)
             umma_bf16_ts(tmem + T_DK, tmem + T_DPT + (kk >> 2) * 64 + (kk & 3) * 8,
-                         smem_desc_sw128(qb + kk * 2048, 8192, 1024), id_kv, (cur.it > 0 || kk > 0) ? 1u : 0u);
+                         sdesc((qb >> 4) + kk * 128, 8192, 1024), id_kv, (cur.it > 0 || kk > 0) ? 1u : 0u);
 #pragma unroll
           for (int kk = 0; kk < BKV / 16; ++kk)  // reduction over the 128 keys
-            umma_bf16(tmem + T_DQ, smem_desc_sw128(ds_base + kk * 2048, 16384, 1024),
-                      smem_desc_sw128(kb + kk * 2048, 8192, 1024), id_dq, kk > 0 ? 1u : 0u);
+            umma_bf16(tmem + T_DQ, sdesc((ds_base >> 4) + kk * 128, 16384, 1024),
+                      sdesc((kb >> 4) + kk * 128, 8192, 1024), id_dq, kk > 0 ? 1u : 0u);
           umma_commit(dq_full);
           umma_commit(&qd_empty[gi % QD_STAGES]);
           umma_commit(ds_free);
