@@ -19,7 +19,7 @@ import sys
 from pathlib import Path
 
 TENSOR = ("gemm", "attn_fwd_kernel", "attn_bwd_kernel")
-LATENCY = ("sample_times", "partition", "wavefront", "rank_metrics", "fanout_merge", "varlen_pack", "pack_tokens",
+LATENCY = ("sample_times", "partition", "wavefront", "rank_metrics", "fanout_merge", "varlen_pack", "pack_tokens", "fp64_",
            "tiles_kernel", "positions")
 UNIT = {"nsecond": 1e-9, "ns": 1e-9, "usecond": 1e-6, "us": 1e-6, "msecond": 1e-3, "ms": 1e-3, "second": 1.0,
         "s": 1.0, "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "%": 1.0}
