@@ -3,6 +3,7 @@
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2605_10501_b200/csrc scripts/micro/umma_rate2.cu -o scripts/micro/umma_rate2
 #include <cstdio>
 #include <cstdlib>
+constexpr int SMEM_DATA = 196608;
 #include "sm100.cuh"
 using namespace mb::sm100;
 
@@ -17,12 +18,12 @@ template <int MODE>
 __global__ void __launch_bounds__(128, 1) rate_kernel(long long* out, int rnd) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* sm = align_smem_1024(smem_raw);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 65536);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + SMEM_DATA);
   uint64_t* dummy = bar + 2;  // [4] commit targets nobody waits on
   uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 1);
   const int warp = threadIdx.x >> 5;
   uint32_t st = 0x12345u + threadIdx.x * 7919u + blockIdx.x * 104729u;
-  for (int i = threadIdx.x; i < 65536 / 4; i += blockDim.x) {
+  for (int i = threadIdx.x; i < SMEM_DATA / 4; i += blockDim.x) {
     st = st * 1664525u + 1013904223u;
     // random bf16 pairs in [-1, 1): sign | exponent 0x3F0..0x3F7 | random mantissa
     const uint32_t lo = ((st >> 16) & 0x807F) | 0x3F00, hi = ((st & 0x807F) | 0x3F00);
@@ -54,17 +55,22 @@ __global__ void __launch_bounds__(128, 1) rate_kernel(long long* out, int rnd) {
     const uint32_t base = smem_u32(sm);
     long long t0 = clock64();
     if (MODE >= 3 && elect_one()) {
+      constexpr bool FENCE = MODE == 6;
+      const uint32_t base0 = base;
       const uint32_t id_sp = idesc_bf16_f32(128, 128, false, false), id_kv = idesc_bf16_f32(128, 64, false, true),
                      id_dq = idesc_bf16_f32(128, 64, true, true);
       for (int i = 0; i < N_MMA; i += 32) {
+        const uint32_t base = MODE == 7 ? base0 + ((i >> 5) % 3) * 65536 : base0;  // rotate operand stages
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
           umma_bf16(tmem + 0, smem_desc_sw128(base + kk * 32, 16, 1024), smem_desc_sw128(base + 16384 + kk * 32, 16, 1024), id_sp, kk > 0);
         if (MODE == 3) umma_commit(&dummy[0]);
+        if (FENCE) tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
           umma_bf16_ts(tmem + 256, tmem + 448 + kk * 8, smem_desc_sw128(base + 32768 + kk * 2048, 8192, 1024), id_kv, 1u);
         if (MODE == 3) umma_commit(&dummy[1]);
+        if (FENCE) tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
           umma_bf16_ts(tmem + 320, tmem + 128 + (kk >> 2) * 64 + (kk & 3) * 8, smem_desc_sw128(base + 32768 + kk * 2048, 8192, 1024), id_kv, 1u);
@@ -76,6 +82,7 @@ __global__ void __launch_bounds__(128, 1) rate_kernel(long long* out, int rnd) {
             umma_bf16(tmem + 384, smem_desc_sw128(base + kk * 2048, 16384, 1024), smem_desc_sw128(base + 32768 + kk * 2048, 8192, 1024), id_dq, kk > 0);
         }
         if (MODE == 3) { umma_commit(&dummy[2]); umma_commit(&dummy[3]); umma_commit(&dummy[0]); }
+        if (FENCE) tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
           umma_bf16(tmem + 128, smem_desc_sw128(base + 32768 + kk * 32, 16, 1024), smem_desc_sw128(base + 49152 + kk * 32, 16, 1024), id_sp, kk > 0);
@@ -112,9 +119,9 @@ __global__ void __launch_bounds__(128, 1) rate_kernel(long long* out, int rnd) {
 
 template <int MODE>
 void run(const char* name, long long* d, int rnd) {
-  cudaFuncSetAttribute(rate_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536 + 2048);
+  cudaFuncSetAttribute(rate_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_DATA + 2048);
   const int reps = getenv("REPS") ? atoi(getenv("REPS")) : 3;
-  for (int rep = 0; rep < reps; ++rep) rate_kernel<MODE><<<148, 128, 65536 + 2048>>>(d, rnd);
+  for (int rep = 0; rep < reps; ++rep) rate_kernel<MODE><<<148, 128, SMEM_DATA + 2048>>>(d, rnd);
   cudaError_t e = cudaDeviceSynchronize();
   long long h[148];
   cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
@@ -137,6 +144,8 @@ int main() {
     run<3>("bwd mix + commits (per MMA; 32/iter)", d, rnd);
     run<4>("bwd mix, no commits", d, rnd);
     run<5>("mix without MN-major-A dQ", d, rnd);
+    run<6>("bwd mix + fence::after_thread_sync", d, rnd);
+    run<7>("bwd mix, operands rotating over 3 stages", d, rnd);
   }
   return 0;
 }
