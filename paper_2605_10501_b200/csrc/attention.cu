@@ -341,7 +341,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       const float sa = ma == -INFINITY ? 0.f : ex2(ma - M), sb = mb == -INFINITY ? 0.f : ex2(mb - M);
       const float l_all = la * sa + lb * sb;
       if (qpos < it.L) {
-        const float fa = sa / l_all, fb = sb / l_all;
+        const float rl = __frcp_rn(l_all);
+        const float fa = sa * rl, fb = sb * rl;
         uint32_t o[16];
 #pragma unroll
         for (int jj = 0; jj < 16; ++jj)
@@ -387,12 +388,29 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
         mbar_arrive(&s_empty[b]);
         const int kv0 = i * BKV + half * 64;
         const bool need_mask = (CAUSAL && kv0 + 63 > it.q0) || (kv0 + 64 > it.L);
+        // valid key columns of this row: c < lim (causal: key <= query; key inside the sequence)
+        const int lim = CAUSAL ? min(qpos - kv0 + 1, it.L - kv0) : it.L - kv0;
+        if (need_mask && __all_sync(kFull, lim <= 0)) {
+          // every row of this warp sees only masked keys in this half-tile (upper triangle of the
+          // diagonal tile): P = 0, running max and sum unchanged
+          uint32_t zero[32];
+#pragma unroll
+          for (int e = 0; e < 32; ++e) zero[e] = 0u;
+          tmem_st_32x32b_x32(tmem + lane_base + b * BKV + half * 64, zero);
+          tmem_st_wait();
+          tc_fence_before();
+          mbar_arrive(&p_full[b]);
+          if (i == 0 && pend) {
+            epilogue(pit, pj, pm, pl);
+            pend = false;
+          }
+          continue;
+        }
         float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
         if (need_mask) {
 #pragma unroll
           for (int c = 0; c < 64; ++c) {
-            const int kv = kv0 + c;
-            if ((CAUSAL && kv > qpos) || kv >= it.L) s[c] = -INFINITY;
+            s[c] = c < lim ? s[c] : -INFINITY;
             mx4[c & 3] = fmaxf(mx4[c & 3], s[c]);
           }
         } else {
