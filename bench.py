@@ -181,13 +181,21 @@ def run_vlm(args):
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        ex = VLMGroupExecutor(world, batch_per_llm_rank=args.batch_per_rank, mbs_llm=args.mbs, mbs_vit=args.vit_mbs)
-        layout = f"disjoint: vit dp{ex.dp_vit} (fanout {ex.f}) -> llm dp{ex.dp_llm}, NCCL handoff (mq)"
+        if args.layout == "colocated":
+            # both sections data-parallel on every GPU: a co-resident step per rank on its own
+            # batch, per-section gradient all-reduce
+            ex = VLMExecutor(batch=args.batch_per_rank, mbs_llm=args.mbs, mbs_vit=args.vit_mbs,
+                             dp_group=dist.group.WORLD)
+            layout = f"colocated vit+llm per GPU, both sections dp{world} (grad all-reduce)"
+        else:
+            ex = VLMGroupExecutor(world, batch_per_llm_rank=args.batch_per_rank, mbs_llm=args.mbs,
+                                  mbs_vit=args.vit_mbs)
+            layout = f"disjoint: vit dp{ex.dp_vit} (fanout {ex.f}) -> llm dp{ex.dp_llm}, NCCL handoff (mq)"
     else:
         ex = VLMExecutor(batch=args.batch_per_rank, mbs_llm=args.mbs, mbs_vit=args.vit_mbs)
         layout = "colocated vit+llm"
     B = ex.batch
-    hb = vlm_host_batch(B, seed=0)
+    hb = vlm_host_batch(B, seed=rank if (world > 1 and args.layout == "colocated") else 0)
 
     def barrier():
         torch.cuda.synchronize()
@@ -215,19 +223,20 @@ def run_vlm(args):
     if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t[0].item())
-    value = B * args.steps / (ms / 1e3)
+    B_all = B * world if (world > 1 and args.layout == "colocated") else B
+    value = B_all * args.steps / (ms / 1e3)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": "vlm_cfg1: ViT-tiny (d192 L12) -> 2-layer GPT (d768), 50/50 text/image, "
-                                   "wavefront schedule on device", "global_batch": B, "seq_len": "64..497",
+                                   "wavefront schedule on device", "global_batch": B_all, "seq_len": "64..497",
                        "parallelism": layout, "micro_batch_llm": args.mbs, "micro_batch_vit": args.vit_mbs,
                        "note": "end-to-end: inputs copied from host every step"},
             "section_stall_pct": 100.0 * float(t[1].item()),
             "gpu_launches": (instrument.launches - launches0) // args.steps,
-            "model_tflops": ex.model_flops_per_step(hb) * args.steps / (ms / 1e3) / 1e12, "loss": st.loss,
+            "model_tflops": ex.model_flops_per_step(hb) * (B_all // B) * args.steps / (ms / 1e3) / 1e12, "loss": st.loss,
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)

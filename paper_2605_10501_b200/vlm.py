@@ -116,10 +116,13 @@ class ViTSection:
 
 
 class VLMExecutor:
-    """Co-resident VLM step on one GPU (cfg 1 layout "1 GPU")."""
+    """Co-resident VLM step on one GPU (cfg 1 layout "1 GPU").  With ``dp_group`` (a
+    torch.distributed group) every rank runs the co-resident step on its own batch and the ViT and
+    LLM gradients are averaged over the group before the optimizer (both sections data-parallel
+    on the same GPUs: the co-located layout at N > 1)."""
 
     def __init__(self, batch: int = 64, mbs_llm: int = 8, mbs_vit: int = 8, seed: int = 0, lr: float = 3e-4,
-                 policy=ExecPolicy.INTERLEAVED, device=None):
+                 policy=ExecPolicy.INTERLEAVED, device=None, dp_group=None):
         self.device = dev = device or torch.device("cuda", torch.cuda.current_device())
         self.batch, self.mbs_llm, self.mbs_vit = batch, mbs_llm, mbs_vit
         self.rec = R.vlm_tiny(1, batch, seed)
@@ -135,6 +138,7 @@ class VLMExecutor:
         self.planner = DevicePlanner(self.graph, self.configs, policy, max_batch=batch, device=dev)
         self.cost = torch.from_numpy(cost_table(self.graph, self.configs, self.rec.params)).to(dev)
         self.lr = lr
+        self.dp_group = dp_group
         self.s_llm = torch.cuda.Stream(device=dev)
         self.s_vit = torch.cuda.Stream(device=dev)
         self.step_idx = 0
@@ -265,11 +269,24 @@ class VLMExecutor:
                 self.s_vit.wait_event(llm_bwd_ev[max(llm_mb_of[int(i)] for i in samples)])
                 a = k * self.mbs_vit * 49
                 self.vit.backward(demb_buf[a: a + len(samples) * 49], vit_ctx[k])
-            self.vit.p.adamw(self.lr)
-        with torch.cuda.stream(self.s_llm):
-            self.llm.p.adamw(self.lr)
+            if self.dp_group is None:
+                self.vit.p.adamw(self.lr)
+        if self.dp_group is None:
+            with torch.cuda.stream(self.s_llm):
+                self.llm.p.adamw(self.lr)
         main.wait_stream(self.s_llm)
         main.wait_stream(self.s_vit)
+        if self.dp_group is not None:
+            # per-section gradient average over the data-parallel group (C2), then the optimizers
+            dist = _dist()
+            world = dist.get_world_size(self.dp_group)
+            for p in (self.llm.p, self.vit.p):
+                dist.all_reduce(p.grad, group=self.dp_group)
+                p.grad.mul_(1.0 / world)
+            dist.all_reduce(loss_acc, group=self.dp_group)
+            loss_acc.mul_(1.0 / world)
+            self.vit.p.adamw(self.lr)
+            self.llm.p.adamw(self.lr)
         t1 = torch.cuda.Event(enable_timing=True)
         t1.record(main)
         self.step_idx += 1

@@ -1,4 +1,5 @@
-# One box, N = 1, 2, 4 GPUs back to back: KD (colocated default), KD disjoint, VLM cfg 1, and the
+# One box, N = 1, 2, 4 GPUs back to back: KD (colocated default), KD disjoint, VLM cfg 1 (colocated
+# DP default, disjoint section groups), and the
 # reference arm; one JSON line per run into gpurun_out/scaling.jsonl.
 #   gpurun --gpus 4 -- bash scripts/scaling_run.sh
 set -u
@@ -16,5 +17,6 @@ run() {  # n, extra args...
 for n in 1 2 4; do run $n; done
 for n in 2 4; do run $n --layout disjoint; done
 for n in 1 2 4; do run $n --workload vlm; done
+for n in 2 4; do run $n --workload vlm --layout disjoint; done
 run 1 --impl reference
 wc -l $OUT

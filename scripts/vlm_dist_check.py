@@ -3,6 +3,8 @@ reorder"): the disjoint-group executor at N GPUs vs the co-resident executor on 
 batch and seeds.  Run under torchrun; rank 0 prints one JSON line.
 
     python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 scripts/vlm_dist_check.py
+    ... scripts/vlm_dist_check.py --colocated   (both sections DP on every GPU, same batch per rank:
+                                                 the averaged gradients equal the single-GPU ones)
 """
 import json
 import os
@@ -20,8 +22,11 @@ torch.cuda.set_device(local)
 dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 world, rank = dist.get_world_size(), dist.get_rank()
 steps = 3
-ex = VLMGroupExecutor(world, batch_per_llm_rank=64 // max(1, {2: 1, 4: 3, 8: 6}[world]) if world > 2 else 64,
-                      mbs_llm=8, mbs_vit=8, lr=1e-3)
+if "--colocated" in sys.argv:
+    ex = VLMExecutor(batch=64, mbs_llm=8, mbs_vit=8, lr=1e-3, dp_group=dist.group.WORLD)
+else:
+    ex = VLMGroupExecutor(world, batch_per_llm_rank=64 // max(1, {2: 1, 4: 3, 8: 6}[world]) if world > 2 else 64,
+                          mbs_llm=8, mbs_vit=8, lr=1e-3)
 hb = vlm_host_batch(ex.batch, seed=0)
 group = [ex.step(hb).loss for _ in range(steps)]
 dist.barrier()

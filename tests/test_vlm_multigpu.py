@@ -1,4 +1,5 @@
-"""VLM on disjoint GPU groups (2 GPUs): same losses as the co-resident single-GPU step.
+"""VLM on 2 GPUs, disjoint section groups or both sections data-parallel per GPU: same losses as
+the co-resident single-GPU step.
 
 Runs scripts/vlm_dist_check.py under torchrun when the box has >= 2 GPUs (skipped otherwise).
 Tolerance: the two layouts run the same kernels on the same micro-batches; only the fp32
@@ -18,9 +19,12 @@ ROOT = Path(__file__).resolve().parents[1]
 
 
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs 2 GPUs")
-def test_vlm_disjoint_groups_match_single_gpu():
+@pytest.mark.parametrize("layout", ["disjoint", "colocated"])
+def test_vlm_layouts_match_single_gpu(layout):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", "29533", str(ROOT / "scripts" / "vlm_dist_check.py")]
+    if layout == "colocated":
+        cmd.append("--colocated")
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT,
                          env={**os.environ, "PYTHONPATH": str(ROOT)})
     assert out.returncode == 0, out.stderr[-3000:]
