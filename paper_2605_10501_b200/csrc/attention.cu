@@ -70,22 +70,6 @@ __global__ void attn_tiles_kernel(const int32_t* __restrict__ cu, int nseq, int2
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
 
-// 2^x for a pair on the FMA pipe (the MUFU unit retires 16 exponentials per clock per SM, the
-// FMA pipe 128 lanes): round-to-nearest split x = n + f via the 1.5*2^23 magic constant, minimax
-// cubic for 2^f on [-1/2, 1/2] (max relative error 7.5e-5, far below the bf16 rounding of P),
-// n added to the exponent field.  x is clamped at -126 so masked (-inf) inputs give ~0.
-__device__ __forceinline__ float2 ex2_fma2(float2 x) {
-  x.x = fmaxf(x.x, -126.f);
-  x.y = fmaxf(x.y, -126.f);
-  const float2 j = __fadd2_rn(x, make_float2(12582912.f, 12582912.f));
-  const float2 r = __fadd2_rn(j, make_float2(-12582912.f, -12582912.f));
-  const float2 f = __ffma2_rn(r, make_float2(-1.f, -1.f), x);
-  float2 p = __ffma2_rn(make_float2(0.05516102f, 0.05516102f), f, make_float2(0.24261291f, 0.24261291f));
-  p = __ffma2_rn(p, f, make_float2(0.6932625f, 0.6932625f));
-  p = __ffma2_rn(p, f, make_float2(0.99992794f, 0.99992794f));
-  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(j.x) << 23)),
-                     __int_as_float(__float_as_int(p.y) + (__float_as_int(j.y) << 23)));
-}
 #ifndef BWD_EMU_BITS
 #define BWD_EMU_BITS 0x00  // backward P^T = exp2(S^T scale2 - lse2): not MUFU-bound, all on MUFU
 #endif
@@ -433,7 +417,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
         for (int c = 0; c < 64; c += 2) {
           const float2 x = __ffma2_rn(make_float2(s[c], s[c + 1]), sc2, nm2);
           if ((FWD_EMU_BITS >> ((c >> 1) & 7)) & 1) {
-            const float2 e = ex2_fma2(x);
+            const float2 e = ex2_fma2<3>(x);
             s[c] = e.x;
             s[c + 1] = e.y;
           } else {
@@ -873,7 +857,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
                 const float2 x = __ffma2_rn(make_float2(__uint_as_float(sr[8 * u + e]), __uint_as_float(sr[8 * u + e + 1])),
                                             make_float2(scale2, scale2), make_float2(lv[e], lv[e + 1]));
                 if ((BWD_EMU_BITS >> (((cc + 8 * u + e) >> 1) & 7)) & 1) {
-                  const float2 y = ex2_fma2(x);
+                  const float2 y = ex2_fma2<3>(x);
                   pv[e] = y.x;
                   pv[e + 1] = y.y;
                 } else {

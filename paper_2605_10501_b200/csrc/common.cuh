@@ -46,4 +46,32 @@ __device__ __forceinline__ float2 rope_cs_at(const float2* __restrict__ cs, int 
   return cs[((size_t)(pos >> 5) * half + k) * 32 + (pos & 31)];
 }
 
+// 2^x for a pair on the FMA pipe (the MUFU unit retires 16 exponentials per clock per SM, the
+// FMA pipe 128 lanes): round-to-nearest split x = n + f with the 1.5*2^23 magic constant, a
+// minimax polynomial for 2^f on [-1/2, 1/2] in paired fp32 FMAs, n added to the exponent field.
+// x is clamped at -126 so -inf (masked) inputs give ~0.  DEG 3: max relative error 7.5e-5 (P is
+// rounded to bf16 anyway); DEG 5: 1.3e-7 (on par with ex2.approx, for fp32 reductions).
+template <int DEG>
+__device__ __forceinline__ float2 ex2_fma2(float2 x) {
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 j = __fadd2_rn(x, make_float2(12582912.f, 12582912.f));
+  const float2 r = __fadd2_rn(j, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __ffma2_rn(r, make_float2(-1.f, -1.f), x);
+  float2 p;
+  if constexpr (DEG == 3) {
+    p = __ffma2_rn(make_float2(0.05516102f, 0.05516102f), f, make_float2(0.24261291f, 0.24261291f));
+    p = __ffma2_rn(p, f, make_float2(0.6932625f, 0.6932625f));
+    p = __ffma2_rn(p, f, make_float2(0.99992794f, 0.99992794f));
+  } else {
+    p = __ffma2_rn(make_float2(0.00134518f, 0.00134518f), f, make_float2(0.00968204f, 0.00968204f));
+    p = __ffma2_rn(p, f, make_float2(0.05550102f, 0.05550102f));
+    p = __ffma2_rn(p, f, make_float2(0.24021935f, 0.24021935f));
+    p = __ffma2_rn(p, f, make_float2(0.6931473f, 0.6931473f));
+    p = __ffma2_rn(p, f, make_float2(1.0000001f, 1.0000001f));
+  }
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(j.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(j.y) << 23)));
+}
+
 }  // namespace mb

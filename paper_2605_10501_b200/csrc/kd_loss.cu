@@ -15,6 +15,9 @@ namespace mb {
 namespace {
 
 constexpr int KD_THREADS = 512;
+#ifndef KD_EMU_BITS
+#define KD_EMU_BITS 0x00  // elements j of each 8-vector whose exponential pair runs on the FMA pipe (measured: no gain, MUFU is not the bound)
+#endif
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float LN2 = 0.6931471805599453f;
 
@@ -114,13 +117,18 @@ __global__ void __launch_bounds__(THREADS, MIN_BLOCKS) kd_loss_kernel(const __nv
           a.ss *= a.ms == -INFINITY ? 0.f : ex2a(a.ms - ms);
           a.ms = ms;
         }
+        // teacher and student exponentials of element j as one pair: paired FMA/add, and
+        // KD_EMU_BITS of the pairs on the FMA pipe (degree-5 polynomial, fp32-accurate)
+        float2 sts = make_float2(a.st, a.ss);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const float et = ex2a(fmaf(ft[j], scale2, -mt));
-          a.st += et;
-          a.at += et * (ft[j] - fs[j]);
-          a.ss += ex2a(fmaf(fs[j], scale2, -ms));
+          const float2 x = __ffma2_rn(make_float2(ft[j], fs[j]), make_float2(scale2, scale2), make_float2(-mt, -ms));
+          const float2 e = ((KD_EMU_BITS >> j) & 1) ? ex2_fma2<5>(x) : make_float2(ex2a(x.x), ex2a(x.y));
+          sts = __fadd2_rn(sts, e);
+          a.at = fmaf(e.x, ft[j] - fs[j], a.at);
         }
+        a.st = sts.x;
+        a.ss = sts.y;
       }
     }
     // block reduction of the online stats
@@ -161,13 +169,16 @@ __global__ void __launch_bounds__(THREADS, MIN_BLOCKS) kd_loss_kernel(const __nv
         unpack8(s4[v], fs);
         uint4 o;
         __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&o);
+        float gg[8];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float g0 = g * (ex2a(fmaf(fs[2 * j], scale2, -f.ms)) * is - ex2a(fmaf(ft[2 * j], scale2, -f.mt)) * it);
-          const float g1 =
-              g * (ex2a(fmaf(fs[2 * j + 1], scale2, -f.ms)) * is - ex2a(fmaf(ft[2 * j + 1], scale2, -f.mt)) * it);
-          oh[j] = __floats2bfloat162_rn(g0, g1);
+        for (int j = 0; j < 8; ++j) {
+          const float2 x = __ffma2_rn(make_float2(fs[j], ft[j]), make_float2(scale2, scale2), make_float2(-f.ms, -f.mt));
+          const float2 e = __fmul2_rn(((KD_EMU_BITS >> j) & 1) ? ex2_fma2<5>(x) : make_float2(ex2a(x.x), ex2a(x.y)),
+                                      make_float2(is, it));
+          gg[j] = g * (e.x - e.y);
         }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) oh[j] = __floats2bfloat162_rn(gg[2 * j], gg[2 * j + 1]);
         d4[v] = o;
       }
     }
