@@ -203,11 +203,13 @@ def run_vlm(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    # the VLM step is ~15 ms, so the sampler (200 ms period, ~100 ms start-up) already runs through
+    # the warm-up steps to have samples under load
+    clocks = ClockSampler(local)
+    clocks.start()
     for _ in range(args.warmup):
         ex.step(hb, want_loss=False)
     barrier()
-    clocks = ClockSampler(local)
-    clocks.start()
     launches0 = instrument.launches
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     stalls = []
