@@ -104,6 +104,33 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------------------------- CPU leg
+def cpu_schedule_baseline(planner, reps: int = 5):
+    """The reference's CPU scheduler path (scheduling.py build_schedule) on the step's own 6-tuples,
+    through the oracle's C port, single-threaded -- the CPU baseline for K1-K5.  The
+    6-tuples and activation masks are read back from the device planner after the timed region;
+    the device orders are compared with the oracle's (bit-exact parity on the benched batch)."""
+    import numpy as np
+
+    import oracle
+
+    tab, B = planner.tables, planner.B
+    times = planner.times[: 6 * B].view(6, B).cpu().numpy()
+    act = planner.act[:B].cpu().numpy().view(np.uint32)
+    dp = [planner.configs[s].dp for s in tab.section_ids]
+    fan = [planner.configs[s].fanout for s in tab.section_ids]
+    best = None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        up, down = oracle.resolve(act, times, tab.sub_owner, tab.side, tab.up_candidates, tab.down_candidates)
+        want, evals = oracle.build_schedule(times, np.arange(B), up, down, len(tab.section_ids), tab.critical, dp,
+                                            fan, tab.neighbor, tab.merge_order, planner.policy.value)
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    got = {k: list(v) for k, v in planner.host_orders().items()}
+    return {"ms": best * 1e3, "cores": 1, "makespan_evals": evals, "device_orders_match": got == want,
+            "sample": f"build_schedule of the benched batch (B={B}), oracle/sched_oracle.c port of scheduling.py"}
+
+
 def cpu_kd_step_sample(seq: int = SEQ, reps: int = 1):
     """The oracle's fp32 CPU restatement of one KD training step on ONE sample (all host threads)."""
     import torch
@@ -461,6 +488,10 @@ def main():
             cpu = {"value": 1.0 / sec, "unit": UNIT, "cores": threads, "kind": "port",
                    "sample": "1 sample of 2048 tokens: oracle/torch_ref.py fp32 KD step on the host CPU "
                              "(teacher fwd + colocated head, student fwd/bwd, KL, AdamW)"}
+            try:
+                cpu["scheduler"] = cpu_schedule_baseline(ex.planner)
+            except Exception as exc:  # noqa: BLE001
+                cpu["scheduler"] = {"error": repr(exc)}
         except Exception as exc:  # noqa: BLE001
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {exc}"}
     xcheck = None
