@@ -234,15 +234,18 @@ def run_vlm(args):
     # the warm-up steps to have samples under load
     clocks = ClockSampler(local)
     clocks.start()
+    # the co-resident executor plans the next step's batch beside the current step (the batch of
+    # step i+1 is known at step i, as with a prefetching loader)
+    nxt = {"next_hb": hb} if isinstance(ex, VLMExecutor) else {}
     for _ in range(args.warmup):
-        ex.step(hb, want_loss=False)
+        ex.step(hb, want_loss=False, **nxt)
     barrier()
     launches0 = instrument.launches
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     stalls = []
     e0.record()
     for _ in range(args.steps):
-        st = ex.step(hb, want_loss=True)
+        st = ex.step(hb, want_loss=True, **nxt)
         stalls.append(st.stall_frac)
     e1.record()
     barrier()

@@ -139,14 +139,41 @@ class VLMExecutor:
         self.cost = torch.from_numpy(cost_table(self.graph, self.configs, self.rec.params)).to(dev)
         self.lr = lr
         self.dp_group = dp_group
+        self.s_plan = torch.cuda.Stream(device=dev)
+        W = N.MAX_DP + 1
+        n_sec = len(self.graph.tables.section_ids)
+        self._h_orders = torch.empty(n_sec * batch, dtype=torch.int32).pin_memory()
+        self._h_off = torch.empty(n_sec * W, dtype=torch.int32).pin_memory()
+        self._pending = None  # (host batch, readback event, live inputs) of a plan enqueued ahead
         self.s_llm = torch.cuda.Stream(device=dev)
         self.s_vit = torch.cuda.Stream(device=dev)
         self.step_idx = 0
         tab = self.graph.tables
         self.bits = {n: i for i, n in enumerate(tab.sub_names)}
 
-    def step(self, hb: dict, want_loss: bool = True) -> StepStats:
-        """One iteration from a host batch (vlm_host_batch); inputs are copied in per step."""
+    def _plan(self, hb: dict, stream):
+        """Enqueue K1-K4 for host batch ``hb`` on ``stream`` plus an asynchronous readback of the
+        rank orders into pinned host buffers; returns (event of the readback, live inputs)."""
+        dev, B = self.device, self.batch
+        tok = np.zeros((len(self.bits), B), dtype=np.int32)
+        tok[self.bits["llm"]] = hb["lens"]
+        tok[self.bits["vit"]] = np.where(hb["has_img"], R.VIT_PATCHES, 0)
+        with torch.cuda.stream(stream):
+            tokens = torch.from_numpy(tok).pin_memory().to(dev, non_blocking=True)
+            ids = torch.arange(B, dtype=torch.int32).pin_memory().to(dev, non_blocking=True)
+            self.planner.ids[:B].copy_(ids)
+            self.planner.plan_tokens(self.cost, tokens, B, stream)
+            self._h_orders.copy_(self.planner.orders[: self._h_orders.numel()], non_blocking=True)
+            self._h_off.copy_(self.planner.sec_off, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+        return ev, (tokens, ids)
+
+    def step(self, hb: dict, want_loss: bool = True, next_hb: dict | None = None) -> StepStats:
+        """One iteration from a host batch (vlm_host_batch); inputs are copied in per step.
+        ``next_hb`` (the following step's batch, e.g. from a prefetching loader) lets the step
+        enqueue that batch's schedule on a side stream while its own kernels run, so the next
+        step starts without a planning round trip (the scheduler overlaps the step)."""
         dev, B = self.device, self.batch
         main = torch.cuda.current_stream(dev)
         t0 = torch.cuda.Event(enable_timing=True)
@@ -155,22 +182,23 @@ class VLMExecutor:
         labels = torch.from_numpy(hb["labels"]).to(dev, non_blocking=True)
         lens = torch.from_numpy(hb["lens"]).to(dev, non_blocking=True)
         pixels = torch.from_numpy(hb["pixels"]).to(dev, non_blocking=True).to(torch.bfloat16)
-        tok = np.zeros((len(self.bits), B), dtype=np.int32)
-        tok[self.bits["llm"]] = hb["lens"]
-        tok[self.bits["vit"]] = np.where(hb["has_img"], R.VIT_PATCHES, 0)
-        tokens = torch.from_numpy(tok).to(dev, non_blocking=True)
-        # ---- device plan: K1 6-tuples -> K2-K4 schedule
-        self.planner.ids[:B].copy_(torch.arange(B, dtype=torch.int32))
-        self.planner.plan_tokens(self.cost, tokens, B)
+        # ---- device plan: K1 6-tuples -> K2-K4 schedule (enqueued by the previous step when it
+        # was given this batch; otherwise now, on the main stream)
+        if self._pending is not None and self._pending[0] is hb:
+            ev = self._pending[1]
+        else:
+            ev, live = self._plan(hb, main)
+        self._pending = None
         tab = self.graph.tables
         ci, vi = tab.critical, tab.section_ids.index("vit")
         W = N.MAX_DP + 1
-        off = self.planner.sec_off.view(-1, W)
         # one small readback: both rank orders (<= 2 x 64 ints) define the micro-batch plan
-        orders = self.planner.orders.view(-1, B)
-        o_llm = orders[ci, :B].cpu().numpy()
-        n_vit = int(off[vi, 1].item())
-        o_vit = orders[vi, :n_vit].cpu().numpy()
+        ev.synchronize()
+        orders = self._h_orders.numpy().reshape(-1, B)
+        off = self._h_off.numpy().reshape(-1, W)
+        o_llm = orders[ci, :B].copy()
+        n_vit = int(off[vi, 1])
+        o_vit = orders[vi, :n_vit].copy()
         # ---- K5 pack of the LLM order; token ids + labels in schedule order
         o_llm_d = torch.from_numpy(o_llm).to(dev)
         n_mb = -(-B // self.mbs_llm)
@@ -274,6 +302,11 @@ class VLMExecutor:
         if self.dp_group is None:
             with torch.cuda.stream(self.s_llm):
                 self.llm.p.adamw(self.lr)
+        if next_hb is not None:
+            # the next batch's schedule runs beside this step's tail (the host copies above were
+            # made before the planner buffers are rewritten)
+            self.s_plan.wait_event(ev)
+            self._pending = (next_hb, *self._plan(next_hb, self.s_plan))
         main.wait_stream(self.s_llm)
         main.wait_stream(self.s_vit)
         if self.dp_group is not None:
