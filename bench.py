@@ -244,11 +244,13 @@ def run_vlm(args):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     stalls = []
     e0.record()
+    sts = []
     for _ in range(args.steps):
-        st = ex.step(hb, want_loss=True, **nxt)
-        stalls.append(st.stall_frac)
+        sts.append(ex.step(hb, want_loss=True, **nxt))
     e1.record()
     barrier()
+    stalls = [x.stall_frac for x in sts]  # read after the timed region (lazy stats synchronise)
+    st = sts[-1]
     clk = clocks.stop()
     t = torch.tensor([e0.elapsed_time(e1), max(stalls) if getattr(ex, "role", "llm") == "llm" else 0.0],
                      device="cuda")

@@ -115,6 +115,27 @@ class ViTSection:
         D.linear_wgrad(dx0, st["pixels"], self.p.g("patch_w"))
 
 
+class LazyStepStats:
+    """StepStats of an enqueued step, evaluated on first access (synchronises on the step's end
+    event then): ``loss``, ``step_ms``, ``critical_busy_ms``, ``critical_span_ms``, ``stall_frac``."""
+
+    def __init__(self, t0, t1, clock, loss_acc, grad_scale):
+        self._args = (t0, t1, clock, loss_acc, grad_scale)
+        self._st = None
+
+    def _eval(self) -> StepStats:
+        if self._st is None:
+            t0, t1, clock, loss_acc, grad_scale = self._args
+            t1.synchronize()
+            busy, span = clock.busy_span()
+            loss = float(loss_acc.item()) * grad_scale if loss_acc is not None else None
+            self._st = StepStats(loss, t0.elapsed_time(t1), busy, span)
+        return self._st
+
+    def __getattr__(self, name):
+        return getattr(self._eval(), name)
+
+
 class VLMExecutor:
     """Co-resident VLM step on one GPU (cfg 1 layout "1 GPU").  With ``dp_group`` (a
     torch.distributed group) every rank runs the co-resident step on its own batch and the ViT and
@@ -323,10 +344,9 @@ class VLMExecutor:
         t1 = torch.cuda.Event(enable_timing=True)
         t1.record(main)
         self.step_idx += 1
-        loss = float(loss_acc.item()) * grad_scale if want_loss else None
-        t1.synchronize()
-        busy, span = clock.busy_span()
-        return StepStats(loss, t0.elapsed_time(t1), busy, span)
+        # no host synchronisation here: the statistics (and the loss) are read on first access, so
+        # the host can enqueue the next step while this one runs
+        return LazyStepStats(t0, t1, clock, loss_acc if want_loss else None, grad_scale)
 
     def model_flops_per_step(self, hb) -> float:
         L = self.llm_shape
