@@ -37,10 +37,6 @@ constexpr int THREADS = 192;
 
 enum Epi { EPI_BF16 = 0, EPI_F32 = 1, EPI_F32_ACC = 2, EPI_F32_ATOMIC = 3 };
 
-__device__ __forceinline__ void red_add_v4f(float* addr, float a, float b, float c, float d) {
-  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
-               : "memory");
-}
 
 struct TileSched {
   int num_m, num_n;
@@ -297,52 +293,48 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           }
           fence_proxy_async_smem();
           named_barrier_sync(1, 128);
-          if (et == 0 && n0 + c < N && row0 < M) {
-            tma_store_2d(&map_c, buf, n0 + c, row0);
-            bulk_commit();
+          if (et == 0) {
+            if (n0 + c < N && row0 < M) tma_store_2d(&map_c, buf, n0 + c, row0);
+            bulk_commit();  // one group per chunk, even when empty: the wait_read<1> above counts chunks
           }
         }
       } else {
+        // fp32 outputs: TMEM -> swizzled smem box (128 rows x 32 fp32, SWIZZLE_128B) -> one TMA op
+        // per chunk: a bulk store (EPI_F32) or an L2 reduce-add (EPI_F32_ACC: C += tile;
+        // EPI_F32_ATOMIC: split-K slices adding into C).  Full-line transactions instead of a
+        // 16-byte segment per row per instruction; the map clips rows/columns past M/N.
+        const int r_in = q * 32 + lane;
 #pragma unroll 1
-      for (int c = 0; c < BN2; c += 32) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + as * BN2 + c, r);
-        tmem_ld_wait();
-        const int col = n0 + c;
-        if (row >= M || col >= N) continue;
-        const bool full_chunk = col + 32 <= N;
-        {
-          float* out = reinterpret_cast<float*>(C) + (size_t)row * ldc + col;
-          const int nv = full_chunk ? 8 : (N - col) / 4;
-          if (EPI == EPI_F32_ATOMIC) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-              if (j < nv)
-                red_add_v4f(out + 4 * j, __uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
-                            __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
-            continue;
+        for (int c = 0; c < BN2; c += 32, ++chunk_ctr) {
+          unsigned char* buf = sC + (chunk_ctr & 1) * CF::EPI_BUF;
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + as * BN2 + c, r);
+          tmem_ld_wait();
+          if (chunk_ctr >= 2) {
+            if (et == 0) bulk_wait_read<1>();  // the op issued from this buffer has read it
+            named_barrier_sync(1, 128);
           }
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            if (j >= nv) break;
-            float4 v = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
-                                   __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
-            if (EPI == EPI_F32_ACC) {
-              const float4 o = reinterpret_cast<const float4*>(out)[j];
-              v.x += o.x;
-              v.y += o.y;
-              v.z += o.z;
-              v.w += o.w;
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<uint4*>(buf + r_in * 128 + ((j ^ (r_in & 7)) << 4)) =
+                make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
+          fence_proxy_async_smem();
+          named_barrier_sync(1, 128);
+          if (et == 0) {
+            if (n0 + c < N && row0 < M) {
+              if (EPI == EPI_F32)
+                tma_store_2d(&map_c, buf, n0 + c, row0);
+              else
+                tma_reduce_add_2d(&map_c, buf, n0 + c, row0);
             }
-            reinterpret_cast<float4*>(out)[j] = v;
+            bulk_commit();  // one group per chunk, even when empty: the wait_read<1> above counts chunks
           }
         }
-      }
       }
       tc_fence_before();
       mbar_arrive_cluster(tempty_leader0 + (uint32_t)(as * sizeof(uint64_t)));
     }
-    if (EPI == EPI_BF16 && et == 0) bulk_wait<0>();
+    if (et == 0) bulk_wait<0>();
   }
   tc_fence_before();
   cluster_sync();
@@ -448,13 +440,13 @@ static int gemm_impl(const void* A, const void* B, void* C, int32_t M, int32_t N
     const int kb = (K + BK - 1) / BK;
     if (epi == EPI_F32_ACC && t256 < pairs && kb >= 8) {
       // split K to fill the pairs; per-pair cost = ceil(tiles*s/pairs) * (k-blocks per slice +
-      // epilogue), where a split slice's epilogue (a 256x256 fp32 tile of red.global.add) costs
-      // ~4 k-blocks of MMA and the unsplit read-modify-write ~1
+      // epilogue), where a slice's epilogue (a 256x256 fp32 tile reduce-added into C by TMA)
+      // costs ~2 k-blocks of MMA and the unsplit one ~1
       bn2 = 256;
       long long best = -1;
       for (int sp = 1; sp <= kb / 2; ++sp) {
         const long long waves = (t256 * sp + pairs - 1) / pairs;
-        const long long cost = waves * ((kb + sp - 1) / sp + (sp > 1 ? 4 : 1));
+        const long long cost = waves * ((kb + sp - 1) / sp + (sp > 1 ? 2 : 1));
         if (best < 0 || cost < best) {
           best = cost;
           splits = sp;
@@ -471,6 +463,8 @@ static int gemm_impl(const void* A, const void* B, void* C, int32_t M, int32_t N
     if (resid != nullptr && (epi_k != EPI_BF16 || !make_map_2d(&mr, resid, N, M, ldr, 64, 128)))
       return (int)cudaErrorInvalidValue;
     if (epi_k == EPI_BF16 && C != nullptr && !make_map_2d(&mc, C, N, M, ldc, 64, 128))
+      return (int)cudaErrorInvalidValue;
+    if (epi_k != EPI_BF16 && !make_map_2d(&mc, C, N, M, ldc, 32, 128, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4))
       return (int)cudaErrorInvalidValue;
     if (C == nullptr && swiglu_out == nullptr) return (int)cudaErrorInvalidValue;
     bool ok = a_mn ? make_map_2d(&ma, A, M, K, lda, 64, 64) : make_map_2d(&ma, A, K, M, lda, 64, 128);

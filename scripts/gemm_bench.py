@@ -25,8 +25,9 @@ def timeit(fn, iters=20, warm=5):
 
 def main():
     shapes = [(8192, 8192, 8192)]
-    if "--student" in sys.argv:  # the student's per-micro-batch GEMMs (T = 4 x 2048)
-        shapes = [(8192, 2304, 768), (8192, 768, 768), (8192, 6144, 768), (8192, 768, 3072), (8192, 32000, 768)]
+    if "--student" in sys.argv:  # the student's per-micro-batch GEMMs (T = mbs x 2048; mbs 8 by default)
+        T = 2048 * int(sys.argv[sys.argv.index("--student") + 1]) if len(sys.argv) > sys.argv.index("--student") + 1 else 16384
+        shapes = [(T, 2304, 768), (T, 768, 768), (T, 6144, 768), (T, 768, 3072), (T, 32000, 768)]
     elif "--step" in sys.argv:  # the exact per-micro-batch GEMMs of the KD step (T = 4 x 2048)
         shapes += [(8192, 2560, 2048), (8192, 2048, 2048), (8192, 11264, 2048), (8192, 2048, 5632),
                    (8192, 32000, 2048), (8192, 2304, 768), (8192, 768, 768), (8192, 6144, 768),
