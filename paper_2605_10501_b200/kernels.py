@@ -44,7 +44,7 @@ def _p(t):
 
 
 def _s():
-    return torch.cuda.current_stream().cuda_stream
+    return N.stream_ptr()
 
 
 def add_rmsnorm(x, a, h, y, w, rstd, eps=1e-5):

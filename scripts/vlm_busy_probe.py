@@ -12,14 +12,14 @@ from paper_2605_10501_b200.vlm import VLMExecutor, vlm_host_batch  # noqa: E402
 ex = VLMExecutor(batch=64, mbs_llm=32, mbs_vit=32)
 hb = vlm_host_batch(64, seed=0)
 for _ in range(3):
-    ex.step(hb, want_loss=False)
+    ex.step(hb, want_loss=False, next_hb=hb)
 torch.cuda.synchronize()
 from torch.profiler import ProfilerActivity, profile  # noqa: E402
 
 with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
     t0 = time.perf_counter()
     for _ in range(5):
-        ex.step(hb, want_loss=False)
+        ex.step(hb, want_loss=False, next_hb=hb)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
 iv = sorted((e.time_range.start, e.time_range.end) for e in prof.events() if e.device_type.name == "CUDA")
