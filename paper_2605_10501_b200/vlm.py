@@ -554,13 +554,15 @@ class VLMGroupExecutor:
         dev, d = self.device, self.llm_shape.d
         mbs = self.mbs_vit
         peers = [r for r in range(self.dp_llm) if r // self.f == self.q]
-        pixels_all = hb["pixels"]
         ordinal = hb["img_ordinal"]
         n_mb = -(-len(order) // mbs)
         ctxs = []
+        with torch.cuda.stream(self.stream):
+            pixels_all = pinned_inputs(hb)["pixels"].to(dev, non_blocking=True).view(torch.bfloat16)
         for k in range(n_mb):
             samples = order[k * mbs: (k + 1) * mbs]
-            px = _h2d(pixels_all[ordinal[samples]], dev).to(torch.bfloat16)
+            with torch.cuda.stream(self.stream):
+                px = pixels_all.index_select(0, _h2d(ordinal[samples].astype(np.int64), dev))
             clock.begin(self.stream, f"f_bc{k}")
             emb, st = self.vit.forward(px.view(-1, PATCH_DIM), len(samples))
             clock.end(self.stream)
@@ -619,9 +621,10 @@ class VLMGroupExecutor:
         s = self.stream.cuda_stream
         lens_h = hb["lens"]
         o_d = _h2d(order.astype(np.int32), dev)
-        lens = _h2d(lens_h, dev)
-        ids = _h2d(hb["ids"], dev)
-        labels = _h2d(hb["labels"], dev)
+        pin = pinned_inputs(hb)
+        lens = pin["lens"].to(dev, non_blocking=True)
+        ids = pin["ids"].to(dev, non_blocking=True)
+        labels = pin["labels"].to(dev, non_blocking=True)
         n_mb = -(-B // mbs)
         z = lambda k: torch.empty(k, dtype=torch.int32, device=dev)  # noqa: E731
         mb, tok_off, mb_tok, cu, mb_start = z(B), z(B), z(n_mb), z(n_mb * (mbs + 1)), z(n_mb)
