@@ -222,7 +222,7 @@ class VLMExecutor:
         n_vit = int(off[vi, 1])
         o_vit = orders[vi, :n_vit].copy()
         # ---- K5 pack of the LLM order; token ids + labels in schedule order
-        o_llm_d = torch.from_numpy(o_llm).to(dev)
+        o_llm_d = _h2d(o_llm, dev)
         n_mb = -(-B // self.mbs_llm)
         z = lambda k: torch.empty(k, dtype=torch.int32, device=dev)  # noqa: E731
         mb, tok_off, mb_tok, cu, mb_start = z(B), z(B), z(n_mb), z(n_mb * (self.mbs_llm + 1)), z(n_mb)
@@ -255,7 +255,7 @@ class VLMExecutor:
         with torch.cuda.stream(self.s_vit):
             for k in range(n_vmb):
                 samples = o_vit[k * self.mbs_vit: (k + 1) * self.mbs_vit]
-                idx = torch.from_numpy(ordinal[samples].astype(np.int64)).to(dev)
+                idx = _h2d(ordinal[samples].astype(np.int64), dev)
                 px = pixels.index_select(0, idx).view(-1, PATCH_DIM)
                 emb, st = self.vit.forward(px, len(samples))
                 emb_buf[k * self.mbs_vit * 49: k * self.mbs_vit * 49 + emb.shape[0]].copy_(emb)
@@ -291,8 +291,8 @@ class VLMExecutor:
                         src_rows.append(np.arange(49) + 49 * vit_pos[int(i)])
                         dst_rows.append(np.arange(49) + base)
                 if src_rows:
-                    sr = torch.from_numpy(np.concatenate(src_rows).astype(np.int32)).to(dev)
-                    dr = torch.from_numpy(np.concatenate(dst_rows).astype(np.int32)).to(dev)
+                    sr = _h2d(np.concatenate(src_rows).astype(np.int32), dev)
+                    dr = _h2d(np.concatenate(dst_rows).astype(np.int32), dev)
                     K.scatter_rows(emb_buf, x0, sr, dr)
                 yf, ctx = self.llm.forward(b, x0=x0)
                 logits = self.llm.logits(yf)
