@@ -244,6 +244,10 @@ int maestro_embed_bwd(const void* dout, const int32_t* ids, float* dtable, int32
    K-major weight copies the dgrad GEMM reads (see FlatParams.refresh_transposed). */
 int maestro_transpose_bf16(const void* src, void* dst, int32_t rows, int32_t cols, int32_t ld_src, int32_t ld_dst,
                            void* stream);
+/* Several transposes in one launch.  desc: device int64[n][8] = {src ptr, dst ptr, rows, cols,
+   ld_src, ld_dst, first tile, tiles along cols}; tiles are 64 x 64, numbered consecutively over
+   the matrices (first tile ascending); total_tiles = sum of ceil(rows/64) * ceil(cols/64). */
+int maestro_transpose_bf16_batched(const int64_t* desc, int32_t n, int32_t total_tiles, void* stream);
 int maestro_adamw(float* p, const float* g, float* m, float* v, void* pb, int64_t n, float lr, float b1, float b2,
                   float eps, float wd, int32_t step, float gscale, void* stream);
 

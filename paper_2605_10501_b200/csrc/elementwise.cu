@@ -576,10 +576,9 @@ MAESTRO_API int maestro_embed_bwd(const void* dout, const int32_t* ids, float* d
 
 // dst[c][r] = src[r][c] (bf16), 64 x 64 tiles through padded shared memory: 16-byte row loads,
 // 16-byte column-gathered stores.  Used to keep K-major copies of weights for the dgrad GEMM.
-__global__ void transpose_bf16_kernel(const __nv_bfloat16* __restrict__ src, __nv_bfloat16* __restrict__ dst,
-                                      int rows, int cols, int ld_src, int ld_dst) {
-  __shared__ __nv_bfloat16 tile[64][64 + 8];
-  const int r0 = blockIdx.y * 64, c0 = blockIdx.x * 64;
+__device__ __forceinline__ void transpose_tile(const __nv_bfloat16* __restrict__ src, __nv_bfloat16* __restrict__ dst,
+                                               int rows, int cols, int ld_src, int ld_dst, int r0, int c0,
+                                               __nv_bfloat16 (*tile)[64 + 8]) {
   for (int i = threadIdx.x; i < 64 * 8; i += blockDim.x) {
     const int r = i >> 3, cv = (i & 7) * 8;
     uint4 v = make_uint4(0, 0, 0, 0);
@@ -597,6 +596,34 @@ __global__ void transpose_bf16_kernel(const __nv_bfloat16* __restrict__ src, __n
   }
 }
 
+__global__ void transpose_bf16_kernel(const __nv_bfloat16* __restrict__ src, __nv_bfloat16* __restrict__ dst,
+                                      int rows, int cols, int ld_src, int ld_dst) {
+  __shared__ __nv_bfloat16 tile[64][64 + 8];
+  transpose_tile(src, dst, rows, cols, ld_src, ld_dst, blockIdx.y * 64, blockIdx.x * 64, tile);
+}
+
+// Many matrices in one launch (the K-major weight copies refreshed after every optimizer step:
+// ~60 small matrices per section, launch-bound one by one).  desc[i] = {src, dst, rows, cols,
+// ld_src, ld_dst, first tile, tiles along cols}; block b handles tile b of the concatenation.
+__global__ void transpose_bf16_batched_kernel(const int64_t* __restrict__ desc, int n) {
+  __shared__ __nv_bfloat16 tile[64][64 + 8];
+  __shared__ int s_i;
+  const int b = blockIdx.x;
+  if (threadIdx.x == 0) {
+    int lo = 0, hi = n - 1;  // last matrix whose first tile <= b
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (desc[mid * 8 + 6] <= b) lo = mid; else hi = mid - 1;
+    }
+    s_i = lo;
+  }
+  __syncthreads();
+  const int64_t* d = desc + s_i * 8;
+  const int t = b - (int)d[6], tx = (int)d[7];
+  transpose_tile(reinterpret_cast<const __nv_bfloat16*>(d[0]), reinterpret_cast<__nv_bfloat16*>(d[1]), (int)d[2],
+                 (int)d[3], (int)d[4], (int)d[5], (t / tx) * 64, (t % tx) * 64, tile);
+}
+
 MAESTRO_API int maestro_transpose_bf16(const void* src, void* dst, int32_t rows, int32_t cols, int32_t ld_src,
                                        int32_t ld_dst, void* stream) {
   if (rows <= 0 || cols <= 0) return 0;
@@ -604,6 +631,12 @@ MAESTRO_API int maestro_transpose_bf16(const void* src, void* dst, int32_t rows,
   dim3 grid((cols + 63) / 64, (rows + 63) / 64);
   transpose_bf16_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)src, (__nv_bfloat16*)dst, rows,
                                                                  cols, ld_src, ld_dst);
+  return launch_status();
+}
+
+MAESTRO_API int maestro_transpose_bf16_batched(const int64_t* desc, int32_t n, int32_t total_tiles, void* stream) {
+  if (n <= 0 || total_tiles <= 0) return 0;
+  transpose_bf16_batched_kernel<<<total_tiles, 256, 0, (cudaStream_t)stream>>>(desc, n);
   return launch_status();
 }
 

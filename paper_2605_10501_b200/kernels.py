@@ -23,6 +23,7 @@ _SIGS = {
     "maestro_embed_fwd": [_P, _P, _P, _I32, _I32, _P],
     "maestro_embed_bwd": [_P, _P, _P, _I32, _I32, _P],
     "maestro_transpose_bf16": [_P, _P, _I32, _I32, _I32, _I32, _P],
+    "maestro_transpose_bf16_batched": [_P, _I32, _I32, _P],
     "maestro_adamw": [_P, _P, _P, _P, _P, _I64, _F, _F, _F, _F, _F, _I32, _F, _P],
     "maestro_kd_loss_fwd_bwd": [_P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32, _F, _F, _P],
     "maestro_ce_loss_fwd_bwd": [_P, _P, _P, _P, _I32, _I32, _I32, _I32, _F, _P],
@@ -95,6 +96,26 @@ def transpose(src, dst):
     """dst[c, r] = src[r, c] (bf16, 2-D, row pitch from the tensors)."""
     R, C = src.shape
     N.check(L().maestro_transpose_bf16(_p(src), _p(dst), R, C, src.stride(0), dst.stride(0), _s()), "transpose_bf16")
+
+
+def transpose_batch_desc(pairs, device) -> tuple[torch.Tensor, int]:
+    """Descriptor table for transpose_batched: pairs = [(src, dst)] of 2-D bf16 tensors (dst is
+    src^T).  Returns (int64 [n, 8] on device, total tiles).  Pointers are captured: rebuild if
+    any tensor is reallocated."""
+    rows, first = [], 0
+    for src, dst in pairs:
+        R, C = src.shape
+        if R % 8 or C % 8 or src.stride(0) % 8 or dst.stride(0) % 8:
+            raise ValueError("transpose_batched: rows, cols and pitches must be multiples of 8")
+        tx, ty = (C + 63) // 64, (R + 63) // 64
+        rows.append([src.data_ptr(), dst.data_ptr(), R, C, src.stride(0), dst.stride(0), first, tx])
+        first += tx * ty
+    return torch.tensor(rows, dtype=torch.int64, device=device), first
+
+
+def transpose_batched(desc: torch.Tensor, total_tiles: int):
+    """All transposes of a transpose_batch_desc table in one launch."""
+    N.check(L().maestro_transpose_bf16_batched(_p(desc), desc.shape[0], total_tiles, _s()), "transpose_batched")
 
 
 def adamw(p, g, m, v, pb, lr, step, b1=0.9, b2=0.95, eps=1e-8, wd=0.1, gscale=1.0):

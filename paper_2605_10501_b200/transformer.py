@@ -135,8 +135,15 @@ class FlatParams:
         return self.wt.get(name)
 
     def refresh_transposed(self):
-        for name, wt in self.wt.items():
-            K.transpose(self[name], wt)
+        """Re-derive every K-major weight copy from the updated bf16 weights: one launch for all
+        (the descriptor table is built once; the arenas are never reallocated)."""
+        if not self.wt:
+            return
+        if getattr(self, "_tdesc", None) is None or self._tdesc_n != len(self.wt):
+            self._tdesc, self._ttiles = K.transpose_batch_desc([(self[n], wt) for n, wt in self.wt.items()],
+                                                               self.w.device)
+            self._tdesc_n = len(self.wt)
+        K.transpose_batched(self._tdesc, self._ttiles)
 
     def zero_grad(self):
         self.grad.zero_()

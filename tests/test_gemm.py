@@ -154,6 +154,19 @@ def test_transpose_ragged():
     assert torch.equal(dst, src.t())
 
 
+def test_transpose_batched_mixed_shapes():
+    from paper_2605_10501_b200 import kernels
+
+    shapes = [(200, 72), (64, 64), (768, 3072), (8, 8), (136, 1000)]
+    srcs = [torch.randn(r, c, device="cuda").bfloat16() for r, c in shapes]
+    dsts = [torch.zeros(c, r, device="cuda", dtype=torch.bfloat16) for r, c in shapes]
+    desc, tiles = kernels.transpose_batch_desc(list(zip(srcs, dsts)), "cuda")
+    kernels.transpose_batched(desc, tiles)
+    torch.cuda.synchronize()
+    for s_, d_ in zip(srcs, dsts):
+        assert torch.equal(d_, s_.t())
+
+
 @pytest.mark.parametrize("M,N,K", [(8192, 2048, 2048), (8192, 768, 3072), (1000, 200, 96), (300, 2048, 5632)])
 def test_residual_epilogue(M, N, K):
     """h = R + A B^T with the add in the epilogue: fp32 sum rounded once (vs fp32 reference)."""
