@@ -464,7 +464,9 @@ static int rmsnorm_generic_bwd(const void* dy, const void* h, const void* w, con
                                void* dx, float* dw, int T, int d, cudaStream_t st) {
   const size_t smem = (size_t)d * sizeof(float);
   if (ensure_smem<rmsnorm_generic_bwd_kernel>(smem)) return launch_status();
-  const int grid = T / 8 < 148 ? (T + 7) / 8 : 148;  // one CTA per SM: 148 x d atomics for dw, ~7 rows per warp
+  // four CTAs per SM (a warp walks its rows with the full load latency per row, so rows in
+  // flight per SM set the speed); 592 x d global atomics for dw at the end
+  const int grid = (T + 7) / 8 < 148 * 4 ? (T + 7) / 8 : 148 * 4;
   rmsnorm_generic_bwd_kernel<<<grid, 256, smem, st>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)h,
                                                       (const __nv_bfloat16*)w, rstd, (const __nv_bfloat16*)dres,
                                                       (__nv_bfloat16*)dx, dw, T, d);
