@@ -1,5 +1,5 @@
 import sys, json, torch
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
 from paper_2605_10501_b200 import kernels as K
 def timeit(fn, iters=50, warm=5):
     for _ in range(warm): fn()
