@@ -12,6 +12,7 @@ import ctypes
 from pathlib import Path
 
 from . import errors as E
+from . import instrument as _instrument
 from .workload import MAX_SECTIONS, SectionConfig, SectionGraph
 
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libmaestro_b200.so"
@@ -111,9 +112,7 @@ def reserve_sms_for_comm(default: int = 16) -> int:
 def check(rc: int, what: str) -> None:
     if rc != 0:
         raise E.NativeError(f"{what} failed with CUDA error {rc}")
-    from . import instrument
-
-    instrument.count(what)
+    _instrument.count(what)
 
 
 def ptr(t) -> int:
