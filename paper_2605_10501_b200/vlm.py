@@ -365,14 +365,19 @@ def pinned_inputs(hb: dict) -> dict:
     """The batch's step inputs in page-locked host memory, built once per host batch (what a
     pinning data loader hands over): token ids, labels, lengths and the image patches as bf16
     bits.  Every step still copies them to the device; a pageable float32 upload of the patches
-    (19 MB at cfg 1) blocked the host for milliseconds per step."""
+    (19 MB at cfg 1) blocked the host for milliseconds per step.  The cache is rebuilt when the
+    dict holds different arrays; arrays modified in place must drop ``hb["_pinned"]``."""
     pin = hb.get("_pinned")
+    keys = ("ids", "labels", "lens", "pixels")
+    if pin is not None and any(pin["_src"][k] is not hb[k] for k in keys):
+        pin = None  # the dict now holds other arrays: rebuild (arrays mutated in place are not detected)
     if pin is None:
         px = np.ascontiguousarray(hb["pixels"], dtype=np.float32).view(np.uint32)
         # round-to-nearest-even fp32 -> bf16 bits (as torch's .to(torch.bfloat16) does)
         px16 = ((px + 0x7FFF + ((px >> 16) & 1)) >> 16).astype(np.uint16)
         pin = {k: torch.from_numpy(np.ascontiguousarray(hb[k])).pin_memory() for k in ("ids", "labels", "lens")}
         pin["pixels"] = torch.from_numpy(px16.view(np.int16)).pin_memory()
+        pin["_src"] = {k: hb[k] for k in keys}
         hb["_pinned"] = pin
     return pin
 

@@ -37,3 +37,24 @@ def test_vlm_loss_decreases():
     hb = vlm.vlm_host_batch(16, seed=1)
     losses = [ex.step(hb).loss for _ in range(4)]
     assert all(np.isfinite(losses)) and losses[-1] < losses[0]
+
+
+def test_pinned_inputs_and_plan_prefetch():
+    """Page-locked step inputs equal the torch conversion, are rebuilt when the dict holds new
+    arrays, and a step planned ahead (next_hb) gives the same result as a synchronous plan."""
+    from paper_2605_10501_b200 import vlm
+
+    hb = vlm.vlm_host_batch(12, seed=5)
+    pin = vlm.pinned_inputs(hb)
+    assert pin["pixels"].is_pinned()
+    assert torch.equal(pin["pixels"].view(torch.bfloat16), torch.from_numpy(hb["pixels"]).to(torch.bfloat16))
+    assert vlm.pinned_inputs(hb) is pin
+    hb2 = vlm.vlm_host_batch(12, seed=6)
+    hb["pixels"] = hb2["pixels"]
+    assert vlm.pinned_inputs(hb) is not pin
+    # prefetched plan vs synchronous plan: identical losses (lr 0, same batch)
+    a = vlm.VLMExecutor(batch=12, mbs_llm=4, mbs_vit=3, lr=0.0)
+    b = vlm.VLMExecutor(batch=12, mbs_llm=4, mbs_vit=3, lr=0.0)
+    la = [a.step(hb2).loss for _ in range(2)]
+    lb = [b.step(hb2, next_hb=hb2).loss for _ in range(2)]
+    assert la == lb
