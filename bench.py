@@ -405,7 +405,7 @@ def main():
 
     p2p = p2p_bandwidth(ex, dist) if (dist is not None and not ex.colocated) else None
     for _ in range(args.warmup):
-        ex.step(ids_dev, want_loss=False)
+        ex.step(ids_dev, want_loss=False, plan_ahead=True)
     barrier()
     # ---- device-timed region (inputs resident in HBM)
     clocks = ClockSampler(local)
@@ -417,7 +417,7 @@ def main():
     stalls, busy, span, stats = [], 0.0, 0.0, []
     e0.record(main_stream)
     for _ in range(args.steps):
-        st = ex.step(ids_dev, want_loss=False)
+        st = ex.step(ids_dev, want_loss=False, plan_ahead=True)
         stalls.append(st.stall_frac)
         busy += st.critical_busy_ms
         span += st.critical_span_ms
@@ -440,7 +440,7 @@ def main():
     f0.record()
     losses = []
     for _ in range(args.steps):
-        st = ex.step(ids_host, want_loss=True)
+        st = ex.step(ids_host, want_loss=True, plan_ahead=True)
         losses.append(st.loss)
     f1.record()
     barrier()
@@ -539,7 +539,7 @@ def main():
                                 "definition": "step time - section busy time, max over ranks"},
             "scheduler": {"device_us_per_step": plan_ms * 1e3, "share_of_step_pct": 100.0 * plan_ms / ms_per_step,
                           "makespan_evals_per_step": sum(n * (n + 1) // 2 for n in n_sched),
-                          "placement": "K1-K5 on the main stream at step start (not overlapped)",
+                          "placement": "K1-K5 of step k+1 on a side stream while step k runs (KDExecutor.step(plan_ahead=True))",
                           "roofline": sched_roof},
             "grad_allreduce": ({"ms": ar_ms, "bytes": grad_bytes,
                                 "bus_GBps": 2 * (dp_s - 1) / dp_s * grad_bytes / (ar_ms / 1e3) / 1e9 if ar_ms else None}

@@ -252,8 +252,31 @@ class KDExecutor:
         return ctx()
 
     # ------------------------------------------------------------------ one step
-    def step(self, ids: torch.Tensor, want_loss: bool = True) -> StepStats:
-        """One training iteration.  ``ids``: [batch, seq] int32 token ids (device or pinned host)."""
+    def _plan_async(self, stream):
+        """K1-K5 for one step on ``stream`` plus an asynchronous readback of the micro-batch token
+        counts into pinned host buffers; returns (tables, host buffers, readback event, device
+        time events of the plan)."""
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        p0.record(stream)
+        plan = self.plan(stream)
+        p1.record(stream)
+        bufs = {}
+        with torch.cuda.stream(stream):
+            for k, v in plan.items():
+                a = torch.empty(v["n_mb"], dtype=torch.int32).pin_memory()
+                b = torch.empty(v["n_mb"], dtype=torch.int32).pin_memory()
+                a.copy_(v["mb_tok"], non_blocking=True)
+                b.copy_(v["mb_start"], non_blocking=True)
+                bufs[k] = (a, b)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+        return plan, bufs, ev, (p0, p1)
+
+    def step(self, ids: torch.Tensor, want_loss: bool = True, plan_ahead: bool = False) -> StepStats:
+        """One training iteration.  ``ids``: [batch, seq] int32 token ids (device or pinned host).
+        ``plan_ahead``: after enqueueing this step, build the next step's schedule on a side stream
+        so it overlaps this step (the sequence lengths -- the schedule's only input -- are fixed
+        per executor), and the next step starts without a planning round trip."""
         dev = self.device
         main = torch.cuda.current_stream(dev)
         if ids.device.type != "cuda":
@@ -263,11 +286,12 @@ class KDExecutor:
             ids_dev = ids
         t_start = torch.cuda.Event(enable_timing=True)
         t_start.record(main)
-        plan = self.plan(main)
-        t_plan = torch.cuda.Event(enable_timing=True)
-        t_plan.record(main)
-        # one small D2H per step: micro-batch token counts of the local rank orders
-        host = {k: (v["mb_tok"].cpu().tolist(), v["mb_start"].cpu().tolist()) for k, v in plan.items()}
+        pending, self._pending = getattr(self, "_pending", None), None
+        plan, bufs, plan_ev, plan_t = pending if pending is not None else self._plan_async(main)
+        # one small readback per step: micro-batch token counts of the local rank orders
+        plan_ev.synchronize()
+        main.wait_event(plan_ev)
+        host = {k: (a.tolist(), b.tolist()) for k, (a, b) in bufs.items()}
         packed = {}
         with torch.cuda.stream(main):
             for sec, v in plan.items():
@@ -308,6 +332,11 @@ class KDExecutor:
             main.wait_stream(self.s_stream)
         if self.teacher is not None and not self.colocated:
             main.wait_stream(self.t_stream)
+        if plan_ahead:
+            if not hasattr(self, "s_plan"):
+                self.s_plan = torch.cuda.Stream(device=dev)
+            self.s_plan.wait_event(plan_ev)  # this step's plan has consumed the planner buffers
+            self._pending = self._plan_async(self.s_plan)
         t_end = torch.cuda.Event(enable_timing=True)
         t_end.record(main)
         self.step_idx += 1
@@ -322,7 +351,7 @@ class KDExecutor:
 
                 raise InconsistentSchedule("handoff delivered unexpected micro-batches", got=got)
         busy, span = clock.busy_span()
-        extra = {"plan_ms": t_start.elapsed_time(t_plan),
+        extra = {"plan_ms": plan_t[0].elapsed_time(plan_t[1]),
                  "teacher_busy_ms": self.t_clock.busy_span()[0] if self.teacher is not None else 0.0}
         if self.student is not None and ar is not None:
             extra["allreduce_ms"] = ar[0].elapsed_time(ar[1])

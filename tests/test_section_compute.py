@@ -265,3 +265,21 @@ def test_kd_uneven_batch_and_micro_batch_ratio():
         res.append((st.loss, ex.student.p.grad.clone()))
     assert abs(res[0][0] - res[1][0]) / abs(res[0][0]) < 1e-3
     assert ((res[0][1] - res[1][1]).abs().max() / res[0][1].abs().max()).item() < 2e-2
+
+
+def test_kd_plan_ahead_matches_synchronous_plan():
+    """step(plan_ahead=True) builds the next schedule beside the current step: same losses and
+    gradients as planning at the start of every step; the plan's device time is still reported."""
+    from paper_2605_10501_b200.executor import KDExecutor, synthetic_ids
+
+    ids = torch.from_numpy(synthetic_ids(8, 128, 512, seed=9)).cuda()
+    out = []
+    for ahead in (False, True):
+        ex = KDExecutor(n_gpus=1, batch_per_rank=8, seq=128, mbs=2, teacher="test_tiny", student="test_tiny",
+                        lr=1e-3)
+        losses = [ex.step(ids, plan_ahead=ahead) for _ in range(3)]
+        out.append(([s.loss for s in losses], ex.student.p.grad.clone(), losses[-1].plan_ms))
+    # split-K weight gradients are reduce-added in L2 (order not fixed): fp32-rounding tolerance
+    assert all(abs(a - b) <= 1e-6 * abs(a) for a, b in zip(out[0][0], out[1][0]))
+    assert ((out[0][1] - out[1][1]).abs().max() / out[0][1].abs().max()).item() < 1e-5
+    assert out[1][2] > 0
