@@ -1,17 +1,23 @@
 """Benchmark: training samples/s of the section-graph executor step (BASELINE.json metric).
 
-Workload (configs[1] of BASELINE.json): knowledge distillation, forward-only 1.1B teacher
+Default workload (configs[1] of BASELINE.json): knowledge distillation, forward-only 1.1B teacher
 (TinyLlama shape) -> 125M student, fused KL over the 32k vocabulary, seq 2048, 64 samples per
 student DP rank, synthetic token ids, random-init weights.  Default layout (--layout colocated):
 every GPU hosts a teacher and a student DP rank (handoff = CUDA event, student gradients
-all-reduced over NCCL); --layout disjoint puts teacher and student on disjoint GPU groups with an
-NCCL send/recv handoff of teacher hidden states (recipes.kd_layout).
+all-reduced over NCCL); --layout disjoint puts teacher and student on disjoint GPU groups with the
+teacher hidden states handed over NVLink (mq.PeerTransport, or NCCL with MAESTRO_HANDOFF=nccl).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+Other workloads (--workload): kd8b = configs[4] (Llama-3-8B -> Llama-3.2-1B, 8k seq, V 128256),
+vlm = configs[0] (tiny VLM), section = the generic section-graph executor on cfg 3 / cfg 4 shapes
+(--graph vlm7b|omni).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload ...]
 
 Prints one JSON line (rank 0).  `value` is device-timed (CUDA events, max over ranks) with
-inputs resident in HBM; `e2e` is the same metric through the public API (KDExecutor.step) with
-token ids in pinned host memory copied in and the loss read back every step.
+inputs resident in HBM; `e2e` is the same metric through the public API (executor.step) timed by
+the host wall clock, with the step inputs copied from pinned host memory and the loss read back
+every step.  Per-kernel timing (roofline) comes from one extra, untimed step with the sections
+serialised on one stream, so kernel durations never overlap and never perturb `value`.
 """
 
 from __future__ import annotations
@@ -23,7 +29,6 @@ import statistics
 import subprocess
 import sys
 import tempfile
-import threading
 import time
 from pathlib import Path
 
@@ -32,12 +37,16 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "training samples/sec (device-timed, max over ranks) at 1/2/4/8 B200; section-stall %"
 UNIT = "samples/s"
-SEQ = 2048
-BATCH_PER_RANK = 64
-MBS = 8  # student micro-batch (samples); measured: 4 -> 8 +4.8 %
-KD_WORKLOAD = ("kd_cfg2: fwd-only 1.1B teacher (TinyLlama shape) -> 125M student, fused KL over 32k vocab, "
-               "seq 2048, teacher head colocated with the student")
-TEACHER_MBS = 16  # forward-only teacher: fuller GEMM waves, fewer launches (8 -> 16 +1.5 %)
+
+KD_PRESETS = {
+    # workload -> (teacher shape, student shape, recipe, seq, batch/rank, student mbs, teacher mbs, vocab, label)
+    "kd": ("kd_teacher_1b", "kd_student_125m", "kd", 2048, 64, 8, 16, 32000,
+           "kd_cfg2: fwd-only 1.1B teacher (TinyLlama shape) -> 125M student, fused KL over 32k vocab, "
+           "seq 2048, teacher head colocated with the student"),
+    "kd8b": ("llama3_8b", "llama32_1b", "kd_8b", 8192, 8, 1, 2, 128256,
+             "kd_cfg5: fwd-only Llama-3-8B-shaped teacher (hd128, GQA 32/8) -> Llama-3.2-1B-shaped student, "
+             "fused KL over 128256 vocab, seq 8192, teacher head colocated with the student"),
+}
 
 
 def load_peaks():
@@ -131,154 +140,125 @@ def cpu_schedule_baseline(planner, reps: int = 5):
             "sample": f"build_schedule of the benched batch (B={B}), oracle/sched_oracle.c port of scheduling.py"}
 
 
-def cpu_kd_step_sample(seq: int = SEQ, reps: int = 1):
-    """The oracle's fp32 CPU restatement of one KD training step on ONE sample (all host threads)."""
+def cpu_kd_step_sample(preset: str = "kd", reps: int = 1):
+    """The oracle's fp32 CPU restatement of one KD training step (all host threads).
+
+    kd: one full sample (2048 tokens, full depth).  kd8b: an 8B fp32 teacher and 8k tokens do not
+    fit a bounded CPU sample, so one 8192-token sample runs through ONE teacher and ONE student
+    layer at full width plus both full-vocab heads and the KL; the step time is extrapolated by the
+    layer counts (t = t_heads + L_t t_teacher_layer + L_s t_student_layer).
+    Returns (seconds per sample, threads, sample description)."""
+    import dataclasses
+    import math
+
     import torch
 
     from oracle import torch_ref as R
     from paper_2605_10501_b200.transformer import SHAPES
 
     torch.set_num_threads(os.cpu_count() or 1)
-    t_shape, s_shape = SHAPES["kd_teacher_1b"], SHAPES["kd_student_125m"]
+    tname, sname, _, seq, _, _, _, vocab, _ = KD_PRESETS[preset]
+    t_full, s_full = SHAPES[tname], SHAPES[sname]
     g = torch.Generator().manual_seed(0)
 
     def flat(shape):
-        n = sum(((__import__("math").prod(s) + 63) // 64 * 64) for _, s in shape.param_shapes())
+        n = sum(((math.prod(s) + 63) // 64 * 64) for _, s in shape.param_shapes())
         return torch.randn(n, generator=g) * 0.02
 
-    t_flat, s_flat = flat(t_shape), flat(s_shape)
-    t_head = torch.randn(t_shape.vocab, t_shape.d, generator=g) * 0.02
-    ids = torch.randint(0, 32000, (seq,), generator=g, dtype=torch.int32)
-    cu = torch.tensor([0, seq], dtype=torch.int32)
-    m, v = torch.zeros_like(s_flat), torch.zeros_like(s_flat)
-    times = []
-    for i in range(reps):
-        t0 = time.perf_counter()
-        _, grad = R.kd_step_reference(t_shape, s_shape, t_flat, s_flat, t_head, ids, cu, global_tokens=seq)
-        R.adamw_reference(s_flat, grad, m, v, 3e-4, i + 1)
-        times.append(time.perf_counter() - t0)
-    return min(times), torch.get_num_threads()
+    def run(t_shape, s_shape):
+        t_flat, s_flat = flat(t_shape), flat(s_shape)
+        t_head = torch.randn(t_shape.vocab, t_shape.d, generator=g) * 0.02
+        ids = torch.randint(0, vocab, (seq,), generator=g, dtype=torch.int32)
+        cu = torch.tensor([0, seq], dtype=torch.int32)
+        m, v = torch.zeros_like(s_flat), torch.zeros_like(s_flat)
+        best = None
+        for i in range(reps):
+            t0 = time.perf_counter()
+            _, grad = R.kd_step_reference(t_shape, s_shape, t_flat, s_flat, t_head, ids, cu, global_tokens=seq)
+            R.adamw_reference(s_flat, grad, m, v, 3e-4, i + 1)
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+        return best
+
+    if preset == "kd":
+        sec = run(t_full, s_full)
+        desc = ("1 sample of 2048 tokens: oracle/torch_ref.py fp32 KD step on the host CPU "
+                "(teacher fwd + colocated head, student fwd/bwd, KL, AdamW)")
+    else:
+        one = lambda s: dataclasses.replace(s, layers=1)  # noqa: E731
+        zero = lambda s: dataclasses.replace(s, layers=0)  # noqa: E731
+        t1 = run(one(t_full), one(s_full))
+        t0 = run(zero(t_full), zero(s_full))
+        t_only = run(one(t_full), zero(s_full))
+        tl, sl = t_only - t0, t1 - t_only
+        sec = t0 + t_full.layers * tl + s_full.layers * sl
+        desc = (f"1 sample of {seq} tokens through 1 teacher + 1 student layer at full width plus both "
+                f"{vocab}-vocab heads and the KL (oracle/torch_ref.py fp32), extrapolated to "
+                f"{t_full.layers} + {s_full.layers} layers: heads {t0:.2f} s, teacher layer {tl:.2f} s, "
+                f"student layer {sl:.2f} s")
+    return sec, torch.get_num_threads(), desc
+
+
+def cpu_vlm_step_sample(batch: int = 8):
+    """The oracle's fp32 CPU restatement of one VLM (cfg 1) step on a bounded batch."""
+    import torch
+
+    from oracle import torch_ref as R
+    from paper_2605_10501_b200 import vlm
+    from paper_2605_10501_b200.transformer import SHAPES
+
+    torch.set_num_threads(os.cpu_count() or 1)
+    ls, vs = SHAPES["vlm_gpt2l"], SHAPES["vit_tiny"]
+    import math
+
+    g = torch.Generator().manual_seed(0)
+
+    def flat(shapes):
+        n = sum(((math.prod(s) + 63) // 64 * 64) for _, s in shapes)
+        return torch.randn(n, generator=g) * 0.02
+
+    lf = flat(ls.param_shapes())
+    vf = flat(vs.param_shapes() + [("patch_w", (vs.d, vlm.PATCH_DIM)), ("proj_w", (ls.d, 4 * vs.d))])
+    hb = vlm.vlm_host_batch(batch, seed=0)
+    t0 = time.perf_counter()
+    R.vlm_step_reference(ls, vs, lf, vf, hb, vlm.merge_index())
+    return (time.perf_counter() - t0) / batch, torch.get_num_threads()
 
 
 def run_reference(args):
-    """--impl reference: the CPU implementation of the path (oracle port; the reference itself is
-    a planning/simulation toolkit with no training step), rank 0 only."""
+    """--impl reference: the CPU implementation of the path (the oracle's fp32 port; the reference
+    itself is a planning/simulation toolkit with no training step), rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    secs = []
-    threads = 1
+    secs, threads, desc = [], 1, ""
     for _ in range(args.warmup + args.steps):
-        t, threads = cpu_kd_step_sample()
+        if args.workload == "vlm":
+            t, threads = cpu_vlm_step_sample()
+            desc = "8 samples per step: oracle/torch_ref.py fp32 VLM step (ViT-tiny, merge, projector, GPT, CE)"
+        else:
+            t, threads, desc = cpu_kd_step_sample(args.workload)
         secs.append(t)
     sec = statistics.mean(secs[args.warmup:]) if args.steps else secs[-1]
     value = 1.0 / sec
+    if args.workload == "vlm":
+        workload, seq, gb = "vlm_cfg1: ViT-tiny (d192 L12) -> 2-layer GPT (d768), 50/50 text/image", "64..497", 64
+    else:
+        P = KD_PRESETS[args.workload]
+        workload, seq, gb = P[8], P[3], (args.batch_per_rank or P[4]) * args.gpus
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": KD_WORKLOAD, "global_batch": args.batch_per_rank * args.gpus, "seq_len": SEQ,
-                   "parallelism": f"host CPU ({threads} threads); each step times a bounded sample of 1 sequence"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": "1 sample of 2048 tokens per step: oracle/torch_ref.py fp32 KD step "
-                                   "(teacher fwd + colocated head, student fwd/bwd, KL, AdamW)"},
+        "config": {"workload": workload, "global_batch": gb, "seq_len": seq,
+                   "parallelism": f"host CPU ({threads} threads); each step times a bounded sample"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": desc},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-# ---------------------------------------------------------------------------------------------- VLM leg
-def run_vlm(args):
-    """configs[0] (tiny VLM: ViT-tiny encoder -> 2-layer GPT, 50/50 text/image).  N=1: sections
-    co-resident on one GPU; N=2/4/8: disjoint ViT / LLM groups (recipes.VLM_LAYOUTS) with the
-    activation and gradient handoff through the reshard message queue; 64 samples per LLM rank."""
-    import torch
-
-    from paper_2605_10501_b200 import instrument
-    from paper_2605_10501_b200.vlm import VLMExecutor, VLMGroupExecutor, vlm_host_batch
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world != args.gpus:
-        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        if args.layout == "colocated":
-            # both sections data-parallel on every GPU: a co-resident step per rank on its own
-            # batch, per-section gradient all-reduce
-            ex = VLMExecutor(batch=args.batch_per_rank, mbs_llm=args.mbs, mbs_vit=args.vit_mbs,
-                             dp_group=dist.group.WORLD)
-            layout = f"colocated vit+llm per GPU, both sections dp{world} (grad all-reduce)"
-        else:
-            ex = VLMGroupExecutor(world, batch_per_llm_rank=args.batch_per_rank, mbs_llm=args.mbs,
-                                  mbs_vit=args.vit_mbs)
-            layout = f"disjoint: vit dp{ex.dp_vit} (fanout {ex.f}) -> llm dp{ex.dp_llm}, NCCL handoff (mq)"
-    else:
-        ex = VLMExecutor(batch=args.batch_per_rank, mbs_llm=args.mbs, mbs_vit=args.vit_mbs)
-        layout = "colocated vit+llm"
-    B = ex.batch
-    hb = vlm_host_batch(B, seed=rank if (world > 1 and args.layout == "colocated") else 0)
-
-    def barrier():
-        torch.cuda.synchronize()
-        if dist is not None:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    # the VLM step is ~15 ms, so the sampler (200 ms period, ~100 ms start-up) already runs through
-    # the warm-up steps to have samples under load
-    clocks = ClockSampler(local)
-    clocks.start()
-    # the co-resident executor plans the next step's batch beside the current step (the batch of
-    # step i+1 is known at step i, as with a prefetching loader)
-    nxt = {"next_hb": hb} if isinstance(ex, VLMExecutor) else {}
-    for _ in range(args.warmup):
-        ex.step(hb, want_loss=False, **nxt)
-    barrier()
-    launches0 = instrument.launches
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    stalls = []
-    e0.record()
-    sts = []
-    for _ in range(args.steps):
-        sts.append(ex.step(hb, want_loss=True, **nxt))
-    e1.record()
-    barrier()
-    stalls = [x.stall_frac for x in sts]  # read after the timed region (lazy stats synchronise)
-    st = sts[-1]
-    clk = clocks.stop()
-    t = torch.tensor([e0.elapsed_time(e1), max(stalls) if getattr(ex, "role", "llm") == "llm" else 0.0],
-                     device="cuda")
-    if dist is not None:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t[0].item())
-    B_all = B * world if (world > 1 and args.layout == "colocated") else B
-    value = B_all * args.steps / (ms / 1e3)
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": "vlm_cfg1: ViT-tiny (d192 L12) -> 2-layer GPT (d768), 50/50 text/image, "
-                                   "wavefront schedule on device", "global_batch": B_all, "seq_len": "64..497",
-                       "parallelism": layout, "micro_batch_llm": args.mbs, "micro_batch_vit": args.vit_mbs,
-                       "note": "end-to-end: inputs copied from host every step"},
-            "section_stall_pct": 100.0 * float(t[1].item()),
-            "gpu_launches": (instrument.launches - launches0) // args.steps,
-            "model_tflops": ex.model_flops_per_step(hb) * (B_all // B) * args.steps / (ms / 1e3) / 1e12, "loss": st.loss,
-            "clocks": clk,
-        }
-        print(json.dumps(line), flush=True)
-    if dist is not None:
-        dist.barrier()
-        dist.destroy_process_group()
-
-
+# ---------------------------------------------------------------------------------------------- helpers
 def fp64_probe():
     """Measured fp64 CUDA-core add throughput (adds/s) and dependent-add latency (s): the
     denominators of the scheduler kernels' roofline (maestro_fp64_probe)."""
@@ -345,37 +325,46 @@ def p2p_bandwidth(ex, dist, nbytes=64 << 20, reps=4):
     return float(t.item())
 
 
-# ---------------------------------------------------------------------------------------------- GPU leg
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--batch-per-rank", type=int, default=BATCH_PER_RANK)
-    ap.add_argument("--mbs", type=int, default=None,
-                    help=f"student (KD, default {MBS}) or LLM (VLM, default 32) micro-batch size")
-    ap.add_argument("--vit-mbs", type=int, default=32,
-                    help="VLM: ViT micro-batch (images); measured 8 -> 32 (with the LLM's): 1724 -> 4471 samples/s")
-    ap.add_argument("--teacher-mbs", type=int, default=TEACHER_MBS,
-                    help="teacher (forward-only) micro-batch size, a multiple of --mbs")
-    ap.add_argument("--layout", default="colocated", choices=["colocated", "disjoint"])
-    ap.add_argument("--trace", default=None, help="write the measured chrome trace of the last step here")
-    ap.add_argument("--workload", default="kd", choices=["kd", "vlm"],
-                    help="kd = BASELINE configs[1] (default); vlm = configs[0] tiny VLM, 1 GPU")
-    args = ap.parse_args()
-    if args.mbs is None:
-        args.mbs = 32 if args.workload == "vlm" else MBS
-    if args.workload == "vlm":
-        run_vlm(args)
-        return
-    if args.impl == "reference":
-        run_reference(args)
-        return
+def kernel_fractions(rec: dict, step_ms: float, peaks: dict, attn_flops=None, kd_bytes=None) -> dict:
+    """Per-kernel roofline fractions from one serialised, untimed step (instrument.stop_timing):
+    tensor-bound kernels against the measured sustained bf16 peak, K9 against measured HBM GB/s."""
+    peak_t = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+    out = {}
+    for kind in ("attn_fwd", "attn_bwd"):
+        if kind in rec and attn_flops is not None:
+            _, ms, n = rec[kind]
+            fl = attn_flops[0 if kind == "attn_fwd" else 1]
+            if ms > 0 and fl > 0:
+                a = fl / (ms / 1e3) / 1e12
+                out[kind] = {"achieved": a, "peak": peak_t, "unit": "TFLOP/s", "frac": a / peak_t,
+                             "launches": n, "ms": ms, "share_of_step": ms / step_ms}
+    if "kd_loss" in rec:
+        by, ms, n = rec["kd_loss"]
+        if ms > 0:
+            a = by / (ms / 1e3) / 1e9
+            out["kd_loss"] = {"achieved": a, "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": a / peaks["hbm_gbs"],
+                              "launches": n, "ms": ms, "share_of_step": ms / step_ms}
+    return out
 
+
+def gemm_traffic(workload: str):
+    """DRAM bytes per launch of the dominant GEMM at the benched shape, from the committed ncu
+    --set full capture (profiles/r02_gemm_traffic.json, one entry per workload), or None."""
+    p = ROOT / "profiles" / "r02_gemm_traffic.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text()).get(workload)
+    return d
+
+
+# ---------------------------------------------------------------------------------------------- KD leg
+def run_kd(args):
     import torch
 
+    tname, sname, recipe, seq, bpr, mbs, tmbs, vocab, workload = KD_PRESETS[args.workload]
+    bpr = args.batch_per_rank or bpr
+    mbs = args.mbs or mbs
+    tmbs = args.teacher_mbs or tmbs
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -389,12 +378,12 @@ def main():
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
 
     from paper_2605_10501_b200 import instrument
-    from paper_2605_10501_b200.executor import KDExecutor, synthetic_ids
+    from paper_2605_10501_b200.executor import KDExecutor, handoff_mode, synthetic_ids
 
-    ex = KDExecutor(n_gpus=args.gpus, batch_per_rank=args.batch_per_rank, seq=SEQ, mbs=args.mbs,
-                    layout=args.layout, teacher_mbs=args.teacher_mbs)
+    ex = KDExecutor(n_gpus=args.gpus, batch_per_rank=bpr, seq=seq, mbs=mbs, layout=args.layout, teacher_mbs=tmbs,
+                    teacher=tname, student=sname, recipe=recipe)
     B = ex.batch
-    ids_host = torch.from_numpy(synthetic_ids(B, SEQ, 32000)).pin_memory()
+    ids_host = torch.from_numpy(synthetic_ids(B, seq, vocab)).pin_memory()
     ids_dev = ids_host.cuda()
 
     def barrier():
@@ -407,10 +396,9 @@ def main():
     for _ in range(args.warmup):
         ex.step(ids_dev, want_loss=False, plan_ahead=True)
     barrier()
-    # ---- device-timed region (inputs resident in HBM)
+    # ---- device-timed region (inputs resident in HBM); no per-kernel events inside it
     clocks = ClockSampler(local)
     clocks.start()
-    instrument.start_gemm_timing()
     launches0 = instrument.launches
     main_stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -425,7 +413,6 @@ def main():
     e1.record(main_stream)
     barrier()
     launches = instrument.launches - launches0
-    gemm_flops, gemm_ms, gemm_n = instrument.stop_gemm_timing()
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
     t = torch.tensor([ms], device="cuda")
@@ -434,31 +421,34 @@ def main():
     ms = float(t.item())
     ms_per_step = ms / max(args.steps, 1)
     value = B * args.steps / (ms / 1e3)
-    # ---- end-to-end through the public API: ids from pinned host memory, loss read back
+    # ---- end-to-end through the public API, host wall clock: ids from pinned host memory every
+    # step (H2D inside the step), the loss read back every step (D2H)
     barrier()
-    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    f0.record()
+    w0 = time.perf_counter()
     losses = []
     for _ in range(args.steps):
         st = ex.step(ids_host, want_loss=True, plan_ahead=True)
         losses.append(st.loss)
-    f1.record()
-    barrier()
-    ems = f0.elapsed_time(f1)
-    # one extra step with the sections serialised on one stream: per-launch GEMM throughput without
-    # the other section's kernels time-sharing the GPU (not part of the timed region)
-    instrument.start_gemm_timing()
-    with ex.serialized():
-        ex.step(ids_dev, want_loss=False)
     torch.cuda.synchronize()
-    s_flops, s_ms, _ = instrument.stop_gemm_timing()
-    serial_tflops = s_flops / (s_ms / 1e3) / 1e12 if s_ms > 0 else None
+    w1 = time.perf_counter()
+    barrier()
+    # ---- per-kernel timing: one extra step with the sections serialised on one stream (untimed)
+    instrument.start_timing()
+    with ex.serialized():
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        ex.step(ids_dev, want_loss=False)
+        s1.record()
+    torch.cuda.synchronize()
+    rec = instrument.stop_timing()
+    serial_ms = s0.elapsed_time(s1)
+    g_flops, g_ms, g_n = rec.get("gemm", (0.0, 0.0, 0))
     if dist is not None:  # loss lives on student ranks; report the first student rank's
         lt = torch.tensor([losses[-1] if losses and losses[-1] is not None else float("nan")], device="cuda")
         src = 0 if ex.colocated else ex.dp_t
         dist.broadcast(lt, src)
         losses = [float(lt.item())]
-    t = torch.tensor([ems], device="cuda")
+    t = torch.tensor([(w1 - w0) * 1e3], device="cuda")
     if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_value = B * args.steps / (float(t.item()) / 1e3)
@@ -480,19 +470,13 @@ def main():
     n_sched = [ex.batch // ex.dp_s] * ex.dp_s + ([ex.batch // ex.dp_t] * ex.dp_t if ex.dp_t else [])
     grad_bytes = ex.student.p.grad.numel() * 4 if ex.student is not None else 0
     peaks, peak_kind = load_peaks()
-    gemm_tflops = (gemm_flops / (gemm_ms / 1e3) / 1e12) if gemm_ms > 0 else None
     peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
-    traffic = None
-    prof = ROOT / "profiles" / "gemm_traffic.json"
-    if prof.exists():
-        traffic = json.loads(prof.read_text()).get("traffic_bytes_per_launch")
+    gemm_tflops = (g_flops / (g_ms / 1e3) / 1e12) if g_ms > 0 else None
     cpu = None
     if rank == 0 and args.gpus == 1 and not args.no_cpu_baseline:
         try:
-            sec, threads = cpu_kd_step_sample()
-            cpu = {"value": 1.0 / sec, "unit": UNIT, "cores": threads, "kind": "port",
-                   "sample": "1 sample of 2048 tokens: oracle/torch_ref.py fp32 KD step on the host CPU "
-                             "(teacher fwd + colocated head, student fwd/bwd, KL, AdamW)"}
+            sec, threads, desc = cpu_kd_step_sample(args.workload)
+            cpu = {"value": 1.0 / sec, "unit": UNIT, "cores": threads, "kind": "port", "sample": desc}
             try:
                 cpu["scheduler"] = cpu_schedule_baseline(ex.planner)
             except Exception as exc:  # noqa: BLE001
@@ -502,9 +486,9 @@ def main():
     xcheck = None
     if ex.colocated or ex.student is not None:
         try:
-            mk, cidle, span, midle = ex.crosscheck()
+            mk, cidle, span_x, midle = ex.crosscheck()
             xcheck = {"model_makespan_ms": mk * 1e3, "model_critical_idle_ms": cidle * 1e3,
-                      "measured_critical_span_ms": span * 1e3, "measured_critical_idle_ms": midle * 1e3}
+                      "measured_critical_span_ms": span_x * 1e3, "measured_critical_idle_ms": midle * 1e3}
         except Exception as exc:  # noqa: BLE001
             xcheck = {"error": repr(exc)}
     if args.trace and rank == 0:
@@ -519,17 +503,21 @@ def main():
             sched_roof = {"error": repr(exc)}
     if rank == 0:
         dp_s, dp_t = ex.dp_s, ex.dp_t
+        transport = ("mq.PeerTransport: copy-engine puts over NVLink + stream memory-op signals"
+                     if handoff_mode() == "nvlink" else "mq.DistTransport over NCCL point-to-point")
+        traffic = gemm_traffic(args.workload)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {
-                "workload": KD_WORKLOAD,
-                "global_batch": B, "seq_len": SEQ, "micro_batch": args.mbs, "teacher_micro_batch": ex.mbs_t,
+                "workload": workload,
+                "global_batch": B, "seq_len": seq, "micro_batch": mbs, "teacher_micro_batch": ex.mbs_t,
                 "parallelism": (f"colocated teacher+student per GPU, student dp{dp_s} (grad all-reduce)"
                                 if ex.colocated
-                                else f"disjoint groups: teacher dp{dp_t} -> student dp{dp_s} (fanout 1, NCCL handoff)"),
-                "l2": "inputs larger than L2 (teacher weights 2.2 GB, logits 1 GB per micro-batch)",
+                                else f"disjoint groups: teacher dp{dp_t} -> student dp{dp_s} (fanout 1, "
+                                     f"{handoff_mode()} handoff)"),
+                "l2": "inputs larger than L2 (teacher weights >= 2.2 GB, logits >= 1 GB per micro-batch)",
             },
             "section_stall_pct": 100.0 * float(stall[0].item()),
             "section_stall": {"max_pct": 100.0 * float(stall[0].item()),
@@ -545,23 +533,25 @@ def main():
                                 "bus_GBps": 2 * (dp_s - 1) / dp_s * grad_bytes / (ar_ms / 1e3) / 1e9 if ar_ms else None}
                                if dp_s > 1 else None),
             "handoff": (None if ex.colocated else
-                        {"bytes_per_step": int(B // max(dp_s, 1) * SEQ * ex.tshape.d * 2),
-                         "p2p_GBps_measured": p2p,
-                         "transport": ("mq.PeerTransport: copy-engine puts over NVLink + stream memory-op signals"
-                                       if os.environ.get("MAESTRO_HANDOFF", "nvlink") == "nvlink"
-                                       else "mq.DistTransport over NCCL point-to-point")}),
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(B * SEQ * 4),
-                    "d2h_bytes_per_step": 4 + 8 * 64},
+                        {"bytes_per_step": int(B // max(dp_s, 1) * seq * ex.tshape.d * 2),
+                         "p2p_GBps_measured": p2p, "transport": transport}),
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(B * seq * 4),
+                    "d2h_bytes_per_step": ex.readback_bytes_per_step(),
+                    "timing": "host wall clock (perf_counter) around the steps, synchronised at both ends"},
             "gpu_launches": launches // max(args.steps, 1),
             "roofline": {"bound": "tensor", "kernel": "maestro tcgen05 GEMM (csrc/gemm.cu)",
                          "achieved": gemm_tflops, "peak": peak, "unit": "TFLOP/s",
-                         "frac": (gemm_tflops / peak) if gemm_tflops else None, "traffic": traffic,
+                         "frac": (gemm_tflops / peak) if gemm_tflops else None,
+                         "traffic": traffic.get("traffic_bytes_per_launch") if traffic else None,
+                         "traffic_source": traffic.get("source") if traffic else None,
                          "peak_kind": f"{peak_kind} bf16_tflops_sustained",
-                         "launches_timed": gemm_n, "share_of_step": gemm_ms / ms if ms > 0 else None,
-                         "achieved_serialized": serial_tflops,
-                         "note": "achieved = per-launch CUDA-event durations in the timed step, where the "
-                                 "co-resident teacher and student streams time-share the GPU; "
-                                 "achieved_serialized = the same with the sections on one stream"},
+                         "launches_timed": g_n, "gemm_ms": g_ms, "serialized_step_ms": serial_ms,
+                         "share_of_step": g_ms / serial_ms if serial_ms > 0 else None,
+                         "note": "achieved = sum of 2MNK over every GEMM launch / sum of their CUDA-event "
+                                 "durations, from one extra step with the sections serialised on one stream, "
+                                 "outside the timed region (durations do not overlap: share_of_step <= 1)"},
+            "kernels": kernel_fractions(rec, serial_ms, peaks, ex.attention_flops_per_step(),
+                                        ex.kd_loss_bytes_per_step()),
             "model_tflops": ex.model_flops_per_step() * args.steps / (ms / 1e3) / 1e12,
             "simulator_crosscheck": xcheck,
             "clocks": clk,
@@ -572,6 +562,187 @@ def main():
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------------------------- VLM leg
+def run_vlm(args):
+    """configs[0] (tiny VLM: ViT-tiny encoder -> 2-layer GPT, 50/50 text/image).  N=1: sections
+    co-resident on one GPU; N>1: --layout colocated (both sections DP on every GPU) or disjoint
+    (ViT / LLM groups, recipes.VLM_LAYOUTS, activation and gradient handoff through mq)."""
+    import torch
+
+    from paper_2605_10501_b200 import instrument
+    from paper_2605_10501_b200.executor import handoff_mode
+    from paper_2605_10501_b200.vlm import VLMExecutor, VLMGroupExecutor, vlm_host_batch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
+    mbs = args.mbs or 32
+    bpr = args.batch_per_rank or 64
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.layout == "colocated":
+            ex = VLMExecutor(batch=bpr, mbs_llm=mbs, mbs_vit=args.vit_mbs, dp_group=dist.group.WORLD)
+            layout = f"colocated vit+llm per GPU, both sections dp{world} (grad all-reduce)"
+        else:
+            ex = VLMGroupExecutor(world, batch_per_llm_rank=bpr, mbs_llm=mbs, mbs_vit=args.vit_mbs)
+            layout = f"disjoint: vit dp{ex.dp_vit} (fanout {ex.f}) -> llm dp{ex.dp_llm}, {handoff_mode()} handoff (mq)"
+    else:
+        ex = VLMExecutor(batch=bpr, mbs_llm=mbs, mbs_vit=args.vit_mbs)
+        layout = "colocated vit+llm"
+    B = ex.batch
+    hb = vlm_host_batch(B, seed=rank if (world > 1 and args.layout == "colocated") else 0)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # the VLM step is ~10 ms, so the sampler (200 ms period, ~100 ms start-up) already runs through
+    # the warm-up steps to have samples under load
+    clocks = ClockSampler(local)
+    clocks.start()
+    # the co-resident executor plans the next step's batch beside the current step (the batch of
+    # step i+1 is known at step i, as with a prefetching loader)
+    nxt = {"next_hb": hb} if isinstance(ex, VLMExecutor) else {}
+    for _ in range(args.warmup):
+        ex.step(hb, want_loss=False, **nxt)
+    barrier()
+    launches0 = instrument.launches
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    sts = []
+    for _ in range(args.steps):
+        sts.append(ex.step(hb, want_loss=False, **nxt))
+    e1.record()
+    barrier()
+    launches = instrument.launches - launches0
+    stalls = [x.stall_frac for x in sts]  # read after the timed region (lazy stats synchronise)
+    clk = clocks.stop()
+    t = torch.tensor([e0.elapsed_time(e1), max(stalls) if getattr(ex, "role", "llm") == "llm" else 0.0],
+                     device="cuda")
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t[0].item())
+    B_all = B * world if (world > 1 and args.layout == "colocated") else B
+    value = B_all * args.steps / (ms / 1e3)
+    # ---- end-to-end, host wall clock: every step copies its inputs from pinned host memory and
+    # the loss is read back every step
+    barrier()
+    w0 = time.perf_counter()
+    losses = []
+    for _ in range(args.steps):
+        losses.append(ex.step(hb, want_loss=True, **nxt).loss)
+    torch.cuda.synchronize()
+    w1 = time.perf_counter()
+    barrier()
+    te = torch.tensor([(w1 - w0) * 1e3], device="cuda")
+    if dist is not None:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = B_all * args.steps / (float(te.item()) / 1e3)
+    # ---- per-kernel timing in one extra untimed step
+    instrument.start_timing()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record()
+    ex.step(hb, want_loss=False, **nxt)
+    s1.record()
+    torch.cuda.synchronize()
+    rec = instrument.stop_timing()
+    serial_ms = s0.elapsed_time(s1)
+    g_flops, g_ms, g_n = rec.get("gemm", (0.0, 0.0, 0))
+    peaks, peak_kind = load_peaks()
+    peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+    gt = g_flops / (g_ms / 1e3) / 1e12 if g_ms > 0 else None
+    cpu = None
+    if rank == 0 and args.gpus == 1 and not args.no_cpu_baseline:
+        try:
+            sec, threads = cpu_vlm_step_sample()
+            cpu = {"value": 1.0 / sec, "unit": UNIT, "cores": threads, "kind": "port",
+                   "sample": "8 samples: oracle/torch_ref.py fp32 VLM step on the host CPU"}
+            try:
+                cpu["scheduler"] = cpu_schedule_baseline(ex.planner)
+            except Exception as exc:  # noqa: BLE001
+                cpu["scheduler"] = {"error": repr(exc)}
+        except Exception as exc:  # noqa: BLE001
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {exc}"}
+    if rank == 0:
+        from paper_2605_10501_b200.vlm import pinned_inputs
+
+        pin = pinned_inputs(hb)
+        h2d = sum(int(pin[k].numel() * pin[k].element_size()) for k in ("ids", "labels", "lens", "pixels"))
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": "vlm_cfg1: ViT-tiny (d192 L12) -> 2-layer GPT (d768), 50/50 text/image, "
+                                   "wavefront schedule on device", "global_batch": B_all, "seq_len": "64..497",
+                       "parallelism": layout, "micro_batch_llm": mbs, "micro_batch_vit": args.vit_mbs,
+                       "l2": "inputs copied from pinned host memory every step (value and e2e alike)"},
+            "section_stall_pct": 100.0 * float(t[1].item()),
+            "gpu_launches": launches // max(args.steps, 1),
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": (4 * (ex._h_orders.numel() + ex._h_off.numel()) + 8 + 4
+                                           if hasattr(ex, "_h_orders") else None),
+                    "timing": "host wall clock (perf_counter) around the steps, synchronised at both ends"},
+            "roofline": {"bound": "tensor", "kernel": "maestro tcgen05 GEMM (csrc/gemm.cu)", "achieved": gt,
+                         "peak": peak, "unit": "TFLOP/s", "frac": gt / peak if gt else None, "traffic": None,
+                         "peak_kind": f"{peak_kind} bf16_tflops_sustained", "launches_timed": g_n,
+                         "share_of_step": g_ms / serial_ms if serial_ms > 0 else None,
+                         "note": "one extra untimed step; the tiny cfg 1 GEMMs (d 192/768) are launch-bound"},
+            "model_tflops": ex.model_flops_per_step(hb) * (B_all // B) * args.steps / (ms / 1e3) / 1e12,
+            "loss": losses[-1] if losses else None,
+            "clocks": clk,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--batch-per-rank", type=int, default=None)
+    ap.add_argument("--mbs", type=int, default=None,
+                    help="student (KD) or LLM (VLM, default 32) micro-batch size")
+    ap.add_argument("--vit-mbs", type=int, default=32,
+                    help="VLM: ViT micro-batch (images); measured 8 -> 32 (with the LLM's): 1724 -> 4471 samples/s")
+    ap.add_argument("--teacher-mbs", type=int, default=None,
+                    help="teacher (forward-only) micro-batch size, a multiple of --mbs")
+    ap.add_argument("--layout", default="colocated", choices=["colocated", "disjoint"])
+    ap.add_argument("--trace", default=None, help="write the measured chrome trace of the last step here")
+    ap.add_argument("--workload", default="kd", choices=["kd", "kd8b", "vlm", "section"],
+                    help="kd = BASELINE configs[1] (default); kd8b = configs[4]; vlm = configs[0]; "
+                         "section = generic section-graph executor (--graph)")
+    ap.add_argument("--graph", default="vlm7b", choices=["vlm7b", "omni"],
+                    help="--workload section: cfg 3 (vlm7b) or cfg 4 (omni) shapes")
+    ap.add_argument("--layers", type=int, default=None, help="--workload section: layers per stack (reduced depth)")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    if args.workload == "vlm":
+        run_vlm(args)
+    elif args.workload == "section":
+        from paper_2605_10501_b200.graph_bench import run_section
+
+        run_section(args, METRIC, UNIT, ClockSampler, load_peaks)
+    else:
+        run_kd(args)
 
 
 if __name__ == "__main__":

@@ -132,11 +132,32 @@ int maestro_varlen_pack(const int32_t* d_order, int32_t n, const int32_t* d_len,
 int maestro_pack_tokens(const int32_t* d_ids, int32_t ld, const int32_t* d_order, const int32_t* d_len,
                         const int32_t* d_tok_off, int32_t n, int32_t* d_out, void* stream);
 
+/* K5b -- handoff (scatter) indices between a producer section's row buffer and the consumer
+ * (critical) rank's packed stream (north_star item 2).  d_up_order[nu]: the
+ * producer's order (its row buffer holds d_rows[i] rows per sample, in that order);
+ * d_crit_order[n] / d_tok_off[n]: the consumer order and its varlen_pack offsets; mbs its
+ * micro-batch size; d_rows[B] / d_dst_off[B] per sample id: rows exchanged (0 = none) and their
+ * offset inside the sample's sequence.  Out: d_pos[n+1] = exclusive scan of d_rows over the
+ * consumer order; for position k (sample i) and r < d_rows[i], at index d_pos[k] + r:
+ * d_src_rows = producer-buffer row, d_dst_rows = row inside consumer micro-batch k / mbs
+ * (d_tok_off[k] - d_tok_off[(k/mbs)*mbs] + d_dst_off[i] + r).  d_scratch: B int32.  A sample with
+ * rows in the consumer order but absent from the producer order sets InconsistentSchedule. */
+int maestro_handoff_index(const int32_t* d_up_order, int32_t nu, const int32_t* d_crit_order, int32_t n,
+                          const int32_t* d_tok_off, int32_t mbs, const int32_t* d_rows, const int32_t* d_dst_off,
+                          int32_t B, int32_t* d_scratch, int32_t* d_pos, int32_t* d_src_rows, int32_t* d_dst_rows,
+                          int64_t* d_err, void* stream);
+
 /* K6 -- row scatter of encoder outputs into the packed token stream and its backward.
  * fwd: dst[dst_row[k], :] = src[src_row[k], :]  (bf16, d multiple of 8)
  * bwd: dsrc[r, :] = sum over k in seg[r]..seg[r+1] of ddst[seg_dst[k], :] (fp32 accumulate). */
 int maestro_scatter_rows_fwd(const void* d_src, void* d_dst, const int32_t* d_src_row,
                              const int32_t* d_dst_row, int32_t n_rows, int32_t d, void* stream);
+/* K6 over one micro-batch of a K5b handoff index: the pairs [d_pos[k0], d_pos[k1]) (read on
+ * device); max_rows >= d_pos[k1] - d_pos[k0] sizes the grid; accumulate != 0: dst += src (bf16,
+ * fp32 sum rounded once). */
+int maestro_scatter_rows_range(const void* d_src, void* d_dst, const int32_t* d_src_row, const int32_t* d_dst_row,
+                               const int32_t* d_pos, int32_t k0, int32_t k1, int32_t max_rows, int32_t d,
+                               int32_t accumulate, void* stream);
 int maestro_gather_rows_bwd(const void* d_ddst, void* d_dsrc, const int32_t* d_seg,
                             const int32_t* d_seg_dst, int32_t n_src_rows, int32_t d, void* stream);
 
@@ -151,12 +172,13 @@ int maestro_gather_rows_bwd(const void* d_ddst, void* d_dsrc, const int32_t* d_s
 int maestro_gemm_bf16(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K, int32_t lda,
                       int32_t ldb, int32_t ldc, int32_t a_mn, int32_t b_mn, int32_t epi, void* stream);
 
-/* K7 + fused RoPE epilogue: C = A B^T (bf16, K-major A/B); every 64-column head in columns
- * [0, rope_cols) is rotated (rotate-half) at position pos[row].  cos_sin is position-tiled:
- * [ceil(P/32)][32 freqs][32 positions] of (cos, sin) fp32 pairs (transformer.rope_table). */
+/* K7 + fused RoPE epilogue: C = A B^T (bf16, K-major A/B); every head_dim-column head (64 or 128)
+ * in columns [0, rope_cols) is rotated (rotate-half) at position pos[row].  cos_sin is
+ * position-tiled: [ceil(P/32)][head_dim/2 freqs][32 positions] of (cos, sin) fp32 pairs
+ * (transformer.rope_table). */
 int maestro_gemm_bf16_rope(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K, int32_t lda,
                            int32_t ldb, int32_t ldc, const int32_t* pos, const void* cos_sin, int32_t rope_cols,
-                           void* stream);
+                           int32_t head_dim, void* stream);
 
 /* K7 + fused residual epilogue: C = R + A B^T (bf16; the sum is formed in fp32 and rounded
  * once).  Used by the attention-output and down projections to write the residual stream. */
@@ -168,8 +190,9 @@ int maestro_gemm_bf16_residual(const void* A, const void* B, void* C, int32_t M,
 int maestro_gemm_bf16_swiglu(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K, int32_t lda,
                              int32_t ldb, int32_t ldc, void* S, int32_t lds, void* stream);
 
-/* K8 -- varlen GQA attention, head_dim 64: q [T,H,64], k/v [T,Hk,64] (pitched), cu [nseq+1];
- * out [T,H,64] bf16, lse [H,T] fp32 (natural LSE of the scaled scores). */
+/* K8 -- varlen GQA attention, head_dim dh: q [T,H,dh], k/v [T,Hk,dh] (pitched), cu [nseq+1];
+ * out [T,H,dh] bf16, lse [H,T] fp32 (natural LSE of the scaled scores).  Forward: dh 64 or 128;
+ * backward: dh 64 or 128. */
 int64_t maestro_attn_workspace(int32_t T, int32_t nseq);
 /* Per-micro-batch work plan (query-tile and KV-tile lists, heavy-first) built once from cu and
  * passed to every layer's attn_fwd / attn_bwd; plan == NULL builds it per call in the workspace. */
@@ -179,7 +202,7 @@ int maestro_attn_fwd(const void* q, const void* k, const void* v, const int32_t*
                      int32_t H, int32_t Hk, int32_t head_dim, int32_t ldq, int32_t ldk, int32_t ldv, void* out,
                      int32_t ldo, float* lse, float softmax_scale, int32_t causal, const void* plan, void* workspace,
                      void* stream);
-int64_t maestro_attn_bwd_workspace(int32_t T, int32_t nseq, int32_t H);
+int64_t maestro_attn_bwd_workspace(int32_t T, int32_t nseq, int32_t H, int32_t head_dim);
 int maestro_attn_bwd(const void* dout, int32_t lddo, const void* q, const void* k, const void* v, const void* o,
                      int32_t ldo, const float* lse, const int32_t* cu, int32_t nseq, int32_t T, int32_t H,
                      int32_t Hk, int32_t head_dim, int32_t ldq, int32_t ldk, int32_t ldv, void* dq, int32_t lddq,

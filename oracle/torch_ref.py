@@ -14,6 +14,8 @@ from __future__ import annotations
 
 import math
 
+import numpy as np
+
 import torch
 import torch.nn.functional as F
 
@@ -174,3 +176,110 @@ def vlm_step_reference(llm_shape, vit_shape, llm_flat, vit_flat, hb, merge_idx, 
     loss = loss_sum / max(nlab, 1)
     loss.backward()
     return loss.item(), lf.grad, vf.grad
+
+
+# ------------------------------------------------------------------------------------------------
+# Generic section graph (graph_exec.SectionGraphExecutor): encoders -> backbone -> decoders
+def unpad_heads(shape, P):
+    """A zero-padded-head shape (head_dim_true < head_dim, real dims laid out [h/2 | pad | h/2 |
+    pad]) -> the true model's (shape, params): the standard rotate-half RoPE over h dims with
+    base^(-2i/h) and scale 1/sqrt(h) -- the model the padded layout must equal."""
+    import dataclasses
+
+    ht, dh = shape.hd_true, shape.head_dim
+    if ht == dh:
+        return shape, P
+    keep = torch.cat([torch.arange(ht // 2), dh // 2 + torch.arange(ht // 2)])
+    nq = shape.heads + 2 * shape.kv_heads
+    rows = (torch.arange(nq)[:, None] * dh + keep[None, :]).reshape(-1)
+    cols = (torch.arange(shape.heads)[:, None] * dh + keep[None, :]).reshape(-1)
+    Q = dict(P)
+    for i in range(shape.layers):
+        Q[f"l{i}.wqkv"] = P[f"l{i}.wqkv"][rows.to(P[f"l{i}.wqkv"].device)]
+        Q[f"l{i}.wo"] = P[f"l{i}.wo"][:, cols.to(P[f"l{i}.wo"].device)]
+    return dataclasses.replace(shape, head_dim=ht, head_dim_true=0), Q
+
+
+def views(shape, flat, extra=()):
+    """Arena views (same offsets as FlatParams) of shape.param_shapes() + extra."""
+    out, off = {}, 0
+    for name, shp in list(shape.param_shapes()) + list(extra):
+        n = math.prod(shp)
+        out[name] = flat[off: off + n].view(*shp)
+        off += (n + 63) // 64 * 64
+    return out
+
+
+def graph_step_reference(crit, ups, downs, gb):
+    """fp32 autograd restatement of one generic-executor step over the WHOLE batch (sample order
+    does not matter: training equivalence).
+
+    crit  = (shape, flat)                      backbone, next-token CE over gb.labels
+    ups   = {name: (shape, flat, in_dim, merge)}  encoder: in_w -> stack -> 4:1 merge -> proj_w
+    downs = {name: (shape, flat, in_d)}        decoder: in_w -> causal stack -> head -> CE
+    Returns (loss, {name: flat grad}).  Loss = mean CE of the backbone + mean CE of each decoder."""
+    dev = crit[1].device
+    leaves = {}
+    cs, cflat = crit
+    lf = cflat.detach().clone().requires_grad_(True)
+    leaves["crit"] = lf
+    Pc = param_views(cs, lf)
+    enc_rows = {}
+    for name, (sh, flat, in_dim, merge) in ups.items():
+        vf = flat.detach().clone().requires_grad_(True)
+        leaves[name] = vf
+        P = views(sh, vf, [("in_w", (sh.d, in_dim)), ("proj_w", (cs.d, merge * sh.d))])
+        ui = gb.up[name]
+        act = [i for i in range(gb.B) if ui.in_len[i] > 0]
+        rows = {}
+        if act:
+            feats = torch.from_numpy(ui.feats).to(dev).to(torch.bfloat16).float()
+            fo = np.concatenate([[0], np.cumsum(ui.in_len)]).astype(np.int64)
+            sh_t, Pt = unpad_heads(sh, P)
+            for i in act:
+                x = feats[fo[i]: fo[i + 1]] @ P["in_w"].t()
+                cu = torch.tensor([0, int(ui.in_len[i])], dtype=torch.int32, device=dev)
+                y = forward(sh_t, Pt, torch.zeros(int(ui.in_len[i]), dtype=torch.int32, device=dev), cu, x0=x)
+                rows[i] = y.reshape(-1, merge * sh.d) @ P["proj_w"].t()
+        enc_rows[name] = rows
+    dec = {}
+    for name, (sh, flat, in_d) in downs.items():
+        vf = flat.detach().clone().requires_grad_(True)
+        leaves[name] = vf
+        dec[name] = (sh, views(sh, vf, [("in_w", (sh.d, in_d))]))
+    cs_t, Pc_t = unpad_heads(cs, Pc)
+    n_lab = max(int((gb.labels >= 0).sum()), 1)
+    loss = torch.zeros((), device=dev)
+    dec_sum = {n: torch.zeros((), device=dev) for n in downs}
+    for i in range(gb.B):
+        L = int(gb.lens[i])
+        ids = torch.from_numpy(gb.ids[i, :L]).to(dev)
+        lab = torch.from_numpy(gb.labels[i, :L]).to(dev).long()
+        x = Pc["embed"][ids.clamp_min(0).long()] * (ids >= 0).float()[:, None]
+        for name in ups:
+            if i in enc_rows[name]:
+                o = int(gb.up[name].dst_off[i])
+                r = enc_rows[name][i]
+                x = torch.cat([x[:o], r, x[o + r.shape[0]:]], 0)
+        cu = torch.tensor([0, L], dtype=torch.int32, device=dev)
+        y = forward(cs_t, Pc_t, ids, cu, x0=x)
+        logits = y @ head_weight(cs, Pc).t()
+        valid = lab >= 0
+        if valid.any():
+            loss = loss + F.cross_entropy(logits[valid], lab[valid], reduction="sum") / n_lab
+        for name, (sh, P) in dec.items():
+            di = gb.down[name]
+            nr = int(di.rows[i])
+            if nr == 0:
+                continue
+            so = int(di.src_off[i])
+            t_off = int(np.sum(di.rows[:i]))
+            tg = torch.from_numpy(di.targets[t_off: t_off + nr]).to(dev).long()
+            xin = y[so: so + nr] @ P["in_w"].t()
+            cu_d = torch.tensor([0, nr], dtype=torch.int32, device=dev)
+            yd = forward(sh, P, torch.zeros(nr, dtype=torch.int32, device=dev), cu_d, x0=xin)
+            dec_sum[name] = dec_sum[name] + F.cross_entropy(yd @ head_weight(sh, P).t(), tg, reduction="sum")
+    for name in downs:
+        loss = loss + dec_sum[name] / max(int(gb.down[name].rows.sum()), 1)
+    loss.backward()
+    return loss.item(), {k: v.grad for k, v in leaves.items()}

@@ -1,4 +1,4 @@
-// K8: varlen (cu_seqlens) attention with GQA on tcgen05/TMEM, head_dim 64, causal or not.
+// K8: varlen (cu_seqlens) attention with GQA on tcgen05/TMEM, head_dim 64 or 128, causal or not.
 //
 // Both directions are persistent: one CTA per SM loops over heavy-first work items dealt in
 // snake order; items come from a per-micro-batch plan (query-tile / KV-tile lists) built once by
@@ -33,10 +33,7 @@ namespace {
 
 using namespace sm100;
 
-constexpr int DH = 64;
-constexpr int BQ = 128, BKV = 128, KV_STAGES = 3;
-constexpr int TILE_BYTES = 128 * DH * 2;  // 16 KB (128 rows x 128 B)
-constexpr int P_BYTES = BQ * BKV * 2;     // 32 KB (two 64-col chunks)
+constexpr int BQ = 128, BKV = 128;  // forward query tile, key tile (rows)
 constexpr int FWD_THREADS = 320;  // w0 TMA, w1 MMA, w2-9 softmax (2 per lane quadrant)
 constexpr float LOG2E_F = 1.4426950408889634f;
 constexpr float LN2_F = 0.6931471805599453f;
@@ -96,18 +93,28 @@ __device__ __forceinline__ uint32_t p_offset(int r, int c) {
 
 // Persistent forward: one CTA per SM loops over work items (query tile, head) in heavy-first
 // order.  All pipeline counters run across items: K/V stream through the ring, S alternates
-// between two TMEM buffers by global tile index, Q and O are double-buffered by item index,
-// so the next item's Q load, first S MMAs and softmax overlap the current item's epilogue.
-// TMEM: S0 [0,128) S1 [128,256), O (item parity 0) [256,384), O (parity 1) [384,512); each O is
-// two 64-column accumulators O_a (keys 0-63 of every tile) and O_b (keys 64-127).
-struct FwdSmemP {
-  static constexpr int Q = 0;                                  // 2 x 16 KB (by item parity)
-  static constexpr int K = Q + 2 * TILE_BYTES;
-  static constexpr int V = K + KV_STAGES * TILE_BYTES;
-  static constexpr int XMAX = V + KV_STAGES * TILE_BYTES;      // [2 items][2 halves][128] row maxima
-  static constexpr int XSUM = XMAX + 2 * 2 * 128 * 4;          // [2 items][2 halves][128] row sums
+// between two TMEM buffers by global tile index, Q is double-buffered by item index, so the
+// next item's Q load, first S MMAs and softmax overlap the current item's epilogue.
+// TMEM: S0 [0,128) S1 [128,256), then the O accumulators: two 64-column halves O_a (keys 0-63
+// of every tile) and O_b (keys 64-127) per item.  head_dim 64: O double-buffered by item
+// parity ([256,384), [384,512)); head_dim 128: one O = O_a [256,384) + O_b [384,512), so the
+// first PV of an item waits for the previous item's epilogue to have read O.
+// A [128 rows][DH] bf16 tile is DH/64 SWIZZLE_128B chunks of 128 rows x 128 B (16 KB each).
+template <int DH>
+struct FwdCfg {
+  static constexpr int NCH = DH / 64;                 // 64-column chunks per tile row
+  static constexpr int TILE = 128 * DH * 2;           // bytes of a 128-row tile
+  static constexpr int KVS = DH == 64 ? 3 : 2;        // K/V ring depth
+  static constexpr int NOB = DH == 64 ? 2 : 1;        // O accumulators (by item)
+  static constexpr int Q = 0;                         // 2 x TILE (by item parity)
+  static constexpr int K = Q + 2 * TILE;
+  static constexpr int V = K + KVS * TILE;
+  static constexpr int XMAX = V + KVS * TILE;         // [2 items][2 halves][128] row maxima
+  static constexpr int XSUM = XMAX + 2 * 2 * 128 * 4; // [2 items][2 halves][128] row sums
   static constexpr int BAR = XSUM + 2 * 2 * 128 * 4;
   static constexpr int TOTAL = BAR + 256;
+  static_assert(TOTAL + 1024 <= 227 * 1024, "forward smem");
+  static_assert(256 + NOB * 2 * DH <= 512, "forward TMEM");
 };
 
 struct FwdItem {
@@ -135,27 +142,36 @@ __device__ __forceinline__ int snake_item(int r) {
   return r * (int)gridDim.x + ((r & 1) ? (int)gridDim.x - 1 - (int)blockIdx.x : (int)blockIdx.x);
 }
 
-template <bool CAUSAL>
+// TMA load of one 128-row tile: DH/64 boxes of 64 columns, one per SWIZZLE_128B chunk.
+template <int DH>
+__device__ __forceinline__ void load_tile(unsigned char* dst, const CUtensorMap* map, uint64_t* bar, int col, int row) {
+#pragma unroll
+  for (int c = 0; c < DH / 64; ++c) tma_load_2d(dst + c * 16384, map, bar, col + 64 * c, row);
+}
+
+template <int DH, bool CAUSAL>
 __global__ void __launch_bounds__(FWD_THREADS, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                     const __grid_constant__ CUtensorMap map_v, const int32_t* __restrict__ cu,
                     const int2* __restrict__ tiles, const int* __restrict__ n_tiles, __nv_bfloat16* __restrict__ out,
                     int ldo, float* __restrict__ lse, int T, int H, int Hk, float scale2) {
+  using C = FwdCfg<DH>;
+  constexpr int KVS = C::KVS, NOB = C::NOB, TB = C::TILE;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* sm = align_smem_1024(smem_raw);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + FwdSmemP::BAR);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::BAR);
   uint64_t* q_full = bar;                  // [2]
   uint64_t* q_empty = bar + 2;             // [2]
-  uint64_t* k_full = bar + 4;              // [KV_STAGES]
-  uint64_t* k_empty = k_full + KV_STAGES;
-  uint64_t* v_full = k_empty + KV_STAGES;
-  uint64_t* v_empty = v_full + KV_STAGES;
-  uint64_t* s_full = v_empty + KV_STAGES;  // [2]
+  uint64_t* k_full = bar + 4;              // [KVS]
+  uint64_t* k_empty = k_full + KVS;
+  uint64_t* v_full = k_empty + KVS;
+  uint64_t* v_empty = v_full + KVS;
+  uint64_t* s_full = v_empty + KVS;        // [2]
   uint64_t* s_empty = s_full + 2;
   uint64_t* p_full = s_empty + 2;
   uint64_t* p_empty = p_full + 2;
-  uint64_t* o_full = p_empty + 2;          // [2]
-  uint64_t* o_empty = o_full + 2;          // [2]
+  uint64_t* o_full = p_empty + 2;          // [NOB]
+  uint64_t* o_empty = o_full + 2;          // [NOB]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
 
   const int n_items = *n_tiles * H;
@@ -174,7 +190,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       mbar_init(&o_full[b], 1);
       mbar_init(&o_empty[b], 256);
     }
-    for (int s = 0; s < KV_STAGES; ++s) {
+    for (int s = 0; s < KVS; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
       mbar_init(&v_full[s], 1);
@@ -193,23 +209,23 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       int g = 0;  // global KV tile counter (ring position)
       int j = 0;  // local item counter
       FwdItem it_n{};
-        if (snake_item(0) < n_items) it_n = fwd_item<CAUSAL>(snake_item(0), H, Hk, cu, tiles);
-        for (int w = snake_item(0); w < n_items; w = snake_item(j + 1), ++j) {
+      if (snake_item(0) < n_items) it_n = fwd_item<CAUSAL>(snake_item(0), H, Hk, cu, tiles);
+      for (int w = snake_item(0); w < n_items; w = snake_item(j + 1), ++j) {
         const FwdItem it = it_n;
         if (snake_item(j + 1) < n_items) it_n = fwd_item<CAUSAL>(snake_item(j + 1), H, Hk, cu, tiles);  // prefetch
         const int qb = j & 1;
         mbar_wait(&q_empty[qb], ((j >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(&q_full[qb], TILE_BYTES);
-        tma_load_2d(sm + FwdSmemP::Q + qb * TILE_BYTES, &map_q, &q_full[qb], it.h * DH, it.s0 + it.q0);
+        mbar_arrive_expect_tx(&q_full[qb], TB);
+        load_tile<DH>(sm + C::Q + qb * TB, &map_q, &q_full[qb], it.h * DH, it.s0 + it.q0);
         for (int i = 0; i < it.n_kv; ++i, ++g) {
-          const int st = g % KV_STAGES;
-          const uint32_t ph = (g / KV_STAGES) & 1;
+          const int st = g % KVS;
+          const uint32_t ph = (g / KVS) & 1;
           mbar_wait(&k_empty[st], ph ^ 1);
-          mbar_arrive_expect_tx(&k_full[st], TILE_BYTES);
-          tma_load_2d(sm + FwdSmemP::K + st * TILE_BYTES, &map_k, &k_full[st], it.hk * DH, it.s0 + i * BKV);
+          mbar_arrive_expect_tx(&k_full[st], TB);
+          load_tile<DH>(sm + C::K + st * TB, &map_k, &k_full[st], it.hk * DH, it.s0 + i * BKV);
           mbar_wait(&v_empty[st], ph ^ 1);
-          mbar_arrive_expect_tx(&v_full[st], TILE_BYTES);
-          tma_load_2d(sm + FwdSmemP::V + st * TILE_BYTES, &map_v, &v_full[st], it.hk * DH, it.s0 + i * BKV);
+          mbar_arrive_expect_tx(&v_full[st], TB);
+          load_tile<DH>(sm + C::V + st * TB, &map_v, &v_full[st], it.hk * DH, it.s0 + i * BKV);
         }
       }
     }
@@ -217,22 +233,25 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     {
       constexpr uint32_t idesc_s = idesc_bf16_f32(BQ, BKV, false, false);
       constexpr uint32_t idesc_o = idesc_bf16_f32(BQ, DH, false, true);
-      // PV of global tile gp (item-local index ip) into O buffer ob
-      auto issue_pv = [&](int gp, int ip, int ob) {
+      // PV of global tile gp (item-local index ip, item counter jp) into O buffer ob
+      auto issue_pv = [&](int gp, int ip, int jp, int ob) {
         const int pb = gp & 1;
+        if (ip == 0) mbar_wait(&o_empty[ob], ((jp / NOB) & 1) ^ 1);  // epilogue of the item that last used O[ob]
         mbar_wait(&p_full[pb], (gp >> 1) & 1);
-        mbar_wait(&v_full[gp % KV_STAGES], (gp / KV_STAGES) & 1);
+        mbar_wait(&v_full[gp % KVS], (gp / KVS) & 1);
         tc_fence_after();
-        const uint32_t v_base = smem_u32(sm + FwdSmemP::V + (gp % KV_STAGES) * TILE_BYTES);
+        const uint32_t v_base = smem_u32(sm + C::V + (gp % KVS) * TB);
         // keys [0,64) accumulate into O_a, keys [64,128) into O_b: each softmax half keeps its own
         // running max, so the halves never synchronise inside the KV loop.  A = P from TMEM: half
         // h's bf16 pairs sit in the first 32 columns of its 64 score columns of S buffer pb.
+        // B = V as an MN-major operand: DH/64 swizzle atoms 16 KB apart (LBO), 8-key groups 1 KB (SBO).
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < BKV / 16; ++kk)
             umma_bf16_ts(tmem + 256 + ob * 2 * DH + (kk >> 2) * DH, tmem + pb * BKV + (kk >> 2) * 64 + (kk & 3) * 8,
-                         sdesc((v_base >> 4) + kk * 128, 8192, 1024), idesc_o, (ip > 0 || (kk & 3) > 0) ? 1u : 0u);
-          umma_commit(&v_empty[gp % KV_STAGES]);
+                         sdesc((v_base >> 4) + kk * 128, DH == 64 ? 8192 : 16384, 1024), idesc_o,
+                         (ip > 0 || (kk & 3) > 0) ? 1u : 0u);
+          umma_commit(&v_empty[gp % KVS]);
           umma_commit(&p_empty[pb]);
         }
         __syncwarp();
@@ -240,11 +259,11 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       int g = 0, j = 0;
       // the PV of each tile is issued after the NEXT tile's S (also across item boundaries), so
       // the tensor core computes S while the softmax warps work on the previous tile
-      int pend_g = -1, pend_i = 0, pend_o = 0;
+      int pend_g = -1, pend_i = 0, pend_j = 0, pend_o = 0;
       bool pend_last = false;
       auto flush = [&]() {
         if (pend_g < 0) return;
-        issue_pv(pend_g, pend_i, pend_o);
+        issue_pv(pend_g, pend_i, pend_j, pend_o);
         if (pend_last) {
           if (elect_one()) umma_commit(&o_full[pend_o]);
           __syncwarp();
@@ -252,34 +271,34 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
         pend_g = -1;
       };
       FwdItem it_n{};
-        if (snake_item(0) < n_items) it_n = fwd_item<CAUSAL>(snake_item(0), H, Hk, cu, tiles);
-        for (int w = snake_item(0); w < n_items; w = snake_item(j + 1), ++j) {
+      if (snake_item(0) < n_items) it_n = fwd_item<CAUSAL>(snake_item(0), H, Hk, cu, tiles);
+      for (int w = snake_item(0); w < n_items; w = snake_item(j + 1), ++j) {
         const FwdItem it = it_n;
         if (snake_item(j + 1) < n_items) it_n = fwd_item<CAUSAL>(snake_item(j + 1), H, Hk, cu, tiles);  // prefetch
-        const int qb = j & 1, ob = j & 1;
+        const int qb = j & 1, ob = j % NOB;
         mbar_wait(&q_full[qb], (j >> 1) & 1);
-        const uint32_t q_base = smem_u32(sm + FwdSmemP::Q + qb * TILE_BYTES);
+        const uint32_t q_base = smem_u32(sm + C::Q + qb * TB);
         for (int i = 0; i < it.n_kv; ++i, ++g) {
           const int b = g & 1;
-          const int st = g % KV_STAGES;
-          mbar_wait(&k_full[st], (g / KV_STAGES) & 1);
+          const int st = g % KVS;
+          mbar_wait(&k_full[st], (g / KVS) & 1);
           mbar_wait(&s_empty[b], ((g >> 1) & 1) ^ 1);
           tc_fence_after();
-          const uint32_t k_base = smem_u32(sm + FwdSmemP::K + st * TILE_BYTES);
+          const uint32_t k_base = smem_u32(sm + C::K + st * TB);
           if (elect_one()) {
 #pragma unroll
-            for (int kk = 0; kk < DH / 16; ++kk)
-              umma_bf16(tmem + b * BKV, sdesc((q_base >> 4) + kk * 2, 16, 1024),
-                        sdesc((k_base >> 4) + kk * 2, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+            for (int kk = 0; kk < DH / 16; ++kk)  // chunk kk/4 (16 KB apart), 32 B per K step inside it
+              umma_bf16(tmem + b * BKV, sdesc((q_base >> 4) + (kk >> 2) * 1024 + (kk & 3) * 2, 16, 1024),
+                        sdesc((k_base >> 4) + (kk >> 2) * 1024 + (kk & 3) * 2, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
             umma_commit(&k_empty[st]);
             umma_commit(&s_full[b]);
             if (i == it.n_kv - 1) umma_commit(&q_empty[qb]);  // last S of the item: Q buffer free
           }
           __syncwarp();
           flush();
-          if (i == 0) mbar_wait(&o_empty[ob], ((j >> 1) & 1) ^ 1);  // epilogue of item j-2 read O[ob]
           pend_g = g;
           pend_i = i;
+          pend_j = j;
           pend_o = ob;
           pend_last = i == it.n_kv - 1;
         }
@@ -290,33 +309,27 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     // Two warps per TMEM lane quadrant split the 128 key columns of a tile (half 0: [0,64),
     // half 1: [64,128)).  Each half runs its own online softmax (max, sum, lazy rescale) into its
     // own O accumulator; the halves combine once per item in the epilogue (named barrier per
-    // quadrant pair), each normalising and storing 32 of the 64 output columns.
+    // quadrant pair), each normalising and storing DH/2 of the DH output columns.
     const int q = warp & 3;
     const int half = (warp - 2) >> 2;
     const int r = q * 32 + lane;
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     const int pair_bar = 2 + q;
-    float* xmax = reinterpret_cast<float*>(sm + FwdSmemP::XMAX);
-    float* xsum = reinterpret_cast<float*>(sm + FwdSmemP::XSUM);
-    // Epilogue of item jj (O buffer ob, final m / l), deferred until after the next item's first
-    // tile: by then the item's last PV has completed, so O is read without waiting on it.
+    float* xmax = reinterpret_cast<float*>(sm + C::XMAX);
+    float* xsum = reinterpret_cast<float*>(sm + C::XSUM);
+    // Epilogue of item jj (final m / l), deferred until after the next item's first tile: by
+    // then the item's last PV has completed, so O is read without waiting on it.
     auto epilogue = [&](const FwdItem& it, int jj, float m, float l) {
-      const int ob = jj & 1;
+      const int ob = jj % NOB;
       const int qpos = it.q0 + r;
-      // epilogue of item jj: exchange (m, l) with the
-      // partner half, O = (O_a 2^(m_a - M) + O_b 2^(m_b - M)) / l for this half's 32 columns
-      float* xm = xmax + ob * 256;  // by item parity: the partner reads it before the next item's barrier
-      float* xs = xsum + ob * 256;
+      // exchange (m, l) with the partner half, O = (O_a 2^(m_a - M) + O_b 2^(m_b - M)) / l for
+      // this half's DH/2 columns
+      float* xm = xmax + (jj & 1) * 256;  // by item parity: the partner reads it before the next item's barrier
+      float* xs = xsum + (jj & 1) * 256;
       xm[half * 128 + r] = m;
       xs[half * 128 + r] = l;
-      mbar_wait(&o_full[ob], (jj >> 1) & 1);
+      mbar_wait(&o_full[ob], (jj / NOB) & 1);
       tc_fence_after();
-      uint32_t ra[32], rb[32];
-      tmem_ld_32x32b_x32(tmem + lane_base + 256 + ob * 2 * DH + half * 32, ra);
-      tmem_ld_32x32b_x32(tmem + lane_base + 256 + ob * 2 * DH + DH + half * 32, rb);
-      tmem_ld_wait();
-      tc_fence_before();
-      mbar_arrive(&o_empty[ob]);
       named_bar(pair_bar, 64);
       const float m_o = xm[(half ^ 1) * 128 + r], l_o = xs[(half ^ 1) * 128 + r];
       const float ma = half == 0 ? m : m_o, mb = half == 0 ? m_o : m;
@@ -324,19 +337,31 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       const float M = fmaxf(ma, mb);
       const float sa = ma == -INFINITY ? 0.f : ex2(ma - M), sb = mb == -INFINITY ? 0.f : ex2(mb - M);
       const float l_all = la * sa + lb * sb;
-      if (qpos < it.L) {
-        const float rl = __frcp_rn(l_all);
-        const float fa = sa * rl, fb = sb * rl;
-        uint32_t o[16];
+      const float rl = __frcp_rn(l_all);
+      const float fa = sa * rl, fb = sb * rl;
 #pragma unroll
-        for (int jj = 0; jj < 16; ++jj)
-          o[jj] = pack_bf16(__uint_as_float(ra[2 * jj]) * fa + __uint_as_float(rb[2 * jj]) * fb,
-                            __uint_as_float(ra[2 * jj + 1]) * fa + __uint_as_float(rb[2 * jj + 1]) * fb);
-        uint4* dst = reinterpret_cast<uint4*>(out + (size_t)(it.s0 + qpos) * ldo + it.h * DH + half * 32);
+      for (int sub = 0; sub < DH / 64; ++sub) {
+        const int c0 = half * (DH / 2) + sub * 32;
+        uint32_t ra[32], rb[32];
+        tmem_ld_32x32b_x32(tmem + lane_base + 256 + ob * 2 * DH + c0, ra);
+        tmem_ld_32x32b_x32(tmem + lane_base + 256 + ob * 2 * DH + DH + c0, rb);
+        tmem_ld_wait();
+        if (sub == DH / 64 - 1) {
+          tc_fence_before();
+          mbar_arrive(&o_empty[ob]);
+        }
+        if (qpos < it.L) {
+          uint32_t o[16];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) dst[u] = make_uint4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);
-        if (half == 0) lse[(size_t)it.h * T + it.s0 + qpos] = (M + log2f(l_all)) * LN2_F;
+          for (int e = 0; e < 16; ++e)
+            o[e] = pack_bf16(__uint_as_float(ra[2 * e]) * fa + __uint_as_float(rb[2 * e]) * fb,
+                             __uint_as_float(ra[2 * e + 1]) * fa + __uint_as_float(rb[2 * e + 1]) * fb);
+          uint4* dst = reinterpret_cast<uint4*>(out + (size_t)(it.s0 + qpos) * ldo + it.h * DH + c0);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) dst[u] = make_uint4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);
+        }
       }
+      if (half == 0 && qpos < it.L) lse[(size_t)it.h * T + it.s0 + qpos] = (M + log2f(l_all)) * LN2_F;
     };
     int g = 0, j = 0;
     bool pend = false;
@@ -350,7 +375,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       const int w_next = snake_item(j + 1);
       FwdItem nxt{};
       if (w_next < n_items) nxt = fwd_item<CAUSAL>(w_next, H, Hk, cu, tiles);  // prefetch the next item
-      const int ob = j & 1;
+      const int ob = j % NOB;
       const int qpos = it.q0 + r;
       float m = -INFINITY, l = 0.f;
       for (int i = 0; i < it.n_kv; ++i, ++g) {
@@ -433,7 +458,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
           mbar_wait(&p_empty[(g - 1) & 1], ((g - 1) >> 1) & 1);  // PV_{g-1} retired: O is final
           tc_fence_after();
 #pragma unroll
-          for (int c = 0; c < 2; ++c) {
+          for (int c = 0; c < DH / 32; ++c) {
             uint32_t rr[32];
             tmem_ld_32x32b_x32(tmem + lane_base + 256 + ob * 2 * DH + half * DH + c * 32, rr);
             tmem_ld_wait();
@@ -480,43 +505,58 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
 // ==========================================================================================
 // Backward, persistent: one CTA per SM loops over items (128-row KV tile, KV head) in
 // heavy-first order; an item loops over the query heads of its GQA group and the query tiles
-// its keys can see.  Thread r of the 4 softmax warps owns KV row r:
+// (BQB rows) its keys can see.  Thread r of the 4 softmax warps owns KV row r:
 //   S^T = K Q^T, dP^T = V dO^T                      (TMEM, M = kv, N = q)
-//   P1: P^T = exp2(S^T * scale2 - lse2[q])            -> bf16 smem operand     (p_ready)
-//   P2: dS^T = P^T (dP^T - D[q])                      -> bf16 smem operand     (ds_ready)
+//   P1: P^T = exp2(S^T * scale2 - lse2[q])            -> bf16 TMEM operand     (p_ready)
+//   P2: dS^T = P^T (dP^T - D[q])                      -> bf16 TMEM + smem      (ds_ready)
 //   dV += P^T dO, dK += dS^T Q                      (TMEM accumulators across the item)
-//   dQ_tile = dS K                                  (TMEM, drained by TMA reduce-add)
+//   dQ_tile = dS K  (head_dim 64)  or  dQ^T_tile = K^T dS^T (head_dim 128)   (TMEM, drained by
+//                                                    TMA reduce-add into an fp32 accumulator)
 // P^T and dS^T go back to TMEM as bf16 pairs (thread = kv row = TMEM lane), so dV and dK are
 // TS-MMAs with A from TMEM (no shared-memory operand traffic; dS^T also goes to smem as the dQ
 // operand).  P1 pulls S^T into registers first and releases it (s_empty), so S(i+1) runs while
-// P1/P2(i) compute; dS^T reuses the dP^T columns, so dP(i+1) is issued after dK(i).  The order
-// also spans item boundaries (K/V are double-buffered by item).
-// Two softmax warps share each TMEM lane quadrant and split the 128 query columns (the backward
+// P1/P2(i) compute; dS^T reuses the dP^T columns, so dP(i+1) is issued after dK(i).
+// Two softmax warps share each TMEM lane quadrant and split the BQB query columns (the backward
 // needs no row reductions), so every SM sub-partition interleaves two softmax warps.
-// TMEM: S^T [0,128), dP^T [128,256), dV [256,320), dK [320,384), dQ [384,448).
+//
+// head_dim 64:  BQB = 128; TMEM S^T [0,128), dP^T [128,256), dV [256,320), dK [320,384),
+//               dQ [384,448) (M = q, N = dh), P^T [448,512); K/V double-buffered by item.
+// head_dim 128: BQB = 64 (the dV / dK accumulators take 256 columns); TMEM S^T [0,64),
+//               dP^T [64,128), dV [128,256), dK [256,384), dQ^T [384,448) (M = dh, N = q: its
+//               A operand is K read as an MN-major view, B = dS^T), P^T [448,480); K/V single-
+//               buffered (smem), so the next item's K/V load waits for the item's last MMAs.
 constexpr int BWD_THREADS = 448;  // w0 TMA, w1 MMA, w2-9 softmax (2 per lane quadrant), w10-13 dQ drain
 
-// Q/dO ring depth: stage i+1's load can only start once dK/dQ(i-1) have read their stage, so two
-// stages expose the TMA latency in front of S(i+1); three hide it.
-constexpr int QD_STAGES = 3;
-struct BwdSmem {
-  static constexpr int KV = 0;                              // 2 items x (K tile, V tile)
-  static constexpr int QD = KV + 2 * 2 * TILE_BYTES;        // QD_STAGES x (Q tile, dO tile)
-  static constexpr int DST = QD + QD_STAGES * 2 * TILE_BYTES;  // dS^T [kv][q] bf16, 2 chunks (dQ operand)
-  static constexpr int LSE = DST + P_BYTES;                 // 2 x 128 fp32 (double-buffered by tile)
-  static constexpr int DD = LSE + 1024;                     // 2 x 128 fp32
-  static constexpr int DQS = DD + 1024;                     // dQ staging: 4 drain warps x 32 rows x 32 fp32
-  static constexpr int BAR = DQS + 4 * 4096;
+template <int DH>
+struct BwdCfg {
+  static constexpr int BQB = DH == 64 ? 128 : 64;     // query rows per iteration
+  static constexpr int QH = BQB / 2;                  // query columns per softmax half
+  static constexpr int KV_TILE = 128 * DH * 2;        // K or V tile (128 kv rows)
+  static constexpr int Q_TILE = BQB * DH * 2;         // Q or dO tile
+  static constexpr int Q_CHUNK = BQB * 128;           // bytes per 64-column chunk of a Q/dO tile
+  static constexpr int KVB = DH == 64 ? 2 : 1;        // K/V buffers (by item)
+  static constexpr int QD_STAGES = 3;                 // Q/dO ring (two expose the TMA latency)
+  static constexpr int KV = 0;
+  static constexpr int QD = KV + KVB * 2 * KV_TILE;
+  static constexpr int DST = QD + QD_STAGES * 2 * Q_TILE;  // dS^T [kv][q] bf16 (dQ operand)
+  static constexpr int LSE = DST + 128 * BQB * 2;           // 2 x BQB fp32 (double-buffered by tile)
+  static constexpr int DD = LSE + 1024;
+  static constexpr int DQS = DD + 1024;                     // dQ staging, 4 drain warps
+  static constexpr int DQS_WARP = DH == 64 ? 4096 : 8192;   // 32 x 32 fp32 | 64 q x 32 dh fp32
+  static constexpr int BAR = DQS + 4 * DQS_WARP;
   static constexpr int TOTAL = BAR + 256;
+  // TMEM columns
+  static constexpr uint32_t T_ST = 0, T_DPT = BQB, T_DV = 2 * BQB, T_DK = 2 * BQB + DH, T_DQ = 2 * BQB + 2 * DH,
+                            T_PT = 448;
+  static_assert(TOTAL + 1024 <= 227 * 1024, "backward smem");
+  static_assert(T_DQ + (DH == 64 ? DH : BQB) <= T_PT && T_PT + BQB / 2 <= 512, "backward TMEM");
 };
-
-
 
 struct BwdItem {
   int kv0, hk, s0, L, qt_first, n_q, n_it;
 };
 
-template <bool CAUSAL>
+template <int BQB, bool CAUSAL>
 __device__ __forceinline__ BwdItem bwd_item(int w, int Hk, int G, const int32_t* cu, const int2* tiles) {
   BwdItem it;
   const int2 tk = tiles[w / Hk];
@@ -524,15 +564,15 @@ __device__ __forceinline__ BwdItem bwd_item(int w, int Hk, int G, const int32_t*
   it.hk = w % Hk;
   it.s0 = cu[tk.x];
   it.L = cu[tk.x + 1] - it.s0;
-  const int n_q_all = (it.L + BQ - 1) / BQ;
-  it.qt_first = CAUSAL ? it.kv0 / BQ : 0;
+  const int n_q_all = (it.L + BQB - 1) / BQB;
+  it.qt_first = CAUSAL ? it.kv0 / BQB : 0;
   it.n_q = n_q_all - it.qt_first;
   it.n_it = G * it.n_q;
   return it;
 }
 
 // Flat cursor over (item, iteration) for the MMA warp's one-iteration lookahead.
-template <bool CAUSAL>
+template <int BQB, bool CAUSAL>
 struct BwdCursor {
   int j, w, it;
   bool valid;
@@ -540,7 +580,7 @@ struct BwdCursor {
   __device__ __forceinline__ void load(int n_items, int Hk, int G, const int32_t* cu, const int2* tiles) {
     w = snake_item(j);
     valid = w < n_items;
-    if (valid) item = bwd_item<CAUSAL>(w, Hk, G, cu, tiles);
+    if (valid) item = bwd_item<BQB, CAUSAL>(w, Hk, G, cu, tiles);
   }
   __device__ __forceinline__ void next(int n_items, int Hk, int G, const int32_t* cu, const int2* tiles) {
     if (++it == item.n_it) {
@@ -551,7 +591,7 @@ struct BwdCursor {
   }
 };
 
-template <bool CAUSAL>
+template <int DH, bool CAUSAL>
 __global__ void __launch_bounds__(BWD_THREADS, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                     const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_do,
@@ -560,13 +600,18 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
                     const float* __restrict__ lse, const float* __restrict__ Dvec,
                     __nv_bfloat16* __restrict__ dk, int lddk, __nv_bfloat16* __restrict__ dv, int lddv, int T, int H,
                     int Hk, float scale2, float scale, const float2* __restrict__ rope_cs) {
+  using C = BwdCfg<DH>;
+  constexpr int BQB = C::BQB, QH = C::QH, QDS = C::QD_STAGES, KVB = C::KVB;
+  constexpr int KVT = C::KV_TILE, QT = C::Q_TILE;
+  constexpr uint32_t T_ST = C::T_ST, T_DPT = C::T_DPT, T_DV = C::T_DV, T_DK = C::T_DK, T_DQ = C::T_DQ,
+                     T_PT = C::T_PT;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* sm = align_smem_1024(smem_raw);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + BwdSmem::BAR);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::BAR);
   uint64_t* kv_full = bar;          // [2]
   uint64_t* kv_empty = bar + 2;     // [2]
-  uint64_t* qd_full = bar + 4;      // [QD_STAGES]
-  uint64_t* qd_empty = bar + 7;     // [QD_STAGES]
+  uint64_t* qd_full = bar + 4;      // [QDS]
+  uint64_t* qd_empty = bar + 7;     // [QDS]
   uint64_t* s_full = bar + 10;
   uint64_t* dp_full = bar + 11;
   uint64_t* p_ready = bar + 12;
@@ -579,8 +624,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   uint64_t* dkv_empty = bar + 19;
   uint64_t* s_empty = bar + 20;   // S^T TMEM loaded by the softmax warps (the next S may overwrite it)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 21);
-  float* s_lse = reinterpret_cast<float*>(sm + BwdSmem::LSE);
-  float* s_D = reinterpret_cast<float*>(sm + BwdSmem::DD);
+  float* s_lse = reinterpret_cast<float*>(sm + C::LSE);
+  float* s_D = reinterpret_cast<float*>(sm + C::DD);
 
   const int G = H / Hk;
   const int n_items = *n_tiles * Hk;
@@ -595,7 +640,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       mbar_init(&kv_full[b], 1);
       mbar_init(&kv_empty[b], 1);
     }
-    for (int b = 0; b < QD_STAGES; ++b) {
+    for (int b = 0; b < QDS; ++b) {
       mbar_init(&qd_full[b], 1);
       mbar_init(&qd_empty[b], 1);
     }
@@ -617,72 +662,79 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // P^T (bf16 pairs) lives in [448, 512): half h at 448 + 32h.  dS^T (bf16 pairs) overwrites the
-  // first 32 of each half's 64 dP^T columns once that half holds dP^T in registers.
-  constexpr uint32_t T_ST = 0, T_DPT = 128, T_DV = 256, T_DK = 320, T_DQ = 384, T_PT = 448;
 
   if (warp == 0) {
     if (lane == 0) {
       int gi = 0, j = 0;
       BwdItem itm_n{};
-      if (snake_item(0) < n_items) itm_n = bwd_item<CAUSAL>(snake_item(0), Hk, G, cu, tiles);
+      if (snake_item(0) < n_items) itm_n = bwd_item<BQB, CAUSAL>(snake_item(0), Hk, G, cu, tiles);
       for (int w = snake_item(0); w < n_items; w = snake_item(j + 1), ++j) {
         const BwdItem itm = itm_n;
-        if (snake_item(j + 1) < n_items) itm_n = bwd_item<CAUSAL>(snake_item(j + 1), Hk, G, cu, tiles);  // prefetch
-        const int kb = j & 1;
-        mbar_wait(&kv_empty[kb], ((j >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(&kv_full[kb], 2 * TILE_BYTES);
-        unsigned char* kvd = sm + BwdSmem::KV + kb * 2 * TILE_BYTES;
-        tma_load_2d(kvd, &map_k, &kv_full[kb], itm.hk * DH, itm.s0 + itm.kv0);
-        tma_load_2d(kvd + TILE_BYTES, &map_v, &kv_full[kb], itm.hk * DH, itm.s0 + itm.kv0);
+        if (snake_item(j + 1) < n_items) itm_n = bwd_item<BQB, CAUSAL>(snake_item(j + 1), Hk, G, cu, tiles);  // prefetch
+        const int kb = j % KVB;
+        mbar_wait(&kv_empty[kb], ((j / KVB) & 1) ^ 1);
+        mbar_arrive_expect_tx(&kv_full[kb], 2 * KVT);
+        unsigned char* kvd = sm + C::KV + kb * 2 * KVT;
+#pragma unroll
+        for (int c = 0; c < DH / 64; ++c) {
+          tma_load_2d(kvd + c * 16384, &map_k, &kv_full[kb], itm.hk * DH + 64 * c, itm.s0 + itm.kv0);
+          tma_load_2d(kvd + KVT + c * 16384, &map_v, &kv_full[kb], itm.hk * DH + 64 * c, itm.s0 + itm.kv0);
+        }
         for (int it = 0; it < itm.n_it; ++it, ++gi) {
           const int g = it / itm.n_q, qt = itm.qt_first + it % itm.n_q;
           const int h = itm.hk * G + g;
-          const int st = gi % QD_STAGES;
-          mbar_wait(&qd_empty[st], ((gi / QD_STAGES) & 1) ^ 1);
-          mbar_arrive_expect_tx(&qd_full[st], 2 * TILE_BYTES);
-          unsigned char* dst = sm + BwdSmem::QD + st * 2 * TILE_BYTES;
-          tma_load_2d(dst, &map_q, &qd_full[st], h * DH, itm.s0 + qt * BQ);
-          tma_load_2d(dst + TILE_BYTES, &map_do, &qd_full[st], h * DH, itm.s0 + qt * BQ);
+          const int st = gi % QDS;
+          mbar_wait(&qd_empty[st], ((gi / QDS) & 1) ^ 1);
+          mbar_arrive_expect_tx(&qd_full[st], 2 * QT);
+          unsigned char* dst = sm + C::QD + st * 2 * QT;
+#pragma unroll
+          for (int c = 0; c < DH / 64; ++c) {
+            tma_load_2d(dst + c * C::Q_CHUNK, &map_q, &qd_full[st], h * DH + 64 * c, itm.s0 + qt * BQB);
+            tma_load_2d(dst + QT + c * C::Q_CHUNK, &map_do, &qd_full[st], h * DH + 64 * c, itm.s0 + qt * BQB);
+          }
         }
       }
     }
   } else if (warp == 1) {
     {  // the whole warp runs the loop; MMAs and commits are issued by one elected lane
-      constexpr uint32_t id_sp = idesc_bf16_f32(BKV, BQ, false, false);  // M = kv, N = q
-      constexpr uint32_t id_kv = idesc_bf16_f32(BKV, DH, false, true);   // dV, dK: A K-major, B MN-major
-      constexpr uint32_t id_dq = idesc_bf16_f32(BQ, DH, true, true);     // dQ: A = dS (MN-major view of dS^T)
-      const uint32_t ds_base = smem_u32(sm + BwdSmem::DST);
-      auto kv_base = [&](int j) { return smem_u32(sm + BwdSmem::KV + (j & 1) * 2 * TILE_BYTES); };
-      auto qd_base = [&](int gi) { return smem_u32(sm + BwdSmem::QD + (gi % QD_STAGES) * 2 * TILE_BYTES); };
+      constexpr uint32_t id_sp = idesc_bf16_f32(BKV, BQB, false, false);  // M = kv, N = q
+      constexpr uint32_t id_kv = idesc_bf16_f32(BKV, DH, false, true);    // dV, dK: A K-major, B MN-major
+      // dQ (dh 64): M = q, N = dh, A = dS (MN-major view of dS^T), B = K (MN-major)
+      // dQ^T (dh 128): M = dh, N = q, A = K^T (MN-major view of K), B = dS^T (MN-major)
+      constexpr uint32_t id_dq = DH == 64 ? idesc_bf16_f32(BQB, DH, true, true) : idesc_bf16_f32(DH, BQB, true, true);
+      const uint32_t ds_base = smem_u32(sm + C::DST);
+      auto kv_base = [&](int j) { return smem_u32(sm + C::KV + (j % KVB) * 2 * KVT); };
+      auto qd_base = [&](int gi) { return smem_u32(sm + C::QD + (gi % QDS) * 2 * QT); };
+      // K-major descriptor of K-step kk over a [rows][DH] tile whose 64-column chunks are `cs` bytes apart
+      auto kdesc = [&](uint32_t base, int kk, uint32_t cs) {
+        return sdesc((base >> 4) + (kk >> 2) * (cs >> 4) + (kk & 3) * 2, 16, 1024);
+      };
       // S^T(gi) = K Q^T and dP^T(gi) = V dO^T of the cursor's iteration
-      auto issue_s = [&](const BwdCursor<CAUSAL>& c, int gi) {
-        mbar_wait(&qd_full[gi % QD_STAGES], (gi / QD_STAGES) & 1);
-        if (c.it == 0) mbar_wait(&kv_full[c.j & 1], (c.j >> 1) & 1);
+      auto issue_s = [&](const BwdCursor<BQB, CAUSAL>& c, int gi) {
+        mbar_wait(&qd_full[gi % QDS], (gi / QDS) & 1);
+        if (c.it == 0) mbar_wait(&kv_full[c.j % KVB], (c.j / KVB) & 1);
         if (gi >= 1) mbar_wait(s_empty, (gi - 1) & 1);  // S^T(gi-1) is in the softmax registers
         tc_fence_after();
         const uint32_t kb = kv_base(c.j), qb = qd_base(gi);
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < DH / 16; ++kk)
-            umma_bf16(tmem + T_ST, sdesc((kb >> 4) + kk * 2, 16, 1024), sdesc((qb >> 4) + kk * 2, 16, 1024),
-                      id_sp, kk > 0);
+            umma_bf16(tmem + T_ST, kdesc(kb, kk, 16384), kdesc(qb, kk, C::Q_CHUNK), id_sp, kk > 0);
           umma_commit(s_full);
         }
         __syncwarp();
       };
-      auto issue_dp = [&](const BwdCursor<CAUSAL>& c, int gi) {
-        const uint32_t vb = kv_base(c.j) + TILE_BYTES, db = qd_base(gi) + TILE_BYTES;
+      auto issue_dp = [&](const BwdCursor<BQB, CAUSAL>& c, int gi) {
+        const uint32_t vb = kv_base(c.j) + KVT, db = qd_base(gi) + QT;
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < DH / 16; ++kk)
-            umma_bf16(tmem + T_DPT, sdesc((vb >> 4) + kk * 2, 16, 1024), sdesc((db >> 4) + kk * 2, 16, 1024),
-                      id_sp, kk > 0);
+            umma_bf16(tmem + T_DPT, kdesc(vb, kk, 16384), kdesc(db, kk, C::Q_CHUNK), id_sp, kk > 0);
           umma_commit(dp_full);
         }
         __syncwarp();
       };
-      BwdCursor<CAUSAL> cur;
+      BwdCursor<BQB, CAUSAL> cur;
       cur.j = 0;
       cur.it = 0;
       cur.load(n_items, Hk, G, cu, tiles);
@@ -692,45 +744,53 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         issue_dp(cur, 0);
       }
       while (cur.valid) {
-        BwdCursor<CAUSAL> nxt = cur;
+        BwdCursor<BQB, CAUSAL> nxt = cur;
         nxt.next(n_items, Hk, G, cu, tiles);
         const uint32_t qb = qd_base(gi), kb = kv_base(cur.j);
         // S^T(gi+1) as soon as P1(gi) has pulled S^T(gi) into registers: it runs while P1/P2(gi) compute
-        if (nxt.valid) issue_s(nxt, gi + 1);
-        // dV += P^T dO
+        // (head_dim 128: a new item's S also waits for its K/V, i.e. for the previous item's last MMAs)
+        if (nxt.valid && (KVB == 2 || nxt.it > 0)) issue_s(nxt, gi + 1);
+        // dV += P^T dO   (B = dO, MN-major: N = dh over DH/64 atoms Q_CHUNK apart, K = q rows)
         mbar_wait(p_ready, gi & 1);
         if (cur.it == 0) mbar_wait(dkv_empty, (cur.j & 1) ^ 1);  // previous item's epilogue read dK/dV
         tc_fence_after();
         if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < BQ / 16; ++kk)  // reduction over the 128 queries; A = P^T from TMEM
-            umma_bf16_ts(tmem + T_DV, tmem + T_PT + kk * 8, sdesc(((qb + TILE_BYTES) >> 4) + kk * 128, 8192, 1024),
+          for (int kk = 0; kk < BQB / 16; ++kk)  // reduction over the BQB queries; A = P^T from TMEM
+            umma_bf16_ts(tmem + T_DV, tmem + T_PT + kk * 8, sdesc(((qb + QT) >> 4) + kk * 128, C::Q_CHUNK, 1024),
                          id_kv, (cur.it > 0 || kk > 0) ? 1u : 0u);
           umma_commit(p_free);
         }
         __syncwarp();
-        // dK += dS^T Q (A = dS^T from TMEM) ; dQ = dS K (A = dS^T smem, MN-major view)
+        // dK += dS^T Q (A = dS^T from TMEM) ; dQ from the dS^T smem operand
         mbar_wait(ds_ready, gi & 1);
         mbar_wait(dq_empty, (gi & 1) ^ 1);
         tc_fence_after();
         if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < BQ / 16; ++kk)
-            umma_bf16_ts(tmem + T_DK, tmem + T_DPT + (kk >> 2) * 64 + (kk & 3) * 8,
-                         sdesc((qb >> 4) + kk * 128, 8192, 1024), id_kv, (cur.it > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < BQB / 16; ++kk)  // half kk / (QH/16) holds dS^T in the first QH/2 of its QH dP^T columns
+            umma_bf16_ts(tmem + T_DK, tmem + T_DPT + (kk / (QH / 16)) * QH + (kk % (QH / 16)) * 8,
+                         sdesc((qb >> 4) + kk * 128, C::Q_CHUNK, 1024), id_kv, (cur.it > 0 || kk > 0) ? 1u : 0u);
 #pragma unroll
-          for (int kk = 0; kk < BKV / 16; ++kk)  // reduction over the 128 keys
-            umma_bf16(tmem + T_DQ, sdesc((ds_base >> 4) + kk * 128, 16384, 1024),
-                      sdesc((kb >> 4) + kk * 128, 8192, 1024), id_dq, kk > 0 ? 1u : 0u);
+          for (int kk = 0; kk < BKV / 16; ++kk) {  // reduction over the 128 keys (16 kv rows = 2 KB per step)
+            if constexpr (DH == 64)
+              umma_bf16(tmem + T_DQ, sdesc((ds_base >> 4) + kk * 128, 16384, 1024),
+                        sdesc((kb >> 4) + kk * 128, 8192, 1024), id_dq, kk > 0 ? 1u : 0u);
+            else
+              umma_bf16(tmem + T_DQ, sdesc((kb >> 4) + kk * 128, 16384, 1024),
+                        sdesc((ds_base >> 4) + kk * 128, 8192, 1024), id_dq, kk > 0 ? 1u : 0u);
+          }
           umma_commit(dq_full);
-          umma_commit(&qd_empty[gi % QD_STAGES]);
+          umma_commit(&qd_empty[gi % QDS]);
           umma_commit(ds_free);
           if (cur.it == cur.item.n_it - 1) {
             umma_commit(dkv_full);
-            umma_commit(&kv_empty[cur.j & 1]);
+            umma_commit(&kv_empty[cur.j % KVB]);
           }
         }
         __syncwarp();
+        // head_dim 128: the first S of the next item once its K/V (single buffer) has landed
+        if (nxt.valid && KVB == 1 && nxt.it == 0) issue_s(nxt, gi + 1);
         // dP^T(gi+1) after dK(gi) (in issue order) has read dS^T out of the dP^T columns
         if (nxt.valid) issue_dp(nxt, gi + 1);
         cur = nxt;
@@ -738,19 +798,19 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       }
     }
   } else if (warp >= 10) {
-    // ---------------- dQ drain: TMEM -> smem (SWIZZLE_128B, 32 rows x 32 fp32 per warp) -> TMA
+    // ---------------- dQ drain: TMEM -> smem (SWIZZLE_128B boxes of 32 fp32 columns) -> TMA
     // reduce-add into the fp32 accumulator.  Rows past the sequence end are exact zeros (their
     // dS columns were masked), so whole boxes are added; the map clips rows past T.
     const int q4 = warp & 3;
     const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
-    unsigned char* stage = sm + BwdSmem::DQS + q4 * 4096;
+    unsigned char* stage = sm + C::DQS + q4 * C::DQS_WARP;
     bool staged = false;
     int gi = 0, j = 0;
     BwdItem itm_n{};
-    if (snake_item(0) < n_items) itm_n = bwd_item<CAUSAL>(snake_item(0), Hk, G, cu, tiles);
+    if (snake_item(0) < n_items) itm_n = bwd_item<BQB, CAUSAL>(snake_item(0), Hk, G, cu, tiles);
     for (int w = snake_item(0); w < n_items; w = snake_item(j + 1), ++j) {
       const BwdItem itm = itm_n;
-      if (snake_item(j + 1) < n_items) itm_n = bwd_item<CAUSAL>(snake_item(j + 1), Hk, G, cu, tiles);  // prefetch
+      if (snake_item(j + 1) < n_items) itm_n = bwd_item<BQB, CAUSAL>(snake_item(j + 1), Hk, G, cu, tiles);  // prefetch
       for (int it = 0; it < itm.n_it; ++it, ++gi) {
         const int g = it / itm.n_q, qt = itm.qt_first + it % itm.n_q;
         const int h = itm.hk * G + g;
@@ -762,21 +822,43 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         tmem_ld_wait();
         tc_fence_before();
         mbar_arrive(dq_empty);  // TMEM free as soon as it is in registers
+        if constexpr (DH == 64) {
+          // lane = query row q4*32 + lane, registers = dh columns [0,32) and [32,64)
 #pragma unroll
-        for (int hc = 0; hc < 2; ++hc) {
-          const uint32_t* x = hc == 0 ? qa : qb;
-          if (staged) {  // the previous box has been read out of the staging buffer
+          for (int hc = 0; hc < 2; ++hc) {
+            const uint32_t* x = hc == 0 ? qa : qb;
+            if (staged) {  // the previous box has been read out of the staging buffer
+              if (lane == 0) bulk_wait_read<0>();
+              __syncwarp();
+            }
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+              *reinterpret_cast<uint4*>(stage + lane * 128 + ((c ^ (lane & 7)) << 4)) =
+                  make_uint4(x[4 * c], x[4 * c + 1], x[4 * c + 2], x[4 * c + 3]);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_reduce_add_2d(&map_dq, stage, h * DH + hc * 32, itm.s0 + qt * BQB + q4 * 32);
+              bulk_commit();
+            }
+            staged = true;
+          }
+        } else {
+          // dQ^T: lane = dh column q4*32 + lane, registers = the 64 query rows; one [64 q][32 dh]
+          // box per warp (each row's 32 floats are one swizzled 128-byte line)
+          if (staged) {
             if (lane == 0) bulk_wait_read<0>();
             __syncwarp();
           }
 #pragma unroll
-          for (int c = 0; c < 8; ++c)
-            *reinterpret_cast<uint4*>(stage + lane * 128 + ((c ^ (lane & 7)) << 4)) =
-                make_uint4(x[4 * c], x[4 * c + 1], x[4 * c + 2], x[4 * c + 3]);
+          for (int r = 0; r < 64; ++r) {
+            const uint32_t v = r < 32 ? qa[r] : qb[r - 32];
+            *reinterpret_cast<uint32_t*>(stage + r * 128 + ((((lane >> 2) ^ (r & 7))) << 4) + (lane & 3) * 4) = v;
+          }
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_reduce_add_2d(&map_dq, stage, h * DH + hc * 32, itm.s0 + qt * BQ + q4 * 32);
+            tma_reduce_add_2d(&map_dq, stage, h * DH + q4 * 32, itm.s0 + qt * BQB);
             bulk_commit();
           }
           staged = true;
@@ -786,62 +868,60 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     if (lane == 0) bulk_wait<0>();
   } else {
     const int q4 = warp & 3;
-    const int half = (warp - 2) >> 2;  // query columns [64 * half, 64 * half + 64)
+    const int half = (warp - 2) >> 2;  // query columns [QH * half, QH * half + QH)
     const int r = q4 * 32 + lane;      // kv row (S^T, dP^T, dK, dV)
     const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
     const int tid = threadIdx.x - 64;  // 0..255
-    unsigned char* dst = sm + BwdSmem::DST;
+    unsigned char* dst = sm + C::DST;
     // This thread's -lse2 (tid < 128) or -D (tid >= 128) entry of iteration `it` of item `im`; loaded
     // one iteration ahead so the global-load latency stays off the per-tile path.
     auto fetch_row = [&](const BwdItem& im, int it) -> float {
       const int hh = im.hk * G + it / im.n_q;
-      const int qi = (im.qt_first + it % im.n_q) * BQ + (tid & 127);
-      if (qi >= im.L) return tid < 128 ? -INFINITY : 0.f;  // stored negated: -lse2, -D
+      const int qi = (im.qt_first + it % im.n_q) * BQB + (tid & 127);
+      if ((tid & 127) >= BQB || qi >= im.L) return tid < 128 ? -INFINITY : 0.f;  // stored negated: -lse2, -D
       return tid < 128 ? -lse[(size_t)hh * T + im.s0 + qi] * LOG2E_F : -Dvec[(size_t)hh * T + im.s0 + qi];
     };
     int gi = 0, j = 0;
     BwdItem itm_n{};
     float row_next = 0.f;
     if (snake_item(0) < n_items) {
-      itm_n = bwd_item<CAUSAL>(snake_item(0), Hk, G, cu, tiles);
+      itm_n = bwd_item<BQB, CAUSAL>(snake_item(0), Hk, G, cu, tiles);
       row_next = fetch_row(itm_n, 0);
     }
     for (int w = snake_item(0); w < n_items; w = snake_item(j + 1), ++j) {
       const BwdItem itm = itm_n;
       const bool has_next = snake_item(j + 1) < n_items;
-      if (has_next) itm_n = bwd_item<CAUSAL>(snake_item(j + 1), Hk, G, cu, tiles);  // prefetch
+      if (has_next) itm_n = bwd_item<BQB, CAUSAL>(snake_item(j + 1), Hk, G, cu, tiles);  // prefetch
       const int kvpos = itm.kv0 + r;
       for (int it = 0; it < itm.n_it; ++it, ++gi) {
-        const int g = it / itm.n_q, qt = itm.qt_first + it % itm.n_q;
-        const int h = itm.hk * G + g;
-        const int q0 = qt * BQ;
+        const int q0 = (itm.qt_first + it % itm.n_q) * BQB;
         float* lse_t = s_lse + (gi & 1) * 128;  // double-buffered: one barrier per tile suffices
         float* D_t = s_D + (gi & 1) * 128;
-        (tid < 128 ? lse_t : D_t)[tid & 127] = row_next;
+        if ((tid & 127) < BQB) (tid < 128 ? lse_t : D_t)[tid & 127] = row_next;
         if (it + 1 < itm.n_it)
           row_next = fetch_row(itm, it + 1);
         else if (has_next)
           row_next = fetch_row(itm_n, 0);
         named_bar(1, 256);
         const bool need_mask =
-            (CAUSAL && q0 < itm.kv0 + BKV - 1) || (q0 + BQ > itm.L) || (itm.kv0 + BKV > itm.L);
+            (CAUSAL && q0 < itm.kv0 + BKV - 1) || (q0 + BQB > itm.L) || (itm.kv0 + BKV > itm.L);
         // ---- P1: S^T -> P^T
         mbar_wait(s_full, gi & 1);
         tc_fence_after();
-        uint32_t sr2[2][32];
-        tmem_ld_32x32b_x32(tmem + lane_base + T_ST + half * 64, sr2[0]);
-        tmem_ld_32x32b_x32(tmem + lane_base + T_ST + half * 64 + 32, sr2[1]);
+        uint32_t sr2[QH / 32][32];
+#pragma unroll
+        for (int c = 0; c < QH / 32; ++c) tmem_ld_32x32b_x32(tmem + lane_base + T_ST + half * QH + 32 * c, sr2[c]);
         tmem_ld_wait();
         tc_fence_before();
         mbar_arrive(s_empty);
         if (gi >= 1) mbar_wait(p_free, (gi - 1) & 1);  // dV(gi-1) has read P^T
-        uint32_t pk[32];  // this row's P^T as bf16 pairs: the dV operand, and P for phase 2
+        uint32_t pk[QH / 2];  // this row's P^T as bf16 pairs: the dV operand, and P for phase 2
         // Two instantiations so that interior tiles carry no per-element mask code (if-converted
         // compares and selects otherwise cost more issue slots than the exponentials).
         auto phase1 = [&](auto masked) {
 #pragma unroll
-          for (int cc = 0; cc < 64; cc += 32) {
-            const int c0 = half * 64 + cc;
+          for (int cc = 0; cc < QH; cc += 32) {
+            const int c0 = half * QH + cc;
             const uint32_t* sr = sr2[cc >> 5];
             // valid columns c0 + i: i >= lo (causal: query not before the key), i < hi (inside the sequence)
             const int lo = CAUSAL ? kvpos - (q0 + c0) : INT_MIN;
@@ -881,7 +961,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
           phase1(std::true_type{});
         else
           phase1(std::false_type{});
-        tmem_st_32x32b_x32(tmem + lane_base + T_PT + half * 32, pk);
+        if constexpr (QH == 64)
+          tmem_st_32x32b_x32(tmem + lane_base + T_PT + half * 32, pk);
+        else
+          tmem_st_32x32b_x16(tmem + lane_base + T_PT + half * 16, pk);
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(p_ready);
@@ -889,10 +972,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         mbar_wait(dp_full, gi & 1);
         tc_fence_after();
         if (gi >= 1) mbar_wait(ds_free, (gi - 1) & 1);  // dQ(gi-1) has read the dS^T smem operand
-        uint32_t dk2[32];  // dS^T as bf16 pairs
+        uint32_t dk2[QH / 2];  // dS^T as bf16 pairs
 #pragma unroll
-        for (int cc = 0; cc < 64; cc += 32) {
-          const int c0 = half * 64 + cc;
+        for (int cc = 0; cc < QH; cc += 32) {
+          const int c0 = half * QH + cc;
           uint32_t pr[32];
           tmem_ld_32x32b_x32(tmem + lane_base + T_DPT + c0, pr);
           tmem_ld_wait();
@@ -913,52 +996,56 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
                 make_uint4(dk2[cc / 2 + 4 * u], dk2[cc / 2 + 4 * u + 1], dk2[cc / 2 + 4 * u + 2], dk2[cc / 2 + 4 * u + 3]);
           }
         }
-        // dS^T into the first 32 of this half's dP^T columns (already in registers)
-        tmem_st_32x32b_x32(tmem + lane_base + T_DPT + half * 64, dk2);
+        // dS^T into the first QH/2 of this half's QH dP^T columns (already in registers)
+        if constexpr (QH == 64)
+          tmem_st_32x32b_x32(tmem + lane_base + T_DPT + half * QH, dk2);
+        else
+          tmem_st_32x32b_x16(tmem + lane_base + T_DPT + half * QH, dk2);
         tmem_st_wait();
         fence_proxy_async_smem();
         tc_fence_before();
         mbar_arrive(ds_ready);
       }
       // ---- item epilogue: dK (scaled, inverse RoPE), then dV -> bf16; TMEM is released after
-      // the dV load so the next item's first dV MMA can start while the stores drain
+      // the loads so the next item's first dV MMA can start while the stores drain
       mbar_wait(dkv_full, j & 1);
       tc_fence_after();
       {
         const int which = half;  // half 0 drains dK, half 1 dV
-        uint32_t lo[32], hi[32];
-        tmem_ld_32x32b_x32(tmem + lane_base + (which == 0 ? T_DK : T_DV), lo);
-        tmem_ld_32x32b_x32(tmem + lane_base + (which == 0 ? T_DK : T_DV) + 32, hi);
+        const uint32_t tbase = tmem + lane_base + (which == 0 ? T_DK : T_DV);
+        uint32_t acc[DH / 32][32];
+#pragma unroll
+        for (int c = 0; c < DH / 32; ++c) tmem_ld_32x32b_x32(tbase + 32 * c, acc[c]);
         tmem_ld_wait();
         tc_fence_before();
         mbar_arrive(dkv_empty);
         if (kvpos < itm.L) {
-        const float f = which == 0 ? scale : 1.f;
-        if (which == 0 && rope_cs != nullptr) {
-          // K was rotated by RoPE in the forward: dK_pre = R(pos)^T dK  (rotate by -theta)
+          const float f = which == 0 ? scale : 1.f;
+          if (which == 0 && rope_cs != nullptr) {
+            // K was rotated by RoPE in the forward: dK_pre = R(pos)^T dK  (rotate by -theta);
+            // rotate-half pairs (k, k + DH/2)
 #pragma unroll
-          for (int k = 0; k < 32; ++k) {
-            const float2 cs = rope_cs_at(rope_cs, kvpos, k, 32);
-            const float a = __uint_as_float(lo[k]), b = __uint_as_float(hi[k]);
-            lo[k] = __float_as_uint(a * cs.x + b * cs.y);
-            hi[k] = __float_as_uint(b * cs.x - a * cs.y);
+            for (int cp = 0; cp < DH / 64; ++cp)
+#pragma unroll
+              for (int k = 0; k < 32; ++k) {
+                const float2 cs = rope_cs_at(rope_cs, kvpos, 32 * cp + k, DH / 2);
+                const float a = __uint_as_float(acc[cp][k]), b = __uint_as_float(acc[cp + DH / 64][k]);
+                acc[cp][k] = __float_as_uint(a * cs.x + b * cs.y);
+                acc[cp + DH / 64][k] = __float_as_uint(b * cs.x - a * cs.y);
+              }
           }
-        }
-        __nv_bfloat16* base = which == 0 ? dk + (size_t)(itm.s0 + kvpos) * lddk : dv + (size_t)(itm.s0 + kvpos) * lddv;
-        uint4* d4 = reinterpret_cast<uint4*>(base + itm.hk * DH);
+          __nv_bfloat16* base = which == 0 ? dk + (size_t)(itm.s0 + kvpos) * lddk : dv + (size_t)(itm.s0 + kvpos) * lddv;
+          uint4* d4 = reinterpret_cast<uint4*>(base + itm.hk * DH);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const uint32_t* x = lo + 8 * u;
-          const uint32_t* y = hi + 8 * u;
-          d4[u] = make_uint4(pack_bf16(__uint_as_float(x[0]) * f, __uint_as_float(x[1]) * f),
-                             pack_bf16(__uint_as_float(x[2]) * f, __uint_as_float(x[3]) * f),
-                             pack_bf16(__uint_as_float(x[4]) * f, __uint_as_float(x[5]) * f),
-                             pack_bf16(__uint_as_float(x[6]) * f, __uint_as_float(x[7]) * f));
-          d4[4 + u] = make_uint4(pack_bf16(__uint_as_float(y[0]) * f, __uint_as_float(y[1]) * f),
-                                 pack_bf16(__uint_as_float(y[2]) * f, __uint_as_float(y[3]) * f),
-                                 pack_bf16(__uint_as_float(y[4]) * f, __uint_as_float(y[5]) * f),
-                                 pack_bf16(__uint_as_float(y[6]) * f, __uint_as_float(y[7]) * f));
-        }
+          for (int c = 0; c < DH / 32; ++c)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const uint32_t* x = acc[c] + 8 * u;
+              d4[4 * c + u] = make_uint4(pack_bf16(__uint_as_float(x[0]) * f, __uint_as_float(x[1]) * f),
+                                         pack_bf16(__uint_as_float(x[2]) * f, __uint_as_float(x[3]) * f),
+                                         pack_bf16(__uint_as_float(x[4]) * f, __uint_as_float(x[5]) * f),
+                                         pack_bf16(__uint_as_float(x[6]) * f, __uint_as_float(x[7]) * f));
+            }
         }
       }
     }
@@ -972,43 +1059,51 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
 }
 
 // D[h][t] = sum_d dO[t,h,d] * O[t,h,d]; zero the fp32 dQ accumulator row.  One warp per (t, h).
+template <int DH>
 __global__ void attn_bwd_pre_kernel(const __nv_bfloat16* __restrict__ o, int ldo, const __nv_bfloat16* __restrict__ dout,
                                     int lddo, float* __restrict__ Dvec, float* __restrict__ dq_acc, int T, int H) {
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (w >= T * H) return;
   const int t = w / H, h = w - t * H;
-  const __nv_bfloat162 a = reinterpret_cast<const __nv_bfloat162*>(o + (size_t)t * ldo + h * DH)[lane];
-  const __nv_bfloat162 b = reinterpret_cast<const __nv_bfloat162*>(dout + (size_t)t * lddo + h * DH)[lane];
-  const float2 fa = __bfloat1622float2(a), fb = __bfloat1622float2(b);
-  float v = fa.x * fb.x + fa.y * fb.y;
+  float v = 0.f;
+#pragma unroll
+  for (int c = 0; c < DH / 64; ++c) {
+    const __nv_bfloat162 a = reinterpret_cast<const __nv_bfloat162*>(o + (size_t)t * ldo + h * DH + 64 * c)[lane];
+    const __nv_bfloat162 b = reinterpret_cast<const __nv_bfloat162*>(dout + (size_t)t * lddo + h * DH + 64 * c)[lane];
+    const float2 fa = __bfloat1622float2(a), fb = __bfloat1622float2(b);
+    v += fa.x * fb.x + fa.y * fb.y;
+    reinterpret_cast<float2*>(dq_acc + ((size_t)t * H + h) * DH + 64 * c)[lane] = make_float2(0.f, 0.f);
+  }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
   if (lane == 0) Dvec[(size_t)h * T + t] = v;
-  reinterpret_cast<float2*>(dq_acc + ((size_t)t * H + h) * DH)[lane] = make_float2(0.f, 0.f);
 }
 
 // dq[t, h, :] (bf16, pitched) = scale * dq_acc[t, h, :], then the inverse RoPE rotation at
-// the token's sequence position (cs == null: no rotation).  Thread per (t, h, 8 pair-groups).
+// the token's sequence position (cs == null: no rotation; rotate-half pairs (k, k + DH/2)).
+// Thread per (t, h, group of 8 rotation pairs).
+template <int DH>
 __global__ void attn_bwd_post_kernel(const float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dq, int lddq, int T,
                                      int H, float scale, const int32_t* __restrict__ pos,
                                      const float2* __restrict__ cs) {
-  const long long n = (long long)T * H * 4;  // 4 groups of 8 rotation pairs per head
+  constexpr int GROUPS = DH / 16;  // groups of 8 pairs per head
+  const long long n = (long long)T * H * GROUPS;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const long long th = i >> 2;
-    const int g = (int)(i & 3);
+    const long long th = i / GROUPS;
+    const int g = (int)(i % GROUPS);
     const long long t = th / H;
     const int h = (int)(th - t * H);
     const float* src = dq_acc + th * DH + 8 * g;
     float a[8], b[8];
     *reinterpret_cast<float4*>(a) = reinterpret_cast<const float4*>(src)[0];
     *reinterpret_cast<float4*>(a + 4) = reinterpret_cast<const float4*>(src)[1];
-    *reinterpret_cast<float4*>(b) = reinterpret_cast<const float4*>(src + 32)[0];
-    *reinterpret_cast<float4*>(b + 4) = reinterpret_cast<const float4*>(src + 32)[1];
+    *reinterpret_cast<float4*>(b) = reinterpret_cast<const float4*>(src + DH / 2)[0];
+    *reinterpret_cast<float4*>(b + 4) = reinterpret_cast<const float4*>(src + DH / 2)[1];
     if (cs != nullptr) {
       const int pt = pos[t];
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        const float2 v = rope_cs_at(cs, pt, 8 * g + k, 32);
+        const float2 v = rope_cs_at(cs, pt, 8 * g + k, DH / 2);
         const float x = a[k], y = b[k];
         a[k] = x * v.x + y * v.y;
         b[k] = y * v.x - x * v.y;
@@ -1025,7 +1120,7 @@ __global__ void attn_bwd_post_kernel(const float* __restrict__ dq_acc, __nv_bflo
     vb.w = pack_bf16(b[6] * scale, b[7] * scale);
     __nv_bfloat16* d = dq + t * lddq + h * DH + 8 * g;
     *reinterpret_cast<uint4*>(d) = va;
-    *reinterpret_cast<uint4*>(d + 32) = vb;
+    *reinterpret_cast<uint4*>(d + DH / 2) = vb;
   }
 }
 
@@ -1087,36 +1182,39 @@ MAESTRO_API int maestro_attn_fwd(const void* q, const void* k, const void* v, co
                                  int32_t ldv, void* out, int32_t ldo, float* lse, float softmax_scale, int32_t causal,
                                  const void* plan, void* workspace, void* stream) {
   if (T <= 0) return 0;
-  if (head_dim != DH || H % Hk) return (int)cudaErrorInvalidValue;
+  if ((head_dim != 64 && head_dim != 128) || H % Hk) return (int)cudaErrorInvalidValue;
   cudaStream_t st = (cudaStream_t)stream;
   const int max_tiles = (T + BQ - 1) / BQ + nseq;
   int2* tiles = reinterpret_cast<int2*>(plan != nullptr ? const_cast<void*>(plan) : workspace);
   int* count = reinterpret_cast<int*>(tiles + max_tiles);
   if (plan == nullptr) attn_tiles_kernel<<<1, 1024, 0, st>>>(cu, nseq, tiles, count);
   CUtensorMap mq, mk, mv;
-  bool ok = make_map_2d(&mq, q, (uint64_t)H * DH, T, ldq, 64, 128);
-  ok = ok && make_map_2d(&mk, k, (uint64_t)Hk * DH, T, ldk, 64, 128);
-  ok = ok && make_map_2d(&mv, v, (uint64_t)Hk * DH, T, ldv, 64, 128);
+  bool ok = make_map_2d(&mq, q, (uint64_t)H * head_dim, T, ldq, 64, 128);
+  ok = ok && make_map_2d(&mk, k, (uint64_t)Hk * head_dim, T, ldk, 64, 128);
+  ok = ok && make_map_2d(&mv, v, (uint64_t)Hk * head_dim, T, ldv, 64, 128);
   if (!ok) return (int)cudaErrorInvalidValue;
-  const int smem = FwdSmemP::TOTAL + 1024;
   const int items = max_tiles * H;  // upper bound; the kernel reads the true count
   dim3 grid(items < num_sms() ? items : num_sms());
   const float scale2 = softmax_scale * LOG2E_F;
-  if (causal) {
-    if (ensure_smem<attn_fwd_kernel<true>>(smem)) return launch_status();
-    attn_fwd_kernel<true><<<grid, FWD_THREADS, smem, st>>>(mq, mk, mv, cu, tiles, count, (__nv_bfloat16*)out, ldo,
-                                                          lse, T, H, Hk, scale2);
-  } else {
-    if (ensure_smem<attn_fwd_kernel<false>>(smem)) return launch_status();
-    attn_fwd_kernel<false><<<grid, FWD_THREADS, smem, st>>>(mq, mk, mv, cu, tiles, count, (__nv_bfloat16*)out, ldo,
-                                                           lse, T, H, Hk, scale2);
+#define MB_ATTN_FWD(D, CZ)                                                                                \
+  {                                                                                                       \
+    const int smem = FwdCfg<D>::TOTAL + 1024;                                                             \
+    if (ensure_smem<attn_fwd_kernel<D, CZ>>(smem)) return launch_status();                                \
+    attn_fwd_kernel<D, CZ><<<grid, FWD_THREADS, smem, st>>>(mq, mk, mv, cu, tiles, count, (__nv_bfloat16*)out, \
+                                                           ldo, lse, T, H, Hk, scale2);                   \
   }
+  if (head_dim == 64) {
+    if (causal) MB_ATTN_FWD(64, true) else MB_ATTN_FWD(64, false)
+  } else {
+    if (causal) MB_ATTN_FWD(128, true) else MB_ATTN_FWD(128, false)
+  }
+#undef MB_ATTN_FWD
   return launch_status();
 }
 
-// Backward workspace: tile list + D [H, T] fp32 + dQ accumulator [T, H, 64] fp32.
-MAESTRO_API int64_t maestro_attn_bwd_workspace(int32_t T, int32_t nseq, int32_t H) {
-  return maestro_attn_workspace(T, nseq) + 256 + (int64_t)4 * H * T + (int64_t)4 * T * H * DH + 256;
+// Backward workspace: tile list + D [H, T] fp32 + dQ accumulator [T, H, head_dim] fp32.
+MAESTRO_API int64_t maestro_attn_bwd_workspace(int32_t T, int32_t nseq, int32_t H, int32_t head_dim) {
+  return maestro_attn_workspace(T, nseq) + 256 + (int64_t)4 * H * T + (int64_t)4 * T * H * head_dim + 256;
 }
 
 MAESTRO_API int maestro_attn_bwd(const void* dout, int32_t lddo, const void* q, const void* k, const void* v,
@@ -1126,7 +1224,7 @@ MAESTRO_API int maestro_attn_bwd(const void* dout, int32_t lddo, const void* q, 
                                  float softmax_scale, int32_t causal, const int32_t* rope_pos, const void* rope_cs,
                                  const void* plan, void* workspace, void* stream) {
   if (T <= 0) return 0;
-  if (head_dim != DH || H % Hk) return (int)cudaErrorInvalidValue;
+  if ((head_dim != 64 && head_dim != 128) || H % Hk) return (int)cudaErrorInvalidValue;
   cudaStream_t st = (cudaStream_t)stream;
   unsigned char* w = reinterpret_cast<unsigned char*>(workspace);
   const int max_tiles = (T + BKV - 1) / BKV + nseq;
@@ -1141,33 +1239,47 @@ MAESTRO_API int maestro_attn_bwd(const void* dout, int32_t lddo, const void* q, 
   float* dq_acc = reinterpret_cast<float*>(w + off_acc);
   if (plan == nullptr) attn_kv_tiles_kernel<<<1, 1024, 0, st>>>(cu, nseq, tiles, count);
   const long long warps = (long long)T * H;
-  attn_bwd_pre_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(
-      (const __nv_bfloat16*)o, ldo, (const __nv_bfloat16*)dout, lddo, Dvec, dq_acc, T, H);
-  CUtensorMap mq, mk, mv, mdo;
-  bool ok = make_map_2d(&mq, q, (uint64_t)H * DH, T, ldq, 64, 128);
-  ok = ok && make_map_2d(&mk, k, (uint64_t)Hk * DH, T, ldk, 64, 128);
-  ok = ok && make_map_2d(&mv, v, (uint64_t)Hk * DH, T, ldv, 64, 128);
-  ok = ok && make_map_2d(&mdo, dout, (uint64_t)H * DH, T, lddo, 64, 128);
-  CUtensorMap mdq;
-  ok = ok && make_map_2d(&mdq, dq_acc, (uint64_t)H * DH, T, (uint64_t)H * DH, 32, 32, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4);
+  const unsigned pre_grid = (unsigned)((warps * 32 + 255) / 256);
+  if (head_dim == 64)
+    attn_bwd_pre_kernel<64><<<pre_grid, 256, 0, st>>>((const __nv_bfloat16*)o, ldo, (const __nv_bfloat16*)dout, lddo,
+                                                     Dvec, dq_acc, T, H);
+  else
+    attn_bwd_pre_kernel<128><<<pre_grid, 256, 0, st>>>((const __nv_bfloat16*)o, ldo, (const __nv_bfloat16*)dout, lddo,
+                                                      Dvec, dq_acc, T, H);
+  const int bqb = head_dim == 64 ? 128 : 64;
+  CUtensorMap mq, mk, mv, mdo, mdq;
+  bool ok = make_map_2d(&mq, q, (uint64_t)H * head_dim, T, ldq, 64, bqb);
+  ok = ok && make_map_2d(&mk, k, (uint64_t)Hk * head_dim, T, ldk, 64, 128);
+  ok = ok && make_map_2d(&mv, v, (uint64_t)Hk * head_dim, T, ldv, 64, 128);
+  ok = ok && make_map_2d(&mdo, dout, (uint64_t)H * head_dim, T, lddo, 64, bqb);
+  // dQ accumulator boxes: 32 fp32 columns x (32 query rows | 64 query rows)
+  ok = ok && make_map_2d(&mdq, dq_acc, (uint64_t)H * head_dim, T, (uint64_t)H * head_dim, 32, head_dim == 64 ? 32 : 64,
+                         CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4);
   if (!ok) return (int)cudaErrorInvalidValue;
-  const int smem = BwdSmem::TOTAL + 1024;
   const int items = max_tiles * Hk;  // upper bound; the kernel reads the true count
   dim3 grid(items < num_sms() ? items : num_sms());
   const float scale2 = softmax_scale * LOG2E_F;
-  if (causal) {
-    if (ensure_smem<attn_bwd_kernel<true>>(smem)) return launch_status();
-    attn_bwd_kernel<true><<<grid, BWD_THREADS, smem, st>>>(mq, mk, mv, mdo, mdq, cu, tiles, count, lse, Dvec,
-                                                          (__nv_bfloat16*)dk, lddk, (__nv_bfloat16*)dv, lddv, T, H, Hk,
-                                                          scale2, softmax_scale, (const float2*)rope_cs);
-  } else {
-    if (ensure_smem<attn_bwd_kernel<false>>(smem)) return launch_status();
-    attn_bwd_kernel<false><<<grid, BWD_THREADS, smem, st>>>(mq, mk, mv, mdo, mdq, cu, tiles, count, lse, Dvec,
-                                                           (__nv_bfloat16*)dk, lddk, (__nv_bfloat16*)dv, lddv, T, H,
-                                                           Hk, scale2, softmax_scale, (const float2*)rope_cs);
+#define MB_ATTN_BWD(D, CZ)                                                                                  \
+  {                                                                                                         \
+    const int smem = BwdCfg<D>::TOTAL + 1024;                                                               \
+    if (ensure_smem<attn_bwd_kernel<D, CZ>>(smem)) return launch_status();                                  \
+    attn_bwd_kernel<D, CZ><<<grid, BWD_THREADS, smem, st>>>(mq, mk, mv, mdo, mdq, cu, tiles, count, lse, Dvec, \
+                                                           (__nv_bfloat16*)dk, lddk, (__nv_bfloat16*)dv, lddv, T, \
+                                                           H, Hk, scale2, softmax_scale, (const float2*)rope_cs); \
   }
-  const long long n4 = (long long)T * H * 4;
-  attn_bwd_post_kernel<<<(unsigned)((n4 + 255) / 256 < 148 * 16 ? (n4 + 255) / 256 : 148 * 16), 256, 0, st>>>(
-      dq_acc, (__nv_bfloat16*)dq, lddq, T, H, softmax_scale, rope_pos, (const float2*)rope_cs);
+  if (head_dim == 64) {
+    if (causal) MB_ATTN_BWD(64, true) else MB_ATTN_BWD(64, false)
+  } else {
+    if (causal) MB_ATTN_BWD(128, true) else MB_ATTN_BWD(128, false)
+  }
+#undef MB_ATTN_BWD
+  const long long ng = (long long)T * H * (head_dim / 16);
+  const unsigned post_grid = (unsigned)((ng + 255) / 256 < 148 * 16 ? (ng + 255) / 256 : 148 * 16);
+  if (head_dim == 64)
+    attn_bwd_post_kernel<64><<<post_grid, 256, 0, st>>>(dq_acc, (__nv_bfloat16*)dq, lddq, T, H, softmax_scale, rope_pos,
+                                                       (const float2*)rope_cs);
+  else
+    attn_bwd_post_kernel<128><<<post_grid, 256, 0, st>>>(dq_acc, (__nv_bfloat16*)dq, lddq, T, H, softmax_scale,
+                                                        rope_pos, (const float2*)rope_cs);
   return launch_status();
 }

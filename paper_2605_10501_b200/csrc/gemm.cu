@@ -73,7 +73,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                  const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_r, void* C, int M,
                  int N, int K, int ldc, int splits,
-                 const int32_t* __restrict__ rope_pos, const float2* __restrict__ rope_cs, int rope_cols,
+                 const int32_t* __restrict__ rope_pos, const float2* __restrict__ rope_cs, int rope_cols, int rope_hd,
                  __nv_bfloat16* __restrict__ swiglu_out, int ld_swiglu, const __nv_bfloat16* __restrict__ resid,
                  int ldr) {
   using CF = Cfg2<BN2>;
@@ -251,15 +251,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             }
           }
           if (rope_cols > 0 && n0 + c < rope_cols && row < M) {
-            // fused RoPE (rotate-half): this 64-column chunk is exactly one head of Q or K;
-            // r0 holds dims [0,32), r1 dims [32,64) of the row
             const int pr = rope_pos[row];
+            if (rope_hd == 64) {
+              // fused RoPE (rotate-half): this 64-column chunk is exactly one head of Q or K;
+              // r0 holds dims [0,32), r1 dims [32,64) of the row
 #pragma unroll
-            for (int k = 0; k < 32; ++k) {
-              const float2 cs = rope_cs_at(rope_cs, pr, k, 32);
-              const float a = __uint_as_float(r0[k]), b = __uint_as_float(r1[k]);
-              r0[k] = __float_as_uint(a * cs.x - b * cs.y);
-              r1[k] = __float_as_uint(b * cs.x + a * cs.y);
+              for (int k = 0; k < 32; ++k) {
+                const float2 cs = rope_cs_at(rope_cs, pr, k, 32);
+                const float a = __uint_as_float(r0[k]), b = __uint_as_float(r1[k]);
+                r0[k] = __float_as_uint(a * cs.x - b * cs.y);
+                r1[k] = __float_as_uint(b * cs.x + a * cs.y);
+              }
+            } else {
+              // 128-wide heads (heads start at multiples of 128 and BN2 is 128 or 256, so both halves
+              // of a head sit in this tile): this chunk is dims [0,64) or [64,128) of a head; the
+              // rotate-half partner is the other chunk, read from TMEM alongside
+              const bool first = ((n0 + c) & 64) == 0;
+              const int pc = first ? c + 64 : c - 64;
+              uint32_t p0[32], p1[32];
+              tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + as * BN2 + pc, p0);
+              tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + as * BN2 + pc + 32, p1);
+              tmem_ld_wait();
+              const float sg = first ? -1.f : 1.f;  // first half: x cos - x' sin; second: x cos + x' sin
+#pragma unroll
+              for (int k = 0; k < 32; ++k) {
+                const float2 c0 = rope_cs_at(rope_cs, pr, k, 64), c1 = rope_cs_at(rope_cs, pr, k + 32, 64);
+                r0[k] = __float_as_uint(__uint_as_float(r0[k]) * c0.x + sg * __uint_as_float(p0[k]) * c0.y);
+                r1[k] = __float_as_uint(__uint_as_float(r1[k]) * c1.x + sg * __uint_as_float(p1[k]) * c1.y);
+              }
             }
           }
           if (swiglu_out != nullptr && row < M && n0 + c < N) {
@@ -348,14 +367,14 @@ template <int BN2, bool A_MN, bool B_MN, int EPI>
 int launch2(const CUtensorMap& ma, const CUtensorMap& mbm, const CUtensorMap& mc, const CUtensorMap& mr, void* C,
             int M, int N, int K,
             int ldc, int splits, cudaStream_t st, const int32_t* rope_pos = nullptr, const float2* rope_cs = nullptr,
-            int rope_cols = 0, __nv_bfloat16* swiglu_out = nullptr, int ld_swiglu = 0,
+            int rope_cols = 0, int rope_hd = 64, __nv_bfloat16* swiglu_out = nullptr, int ld_swiglu = 0,
             const __nv_bfloat16* resid = nullptr, int ldr = 0) {
   constexpr int SMEM = Cfg2<BN2>::SMEM;
   if (ensure_smem<gemm2_kernel<BN2, A_MN, B_MN, EPI>>(SMEM)) return launch_status();
   const int units = ((M + 255) / 256) * ((N + BN2 - 1) / BN2) * splits;
   const int pairs = units < num_sms() / 2 ? units : num_sms() / 2;
   gemm2_kernel<BN2, A_MN, B_MN, EPI><<<2 * pairs, THREADS, SMEM, st>>>(ma, mbm, mc, mr, C, M, N, K, ldc, splits,
-                                                                        rope_pos, rope_cs, rope_cols, swiglu_out,
+                                                                        rope_pos, rope_cs, rope_cols, rope_hd, swiglu_out,
                                                                         ld_swiglu, resid, ldr);
   return launch_status();
 }
@@ -370,7 +389,7 @@ using namespace mb;
 static int gemm_impl(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K, int32_t lda,
                      int32_t ldb, int32_t ldc, int32_t a_mn, int32_t b_mn, int32_t epi, void* stream,
                      const int32_t* rope_pos, const float2* rope_cs, int rope_cols, void* swiglu_out = nullptr,
-                     int ld_swiglu = 0, const void* resid = nullptr, int ldr = 0);
+                     int ld_swiglu = 0, const void* resid = nullptr, int ldr = 0, int rope_hd = 64);
 
 MAESTRO_API int maestro_gemm_bf16(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K,
                                   int32_t lda, int32_t ldb, int32_t ldc, int32_t a_mn, int32_t b_mn, int32_t epi,
@@ -379,12 +398,15 @@ MAESTRO_API int maestro_gemm_bf16(const void* A, const void* B, void* C, int32_t
 }
 
 // Forward projection with RoPE fused into the epilogue: C = A B^T (bf16), then every
-// 64-column head in columns [0, rope_cols) is rotated (rotate-half) at position pos[row];
-// cos_sin[p][32] = (cos, sin).  Replaces the separate RoPE pass on the fused QKV output.
+// head_dim-column head (64 or 128) in columns [0, rope_cols) is rotated (rotate-half) at
+// position pos[row]; cos_sin is the position-tiled (cos, sin) table of head_dim/2 frequencies.
+// Replaces the separate RoPE pass on the fused QKV output.
 MAESTRO_API int maestro_gemm_bf16_rope(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K,
                                        int32_t lda, int32_t ldb, int32_t ldc, const int32_t* pos,
-                                       const void* cos_sin, int32_t rope_cols, void* stream) {
-  return gemm_impl(A, B, C, M, N, K, lda, ldb, ldc, 0, 0, 0, stream, pos, (const float2*)cos_sin, rope_cols);
+                                       const void* cos_sin, int32_t rope_cols, int32_t head_dim, void* stream) {
+  if ((head_dim != 64 && head_dim != 128) || rope_cols % head_dim) return (int)cudaErrorInvalidValue;
+  return gemm_impl(A, B, C, M, N, K, lda, ldb, ldc, 0, 0, 0, stream, pos, (const float2*)cos_sin, rope_cols,
+                   nullptr, 0, nullptr, 0, head_dim);
 }
 
 // Gate/up projection with SwiGLU fused into the epilogue: C = A B^T is the interleaved [g|u]
@@ -408,7 +430,7 @@ MAESTRO_API int maestro_gemm_bf16_swiglu(const void* A, const void* B, void* C, 
 static int gemm_impl(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K, int32_t lda,
                      int32_t ldb, int32_t ldc, int32_t a_mn, int32_t b_mn, int32_t epi, void* stream,
                      const int32_t* rope_pos, const float2* rope_cs, int rope_cols, void* swiglu_out,
-                     int ld_swiglu, const void* resid, int ldr) {
+                     int ld_swiglu, const void* resid, int ldr, int rope_hd) {
   if (M <= 0 || N <= 0 || K <= 0) return (int)cudaErrorInvalidValue;
   if ((lda % 8) || (ldb % 8) || (N % 8) || (ldc % 8)) return (int)cudaErrorInvalidValue;
   const int sms = num_sms();
@@ -430,11 +452,12 @@ static int gemm_impl(const void* A, const void* B, void* C, int32_t M, int32_t N
       const long long t192 = tm * ((N + 191) / 192);
       const long long c192 = (t192 + pairs - 1) / pairs;  // x 0.8 of a 256-wide tile
       const long long cur = bn2 == 256 ? 10 * c256 / 2 : 6 * c128;  // in tenths of a 256 tile
-      if (8 * c192 < cur) bn2 = 192;
+      // (not with 128-wide RoPE heads: both halves of a head must sit in one tile)
+      if (8 * c192 < cur && !(rope_cols > 0 && rope_hd == 128)) bn2 = 192;
     }
     if (const char* e = getenv("MAESTRO_GEMM_BN")) {  // experiments
       const int v = atoi(e);
-      bn2 = v == 128 ? 128 : (v == 192 && !b_mn) ? 192 : 256;
+      bn2 = v == 128 ? 128 : (v == 192 && !b_mn && !(rope_cols > 0 && rope_hd == 128)) ? 192 : 256;
     }
     int splits = 1;
     const int kb = (K + BK - 1) / BK;
@@ -471,7 +494,7 @@ static int gemm_impl(const void* A, const void* B, void* C, int32_t M, int32_t N
     ok = ok && (b_mn ? make_map_2d(&mbm, B, N, K, ldb, 64, 64) : make_map_2d(&mbm, B, K, N, ldb, 64, brows));
     if (!ok) return (int)cudaErrorInvalidValue;
 #define MB_GEMM2_LAUNCH(W, AM, BMN, E)                                                                  \
-  launch2<W, AM, BMN, E>(ma, mbm, mc, mr, C, M, N, K, ldc, splits, st, rope_pos, rope_cs, rope_cols,     \
+  launch2<W, AM, BMN, E>(ma, mbm, mc, mr, C, M, N, K, ldc, splits, st, rope_pos, rope_cs, rope_cols, rope_hd, \
                          (__nv_bfloat16*)swiglu_out, ld_swiglu, (const __nv_bfloat16*)resid, ldr)
 #define MB_GEMM2_CASE(AM, BMN, E)                                                                    \
   if (a_mn == AM && b_mn == BMN && epi_k == E)                                                       \

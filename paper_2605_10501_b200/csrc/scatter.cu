@@ -12,17 +12,26 @@ namespace mb {
 namespace {
 
 constexpr int kRowsPerWarp = 4;
+// pos != nullptr: the pair range is [pos[k0], pos[k1]) read on device (K5b handoff index of one
+// micro-batch), n_rows only bounds the grid
+template <bool ACC>
 __global__ void __launch_bounds__(256) scatter_rows_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
                                                            const int32_t* __restrict__ src_row,
                                                            const int32_t* __restrict__ dst_row, int n_rows,
-                                                           int vec_per_row) {
+                                                           int vec_per_row, const int32_t* __restrict__ pos, int k0,
+                                                           int k1) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  const int r0 = warp * kRowsPerWarp;
+  int lo = 0, hi = n_rows;
+  if (pos != nullptr) {
+    lo = pos[k0];
+    hi = pos[k1];
+  }
+  const int r0 = lo + warp * kRowsPerWarp;
 #pragma unroll
   for (int k = 0; k < kRowsPerWarp; ++k) {
     const int r = r0 + k;
-    if (r >= n_rows) return;
+    if (r >= hi) return;
     const uint4* s = src + (size_t)src_row[r] * vec_per_row;
     uint4* d = dst + (size_t)dst_row[r] * vec_per_row;
     for (int v0 = lane; v0 < vec_per_row; v0 += 4 * 32) {  // four 16-byte loads in flight per lane
@@ -37,7 +46,21 @@ __global__ void __launch_bounds__(256) scatter_rows_kernel(const uint4* __restri
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        if (v0 + u * 32 < vec_per_row) d[v0 + u * 32] = x[u];
+        if (v0 + u * 32 < vec_per_row) {
+          if constexpr (ACC) {  // dst += src (bf16 rows, fp32 sum rounded once)
+            uint4 y = d[v0 + u * 32];
+            __nv_bfloat162* yh = reinterpret_cast<__nv_bfloat162*>(&y);
+            const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&x[u]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 a = __bfloat1622float2(yh[e]), c = __bfloat1622float2(xh[e]);
+              yh[e] = __floats2bfloat162_rn(a.x + c.x, a.y + c.y);
+            }
+            d[v0 + u * 32] = y;
+          } else {
+            d[v0 + u * 32] = x[u];
+          }
+        }
     }
   }
 }
@@ -96,8 +119,27 @@ MAESTRO_API int maestro_scatter_rows_fwd(const void* d_src, void* d_dst, const i
   if (d % 8) return (int)cudaErrorInvalidValue;
   const int warps = (n_rows + kRowsPerWarp - 1) / kRowsPerWarp;
   const int blocks = (warps * 32 + 255) / 256;
-  scatter_rows_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>((const uint4*)d_src, (uint4*)d_dst, d_src_row,
-                                                                d_dst_row, n_rows, d / 8);
+  scatter_rows_kernel<false><<<blocks, 256, 0, (cudaStream_t)stream>>>((const uint4*)d_src, (uint4*)d_dst, d_src_row,
+                                                                       d_dst_row, n_rows, d / 8, nullptr, 0, 0);
+  return launch_status();
+}
+
+// Row scatter over the pairs [d_pos[k0], d_pos[k1]) of a handoff index (maestro_handoff_index):
+// the range stays on device; max_rows (>= the range length) sizes the grid.  accumulate != 0:
+// dst rows += src rows (a downstream section's gradient added into the backbone's).
+MAESTRO_API int maestro_scatter_rows_range(const void* d_src, void* d_dst, const int32_t* d_src_row,
+                                           const int32_t* d_dst_row, const int32_t* d_pos, int32_t k0, int32_t k1,
+                                           int32_t max_rows, int32_t d, int32_t accumulate, void* stream) {
+  if (max_rows <= 0 || k1 <= k0) return 0;
+  if (d % 8) return (int)cudaErrorInvalidValue;
+  const int warps = (max_rows + kRowsPerWarp - 1) / kRowsPerWarp;
+  const int blocks = (warps * 32 + 255) / 256;
+  if (accumulate)
+    scatter_rows_kernel<true><<<blocks, 256, 0, (cudaStream_t)stream>>>(
+        (const uint4*)d_src, (uint4*)d_dst, d_src_row, d_dst_row, max_rows, d / 8, d_pos, k0, k1);
+  else
+    scatter_rows_kernel<false><<<blocks, 256, 0, (cudaStream_t)stream>>>(
+        (const uint4*)d_src, (uint4*)d_dst, d_src_row, d_dst_row, max_rows, d / 8, d_pos, k0, k1);
   return launch_status();
 }
 

@@ -26,7 +26,7 @@ def _lib():
         I32, P = ctypes.c_int32, ctypes.c_void_p
         N.extra_symbols({
             "maestro_gemm_bf16": ([P, P, P, I32, I32, I32, I32, I32, I32, I32, I32, I32, P], ctypes.c_int),
-            "maestro_gemm_bf16_rope": ([P, P, P, I32, I32, I32, I32, I32, I32, P, P, I32, P], ctypes.c_int),
+            "maestro_gemm_bf16_rope": ([P, P, P, I32, I32, I32, I32, I32, I32, P, P, I32, I32, P], ctypes.c_int),
             "maestro_gemm_bf16_swiglu": ([P, P, P, I32, I32, I32, I32, I32, I32, P, I32, P], ctypes.c_int),
             "maestro_gemm_bf16_residual": ([P, P, P, I32, I32, I32, I32, I32, I32, P, I32, P], ctypes.c_int),
         })
@@ -66,8 +66,9 @@ def linear_fwd(x: torch.Tensor, w: torch.Tensor, out: torch.Tensor | None = None
 
 
 def linear_fwd_rope(x: torch.Tensor, w: torch.Tensor, pos: torch.Tensor, cos_sin: torch.Tensor, rope_cols: int,
-                    out: torch.Tensor | None = None) -> torch.Tensor:
-    """qkv = x @ w^T with RoPE applied to the first ``rope_cols`` columns inside the GEMM epilogue."""
+                    out: torch.Tensor | None = None, head_dim: int = 64) -> torch.Tensor:
+    """qkv = x @ w^T with RoPE applied to the ``head_dim``-wide heads (64 or 128) of the first
+    ``rope_cols`` columns inside the GEMM epilogue."""
     T, K = x.shape
     Nn = w.shape[0]
     if out is None:
@@ -77,7 +78,8 @@ def linear_fwd_rope(x: torch.Tensor, w: torch.Tensor, pos: torch.Tensor, cos_sin
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
     rc = _lib().maestro_gemm_bf16_rope(N.ptr(x), N.ptr(w), N.ptr(out), T, Nn, K, x.stride(0), w.stride(0),
-                                       out.stride(0), N.ptr(pos), N.ptr(cos_sin), rope_cols, N.stream_ptr())
+                                       out.stride(0), N.ptr(pos), N.ptr(cos_sin), rope_cols, head_dim,
+                                       N.stream_ptr())
     N.check(rc, "gemm_bf16_rope")
     if rec is not None:
         e1.record()

@@ -126,7 +126,7 @@ class KDExecutor:
     def __init__(self, n_gpus: int = 1, batch_per_rank: int = 64, seq: int = R.KD_SEQ, mbs: int = 4,
                  teacher: str = "kd_teacher_1b", student: str = "kd_student_125m", seed: int = 0,
                  lr: float = 3e-4, policy=ExecPolicy.INTERLEAVED, device=None, layout: str = "colocated",
-                 teacher_mbs: int | None = None):
+                 teacher_mbs: int | None = None, recipe: str = "kd"):
         dist = _dist()
         self.rank = dist.get_rank() if dist else 0
         self.world = dist.get_world_size() if dist else 1
@@ -144,7 +144,8 @@ class KDExecutor:
         dp_s, dp_t, f_t, colocated = R.kd_layout(n_gpus, layout)
         self.layout = "colocated" if colocated else "disjoint"
         self.batch = batch_per_rank * dp_s
-        self.recipe = R.kd(n_gpus, self.batch, seq, self.layout)
+        # cfg 2 (recipes.kd) or cfg 5 (recipes.kd_8b): same graph shape, different cost knobs
+        self.recipe = (R.kd_8b if recipe == "kd_8b" else R.kd)(n_gpus, self.batch, seq, self.layout)
         cfg = {"student": self.recipe.configs["student"].__class__(dp=dp_s, mbs=mbs),
                "teacher": self.recipe.configs["teacher"].__class__(dp=dp_t, fanout=f_t, mbs=self.mbs_t)}
         self.configs = cfg
@@ -268,6 +269,11 @@ class KDExecutor:
                 a.copy_(v["mb_tok"], non_blocking=True)
                 b.copy_(v["mb_start"], non_blocking=True)
                 bufs[k] = (a, b)
+            # the K1-K4 device error word travels with the readback: an invalid batch raises the
+            # reference's exception class before any micro-batch is built (scheduling.py:217-365)
+            err = torch.empty(1, dtype=torch.int64).pin_memory()
+            err.copy_(self.planner.err, non_blocking=True)
+            bufs["_err"] = err
             ev = torch.cuda.Event()
             ev.record(stream)
         return plan, bufs, ev, (p0, p1)
@@ -291,7 +297,10 @@ class KDExecutor:
         # one small readback per step: micro-batch token counts of the local rank orders
         plan_ev.synchronize()
         main.wait_event(plan_ev)
-        host = {k: (a.tolist(), b.tolist()) for k, (a, b) in bufs.items()}
+        err = int(bufs["_err"].item())
+        if err != N.ERR_CLEAN:
+            N.raise_device_error(err, self.planner.ids[: self.batch].tolist(), self.graph.tables.section_ids)
+        host = {k: (a.tolist(), b.tolist()) for k, (a, b) in bufs.items() if k != "_err"}
         packed = {}
         with torch.cuda.stream(main):
             for sec, v in plan.items():
@@ -309,7 +318,7 @@ class KDExecutor:
         loss_acc = None
         if self.student is not None:
             loss_acc = torch.zeros(1, device=dev, dtype=torch.float32)
-            self.student.p.zero_grad() if self.step_idx == 0 or True else None
+            self.student.p.zero_grad()
         global_tokens = float(self.batch * self.seq)
         if self.colocated:
             self._run_colocated(plan, host, packed, ready, clock, loss_acc, global_tokens)
@@ -545,6 +554,29 @@ class KDExecutor:
         return rep.makespan, rep.critical_idle, span, span - busy
 
     # ------------------------------------------------------------------ accounting
+    def attention_flops_per_step(self) -> tuple[float, float]:
+        """Algorithmic attention FLOPs of one step over the whole job: (forward launches, backward
+        launches) -- forward = teacher + student, 4*H*dh*L^2/2 per causal sequence per layer;
+        backward = 2.5x the student's forward."""
+        L = self.seq
+        per = lambda s: s.layers * 4.0 * s.heads * s.head_dim * L * L * 0.5  # noqa: E731
+        fwd = self.batch * (per(self.tshape) + per(self.sshape))
+        return fwd, self.batch * 2.5 * per(self.sshape)
+
+    def kd_loss_bytes_per_step(self) -> float:
+        """Algorithmic bytes of K9 per step: read teacher + student logits, write dlogits (bf16)."""
+        return self.batch * self.seq * self.tshape.vocab * 2.0 * 3
+
+    def readback_bytes_per_step(self) -> int:
+        """D2H bytes of one step on a student rank: the plan readback (micro-batch token counts and
+        starts, int32, per hosted section) + the 8-byte error word + the fp32 loss."""
+        n = 0
+        for sec, rank in (("student", self.s_rank), ("teacher", self.t_rank)):
+            if rank is not None:
+                per = self.batch // (self.dp_s if sec == "student" else self.dp_t)
+                n += 2 * 4 * (-(-per // self.mbs_of[sec]))
+        return n + 8 + 4
+
     def model_flops_per_step(self) -> float:
         """Algorithmic FLOPs of one step over the whole job (teacher fwd + head, student train)."""
         s, t, L = self.sshape, self.tshape, self.seq

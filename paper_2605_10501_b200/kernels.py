@@ -11,6 +11,7 @@ import ctypes
 import torch
 
 from . import _native as N
+from . import instrument
 
 _P, _I32, _I64, _F = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_float
 _SIGS = {
@@ -126,9 +127,11 @@ def adamw(p, g, m, v, pb, lr, step, b1=0.9, b2=0.95, eps=1e-8, wd=0.1, gscale=1.
 def kd_loss(t_logits, s_logits, ds, loss, grad_scale, tau=1.0):
     """Fused full-vocab KL(teacher || student) per token + d/ds (K9).  ds may be s_logits."""
     T, V = s_logits.shape
+    tok = instrument.begin("kd_loss", 2.0 * T * V * (3 if ds is not None else 2))  # read t, s (+ write ds)
     N.check(L().maestro_kd_loss_fwd_bwd(_p(t_logits), _p(s_logits), _p(ds), _p(loss), T, V, t_logits.stride(0),
                                         s_logits.stride(0), ds.stride(0) if ds is not None else 8, grad_scale,
                                         1.0 / tau, _s()), "kd_loss")
+    instrument.end(tok)
 
 
 def ce_loss(logits, labels, ds, loss, grad_scale):

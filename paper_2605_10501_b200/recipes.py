@@ -243,10 +243,14 @@ def kd_8b_graph() -> SectionGraph:
 KD8B_LAYOUTS = {1: (1, 1, 1), 2: (1, 1, 1), 4: (2, 2, 1), 8: (4, 4, 1)}
 
 
-def kd_8b(n_gpus: int = 8, batch: int = 32, seq: int = 8192) -> Recipe:
-    """cfg 5: Llama-3-8B teacher -> Llama-3.2-1B student, 8k seq, disjoint GPU groups."""
+def kd_8b(n_gpus: int = 8, batch: int = 32, seq: int = 8192, layout: str = "disjoint") -> Recipe:
+    """cfg 5: Llama-3-8B teacher -> Llama-3.2-1B student, 8k seq, disjoint GPU groups (the
+    co-located layout puts a teacher and a student rank on every GPU, as for cfg 2)."""
     g = kd_8b_graph()
-    dp_s, dp_t, f_t = KD8B_LAYOUTS[n_gpus]
+    if layout == "colocated" or n_gpus == 1:
+        dp_s, dp_t, f_t = n_gpus, n_gpus, 1
+    else:
+        dp_s, dp_t, f_t = KD8B_LAYOUTS[n_gpus]
     configs = {"student": SectionConfig(dp=dp_s), "teacher": SectionConfig(dp=dp_t, fanout=f_t)}
     params = {
         "teacher": CostParams(flops_per_token_fwd=2.0 * 7.5e9 + 4 * 32 * 4096 * seq / 2,

@@ -38,6 +38,20 @@ class Shape:
     eps: float = 1e-5
     rope_base: float = 10000.0
     causal: bool = True
+    # zero-padded layouts (exactly equivalent to the unpadded model): a true head size below
+    # head_dim (Qwen2.5-VL ViT: 80 in a 128-wide head, laid out [h/2 real | pad | h/2 real | pad]
+    # so rotate-half pairs never mix real and pad dims) and a true FFN width below ffn (3420 in
+    # 3456: TMA row pitches are 16-byte multiples and the SwiGLU epilogue works on 32-feature blocks)
+    head_dim_true: int = 0
+    ffn_true: int = 0
+
+    @property
+    def hd_true(self) -> int:
+        return self.head_dim_true or self.head_dim
+
+    @property
+    def ffn_real(self) -> int:
+        return self.ffn_true or self.ffn
 
     @property
     def qkv_dim(self) -> int:
@@ -61,8 +75,10 @@ class Shape:
 
     def fwd_flops_per_token(self, seq_len: int, with_head: bool = True) -> float:
         """Model FLOPs of one forward token (GEMMs + causal attention at seq_len)."""
-        lin = self.layers * (self.d * self.qkv_dim + self.heads * self.head_dim * self.d + 3 * self.d * self.ffn)
-        attn = self.layers * 4 * self.heads * self.head_dim * seq_len * (0.5 if self.causal else 1.0)
+        hd, F = self.hd_true, self.ffn_real  # algorithmic FLOPs of the unpadded model
+        lin = self.layers * (self.d * (self.heads + 2 * self.kv_heads) * hd + self.heads * hd * self.d
+                             + 3 * self.d * F)
+        attn = self.layers * 4 * self.heads * hd * seq_len * (0.5 if self.causal else 1.0)
         head = self.vocab * self.d if with_head else 0
         return 2.0 * (lin + head) + attn
 
@@ -74,8 +90,15 @@ SHAPES = {
     # cfg 1: 2-layer GPT backbone (d=768) and ViT-tiny encoder (bidirectional, no vocab)
     "vlm_gpt2l": Shape(d=768, layers=2, heads=12, kv_heads=12, ffn=3072, vocab=32768),
     "vit_tiny": Shape(d=192, layers=12, heads=3, kv_heads=3, ffn=768, vocab=8, causal=False),
+    # cfg 5: Llama-3-8B-shaped teacher (head_dim 128, GQA 32/8), Llama-3.2-1B-shaped student (tied)
+    "llama3_8b": Shape(d=4096, layers=32, heads=32, kv_heads=8, ffn=14336, vocab=128256, head_dim=128,
+                       rope_base=500000.0),
+    "llama32_1b": Shape(d=2048, layers=16, heads=32, kv_heads=8, ffn=8192, vocab=128256, tied=True,
+                        rope_base=500000.0),
     # tiny shapes for tests
     "test_tiny": Shape(d=128, layers=2, heads=2, kv_heads=1, ffn=256, vocab=512),
+    "test_tiny_hd128": Shape(d=256, layers=2, heads=4, kv_heads=2, ffn=512, vocab=512, head_dim=128,
+                             rope_base=500000.0),
 }
 
 
@@ -154,16 +177,52 @@ class FlatParams:
         self.refresh_transposed()
 
 
-def rope_table(max_pos: int, head_dim: int, base: float, device) -> torch.Tensor:
+def rope_table(max_pos: int, head_dim: int, base: float, device, true_dim: int = 0) -> torch.Tensor:
     """(cos, sin) of every (position, frequency) in the position-tiled layout the kernels read:
     [ceil(P/32)][head_dim/2][32 positions][2] fp32 (include/maestro_b200.h).  A warp's 32 rows
-    are 32 consecutive positions, so each per-frequency read is one contiguous 256-byte segment."""
+    are 32 consecutive positions, so each per-frequency read is one contiguous 256-byte segment.
+    ``true_dim`` < head_dim (zero-padded heads): pair i < true_dim/2 gets the true model's
+    frequency base^(-2i/true_dim); the pad pairs get frequency 0 (identity rotation of zeros)."""
     half = head_dim // 2
     P = (max_pos + 31) // 32 * 32
-    inv = base ** (-torch.arange(0, head_dim, 2, dtype=torch.float64) / head_dim)
+    td = true_dim or head_dim
+    inv = base ** (-torch.arange(0, head_dim, 2, dtype=torch.float64) / td)
+    inv[td // 2:] = 0.0
     ang = torch.arange(P, dtype=torch.float64)[:, None] * inv[None, :]  # [P, half]
     cs = torch.stack([ang.cos(), ang.sin()], -1).to(torch.float32)      # [P, half, 2]
     return cs.view(P // 32, 32, half, 2).transpose(1, 2).contiguous().to(device)
+
+
+def pad_masks(shape: Shape, device):
+    """Boolean masks of the padding of a zero-padded shape: (qkv rows [qkv_dim], wo columns
+    [H*dh], gate/up rows [2F], wd columns [F]); True = pad (always zero)."""
+    dh, ht = shape.head_dim, shape.hd_true // 2
+    j = torch.arange(dh, device=device)
+    head_pad = (j % (dh // 2)) >= ht  # [real h/2 | pad | real h/2 | pad]
+    qkv = head_pad.repeat(shape.heads + 2 * shape.kv_heads)
+    wo = head_pad.repeat(shape.heads)
+    f = torch.arange(shape.ffn, device=device)
+    fpad = f >= shape.ffn_real
+    gu = torch.empty(2 * shape.ffn, dtype=torch.bool, device=device)
+    gi = (f // 32) * 64 + f % 32  # gate row of feature f; its up row is gi + 32
+    gu[gi] = fpad
+    gu[gi + 32] = fpad
+    return qkv, wo, gu, fpad
+
+
+def zero_padding(shape: Shape, p: "FlatParams") -> None:
+    """Zero the pad rows / columns of every layer (master, working copy, transposed copies).
+    Their gradients are exactly zero (the pad activations are zero and feed nothing), so AdamW
+    keeps them at zero and the padded model stays equivalent to the unpadded one."""
+    qkv, wo, gu, fpad = pad_masks(shape, p.w.device)
+    bufs = [p.w] + ([p.master] if p.master is not None else [])
+    for i in range(shape.layers):
+        for buf in bufs:
+            p._view(buf, f"l{i}.wqkv")[qkv] = 0
+            p._view(buf, f"l{i}.wo")[:, wo] = 0
+            p._view(buf, f"l{i}.wgu")[gu] = 0
+            p._view(buf, f"l{i}.wd")[:, fpad] = 0
+    p.refresh_transposed()
 
 
 @dataclass
@@ -187,12 +246,15 @@ class Transformer:
         self.s = shape
         self.p = params
         self.device = device
-        self.cs = rope_table(max_pos, shape.head_dim, shape.rope_base, device)
-        self.scale = 1.0 / math.sqrt(shape.head_dim)
+        self.cs = rope_table(max_pos, shape.head_dim, shape.rope_base, device, shape.hd_true)
+        self.scale = 1.0 / math.sqrt(shape.hd_true)
+        if shape.hd_true != shape.head_dim or shape.ffn_real != shape.ffn:
+            zero_padding(shape, params)
 
     # -------------------------------------------------------------------- forward
-    def forward(self, b: Batch, x0: torch.Tensor | None = None, save: bool = True):
-        """Returns (yf [T, d] final-normed hidden, ctx for backward).  x0 overrides the embedding."""
+    def forward(self, b: Batch, x0: torch.Tensor | None = None, save: bool = True, yf_out: torch.Tensor | None = None):
+        """Returns (yf [T, d] final-normed hidden, ctx for backward).  x0 overrides the embedding;
+        ``yf_out`` receives the final hidden state (e.g. rows of a handoff buffer)."""
         s, p, T = self.s, self.p, b.T
         dev, bf = self.device, torch.bfloat16
         if x0 is None:
@@ -207,7 +269,7 @@ class Transformer:
             r1 = torch.empty(T, device=dev, dtype=torch.float32)
             K.add_rmsnorm(h1, None, h1, y1, p[f"l{i}.ln1"], r1, s.eps)
             # QKV projection with RoPE fused into the GEMM epilogue (one head per 64-col chunk)
-            qkv = D.linear_fwd_rope(y1, p[f"l{i}.wqkv"], b.pos, self.cs, (H + Hk) * dh)
+            qkv = D.linear_fwd_rope(y1, p[f"l{i}.wqkv"], b.pos, self.cs, (H + Hk) * dh, head_dim=dh)
             q = qkv[:, : H * dh].view(T, H, dh)
             k = qkv[:, H * dh: (H + Hk) * dh].view(T, Hk, dh)
             v = qkv[:, (H + Hk) * dh:].view(T, Hk, dh)
@@ -227,7 +289,7 @@ class Transformer:
             # next block's residual stream: h2 + sw Wd^T
             x = D.linear_fwd_residual(sw, p[f"l{i}.wd"], h2)
         hf = x
-        yf = torch.empty(T, s.d, device=dev, dtype=bf)
+        yf = torch.empty(T, s.d, device=dev, dtype=bf) if yf_out is None else yf_out
         rf = torch.empty(T, device=dev, dtype=torch.float32)
         K.add_rmsnorm(hf, None, hf, yf, p["lnf"], rf, s.eps)
         ctx["final"] = (hf, rf, yf)
@@ -241,8 +303,10 @@ class Transformer:
 
     # -------------------------------------------------------------------- backward
     def backward(self, ctx, dlogits: torch.Tensor | None = None, dyf: torch.Tensor | None = None,
-                 need_dx0: bool = False):
-        """Accumulates parameter grads (fp32) from dlogits (or dyf); returns dx0 if asked."""
+                 need_dx0: bool = False, dyf_hook=None):
+        """Accumulates parameter grads (fp32) from dlogits (or dyf); returns dx0 if asked.
+        ``dyf_hook(dyf)`` may add further gradient into the final hidden state's gradient (e.g. a
+        downstream section's) before the stack's backward."""
         s, p, b = self.s, self.p, ctx["b"]
         T, dev, bf = b.T, self.device, torch.bfloat16
         H, Hk, dh = s.heads, s.kv_heads, s.head_dim
@@ -251,6 +315,8 @@ class Transformer:
             hw = "embed" if s.tied else "head"
             dyf = D.linear_dgrad(dlogits, p[hw], wt=p.t(hw))
             D.linear_wgrad(dlogits, yf, p.g(hw))
+        if dyf_hook is not None:
+            dyf_hook(dyf)
         dh_ = torch.empty(T, s.d, device=dev, dtype=bf)
         K.rmsnorm_bwd(dyf, hf, p["lnf"], rf, None, dh_, p.g("lnf"))
         for i in reversed(range(s.layers)):

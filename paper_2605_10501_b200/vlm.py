@@ -165,6 +165,7 @@ class VLMExecutor:
         n_sec = len(self.graph.tables.section_ids)
         self._h_orders = torch.empty(n_sec * batch, dtype=torch.int32).pin_memory()
         self._h_off = torch.empty(n_sec * W, dtype=torch.int32).pin_memory()
+        self._h_err = torch.empty(1, dtype=torch.int64).pin_memory()
         self._pending = None  # (host batch, readback event, live inputs) of a plan enqueued ahead
         self.s_llm = torch.cuda.Stream(device=dev)
         self.s_vit = torch.cuda.Stream(device=dev)
@@ -186,6 +187,7 @@ class VLMExecutor:
             self.planner.plan_tokens(self.cost, tokens, B, stream)
             self._h_orders.copy_(self.planner.orders[: self._h_orders.numel()], non_blocking=True)
             self._h_off.copy_(self.planner.sec_off, non_blocking=True)
+            self._h_err.copy_(self.planner.err, non_blocking=True)  # K1-K4 error word
             ev = torch.cuda.Event()
             ev.record(stream)
         return ev, (tokens, ids)
@@ -209,6 +211,10 @@ class VLMExecutor:
         if self._pending is not None and self._pending[0] is hb:
             ev = self._pending[1]
         else:
+            if self._pending is not None:
+                # a plan for another batch is in flight on s_plan and writes the same planner and
+                # pinned buffers: let it land before re-planning on the main stream
+                self._pending[1].synchronize()
             ev, live = self._plan(hb, main)
         self._pending = None
         tab = self.graph.tables
@@ -216,6 +222,9 @@ class VLMExecutor:
         W = N.MAX_DP + 1
         # one small readback: both rank orders (<= 2 x 64 ints) define the micro-batch plan
         ev.synchronize()
+        err = int(self._h_err.item())
+        if err != N.ERR_CLEAN:
+            N.raise_device_error(err, list(range(B)), self.graph.tables.section_ids)
         orders = self._h_orders.numpy().reshape(-1, B)
         off = self._h_off.numpy().reshape(-1, W)
         o_llm = orders[ci, :B].copy()
@@ -457,7 +466,9 @@ class VLMGroupExecutor:
         self.sec_group = g_llm if self.role == "llm" else g_vit
         self.chan_fwd, self.chan_bwd = {}, {}
         nvlink = handoff_mode() == "nvlink"
-        slot = self.mbs_vit * 49 * self.llm_shape.d * 2 + (1 << 16)  # largest fragment of a pair
+        # largest fragment of a pair: a ViT micro-batch's images forward, an LLM micro-batch's
+        # image rows backward
+        slot = max(self.mbs_vit, self.mbs_llm) * 49 * self.llm_shape.d * 2 + (1 << 16)
 
         def transport(peer, group, role):
             if nvlink:  # one-sided copy-engine puts into the receiver's slot ring (csrc/p2p.cu)

@@ -71,3 +71,45 @@ def test_attention_fwd_bwd(lens, H, Hk, causal, use_plan):
     assert rel(dk, kf.grad) < 3e-2
     assert rel(dq, qf.grad) < 3e-2
     assert torch.all(dqkv[:, (H + 2 * Hk) * dh:] == 0)  # pitch padding untouched
+
+
+CASES_128 = [
+    ([128], 2, 1, True), ([1, 127, 128, 129, 300], 4, 2, True), ([8192], 4, 1, True),
+    ([196, 1024, 77], 4, 4, False), ([2048, 2048], 8, 2, True),
+]
+
+
+@pytest.mark.parametrize("lens,H,Hk,causal", CASES_128)
+def test_attention_fwd_bwd_hd128(lens, H, Hk, causal):
+    """head_dim 128 (Llama-3-8B teacher, Qwen2.5 backbone): forward + LSE + backward vs fp32."""
+    from paper_2605_10501_b200 import attention as A
+
+    torch.manual_seed(sum(lens) + 7 * H)
+    dh = 128
+    T = sum(lens)
+    cu = torch.tensor([0] + list(torch.tensor(lens).cumsum(0)), dtype=torch.int32, device="cuda")
+    W = (H + 2 * Hk) * dh + 64
+    qkv = torch.randn(T, W, device="cuda").bfloat16()
+    q = qkv[:, : H * dh].view(T, H, dh)
+    k = qkv[:, H * dh: (H + Hk) * dh].view(T, Hk, dh)
+    v = qkv[:, (H + Hk) * dh: (H + 2 * Hk) * dh].view(T, Hk, dh)
+    scale = 1.0 / math.sqrt(dh)
+    o = torch.empty(T, H, dh, device="cuda", dtype=torch.bfloat16)
+    lse = A.attn_fwd(q, k, v, cu, max(lens), causal, o, scale, plan=A.plan(cu, T))
+    qf, kf, vf = (x.float().clone().requires_grad_(True) for x in (q, k, v))
+    ref = R.varlen_attention(qf, kf, vf, cu, causal, scale)
+    assert rel(o, ref) < 2e-2
+    assert (lse - ref_lse(q, k, cu, causal, scale)).abs().max().item() < 1e-3
+    if T > 4096:
+        return  # the fp32 autograd reference of an 8k sequence does not fit the test budget
+    do = torch.randn(T, H, dh, device="cuda").bfloat16()
+    ref.backward(do.float())
+    dqkv = torch.zeros_like(qkv)
+    dq = dqkv[:, : H * dh].view(T, H, dh)
+    dk = dqkv[:, H * dh: (H + Hk) * dh].view(T, Hk, dh)
+    dv = dqkv[:, (H + Hk) * dh: (H + 2 * Hk) * dh].view(T, Hk, dh)
+    A.attn_bwd(do, q, k, v, o, lse, cu, max(lens), causal, dq, dk, dv, scale, plan=A.plan(cu, T))
+    assert rel(dv, vf.grad) < 2e-2
+    assert rel(dk, kf.grad) < 3e-2
+    assert rel(dq, qf.grad) < 3e-2
+    assert torch.all(dqkv[:, (H + 2 * Hk) * dh:] == 0)  # pitch padding untouched

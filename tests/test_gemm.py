@@ -197,3 +197,22 @@ def test_swiglu_without_gu_store(T, F, K):
     gi = R.gate_index(F, "cuda")
     sref = torch.nn.functional.silu(gref[:, gi]) * gref[:, gi + 32]
     assert _rel(s, sref) < 2e-2
+
+
+def test_rope_epilogue_hd128():
+    """RoPE over 128-wide heads (pairs (i, i+64), 64 frequencies) in the GEMM epilogue."""
+    from oracle import torch_ref as R
+    from paper_2605_10501_b200 import dense
+    from paper_2605_10501_b200.transformer import rope_table
+
+    torch.manual_seed(12)
+    for T, H in ((1000, 5), (4096, 12)):
+        K = 1024
+        x = torch.randn(T, K, device="cuda").bfloat16()
+        w = torch.randn(H * 128 + 256, K, device="cuda").bfloat16()
+        pos = torch.randint(0, 8192, (T,), device="cuda", dtype=torch.int32)
+        cs = rope_table(8192, 128, 500000.0, "cuda")
+        y = dense.linear_fwd_rope(x, w, pos, cs, H * 128, head_dim=128)
+        ref = x.float() @ w.float().t()
+        rot = R.rope(ref[:, : H * 128].view(T, H, 128), pos, 500000.0).view(T, H * 128)
+        assert _rel(y[:, : H * 128], rot) < 1e-2 and _rel(y[:, H * 128:], ref[:, H * 128:]) < 8e-3

@@ -134,14 +134,15 @@ def _tiny_model(seed=0, shape_name="test_tiny"):
     return shape, Transformer(shape, p, torch.device("cuda"), max_pos=1024)
 
 
+@pytest.mark.parametrize("shape_name", ["test_tiny", "test_tiny_hd128"])
 @pytest.mark.parametrize("causal", [True, False])
-def test_transformer_fwd_bwd_vs_fp32(causal):
+def test_transformer_fwd_bwd_vs_fp32(causal, shape_name):
     import dataclasses
 
     from paper_2605_10501_b200 import kernels as K
     from paper_2605_10501_b200.transformer import Batch, SHAPES, FlatParams, Transformer
 
-    shape = dataclasses.replace(SHAPES["test_tiny"], causal=causal)
+    shape = dataclasses.replace(SHAPES[shape_name], causal=causal)
     p = FlatParams(shape.param_shapes(), torch.device("cuda"), trainable=True, seed=3)
     model = Transformer(shape, p, torch.device("cuda"), max_pos=1024)
     lens = [100, 37, 256, 1]
@@ -283,3 +284,25 @@ def test_kd_plan_ahead_matches_synchronous_plan():
     assert all(abs(a - b) <= 1e-6 * abs(a) for a, b in zip(out[0][0], out[1][0]))
     assert ((out[0][1] - out[1][1]).abs().max() / out[0][1].abs().max()).item() < 1e-5
     assert out[1][2] > 0
+
+
+def test_kd_executor_hd128_teacher_matches_reference():
+    """KD step with a head_dim-128 GQA teacher (the cfg 5 teacher's attention / RoPE shape) ==
+    fp32 autograd restatement (loss + student grads)."""
+    from paper_2605_10501_b200.executor import KDExecutor, synthetic_ids
+
+    ex = KDExecutor(n_gpus=1, batch_per_rank=4, seq=256, mbs=2, teacher="test_tiny_hd128", student="test_tiny",
+                    lr=0.0)
+    ids = torch.from_numpy(synthetic_ids(4, 256, 512, seed=15)).cuda()
+    t_flat = ex.teacher.p.w.float()
+    s_flat = ex.student.p.w.float()
+    st = ex.step(ids)
+    cu = torch.arange(0, 4 * 256 + 1, 256, dtype=torch.int32, device="cuda")
+    tok, grad = R.kd_step_reference(ex.tshape, ex.sshape, t_flat, s_flat, ex.t_head.float(), ids.reshape(-1), cu,
+                                    global_tokens=4 * 256)
+    ref_loss = tok.sum().item() / (4 * 256)
+    assert abs(st.loss - ref_loss) / max(abs(ref_loss), 1e-6) < 3e-2
+    got = R.param_views(ex.sshape, ex.student.p.grad)
+    want = R.param_views(ex.sshape, grad)
+    for name in ("embed", "lnf", "l0.wqkv", "l1.wd"):
+        assert rel(got[name], want[name]) < 6e-2, name
