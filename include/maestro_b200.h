@@ -66,6 +66,10 @@ typedef struct {
   int32_t mbs[MAESTRO_MAX_SECTIONS];
   uint32_t sec_bits[MAESTRO_MAX_SECTIONS];     /* submodule bits owned by each section */
   int32_t crit_bit;                            /* bit of the critical section's own id */
+  int32_t par_up;                              /* NOT IN REF: 1 = a sample may activate several
+                                                  upstream sections (parallel resources):
+                                                  t_f_bc/t_b_ac = max over them, the sample joins
+                                                  each one's order; 0 = reference behaviour */
 } maestro_graph_t;
 
 /* Reset a device error word to "no error" (INT64_MAX). */

@@ -120,12 +120,17 @@ def merge_fanout(lists, fanout):
     return out
 
 
-def resolve(act_masks, times: np.ndarray, sub_owner, side, up_candidates, down_candidates):
+MAX_SECTIONS = 16
+
+
+def resolve(act_masks, times: np.ndarray, sub_owner, side, up_candidates, down_candidates,
+            parallel_upstream: bool = False):
     """workload.py:297-355 over submodule bitmasks (bit order = sorted names).
 
     Returns (up_sec, down_sec) arrays of section indices (-1 = none) or raises
     ``ValueError((code, batch_index))`` with the reference's error: 2 =
-    BothActivated, 3 = ActivationError.
+    BothActivated, 3 = ActivationError.  ``parallel_upstream`` (extension, not in the
+    reference): several upstream sections resolve to MAX_SECTIONS + their section mask.
     """
     B = times.shape[1]
     up_out = np.full(B, -1, dtype=np.int32)
@@ -144,14 +149,16 @@ def resolve(act_masks, times: np.ndarray, sub_owner, side, up_candidates, down_c
                 ups.append(o)
             elif side[o] == 2:
                 downs.append(o)
-        if len(set(ups)) > 1 or len(set(downs)) > 1:
+        if (len(set(ups)) > 1 and not parallel_upstream) or len(set(downs)) > 1:
             raise ValueError((3, i))
         up_t = times[0, i] + times[5, i]
         down_t = times[2, i] + times[3, i]
         for t_side, decl, pool, out in ((up_t, ups, up_candidates, up_out), (down_t, downs, down_candidates, down_out)):
             if t_side <= 0:
                 continue
-            if decl:
+            if len(set(decl)) > 1:
+                out[i] = MAX_SECTIONS + sum(1 << x for x in set(decl))
+            elif decl:
                 out[i] = decl[0]
             elif len(pool) == 1:
                 out[i] = pool[0]
@@ -188,6 +195,71 @@ def build_schedule(times, ids, up_sec, down_sec, n_sec, critical, dp, fanout, ne
             o, c = off[s * max_dp + q], cnt[s * max_dp + q]
             out[(s, q)] = orders[s * B + o: s * B + o + c].tolist()
     return out, int(ev.value)
+
+
+def sample_times(cost, tokens, sub_owner, side, crit_bit, parallel_upstream=False):
+    """K1 restatement (costs.py:105-123 estimate_step_time, :182-200 per_sample_times, :264-286
+    derive_batch's per-side sums) over the device cost table [n_bits, 8] and token counts
+    [n_bits, B] -> (times [6, B] phase-major, activation masks [B]).  ``parallel_upstream``
+    (extension, not in the reference): the upstream phases are the max over the activated
+    upstream sections instead of their sum (identical when at most one is activated)."""
+    cost = np.asarray(cost, dtype=np.float64)
+    tokens = np.asarray(tokens, dtype=np.int64)
+    n_bits, B = tokens.shape
+    crit_owner = sub_owner[crit_bit]
+    act = np.zeros(B, dtype=np.uint32)
+    cnt = {}
+    for i in range(B):
+        secs = set()
+        for b in range(n_bits):
+            if sub_owner[b] == crit_owner:
+                continue
+            if tokens[b, i] > 0:
+                act[i] |= np.uint32(1 << b)
+                secs.add(sub_owner[b])
+        for s_ in secs:
+            cnt[s_] = cnt.get(s_, 0) + 1
+
+    def pst(row, tok, n):
+        fpt, eff, ratio, fwd_only, mbs, pp = row[0], row[1], row[2], row[3] != 0.0, int(row[4]), int(row[5])
+        if n <= 0:
+            return 0.0, 0.0
+        fwd = float(mbs * int(tok)) * fpt / eff
+        bwd = 0.0 if fwd_only else fwd * ratio
+        m = (n + mbs - 1) // mbs
+        sc = float(m + pp - 1) / float(m * pp * mbs)
+        return fwd * sc, bwd * sc
+
+    times = np.zeros((6, B), dtype=np.float64)
+    crow = cost[crit_bit]
+    dpc = int(crow[6])
+    n_crit = (B + dpc - 1) // dpc
+    for i in range(B):
+        t = [0.0] * 6
+        t[1], t[4] = pst(crow, tokens[crit_bit, i], n_crit)
+        upf, upb = {}, {}
+        for b in range(n_bits):
+            if not (int(act[i]) >> b) & 1:
+                continue
+            s_ = sub_owner[b]
+            row = cost[b]
+            dps = int(row[6])
+            n_aux = (cnt[s_] + dps - 1) // dps if cnt.get(s_, 0) > 0 else 0
+            f, bw = pst(row, tokens[b, i], n_aux)
+            if side[s_] == 0 and parallel_upstream:
+                upf[s_] = upf.get(s_, 0.0) + f
+                upb[s_] = upb.get(s_, 0.0) + bw
+            elif side[s_] == 0:
+                t[0] += f
+                t[5] += bw
+            else:
+                t[2] += f
+                t[3] += bw
+        for s_ in sorted(upf):
+            t[0] = upf[s_] if upf[s_] > t[0] else t[0]
+            t[5] = upb[s_] if upb[s_] > t[5] else t[5]
+        times[:, i] = [x + 0.0 for x in t]
+    return times, act
 
 
 def cpu_count() -> int:

@@ -174,6 +174,9 @@ static int lpt_cmp(const void* a_, const void* b_) {
   return a->idx < b->idx ? -1 : (a->idx > b->idx);
 }
 
+#define MAX_SEC 16 /* MAESTRO_MAX_SECTIONS */
+static int up_has(int u, int s) { return u == s || (u >= MAX_SEC && (((u - MAX_SEC) >> s) & 1)); }
+
 /* up_sec/down_sec: resolved section index per sample or -1.  lists must hold B
  * ints (rank r's list starts at offsets[r]); counts[dp].  LPT order written to
  * lpt_out (optional).  aux load is tracked per (rank, section) in n_sec slots. */
@@ -204,9 +207,14 @@ int oracle_partition(const double* t, const int* ids, const int* up_sec, const i
   for (int q = 0; q < B; ++q) {
     int i = keys[q].idx;
     if (lpt_out) lpt_out[q] = i;
-    int nk = 0, ks[2];
-    double kt[2];
-    if (up_sec[i] >= 0) { ks[nk] = up_sec[i]; kt[nk] = T(F_BC, i) + T(B_AC, i); ++nk; }
+    int nk = 0, ks[MAX_SEC + 1];
+    double kt[MAX_SEC + 1];
+    if (up_sec[i] >= MAX_SEC) {
+      /* extension (parallel upstream sections, NOT IN REF): code MAX_SEC + section mask; the
+       * sample's upstream time is charged to every activated upstream section, ascending */
+      for (int s = 0; s < MAX_SEC; ++s)
+        if (((up_sec[i] - MAX_SEC) >> s) & 1) { ks[nk] = s; kt[nk] = T(F_BC, i) + T(B_AC, i); ++nk; }
+    } else if (up_sec[i] >= 0) { ks[nk] = up_sec[i]; kt[nk] = T(F_BC, i) + T(B_AC, i); ++nk; }
     if (down_sec[i] >= 0) { ks[nk] = down_sec[i]; kt[nk] = T(F_AC, i) + T(B_BC, i); ++nk; }
     int best = -1;
     double bc = 0.0, ba = 0.0;
@@ -292,7 +300,7 @@ int oracle_build_schedule(const double* t, const int* ids, const int* up_sec, co
         lens[j] = 0;
         for (int k = 0; k < n; ++k) {
           int i = src[k];
-          if (up_sec[i] == s || down_sec[i] == s) filtered[fill + lens[j]++] = i;
+          if (up_has(up_sec[i], s) || down_sec[i] == s) filtered[fill + lens[j]++] = i;
         }
         fill += lens[j];
       }

@@ -46,6 +46,7 @@ class GraphStruct(ctypes.Structure):
         ("mbs", ctypes.c_int32 * S),
         ("sec_bits", ctypes.c_uint32 * S),
         ("crit_bit", ctypes.c_int32),
+        ("par_up", ctypes.c_int32),
     ]
 
 
@@ -153,6 +154,7 @@ def graph_struct(graph: SectionGraph, configs) -> GraphStruct:
     for k, v in enumerate(t.merge_order):
         g.merge_order[k] = v
     g.crit_bit = t.sub_names.index(t.section_ids[t.critical])
+    g.par_up = int(getattr(graph, "parallel_upstream", False))
     return g
 
 

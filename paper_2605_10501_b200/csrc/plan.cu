@@ -74,6 +74,12 @@ __global__ void __launch_bounds__(1024) sample_times_kernel(maestro_graph_t g, c
     }
     per_sample_times(crow, tc, n_crit, t[F_C], t[B_C]);
     uint32_t m = act[i];
+    // parallel upstream sections (g.par_up): per-section upstream times, the sample's t_f_bc /
+    // t_b_ac is the max over them (one activated bit per section, BothActivated otherwise, so
+    // a single-section sample gets exactly the reference's 0 + fwd)
+    double upf[MAESTRO_MAX_SECTIONS], upb[MAESTRO_MAX_SECTIONS];
+    if (g.par_up)
+      for (int s2 = 0; s2 < MAESTRO_MAX_SECTIONS; ++s2) upf[s2] = upb[s2] = 0.0;
     while (m) {
       const int b = __ffs(m) - 1;
       m &= m - 1;
@@ -83,7 +89,10 @@ __global__ void __launch_bounds__(1024) sample_times_kernel(maestro_graph_t g, c
       const long long n_aux = cnt[s] > 0 ? ((long long)cnt[s] + dps - 1) / dps : 0;
       double fwd, bwd;
       per_sample_times(row, tokens[(size_t)b * B + i], n_aux, fwd, bwd);
-      if (g.side[s] == 0) {
+      if (g.side[s] == 0 && g.par_up) {
+        upf[s] += fwd;
+        upb[s] += bwd;
+      } else if (g.side[s] == 0) {
         t[F_BC] += fwd;
         t[B_AC] += bwd;
       } else {
@@ -91,6 +100,11 @@ __global__ void __launch_bounds__(1024) sample_times_kernel(maestro_graph_t g, c
         t[B_BC] += bwd;
       }
     }
+    if (g.par_up)
+      for (int s2 = 0; s2 < g.n_sections; ++s2) {
+        t[F_BC] = pmax(t[F_BC], upf[s2]);
+        t[B_AC] = pmax(t[B_AC], upb[s2]);
+      }
     bool bad = !(t[F_C] > 0.0);
     for (int p = 0; p < 6; ++p) bad |= !(t[p] >= 0.0) || isinf(t[p]);
     if (bad) report(err, (uint32_t)i, MAESTRO_E_NEGATIVE_TIME, i);
@@ -175,10 +189,12 @@ __global__ void __launch_bounds__(1024) partition_kernel(maestro_graph_t g, cons
       if (g.side[s] == 0) up_secs |= 1u << s;
       if (g.side[s] == 2) down_secs |= 1u << s;
     }
-    if (!code && (__popc(up_secs) > 1 || __popc(down_secs) > 1)) code = MAESTRO_E_ACTIVATION;
+    if (!code && ((__popc(up_secs) > 1 && !g.par_up) || __popc(down_secs) > 1)) code = MAESTRO_E_ACTIVATION;
     int up_sec = -1, down_sec = -1;
     if (!code && up_t > 0) {  // _attribute (workload.py:336-355)
-      if (up_secs) up_sec = __ffs(up_secs) - 1;
+      // several upstream sections (par_up): encoded MAESTRO_MAX_SECTIONS + section mask
+      if (__popc(up_secs) > 1) up_sec = MAESTRO_MAX_SECTIONS + (int)up_secs;
+      else if (up_secs) up_sec = __ffs(up_secs) - 1;
       else if (g.n_up == 1) up_sec = g.up_cand[0];
       else code = MAESTRO_E_ACTIVATION;
     }
@@ -232,7 +248,12 @@ __global__ void __launch_bounds__(1024) partition_kernel(maestro_graph_t g, cons
       const int r = lane + 32 * h;
       if (r >= dp || cnt[r] >= cap[r]) continue;
       double sa = 0.0;  // sum() starts from int 0; 0 + x == x
-      if (s.up_sec >= 0) sa = sa + aux_load[r * MAESTRO_MAX_SECTIONS + s.up_sec];
+      if (s.up_sec >= MAESTRO_MAX_SECTIONS) {  // par_up: every activated upstream section, ascending
+        for (uint32_t mm = (uint32_t)(s.up_sec - MAESTRO_MAX_SECTIONS); mm; mm &= mm - 1)
+          sa = sa + aux_load[r * MAESTRO_MAX_SECTIONS + __ffs(mm) - 1];
+      } else if (s.up_sec >= 0) {
+        sa = sa + aux_load[r * MAESTRO_MAX_SECTIONS + s.up_sec];
+      }
       if (s.down_sec >= 0) sa = sa + aux_load[r * MAESTRO_MAX_SECTIONS + s.down_sec];
       const uint64_t c = dbits(crit_load[r]), a = dbits(sa);
       if (c < kc || (c == kc && a < ka)) {  // r ascending: strict less keeps the smaller r
@@ -249,7 +270,12 @@ __global__ void __launch_bounds__(1024) partition_kernel(maestro_graph_t g, cons
       part[off + cnt[best]] = s.idx;
       cnt[best] += 1;
       crit_load[best] += s.crit;
-      if (s.up_sec >= 0) aux_load[best * MAESTRO_MAX_SECTIONS + s.up_sec] += s.up;
+      if (s.up_sec >= MAESTRO_MAX_SECTIONS) {
+        for (uint32_t mm = (uint32_t)(s.up_sec - MAESTRO_MAX_SECTIONS); mm; mm &= mm - 1)
+          aux_load[best * MAESTRO_MAX_SECTIONS + __ffs(mm) - 1] += s.up;
+      } else if (s.up_sec >= 0) {
+        aux_load[best * MAESTRO_MAX_SECTIONS + s.up_sec] += s.up;
+      }
       if (s.down_sec >= 0) aux_load[best * MAESTRO_MAX_SECTIONS + s.down_sec] += s.down;
     }
     __syncwarp();
@@ -567,6 +593,11 @@ __device__ int block_exclusive_scan(int flag, int* warp_tot, int& total) {
   return res;
 }
 
+// Does resolved upstream code u (section index, -1, or MAESTRO_MAX_SECTIONS + mask) include s?
+__device__ __forceinline__ bool up_has(int u, int s) {
+  return u == s || (u >= MAESTRO_MAX_SECTIONS && (((u - MAESTRO_MAX_SECTIONS) >> s) & 1));
+}
+
 __global__ void __launch_bounds__(1024) fanout_merge_kernel(maestro_graph_t g, int B,
                                                             const int32_t* __restrict__ up,
                                                             const int32_t* __restrict__ down,
@@ -604,7 +635,7 @@ __global__ void __launch_bounds__(1024) fanout_merge_kernel(maestro_graph_t g, i
         int flag = 0, j = 0;
         if (e < hi) {
           const int i = src[e];
-          flag = (up[i] == s) || (down[i] == s);
+          flag = up_has(up[i], s) || (down[i] == s);
           while (j + 1 < f && sec_off[nb * W + q * f + j + 1] <= e) ++j;
         }
         if (flag) atomicAdd(&list_len[j], 1);
@@ -624,7 +655,7 @@ __global__ void __launch_bounds__(1024) fanout_merge_kernel(maestro_graph_t g, i
         int flag = 0, j = 0, i = -1;
         if (e < hi) {
           i = src[e];
-          flag = (up[i] == s) || (down[i] == s);
+          flag = up_has(up[i], s) || (down[i] == s);
           while (j + 1 < f && sec_off[nb * W + q * f + j + 1] <= e) ++j;
         }
         int total;

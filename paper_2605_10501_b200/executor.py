@@ -300,7 +300,7 @@ class KDExecutor:
         err = int(bufs["_err"].item())
         if err != N.ERR_CLEAN:
             N.raise_device_error(err, self.planner.ids[: self.batch].tolist(), self.graph.tables.section_ids)
-        host = {k: (a.tolist(), b.tolist()) for k, (a, b) in bufs.items() if k != "_err"}
+        host = {k: (v[0].tolist(), v[1].tolist()) for k, v in bufs.items() if k != "_err"}
         packed = {}
         with torch.cuda.stream(main):
             for sec, v in plan.items():

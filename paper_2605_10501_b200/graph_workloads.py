@@ -9,7 +9,8 @@ cfg 4  omni: image encoder (the cfg 3 ViT) + audio encoder (Whisper-large-v3-enc
        d 1280, 32 layers, 20 heads of 64, 1500 frames of 128 mel bins, 4:1 -> 375 tokens)
        upstream, the 7B backbone, and an audio decoder downstream (d 1024, 12 layers, 16 heads,
        4096 audio codes) on the backbone's last 512 positions of audio samples; mix text / img /
-       audio (recipes.omni "3way"; the img+audio class needs two upstream sections per sample).
+       audio / img+audio (recipes.omni "4way"; the img+audio class activates two upstream
+       sections, scheduled with this build's parallel-upstream generalisation).
 
 ``layers`` scales every stack's depth (reduced-depth runs keep the widths and sequence shapes:
 one GPU cannot hold a 7.6B model with fp32 master weights, gradients and Adam moments plus
@@ -172,7 +173,7 @@ def omni_executor(n_gpus: int = 1, layers: int | None = None, tiny: bool = False
     llm = TINY_LLM if tiny else depth(QWEN_7B, layers)
     dec = TINY_DEC if tiny else depth(AUDIO_DEC, layers)
     pd = 128 if tiny else PATCH_DIM
-    graph = R.omni_graph()
+    graph = R.omni_graph(parallel_upstream=True)  # img+audio samples: both encoders, in parallel
     configs = {"llm": SectionConfig(dp=n_gpus, mbs=mbs_llm), "image_enc": SectionConfig(dp=n_gpus, mbs=mbs_enc),
                "audio_enc": SectionConfig(dp=n_gpus, mbs=mbs_enc), "audio_dec": SectionConfig(dp=n_gpus, mbs=mbs_llm)}
     dev = torch.device("cuda", torch.cuda.current_device())

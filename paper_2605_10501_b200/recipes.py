@@ -174,7 +174,7 @@ def vlm_7b(n_gpus: int = 8, batch: int = 64, seed: int = 0) -> Recipe:
 
 
 # ----------------------------------------------------------------------------- cfg 4
-def omni_graph() -> SectionGraph:
+def omni_graph(parallel_upstream: bool = False) -> SectionGraph:
     img = SectionSpec("image_enc", Role.AUXILIARY, ExecMode.FORWARD_BACKWARD,
                       StructuralParams(1280, 16, 32, 1, 16384, QWEN_VIT_PARAMS))
     aud = SectionSpec("audio_enc", Role.AUXILIARY, ExecMode.FORWARD_BACKWARD,
@@ -185,24 +185,28 @@ def omni_graph() -> SectionGraph:
                       StructuralParams(1024, 16, 12, 4096, 4096, 300_000_000))
     return build_graph([img, aud, llm, dec], [Edge("image_enc", "llm", 1024 * 3584 * 2.0),
                                              Edge("audio_enc", "llm", 375 * 3584 * 2.0),
-                                             Edge("llm", "audio_dec", 512 * 3584 * 2.0)])
+                                             Edge("llm", "audio_dec", 512 * 3584 * 2.0)],
+                       parallel_upstream=parallel_upstream)
 
 
 OMNI_LAYOUTS = {1: (1, 1, 1), 2: (2, 1, 2), 4: (4, 2, 2), 8: (8, 2, 4)}
 
 
-def omni(n_gpus: int = 8, batch: int = 64, seed: int = 0, mix: str = "4way") -> Recipe:
+def omni(n_gpus: int = 8, batch: int = 64, seed: int = 0, mix: str = "4way",
+         parallel_upstream: bool = False) -> Recipe:
     """cfg 4: image + audio encoders (upstream), 7B backbone, audio decoder (downstream).
 
     mix "4way" = text / img / audio / img+audio in equal shares.  The img+audio class activates
     two upstream sections; the reference's 6-tuple model rejects it (ActivationError,
     workload.py:323-328) and so does the device resolver -- that is the parity-pinned behaviour.
     mix "3way" drops that class (text / img / audio) and schedules.  Audio samples also run the
-    downstream audio decoder on 512 generated tokens.
+    downstream audio decoder on 512 generated tokens.  ``parallel_upstream=True`` switches on this
+    build's generalisation (workload.SectionGraph.parallel_upstream): the img+audio class runs
+    both encoders in parallel and schedules with t_f_bc = max of the two.
     """
     from .synthetic import permutation
 
-    g = omni_graph()
+    g = omni_graph(parallel_upstream)
     dp_llm, dp_enc, f_enc = OMNI_LAYOUTS[n_gpus]
     configs = {"llm": SectionConfig(dp=dp_llm), "image_enc": SectionConfig(dp=dp_enc, fanout=f_enc),
                "audio_enc": SectionConfig(dp=dp_enc, fanout=f_enc), "audio_dec": SectionConfig(dp=dp_llm)}

@@ -29,6 +29,7 @@ from . import kernels as K
 from . import recipes as R
 from .costs import cost_table
 from .executor import StageClock, StepStats, handoff_mode
+from .handoff import handoff_index, scatter_mb
 from .scheduling import DevicePlanner, ExecPolicy
 from .synthetic import rand_int
 from .transformer import SHAPES, Batch, FlatParams, Transformer
@@ -247,8 +248,14 @@ class VLMExecutor:
         # host mirrors of the per-sample offsets (the orders are already on the host)
         toff_h = np.concatenate([[0], np.cumsum(lens_h[o_llm])[:-1]]).astype(np.int64)
         ordinal = hb["img_ordinal"]
-        vit_pos = {int(i): k for k, i in enumerate(o_vit)}  # sample -> slot in ViT order
         n_vmb = -(-n_vit // self.mbs_vit)
+        # K5b on device: (ViT-buffer row, LLM micro-batch row) pairs of every image token -- the
+        # ViT writes 49 merged rows per image in its own order, each lands at the sample's
+        # placeholder offset inside its LLM micro-batch
+        pin_idx = pinned_index_inputs(hb)
+        ix = handoff_index(_h2d(o_vit.astype(np.int32), dev), o_llm_d, tok_off, self.mbs_llm,
+                           pin_idx["rows"].to(dev, non_blocking=True), pin_idx["dst_off"].to(dev, non_blocking=True),
+                           49 * max(n_vit, 1), 49 * min(self.mbs_llm, max(n_vit, 1)))
         ready = torch.cuda.Event()
         ready.record(main)
         clock = StageClock()
@@ -258,6 +265,7 @@ class VLMExecutor:
         self.vit.p.zero_grad()
         emb_buf = torch.empty(max(n_vit, 1) * 49, self.llm_shape.d, device=dev, dtype=torch.bfloat16)
         demb_buf = torch.zeros_like(emb_buf)
+        vit_slot = {int(i): k for k, i in enumerate(o_vit)}  # sample -> slot in ViT order (dependencies)
         # ---- ViT forward queue (upstream f_bc in merged order)
         vit_fwd_ev, vit_ctx = [], []
         self.s_vit.wait_event(ready)
@@ -284,7 +292,7 @@ class VLMExecutor:
                 T = int(lens_h[samples].sum())
                 cu_m = cu[m * (self.mbs_llm + 1): m * (self.mbs_llm + 1) + len(ks) + 1]
                 # dependencies: ViT micro-batches holding this micro-batch's images
-                slots = [vit_pos[int(i)] for i in samples if hb["has_img"][i]]
+                slots = [vit_slot[int(i)] for i in samples if hb["has_img"][i]]
                 if slots:
                     self.s_llm.wait_event(vit_fwd_ev[max(slots) // self.mbs_vit])
                 clock.begin(self.s_llm, f"llm{m}")
@@ -293,16 +301,8 @@ class VLMExecutor:
                 b = Batch(ids=p_ids[start: start + T], cu=cu_m, pos=pos, max_len=int(lens_h[samples].max()))
                 x0 = torch.empty(T, d, device=dev, dtype=torch.bfloat16)
                 K.embed(self.llm.p["embed"], b.ids, x0)
-                src_rows, dst_rows = [], []
-                for k, i in zip(ks, samples):
-                    if hb["has_img"][i]:
-                        base = int(toff_h[k]) - start + int(hb["img_offset"][i])
-                        src_rows.append(np.arange(49) + 49 * vit_pos[int(i)])
-                        dst_rows.append(np.arange(49) + base)
-                if src_rows:
-                    sr = _h2d(np.concatenate(src_rows).astype(np.int32), dev)
-                    dr = _h2d(np.concatenate(dst_rows).astype(np.int32), dev)
-                    K.scatter_rows(emb_buf, x0, sr, dr)
+                if slots:  # K6 over this micro-batch's pairs of the device index
+                    scatter_mb(ix, m, emb_buf, x0)
                 yf, ctx = self.llm.forward(b, x0=x0)
                 logits = self.llm.logits(yf)
                 tl = torch.empty(T, device=dev)
@@ -310,12 +310,10 @@ class VLMExecutor:
                 loss_acc.add_(tl.sum())
                 dx0 = self.llm.backward(ctx, dlogits=logits, need_dx0=True)
                 K.embed_bwd(dx0, b.ids, self.llm.p.g("embed"))
-                if src_rows:
-                    # gradients of the placeholder rows back to the image-token slots (1:1 -> gather)
-                    seg = torch.arange(0, dr.numel() + 1, dtype=torch.int32, device=dev)
-                    tmp = torch.empty(dr.numel(), d, device=dev, dtype=torch.bfloat16)
-                    K.gather_rows_bwd(dx0, tmp, seg, dr)
-                    K.scatter_rows(tmp, demb_buf, torch.arange(sr.numel(), dtype=torch.int32, device=dev), sr)
+                if slots:
+                    # gradients of the placeholder rows back to the image-token slots (the same
+                    # pairs, reverse direction)
+                    scatter_mb(ix, m, dx0, demb_buf, reverse=True)
                 clock.end(self.s_llm)
                 e = torch.cuda.Event()
                 e.record(self.s_llm)
@@ -388,6 +386,19 @@ def pinned_inputs(hb: dict) -> dict:
         pin["pixels"] = torch.from_numpy(px16.view(np.int16)).pin_memory()
         pin["_src"] = {k: hb[k] for k in keys}
         hb["_pinned"] = pin
+    return pin
+
+
+def pinned_index_inputs(hb: dict) -> dict:
+    """Per-sample handoff inputs of K5b in page-locked memory, built once per host batch: rows
+    exchanged (49 merged image tokens, 0 for text-only samples) and their placeholder offset."""
+    pin = hb.get("_pinned_idx")
+    if pin is None or pin["_src"] is not hb["has_img"]:
+        rows = np.where(hb["has_img"], 49, 0).astype(np.int32)
+        off = np.where(hb["has_img"], hb["img_offset"], 0).astype(np.int32)
+        pin = {"rows": torch.from_numpy(rows).pin_memory(), "dst_off": torch.from_numpy(off).pin_memory(),
+               "_src": hb["has_img"]}
+        hb["_pinned_idx"] = pin
     return pin
 
 

@@ -74,13 +74,18 @@ def test_padded_vit_heads_stay_zero_and_exact():
         assert torch.all(vit.p[f"l{i}.wgu"][gu] == 0) and torch.all(vit.p[f"l{i}.wd"][:, fpad] == 0)
 
 
-@pytest.mark.parametrize("policy", ["interleaved", "all-fwd-then-bwd"])
-def test_omni_structure_matches_reference(policy):
+@pytest.mark.parametrize("policy,mix", [("interleaved", "3way"), ("all-fwd-then-bwd", "3way"),
+                                        ("interleaved", "4way"), ("all-fwd-then-bwd", "4way")])
+def test_omni_structure_matches_reference(policy, mix):
+    """cfg 4 structure: image + audio encoders, backbone, audio decoder; the 4-way mix has
+    img+audio samples that take rows from both encoders (parallel-upstream generalisation)."""
     from paper_2605_10501_b200 import graph_workloads as W
 
     ex = W.omni_executor(tiny=True, mbs_llm=2, mbs_enc=2, lr=0.0, policy=policy, max_pos=2048)
-    gb = W.omni_batch(9, seed=5, vocab=W.TINY_LLM.vocab, patch_dim=128, n_codes=W.TINY_DEC.vocab, img_patches=64,
-                      frames=40, dec_rows=12, text_lo=16, text_hi=60)
+    gb = W.omni_batch(12, seed=5, vocab=W.TINY_LLM.vocab, patch_dim=128, n_codes=W.TINY_DEC.vocab, img_patches=64,
+                      frames=40, dec_rows=12, text_lo=16, text_hi=60, mix=mix)
+    if mix == "4way":
+        assert ((gb.up["image_enc"].rows > 0) & (gb.up["audio_enc"].rows > 0)).any()
     _snapshot(ex)
     st = ex.step(gb)
     _check(ex, gb, st)
@@ -93,8 +98,8 @@ def test_policies_give_the_same_step():
     out = []
     for policy in ("interleaved", "all-fwd-then-bwd"):
         ex = W.omni_executor(tiny=True, mbs_llm=2, mbs_enc=2, lr=0.0, policy=policy, max_pos=2048)
-        gb = W.omni_batch(9, seed=6, vocab=W.TINY_LLM.vocab, patch_dim=128, n_codes=W.TINY_DEC.vocab,
-                          img_patches=64, frames=40, dec_rows=12, text_lo=16, text_hi=60)
+        gb = W.omni_batch(12, seed=6, vocab=W.TINY_LLM.vocab, patch_dim=128, n_codes=W.TINY_DEC.vocab,
+                          img_patches=64, frames=40, dec_rows=12, text_lo=16, text_hi=60, mix="4way")
         st = ex.step(gb)
         out.append((st.loss, {n: m.p.grad.clone() for n, m in ex.mod.items() if m.trainable}))
         ev = ex.stage_events()

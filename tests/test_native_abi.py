@@ -35,10 +35,10 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_graph_struct_layout_matches_header():
-    """sizeof(maestro_graph_t): 6 ints + sub_owner[32] + 9 arrays of 16 + crit_bit."""
+    """sizeof(maestro_graph_t): 6 ints + sub_owner[32] + 9 arrays of 16 + crit_bit + par_up."""
     from paper_2605_10501_b200._native import GraphStruct
 
-    assert ctypes.sizeof(GraphStruct) == 4 * (6 + 32 + 16 * 9 + 1)
+    assert ctypes.sizeof(GraphStruct) == 4 * (6 + 32 + 16 * 9 + 2)
 
 
 def test_graph_tables_for_recipes():
