@@ -236,6 +236,11 @@ def run_reference(args):
         if args.workload == "vlm":
             t, threads = cpu_vlm_step_sample()
             desc = "8 samples per step: oracle/torch_ref.py fp32 VLM step (ViT-tiny, merge, projector, GPT, CE)"
+        elif args.workload == "section":
+            from paper_2605_10501_b200.graph_bench import _cpu_sample
+
+            v, threads, desc = _cpu_sample(args.graph, args.layers or 4)
+            t = 1.0 / v
         else:
             t, threads, desc = cpu_kd_step_sample(args.workload)
         secs.append(t)
@@ -243,6 +248,8 @@ def run_reference(args):
     value = 1.0 / sec
     if args.workload == "vlm":
         workload, seq, gb = "vlm_cfg1: ViT-tiny (d192 L12) -> 2-layer GPT (d768), 50/50 text/image", "64..497", 64
+    elif args.workload == "section":
+        workload, seq, gb = f"{args.graph} (generic section-graph executor)", "varlen", (args.batch_per_rank or 8) * args.gpus
     else:
         P = KD_PRESETS[args.workload]
         workload, seq, gb = P[8], P[3], (args.batch_per_rank or P[4]) * args.gpus

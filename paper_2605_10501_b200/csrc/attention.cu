@@ -1013,39 +1013,46 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       {
         const int which = half;  // half 0 drains dK, half 1 dV
         const uint32_t tbase = tmem + lane_base + (which == 0 ? T_DK : T_DV);
-        uint32_t acc[DH / 32][32];
+        const float f = which == 0 ? scale : 1.f;
+        __nv_bfloat16* base = which == 0 ? dk + (size_t)(itm.s0 + kvpos) * lddk : dv + (size_t)(itm.s0 + kvpos) * lddv;
+        uint4* d4 = reinterpret_cast<uint4*>(base + itm.hk * DH);
+        // DH/64 passes over the rotate-half column pairs (c, c + DH/2), 32 columns each side, so
+        // only 64 accumulator registers are live (head_dim 128 would otherwise spill)
 #pragma unroll
-        for (int c = 0; c < DH / 32; ++c) tmem_ld_32x32b_x32(tbase + 32 * c, acc[c]);
-        tmem_ld_wait();
-        tc_fence_before();
-        mbar_arrive(dkv_empty);
-        if (kvpos < itm.L) {
-          const float f = which == 0 ? scale : 1.f;
-          if (which == 0 && rope_cs != nullptr) {
-            // K was rotated by RoPE in the forward: dK_pre = R(pos)^T dK  (rotate by -theta);
-            // rotate-half pairs (k, k + DH/2)
-#pragma unroll
-            for (int cp = 0; cp < DH / 64; ++cp)
+        for (int cp = 0; cp < DH / 64; ++cp) {
+          uint32_t lo[32], hi[32];
+          tmem_ld_32x32b_x32(tbase + 32 * cp, lo);
+          tmem_ld_32x32b_x32(tbase + DH / 2 + 32 * cp, hi);
+          tmem_ld_wait();
+          if (cp == DH / 64 - 1) {
+            tc_fence_before();
+            mbar_arrive(dkv_empty);
+          }
+          if (kvpos < itm.L) {
+            if (which == 0 && rope_cs != nullptr) {
+              // K was rotated by RoPE in the forward: dK_pre = R(pos)^T dK  (rotate by -theta)
 #pragma unroll
               for (int k = 0; k < 32; ++k) {
                 const float2 cs = rope_cs_at(rope_cs, kvpos, 32 * cp + k, DH / 2);
-                const float a = __uint_as_float(acc[cp][k]), b = __uint_as_float(acc[cp + DH / 64][k]);
-                acc[cp][k] = __float_as_uint(a * cs.x + b * cs.y);
-                acc[cp + DH / 64][k] = __float_as_uint(b * cs.x - a * cs.y);
+                const float a = __uint_as_float(lo[k]), b = __uint_as_float(hi[k]);
+                lo[k] = __float_as_uint(a * cs.x + b * cs.y);
+                hi[k] = __float_as_uint(b * cs.x - a * cs.y);
               }
-          }
-          __nv_bfloat16* base = which == 0 ? dk + (size_t)(itm.s0 + kvpos) * lddk : dv + (size_t)(itm.s0 + kvpos) * lddv;
-          uint4* d4 = reinterpret_cast<uint4*>(base + itm.hk * DH);
-#pragma unroll
-          for (int c = 0; c < DH / 32; ++c)
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const uint32_t* x = acc[c] + 8 * u;
-              d4[4 * c + u] = make_uint4(pack_bf16(__uint_as_float(x[0]) * f, __uint_as_float(x[1]) * f),
-                                         pack_bf16(__uint_as_float(x[2]) * f, __uint_as_float(x[3]) * f),
-                                         pack_bf16(__uint_as_float(x[4]) * f, __uint_as_float(x[5]) * f),
-                                         pack_bf16(__uint_as_float(x[6]) * f, __uint_as_float(x[7]) * f));
             }
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+              const uint32_t* acc = h2 == 0 ? lo : hi;
+              const int c0 = h2 * (DH / 2) + 32 * cp;  // first column of this 32-column chunk
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const uint32_t* x = acc + 8 * u;
+                d4[c0 / 8 + u] = make_uint4(pack_bf16(__uint_as_float(x[0]) * f, __uint_as_float(x[1]) * f),
+                                            pack_bf16(__uint_as_float(x[2]) * f, __uint_as_float(x[3]) * f),
+                                            pack_bf16(__uint_as_float(x[4]) * f, __uint_as_float(x[5]) * f),
+                                            pack_bf16(__uint_as_float(x[6]) * f, __uint_as_float(x[7]) * f));
+              }
+            }
+          }
         }
       }
     }

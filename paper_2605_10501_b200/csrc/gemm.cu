@@ -250,8 +250,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               }
             }
           }
-          if (rope_cols > 0 && n0 + c < rope_cols && row < M) {
-            const int pr = rope_pos[row];
+          if (rope_cols > 0 && n0 + c < rope_cols) {  // warp-uniform: the tcgen05.ld below is .sync.aligned
+            const int pr = row < M ? rope_pos[row] : 0;  // rows past M are computed but never stored
             if (rope_hd == 64) {
               // fused RoPE (rotate-half): this 64-column chunk is exactly one head of Q or K;
               // r0 holds dims [0,32), r1 dims [32,64) of the row
