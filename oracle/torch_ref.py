@@ -65,8 +65,17 @@ def param_views(shape, flat):
     return out
 
 
-def forward(shape, P, ids, cu, x0=None):
-    """fp32 forward of the stack -> final normed hidden [T, d]."""
+def rb(t, on=True):
+    """Straight-through bf16 rounding: the forward value is rounded to bf16 (where the kernels
+    store an activation in bf16), the gradient passes through in fp32."""
+    return t + (t.bfloat16().float() - t).detach() if on else t
+
+
+def forward(shape, P, ids, cu, x0=None, bf16=False):
+    """fp32 forward of the stack -> final normed hidden [T, d].  ``bf16``: round activations at
+    the points where the kernels store them in bf16 (norm outputs, the RoPE'd QKV, attention
+    output, the residual stream after each fused residual-add epilogue, the SwiGLU output and the
+    final hidden), so only accumulation order separates the two -- the rounding-aware oracle."""
     T = ids.shape[0]
     x = P["embed"][ids.long()] if x0 is None else x0
     cu_l = cu.tolist()
@@ -74,19 +83,19 @@ def forward(shape, P, ids, cu, x0=None):
     H, Hk, dh = shape.heads, shape.kv_heads, shape.head_dim
     scale = 1.0 / math.sqrt(dh)
     for i in range(shape.layers):
-        y = rms_norm(x, P[f"l{i}.ln1"], shape.eps)
+        y = rb(rms_norm(x, P[f"l{i}.ln1"], shape.eps), bf16)
         qkv = y @ P[f"l{i}.wqkv"].t()
         q = qkv[:, : H * dh].view(T, H, dh)
         k = qkv[:, H * dh: (H + Hk) * dh].view(T, Hk, dh)
-        v = qkv[:, (H + Hk) * dh:].view(T, Hk, dh)
-        q, k = rope(q, pos, shape.rope_base), rope(k, pos, shape.rope_base)
-        o = varlen_attention(q, k, v, cu, shape.causal, scale)
-        x = x + o.reshape(T, H * dh) @ P[f"l{i}.wo"].t()
-        y = rms_norm(x, P[f"l{i}.ln2"], shape.eps)
+        v = rb(qkv[:, (H + Hk) * dh:].view(T, Hk, dh), bf16)
+        q, k = rb(rope(q, pos, shape.rope_base), bf16), rb(rope(k, pos, shape.rope_base), bf16)
+        o = rb(varlen_attention(q, k, v, cu, shape.causal, scale), bf16)
+        x = rb(x + o.reshape(T, H * dh) @ P[f"l{i}.wo"].t(), bf16)
+        y = rb(rms_norm(x, P[f"l{i}.ln2"], shape.eps), bf16)
         gu = y @ P[f"l{i}.wgu"].t()
         g, u = gu[:, gate_index(shape.ffn, gu.device)], gu[:, gate_index(shape.ffn, gu.device) + 32]
-        x = x + (F.silu(g) * u) @ P[f"l{i}.wd"].t()
-    return rms_norm(x, P["lnf"], shape.eps)
+        x = rb(x + rb(F.silu(g) * u, bf16) @ P[f"l{i}.wd"].t(), bf16)
+    return rb(rms_norm(x, P["lnf"], shape.eps), bf16)
 
 
 def gate_index(F, device):
@@ -106,14 +115,15 @@ def kd_loss(t_logits, s_logits, tau=1.0):
     return (lt.exp() * (lt - ls)).sum(-1)
 
 
-def kd_step_reference(tshape, sshape, t_flat, s_flat, t_head, ids, cu, global_tokens):
-    """One KD micro-batch in fp32 autograd: returns (sum of token KL, student grads flat)."""
+def kd_step_reference(tshape, sshape, t_flat, s_flat, t_head, ids, cu, global_tokens, bf16=False):
+    """One KD micro-batch in fp32 autograd: returns (sum of token KL, student grads flat).
+    ``bf16``: the rounding-aware forward (see forward); logits rounded like the GEMM outputs."""
     Pt = param_views(tshape, t_flat)
     s_flat = s_flat.detach().clone().requires_grad_(True)
     Ps = param_views(sshape, s_flat)
     with torch.no_grad():
-        t_logits = forward(tshape, Pt, ids, cu) @ t_head.t()
-    s_logits = forward(sshape, Ps, ids, cu) @ head_weight(sshape, Ps).t()
+        t_logits = rb(forward(tshape, Pt, ids, cu, bf16=bf16) @ t_head.t(), bf16)
+    s_logits = rb(forward(sshape, Ps, ids, cu, bf16=bf16) @ head_weight(sshape, Ps).t(), bf16)
     tok = kd_loss(t_logits, s_logits)
     (tok.sum() / global_tokens).backward()
     return tok.detach(), s_flat.grad
@@ -210,7 +220,7 @@ def views(shape, flat, extra=()):
     return out
 
 
-def graph_step_reference(crit, ups, downs, gb):
+def graph_step_reference(crit, ups, downs, gb, bf16=False):
     """fp32 autograd restatement of one generic-executor step over the WHOLE batch (sample order
     does not matter: training equivalence).
 
@@ -237,10 +247,11 @@ def graph_step_reference(crit, ups, downs, gb):
             fo = np.concatenate([[0], np.cumsum(ui.in_len)]).astype(np.int64)
             sh_t, Pt = unpad_heads(sh, P)
             for i in act:
-                x = feats[fo[i]: fo[i + 1]] @ P["in_w"].t()
+                x = rb(feats[fo[i]: fo[i + 1]] @ P["in_w"].t(), bf16)
                 cu = torch.tensor([0, int(ui.in_len[i])], dtype=torch.int32, device=dev)
-                y = forward(sh_t, Pt, torch.zeros(int(ui.in_len[i]), dtype=torch.int32, device=dev), cu, x0=x)
-                rows[i] = y.reshape(-1, merge * sh.d) @ P["proj_w"].t()
+                y = forward(sh_t, Pt, torch.zeros(int(ui.in_len[i]), dtype=torch.int32, device=dev), cu, x0=x,
+                            bf16=bf16)
+                rows[i] = rb(y.reshape(-1, merge * sh.d) @ P["proj_w"].t(), bf16)
         enc_rows[name] = rows
     dec = {}
     for name, (sh, flat, in_d) in downs.items():
@@ -262,8 +273,8 @@ def graph_step_reference(crit, ups, downs, gb):
                 r = enc_rows[name][i]
                 x = torch.cat([x[:o], r, x[o + r.shape[0]:]], 0)
         cu = torch.tensor([0, L], dtype=torch.int32, device=dev)
-        y = forward(cs_t, Pc_t, ids, cu, x0=x)
-        logits = y @ head_weight(cs, Pc).t()
+        y = forward(cs_t, Pc_t, ids, cu, x0=x, bf16=bf16)
+        logits = rb(y @ head_weight(cs, Pc).t(), bf16)
         valid = lab >= 0
         if valid.any():
             loss = loss + F.cross_entropy(logits[valid], lab[valid], reduction="sum") / n_lab
@@ -275,10 +286,11 @@ def graph_step_reference(crit, ups, downs, gb):
             so = int(di.src_off[i])
             t_off = int(np.sum(di.rows[:i]))
             tg = torch.from_numpy(di.targets[t_off: t_off + nr]).to(dev).long()
-            xin = y[so: so + nr] @ P["in_w"].t()
+            xin = rb(y[so: so + nr] @ P["in_w"].t(), bf16)
             cu_d = torch.tensor([0, nr], dtype=torch.int32, device=dev)
-            yd = forward(sh, P, torch.zeros(nr, dtype=torch.int32, device=dev), cu_d, x0=xin)
-            dec_sum[name] = dec_sum[name] + F.cross_entropy(yd @ head_weight(sh, P).t(), tg, reduction="sum")
+            yd = forward(sh, P, torch.zeros(nr, dtype=torch.int32, device=dev), cu_d, x0=xin, bf16=bf16)
+            dec_sum[name] = dec_sum[name] + F.cross_entropy(rb(yd @ head_weight(sh, P).t(), bf16), tg,
+                                                            reduction="sum")
     for name in downs:
         loss = loss + dec_sum[name] / max(int(gb.down[name].rows.sum()), 1)
     loss.backward()
