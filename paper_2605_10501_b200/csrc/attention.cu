@@ -454,7 +454,10 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
         const float2 t01 = __fadd2_rn(sum2[0], sum2[1]), t23 = __fadd2_rn(sum2[2], sum2[3]);
         const float2 t = __fadd2_rn(t01, t23);
         l = l * alpha + (t.x + t.y);
-        if (rescale) {
+        // the rescale decision is per row; the TMEM load/store are warp-collective (.sync.aligned),
+        // so the whole warp takes the branch when any lane needs it (the others scale by 1, exact)
+        if (__any_sync(kFull, rescale)) {
+          if (!rescale) alpha = 1.f;
           mbar_wait(&p_empty[(g - 1) & 1], ((g - 1) >> 1) & 1);  // PV_{g-1} retired: O is final
           tc_fence_after();
 #pragma unroll

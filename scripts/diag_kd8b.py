@@ -49,11 +49,17 @@ def main():
         attn(4096, 4, 16, 16, 128, False, True)
         attn(8192, 1, 32, 8, 64, True, True)
     elif which == "kd8b":
-        from paper_2605_10501_b200 import instrument
-        from paper_2605_10501_b200.executor import KDExecutor, synthetic_ids
+        import dataclasses
 
-        ex = KDExecutor(n_gpus=1, batch_per_rank=2, seq=8192, mbs=1, teacher="llama3_8b", student="llama32_1b",
-                        recipe="kd_8b", teacher_mbs=2)
+        from paper_2605_10501_b200.executor import KDExecutor, synthetic_ids
+        from paper_2605_10501_b200.transformer import SHAPES
+
+        nl = int(os.environ.get("LAYERS", "0"))
+        if nl:
+            SHAPES["t_dbg"] = dataclasses.replace(SHAPES["llama3_8b"], layers=nl)
+            SHAPES["s_dbg"] = dataclasses.replace(SHAPES["llama32_1b"], layers=nl)
+        ex = KDExecutor(n_gpus=1, batch_per_rank=2, seq=8192, mbs=1, teacher="t_dbg" if nl else "llama3_8b",
+                        student="s_dbg" if nl else "llama32_1b", recipe="kd_8b", teacher_mbs=2)
         log("executor built", torch.cuda.memory_allocated() / 2**30, "GiB")
         ids = torch.from_numpy(synthetic_ids(2, 8192, 128256)).cuda()
         for i in range(2):

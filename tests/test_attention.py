@@ -113,3 +113,26 @@ def test_attention_fwd_bwd_hd128(lens, H, Hk, causal):
     assert rel(dk, kf.grad) < 3e-2
     assert rel(dq, qf.grad) < 3e-2
     assert torch.all(dqkv[:, (H + 2 * Hk) * dh:] == 0)  # pitch padding untouched
+
+
+@pytest.mark.parametrize("dh", [64, 128])
+def test_attention_fwd_rescale_divergence(dh):
+    """Rows whose running max grows by > 2^8 mid-sequence next to rows whose max does not: the
+    lazy O rescale is a per-row decision inside a warp (regression: it used to run warp-collective
+    TMEM loads under a per-lane branch and hang on real model activations)."""
+    from paper_2605_10501_b200 import attention as A
+
+    torch.manual_seed(dh)
+    lens, H, Hk = [1024, 700], 4, 2
+    T = sum(lens)
+    cu = torch.tensor([0] + list(torch.tensor(lens).cumsum(0)), dtype=torch.int32, device="cuda")
+    q = torch.randn(T, H, dh, device="cuda") * torch.empty(T, 1, 1, device="cuda").uniform_(0.2, 6.0)
+    k = torch.randn(T, Hk, dh, device="cuda") * torch.linspace(0.3, 3.0, T, device="cuda")[:, None, None]
+    v = torch.randn(T, Hk, dh, device="cuda")
+    q, k, v = q.bfloat16(), k.bfloat16(), v.bfloat16()
+    scale = 1.0 / math.sqrt(dh)
+    o = torch.empty(T, H, dh, device="cuda", dtype=torch.bfloat16)
+    lse = A.attn_fwd(q, k, v, cu, max(lens), True, o, scale, plan=A.plan(cu, T))
+    ref = R.varlen_attention(q.float(), k.float(), v.float(), cu, True, scale)
+    assert rel(o, ref) < 2e-2
+    assert (lse - ref_lse(q, k, cu, True, scale)).abs().max().item() < 2e-3
