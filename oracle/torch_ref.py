@@ -137,7 +137,7 @@ def adamw_reference(p, g, m, v, lr, step, b1=0.9, b2=0.95, eps=1e-8, wd=0.1):
     return p
 
 
-def vlm_step_reference(llm_shape, vit_shape, llm_flat, vit_flat, hb, merge_idx, patch_dim=768):
+def vlm_step_reference(llm_shape, vit_shape, llm_flat, vit_flat, hb, merge_idx, patch_dim=768, bf16=False):
     """fp32 autograd restatement of one VLM step (ViT -> 2x2 merge -> projector -> scatter into the
     LLM sequence at the placeholder offset -> LLM -> next-token CE).  Returns (loss, llm grad, vit grad)."""
     dev = llm_flat.device
@@ -159,12 +159,12 @@ def vlm_step_reference(llm_shape, vit_shape, llm_flat, vit_flat, hb, merge_idx, 
     emb = None
     if n_img:
         px = torch.from_numpy(hb["pixels"]).to(dev).to(torch.bfloat16).float().view(-1, patch_dim)
-        x0 = px @ Pv["patch_w"].t()
+        x0 = rb(px @ Pv["patch_w"].t(), bf16)
         cu = torch.arange(0, n_img * 196 + 1, 196, dtype=torch.int32, device=dev)
-        yf = forward(vit_shape, Pv, torch.zeros(n_img * 196, dtype=torch.int32, device=dev), cu, x0=x0)
+        yf = forward(vit_shape, Pv, torch.zeros(n_img * 196, dtype=torch.int32, device=dev), cu, x0=x0, bf16=bf16)
         src = (torch.from_numpy(merge_idx).to(dev)[None, :].long() + 196 * torch.arange(n_img, device=dev)[:, None]).reshape(-1)
         merged = yf[src].view(n_img * 49, 4 * vit_shape.d)
-        emb = merged @ Pv["proj_w"].t()
+        emb = rb(merged @ Pv["proj_w"].t(), bf16)
     total, nlab = 0.0, 0
     loss_sum = torch.zeros((), device=dev)
     for i in range(hb["ids"].shape[0]):
@@ -177,8 +177,8 @@ def vlm_step_reference(llm_shape, vit_shape, llm_flat, vit_flat, hb, merge_idx, 
             k = int(hb["img_ordinal"][i])
             x = torch.cat([x[:o], emb[49 * k: 49 * k + 49], x[o + 49:]], 0)
         cu = torch.tensor([0, L], dtype=torch.int32, device=dev)
-        y = forward(llm_shape, Pl, ids, cu, x0=x)
-        logits = y @ head_weight(llm_shape, Pl).t()
+        y = forward(llm_shape, Pl, ids, cu, x0=x, bf16=bf16)
+        logits = rb(y @ head_weight(llm_shape, Pl).t(), bf16)
         valid = lab >= 0
         if valid.any():
             loss_sum = loss_sum + F.cross_entropy(logits[valid], lab[valid], reduction="sum")

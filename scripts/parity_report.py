@@ -75,6 +75,22 @@ def kd_step():
     return out
 
 
+def vlm_step():
+    from paper_2605_10501_b200 import vlm
+
+    ex = vlm.VLMExecutor(batch=12, mbs_llm=4, mbs_vit=3, lr=0.0)
+    hb = vlm.vlm_host_batch(12, seed=3)
+    lf, vf = ex.llm.p.w.float().clone(), ex.vit.p.w.float().clone()
+    st = ex.step(hb)
+    out = {}
+    for mode in (False, True):
+        loss, gl, gv = R.vlm_step_reference(ex.llm_shape, ex.vit_shape, lf, vf, hb, vlm.merge_index(), bf16=mode)
+        out["bf16_oracle" if mode else "fp32_oracle"] = {"loss_rel": abs(st.loss - loss) / abs(loss),
+                                                         "grad:llm": errs(ex.llm.p.grad, gl),
+                                                         "grad:vit": errs(ex.vit.p.grad[: gv.numel()], gv)}
+    return out
+
+
 def graph(kind):
     import test_graph_exec as T
 
@@ -114,7 +130,7 @@ def main():
     for name, fn in [("transformer_hd64_causal", lambda: transformer("test_tiny", True)),
                      ("transformer_hd64_bidir", lambda: transformer("test_tiny", False)),
                      ("transformer_hd128_causal", lambda: transformer("test_tiny_hd128", True)),
-                     ("kd_step", kd_step), ("graph_vlm7b", lambda: graph("vlm7b")),
+                     ("kd_step", kd_step), ("vlm_step", vlm_step), ("graph_vlm7b", lambda: graph("vlm7b")),
                      ("graph_omni4way", lambda: graph("omni"))]:
         try:
             rep[name] = fn()

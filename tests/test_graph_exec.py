@@ -2,9 +2,11 @@
 
 Tiny shapes with the configs' structure: zero-padded 80-in-128 ViT heads and a padded SwiGLU,
 GQA backbone, image + audio encoders, a downstream audio decoder.  Every step is checked against
-the fp32 autograd restatement of the whole graph (oracle/torch_ref.graph_step_reference; padded
-heads are compared with the TRUE unpadded model).  Tolerance: bf16 activations -> loss within
-2e-2 relative, gradients within 6e-2 of the max magnitude.
+the fp32 autograd restatement of the whole graph in its bf16-rounding-aware mode
+(oracle/torch_ref.graph_step_reference(bf16=True); padded heads are compared with the TRUE
+unpadded model).  Tolerance: loss within 1e-3 relative; every section's gradient within 1.2e-2
+relative L2 and 2e-2 of its max magnitude (measured 7.3e-3 .. 8.8e-3 relative L2,
+profiles/r02_parity_report.json).
 """
 
 import numpy as np
@@ -20,7 +22,11 @@ def rel(a, b):
     return ((a.float() - b.float()).abs().max() / b.float().abs().max().clamp_min(1e-6)).item()
 
 
-def _check(ex, gb, st, tol=6e-2):
+def relnorm(a, b):
+    return ((a.float() - b.float()).norm() / b.float().norm().clamp_min(1e-12)).item()
+
+
+def _check(ex, gb, st, tol=2e-2):
     from paper_2605_10501_b200.graph_exec import BackboneModule, DecoderModule, EncoderModule
 
     crit = None
@@ -32,13 +38,15 @@ def _check(ex, gb, st, tol=6e-2):
             ups[name] = (m.s, ex._w0[name], m.in_dim, m.merge)
         elif isinstance(m, DecoderModule):
             downs[name] = (m.s, ex._w0[name], m.in_d)
-    loss, grads = R.graph_step_reference(crit, ups, downs, gb)
-    assert abs(st.loss - loss) / abs(loss) < 2e-2, (st.loss, loss)
+    loss, grads = R.graph_step_reference(crit, ups, downs, gb, bf16=True)
+    assert abs(st.loss - loss) / abs(loss) < 1e-3, (st.loss, loss)  # measured <= 8e-6
     for name, m in ex.mod.items():
         if not m.trainable:
             continue
         g = grads["crit" if isinstance(m, BackboneModule) else name]
-        assert rel(m.p.grad[: g.numel()], g) < tol, name
+        got = m.p.grad[: g.numel()]
+        # measured relative L2 7.3e-3 .. 8.8e-3 (4 sections, 2 layers each, bf16 end to end)
+        assert rel(got, g) < tol and relnorm(got, g) < 1.2e-2, (name, rel(got, g), relnorm(got, g))
 
 
 def _snapshot(ex):

@@ -1,8 +1,10 @@
 """GPU numerics of the section compute against the plain PyTorch fp32 restatement (oracle/torch_ref.py).
 
 Parity for this part is unpinned by the reference (it has no model code); tolerances are stated
-per test: bf16 storage of activations and weights bounds agreement to ~1e-2 relative, fp32
-reductions (losses, norms) to ~1e-4.
+per test.  Model-level checks compare with the bf16-rounding-aware oracle (activations rounded to
+bf16 where the kernels store them): relative L2 error <= 1e-2 on outputs and every gradient
+(measured 2.6e-3 .. 7.6e-3, profiles/r02_parity_report.json), max-normalised error <= 2e-2, losses
+<= 1e-3 relative; single-kernel checks: bf16 outputs ~1e-2, fp32 reductions ~1e-4.
 """
 
 import math
@@ -17,6 +19,11 @@ pytestmark = pytest.mark.gpu
 
 def rel(a, b):
     return ((a.float() - b.float()).abs().max() / b.float().abs().max().clamp_min(1e-6)).item()
+
+
+def relnorm(a, b):
+    """Relative L2 error ||a - b|| / ||b|| (profiles/r02_parity_report.json: 2.6e-3 .. 7.6e-3 here)."""
+    return ((a.float() - b.float()).norm() / b.float().norm().clamp_min(1e-12)).item()
 
 
 def test_rmsnorm_fwd_bwd():
@@ -156,17 +163,17 @@ def test_transformer_fwd_bwd_vs_fp32(causal, shape_name):
     logits = model.logits(yf)
     flat = p.w.float().clone().requires_grad_(True)
     P = R.param_views(shape, flat)
-    yr = R.forward(shape, P, ids, cu)
-    lr_ = yr @ R.head_weight(shape, P).t()
-    assert rel(yf, yr) < 3e-2
-    assert rel(logits, lr_) < 3e-2
+    yr = R.forward(shape, P, ids, cu, bf16=True)  # rounding-aware oracle (bf16 at the kernels' store points)
+    lr_ = R.rb(yr @ R.head_weight(shape, P).t())
+    assert rel(yf, yr) < 2e-2 and relnorm(yf, yr) < 1e-2
+    assert rel(logits, lr_) < 2e-2 and relnorm(logits, lr_) < 1e-2
     dl = (torch.randn_like(lr_) * 0.01).bfloat16()
     lr_.backward(dl.float())
     p.zero_grad()
     model.backward(ctx, dlogits=dl)
     for name in ("embed", "head", "lnf", "l1.wd", "l1.wgu", "l0.wqkv", "l0.wo", "l0.ln1"):
         got, want = p.g(name), R.param_views(shape, flat.grad)[name]
-        assert rel(got, want) < 5e-2, name
+        assert rel(got, want) < 2e-2 and relnorm(got, want) < 1e-2, name
 
 
 def test_kd_executor_step_matches_reference():
@@ -180,13 +187,14 @@ def test_kd_executor_step_matches_reference():
     st = ex.step(ids)
     cu = torch.arange(0, 4 * 128 + 1, 128, dtype=torch.int32, device="cuda")
     tok, grad = R.kd_step_reference(ex.tshape, ex.sshape, t_flat, s_flat, ex.t_head.float(), ids.reshape(-1), cu,
-                                    global_tokens=4 * 128)
+                                    global_tokens=4 * 128, bf16=True)
     ref_loss = tok.sum().item() / (4 * 128)
-    assert abs(st.loss - ref_loss) / max(abs(ref_loss), 1e-6) < 3e-2
+    assert abs(st.loss - ref_loss) / max(abs(ref_loss), 1e-6) < 1e-3  # measured 4e-5
     got = R.param_views(ex.sshape, ex.student.p.grad)
     want = R.param_views(ex.sshape, grad)
+    assert relnorm(ex.student.p.grad, grad) < 1e-2  # measured 2.6e-3
     for name in ("embed", "lnf", "l0.wqkv", "l1.wd"):
-        assert rel(got[name], want[name]) < 6e-2, name
+        assert rel(got[name], want[name]) < 2e-2 and relnorm(got[name], want[name]) < 1e-2, name
     assert 0.0 <= st.stall_frac <= 1.0
 
 
@@ -299,10 +307,11 @@ def test_kd_executor_hd128_teacher_matches_reference():
     st = ex.step(ids)
     cu = torch.arange(0, 4 * 256 + 1, 256, dtype=torch.int32, device="cuda")
     tok, grad = R.kd_step_reference(ex.tshape, ex.sshape, t_flat, s_flat, ex.t_head.float(), ids.reshape(-1), cu,
-                                    global_tokens=4 * 256)
+                                    global_tokens=4 * 256, bf16=True)
     ref_loss = tok.sum().item() / (4 * 256)
-    assert abs(st.loss - ref_loss) / max(abs(ref_loss), 1e-6) < 3e-2
+    assert abs(st.loss - ref_loss) / max(abs(ref_loss), 1e-6) < 1e-3
     got = R.param_views(ex.sshape, ex.student.p.grad)
     want = R.param_views(ex.sshape, grad)
+    assert relnorm(ex.student.p.grad, grad) < 1e-2
     for name in ("embed", "lnf", "l0.wqkv", "l1.wd"):
-        assert rel(got[name], want[name]) < 6e-2, name
+        assert rel(got[name], want[name]) < 2e-2 and relnorm(got[name], want[name]) < 1e-2, name
