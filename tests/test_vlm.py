@@ -13,6 +13,10 @@ def rel(a, b):
     return ((a.float() - b.float()).abs().max() / b.float().abs().max().clamp_min(1e-6)).item()
 
 
+def relnorm(a, b):
+    return ((a.float() - b.float()).norm() / b.float().norm().clamp_min(1e-12)).item()
+
+
 def test_vlm_step_matches_reference():
     from paper_2605_10501_b200 import vlm
 
@@ -20,14 +24,18 @@ def test_vlm_step_matches_reference():
     hb = vlm.vlm_host_batch(12, seed=3)
     lf, vf = ex.llm.p.w.float().clone(), ex.vit.p.w.float().clone()
     st = ex.step(hb)
-    loss, gl, gv = R.vlm_step_reference(ex.llm_shape, ex.vit_shape, lf, vf, hb, vlm.merge_index())
-    assert abs(st.loss - loss) / loss < 2e-2
+    # bf16-rounding-aware oracle (profiles/r02_parity_report.json: loss 2e-6, LLM grads 9.3e-3 and
+    # ViT grads 1.2e-2 relative L2 -- the ViT is 12 layers deep, every layer adds bf16 rounding)
+    loss, gl, gv = R.vlm_step_reference(ex.llm_shape, ex.vit_shape, lf, vf, hb, vlm.merge_index(), bf16=True)
+    assert abs(st.loss - loss) / loss < 1e-3
+    assert relnorm(ex.llm.p.grad, gl) < 1.5e-2
     Pg = R.param_views(ex.llm_shape, ex.llm.p.grad)
     Pr = R.param_views(ex.llm_shape, gl)
     for name in ("embed", "head", "l0.wqkv", "l1.wd", "lnf"):
-        assert rel(Pg[name], Pr[name]) < 6e-2, name
+        assert rel(Pg[name], Pr[name]) < 2.5e-2, name
     # ViT section gradients (flat arena incl. patch / projector weights)
-    assert rel(ex.vit.p.grad[: gv.numel()], gv) < 8e-2
+    vg = ex.vit.p.grad[: gv.numel()]
+    assert rel(vg, gv) < 2.5e-2 and relnorm(vg, gv) < 2e-2
 
 
 def test_vlm_loss_decreases():
