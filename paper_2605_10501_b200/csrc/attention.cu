@@ -21,6 +21,7 @@
 // phases; dV/dK accumulate in TMEM across the item; dQ tiles are drained by a dedicated
 // warpgroup through swizzled smem boxes and TMA reduce-add; inverse RoPE fused into the dQ/dK stores.
 #include <cuda_bf16.h>
+#include <stdlib.h>
 #include <climits>
 #include <type_traits>
 
@@ -34,7 +35,6 @@ namespace {
 using namespace sm100;
 
 constexpr int BQ = 128, BKV = 128;  // forward query tile, key tile (rows)
-constexpr int FWD_THREADS = 320;  // w0 TMA, w1 MMA, w2-9 softmax (2 per lane quadrant)
 constexpr float LOG2E_F = 1.4426950408889634f;
 constexpr float LN2_F = 0.6931471805599453f;
 
@@ -70,6 +70,9 @@ __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.syn
 #ifndef BWD_EMU_BITS
 #define BWD_EMU_BITS 0x00  // backward P^T = exp2(S^T scale2 - lse2): not MUFU-bound, all on MUFU
 #endif
+#ifndef ATTN_FWD_CG64
+#define ATTN_FWD_CG64 2  // default column groups of the head_dim-64 forward (see FwdCfg)
+#endif
 #ifndef FWD_EMU_BITS
 #define FWD_EMU_BITS 0x92  // pair p of a row's 32 goes to the FMA pipe if bit (p & 7) is set (3/8)
 #endif
@@ -95,26 +98,41 @@ __device__ __forceinline__ uint32_t p_offset(int r, int c) {
 // order.  All pipeline counters run across items: K/V stream through the ring, S alternates
 // between two TMEM buffers by global tile index, Q is double-buffered by item index, so the
 // next item's Q load, first S MMAs and softmax overlap the current item's epilogue.
-// TMEM: S0 [0,128) S1 [128,256), then the O accumulators: two 64-column halves O_a (keys 0-63
-// of every tile) and O_b (keys 64-127) per item.  head_dim 64: O double-buffered by item
-// parity ([256,384), [384,512)); head_dim 128: one O = O_a [256,384) + O_b [384,512), so the
-// first PV of an item waits for the previous item's epilogue to have read O.
+//
+// The 128 key columns of a tile are split into CG column groups; each lane quadrant has one
+// softmax warp per group, each group runs its own online softmax (max, sum, lazy rescale) into
+// its own O accumulator (keys of its columns), and the groups combine once per item in the
+// epilogue.  CG = 2: 8 softmax warps, 64 columns per thread.  CG = 4 (head_dim 64 only): 16
+// softmax warps, 32 columns per thread -- twice the warps per SM sub-partition to hide the
+// per-tile latency chain (TMEM load -> max -> exp -> sum -> pack -> TMEM store), at half the
+// registers per thread.
+// TMEM: S0 [0,128) S1 [128,256), then NOB x CG O accumulators of DH columns:
+//   DH 64, CG 2: O double-buffered by item ([256,384), [384,512));
+//   DH 64, CG 4 and DH 128, CG 2: one set of O accumulators ([256,512)), so the first PV of an
+//   item waits for the previous item's (deferred) epilogue to have read them.
 // A [128 rows][DH] bf16 tile is DH/64 SWIZZLE_128B chunks of 128 rows x 128 B (16 KB each).
-template <int DH>
+template <int DH, int CG>
 struct FwdCfg {
-  static constexpr int NCH = DH / 64;                 // 64-column chunks per tile row
+  // w0 TMA, w1 MMA, softmax warps from SW0 on (CG per lane quadrant).  CG = 4: warps 2-3 idle so
+  // the softmax warps fill whole warpgroups and setmaxnreg can move registers to them
+  static constexpr int SW0 = CG == 4 ? 4 : 2;
+  static constexpr int THREADS = 32 * SW0 + 128 * CG;
+  static constexpr int REG_LO = 64, REG_HI = 112;     // CG = 4: TMA/MMA warpgroup, softmax warpgroups
+  static constexpr int SMX = 128 * CG;                // softmax threads
+  static constexpr int CW = BKV / CG;                 // key columns per group
   static constexpr int TILE = 128 * DH * 2;           // bytes of a 128-row tile
   static constexpr int KVS = DH == 64 ? 3 : 2;        // K/V ring depth
-  static constexpr int NOB = DH == 64 ? 2 : 1;        // O accumulators (by item)
+  static constexpr int NOB = (256 + 2 * CG * DH <= 512) ? 2 : 1;  // O accumulator sets (by item)
   static constexpr int Q = 0;                         // 2 x TILE (by item parity)
   static constexpr int K = Q + 2 * TILE;
   static constexpr int V = K + KVS * TILE;
-  static constexpr int XMAX = V + KVS * TILE;         // [2 items][2 halves][128] row maxima
-  static constexpr int XSUM = XMAX + 2 * 2 * 128 * 4; // [2 items][2 halves][128] row sums
-  static constexpr int BAR = XSUM + 2 * 2 * 128 * 4;
+  static constexpr int XMAX = V + KVS * TILE;         // [2 items][CG groups][128] row maxima
+  static constexpr int XSUM = XMAX + 2 * CG * 128 * 4; // [2 items][CG groups][128] row sums
+  static constexpr int BAR = XSUM + 2 * CG * 128 * 4;
   static constexpr int TOTAL = BAR + 256;
   static_assert(TOTAL + 1024 <= 227 * 1024, "forward smem");
-  static_assert(256 + NOB * 2 * DH <= 512, "forward TMEM");
+  static_assert(256 + NOB * CG * DH <= 512, "forward TMEM");
+  static_assert(CW == 32 || CW == 64, "column group width");
 };
 
 struct FwdItem {
@@ -149,14 +167,33 @@ __device__ __forceinline__ void load_tile(unsigned char* dst, const CUtensorMap*
   for (int c = 0; c < DH / 64; ++c) tma_load_2d(dst + c * 16384, map, bar, col + 64 * c, row);
 }
 
-template <int DH, bool CAUSAL>
-__global__ void __launch_bounds__(FWD_THREADS, 1)
+template <int N>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t (&r)[N]) {
+  if constexpr (N == 32) {
+    tmem_ld_32x32b_x32(taddr, r);
+  } else {
+    static_assert(N == 16, "tmem_ld_cols");
+    tmem_ld_32x32b_x16(taddr, r);
+  }
+}
+template <int N>
+__device__ __forceinline__ void tmem_st_cols(uint32_t taddr, const uint32_t (&r)[N]) {
+  if constexpr (N == 32) {
+    tmem_st_32x32b_x32(taddr, r);
+  } else {
+    static_assert(N == 16, "tmem_st_cols");
+    tmem_st_32x32b_x16(taddr, r);
+  }
+}
+
+template <int DH, int CG, bool CAUSAL>
+__global__ void __launch_bounds__(FwdCfg<DH, CG>::THREADS, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                     const __grid_constant__ CUtensorMap map_v, const int32_t* __restrict__ cu,
                     const int2* __restrict__ tiles, const int* __restrict__ n_tiles, __nv_bfloat16* __restrict__ out,
                     int ldo, float* __restrict__ lse, int T, int H, int Hk, float scale2) {
-  using C = FwdCfg<DH>;
-  constexpr int KVS = C::KVS, NOB = C::NOB, TB = C::TILE;
+  using C = FwdCfg<DH, CG>;
+  constexpr int KVS = C::KVS, NOB = C::NOB, TB = C::TILE, CW = C::CW, SMX = C::SMX;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* sm = align_smem_1024(smem_raw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::BAR);
@@ -184,11 +221,11 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       mbar_init(&q_full[b], 1);
       mbar_init(&q_empty[b], 1);
       mbar_init(&s_full[b], 1);
-      mbar_init(&s_empty[b], 256);
-      mbar_init(&p_full[b], 256);
+      mbar_init(&s_empty[b], SMX);
+      mbar_init(&p_full[b], SMX);
       mbar_init(&p_empty[b], 1);
       mbar_init(&o_full[b], 1);
-      mbar_init(&o_empty[b], 256);
+      mbar_init(&o_empty[b], SMX);
     }
     for (int s = 0; s < KVS; ++s) {
       mbar_init(&k_full[s], 1);
@@ -203,6 +240,12 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if constexpr (CG == 4) {  // registers from the TMA/MMA warpgroup to the 16 softmax warps
+    if (warp < 4)
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(C::REG_LO));
+    else
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(C::REG_HI));
+  }
 
   if (warp == 0) {
     if (lane == 0) {
@@ -233,24 +276,26 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     {
       constexpr uint32_t idesc_s = idesc_bf16_f32(BQ, BKV, false, false);
       constexpr uint32_t idesc_o = idesc_bf16_f32(BQ, DH, false, true);
-      // PV of global tile gp (item-local index ip, item counter jp) into O buffer ob
+      // PV of global tile gp (item-local index ip, item counter jp) into O set ob
       auto issue_pv = [&](int gp, int ip, int jp, int ob) {
         const int pb = gp & 1;
-        if (ip == 0) mbar_wait(&o_empty[ob], ((jp / NOB) & 1) ^ 1);  // epilogue of the item that last used O[ob]
+        if (ip == 0) mbar_wait(&o_empty[ob], ((jp / NOB) & 1) ^ 1);  // epilogue of the item that last used O set ob
         mbar_wait(&p_full[pb], (gp >> 1) & 1);
         mbar_wait(&v_full[gp % KVS], (gp / KVS) & 1);
         tc_fence_after();
         const uint32_t v_base = smem_u32(sm + C::V + (gp % KVS) * TB);
-        // keys [0,64) accumulate into O_a, keys [64,128) into O_b: each softmax half keeps its own
-        // running max, so the halves never synchronise inside the KV loop.  A = P from TMEM: half
-        // h's bf16 pairs sit in the first 32 columns of its 64 score columns of S buffer pb.
-        // B = V as an MN-major operand: DH/64 swizzle atoms 16 KB apart (LBO), 8-key groups 1 KB (SBO).
+        // keys of column group c accumulate into O_c: each group keeps its own running max, so
+        // the groups never synchronise inside the KV loop.  A = P from TMEM: group c's bf16
+        // pairs sit in the first CW/2 of its CW score columns of S buffer pb.  B = V as an
+        // MN-major operand: DH/64 swizzle atoms 16 KB apart (LBO), 8-key groups 1 KB (SBO).
         if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < BKV / 16; ++kk)
-            umma_bf16_ts(tmem + 256 + ob * 2 * DH + (kk >> 2) * DH, tmem + pb * BKV + (kk >> 2) * 64 + (kk & 3) * 8,
+          for (int kk = 0; kk < BKV / 16; ++kk) {
+            const int c = kk / (CW / 16), kc = kk % (CW / 16);
+            umma_bf16_ts(tmem + 256 + (ob * CG + c) * DH, tmem + pb * BKV + c * CW + kc * 8,
                          sdesc((v_base >> 4) + kk * 128, DH == 64 ? 8192 : 16384, 1024), idesc_o,
-                         (ip > 0 || (kk & 3) > 0) ? 1u : 0u);
+                         (ip > 0 || kc > 0) ? 1u : 0u);
+          }
           umma_commit(&v_empty[gp % KVS]);
           umma_commit(&p_empty[pb]);
         }
@@ -305,16 +350,15 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       }
       flush();
     }
-  } else {
-    // Two warps per TMEM lane quadrant split the 128 key columns of a tile (half 0: [0,64),
-    // half 1: [64,128)).  Each half runs its own online softmax (max, sum, lazy rescale) into its
-    // own O accumulator; the halves combine once per item in the epilogue (named barrier per
-    // quadrant pair), each normalising and storing DH/2 of the DH output columns.
+  } else if (warp >= C::SW0) {
+    // Softmax: warp (SW0 + 4 grp + q) owns TMEM lane quadrant q (rows 32q..32q+31) and key columns
+    // [grp*CW, grp*CW + CW) of every tile.  The groups combine once per item in the epilogue
+    // (named barrier per quadrant), each normalising and storing DH/CG of the DH output columns.
     const int q = warp & 3;
-    const int half = (warp - 2) >> 2;
+    const int grp = (warp - C::SW0) >> 2;
     const int r = q * 32 + lane;
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
-    const int pair_bar = 2 + q;
+    const int quad_bar = 2 + q;
     float* xmax = reinterpret_cast<float*>(sm + C::XMAX);
     float* xsum = reinterpret_cast<float*>(sm + C::XSUM);
     // Epilogue of item jj (final m / l), deferred until after the next item's first tile: by
@@ -322,46 +366,61 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     auto epilogue = [&](const FwdItem& it, int jj, float m, float l) {
       const int ob = jj % NOB;
       const int qpos = it.q0 + r;
-      // exchange (m, l) with the partner half, O = (O_a 2^(m_a - M) + O_b 2^(m_b - M)) / l for
-      // this half's DH/2 columns
-      float* xm = xmax + (jj & 1) * 256;  // by item parity: the partner reads it before the next item's barrier
-      float* xs = xsum + (jj & 1) * 256;
-      xm[half * 128 + r] = m;
-      xs[half * 128 + r] = l;
+      float* xm = xmax + (jj & 1) * CG * 128;  // by item parity: the groups read it before the next item's barrier
+      float* xs = xsum + (jj & 1) * CG * 128;
+      xm[grp * 128 + r] = m;
+      xs[grp * 128 + r] = l;
       mbar_wait(&o_full[ob], (jj / NOB) & 1);
       tc_fence_after();
-      named_bar(pair_bar, 64);
-      const float m_o = xm[(half ^ 1) * 128 + r], l_o = xs[(half ^ 1) * 128 + r];
-      const float ma = half == 0 ? m : m_o, mb = half == 0 ? m_o : m;
-      const float la = half == 0 ? l : l_o, lb = half == 0 ? l_o : l;
-      const float M = fmaxf(ma, mb);
-      const float sa = ma == -INFINITY ? 0.f : ex2(ma - M), sb = mb == -INFINITY ? 0.f : ex2(mb - M);
-      const float l_all = la * sa + lb * sb;
-      const float rl = __frcp_rn(l_all);
-      const float fa = sa * rl, fb = sb * rl;
+      named_bar(quad_bar, 32 * CG);
+      float mg[CG], lg[CG];
+      float M = -INFINITY;
 #pragma unroll
-      for (int sub = 0; sub < DH / 64; ++sub) {
-        const int c0 = half * (DH / 2) + sub * 32;
-        uint32_t ra[32], rb[32];
-        tmem_ld_32x32b_x32(tmem + lane_base + 256 + ob * 2 * DH + c0, ra);
-        tmem_ld_32x32b_x32(tmem + lane_base + 256 + ob * 2 * DH + DH + c0, rb);
-        tmem_ld_wait();
-        if (sub == DH / 64 - 1) {
+      for (int c = 0; c < CG; ++c) {
+        mg[c] = xm[c * 128 + r];
+        lg[c] = xs[c * 128 + r];
+        M = fmaxf(M, mg[c]);
+      }
+      float l_all = 0.f, fct[CG];
+#pragma unroll
+      for (int c = 0; c < CG; ++c) {
+        fct[c] = mg[c] == -INFINITY ? 0.f : ex2(mg[c] - M);
+        l_all += lg[c] * fct[c];
+      }
+      const float rl = __frcp_rn(l_all);
+#pragma unroll
+      for (int c = 0; c < CG; ++c) fct[c] *= rl;
+      // this group's DH/CG output columns, in chunks of 16 or 32
+      constexpr int OC = DH / CG;                      // 32 (DH 64, CG 2 / DH 128 ... ) or 16 (DH 64, CG 4)
+      constexpr int CH = OC >= 32 ? 32 : OC;           // columns per TMEM load
+#pragma unroll
+      for (int sub = 0; sub < OC / CH; ++sub) {
+        const int c0 = grp * OC + sub * CH;
+        float acc[CH];
+#pragma unroll
+        for (int e = 0; e < CH; ++e) acc[e] = 0.f;
+#pragma unroll
+        for (int c = 0; c < CG; ++c) {
+          uint32_t ra[CH];
+          tmem_ld_cols<CH>(tmem + lane_base + 256 + (ob * CG + c) * DH + c0, ra);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < CH; ++e) acc[e] = fmaf(__uint_as_float(ra[e]), fct[c], acc[e]);
+        }
+        if (sub == OC / CH - 1) {
           tc_fence_before();
           mbar_arrive(&o_empty[ob]);
         }
         if (qpos < it.L) {
-          uint32_t o[16];
+          uint32_t o[CH / 2];
 #pragma unroll
-          for (int e = 0; e < 16; ++e)
-            o[e] = pack_bf16(__uint_as_float(ra[2 * e]) * fa + __uint_as_float(rb[2 * e]) * fb,
-                             __uint_as_float(ra[2 * e + 1]) * fa + __uint_as_float(rb[2 * e + 1]) * fb);
+          for (int e = 0; e < CH / 2; ++e) o[e] = pack_bf16(acc[2 * e], acc[2 * e + 1]);
           uint4* dst = reinterpret_cast<uint4*>(out + (size_t)(it.s0 + qpos) * ldo + it.h * DH + c0);
 #pragma unroll
-          for (int u = 0; u < 4; ++u) dst[u] = make_uint4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);
+          for (int u = 0; u < CH / 8; ++u) dst[u] = make_uint4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);
         }
       }
-      if (half == 0 && qpos < it.L) lse[(size_t)it.h * T + it.s0 + qpos] = (M + log2f(l_all)) * LN2_F;
+      if (grp == 0 && qpos < it.L) lse[(size_t)it.h * T + it.s0 + qpos] = (M + log2f(l_all)) * LN2_F;
     };
     int g = 0, j = 0;
     bool pend = false;
@@ -382,30 +441,30 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
         const int b = g & 1;
         mbar_wait(&s_full[b], (g >> 1) & 1);
         tc_fence_after();
-        float s[64];
+        float s[CW];
         {
-          uint32_t raw[2][32];
-          tmem_ld_32x32b_x32(tmem + lane_base + b * BKV + half * 64, raw[0]);
-          tmem_ld_32x32b_x32(tmem + lane_base + b * BKV + half * 64 + 32, raw[1]);
+          uint32_t raw[CW / 32][32];
+#pragma unroll
+          for (int c = 0; c < CW / 32; ++c) tmem_ld_32x32b_x32(tmem + lane_base + b * BKV + grp * CW + 32 * c, raw[c]);
           tmem_ld_wait();
 #pragma unroll
-          for (int c = 0; c < 2; ++c)
+          for (int c = 0; c < CW / 32; ++c)
 #pragma unroll
             for (int jj = 0; jj < 32; ++jj) s[c * 32 + jj] = __uint_as_float(raw[c][jj]);
         }
         tc_fence_before();
         mbar_arrive(&s_empty[b]);
-        const int kv0 = i * BKV + half * 64;
-        const bool need_mask = (CAUSAL && kv0 + 63 > it.q0) || (kv0 + 64 > it.L);
+        const int kv0 = i * BKV + grp * CW;
+        const bool need_mask = (CAUSAL && kv0 + CW - 1 > it.q0) || (kv0 + CW > it.L);
         // valid key columns of this row: c < lim (causal: key <= query; key inside the sequence)
         const int lim = CAUSAL ? min(qpos - kv0 + 1, it.L - kv0) : it.L - kv0;
         if (need_mask && __all_sync(kFull, lim <= 0)) {
-          // every row of this warp sees only masked keys in this half-tile (upper triangle of the
-          // diagonal tile): P = 0, running max and sum unchanged
-          uint32_t zero[32];
+          // every row of this warp sees only masked keys in this group's columns (upper triangle
+          // of the diagonal tile): P = 0, running max and sum unchanged
+          uint32_t zero[CW / 2];
 #pragma unroll
-          for (int e = 0; e < 32; ++e) zero[e] = 0u;
-          tmem_st_32x32b_x32(tmem + lane_base + b * BKV + half * 64, zero);
+          for (int e = 0; e < CW / 2; ++e) zero[e] = 0u;
+          tmem_st_cols<CW / 2>(tmem + lane_base + b * BKV + grp * CW, zero);
           tmem_st_wait();
           tc_fence_before();
           mbar_arrive(&p_full[b]);
@@ -418,13 +477,13 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
         float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
         if (need_mask) {
 #pragma unroll
-          for (int c = 0; c < 64; ++c) {
+          for (int c = 0; c < CW; ++c) {
             s[c] = c < lim ? s[c] : -INFINITY;
             mx4[c & 3] = fmaxf(mx4[c & 3], s[c]);
           }
         } else {
 #pragma unroll
-          for (int c = 0; c < 64; ++c) mx4[c & 3] = fmaxf(mx4[c & 3], s[c]);
+          for (int c = 0; c < CW; ++c) mx4[c & 3] = fmaxf(mx4[c & 3], s[c]);
         }
         const float m_new = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * scale2;
         bool rescale = false;
@@ -434,12 +493,12 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
           m = m_new;
           rescale = i > 0;
         }
-        const float neg_m = m == -INFINITY ? 0.f : -m;  // half fully masked so far: P = 0
+        const float neg_m = m == -INFINITY ? 0.f : -m;  // group fully masked so far: P = 0
         // paired fp32 FMA/add (FFMA2/FADD2): half the issue slots of the scalar forms
         const float2 sc2 = make_float2(scale2, scale2), nm2 = make_float2(neg_m, neg_m);
         float2 sum2[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
 #pragma unroll
-        for (int c = 0; c < 64; c += 2) {
+        for (int c = 0; c < CW; c += 2) {
           const float2 x = __ffma2_rn(make_float2(s[c], s[c + 1]), sc2, nm2);
           if ((FWD_EMU_BITS >> ((c >> 1) & 7)) & 1) {
             const float2 e = ex2_fma2<3>(x);
@@ -463,21 +522,21 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
 #pragma unroll
           for (int c = 0; c < DH / 32; ++c) {
             uint32_t rr[32];
-            tmem_ld_32x32b_x32(tmem + lane_base + 256 + ob * 2 * DH + half * DH + c * 32, rr);
+            tmem_ld_32x32b_x32(tmem + lane_base + 256 + (ob * CG + grp) * DH + c * 32, rr);
             tmem_ld_wait();
 #pragma unroll
             for (int jj = 0; jj < 32; ++jj) rr[jj] = __float_as_uint(__uint_as_float(rr[jj]) * alpha);
-            tmem_st_32x32b_x32(tmem + lane_base + 256 + ob * 2 * DH + half * DH + c * 32, rr);
+            tmem_st_32x32b_x32(tmem + lane_base + 256 + (ob * CG + grp) * DH + c * 32, rr);
           }
           tmem_st_wait();
         }
-        // P (bf16 pairs) over the first 32 of this half's score columns: S_{g+2} is issued after
-        // PV_g, so the buffer is not rewritten before the tensor core has read P
+        // P (bf16 pairs) over the first CW/2 of this group's score columns: S_{g+2} is issued
+        // after PV_g, so the buffer is not rewritten before the tensor core has read P
         {
-          uint32_t pk[32];
+          uint32_t pk[CW / 2];
 #pragma unroll
-          for (int e = 0; e < 32; ++e) pk[e] = pack_bf16(s[2 * e], s[2 * e + 1]);
-          tmem_st_32x32b_x32(tmem + lane_base + b * BKV + half * 64, pk);
+          for (int e = 0; e < CW / 2; ++e) pk[e] = pack_bf16(s[2 * e], s[2 * e + 1]);
+          tmem_st_cols<CW / 2>(tmem + lane_base + b * BKV + grp * CW, pk);
         }
         tmem_st_wait();
         tc_fence_before();
@@ -1206,17 +1265,26 @@ MAESTRO_API int maestro_attn_fwd(const void* q, const void* k, const void* v, co
   const int items = max_tiles * H;  // upper bound; the kernel reads the true count
   dim3 grid(items < num_sms() ? items : num_sms());
   const float scale2 = softmax_scale * LOG2E_F;
-#define MB_ATTN_FWD(D, CZ)                                                                                \
+#define MB_ATTN_FWD(D, G, CZ)                                                                             \
   {                                                                                                       \
-    const int smem = FwdCfg<D>::TOTAL + 1024;                                                             \
-    if (ensure_smem<attn_fwd_kernel<D, CZ>>(smem)) return launch_status();                                \
-    attn_fwd_kernel<D, CZ><<<grid, FWD_THREADS, smem, st>>>(mq, mk, mv, cu, tiles, count, (__nv_bfloat16*)out, \
-                                                           ldo, lse, T, H, Hk, scale2);                   \
+    using CF = FwdCfg<D, G>;                                                                              \
+    const int smem = CF::TOTAL + 1024;                                                                    \
+    if (ensure_smem<attn_fwd_kernel<D, G, CZ>>(smem)) return launch_status();                             \
+    attn_fwd_kernel<D, G, CZ><<<grid, CF::THREADS, smem, st>>>(mq, mk, mv, cu, tiles, count,               \
+                                                              (__nv_bfloat16*)out, ldo, lse, T, H, Hk, scale2); \
   }
-  if (head_dim == 64) {
-    if (causal) MB_ATTN_FWD(64, true) else MB_ATTN_FWD(64, false)
+  // column groups per tile (head_dim 64): 4 (16 softmax warps) or 2 (8); MAESTRO_ATTN_CG overrides
+  static const int cg_env = [] {
+    const char* e = getenv("MAESTRO_ATTN_CG");
+    return e ? atoi(e) : 0;
+  }();
+  const int cg = cg_env == 2 || cg_env == 4 ? cg_env : ATTN_FWD_CG64;
+  if (head_dim == 64 && cg == 4) {
+    if (causal) MB_ATTN_FWD(64, 4, true) else MB_ATTN_FWD(64, 4, false)
+  } else if (head_dim == 64) {
+    if (causal) MB_ATTN_FWD(64, 2, true) else MB_ATTN_FWD(64, 2, false)
   } else {
-    if (causal) MB_ATTN_FWD(128, true) else MB_ATTN_FWD(128, false)
+    if (causal) MB_ATTN_FWD(128, 2, true) else MB_ATTN_FWD(128, 2, false)
   }
 #undef MB_ATTN_FWD
   return launch_status();
