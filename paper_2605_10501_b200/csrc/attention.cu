@@ -70,6 +70,9 @@ __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.syn
 #ifndef BWD_EMU_BITS
 #define BWD_EMU_BITS 0x00  // backward P^T = exp2(S^T scale2 - lse2): not MUFU-bound, all on MUFU
 #endif
+#ifndef ATTN_SETMAXNREG
+#define ATTN_SETMAXNREG 0
+#endif
 #ifndef ATTN_FWD_CG64
 #define ATTN_FWD_CG64 2  // default column groups of the head_dim-64 forward (see FwdCfg)
 #endif
@@ -115,9 +118,9 @@ template <int DH, int CG>
 struct FwdCfg {
   // w0 TMA, w1 MMA, softmax warps from SW0 on (CG per lane quadrant).  CG = 4: warps 2-3 idle so
   // the softmax warps fill whole warpgroups and setmaxnreg can move registers to them
-  static constexpr int SW0 = CG == 4 ? 4 : 2;
+  static constexpr int SW0 = (CG == 4 && ATTN_SETMAXNREG) ? 4 : 2;
   static constexpr int THREADS = 32 * SW0 + 128 * CG;
-  static constexpr int REG_LO = 64, REG_HI = 112;     // CG = 4: TMA/MMA warpgroup, softmax warpgroups
+  static constexpr int REG_LO = 88, REG_HI = 104;     // CG = 4: TMA/MMA warpgroup, softmax warpgroups
   static constexpr int SMX = 128 * CG;                // softmax threads
   static constexpr int CW = BKV / CG;                 // key columns per group
   static constexpr int TILE = 128 * DH * 2;           // bytes of a 128-row tile
@@ -240,7 +243,7 @@ __global__ void __launch_bounds__(FwdCfg<DH, CG>::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  if constexpr (CG == 4) {  // registers from the TMA/MMA warpgroup to the 16 softmax warps
+  if constexpr (CG == 4 && ATTN_SETMAXNREG) {  // registers from the TMA/MMA warpgroup to the 16 softmax warps
     if (warp < 4)
       asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(C::REG_LO));
     else

@@ -18,6 +18,9 @@ for _ in range(3):
     if mode == "swiglu":
         s = torch.empty(M, N // 2, device="cuda", dtype=torch.bfloat16)
         dense.linear_fwd_swiglu(a, w, s)
+    elif mode == "swiglu_only":  # forward-only sections: only silu(g) * u is stored
+        s = torch.empty(M, N // 2, device="cuda", dtype=torch.bfloat16)
+        dense.linear_fwd_swiglu(a, w, s, store_gu=False)
     elif mode == "residual":
         r = torch.randn(M, N, device="cuda").bfloat16()
         dense.linear_fwd_residual(a, w, r)
