@@ -32,7 +32,8 @@ Data between sections moves through per-step row buffers, placed by the K5b hand
 
 With ``torch.distributed`` initialised every section is data-parallel over all ranks (the
 co-located layout: each GPU hosts one rank of every section, fan-out 1) and each section's
-gradients are averaged over the group before its optimizer (C2).  ``KDExecutor`` / ``VLMExecutor``
+gradients are summed over the group before its optimizer (C2; the loss scales use the global
+batch's label / token counts, so the sum is the global gradient).  ``KDExecutor`` / ``VLMExecutor``
 are the tuned special cases of this contract for cfg 2/5 and cfg 1 (plan-ahead, disjoint GPU
 groups); ``tests/test_graph_exec.py`` checks that this executor reproduces their steps.
 """
@@ -427,7 +428,7 @@ class SectionGraphExecutor:
             if not progressed:
                 blocked = tuple(r for r in stages if head[r] < len(stages[r]))
                 raise DependencyDeadlock(f"no enqueueable stage; blocked resources: {blocked}", resources=blocked)
-        # ---- per-section gradient average (C2) and optimizers, on each section's stream
+        # ---- per-section gradient all-reduce (C2, sum) and optimizers, on each section's stream
         dist = _dist()
         for sec, mod in self.mod.items():
             if not mod.trainable:
@@ -435,8 +436,9 @@ class SectionGraphExecutor:
             stream = self.streams[sec]
             with torch.cuda.stream(stream):
                 if dist is not None and self.world > 1:
+                    # every rank scaled its loss by the GLOBAL label / token counts (all ranks see
+                    # the whole host batch), so the global gradient is the sum over ranks
                     dist.all_reduce(mod.p.grad, group=self.dp_group)
-                    mod.p.grad.mul_(1.0 / self.world)
                 mod.p.adamw(self.lr)
         for r in self.streams.values():
             main.wait_stream(r)
