@@ -184,6 +184,13 @@ class KDExecutor:
         self.tokens[self._bits["teacher"]] = seq
         self.planner.ids[: self.batch].copy_(torch.arange(self.batch, dtype=torch.int32))
         self.groups = self._make_groups()
+        # C2 overlapped with the last student micro-batch's backward (gradsync.GradSync)
+        self.gsync = None
+        if _dist() is not None and self.student is not None and dp_s > 1 and os.environ.get(
+                "MAESTRO_C2_OVERLAP", "1") != "0":
+            from .gradsync import GradSync
+
+            self.gsync = GradSync(self.student.p, self.sshape.layers, group=self.groups.get("student"), device=dev)
         if not colocated and handoff_mode() == "nccl":
             N.reserve_sms_for_comm()  # NCCL handoff kernels run concurrently with the section compute
         self.step_idx = 0
@@ -334,7 +341,10 @@ class KDExecutor:
                 if dist is not None and self.dp_s > 1:
                     ar = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                     ar[0].record(self.s_stream)
-                    dist.all_reduce(self.student.p.grad, group=self.groups.get("student"))
+                    if self.gsync is not None:  # per-layer buckets already in flight: the tail only
+                        self.gsync.finish(self.s_stream)
+                    else:
+                        dist.all_reduce(self.student.p.grad, group=self.groups.get("student"))
                     dist.all_reduce(loss_acc, group=self.groups.get("student"))
                     ar[1].record(self.s_stream)
                 self.student.p.adamw(self.lr)
@@ -378,7 +388,7 @@ class KDExecutor:
         K.positions(cu, cu.numel() - 1, pos)
         return pos
 
-    def _student_mb(self, yf_t, packed, cu, start, T, loss_acc, global_tokens, clock, m):
+    def _student_mb(self, yf_t, packed, cu, start, T, loss_acc, global_tokens, clock, m, last=False):
         b = Batch(ids=packed[start: start + T], cu=cu, pos=self._positions(cu, T), max_len=self.seq)
         clock.begin(self.s_stream, f"f_c{m}")
         yf, ctx = self.student.forward(b)
@@ -393,7 +403,11 @@ class KDExecutor:
         del t_logits
         clock.end(self.s_stream)
         clock.begin(self.s_stream, f"b_c{m}")
-        self.student.backward(ctx, dlogits=s_logits)
+        hook = None
+        if last and self.gsync is not None:  # this backward finalises every layer's gradient
+            self.gsync.begin()
+            hook = self.gsync.layer_done
+        self.student.backward(ctx, dlogits=s_logits, layer_hook=hook)
         clock.end(self.s_stream)
 
     def _mb_cu(self, plan_sec, m, T):
@@ -429,7 +443,7 @@ class KDExecutor:
                 T = hs[0][m]
                 o = hs[1][m] - ht[1][k]
                 self._student_mb(outs[k][o: o + T], packed["student"], self._mb_cu(ps, m, T), hs[1][m], T, loss_acc,
-                                 global_tokens, clock, m)
+                                 global_tokens, clock, m, last=m == ps["n_mb"] - 1)
                 if m % ratio == ratio - 1 or m == ps["n_mb"] - 1:
                     outs[k].record_stream(self.s_stream)
                     outs[k] = None
@@ -494,7 +508,7 @@ class KDExecutor:
                     cur_start = hs[1][m]
                 o = hs[1][m] - cur_start
                 self._student_mb(cur[o: o + T], packed["student"], self._mb_cu(ps, m, T), hs[1][m], T, loss_acc,
-                                 global_tokens, clock, m)
+                                 global_tokens, clock, m, last=m == ps["n_mb"] - 1)
 
     def verify_handoff(self):
         """Check the deferred control headers of this step's pulls (sample ids in schedule order)."""

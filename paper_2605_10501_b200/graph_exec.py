@@ -241,6 +241,15 @@ class SectionGraphExecutor:
         self.lr = lr
         self.step_idx = 0
         self._h_err = torch.empty(1, dtype=torch.int64).pin_memory()
+        # C2 of the critical section overlapped with its last micro-batch's backward
+        self.gsync = None
+        import os
+
+        if dist is not None and self.world > 1 and os.environ.get("MAESTRO_C2_OVERLAP", "1") != "0":
+            from .gradsync import GradSync
+
+            cm = self.mod[self.crit]
+            self.gsync = GradSync(cm.p, cm.s.layers, group=dp_group, device=dev)
 
     # ---------------------------------------------------------------- planning (device, K1-K5)
     def _tokens(self, gb: GraphBatch) -> np.ndarray:
@@ -438,7 +447,10 @@ class SectionGraphExecutor:
                 if dist is not None and self.world > 1:
                     # every rank scaled its loss by the GLOBAL label / token counts (all ranks see
                     # the whole host batch), so the global gradient is the sum over ranks
-                    dist.all_reduce(mod.p.grad, group=self.dp_group)
+                    if sec == self.crit and self.gsync is not None:
+                        self.gsync.finish(stream)  # per-layer buckets already in flight
+                    else:
+                        dist.all_reduce(mod.p.grad, group=self.dp_group)
                 mod.p.adamw(self.lr)
         for r in self.streams.values():
             main.wait_stream(r)
@@ -575,7 +587,12 @@ class SectionGraphExecutor:
                 scatter_mb(c["down"][sec]["ix"], m, c["down"][sec]["gbuf"], dyf, accumulate=True)
 
         need_dx0 = any(self.mod[s].trainable and self.mod[s].kind == "features" for s in self.ups)
-        dx0 = mod.model.backward(sc["ctx"], dlogits=sc["logits"], need_dx0=True, dyf_hook=hook if self.downs else None)
+        layer_hook = None
+        if self.gsync is not None and m == len(c["mb_c"]) - 1:  # the last b_c finalises every layer
+            self.gsync.begin()
+            layer_hook = self.gsync.layer_done
+        dx0 = mod.model.backward(sc["ctx"], dlogits=sc["logits"], need_dx0=True, dyf_hook=hook if self.downs else None,
+                                 layer_hook=layer_hook)
         K.embed_bwd(dx0, sc["ids"], mod.p.g("embed"))
         if need_dx0:
             for sec in self.ups:

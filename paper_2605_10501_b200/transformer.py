@@ -303,10 +303,12 @@ class Transformer:
 
     # -------------------------------------------------------------------- backward
     def backward(self, ctx, dlogits: torch.Tensor | None = None, dyf: torch.Tensor | None = None,
-                 need_dx0: bool = False, dyf_hook=None):
+                 need_dx0: bool = False, dyf_hook=None, layer_hook=None):
         """Accumulates parameter grads (fp32) from dlogits (or dyf); returns dx0 if asked.
         ``dyf_hook(dyf)`` may add further gradient into the final hidden state's gradient (e.g. a
-        downstream section's) before the stack's backward."""
+        downstream section's) before the stack's backward; ``layer_hook(i)`` runs (on the current
+        stream) once layer i's parameter gradients of this call have been enqueued -- the per-layer
+        buckets of an overlapped gradient all-reduce (gradsync.GradSync)."""
         s, p, b = self.s, self.p, ctx["b"]
         T, dev, bf = b.T, self.device, torch.bfloat16
         H, Hk, dh = s.heads, s.kv_heads, s.head_dim
@@ -348,6 +350,8 @@ class Transformer:
             dh1 = torch.empty(T, s.d, device=dev, dtype=bf)
             K.rmsnorm_bwd(dy1, h1, p[f"l{i}.ln1"], r1, dh2, dh1, p.g(f"l{i}.ln1"))
             dh_ = dh1
+            if layer_hook is not None:
+                layer_hook(i)
         if need_dx0:
             return dh_
         K.embed_bwd(dh_, b.ids, p.g("embed"))
