@@ -550,7 +550,12 @@ def run_kd(args):
                                   "(mostly waiting for SMs); isolated_us: the same plan alone on an idle GPU "
                                   "(roofline computed on it)"},
             "grad_allreduce": ({"ms": ar_ms, "bytes": grad_bytes,
-                                "bus_GBps": 2 * (dp_s - 1) / dp_s * grad_bytes / (ar_ms / 1e3) / 1e9 if ar_ms else None}
+                                "overlapped": ex.gsync is not None,
+                                "note": ("ms = the exposed tail after the student backward; the per-layer buckets "
+                                         "run during the last micro-batch's backward (gradsync.GradSync)"
+                                         if ex.gsync is not None else "ms = the whole all-reduce after the backward"),
+                                "bus_GBps": (2 * (dp_s - 1) / dp_s * grad_bytes / (ar_ms / 1e3) / 1e9
+                                             if ar_ms and ex.gsync is None else None)}
                                if dp_s > 1 else None),
             "handoff": (None if ex.colocated else
                         {"bytes_per_step": int(B // max(dp_s, 1) * seq * ex.tshape.d * 2),
