@@ -637,7 +637,7 @@ def run_vlm(args):
     clocks.start()
     # the co-resident executor plans the next step's batch beside the current step (the batch of
     # step i+1 is known at step i, as with a prefetching loader)
-    nxt = {"next_hb": hb} if isinstance(ex, VLMExecutor) else {}
+    nxt = {"next_hb": hb}  # both executors plan the next batch beside the current step
     for _ in range(args.warmup):
         ex.step(hb, want_loss=False, **nxt)
     barrier()

@@ -310,12 +310,18 @@ struct View {  // current partial order, SoA in smem
   }
 };
 
-// Visit candidate elements in order: view[0..p), x, view[p..len)
+// Visit candidate elements in order: view[0..p), x, view[p..len).  One loop of len + 1 steps
+// with the element chosen by index (cur[j] before p, x at p, cur[j-1] after), so every thread of
+// a warp runs the same trip count -- no divergent loop nests -- and the unrolled body issues the
+// next elements' shared-memory loads ahead of the dependent fp64 recurrence.
 template <class F>
 __device__ __forceinline__ void for_candidate(const View& v, int len, int p, const Sample6& x, F&& f) {
-  for (int j = 0; j < p; ++j) f(v.at(j));
-  f(x);
-  for (int j = p; j < len; ++j) f(v.at(j));
+#pragma unroll 4
+  for (int j = 0; j <= len; ++j) {
+    Sample6 s = v.at(j - (j > p ? 1 : 0));  // j == p reads a stale slot (< cap), replaced by x
+    if (j == p) s = x;
+    f(s);
+  }
 }
 
 struct Metrics {

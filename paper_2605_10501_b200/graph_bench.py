@@ -60,9 +60,7 @@ def _cpu_sample(graph: str, layers_full: int):
         d = lambda s: dataclasses.replace(s, layers=L)  # noqa: E731
         if graph == "vlm7b":
             vit, llm = d(W.QWEN_VIT), d(W.QWEN_7B)
-            gb = W.vlm7b_batch(2, seed=1, vocab=llm.vocab, patch_dim=W.PATCH_DIM, lo=1024, hi=1024)
-            gb.up["vit"].in_len[:] = 1024
-            gb.up["vit"].rows[:] = 256
+            gb = W.vlm7b_batch(2, seed=1, vocab=llm.vocab, patch_dim=W.PATCH_DIM, lo=1024, hi=1024)  # 1 image + 1 text
             ups = {"vit": (vit, flat(vit, [("in_w", (vit.d, W.PATCH_DIM)), ("proj_w", (llm.d, 4 * vit.d))]),
                            W.PATCH_DIM, 4)}
             downs = {}

@@ -500,19 +500,52 @@ class VLMGroupExecutor:
         self.step_idx = 0
 
     # ------------------------------------------------------------------ plan (host view)
-    def _orders(self, hb):
+    def _plan_async(self, hb, stream):
+        """Enqueue K1-K4 for ``hb`` on ``stream`` and an asynchronous readback of the orders, the
+        rank offsets and the error word into pinned host buffers; returns the readback event."""
         dev, B = self.device, self.batch
         tok = np.zeros((len(self.bits), B), dtype=np.int32)
         tok[self.bits["llm"]] = hb["lens"]
         tok[self.bits["vit"]] = np.where(hb["has_img"], R.VIT_PATCHES, 0)
-        tokens = _h2d(tok, dev)
-        self.planner.ids[:B].copy_(torch.arange(B, dtype=torch.int32))
-        self.planner.plan_tokens(self.cost, tokens, B)
+        if not hasattr(self, "_h_orders"):
+            n_sec = len(self.graph.tables.section_ids)
+            self._h_orders = torch.empty(n_sec * B, dtype=torch.int32).pin_memory()
+            self._h_off = torch.empty(n_sec * (N.MAX_DP + 1), dtype=torch.int32).pin_memory()
+            self._h_err = torch.empty(1, dtype=torch.int64).pin_memory()
+        with torch.cuda.stream(stream):
+            tokens = _h2d(tok, dev)
+            self.planner.ids[:B].copy_(_h2d(np.arange(B, dtype=np.int32), dev))
+            self.planner.plan_tokens(self.cost, tokens, B, stream)
+            self._h_orders.copy_(self.planner.orders[: self._h_orders.numel()], non_blocking=True)
+            self._h_off.copy_(self.planner.sec_off, non_blocking=True)
+            self._h_err.copy_(self.planner.err, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+        return ev
+
+    def _orders(self, hb, main, next_hb=None):
+        """Rank orders of ``hb``: from a plan enqueued ahead by the previous step (plan-ahead) or
+        planned now; with ``next_hb`` the next batch's plan is enqueued on a side stream so it
+        overlaps this step (the host reads it at the next step without a device round trip)."""
+        B = self.batch
+        pend, self._pending = getattr(self, "_pending", None), None
+        if pend is not None and pend[0] is hb:
+            ev = pend[1]
+        else:
+            if pend is not None:
+                pend[1].synchronize()  # a plan for another batch still writes the same buffers
+            ev = self._plan_async(hb, main)
+        ev.synchronize()
+        N.raise_device_error(int(self._h_err.item()), list(range(B)), self.graph.tables.section_ids)
         tab = self.graph.tables
         ci, vi = tab.critical, tab.section_ids.index("vit")
         W = N.MAX_DP + 1
-        off = self.planner.sec_off.view(-1, W).cpu().numpy()
-        orders = self.planner.orders.view(-1, B).cpu().numpy()
+        off = self._h_off.numpy().reshape(-1, W).copy()
+        orders = self._h_orders.numpy().reshape(-1, B).copy()
+        if next_hb is not None:
+            if not hasattr(self, "s_plan"):
+                self.s_plan = torch.cuda.Stream(device=self.device)
+            self._pending = (next_hb, self._plan_async(next_hb, self.s_plan))
         llm = [orders[ci, off[ci, r]: off[ci, r + 1]] for r in range(self.dp_llm)]
         vit = [orders[vi, off[vi, q]: off[vi, q + 1]] for q in range(self.dp_vit)]
         return llm, vit
@@ -528,13 +561,15 @@ class VLMGroupExecutor:
         return self._eps[key]
 
     # ------------------------------------------------------------------ one step
-    def step(self, hb: dict, want_loss: bool = True) -> StepStats:
+    def step(self, hb: dict, want_loss: bool = True, next_hb: dict | None = None) -> StepStats:
+        """One iteration; ``next_hb`` (the following step's batch) lets the step plan that batch on a
+        side stream while its own kernels run (plan-ahead, as VLMExecutor.step)."""
         dist = _dist()
         dev = self.device
         main = torch.cuda.current_stream(dev)
         t0 = torch.cuda.Event(enable_timing=True)
         t0.record(main)
-        llm_orders, vit_orders = self._orders(hb)
+        llm_orders, vit_orders = self._orders(hb, main, next_hb)
         owner = np.full(self.batch, -1, dtype=np.int64)
         for r, o in enumerate(llm_orders):
             owner[o] = r
