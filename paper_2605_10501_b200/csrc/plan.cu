@@ -329,13 +329,17 @@ struct Metrics {
   bool have_first;
 };
 
+// need_ub = false when no sample of the sequence has t_b_ac > 0 (e.g. a forward-only upstream
+// section): ub is then never read, so the pass that computes its start value is skipped -- the
+// makespan bits are unchanged.
 template <int POLICY, bool WITH_METRICS, class Seq>
-__device__ Metrics eval_order(Seq&& seq) {
+__device__ Metrics eval_order(Seq&& seq, bool need_ub = true) {
   // pass 1: u = sum of positive t_f_bc in order (ub starts there, scheduling.py:97)
   double u_total = 0.0;
-  seq([&](const Sample6& s) {
-    if (s.fbc > 0) u_total += s.fbc;
-  });
+  if (need_ub)
+    seq([&](const Sample6& s) {
+      if (s.fbc > 0) u_total += s.fbc;
+    });
   Metrics m{0.0, 0.0, 0.0, 0.0, false};
   double c = 0.0, d = 0.0, ub = u_total, u = 0.0, mk = 0.0;
   auto crit = [&](double floor_, double ready, double dur) {
@@ -474,6 +478,8 @@ __global__ void __launch_bounds__(1024) wavefront_kernel(const double* __restric
   __syncthreads();
   View cv{{cur, cur + cap, cur + 2 * cap, cur + 3 * cap, cur + 4 * cap, cur + 5 * cap}};
   View sv{{stg, stg + cap, stg + 2 * cap, stg + 3 * cap, stg + 4 * cap, stg + 5 * cap}};
+  // does any sample of this rank have a b_ac stage (the ub chain)?
+  const bool need_ub = __syncthreads_or(tid < n && stg[5 * cap + tid] > 0.0) != 0;
   if (tid == 0) {
     ord[0] = init[0];
     for (int p = 0; p < 6; ++p) cur[p * cap] = stg[p * cap];
@@ -485,7 +491,7 @@ __global__ void __launch_bounds__(1024) wavefront_kernel(const double* __restric
     double v = __longlong_as_double(0x7ff0000000000000ll);  // +inf
     int pos = 0x7fffffff;
     if (tid <= len) {
-      Metrics m = eval_order<POLICY, false>([&](auto&& f) { for_candidate(cv, len, tid, x, f); });
+      Metrics m = eval_order<POLICY, false>([&](auto&& f) { for_candidate(cv, len, tid, x, f); }, need_ub);
       v = m.mk;
       pos = tid;
     }
