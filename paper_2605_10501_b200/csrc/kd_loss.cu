@@ -8,8 +8,10 @@
 // sum_v e^{t-m}(t - s); pass 2 re-reads the rows (L2-resident: a CTA's row is < 0.6 MB and
 // just touched) and writes ds.  HBM traffic ~ 2 x V x 2 B read + V x 2 B written per token.
 #include <cuda_bf16.h>
+#include <stdlib.h>
 
 #include "common.cuh"
+#include "tma_host.cuh"
 
 namespace mb {
 namespace {
@@ -289,6 +291,23 @@ MAESTRO_API int maestro_kd_loss_fwd_bwd(const void* d_t, const void* d_s, void* 
 #define KD_UN 4
 #endif
   constexpr int TH = KD_TH, MB = KD_MB, UN = KD_UN;
+  // Experiment knob (MAESTRO_KD_ROWS_PER_SM=1): one row per SM at a time, 512 threads x 8 vector
+  // pairs in flight, so the rows touched by the first pass stay L2-resident for the second at
+  // V = 128256.  Measured slower (2840 vs 3612 GB/s at 8192 x 128256, 2936 vs 3870 at
+  // 16384 x 32000): the kernel is bound by its exponentials (2 per element per pass) as much as
+  // by HBM, and 4 rows per SM overlap them better.  Default: 4 rows per SM.
+  static const int rows_env = [] {
+    const char* e = getenv("MAESTRO_KD_ROWS_PER_SM");
+    return e ? atoi(e) : 0;
+  }();
+  const bool big = rows_env == 1;
+  if (big) {
+    const int grid = T < num_sms() ? T : num_sms();
+    kd_loss_kernel<512, 1, 8><<<grid, 512, 0, (cudaStream_t)stream>>>(
+        (const __nv_bfloat16*)d_t, (const __nv_bfloat16*)d_s, (__nv_bfloat16*)d_ds, d_loss, T, V, ldt, lds, ldd,
+        inv_tau * LOG2E, grad_scale, inv_tau);
+    return launch_status();
+  }
   const int grid = T < 148 * MB * 4 ? T : 148 * MB * 4;
   kd_loss_kernel<TH, MB, UN><<<grid, TH, 0, (cudaStream_t)stream>>>(
       (const __nv_bfloat16*)d_t, (const __nv_bfloat16*)d_s, (__nv_bfloat16*)d_ds, d_loss, T, V, ldt, lds, ldd,
