@@ -411,14 +411,14 @@ def run_kd(args):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     stalls, busy, span, stats = [], 0.0, 0.0, []
     e0.record(main_stream)
-    for _ in range(args.steps):
-        st = ex.step(ids_dev, want_loss=False, plan_ahead=True)
+    for _ in range(args.steps):  # step() does not synchronise: the host runs a step ahead
+        stats.append(ex.step(ids_dev, want_loss=False, plan_ahead=True))
+    e1.record(main_stream)
+    barrier()
+    for st in stats:  # lazy statistics, read after the timed region
         stalls.append(st.stall_frac)
         busy += st.critical_busy_ms
         span += st.critical_span_ms
-        stats.append(st)
-    e1.record(main_stream)
-    barrier()
     launches = instrument.launches - launches0
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
@@ -432,10 +432,13 @@ def run_kd(args):
     # step (H2D inside the step), the loss read back every step (D2H)
     barrier()
     w0 = time.perf_counter()
-    losses = []
+    losses, prev = [], None
     for _ in range(args.steps):
         st = ex.step(ids_host, want_loss=True, plan_ahead=True)
-        losses.append(st.loss)
+        if prev is not None:
+            losses.append(prev.loss)  # the previous step's loss, read while this step runs
+        prev = st
+    losses.append(prev.loss)
     torch.cuda.synchronize()
     w1 = time.perf_counter()
     barrier()

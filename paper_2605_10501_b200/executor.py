@@ -59,6 +59,39 @@ class StepStats:
         return 0.0 if self.critical_span_ms <= 0 else max(0.0, 1.0 - self.critical_busy_ms / self.critical_span_ms)
 
 
+class LazyKDStats:
+    """StepStats of an enqueued KDExecutor step, evaluated on first attribute access (it then
+    synchronises on the step's end event, reads the loss and checks the step's handoff headers)."""
+
+    def __init__(self, ex, t0, t1, clock, t_clock, plan_t, ar, loss_acc, global_tokens, n_msgs):
+        self._args = (ex, t0, t1, clock, t_clock, plan_t, ar, loss_acc, global_tokens, n_msgs)
+        self._st = None
+
+    def _eval(self) -> StepStats:
+        if self._st is None:
+            ex, t0, t1, clock, t_clock, plan_t, ar, loss_acc, global_tokens, n_msgs = self._args
+            t1.synchronize()
+            if n_msgs is not None:
+                want, taken = n_msgs
+                got = sorted(m.sample_id for ep, d in taken for m in ep.verify(d))  # this step's headers
+                if got != list(range(want)):
+                    from .errors import InconsistentSchedule
+
+                    raise InconsistentSchedule("handoff delivered unexpected micro-batches", got=got)
+            loss = float(loss_acc.item()) / global_tokens if loss_acc is not None else None
+            busy, span = clock.busy_span()
+            extra = {"plan_ms": plan_t[0].elapsed_time(plan_t[1]),
+                     "teacher_busy_ms": t_clock.busy_span()[0] if ex.teacher is not None else 0.0}
+            if ex.student is not None and ar is not None:
+                extra["allreduce_ms"] = ar[0].elapsed_time(ar[1])
+            self._st = StepStats(loss, t0.elapsed_time(t1), busy, span, **extra)
+            self._args = (ex, None, None, None, None, None, None, None, None, None)
+        return self._st
+
+    def __getattr__(self, name):
+        return getattr(self._eval(), name)
+
+
 class StageClock:
     """CUDA events around every stage of one resource (stream)."""
 
@@ -359,22 +392,19 @@ class KDExecutor:
         t_end = torch.cuda.Event(enable_timing=True)
         t_end.record(main)
         self.step_idx += 1
-        loss = None
-        if want_loss and loss_acc is not None:
-            loss = float(loss_acc.item()) / global_tokens
-        t_end.synchronize()
-        if self.student is not None and not self.colocated:
-            got = sorted(self.verify_handoff())  # control headers of this step's pulls
-            if got != list(range(-(-plan["student"]["n_mb"] // (self.mbs_t // self.mbs)))):
-                from .errors import InconsistentSchedule
-
-                raise InconsistentSchedule("handoff delivered unexpected micro-batches", got=got)
-        busy, span = clock.busy_span()
-        extra = {"plan_ms": plan_t[0].elapsed_time(plan_t[1]),
-                 "teacher_busy_ms": self.t_clock.busy_span()[0] if self.teacher is not None else 0.0}
-        if self.student is not None and ar is not None:
-            extra["allreduce_ms"] = ar[0].elapsed_time(ar[1])
-        return StepStats(loss, t_start.elapsed_time(t_end), busy, span, **extra)
+        # No end-of-step host synchronisation: the statistics (loss, stall, timings) and the
+        # deferred handoff-header check are evaluated on first access, and at the latest when the
+        # NEXT step has been enqueued -- so the host stays one step ahead of the device.
+        n_msgs = None
+        if self.student is not None and not self.colocated:  # this step's handoff headers, checked lazily
+            n_msgs = (-(-plan["student"]["n_mb"] // (self.mbs_t // self.mbs)),
+                      [(ep, ep.take_deferred()) for ep in getattr(self, "_h_eps", {}).values()])
+        stats = LazyKDStats(self, t_start, t_end, clock, self.t_clock, plan_t, ar,
+                            loss_acc if want_loss else None, global_tokens, n_msgs)
+        prev, self._unchecked = getattr(self, "_unchecked", None), stats
+        if prev is not None:
+            prev._eval()
+        return stats
 
     # --- co-resident sections on one GPU: the teacher stream runs ahead (upstream queue),
     # the student stream waits per micro-batch on a CUDA event.
@@ -521,6 +551,9 @@ class KDExecutor:
     def measured_events(self):
         """Device stage timestamps of the last step as simulator StageEvents (sample id = micro-batch)."""
         from .simulator import measured_events
+
+        if getattr(self, "_unchecked", None) is not None:
+            self._unchecked._eval()  # the last step has completed (its events are readable)
 
         ev = []
         if self.teacher is not None and getattr(self, "t_clock", None) is not None:

@@ -702,14 +702,22 @@ class Endpoint:
             raise IncompatibleShapes(f"fragment streams disagree: sections={sorted(sections)}, "
                                      f"samples={sorted(samples)}")
 
-    def verify(self) -> list[MessageMeta]:
-        """Decode and check the deferred headers (one host sync); returns their metadata."""
+    def take_deferred(self) -> list:
+        """Detach the deferred headers pulled so far (to verify them later with ``verify``)."""
+        out, self._deferred = self._deferred, []
+        return out
+
+    def verify(self, deferred: list | None = None) -> list[MessageMeta]:
+        """Decode and check deferred headers (one host sync): this endpoint's pending ones, or a
+        list detached earlier by ``take_deferred``; returns their metadata."""
+        lists = self._deferred if deferred is None else deferred
         out = []
-        for frags in self._deferred:
+        for frags in lists:
             metas = [f.decoded() for f in frags]
             self._check(metas)
             out.append(metas[0])
-        self._deferred.clear()
+        if deferred is None:
+            self._deferred.clear()
         return out
 
 
