@@ -453,6 +453,27 @@ def run_kd(args):
     rec = instrument.stop_timing()
     serial_ms = s0.elapsed_time(s1)
     g_flops, g_ms, g_n = rec.get("gemm", (0.0, 0.0, 0))
+    # planner calibration: fit each section's CostParams (costs.py:105-123) to the
+    # serialised step's measured stage times, then predict that step with the fitted model
+    calib = None
+    try:
+        from paper_2605_10501_b200.costs import section_iteration_time
+        from paper_2605_10501_b200.planner import fit_cost_params, kd_stage_samples
+
+        samples = kd_stage_samples(ex)
+        fpt = {k: v.flops_per_token_fwd for k, v in ex.recipe.params.items()}
+        fit = fit_cost_params(samples, fpt, ex.recipe.params)
+        pred = sum(section_iteration_time(ex.graph.section(sec), ex.configs[sec], fit[sec], seq,
+                                          ex.batch // ex.configs[sec].dp) for sec in fit)
+        calib = {"fitted": {k: {"effective_flops": v.peak_flops_per_gpu, "bwd_fwd_ratio": v.bwd_fwd_ratio}
+                            for k, v in fit.items()},
+                 "stages": len(samples), "predicted_sections_ms": pred * 1e3,
+                 "measured_sections_ms": sum(x.seconds for x in samples) * 1e3,
+                 "measured_serialized_step_ms": serial_ms,
+                 "note": "planner.fit_cost_params on the serialised step's device stage times; the fitted "
+                         "CostParams replace the presets' nominal 3e14 FLOP/s (costs.py:309,327,348)"}
+    except Exception as exc:  # noqa: BLE001
+        calib = {"error": repr(exc)}
     # the step's K1-K5 plan alone on an idle GPU (in the step it shares the SMs with the running
     # persistent kernels, so its in-step device time is mostly queueing)
     iso = []
@@ -582,6 +603,7 @@ def run_kd(args):
                                         ex.kd_loss_bytes_per_step()),
             "model_tflops": ex.model_flops_per_step() * args.steps / (ms / 1e3) / 1e12,
             "simulator_crosscheck": xcheck,
+            "planner_calibration": calib,
             "clocks": clk,
             "cpu_baseline": cpu,
             "loss": losses[-1] if losses else None,

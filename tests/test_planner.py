@@ -124,3 +124,33 @@ def test_b200_calibrated_plans():
            for k, p in kd.params.items()}
     with pytest.raises(E.CannotAvoidStall):
         PL.solve(kd.graph, PL.b200_cluster(8), par, BatchProfile(512, {"teacher": 1.0}), evaluate=False)
+
+
+def test_fit_cost_params_recovers_the_cost_model():
+    """Stage times generated by estimate_step_time (costs.py:105-123) with known knobs -> the fit
+    returns those knobs; the fitted params then predict the stages exactly."""
+    from paper_2605_10501_b200 import recipes as R
+    from paper_2605_10501_b200.costs import CostParams, estimate_step_time
+    from paper_2605_10501_b200.planner import StageSample, fit_cost_params
+    from paper_2605_10501_b200.workload import SectionConfig
+
+    g = R.kd_graph()
+    true = {"student": CostParams(flops_per_token_fwd=3e9, peak_flops_per_gpu=9.1e14, bwd_fwd_ratio=2.3,
+                                  mbs_efficiency={4: 0.8}),
+            "teacher": CostParams(flops_per_token_fwd=5e9, peak_flops_per_gpu=1.2e15)}
+    samples = []
+    for sec in ("student", "teacher"):
+        for mbs in (4, 8):
+            for tok in (1024, 2048):
+                f, b = estimate_step_time(g.section(sec), SectionConfig(mbs=mbs), true[sec], tok)
+                samples.append(StageSample(sec, "fwd", mbs, tok, f))
+                if b:
+                    samples.append(StageSample(sec, "bwd", mbs, tok, b))
+    fit = fit_cost_params(samples, {s: true[s].flops_per_token_fwd for s in true})
+    assert abs(fit["student"].peak_flops_per_gpu / 9.1e14 - 1) < 1e-12
+    assert abs(fit["student"].bwd_fwd_ratio - 2.3) < 1e-12
+    assert abs(fit["student"].mbs_efficiency[4] - 0.8) < 1e-12
+    assert abs(fit["teacher"].peak_flops_per_gpu / 1.2e15 - 1) < 1e-12
+    for x in samples:
+        f, b = estimate_step_time(g.section(x.section), SectionConfig(mbs=x.mbs), fit[x.section], x.tokens)
+        assert abs((f if x.phase == "fwd" else b) / x.seconds - 1) < 1e-9
