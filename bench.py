@@ -442,7 +442,11 @@ def run_kd(args):
     torch.cuda.synchronize()
     w1 = time.perf_counter()
     barrier()
-    # ---- per-kernel timing: one extra step with the sections serialised on one stream (untimed)
+    # ---- per-kernel timing: one extra step with the sections serialised on one stream (untimed),
+    # after one serialised warm-up step (its different buffer lifetimes settle in the allocator)
+    with ex.serialized():
+        ex.step(ids_dev, want_loss=False)
+    torch.cuda.synchronize()
     instrument.start_timing()
     with ex.serialized():
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
