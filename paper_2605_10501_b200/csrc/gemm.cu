@@ -75,7 +75,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                  int N, int K, int ldc, int splits,
                  const int32_t* __restrict__ rope_pos, const float2* __restrict__ rope_cs, int rope_cols, int rope_hd,
                  __nv_bfloat16* __restrict__ swiglu_out, int ld_swiglu, const __nv_bfloat16* __restrict__ resid,
-                 int ldr) {
+                 int ldr, int l2hint) {
   using CF = Cfg2<BN2>;
   constexpr int STAGES = CF::STAGES, B_BYTES = CF::B_BYTES, STAGE_BYTES = CF::STAGE_BYTES, B_ROWS = CF::B_ROWS;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -129,6 +129,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
+      // l2hint: B (swept once per grouped-M band, re-read by every band) is kept in L2
+      const uint64_t pol_b = l2_policy_evict_last();
       for (int t = pair; t < num_units; t += npairs) {
         int mb_, nb_, kb0, kb1;
         unit(t, mb_, nb_, kb0, kb1);
@@ -147,7 +149,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             tma_load_2d_2sm(a + 8192, &map_a, fb, m0 + 64, k0);
           }
           if (!B_MN) {
-            tma_load_2d_2sm(b, &map_b, fb, k0, n0);
+            if (l2hint)
+              tma_load_2d_2sm_hint(b, &map_b, fb, k0, n0, pol_b);
+            else
+              tma_load_2d_2sm(b, &map_b, fb, k0, n0);
           } else {
 #pragma unroll
             for (int j = 0; j < B_ROWS / 64; ++j) tma_load_2d_2sm(b + 8192 * j, &map_b, fb, n0 + 64 * j, k0);
@@ -293,7 +298,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             }
             uint4* dst = reinterpret_cast<uint4*>(swiglu_out + (size_t)row * ld_swiglu + (n0 + c) / 2);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) dst[k] = make_uint4(sv[4 * k], sv[4 * k + 1], sv[4 * k + 2], sv[4 * k + 3]);
+            for (int k = 0; k < 4; ++k) {
+              const uint4 val = make_uint4(sv[4 * k], sv[4 * k + 1], sv[4 * k + 2], sv[4 * k + 3]);
+              if (l2hint)
+                __stcs(dst + k, val);  // streaming store: evict-first in L2
+              else
+                dst[k] = val;
+            }
           }
           if (C == nullptr) continue;  // SwiGLU-only output (forward-only sections): gu is not stored
           if (!use_r && chunk_ctr >= 2) {
@@ -313,7 +324,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           fence_proxy_async_smem();
           named_barrier_sync(1, 128);
           if (et == 0) {
-            if (n0 + c < N && row0 < M) tma_store_2d(&map_c, buf, n0 + c, row0);
+            if (n0 + c < N && row0 < M) {
+              if (l2hint)
+                tma_store_2d_hint(&map_c, buf, n0 + c, row0, l2_policy_evict_first());
+              else
+                tma_store_2d(&map_c, buf, n0 + c, row0);
+            }
             bulk_commit();  // one group per chunk, even when empty: the wait_read<1> above counts chunks
           }
         }
@@ -373,9 +389,14 @@ int launch2(const CUtensorMap& ma, const CUtensorMap& mbm, const CUtensorMap& mc
   if (ensure_smem<gemm2_kernel<BN2, A_MN, B_MN, EPI>>(SMEM)) return launch_status();
   const int units = ((M + 255) / 256) * ((N + BN2 - 1) / BN2) * splits;
   const int pairs = units < num_sms() / 2 ? units : num_sms() / 2;
+  // L2 hints (weights evict-last, outputs evict-first); MAESTRO_GEMM_L2HINT=0 disables
+  static const int l2hint = [] {
+    const char* e = getenv("MAESTRO_GEMM_L2HINT");
+    return e ? atoi(e) : 1;
+  }();
   gemm2_kernel<BN2, A_MN, B_MN, EPI><<<2 * pairs, THREADS, SMEM, st>>>(ma, mbm, mc, mr, C, M, N, K, ldc, splits,
                                                                         rope_pos, rope_cs, rope_cols, rope_hd, swiglu_out,
-                                                                        ld_swiglu, resid, ldr);
+                                                                        ld_swiglu, resid, ldr, l2hint);
   return launch_status();
 }
 
