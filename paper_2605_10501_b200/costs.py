@@ -248,3 +248,41 @@ def derive_batch(graph: SectionGraph, configs: Mapping[str, SectionConfig],
         out.append(SampleTiming(sample_id=i, t_f_bc=up_f, t_f_c=fwd_c, t_f_ac=down_f, t_b_bc=down_b, t_b_c=bwd_c,
                                 t_b_ac=up_b, activated_sections=frozenset(act)))
     return out
+
+
+# --- shipped presets (costs.py:300-373) --------------------------------------------------------
+# The reference's calibrations of its documented workload archetypes, used by `maestro-spec v1`
+# files (`cost: {preset: ...}`).  They assume 3e14 FLOP/s per GPU; planner.fit_cost_params
+# replaces that with B200-measured rates.
+
+
+def _eff(*rows):
+    return {tuple(r[:3]): r[3] for r in rows}
+
+
+PRESETS: dict[str, CostParams] = {
+    "vit-encoder": CostParams(
+        flops_per_token_fwd=2.4e9, peak_flops_per_gpu=3.0e14, bwd_fwd_ratio=2.0,
+        parallel_efficiency=_eff((1, 1, 2, 0.97), (1, 1, 4, 0.93), (1, 1, 8, 0.88), (1, 1, 16, 0.80),
+                                 (2, 1, 1, 0.95), (2, 1, 2, 0.92), (2, 1, 4, 0.88), (4, 1, 1, 0.90)),
+        bytes_per_param_weights=2.0, bytes_per_param_optimizer=12.0, activation_bytes_per_token=4096.0),
+    "moe-backbone": CostParams(
+        flops_per_token_fwd=3.4e10, peak_flops_per_gpu=3.0e14, bwd_fwd_ratio=2.0,
+        parallel_efficiency=_eff((2, 1, 1, 0.96), (4, 1, 1, 0.92), (8, 1, 1, 0.85), (2, 2, 1, 0.93),
+                                 (4, 2, 1, 0.89), (4, 4, 1, 0.84), (8, 2, 1, 0.82), (8, 4, 1, 0.78),
+                                 (2, 1, 2, 0.92), (4, 1, 2, 0.88), (2, 2, 2, 0.89)),
+        bytes_per_param_weights=2.0, bytes_per_param_optimizer=12.0, activation_bytes_per_token=24576.0),
+    "frozen-teacher": CostParams(
+        flops_per_token_fwd=5.6e10, peak_flops_per_gpu=3.0e14, bwd_fwd_ratio=2.0,
+        parallel_efficiency=_eff((2, 1, 1, 0.96), (4, 1, 1, 0.92), (8, 1, 1, 0.86), (2, 2, 1, 0.93),
+                                 (4, 2, 1, 0.88), (1, 1, 2, 0.93), (1, 1, 4, 0.88), (2, 1, 2, 0.90)),
+        mbs_efficiency={1: 0.35, 2: 0.62, 3: 0.80, 4: 0.91, 8: 1.0},
+        bytes_per_param_weights=2.0, bytes_per_param_optimizer=0.0, activation_bytes_per_token=1024.0),
+}
+
+
+def preset(name: str) -> CostParams:
+    """A shipped preset by name; unknown names raise InvalidDims listing the known ones."""
+    if name not in PRESETS:
+        raise InvalidDims(f"unknown cost preset '{name}' (known: {', '.join(sorted(PRESETS))})", preset=name)
+    return PRESETS[name]

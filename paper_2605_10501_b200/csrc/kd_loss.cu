@@ -8,9 +8,11 @@
 // sum_v e^{t-m}(t - s); pass 2 re-reads the rows (L2-resident: a CTA's row is < 0.6 MB and
 // just touched) and writes ds.  HBM traffic ~ 2 x V x 2 B read + V x 2 B written per token.
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <stdlib.h>
 
 #include "common.cuh"
+#include "sm100.cuh"
 #include "tma_host.cuh"
 
 namespace mb {
@@ -189,6 +191,233 @@ __global__ void __launch_bounds__(THREADS, MIN_BLOCKS) kd_loss_kernel(const __nv
 }
 
 
+// ---------------------------------------------------------------------------------------------
+// Shared-memory-resident K9.  A token row is read from HBM exactly once: a cluster of C CTAs
+// (three per SM, so row slices in different phases overlap) holds the row, CTA c owning columns
+// [c*VC, c*VC + VC), VC <= 16384, as eight 2048-column chunks of (t, s) bf16 = 64 KB, filled by
+// 1-D TMA bulk copies from a producer warp.
+//   pass 1 (as chunks land): per thread one 8-column vector of t and s per chunk; online (max,
+//          sum-exp) of both plus sum e^t (t - s); the exponentials are written back IN PLACE as
+//          fp16 (relative to the thread's running max at that chunk, kept in registers), so
+//          pass 2 needs no exponentials: MUFU work is 2 per column instead of 4.
+//   stats: warp/CTA reduction, then each CTA pushes its partial into every cluster peer's
+//          shared memory (st.shared::cluster + remote mbarrier arrive); every CTA merges the C
+//          partials in rank order (identical bits everywhere).
+//   pass 2: ds = g (e_s 2^(m_s,k - M_s)/S_s - e_t 2^(m_t,k - M_t)/S_t), bf16 stores; each chunk is
+//          released to the producer as soon as it is consumed, so row r+1 streams in behind
+//          row r's pass 2.
+// HBM traffic is the algorithmic 2 x V x 2 B read + V x 2 B written per row.  fp16 storage of
+// the exponentials (all <= 1) adds a relative error <= 2^-12 per probability to ds (which is then
+// rounded to bf16, 2^-9); the loss uses the fp32 exponentials.
+constexpr int KDS_CONS = 256;              // consumer threads: one 8-column vector per chunk each
+constexpr int KDS_CH = 8 * KDS_CONS;       // columns per chunk
+constexpr int KDS_NCH = 8;                 // chunks per CTA slice
+constexpr int KDS_VC_MAX = KDS_CH * KDS_NCH;  // 16384 columns = 64 KB of (t, s) per CTA
+constexpr int KDS_THREADS = KDS_CONS + 32; // + producer warp
+constexpr int KDS_SMEM = KDS_NCH * KDS_CH * 4 + 1024;
+constexpr int KDS_CTAS_PER_SM = 3;         // three row slices in flight per SM (different phases)
+
+__device__ __forceinline__ bool mbar_try_wait_cluster(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, "
+      "0, p;\n}"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void st_cluster_f32(uint32_t addr, float v) {
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+
+template <int C>
+__global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(KDS_THREADS, KDS_CTAS_PER_SM)
+    kd_loss_smem_kernel(const __nv_bfloat16* __restrict__ tl, const __nv_bfloat16* sl, __nv_bfloat16* ds,
+                        float* __restrict__ loss, int T, int V, int VC, int ldt, int lds, int ldd, float scale2,
+                        float grad_scale, float inv_tau) {
+  using namespace sm100;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* sm = align_smem_1024(smem_raw);
+  // chunk k: t at sm + k * 16 KB, s at + 8 KB
+  __shared__ __align__(8) uint64_t full[KDS_NCH], empty[KDS_NCH], stats_bar[2];
+  __shared__ Stat red[KDS_CONS / 32];
+  __shared__ float slot[2][C][8];  // [row parity][source rank] partial stats
+  const int rank = C > 1 ? (int)cluster_ctarank() : 0;
+  const int n_clusters = gridDim.x / C, cid = blockIdx.x / C;
+  const int c0 = rank * VC;
+  const int cols = max(0, min(V - c0, VC));  // this CTA's slice width (multiple of 8)
+  const int nch = (cols + KDS_CH - 1) / KDS_CH;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < KDS_NCH; ++k) {
+      mbar_init(&full[k], 1);
+      mbar_init(&empty[k], KDS_CONS / 32);
+    }
+    mbar_init(&stats_bar[0], C);
+    mbar_init(&stats_bar[1], C);
+    fence_barrier_init();
+  }
+  if constexpr (C > 1) cluster_sync();  // peers' barriers initialised before any remote arrive
+  else __syncthreads();
+
+  if (warp == KDS_CONS / 32) {  // producer
+    if (lane == 0) {
+      int it = 0;
+      for (int row = cid; row < T; row += n_clusters, ++it) {
+        const __nv_bfloat16* tr = tl + (size_t)row * ldt + c0;
+        const __nv_bfloat16* sr = sl + (size_t)row * lds + c0;
+        for (int k = 0; k < nch; ++k) {
+          const int w = min(KDS_CH, cols - k * KDS_CH);
+          mbar_wait(&empty[k], (it & 1) ^ 1);
+          mbar_arrive_expect_tx(&full[k], 4u * (uint32_t)w);
+          bulk_load_1d(sm + k * (KDS_CH * 4), tr + k * KDS_CH, 2u * (uint32_t)w, &full[k]);
+          bulk_load_1d(sm + k * (KDS_CH * 4) + KDS_CH * 2, sr + k * KDS_CH, 2u * (uint32_t)w, &full[k]);
+        }
+      }
+    }
+  } else {
+    const int tid = threadIdx.x;
+    int it = 0;
+    for (int row = cid; row < T; row += n_clusters, ++it) {
+      const uint32_t ph = it & 1;
+      Stat a{-INFINITY, 0.f, 0.f, -INFINITY, 0.f};
+      float mh_t[KDS_NCH], mh_s[KDS_NCH];
+      // ---- pass 1
+#pragma unroll
+      for (int k = 0; k < KDS_NCH; ++k) {
+        mh_t[k] = mh_s[k] = 0.f;
+        if (k >= nch) break;
+        mbar_wait(&full[k], ph);
+        const bool mine = k * KDS_CH + 8 * tid < cols;
+        uint4* pt = reinterpret_cast<uint4*>(sm + k * (KDS_CH * 4)) + tid;
+        uint4* ps = reinterpret_cast<uint4*>(sm + k * (KDS_CH * 4) + KDS_CH * 2) + tid;
+        if (mine) {
+          float ft[8], fs[8];
+          unpack8(*pt, ft);
+          unpack8(*ps, fs);
+          float mt = a.mt, ms = a.ms;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            mt = fmaxf(mt, ft[j] * scale2);
+            ms = fmaxf(ms, fs[j] * scale2);
+          }
+          if (mt > a.mt) {
+            const float ct = a.mt == -INFINITY ? 0.f : ex2a(a.mt - mt);
+            a.st *= ct;
+            a.at *= ct;
+            a.mt = mt;
+          }
+          if (ms > a.ms) {
+            a.ss *= a.ms == -INFINITY ? 0.f : ex2a(a.ms - ms);
+            a.ms = ms;
+          }
+          mh_t[k] = mt;
+          mh_s[k] = ms;
+          float2 sts = make_float2(a.st, a.ss);
+          uint32_t et[4], es[4];
+#pragma unroll
+          for (int j = 0; j < 8; j += 2) {
+            const float2 x0 = __ffma2_rn(make_float2(ft[j], fs[j]), make_float2(scale2, scale2), make_float2(-mt, -ms));
+            const float2 x1 =
+                __ffma2_rn(make_float2(ft[j + 1], fs[j + 1]), make_float2(scale2, scale2), make_float2(-mt, -ms));
+            const float2 e0 = make_float2(ex2a(x0.x), ex2a(x0.y));
+            const float2 e1 = make_float2(ex2a(x1.x), ex2a(x1.y));
+            sts = __fadd2_rn(__fadd2_rn(sts, e0), e1);
+            a.at = fmaf(e0.x, ft[j] - fs[j], a.at);
+            a.at = fmaf(e1.x, ft[j + 1] - fs[j + 1], a.at);
+            if (ds != nullptr) {
+              const __half2 ht = __floats2half2_rn(e0.x, e1.x), hs = __floats2half2_rn(e0.y, e1.y);
+              et[j >> 1] = *reinterpret_cast<const uint32_t*>(&ht);
+              es[j >> 1] = *reinterpret_cast<const uint32_t*>(&hs);
+            }
+          }
+          a.st = sts.x;
+          a.ss = sts.y;
+          if (ds != nullptr) {
+            *pt = make_uint4(et[0], et[1], et[2], et[3]);
+            *ps = make_uint4(es[0], es[1], es[2], es[3]);
+          }
+        }
+        if (ds == nullptr) {  // loss only: the chunk is free once read
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[k]);
+        }
+      }
+      // ---- row statistics: warp -> CTA -> cluster (every CTA merges the C partials in rank order)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        Stat b{__shfl_xor_sync(kFull, a.mt, o), __shfl_xor_sync(kFull, a.st, o), __shfl_xor_sync(kFull, a.at, o),
+               __shfl_xor_sync(kFull, a.ms, o), __shfl_xor_sync(kFull, a.ss, o)};
+        merge(a, b);
+      }
+      if (lane == 0) red[warp] = a;
+      named_barrier_sync(1, KDS_CONS);
+      if (tid == 0) {
+        Stat b = red[0];
+        for (int w = 1; w < KDS_CONS / 32; ++w) merge(b, red[w]);
+        const float v[5] = {b.mt, b.st, b.at, b.ms, b.ss};
+        for (int q = 0; q < C; ++q) {
+          const uint32_t dst = smem_u32(&slot[ph][rank][0]);
+          const uint32_t bar = smem_u32(&stats_bar[ph]);
+          if constexpr (C > 1) {
+            for (int e = 0; e < 5; ++e) st_cluster_f32(mapa_shared(dst + 4 * e, q), v[e]);
+            mbar_arrive_cluster(mapa_shared(bar, q));
+          } else {
+            for (int e = 0; e < 5; ++e) slot[ph][0][e] = v[e];
+            mbar_arrive(&stats_bar[ph]);
+          }
+        }
+      }
+      {
+        const uint32_t a_bar = smem_u32(&stats_bar[ph]);
+        while (!mbar_try_wait_cluster(a_bar, (it >> 1) & 1)) {
+        }
+      }
+      Stat f{slot[ph][0][0], slot[ph][0][1], slot[ph][0][2], slot[ph][0][3], slot[ph][0][4]};
+#pragma unroll
+      for (int q = 1; q < C; ++q) merge(f, Stat{slot[ph][q][0], slot[ph][q][1], slot[ph][q][2], slot[ph][q][3], slot[ph][q][4]});
+      if (rank == 0 && tid == 0) {
+        const float lse_t = (f.mt + log2f(f.st)) * LN2;
+        const float lse_s = (f.ms + log2f(f.ss)) * LN2;
+        loss[row] = f.at / f.st * inv_tau - lse_t + lse_s;
+      }
+      if (ds == nullptr) continue;
+      // ---- pass 2: ds from the stored exponentials, chunk by chunk (each released when done)
+      const float g = grad_scale * inv_tau;
+      const float gt = g / f.st, gs = g / f.ss;
+      __nv_bfloat16* drow = ds + (size_t)row * ldd + c0;
+#pragma unroll
+      for (int k = 0; k < KDS_NCH; ++k) {
+        if (k >= nch) break;
+        const int col = k * KDS_CH + 8 * tid;
+        if (col < cols) {
+          const uint4 ut = reinterpret_cast<const uint4*>(sm + k * (KDS_CH * 4))[tid];
+          const uint4 us = reinterpret_cast<const uint4*>(sm + k * (KDS_CH * 4) + KDS_CH * 2)[tid];
+          const float fct = gt * ex2a(mh_t[k] - f.mt), fcs = gs * ex2a(mh_s[k] - f.ms);
+          const uint32_t* ht = reinterpret_cast<const uint32_t*>(&ut);
+          const uint32_t* hs = reinterpret_cast<const uint32_t*>(&us);
+          uint32_t o[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float2 et = __half22float2(*reinterpret_cast<const __half2*>(&ht[j]));
+            const float2 es = __half22float2(*reinterpret_cast<const __half2*>(&hs[j]));
+            const float2 d = __ffma2_rn(es, make_float2(fcs, fcs), __fmul2_rn(et, make_float2(-fct, -fct)));
+            o[j] = pack_bf16(d.x, d.y);
+          }
+          *reinterpret_cast<uint4*>(drow + col) = make_uint4(o[0], o[1], o[2], o[3]);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[k]);
+      }
+    }
+  }
+  __syncwarp();
+  if constexpr (C > 1) cluster_sync();  // no CTA exits while peers may still write its slots
+}
+
 // Next-token cross entropy over the full vocabulary with ignore index (label < 0):
 // loss[row] = lse(s) - s[label];  ds = grad_scale * (softmax(s) - onehot(label)).  Same
 // single-pass online max/sum-exp + L2-resident second pass as the KL kernel.
@@ -273,6 +502,29 @@ __global__ void __launch_bounds__(KD_THREADS) ce_loss_kernel(const __nv_bfloat16
 
 using namespace mb;
 
+// Clusters of `cs` CTAs that can be resident at once (a grid larger than this runs a second wave
+// of whole clusters: GPCs do not all hold a multiple of the cluster size).
+template <class K>
+static int max_clusters(K kernel, int cs, int threads, int smem) {
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = cs;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.gridDim = dim3(cs * 64, 1, 1);
+  cfg.blockDim = dim3(threads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, (void*)kernel, &cfg) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    n = num_sms() * KDS_CTAS_PER_SM / cs;
+  }
+  return n;
+}
+
 // loss[T] (fp32, per token) and, if d_ds != null, ds = grad_scale * d loss / d s (bf16).
 // ds may alias the student logits (in-place): every element is read before it is written
 // by the same thread.
@@ -296,6 +548,42 @@ MAESTRO_API int maestro_kd_loss_fwd_bwd(const void* d_t, const void* d_s, void* 
   // V = 128256.  Measured slower (2840 vs 3612 GB/s at 8192 x 128256, 2936 vs 3870 at
   // 16384 x 32000): the kernel is bound by its exponentials (2 per element per pass) as much as
   // by HBM, and 4 rows per SM overlap them better.  Default: 4 rows per SM.
+  // default: the shared-memory-resident kernel (one HBM read per row, 2 exponentials per column)
+  static const int impl_env = [] {
+    const char* e = getenv("MAESTRO_KD_IMPL");  // "stream": the L2 re-read kernel below; "smem": any C <= 8
+    if (!e) return 0;
+    return e[0] == 's' && e[1] == 't' ? 1 : (e[0] == 's' && e[1] == 'm' ? 2 : 0);
+  }();
+  const int C = (V + KDS_VC_MAX - 1) / KDS_VC_MAX;
+  const bool aligned = (((uintptr_t)d_t | (uintptr_t)d_s | (uintptr_t)d_ds) & 15) == 0;
+  // Cluster row slices pay a per-row stats exchange and cluster co-scheduling: measured (16384 x
+  // 32000, C = 2) 3914 GB/s vs 3860 for the streaming kernel, but (8192 x 128256, C = 8) 2766 vs
+  // 3609 -- so rows wider than two slices stay on the streaming kernel (MAESTRO_KD_IMPL=smem forces).
+  const int c_max = (impl_env == 0) ? 2 : (impl_env == 2 ? 8 : 0);
+  if (C <= c_max && aligned) {
+    const int VC = ((V + C - 1) / C + 7) / 8 * 8;
+    switch (C) {
+#define KDS_LAUNCH(CC)                                                                                          \
+  case CC: {                                                                                                    \
+    if (ensure_smem<kd_loss_smem_kernel<CC>>(KDS_SMEM)) return launch_status();                                \
+    static const int max_cl = max_clusters(kd_loss_smem_kernel<CC>, CC, KDS_THREADS, KDS_SMEM);                \
+    const int n_cl = T < max_cl ? T : max_cl;                                                                   \
+    kd_loss_smem_kernel<CC><<<n_cl * CC, KDS_THREADS, KDS_SMEM, (cudaStream_t)stream>>>(                        \
+        (const __nv_bfloat16*)d_t, (const __nv_bfloat16*)d_s, (__nv_bfloat16*)d_ds, d_loss, T, V, VC, ldt, lds, \
+        ldd, inv_tau * LOG2E, grad_scale, inv_tau);                                                             \
+    return launch_status();                                                                                     \
+  }
+      KDS_LAUNCH(1)
+      KDS_LAUNCH(2)
+      KDS_LAUNCH(3)
+      KDS_LAUNCH(4)
+      KDS_LAUNCH(5)
+      KDS_LAUNCH(6)
+      KDS_LAUNCH(7)
+      KDS_LAUNCH(8)
+#undef KDS_LAUNCH
+    }
+  }
   static const int rows_env = [] {
     const char* e = getenv("MAESTRO_KD_ROWS_PER_SM");
     return e ? atoi(e) : 0;

@@ -402,6 +402,34 @@ __device__ Metrics eval_order(Seq&& seq, bool need_ub = true) {
   return m;
 }
 
+// Interleaved policy, no downstream stage in the rank (no sample has t_f_ac or t_b_bc): the
+// recurrence without branches.  Bit-exact with eval_order because, for these samples,
+//  * u + 0.0 == u (so u is advanced unconditionally; ready = t_f_bc > 0 ? u : 0),
+//  * the critical backward starts at pmax(c, ch) with ch == c, i.e. at c, and c + 0.0 == c,
+//  * without a b_ac stage mk = pmax over a non-decreasing sequence of c = its last value.
+// Candidate elements are {t_f_bc, t_f_c, t_b_c, t_b_ac} (AoS, two 16-byte loads per element).
+template <bool UB>
+__device__ __forceinline__ double eval_nodown(const double4* __restrict__ cur, int len, int p, const double4& x,
+                                              double u_total) {
+  double u = 0.0, c = 0.0, ub = u_total, mk = 0.0;
+#pragma unroll 8
+  for (int j = 0; j <= len; ++j) {
+    double4 s = cur[j - (j > p ? 1 : 0)];
+    if (j == p) s = x;
+    u = u + s.x;
+    const double ready = s.x > 0 ? u : 0.0;
+    c = pmax(c, ready) + s.y;
+    c = c + s.z;
+    if (UB) {
+      const double t = pmax(ub, c) + s.w;
+      const bool has = s.w > 0;
+      ub = has ? t : ub;
+      mk = pmax(mk, has ? t : c);
+    }
+  }
+  return UB ? mk : c;
+}
+
 __device__ __forceinline__ void argmin_combine(double& v, int& p, double ov, int op) {
   if (ov < v || (ov == v && op < p)) {
     v = ov;
@@ -409,8 +437,9 @@ __device__ __forceinline__ void argmin_combine(double& v, int& p, double ov, int
   }
 }
 
-template <int POLICY>
-__global__ void __launch_bounds__(1024) wavefront_kernel(const double* __restrict__ times, int B,
+// MAXT: launch bound (256 for ranks of <= 255 samples: registers for the unrolled recurrence)
+template <int POLICY, int MAXT>
+__global__ void __launch_bounds__(MAXT) wavefront_kernel(const double* __restrict__ times, int B,
                                                          const int32_t* __restrict__ part,
                                                          const int32_t* __restrict__ part_off,
                                                          int32_t* __restrict__ orders, double* __restrict__ metrics,
@@ -423,7 +452,8 @@ __global__ void __launch_bounds__(1024) wavefront_kernel(const double* __restric
   const int cap = (int)blockDim.x;  // >= n + 1
   double* cur = reinterpret_cast<double*>(smem_raw);  // [6][cap]  current partial order
   double* stg = cur + 6 * cap;                        // [6][cap]  staged samples (init order)
-  int* ord = reinterpret_cast<int*>(stg + 6 * cap);   // [cap]     batch index per position
+  double4* cur4 = reinterpret_cast<double4*>(stg + 6 * cap);  // [cap] {fbc, fc, bc, bac} (fast path)
+  int* ord = reinterpret_cast<int*>(cur4 + cap);      // [cap]     batch index per position
   int* init = ord + cap;                              // [cap]
   __shared__ double red_v[32];
   __shared__ int red_p[32];
@@ -480,9 +510,13 @@ __global__ void __launch_bounds__(1024) wavefront_kernel(const double* __restric
   View sv{{stg, stg + cap, stg + 2 * cap, stg + 3 * cap, stg + 4 * cap, stg + 5 * cap}};
   // does any sample of this rank have a b_ac stage (the ub chain)?
   const bool need_ub = __syncthreads_or(tid < n && stg[5 * cap + tid] > 0.0) != 0;
+  // no downstream stage anywhere in the rank: the branch-free interleaved recurrence (eval_nodown)
+  const bool fast = POLICY == MAESTRO_POLICY_INTERLEAVED &&
+                    __syncthreads_or(tid < n && (stg[2 * cap + tid] > 0.0 || stg[3 * cap + tid] > 0.0)) == 0;
   if (tid == 0) {
     ord[0] = init[0];
     for (int p = 0; p < 6; ++p) cur[p * cap] = stg[p * cap];
+    cur4[0] = make_double4(stg[0], stg[cap], stg[4 * cap], stg[5 * cap]);
   }
   __syncthreads();
   double best_mk = 0.0;
@@ -491,8 +525,19 @@ __global__ void __launch_bounds__(1024) wavefront_kernel(const double* __restric
     double v = __longlong_as_double(0x7ff0000000000000ll);  // +inf
     int pos = 0x7fffffff;
     if (tid <= len) {
-      Metrics m = eval_order<POLICY, false>([&](auto&& f) { for_candidate(cv, len, tid, x, f); }, need_ub);
-      v = m.mk;
+      if (fast) {
+        const double4 x4 = make_double4(x.fbc, x.fc, x.bc, x.bac);
+        if (need_ub) {
+          double u_total = 0.0;  // sum of t_f_bc in candidate order (ub starts there)
+          for (int j = 0; j <= len; ++j) u_total = u_total + (j == tid ? x.fbc : cur4[j - (j > tid ? 1 : 0)].x);
+          v = eval_nodown<true>(cur4, len, tid, x4, u_total);
+        } else {
+          v = eval_nodown<false>(cur4, len, tid, x4, 0.0);
+        }
+      } else {
+        Metrics m = eval_order<POLICY, false>([&](auto&& f) { for_candidate(cv, len, tid, x, f); }, need_ub);
+        v = m.mk;
+      }
       pos = tid;
     }
     for (int o = 16; o > 0; o >>= 1) {
@@ -524,18 +569,22 @@ __global__ void __launch_bounds__(1024) wavefront_kernel(const double* __restric
     best_mk = red_v[0];
     // res.insert(bp, x): shift [bp, len) right by one
     double keep[6];
+    double4 keep4;
     int keep_idx = 0;
     const bool mover = tid >= bp && tid < len;
     if (mover) {
       for (int p = 0; p < 6; ++p) keep[p] = cur[p * cap + tid];
+      keep4 = cur4[tid];
       keep_idx = ord[tid];
     }
     __syncthreads();
     if (mover) {
       for (int p = 0; p < 6; ++p) cur[p * cap + tid + 1] = keep[p];
+      cur4[tid + 1] = keep4;
       ord[tid + 1] = keep_idx;
     }
     if (tid == 0) {
+      cur4[bp] = make_double4(x.fbc, x.fc, x.bc, x.bac);
       cur[0 * cap + bp] = x.fbc;
       cur[1 * cap + bp] = x.fc;
       cur[2 * cap + bp] = x.fac;
@@ -796,7 +845,7 @@ size_t partition_smem(int B) {
 
 int wavefront_threads(int max_n) { return ((max_n + 1 + 31) / 32) * 32; }
 
-size_t wavefront_smem(int threads) { return (size_t)threads * (12 * sizeof(double) + 2 * sizeof(int)); }
+size_t wavefront_smem(int threads) { return (size_t)threads * (16 * sizeof(double) + 2 * sizeof(int)); }
 
 }  // namespace
 }  // namespace mb
@@ -847,13 +896,21 @@ MAESTRO_API int maestro_wavefront(const double* d_times, int32_t B, const int32_
   if (max_n > MAESTRO_MAX_RANK_SAMPLES) return (int)cudaErrorInvalidValue;
   const int threads = wavefront_threads(max_n);
   const size_t smem = wavefront_smem(threads);
-  if (ensure_smem<wavefront_kernel<0>>(smem) || ensure_smem<wavefront_kernel<1>>(smem)) return launch_status();
-  if (policy == MAESTRO_POLICY_INTERLEAVED)
-    wavefront_kernel<0><<<dp, threads, smem, (cudaStream_t)stream>>>(d_times, B, d_part, d_part_off, d_orders,
-                                                                      d_metrics, d_evals);
-  else
-    wavefront_kernel<1><<<dp, threads, smem, (cudaStream_t)stream>>>(d_times, B, d_part, d_part_off, d_orders,
-                                                                      d_metrics, d_evals);
+#define WF_LAUNCH(P, T)                                                                                  \
+  do {                                                                                                   \
+    if (ensure_smem<wavefront_kernel<P, T>>(smem)) return launch_status();                               \
+    wavefront_kernel<P, T><<<dp, threads, smem, (cudaStream_t)stream>>>(d_times, B, d_part, d_part_off, \
+                                                                       d_orders, d_metrics, d_evals);    \
+  } while (0)
+  const bool small = threads <= 256;
+  if (policy == MAESTRO_POLICY_INTERLEAVED) {
+    if (small) WF_LAUNCH(0, 256);
+    else WF_LAUNCH(0, 1024);
+  } else {
+    if (small) WF_LAUNCH(1, 256);
+    else WF_LAUNCH(1, 1024);
+  }
+#undef WF_LAUNCH
   return launch_status();
 }
 

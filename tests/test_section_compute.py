@@ -112,7 +112,7 @@ def test_adamw_matches_reference():
     assert rel(p, pr) < 1e-6 and torch.equal(pb, p.bfloat16())
 
 
-@pytest.mark.parametrize("T,V", [(64, 32000), (33, 128256 // 8 * 8), (8, 64)])
+@pytest.mark.parametrize("T,V", [(64, 32000), (33, 128256 // 8 * 8), (8, 64), (300, 40000), (5, 150000), (3, 4104)])
 def test_kd_loss_fused(T, V):
     from paper_2605_10501_b200 import kernels as K
 
@@ -131,6 +131,10 @@ def test_kd_loss_fused(T, V):
     s2 = s.clone()
     K.kd_loss(t, s2, s2, loss, grad_scale=0.5)
     assert torch.equal(s2, ds)
+    # loss only (no gradient)
+    loss2 = torch.empty(T, device="cuda")
+    K.kd_loss(t, s, None, loss2, grad_scale=0.5)
+    assert torch.equal(loss2, loss)
 
 
 def _tiny_model(seed=0, shape_name="test_tiny"):
