@@ -15,7 +15,11 @@ from . import errors as E
 from . import instrument as _instrument
 from .workload import MAX_SECTIONS, SectionConfig, SectionGraph
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libmaestro_b200.so"
+import os as _os
+
+# MAESTRO_LIB_PATH: an alternative build of the same library (scripts/build_variant.py, kernel A/B
+# experiments); the default is the in-tree build
+LIB_PATH = Path(_os.environ.get("MAESTRO_LIB_PATH") or Path(__file__).resolve().parent / "_lib" / "libmaestro_b200.so")
 MAX_DP = 64
 MAX_BATCH = 4096
 MAX_RANK_SAMPLES = 1023

@@ -67,6 +67,22 @@ __global__ void attn_tiles_kernel(const int32_t* __restrict__ cu, int nseq, int2
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
 
+// One arrive per warp (barrier count = warps) instead of one per thread: each lane's tcgen05
+// ld/st wait + fence::before_thread_sync precede the __syncwarp, so lane 0's release covers the
+// whole warp -- 8 shared-memory arrives per tile-barrier instead of 256.
+#ifndef ATTN_WARP_ARRIVE
+#define ATTN_WARP_ARRIVE 1  // 0: every thread arrives (barrier counts in threads)
+#endif
+constexpr int ARRIVE_UNIT = ATTN_WARP_ARRIVE ? 32 : 1;  // threads per arrive
+__device__ __forceinline__ void warp_arrive(uint64_t* bar) {
+  if (ATTN_WARP_ARRIVE) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
+  } else {
+    mbar_arrive(bar);
+  }
+}
+
 #ifndef BWD_EMU_BITS
 #define BWD_EMU_BITS 0x00  // backward P^T = exp2(S^T scale2 - lse2): not MUFU-bound, all on MUFU
 #endif
@@ -194,7 +210,7 @@ __global__ void __launch_bounds__(FwdCfg<DH, CG>::THREADS, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                     const __grid_constant__ CUtensorMap map_v, const int32_t* __restrict__ cu,
                     const int2* __restrict__ tiles, const int* __restrict__ n_tiles, __nv_bfloat16* __restrict__ out,
-                    int ldo, float* __restrict__ lse, int T, int H, int Hk, float scale2) {
+                    int ldo, float* __restrict__ lse, int T, int H, int Hk, float scale2, int stagger_ns) {
   using C = FwdCfg<DH, CG>;
   constexpr int KVS = C::KVS, NOB = C::NOB, TB = C::TILE, CW = C::CW, SMX = C::SMX;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -224,11 +240,11 @@ __global__ void __launch_bounds__(FwdCfg<DH, CG>::THREADS, 1)
       mbar_init(&q_full[b], 1);
       mbar_init(&q_empty[b], 1);
       mbar_init(&s_full[b], 1);
-      mbar_init(&s_empty[b], SMX);
-      mbar_init(&p_full[b], SMX);
+      mbar_init(&s_empty[b], SMX / ARRIVE_UNIT);
+      mbar_init(&p_full[b], SMX / ARRIVE_UNIT);
       mbar_init(&p_empty[b], 1);
       mbar_init(&o_full[b], 1);
-      mbar_init(&o_empty[b], SMX);
+      mbar_init(&o_empty[b], SMX / ARRIVE_UNIT);
     }
     for (int s = 0; s < KVS; ++s) {
       mbar_init(&k_full[s], 1);
@@ -412,7 +428,7 @@ __global__ void __launch_bounds__(FwdCfg<DH, CG>::THREADS, 1)
         }
         if (sub == OC / CH - 1) {
           tc_fence_before();
-          mbar_arrive(&o_empty[ob]);
+          warp_arrive(&o_empty[ob]);
         }
         if (qpos < it.L) {
           uint32_t o[CH / 2];
@@ -425,6 +441,9 @@ __global__ void __launch_bounds__(FwdCfg<DH, CG>::THREADS, 1)
       }
       if (grp == 0 && qpos < it.L) lse[(size_t)it.h * T + it.s0 + qpos] = (M + log2f(l_all)) * LN2_F;
     };
+    // experiment knob (MAESTRO_ATTN_STAGGER_NS): start the second column group late so the two
+    // softmax warps of an SM sub-partition run their phases (max / exp / pack) out of step
+    if (grp == 1 && stagger_ns > 0) __nanosleep(stagger_ns);
     int g = 0, j = 0;
     bool pend = false;
     FwdItem pit{};
@@ -456,7 +475,7 @@ __global__ void __launch_bounds__(FwdCfg<DH, CG>::THREADS, 1)
             for (int jj = 0; jj < 32; ++jj) s[c * 32 + jj] = __uint_as_float(raw[c][jj]);
         }
         tc_fence_before();
-        mbar_arrive(&s_empty[b]);
+        warp_arrive(&s_empty[b]);
         const int kv0 = i * BKV + grp * CW;
         const bool need_mask = (CAUSAL && kv0 + CW - 1 > it.q0) || (kv0 + CW > it.L);
         // valid key columns of this row: c < lim (causal: key <= query; key inside the sequence)
@@ -470,7 +489,7 @@ __global__ void __launch_bounds__(FwdCfg<DH, CG>::THREADS, 1)
           tmem_st_cols<CW / 2>(tmem + lane_base + b * BKV + grp * CW, zero);
           tmem_st_wait();
           tc_fence_before();
-          mbar_arrive(&p_full[b]);
+          warp_arrive(&p_full[b]);
           if (i == 0 && pend) {
             epilogue(pit, pj, pm, pl);
             pend = false;
@@ -543,7 +562,7 @@ __global__ void __launch_bounds__(FwdCfg<DH, CG>::THREADS, 1)
         }
         tmem_st_wait();
         tc_fence_before();
-        mbar_arrive(&p_full[b]);
+        warp_arrive(&p_full[b]);
         if (i == 0 && pend) {
           epilogue(pit, pj, pm, pl);
           pend = false;
@@ -711,15 +730,15 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     }
     mbar_init(s_full, 1);
     mbar_init(dp_full, 1);
-    mbar_init(p_ready, 256);
+    mbar_init(p_ready, 256 / ARRIVE_UNIT);
     mbar_init(p_free, 1);
-    mbar_init(ds_ready, 256);
+    mbar_init(ds_ready, 256 / ARRIVE_UNIT);
     mbar_init(ds_free, 1);
     mbar_init(dq_full, 1);
-    mbar_init(dq_empty, 128);
+    mbar_init(dq_empty, 128 / ARRIVE_UNIT);
     mbar_init(dkv_full, 1);
-    mbar_init(dkv_empty, 256);
-    mbar_init(s_empty, 256);
+    mbar_init(dkv_empty, 256 / ARRIVE_UNIT);
+    mbar_init(s_empty, 256 / ARRIVE_UNIT);  // arrive counts: see warp_arrive
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -886,7 +905,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         tmem_ld_32x32b_x32(tmem + lane_base + T_DQ + 32, qb);
         tmem_ld_wait();
         tc_fence_before();
-        mbar_arrive(dq_empty);  // TMEM free as soon as it is in registers
+        warp_arrive(dq_empty);  // TMEM free as soon as it is in registers
         if constexpr (DH == 64) {
           // lane = query row q4*32 + lane, registers = dh columns [0,32) and [32,64)
 #pragma unroll
@@ -978,7 +997,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         for (int c = 0; c < QH / 32; ++c) tmem_ld_32x32b_x32(tmem + lane_base + T_ST + half * QH + 32 * c, sr2[c]);
         tmem_ld_wait();
         tc_fence_before();
-        mbar_arrive(s_empty);
+        warp_arrive(s_empty);
         if (gi >= 1) mbar_wait(p_free, (gi - 1) & 1);  // dV(gi-1) has read P^T
         uint32_t pk[QH / 2];  // this row's P^T as bf16 pairs: the dV operand, and P for phase 2
         // Two instantiations so that interior tiles carry no per-element mask code (if-converted
@@ -1032,7 +1051,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
           tmem_st_32x32b_x16(tmem + lane_base + T_PT + half * 16, pk);
         tmem_st_wait();
         tc_fence_before();
-        mbar_arrive(p_ready);
+        warp_arrive(p_ready);
         // ---- P2: dP^T -> dS^T
         mbar_wait(dp_full, gi & 1);
         tc_fence_after();
@@ -1069,7 +1088,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         tmem_st_wait();
         fence_proxy_async_smem();
         tc_fence_before();
-        mbar_arrive(ds_ready);
+        warp_arrive(ds_ready);
       }
       // ---- item epilogue: dK (scaled, inverse RoPE), then dV -> bf16; TMEM is released after
       // the loads so the next item's first dV MMA can start while the stores drain
@@ -1091,7 +1110,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
           tmem_ld_wait();
           if (cp == DH / 64 - 1) {
             tc_fence_before();
-            mbar_arrive(dkv_empty);
+            warp_arrive(dkv_empty);
           }
           if (kvpos < itm.L) {
             if (which == 0 && rope_cs != nullptr) {
@@ -1274,8 +1293,13 @@ MAESTRO_API int maestro_attn_fwd(const void* q, const void* k, const void* v, co
     const int smem = CF::TOTAL + 1024;                                                                    \
     if (ensure_smem<attn_fwd_kernel<D, G, CZ>>(smem)) return launch_status();                             \
     attn_fwd_kernel<D, G, CZ><<<grid, CF::THREADS, smem, st>>>(mq, mk, mv, cu, tiles, count,               \
-                                                              (__nv_bfloat16*)out, ldo, lse, T, H, Hk, scale2); \
+                                                              (__nv_bfloat16*)out, ldo, lse, T, H, Hk, scale2,   \
+                                                              stagger);                                         \
   }
+  static const int stagger = [] {
+    const char* e = getenv("MAESTRO_ATTN_STAGGER_NS");
+    return e ? atoi(e) : 0;
+  }();
   // column groups per tile (head_dim 64): 4 (16 softmax warps) or 2 (8); MAESTRO_ATTN_CG overrides
   static const int cg_env = [] {
     const char* e = getenv("MAESTRO_ATTN_CG");

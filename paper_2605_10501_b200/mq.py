@@ -455,13 +455,17 @@ class PeerTransport(Transport):
             return
         import torch.distributed as dist
 
+        # the 64-byte IPC handles travel over the pair's process group (host tensors under gloo,
+        # e.g. two processes sharing one GPU; device tensors under NCCL)
+        hdev = torch.device("cpu") if dist.get_backend(group) == "gloo" else dev
+
         def send_handle(ptr):
             h = (ctypes.c_ubyte * 64)()
             N.check(L.maestro_ipc_get_handle(ptr, h), "ipc_get_handle")
-            dist.send(torch.tensor(list(h), dtype=torch.uint8, device=dev), peer, group=group)
+            dist.send(torch.tensor(list(h), dtype=torch.uint8, device=hdev), peer, group=group)
 
         def recv_handle():
-            t = torch.empty(64, dtype=torch.uint8, device=dev)
+            t = torch.empty(64, dtype=torch.uint8, device=hdev)
             dist.recv(t, peer, group=group)
             h = (ctypes.c_ubyte * 64)(*t.cpu().tolist())
             ptr = ctypes.c_void_p()

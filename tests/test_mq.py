@@ -307,3 +307,69 @@ def test_peer_transport_ring_protocol_on_one_gpu():
     with pytest.raises(E.SlotExhausted):
         ch_tx.push(torch.zeros(65, 256, device="cuda").bfloat16(), mq.MessageMeta((65, 256), 2, "t", (0, 0), 0))
     rx.close()
+
+
+def _peer_worker(rank, port, q):
+    """Two processes on cuda:0: rank 0 pushes six messages through a two-slot PeerTransport ring
+    (IPC-mapped slots, cross-process credits), rank 1 pulls them on its own stream."""
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    try:
+        torch.cuda.set_device(0)
+        layout = mq.ShardLayout((64, 256))
+        plan = mq.plan_reshard(layout, layout)
+        g = torch.Generator().manual_seed(7)
+        xs = [torch.randn(64, 256, generator=g).bfloat16() for _ in range(6)]
+        if rank == 0:
+            tx = mq.PeerTransport(peer=1, role="send", slot_bytes=64 * 256 * 2, slots=2)
+            ch = mq.Channel((0, 0), (0, 0), tx)
+            for i, x in enumerate(xs):
+                ch.push(x.cuda(), mq.MessageMeta((64, 256), 2, "teacher", (0, 0), 100 + i))
+            torch.cuda.synchronize()
+            dist.barrier()  # the receiver has copied everything out before the sender frees
+            tx.close()
+            q.put(("ok", None))
+        else:
+            rx = mq.PeerTransport(peer=0, role="recv", slot_bytes=64 * 256 * 2, slots=2)
+            ep = mq.Endpoint((0, 0), plan, {(0, 0): mq.Channel((0, 0), (0, 0), rx)}, torch.bfloat16)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                got = [ep.pull(validate=False)[0] for _ in xs]
+            torch.cuda.synchronize()
+            ids = [m.sample_id for m in ep.verify()]
+            ok = all(torch.equal(a.cpu(), b) for a, b in zip(got, xs))
+            dist.barrier()
+            rx.close()
+            q.put(("ok", (ok, ids)))
+    except Exception as e:  # noqa: BLE001
+        q.put(("err", repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_peer_transport_two_processes_one_gpu():
+    """The cross-process PeerTransport path (IPC handle exchange over the process group, slot
+    ring in the receiver's memory, credits in the sender's) between two processes sharing one
+    GPU, so it runs on a single-GPU box; the ring has two slots for six messages, so the sender's
+    later puts wait in-stream for the receiver's credits."""
+    import torch.multiprocessing as tmp
+
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    port = 31500 + random.Random(os.getpid()).randint(0, 2000)
+    procs = [ctx.Process(target=_peer_worker, args=(r, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    try:
+        res = [q.get(timeout=180) for _ in procs]
+    finally:
+        for p in procs:
+            p.join(timeout=30)
+            if p.is_alive():
+                p.kill()
+    assert all(r[0] == "ok" for r in res), res
+    ok, ids = [r[1] for r in res if r[1] is not None][0]
+    assert ok and ids == [100 + i for i in range(6)]
