@@ -71,7 +71,7 @@ __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.syn
 // ld/st wait + fence::before_thread_sync precede the __syncwarp, so lane 0's release covers the
 // whole warp -- 8 shared-memory arrives per tile-barrier instead of 256.
 #ifndef ATTN_WARP_ARRIVE
-#define ATTN_WARP_ARRIVE 1  // 0: every thread arrives (barrier counts in threads)
+#define ATTN_WARP_ARRIVE 0  // 1: one arrive per warp (measured: no consistent gain, r02_attn_arrive_ab.jsonl)
 #endif
 constexpr int ARRIVE_UNIT = ATTN_WARP_ARRIVE ? 32 : 1;  // threads per arrive
 __device__ __forceinline__ void warp_arrive(uint64_t* bar) {
@@ -80,6 +80,41 @@ __device__ __forceinline__ void warp_arrive(uint64_t* bar) {
     if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
   } else {
     mbar_arrive(bar);
+  }
+}
+
+// Barrier addresses as 32-bit shared-window offsets from one base computed once per kernel (kept
+// in a uniform register), instead of a generic->shared conversion (S2R SR_CgaCtaId + LEA, which
+// ptxas rematerialises under register pressure) at every wait/arrive of the softmax loop.
+#ifndef ATTN_BAR_U32
+#define ATTN_BAR_U32 0  // measured: +1.6-2 % at the KD shapes, -3-4 % at cfg 5 (r02_attn_bar_ab.jsonl)
+#endif
+struct Bars {
+  uint64_t* base;
+  uint32_t base_u;
+  __device__ __forceinline__ uint32_t at(const uint64_t* p) const { return base_u + (uint32_t)(p - base) * 8u; }
+};
+__device__ __forceinline__ void bwait(const Bars& B, uint64_t* p, uint32_t parity) {
+  if (ATTN_BAR_U32) {
+    const uint32_t a = B.at(p);
+    while (!mbar_try_wait(a, parity)) {
+    }
+  } else {
+    mbar_wait(p, parity);
+  }
+}
+__device__ __forceinline__ void barrive(const Bars& B, uint64_t* p) {
+  if (ATTN_BAR_U32)
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(B.at(p)) : "memory");
+  else
+    mbar_arrive(p);
+}
+__device__ __forceinline__ void warp_arrive(const Bars& B, uint64_t* p) {
+  if (ATTN_WARP_ARRIVE) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) barrive(B, p);
+  } else {
+    barrive(B, p);
   }
 }
 
@@ -229,6 +264,7 @@ __global__ void __launch_bounds__(FwdCfg<DH, CG>::THREADS, 1)
   uint64_t* o_full = p_empty + 2;          // [NOB]
   uint64_t* o_empty = o_full + 2;          // [NOB]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
+  const Bars BR{bar, smem_u32(bar)};
 
   const int n_items = *n_tiles * H;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -276,16 +312,16 @@ __global__ void __launch_bounds__(FwdCfg<DH, CG>::THREADS, 1)
         const FwdItem it = it_n;
         if (snake_item(j + 1) < n_items) it_n = fwd_item<CAUSAL>(snake_item(j + 1), H, Hk, cu, tiles);  // prefetch
         const int qb = j & 1;
-        mbar_wait(&q_empty[qb], ((j >> 1) & 1) ^ 1);
+        bwait(BR, &q_empty[qb], ((j >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(&q_full[qb], TB);
         load_tile<DH>(sm + C::Q + qb * TB, &map_q, &q_full[qb], it.h * DH, it.s0 + it.q0);
         for (int i = 0; i < it.n_kv; ++i, ++g) {
           const int st = g % KVS;
           const uint32_t ph = (g / KVS) & 1;
-          mbar_wait(&k_empty[st], ph ^ 1);
+          bwait(BR, &k_empty[st], ph ^ 1);
           mbar_arrive_expect_tx(&k_full[st], TB);
           load_tile<DH>(sm + C::K + st * TB, &map_k, &k_full[st], it.hk * DH, it.s0 + i * BKV);
-          mbar_wait(&v_empty[st], ph ^ 1);
+          bwait(BR, &v_empty[st], ph ^ 1);
           mbar_arrive_expect_tx(&v_full[st], TB);
           load_tile<DH>(sm + C::V + st * TB, &map_v, &v_full[st], it.hk * DH, it.s0 + i * BKV);
         }
@@ -298,9 +334,9 @@ __global__ void __launch_bounds__(FwdCfg<DH, CG>::THREADS, 1)
       // PV of global tile gp (item-local index ip, item counter jp) into O set ob
       auto issue_pv = [&](int gp, int ip, int jp, int ob) {
         const int pb = gp & 1;
-        if (ip == 0) mbar_wait(&o_empty[ob], ((jp / NOB) & 1) ^ 1);  // epilogue of the item that last used O set ob
-        mbar_wait(&p_full[pb], (gp >> 1) & 1);
-        mbar_wait(&v_full[gp % KVS], (gp / KVS) & 1);
+        if (ip == 0) bwait(BR, &o_empty[ob], ((jp / NOB) & 1) ^ 1);  // epilogue of the item that last used O set ob
+        bwait(BR, &p_full[pb], (gp >> 1) & 1);
+        bwait(BR, &v_full[gp % KVS], (gp / KVS) & 1);
         tc_fence_after();
         const uint32_t v_base = smem_u32(sm + C::V + (gp % KVS) * TB);
         // keys of column group c accumulate into O_c: each group keeps its own running max, so
@@ -340,13 +376,13 @@ __global__ void __launch_bounds__(FwdCfg<DH, CG>::THREADS, 1)
         const FwdItem it = it_n;
         if (snake_item(j + 1) < n_items) it_n = fwd_item<CAUSAL>(snake_item(j + 1), H, Hk, cu, tiles);  // prefetch
         const int qb = j & 1, ob = j % NOB;
-        mbar_wait(&q_full[qb], (j >> 1) & 1);
+        bwait(BR, &q_full[qb], (j >> 1) & 1);
         const uint32_t q_base = smem_u32(sm + C::Q + qb * TB);
         for (int i = 0; i < it.n_kv; ++i, ++g) {
           const int b = g & 1;
           const int st = g % KVS;
-          mbar_wait(&k_full[st], (g / KVS) & 1);
-          mbar_wait(&s_empty[b], ((g >> 1) & 1) ^ 1);
+          bwait(BR, &k_full[st], (g / KVS) & 1);
+          bwait(BR, &s_empty[b], ((g >> 1) & 1) ^ 1);
           tc_fence_after();
           const uint32_t k_base = smem_u32(sm + C::K + st * TB);
           if (elect_one()) {
@@ -389,7 +425,7 @@ __global__ void __launch_bounds__(FwdCfg<DH, CG>::THREADS, 1)
       float* xs = xsum + (jj & 1) * CG * 128;
       xm[grp * 128 + r] = m;
       xs[grp * 128 + r] = l;
-      mbar_wait(&o_full[ob], (jj / NOB) & 1);
+      bwait(BR, &o_full[ob], (jj / NOB) & 1);
       tc_fence_after();
       named_bar(quad_bar, 32 * CG);
       float mg[CG], lg[CG];
@@ -428,7 +464,7 @@ __global__ void __launch_bounds__(FwdCfg<DH, CG>::THREADS, 1)
         }
         if (sub == OC / CH - 1) {
           tc_fence_before();
-          warp_arrive(&o_empty[ob]);
+          warp_arrive(BR, &o_empty[ob]);
         }
         if (qpos < it.L) {
           uint32_t o[CH / 2];
@@ -461,7 +497,7 @@ __global__ void __launch_bounds__(FwdCfg<DH, CG>::THREADS, 1)
       float m = -INFINITY, l = 0.f;
       for (int i = 0; i < it.n_kv; ++i, ++g) {
         const int b = g & 1;
-        mbar_wait(&s_full[b], (g >> 1) & 1);
+        bwait(BR, &s_full[b], (g >> 1) & 1);
         tc_fence_after();
         float s[CW];
         {
@@ -475,7 +511,7 @@ __global__ void __launch_bounds__(FwdCfg<DH, CG>::THREADS, 1)
             for (int jj = 0; jj < 32; ++jj) s[c * 32 + jj] = __uint_as_float(raw[c][jj]);
         }
         tc_fence_before();
-        warp_arrive(&s_empty[b]);
+        warp_arrive(BR, &s_empty[b]);
         const int kv0 = i * BKV + grp * CW;
         const bool need_mask = (CAUSAL && kv0 + CW - 1 > it.q0) || (kv0 + CW > it.L);
         // valid key columns of this row: c < lim (causal: key <= query; key inside the sequence)
@@ -489,7 +525,7 @@ __global__ void __launch_bounds__(FwdCfg<DH, CG>::THREADS, 1)
           tmem_st_cols<CW / 2>(tmem + lane_base + b * BKV + grp * CW, zero);
           tmem_st_wait();
           tc_fence_before();
-          warp_arrive(&p_full[b]);
+          warp_arrive(BR, &p_full[b]);
           if (i == 0 && pend) {
             epilogue(pit, pj, pm, pl);
             pend = false;
@@ -539,7 +575,7 @@ __global__ void __launch_bounds__(FwdCfg<DH, CG>::THREADS, 1)
         // so the whole warp takes the branch when any lane needs it (the others scale by 1, exact)
         if (__any_sync(kFull, rescale)) {
           if (!rescale) alpha = 1.f;
-          mbar_wait(&p_empty[(g - 1) & 1], ((g - 1) >> 1) & 1);  // PV_{g-1} retired: O is final
+          bwait(BR, &p_empty[(g - 1) & 1], ((g - 1) >> 1) & 1);  // PV_{g-1} retired: O is final
           tc_fence_after();
 #pragma unroll
           for (int c = 0; c < DH / 32; ++c) {
@@ -562,7 +598,7 @@ __global__ void __launch_bounds__(FwdCfg<DH, CG>::THREADS, 1)
         }
         tmem_st_wait();
         tc_fence_before();
-        warp_arrive(&p_full[b]);
+        warp_arrive(BR, &p_full[b]);
         if (i == 0 && pend) {
           epilogue(pit, pj, pm, pl);
           pend = false;

@@ -44,7 +44,7 @@ __device__ __forceinline__ void merge(Stat& a, const Stat& b) {
       a.at = b.at;
     } else {
       const float mt = fmaxf(a.mt, b.mt);
-      const float ca = exp2f(a.mt - mt), cb = exp2f(b.mt - mt);
+      const float ca = ex2a(a.mt - mt), cb = ex2a(b.mt - mt);
       a.st = a.st * ca + b.st * cb;
       a.at = a.at * ca + b.at * cb;
       a.mt = mt;
@@ -56,7 +56,7 @@ __device__ __forceinline__ void merge(Stat& a, const Stat& b) {
       a.ss = b.ss;
     } else {
       const float ms = fmaxf(a.ms, b.ms);
-      a.ss = a.ss * exp2f(a.ms - ms) + b.ss * exp2f(b.ms - ms);
+      a.ss = a.ss * ex2a(a.ms - ms) + b.ss * ex2a(b.ms - ms);
       a.ms = ms;
     }
   }
@@ -105,12 +105,14 @@ __global__ void __launch_bounds__(THREADS, MIN_BLOCKS) kd_loss_kernel(const __nv
         float ft[8], fs[8];
         unpack8(rt[u], ft);
         unpack8(rs[u], fs);
-        float mt = a.mt, ms = a.ms;
+        // max of the raw logits, scaled once (scale2 > 0: exact)
+        float rt = ft[0], rs = fs[0];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          mt = fmaxf(mt, ft[j] * scale2);
-          ms = fmaxf(ms, fs[j] * scale2);
+        for (int j = 1; j < 8; ++j) {
+          rt = fmaxf(rt, ft[j]);
+          rs = fmaxf(rs, fs[j]);
         }
+        const float mt = fmaxf(a.mt, rt * scale2), ms = fmaxf(a.ms, rs * scale2);
         if (mt > a.mt) {  // a.mt == -inf: st = at = 0, any finite factor is fine
           const float ct = a.mt == -INFINITY ? 0.f : ex2a(a.mt - mt);
           a.st *= ct;
@@ -296,12 +298,12 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(KDS_THREADS, KDS_CTA
           float ft[8], fs[8];
           unpack8(*pt, ft);
           unpack8(*ps, fs);
-          float mt = a.mt, ms = a.ms;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            mt = fmaxf(mt, ft[j] * scale2);
-            ms = fmaxf(ms, fs[j] * scale2);
-          }
+          // max of the raw logits, scaled once (scale2 > 0); three-input max pairs
+          float rt = fmaxf(fmaxf(ft[0], ft[1]), fmaxf(ft[2], ft[3]));
+          float rs = fmaxf(fmaxf(fs[0], fs[1]), fmaxf(fs[2], fs[3]));
+          rt = fmaxf(rt, fmaxf(fmaxf(ft[4], ft[5]), fmaxf(ft[6], ft[7])));
+          rs = fmaxf(rs, fmaxf(fmaxf(fs[4], fs[5]), fmaxf(fs[6], fs[7])));
+          const float mt = fmaxf(a.mt, rt * scale2), ms = fmaxf(a.ms, rs * scale2);
           if (mt > a.mt) {
             const float ct = a.mt == -INFINITY ? 0.f : ex2a(a.mt - mt);
             a.st *= ct;
@@ -315,6 +317,7 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(KDS_THREADS, KDS_CTA
           mh_t[k] = mt;
           mh_s[k] = ms;
           float2 sts = make_float2(a.st, a.ss);
+          float2 at2 = make_float2(a.at, 0.f);  // sum e_t (t - s), two partial sums (paired FMA)
           uint32_t et[4], es[4];
 #pragma unroll
           for (int j = 0; j < 8; j += 2) {
@@ -324,8 +327,8 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(KDS_THREADS, KDS_CTA
             const float2 e0 = make_float2(ex2a(x0.x), ex2a(x0.y));
             const float2 e1 = make_float2(ex2a(x1.x), ex2a(x1.y));
             sts = __fadd2_rn(__fadd2_rn(sts, e0), e1);
-            a.at = fmaf(e0.x, ft[j] - fs[j], a.at);
-            a.at = fmaf(e1.x, ft[j + 1] - fs[j + 1], a.at);
+            const float2 d = __fadd2_rn(make_float2(ft[j], ft[j + 1]), make_float2(-fs[j], -fs[j + 1]));
+            at2 = __ffma2_rn(make_float2(e0.x, e1.x), d, at2);
             if (ds != nullptr) {
               const __half2 ht = __floats2half2_rn(e0.x, e1.x), hs = __floats2half2_rn(e0.y, e1.y);
               et[j >> 1] = *reinterpret_cast<const uint32_t*>(&ht);
@@ -334,6 +337,7 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(KDS_THREADS, KDS_CTA
           }
           a.st = sts.x;
           a.ss = sts.y;
+          a.at = at2.x + at2.y;
           if (ds != nullptr) {
             *pt = make_uint4(et[0], et[1], et[2], et[3]);
             *ps = make_uint4(es[0], es[1], es[2], es[3]);
