@@ -38,7 +38,8 @@ constexpr int BQ = 128, BKV = 128;  // forward query tile, key tile (rows)
 constexpr float LOG2E_F = 1.4426950408889634f;
 constexpr float LN2_F = 0.6931471805599453f;
 
-// Query-tile list, heaviest (largest causal row count) first: tiles[i] = (seq, q0)
+// Query-tile list (tiles of QT rows), heaviest (largest causal row count) first: tiles[i] = (seq, q0)
+template <int QT = BQ>
 __global__ void attn_tiles_kernel(const int32_t* __restrict__ cu, int nseq, int2* __restrict__ tiles,
                                   int* __restrict__ count) {
   __shared__ int s_max, s_n;
@@ -47,18 +48,18 @@ __global__ void attn_tiles_kernel(const int32_t* __restrict__ cu, int nseq, int2
     s_n = 0;
   }
   __syncthreads();
-  for (int j = threadIdx.x; j < nseq; j += blockDim.x) atomicMax(&s_max, (cu[j + 1] - cu[j] + BQ - 1) / BQ);
+  for (int j = threadIdx.x; j < nseq; j += blockDim.x) atomicMax(&s_max, (cu[j + 1] - cu[j] + QT - 1) / QT);
   __syncthreads();
   for (int qb = s_max - 1; qb >= 0; --qb) {
     for (int j0 = 0; j0 < nseq; j0 += blockDim.x) {
       const int j = j0 + threadIdx.x;
-      const bool has = j < nseq && (cu[j + 1] - cu[j] + BQ - 1) / BQ > qb;
+      const bool has = j < nseq && (cu[j + 1] - cu[j] + QT - 1) / QT > qb;
       const unsigned bal = __ballot_sync(kFull, has);
       // warp-aggregated append (order inside a qb level is irrelevant)
       int base = 0;
       if ((threadIdx.x & 31) == 0 && bal) base = atomicAdd(&s_n, __popc(bal));
       base = __shfl_sync(kFull, base, 0);
-      if (has) tiles[base + __popc(bal & ((1u << (threadIdx.x & 31)) - 1u))] = make_int2(j, qb * BQ);
+      if (has) tiles[base + __popc(bal & ((1u << (threadIdx.x & 31)) - 1u))] = make_int2(j, qb * QT);
     }
     __syncthreads();
   }
@@ -126,6 +127,9 @@ __device__ __forceinline__ void warp_arrive(const Bars& B, uint64_t* p) {
 #endif
 #ifndef ATTN_FWD_CG64
 #define ATTN_FWD_CG64 2  // default column groups of the head_dim-64 forward (see FwdCfg)
+#endif
+#ifndef ATTN_FWD_VARIANT
+#define ATTN_FWD_VARIANT 0  // default forward: 0 shared tile, 1 decoupled groups, 2 ping-pong (MAESTRO_ATTN_FWD=base|dec|pp)
 #endif
 #ifndef FWD_EMU_BITS
 #define FWD_EMU_BITS 0x92  // pair p of a row's 32 goes to the FMA pipe if bit (p & 7) is set (3/8)
@@ -613,6 +617,758 @@ __global__ void __launch_bounds__(FwdCfg<DH, CG>::THREADS, 1)
       w = w_next;
     }
     if (pend) epilogue(pit, pj, pm, pl);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Forward, decoupled column groups.  The two 64-key column groups of a tile get independent
+// pipelines: each has its own MMA-issuing warp (S_g = Q K_g^T with N = 64 into its own
+// double-buffered score columns, O_g += P_g V_g), its own barriers and its own O accumulator;
+// they share only the Q buffers and the K/V ring (stages released after both groups' MMAs).
+// With one shared S tile (attn_fwd_kernel) the two softmax warps of an SM sub-partition wait
+// on the same barriers and run the same phase (TMEM load -> max -> exponentials -> pack ->
+// TMEM store) at the same time, so the exponential unit idles through the other phases.  Here
+// group 1 starts `stagger_ns` late and nothing re-synchronises the groups inside an item, so the
+// two warps of a sub-partition work on different phases.  The item epilogue is done by whichever
+// group's warp of a lane quadrant arrives second (shared-memory counter): it combines both O
+// halves and stores O and the LSE; the first arriver moves on to the next item.
+// Warps: w0 TMA, w1 / w2 MMA for groups 0 / 1, w3..w10 softmax (group (w - 3) / 4, quadrant w & 3).
+// TMEM: S_g buffer b at g * 128 + b * 64; O_g at 256 + (ob * 2 + g) * 64 (head_dim 64, two sets by
+// item) or 256 + g * 128 (head_dim 128, one set).
+template <int DH>
+struct FwdDecCfg {
+  static constexpr int SW0 = 3;
+  static constexpr int THREADS = 32 * SW0 + 256;
+  static constexpr int TILE = 128 * DH * 2;
+  static constexpr int KVS = DH == 64 ? 3 : 2;
+  static constexpr int NOB = DH == 64 ? 2 : 1;
+  static constexpr int Q = 0;
+  static constexpr int K = Q + 2 * TILE;
+  static constexpr int V = K + KVS * TILE;
+  static constexpr int XMAX = V + KVS * TILE;  // [2 items][2 groups][128]
+  static constexpr int XSUM = XMAX + 2 * 2 * 128 * 4;
+  static constexpr int CNT = XSUM + 2 * 2 * 128 * 4;  // [2 items][4 quadrants] arrivals
+  static constexpr int BAR = CNT + 64;
+  static constexpr int TOTAL = BAR + 512;
+  static_assert(TOTAL + 1024 <= 227 * 1024, "forward smem");
+  __device__ static constexpr uint32_t o_col(int ob, int g) { return NOB == 2 ? 256 + (ob * 2 + g) * DH : 256 + g * DH; }
+};
+
+template <int DH, bool CAUSAL>
+__global__ void __launch_bounds__(FwdDecCfg<DH>::THREADS, 1)
+    attn_fwd_dec_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
+                        const __grid_constant__ CUtensorMap map_v, const int32_t* __restrict__ cu,
+                        const int2* __restrict__ tiles, const int* __restrict__ n_tiles,
+                        __nv_bfloat16* __restrict__ out, int ldo, float* __restrict__ lse, int T, int H, int Hk,
+                        float scale2, int stagger_ns) {
+  using C = FwdDecCfg<DH>;
+  constexpr int KVS = C::KVS, NOB = C::NOB, TB = C::TILE, CW = 64;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* sm = align_smem_1024(smem_raw);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::BAR);
+  uint64_t* q_full = bar;          // [2]
+  uint64_t* q_empty = bar + 2;     // [2]
+  uint64_t* k_full = bar + 4;      // [KVS]
+  uint64_t* k_empty = k_full + KVS;
+  uint64_t* v_full = k_empty + KVS;
+  uint64_t* v_empty = v_full + KVS;
+  uint64_t* gb = v_empty + KVS;    // per group: s_full[2] s_empty[2] p_full[2] p_empty[2] o_full[2] o_empty[2]
+  auto s_full = [&](int g) { return gb + 12 * g; };
+  auto s_empty = [&](int g) { return gb + 12 * g + 2; };
+  auto p_full = [&](int g) { return gb + 12 * g + 4; };
+  auto p_empty = [&](int g) { return gb + 12 * g + 6; };
+  auto o_full = [&](int g) { return gb + 12 * g + 8; };
+  auto o_empty = [&](int g) { return gb + 12 * g + 10; };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gb + 24);
+  int* cnt = reinterpret_cast<int*>(sm + C::CNT);
+
+  const int n_items = *n_tiles * H;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&map_q);
+    tma_prefetch(&map_k);
+    tma_prefetch(&map_v);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&q_full[b], 1);
+      mbar_init(&q_empty[b], 2);
+    }
+    for (int s = 0; s < KVS; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 2);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 2);
+    }
+    for (int g = 0; g < 2; ++g)
+      for (int b = 0; b < 2; ++b) {
+        mbar_init(&s_full(g)[b], 1);
+        mbar_init(&s_empty(g)[b], 128);
+        mbar_init(&p_full(g)[b], 128);
+        mbar_init(&p_empty(g)[b], 1);
+        mbar_init(&o_full(g)[b], 1);
+        mbar_init(&o_empty(g)[b], 128);
+      }
+    for (int k = 0; k < 8; ++k) cnt[k] = 0;
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int g = 0, j = 0;
+      FwdItem it_n{};
+      if (snake_item(0) < n_items) it_n = fwd_item<CAUSAL>(snake_item(0), H, Hk, cu, tiles);
+      for (int w = snake_item(0); w < n_items; w = snake_item(j + 1), ++j) {
+        const FwdItem it = it_n;
+        if (snake_item(j + 1) < n_items) it_n = fwd_item<CAUSAL>(snake_item(j + 1), H, Hk, cu, tiles);
+        const int qb = j & 1;
+        mbar_wait(&q_empty[qb], ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&q_full[qb], TB);
+        load_tile<DH>(sm + C::Q + qb * TB, &map_q, &q_full[qb], it.h * DH, it.s0 + it.q0);
+        for (int i = 0; i < it.n_kv; ++i, ++g) {
+          const int st = g % KVS;
+          const uint32_t ph = (g / KVS) & 1;
+          mbar_wait(&k_empty[st], ph ^ 1);
+          mbar_arrive_expect_tx(&k_full[st], TB);
+          load_tile<DH>(sm + C::K + st * TB, &map_k, &k_full[st], it.hk * DH, it.s0 + i * BKV);
+          mbar_wait(&v_empty[st], ph ^ 1);
+          mbar_arrive_expect_tx(&v_full[st], TB);
+          load_tile<DH>(sm + C::V + st * TB, &map_v, &v_full[st], it.hk * DH, it.s0 + i * BKV);
+        }
+      }
+    }
+  } else if (warp <= 2) {
+    const int mg = warp - 1;  // column group served by this MMA warp
+    if (mg == 1 && stagger_ns > 0) __nanosleep(stagger_ns);
+    constexpr uint32_t idesc_s = idesc_bf16_f32(BQ, CW, false, false);
+    constexpr uint32_t idesc_o = idesc_bf16_f32(BQ, DH, false, true);
+    uint64_t *sf = s_full(mg), *se = s_empty(mg), *pf = p_full(mg), *pe = p_empty(mg), *of = o_full(mg),
+             *oe = o_empty(mg);
+    auto issue_pv = [&](int gp, int ip, int jp, int ob) {
+      const int pb = gp & 1;
+      if (ip == 0) mbar_wait(&oe[ob], ((jp / NOB) & 1) ^ 1);
+      mbar_wait(&pf[pb], (gp >> 1) & 1);
+      mbar_wait(&v_full[gp % KVS], (gp / KVS) & 1);
+      tc_fence_after();
+      const uint32_t v_base = smem_u32(sm + C::V + (gp % KVS) * TB);
+      if (elect_one()) {
+#pragma unroll
+        for (int kc = 0; kc < CW / 16; ++kc)  // keys 64 mg + 16 kc (V as an MN-major operand)
+          umma_bf16_ts(tmem + C::o_col(ob, mg), tmem + mg * 128 + pb * CW + kc * 8,
+                       sdesc((v_base >> 4) + (4 * mg + kc) * 128, DH == 64 ? 8192 : 16384, 1024), idesc_o,
+                       (ip > 0 || kc > 0) ? 1u : 0u);
+        umma_commit(&v_empty[gp % KVS]);
+        umma_commit(&pe[pb]);
+      }
+      __syncwarp();
+    };
+    int g = 0, j = 0;
+    int pend_g = -1, pend_i = 0, pend_j = 0, pend_o = 0;
+    bool pend_last = false;
+    auto flush = [&]() {
+      if (pend_g < 0) return;
+      issue_pv(pend_g, pend_i, pend_j, pend_o);
+      if (pend_last) {
+        if (elect_one()) umma_commit(&of[pend_o]);
+        __syncwarp();
+      }
+      pend_g = -1;
+    };
+    FwdItem it_n{};
+    if (snake_item(0) < n_items) it_n = fwd_item<CAUSAL>(snake_item(0), H, Hk, cu, tiles);
+    for (int w = snake_item(0); w < n_items; w = snake_item(j + 1), ++j) {
+      const FwdItem it = it_n;
+      if (snake_item(j + 1) < n_items) it_n = fwd_item<CAUSAL>(snake_item(j + 1), H, Hk, cu, tiles);
+      const int qb = j & 1, ob = j % NOB;
+      mbar_wait(&q_full[qb], (j >> 1) & 1);
+      const uint32_t q_base = smem_u32(sm + C::Q + qb * TB);
+      for (int i = 0; i < it.n_kv; ++i, ++g) {
+        const int b = g & 1;
+        const int st = g % KVS;
+        mbar_wait(&k_full[st], (g / KVS) & 1);
+        mbar_wait(&se[b], ((g >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t k_base = smem_u32(sm + C::K + st * TB);
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < DH / 16; ++kk)  // B = keys 64 mg .. 64 mg + 63 of the tile (8 KB into each chunk)
+            umma_bf16(tmem + mg * 128 + b * CW, sdesc((q_base >> 4) + (kk >> 2) * 1024 + (kk & 3) * 2, 16, 1024),
+                      sdesc((k_base >> 4) + (kk >> 2) * 1024 + (kk & 3) * 2 + 512 * mg, 16, 1024), idesc_s,
+                      kk > 0 ? 1u : 0u);
+          umma_commit(&k_empty[st]);
+          umma_commit(&sf[b]);
+          if (i == it.n_kv - 1) umma_commit(&q_empty[qb]);
+        }
+        __syncwarp();
+        flush();
+        pend_g = g;
+        pend_i = i;
+        pend_j = j;
+        pend_o = ob;
+        pend_last = i == it.n_kv - 1;
+      }
+    }
+    flush();
+  } else {
+    const int q = warp & 3;
+    const int grp = (warp - C::SW0) >> 2;
+    const int r = q * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    float* xmax = reinterpret_cast<float*>(sm + C::XMAX);
+    float* xsum = reinterpret_cast<float*>(sm + C::XSUM);
+    uint64_t *sf = s_full(grp), *se = s_empty(grp), *pf = p_full(grp), *pe = p_empty(grp);
+    // Item jj is finished by whichever group's warp of this quadrant arrives second.
+    auto epilogue = [&](const FwdItem& it, int jj, float m, float l) {
+      const int ob = jj % NOB, par = jj & 1;
+      xmax[(par * 2 + grp) * 128 + r] = m;
+      xsum[(par * 2 + grp) * 128 + r] = l;
+      __threadfence_block();
+      __syncwarp();
+      int old = 0;
+      if (lane == 0) old = atomicAdd(&cnt[par * 4 + q], 1);
+      old = __shfl_sync(kFull, old, 0);
+      if (old == 0) return;
+      __threadfence_block();
+      const uint32_t ph = (jj / NOB) & 1;
+      mbar_wait(&o_full(0)[ob], ph);
+      mbar_wait(&o_full(1)[ob], ph);
+      tc_fence_after();
+      const float m0 = xmax[(par * 2) * 128 + r], m1 = xmax[(par * 2 + 1) * 128 + r];
+      const float l0 = xsum[(par * 2) * 128 + r], l1 = xsum[(par * 2 + 1) * 128 + r];
+      const float M = fmaxf(m0, m1);
+      float f0 = m0 == -INFINITY ? 0.f : ex2(m0 - M), f1 = m1 == -INFINITY ? 0.f : ex2(m1 - M);
+      const float l_all = l0 * f0 + l1 * f1;
+      const float rl = __frcp_rn(l_all);
+      f0 *= rl;
+      f1 *= rl;
+      const int qpos = it.q0 + r;
+#pragma unroll
+      for (int sub = 0; sub < DH / 32; ++sub) {
+        uint32_t ra[32], rb[32];
+        tmem_ld_32x32b_x32(tmem + lane_base + C::o_col(ob, 0) + sub * 32, ra);
+        tmem_ld_32x32b_x32(tmem + lane_base + C::o_col(ob, 1) + sub * 32, rb);
+        tmem_ld_wait();
+        if (sub == DH / 32 - 1) {  // both O sets read: the slot's counter is reset before release
+          if (lane == 0) cnt[par * 4 + q] = 0;
+          __threadfence_block();
+          tc_fence_before();
+          mbar_arrive(&o_empty(0)[ob]);
+          mbar_arrive(&o_empty(1)[ob]);
+        }
+        if (qpos < it.L) {
+          uint32_t o[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            o[e] = pack_bf16(__uint_as_float(ra[2 * e]) * f0 + __uint_as_float(rb[2 * e]) * f1,
+                             __uint_as_float(ra[2 * e + 1]) * f0 + __uint_as_float(rb[2 * e + 1]) * f1);
+          uint4* dst = reinterpret_cast<uint4*>(out + (size_t)(it.s0 + qpos) * ldo + it.h * DH + sub * 32);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) dst[u] = make_uint4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);
+        }
+      }
+      if (qpos < it.L) lse[(size_t)it.h * T + it.s0 + qpos] = (M + log2f(l_all)) * LN2_F;
+    };
+    int g = 0, j = 0;
+    bool pend = false;
+    FwdItem pit{};
+    int pj = 0;
+    float pm = 0.f, pl = 0.f;
+    int w = snake_item(0);
+    FwdItem it{};
+    if (w < n_items) it = fwd_item<CAUSAL>(w, H, Hk, cu, tiles);
+    for (; w < n_items; ++j) {
+      const int w_next = snake_item(j + 1);
+      FwdItem nxt{};
+      if (w_next < n_items) nxt = fwd_item<CAUSAL>(w_next, H, Hk, cu, tiles);
+      const int ob = j % NOB;
+      const int qpos = it.q0 + r;
+      float m = -INFINITY, l = 0.f;
+      for (int i = 0; i < it.n_kv; ++i, ++g) {
+        const int b = g & 1;
+        mbar_wait(&sf[b], (g >> 1) & 1);
+        tc_fence_after();
+        const uint32_t s_col = tmem + lane_base + grp * 128 + b * CW;
+        float s[CW];
+        {
+          uint32_t raw[2][32];
+          tmem_ld_32x32b_x32(s_col, raw[0]);
+          tmem_ld_32x32b_x32(s_col + 32, raw[1]);
+          tmem_ld_wait();
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) s[c * 32 + jj] = __uint_as_float(raw[c][jj]);
+        }
+        tc_fence_before();
+        mbar_arrive(&se[b]);
+        const int kv0 = i * BKV + grp * CW;
+        const bool need_mask = (CAUSAL && kv0 + CW - 1 > it.q0) || (kv0 + CW > it.L);
+        const int lim = CAUSAL ? min(qpos - kv0 + 1, it.L - kv0) : it.L - kv0;
+        if (need_mask && __all_sync(kFull, lim <= 0)) {
+          uint32_t zero[CW / 2];
+#pragma unroll
+          for (int e = 0; e < CW / 2; ++e) zero[e] = 0u;
+          tmem_st_32x32b_x32(s_col, zero);
+          tmem_st_wait();
+          tc_fence_before();
+          mbar_arrive(&pf[b]);
+          if (i == 0 && pend) {
+            epilogue(pit, pj, pm, pl);
+            pend = false;
+          }
+          continue;
+        }
+        float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        if (need_mask) {
+#pragma unroll
+          for (int c = 0; c < CW; ++c) {
+            s[c] = c < lim ? s[c] : -INFINITY;
+            mx4[c & 3] = fmaxf(mx4[c & 3], s[c]);
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < CW; ++c) mx4[c & 3] = fmaxf(mx4[c & 3], s[c]);
+        }
+        const float m_new = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * scale2;
+        bool rescale = false;
+        float alpha = 1.f;
+        if (m_new > m + 8.0f) {
+          alpha = ex2(m - m_new);
+          m = m_new;
+          rescale = i > 0;
+        }
+        const float neg_m = m == -INFINITY ? 0.f : -m;
+        const float2 sc2 = make_float2(scale2, scale2), nm2 = make_float2(neg_m, neg_m);
+        float2 sum2[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+#pragma unroll
+        for (int c = 0; c < CW; c += 2) {
+          const float2 x = __ffma2_rn(make_float2(s[c], s[c + 1]), sc2, nm2);
+          if ((FWD_EMU_BITS >> ((c >> 1) & 7)) & 1) {
+            const float2 e = ex2_fma2<3>(x);
+            s[c] = e.x;
+            s[c + 1] = e.y;
+          } else {
+            s[c] = ex2(x.x);
+            s[c + 1] = ex2(x.y);
+          }
+          sum2[(c >> 1) & 3] = __fadd2_rn(sum2[(c >> 1) & 3], make_float2(s[c], s[c + 1]));
+        }
+        const float2 t01 = __fadd2_rn(sum2[0], sum2[1]), t23 = __fadd2_rn(sum2[2], sum2[3]);
+        const float2 t = __fadd2_rn(t01, t23);
+        l = l * alpha + (t.x + t.y);
+        if (__any_sync(kFull, rescale)) {  // warp-collective TMEM access (see attn_fwd_kernel)
+          if (!rescale) alpha = 1.f;
+          mbar_wait(&pe[(g - 1) & 1], ((g - 1) >> 1) & 1);  // PV_{g-1} of this group retired
+          tc_fence_after();
+#pragma unroll
+          for (int c = 0; c < DH / 32; ++c) {
+            uint32_t rr[32];
+            tmem_ld_32x32b_x32(tmem + lane_base + C::o_col(ob, grp) + c * 32, rr);
+            tmem_ld_wait();
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) rr[jj] = __float_as_uint(__uint_as_float(rr[jj]) * alpha);
+            tmem_st_32x32b_x32(tmem + lane_base + C::o_col(ob, grp) + c * 32, rr);
+          }
+          tmem_st_wait();
+        }
+        {
+          uint32_t pk[CW / 2];
+#pragma unroll
+          for (int e = 0; e < CW / 2; ++e) pk[e] = pack_bf16(s[2 * e], s[2 * e + 1]);
+          tmem_st_32x32b_x32(s_col, pk);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&pf[b]);
+        if (i == 0 && pend) {
+          epilogue(pit, pj, pm, pl);
+          pend = false;
+        }
+      }
+      pend = true;
+      pit = it;
+      pj = j;
+      pm = m;
+      pl = l;
+      it = nxt;
+      w = w_next;
+    }
+    if (pend) epilogue(pit, pj, pm, pl);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Forward, ping-pong (FA4-style): one CTA item = 256 queries (two 128-row Q tiles A and B) of
+// one head, sharing every K/V tile.  Each Q tile has its own softmax warpgroup (thread = row, all
+// 128 key columns, read from TMEM in two 64-column halves: row max, then exponentials), its own
+// S buffer and O accumulator.  The MMA warp issues S_A(0) S_B(0), then per KV tile
+// PV_A(i) S_A(i+1) PV_B(i) S_B(i+1), so while warpgroup A turns S_A(i) into P_A(i) the tensor core
+// works on tile B and vice versa: the two softmax warps of an SM sub-partition (one per Q tile)
+// are half a period apart instead of running the same phase at the same time.  S_t(i+1) is issued
+// after PV_t(i), so its completion barrier also covers O_t (lazy rescale without another wait).
+// Warps: w0 TMA, w1 MMA, w2-3 idle, w4-7 softmax A, w8-11 softmax B (quadrant = warp & 3).
+// TMEM: S_A [0,128) S_B [128,256); O_t at 256 + (ob * 2 + t) * DH (head_dim 64: two sets by item)
+// or 256 + t * 128 (head_dim 128).
+template <int DH>
+struct FwdPPCfg {
+  static constexpr int THREADS = 384;
+  static constexpr int TILE = 128 * DH * 2;
+  static constexpr int QB = DH == 64 ? 2 : 1;  // Q-pair buffers (by item)
+  static constexpr int KVS = DH == 64 ? 3 : 2;
+  static constexpr int NOB = DH == 64 ? 2 : 1;
+  static constexpr int Q = 0;  // [QB][2] tiles
+  static constexpr int K = Q + QB * 2 * TILE;
+  static constexpr int V = K + KVS * TILE;
+  static constexpr int BAR = V + KVS * TILE;
+  static constexpr int TOTAL = BAR + 512;
+  static_assert(TOTAL + 1024 <= 227 * 1024, "forward smem");
+  __device__ static constexpr uint32_t o_col(int ob, int t) { return 256 + (ob * 2 + t) * DH; }
+};
+
+struct PPItem {
+  int seq, q0, h, hk, s0, L, n[2], nk;
+};
+
+template <bool CAUSAL>
+__device__ __forceinline__ PPItem pp_item(int w, int H, int Hk, const int32_t* cu, const int2* tiles) {
+  PPItem it;
+  const int2 tq = tiles[w / H];
+  it.seq = tq.x;
+  it.q0 = tq.y;
+  it.h = w % H;
+  it.hk = it.h / (H / Hk);
+  it.s0 = cu[it.seq];
+  it.L = cu[it.seq + 1] - it.s0;
+  const int n_all = (it.L + BKV - 1) / BKV;
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const int q0t = it.q0 + t * BQ;
+    it.n[t] = q0t >= it.L ? 0 : (CAUSAL ? min(n_all, q0t / BKV + 1) : n_all);
+  }
+  it.nk = max(it.n[0], it.n[1]);
+  return it;
+}
+
+template <int DH, bool CAUSAL>
+__global__ void __launch_bounds__(FwdPPCfg<DH>::THREADS, 1)
+    attn_fwd_pp_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
+                       const __grid_constant__ CUtensorMap map_v, const int32_t* __restrict__ cu,
+                       const int2* __restrict__ tiles, const int* __restrict__ n_tiles,
+                       __nv_bfloat16* __restrict__ out, int ldo, float* __restrict__ lse, int T, int H, int Hk,
+                       float scale2) {
+  using C = FwdPPCfg<DH>;
+  constexpr int KVS = C::KVS, NOB = C::NOB, QB = C::QB, TB = C::TILE;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* sm = align_smem_1024(smem_raw);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::BAR);
+  uint64_t* q_full = bar;           // [QB]
+  uint64_t* q_empty = bar + 2;      // [QB]
+  uint64_t* k_full = bar + 4;       // [KVS]
+  uint64_t* k_empty = k_full + KVS;
+  uint64_t* v_full = k_empty + KVS;
+  uint64_t* v_empty = v_full + KVS;
+  uint64_t* s_full = v_empty + KVS;  // [2 tiles]
+  uint64_t* p_full = s_full + 2;     // [2 tiles]
+  uint64_t* o_full = p_full + 2;     // [2 tiles][2 sets]
+  uint64_t* o_empty = o_full + 4;    // [2 tiles][2 sets]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 4);
+
+  const int n_items = *n_tiles * H;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&map_q);
+    tma_prefetch(&map_k);
+    tma_prefetch(&map_v);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&q_full[b], 1);
+      mbar_init(&q_empty[b], 1);
+      mbar_init(&s_full[b], 1);
+      mbar_init(&p_full[b], 128);
+    }
+    for (int b = 0; b < 4; ++b) {
+      mbar_init(&o_full[b], 1);
+      mbar_init(&o_empty[b], 128);
+    }
+    for (int s = 0; s < KVS; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int g = 0, j = 0;
+      for (int w = snake_item(0); w < n_items; w = snake_item(++j)) {
+        const PPItem it = pp_item<CAUSAL>(w, H, Hk, cu, tiles);
+        const int qb = j % QB;
+        mbar_wait(&q_empty[qb], ((j / QB) & 1) ^ 1);
+        mbar_arrive_expect_tx(&q_full[qb], TB * (it.n[1] > 0 ? 2 : 1));
+        load_tile<DH>(sm + C::Q + qb * 2 * TB, &map_q, &q_full[qb], it.h * DH, it.s0 + it.q0);
+        if (it.n[1] > 0) load_tile<DH>(sm + C::Q + (qb * 2 + 1) * TB, &map_q, &q_full[qb], it.h * DH, it.s0 + it.q0 + BQ);
+        for (int i = 0; i < it.nk; ++i, ++g) {
+          const int st = g % KVS;
+          const uint32_t ph = (g / KVS) & 1;
+          mbar_wait(&k_empty[st], ph ^ 1);
+          mbar_arrive_expect_tx(&k_full[st], TB);
+          load_tile<DH>(sm + C::K + st * TB, &map_k, &k_full[st], it.hk * DH, it.s0 + i * BKV);
+          mbar_wait(&v_empty[st], ph ^ 1);
+          mbar_arrive_expect_tx(&v_full[st], TB);
+          load_tile<DH>(sm + C::V + st * TB, &map_v, &v_full[st], it.hk * DH, it.s0 + i * BKV);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc_s = idesc_bf16_f32(BQ, BKV, false, false);
+    constexpr uint32_t idesc_o = idesc_bf16_f32(BQ, DH, false, true);
+    int g = 0, j = 0;
+    int np[2] = {0, 0};   // PVs issued per tile (p_full parity)
+    int nw[2] = {0, 0};   // items with work per tile (O set, o_empty parity)
+    for (int w = snake_item(0); w < n_items; w = snake_item(++j)) {
+      const PPItem it = pp_item<CAUSAL>(w, H, Hk, cu, tiles);
+      const int qb = j % QB;
+      mbar_wait(&q_full[qb], (j / QB) & 1);
+      const uint32_t q_base = smem_u32(sm + C::Q + qb * 2 * TB);
+      const int n_s = it.n[0] + it.n[1];
+      int s_done = 0;
+      auto issue_s = [&](int t, int kst) {  // S_t = Q_t K^T (K tile in ring stage kst)
+        const uint32_t k_base = smem_u32(sm + C::K + kst * TB);
+        const uint32_t qt = q_base + t * TB;
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < DH / 16; ++kk)
+            umma_bf16(tmem + t * BKV, sdesc((qt >> 4) + (kk >> 2) * 1024 + (kk & 3) * 2, 16, 1024),
+                      sdesc((k_base >> 4) + (kk >> 2) * 1024 + (kk & 3) * 2, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+          umma_commit(&s_full[t]);
+          if (++s_done == n_s) umma_commit(&q_empty[qb]);  // last S of the item: Q pair free
+        } else {
+          ++s_done;
+        }
+        __syncwarp();
+      };
+      auto issue_pv = [&](int t, int i, int vst) {  // O_t += P_t V (V tile in ring stage vst)
+        const int ob = nw[t] % NOB;
+        if (i == 0) mbar_wait(&o_empty[t * 2 + ob], ((nw[t] / NOB) & 1) ^ 1);
+        mbar_wait(&p_full[t], np[t] & 1);
+        ++np[t];
+        tc_fence_after();
+        const uint32_t v_base = smem_u32(sm + C::V + vst * TB);
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < BKV / 16; ++kk)
+            umma_bf16_ts(tmem + C::o_col(ob, t), tmem + t * BKV + kk * 8,
+                         sdesc((v_base >> 4) + kk * 128, DH == 64 ? 8192 : 16384, 1024), idesc_o,
+                         (i > 0 || kk > 0) ? 1u : 0u);
+          if (i == it.n[t] - 1) umma_commit(&o_full[t * 2 + ob]);
+        }
+        __syncwarp();
+        if (i == it.n[t] - 1) ++nw[t];
+      };
+      // prologue: S_A(0), S_B(0)
+      {
+        const int st = g % KVS;
+        mbar_wait(&k_full[st], (g / KVS) & 1);
+        tc_fence_after();
+        for (int t = 0; t < 2; ++t)
+          if (it.n[t] > 0) issue_s(t, st);
+        if (elect_one()) umma_commit(&k_empty[st]);
+        __syncwarp();
+      }
+      for (int i = 0; i < it.nk; ++i) {
+        const int st = (g + i) % KVS, st1 = (g + i + 1) % KVS;
+        mbar_wait(&v_full[st], ((g + i) / KVS) & 1);
+        const bool more = i + 1 < it.nk;
+        if (more) mbar_wait(&k_full[st1], ((g + i + 1) / KVS) & 1);
+        for (int t = 0; t < 2; ++t) {
+          if (i < it.n[t]) issue_pv(t, i, st);
+          if (i + 1 < it.n[t]) {
+            tc_fence_after();
+            issue_s(t, st1);
+          }
+        }
+        if (elect_one()) {
+          umma_commit(&v_empty[st]);
+          if (more) umma_commit(&k_empty[st1]);
+        }
+        __syncwarp();
+      }
+      g += it.nk;
+    }
+  } else if (warp >= 4) {
+    const int t = (warp - 4) >> 2;  // Q tile of this warpgroup
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    const uint32_t s_col = tmem + lane_base + t * BKV;
+    int c = 0;                       // S tiles consumed (s_full parity)
+    int nw = 0;                      // items with work for this tile
+    auto epilogue = [&](const PPItem& it, int wi, float m, float l) {
+      const int ob = wi % NOB;
+      mbar_wait(&o_full[t * 2 + ob], (wi / NOB) & 1);
+      tc_fence_after();
+      const int qpos = it.q0 + t * BQ + r;
+      const float rl = __frcp_rn(l);
+#pragma unroll
+      for (int sub = 0; sub < DH / 32; ++sub) {
+        uint32_t ra[32];
+        tmem_ld_32x32b_x32(tmem + lane_base + C::o_col(ob, t) + sub * 32, ra);
+        tmem_ld_wait();
+        if (sub == DH / 32 - 1) {
+          tc_fence_before();
+          mbar_arrive(&o_empty[t * 2 + ob]);
+        }
+        if (qpos < it.L) {
+          uint32_t o[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            o[e] = pack_bf16(__uint_as_float(ra[2 * e]) * rl, __uint_as_float(ra[2 * e + 1]) * rl);
+          uint4* dst = reinterpret_cast<uint4*>(out + (size_t)(it.s0 + qpos) * ldo + it.h * DH + sub * 32);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) dst[u] = make_uint4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);
+        }
+      }
+      if (qpos < it.L) lse[(size_t)it.h * T + it.s0 + qpos] = (m + log2f(l)) * LN2_F;
+    };
+    bool pend = false;
+    PPItem pit{};
+    int pw = 0;
+    float pm = 0.f, pl = 0.f;
+    int j = 0;
+    for (int w = snake_item(0); w < n_items; w = snake_item(++j)) {
+      const PPItem it = pp_item<CAUSAL>(w, H, Hk, cu, tiles);
+      const int n_t = it.n[t];
+      if (n_t == 0) {  // no rows of this tile in the sequence: nothing to compute
+        if (pend) {
+          epilogue(pit, pw, pm, pl);
+          pend = false;
+        }
+        continue;
+      }
+      const int ob = nw % NOB;
+      const int q0t = it.q0 + t * BQ;
+      const int qpos = q0t + r;
+      float m = -INFINITY, l = 0.f;
+      for (int i = 0; i < n_t; ++i, ++c) {
+        mbar_wait(&s_full[t], c & 1);
+        tc_fence_after();
+        const int kv0 = i * BKV;
+        const bool need_mask = (CAUSAL && kv0 + BKV - 1 > q0t) || (kv0 + BKV > it.L);
+        const int lim = CAUSAL ? min(qpos - kv0 + 1, it.L - kv0) : it.L - kv0;
+        // pass 1: row max over both 64-column halves
+        float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint32_t raw[2][32];
+          tmem_ld_32x32b_x32(s_col + h * 64, raw[0]);
+          tmem_ld_32x32b_x32(s_col + h * 64 + 32, raw[1]);
+          tmem_ld_wait();
+          if (need_mask) {
+#pragma unroll
+            for (int e = 0; e < 64; ++e)
+              mx4[e & 3] = fmaxf(mx4[e & 3], h * 64 + e < lim ? __uint_as_float(raw[e >> 5][e & 31]) : -INFINITY);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 64; ++e) mx4[e & 3] = fmaxf(mx4[e & 3], __uint_as_float(raw[e >> 5][e & 31]));
+          }
+        }
+        const float m_new = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * scale2;
+        bool rescale = false;
+        float alpha = 1.f;
+        if (m_new > m + 8.0f) {
+          alpha = ex2(m - m_new);
+          m = m_new;
+          rescale = i > 0;
+        }
+        // O_t is final for the previous tiles: S_t(i) was issued after PV_t(i-1)
+        if (__any_sync(kFull, rescale)) {
+          if (!rescale) alpha = 1.f;
+#pragma unroll
+          for (int cc = 0; cc < DH / 32; ++cc) {
+            uint32_t rr[32];
+            tmem_ld_32x32b_x32(tmem + lane_base + C::o_col(ob, t) + cc * 32, rr);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) rr[e] = __float_as_uint(__uint_as_float(rr[e]) * alpha);
+            tmem_st_32x32b_x32(tmem + lane_base + C::o_col(ob, t) + cc * 32, rr);
+          }
+        }
+        const float neg_m = m == -INFINITY ? 0.f : -m;
+        const float2 sc2 = make_float2(scale2, scale2), nm2 = make_float2(neg_m, neg_m);
+        float2 sum2[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+        // pass 2: exponentials of each half, packed to bf16 P over the first 64 columns of S_t
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          float s[64];
+          {
+            uint32_t raw[2][32];
+            tmem_ld_32x32b_x32(s_col + h * 64, raw[0]);
+            tmem_ld_32x32b_x32(s_col + h * 64 + 32, raw[1]);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 64; ++e) {
+              const float x = __uint_as_float(raw[e >> 5][e & 31]);
+              s[e] = (!need_mask || h * 64 + e < lim) ? x : -INFINITY;
+            }
+          }
+#pragma unroll
+          for (int e = 0; e < 64; e += 2) {
+            const float2 x = __ffma2_rn(make_float2(s[e], s[e + 1]), sc2, nm2);
+            if ((FWD_EMU_BITS >> ((e >> 1) & 7)) & 1) {
+              const float2 y = ex2_fma2<3>(x);
+              s[e] = y.x;
+              s[e + 1] = y.y;
+            } else {
+              s[e] = ex2(x.x);
+              s[e + 1] = ex2(x.y);
+            }
+            sum2[(e >> 1) & 3] = __fadd2_rn(sum2[(e >> 1) & 3], make_float2(s[e], s[e + 1]));
+          }
+          uint32_t pk[32];
+#pragma unroll
+          for (int e = 0; e < 32; ++e) pk[e] = pack_bf16(s[2 * e], s[2 * e + 1]);
+          tmem_st_32x32b_x32(s_col + h * 32, pk);
+        }
+        const float2 t01 = __fadd2_rn(sum2[0], sum2[1]), t23 = __fadd2_rn(sum2[2], sum2[3]);
+        const float2 tt = __fadd2_rn(t01, t23);
+        l = l * alpha + (tt.x + tt.y);
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&p_full[t]);
+        if (i == 0 && pend) {
+          epilogue(pit, pw, pm, pl);
+          pend = false;
+        }
+      }
+      pend = true;
+      pit = it;
+      pw = nw;
+      pm = m;
+      pl = l;
+      ++nw;
+    }
+    if (pend) epilogue(pit, pw, pm, pl);
   }
   tc_fence_before();
   __syncthreads();
@@ -1290,8 +2046,9 @@ MAESTRO_API int64_t maestro_attn_workspace(int32_t T, int32_t nseq) {
 
 // q [T, H, 64] (row pitch ldq elements), k/v [T, Hk, 64] (pitch ldk/ldv), cu [nseq+1];
 // out [T, H, 64] (pitch ldo), lse [H, T] fp32 (natural log-sum-exp of the scaled scores).
-// Plan = [query-tile list | count] [KV-tile list | count], each maestro_attn_workspace bytes.
-MAESTRO_API int64_t maestro_attn_plan_size(int32_t T, int32_t nseq) { return 2 * maestro_attn_workspace(T, nseq); }
+// Plan = [query-tile list | count] [KV-tile list | count] [256-row query-tile list | count], each
+// maestro_attn_workspace bytes (the last one for the ping-pong forward).
+MAESTRO_API int64_t maestro_attn_plan_size(int32_t T, int32_t nseq) { return 3 * maestro_attn_workspace(T, nseq); }
 
 MAESTRO_API int maestro_attn_plan(const int32_t* cu, int32_t nseq, int32_t T, void* plan, void* stream) {
   if (T <= 0) return 0;
@@ -1301,6 +2058,8 @@ MAESTRO_API int maestro_attn_plan(const int32_t* cu, int32_t nseq, int32_t T, vo
   int2* bw = reinterpret_cast<int2*>(reinterpret_cast<unsigned char*>(plan) + maestro_attn_workspace(T, nseq));
   attn_tiles_kernel<<<1, 1024, 0, st>>>(cu, nseq, fw, reinterpret_cast<int*>(fw + max_tiles));
   attn_kv_tiles_kernel<<<1, 1024, 0, st>>>(cu, nseq, bw, reinterpret_cast<int*>(bw + max_tiles));
+  int2* pw = reinterpret_cast<int2*>(reinterpret_cast<unsigned char*>(plan) + 2 * maestro_attn_workspace(T, nseq));
+  attn_tiles_kernel<2 * BQ><<<1, 1024, 0, st>>>(cu, nseq, pw, reinterpret_cast<int*>(pw + max_tiles));
   return launch_status();
 }
 
@@ -1314,6 +2073,42 @@ MAESTRO_API int maestro_attn_fwd(const void* q, const void* k, const void* v, co
   const int max_tiles = (T + BQ - 1) / BQ + nseq;
   int2* tiles = reinterpret_cast<int2*>(plan != nullptr ? const_cast<void*>(plan) : workspace);
   int* count = reinterpret_cast<int*>(tiles + max_tiles);
+  // forward variant: "pp" = ping-pong Q-tile pairs, "dec" = decoupled column groups, "base"
+  static const int variant = [] {
+    const char* e = getenv("MAESTRO_ATTN_FWD");
+    if (!e) return ATTN_FWD_VARIANT;
+    return e[0] == 'p' ? 2 : (e[0] == 'd' ? 1 : 0);
+  }();
+  if (variant == 2) {  // 256-row items: the plan's third list, or built into the workspace
+    int2* t2 = plan != nullptr ? reinterpret_cast<int2*>(reinterpret_cast<unsigned char*>(const_cast<void*>(plan)) +
+                                                         2 * maestro_attn_workspace(T, nseq))
+                               : reinterpret_cast<int2*>(workspace);
+    int* c2 = reinterpret_cast<int*>(t2 + max_tiles);
+    if (plan == nullptr) attn_tiles_kernel<2 * BQ><<<1, 1024, 0, st>>>(cu, nseq, t2, c2);
+    CUtensorMap mq, mk, mv;
+    bool ok = make_map_2d(&mq, q, (uint64_t)H * head_dim, T, ldq, 64, 128);
+    ok = ok && make_map_2d(&mk, k, (uint64_t)Hk * head_dim, T, ldk, 64, 128);
+    ok = ok && make_map_2d(&mv, v, (uint64_t)Hk * head_dim, T, ldv, 64, 128);
+    if (!ok) return (int)cudaErrorInvalidValue;
+    const int items = ((T + 2 * BQ - 1) / (2 * BQ) + nseq) * H;
+    dim3 grid(items < num_sms() ? items : num_sms());
+    const float scale2 = softmax_scale * LOG2E_F;
+#define MB_ATTN_PP(D, CZ)                                                                                   \
+  {                                                                                                         \
+    const int smem = FwdPPCfg<D>::TOTAL + 1024;                                                             \
+    if (ensure_smem<attn_fwd_pp_kernel<D, CZ>>(smem)) return launch_status();                               \
+    attn_fwd_pp_kernel<D, CZ><<<grid, FwdPPCfg<D>::THREADS, smem, st>>>(mq, mk, mv, cu, t2, c2,              \
+                                                                         (__nv_bfloat16*)out, ldo, lse, T, H, \
+                                                                         Hk, scale2);                        \
+  }
+    if (head_dim == 64) {
+      if (causal) MB_ATTN_PP(64, true) else MB_ATTN_PP(64, false)
+    } else {
+      if (causal) MB_ATTN_PP(128, true) else MB_ATTN_PP(128, false)
+    }
+#undef MB_ATTN_PP
+    return launch_status();
+  }
   if (plan == nullptr) attn_tiles_kernel<<<1, 1024, 0, st>>>(cu, nseq, tiles, count);
   CUtensorMap mq, mk, mv;
   bool ok = make_map_2d(&mq, q, (uint64_t)H * head_dim, T, ldq, 64, 128);
@@ -1336,12 +2131,33 @@ MAESTRO_API int maestro_attn_fwd(const void* q, const void* k, const void* v, co
     const char* e = getenv("MAESTRO_ATTN_STAGGER_NS");
     return e ? atoi(e) : 0;
   }();
+  static const int dec_stagger = [] {  // group 1's late start in the decoupled forward
+    const char* e = getenv("MAESTRO_ATTN_DEC_STAGGER_NS");
+    return e ? atoi(e) : 400;
+  }();
   // column groups per tile (head_dim 64): 4 (16 softmax warps) or 2 (8); MAESTRO_ATTN_CG overrides
   static const int cg_env = [] {
     const char* e = getenv("MAESTRO_ATTN_CG");
     return e ? atoi(e) : 0;
   }();
   const int cg = cg_env == 2 || cg_env == 4 ? cg_env : ATTN_FWD_CG64;
+  if (variant == 1) {
+#define MB_ATTN_DEC(D, CZ)                                                                                   \
+  {                                                                                                          \
+    const int smem = FwdDecCfg<D>::TOTAL + 1024;                                                             \
+    if (ensure_smem<attn_fwd_dec_kernel<D, CZ>>(smem)) return launch_status();                               \
+    attn_fwd_dec_kernel<D, CZ><<<grid, FwdDecCfg<D>::THREADS, smem, st>>>(mq, mk, mv, cu, tiles, count,       \
+                                                                           (__nv_bfloat16*)out, ldo, lse, T, H, \
+                                                                           Hk, scale2, dec_stagger);         \
+  }
+    if (head_dim == 64) {
+      if (causal) MB_ATTN_DEC(64, true) else MB_ATTN_DEC(64, false)
+    } else {
+      if (causal) MB_ATTN_DEC(128, true) else MB_ATTN_DEC(128, false)
+    }
+#undef MB_ATTN_DEC
+    return launch_status();
+  }
   if (head_dim == 64 && cg == 4) {
     if (causal) MB_ATTN_FWD(64, 4, true) else MB_ATTN_FWD(64, 4, false)
   } else if (head_dim == 64) {
