@@ -129,7 +129,7 @@ __device__ __forceinline__ void warp_arrive(const Bars& B, uint64_t* p) {
 #define ATTN_FWD_CG64 2  // default column groups of the head_dim-64 forward (see FwdCfg)
 #endif
 #ifndef ATTN_FWD_VARIANT
-#define ATTN_FWD_VARIANT 0  // default forward: 0 shared tile, 1 decoupled groups, 2 ping-pong (MAESTRO_ATTN_FWD=base|dec|pp)
+#define ATTN_FWD_VARIANT -1  // forward: -1 by shape, 0 shared tile, 1 decoupled groups, 2 ping-pong (MAESTRO_ATTN_FWD=base|dec|pp)
 #endif
 #ifndef FWD_EMU_BITS
 #define FWD_EMU_BITS 0x92  // pair p of a row's 32 goes to the FMA pipe if bit (p & 7) is set (3/8)
@@ -2074,11 +2074,16 @@ MAESTRO_API int maestro_attn_fwd(const void* q, const void* k, const void* v, co
   int2* tiles = reinterpret_cast<int2*>(plan != nullptr ? const_cast<void*>(plan) : workspace);
   int* count = reinterpret_cast<int*>(tiles + max_tiles);
   // forward variant: "pp" = ping-pong Q-tile pairs, "dec" = decoupled column groups, "base"
-  static const int variant = [] {
+  // Default by shape (scripts/attn_quick.py A/B on one B200, r02_attn_fwd_variants.jsonl): head_dim 64
+  // -> decoupled groups (+3 % over the shared tile at the KD / cfg 5 student shapes); head_dim 128
+  // bidirectional -> ping-pong (+17 % at the cfg 3 ViT shape); head_dim 128 causal -> shared tile
+  // (ping-pong +2 % at 8k, -5 % at 4k).
+  static const int env_variant = [] {
     const char* e = getenv("MAESTRO_ATTN_FWD");
     if (!e) return ATTN_FWD_VARIANT;
-    return e[0] == 'p' ? 2 : (e[0] == 'd' ? 1 : 0);
+    return e[0] == 'p' ? 2 : (e[0] == 'd' ? 1 : (e[0] == 'b' ? 0 : ATTN_FWD_VARIANT));
   }();
+  const int variant = env_variant >= 0 ? env_variant : (head_dim == 64 ? 1 : (causal ? 0 : 2));
   if (variant == 2) {  // 256-row items: the plan's third list, or built into the workspace
     int2* t2 = plan != nullptr ? reinterpret_cast<int2*>(reinterpret_cast<unsigned char*>(const_cast<void*>(plan)) +
                                                          2 * maestro_attn_workspace(T, nseq))
