@@ -651,9 +651,13 @@ struct FwdDecCfg {
   static constexpr int Q = 0;
   static constexpr int K = Q + 2 * TILE;
   static constexpr int V = K + KVS * TILE;
-  static constexpr int XMAX = V + KVS * TILE;  // [2 items][2 groups][128]
-  static constexpr int XSUM = XMAX + 2 * 2 * 128 * 4;
-  static constexpr int CNT = XSUM + 2 * 2 * 128 * 4;  // [2 items][4 quadrants] arrivals
+  // epilogue exchange slots by item % 4: a group can run up to two items ahead of the other (a
+  // one-tile item's S is issued before the PV that waits for the item-before-last's epilogue),
+  // so three items can have an epilogue in flight
+  static constexpr int XS = 4;
+  static constexpr int XMAX = V + KVS * TILE;  // [XS items][2 groups][128]
+  static constexpr int XSUM = XMAX + XS * 2 * 128 * 4;
+  static constexpr int CNT = XSUM + XS * 2 * 128 * 4;  // [XS items][4 quadrants] arrivals
   static constexpr int BAR = CNT + 64;
   static constexpr int TOTAL = BAR + 512;
   static_assert(TOTAL + 1024 <= 227 * 1024, "forward smem");
@@ -713,7 +717,7 @@ __global__ void __launch_bounds__(FwdDecCfg<DH>::THREADS, 1)
         mbar_init(&o_full(g)[b], 1);
         mbar_init(&o_empty(g)[b], 128);
       }
-    for (int k = 0; k < 8; ++k) cnt[k] = 0;
+    for (int k = 0; k < 4 * C::XS; ++k) cnt[k] = 0;
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -828,7 +832,7 @@ __global__ void __launch_bounds__(FwdDecCfg<DH>::THREADS, 1)
     uint64_t *sf = s_full(grp), *se = s_empty(grp), *pf = p_full(grp), *pe = p_empty(grp);
     // Item jj is finished by whichever group's warp of this quadrant arrives second.
     auto epilogue = [&](const FwdItem& it, int jj, float m, float l) {
-      const int ob = jj % NOB, par = jj & 1;
+      const int ob = jj % NOB, par = jj % C::XS;
       xmax[(par * 2 + grp) * 128 + r] = m;
       xsum[(par * 2 + grp) * 128 + r] = l;
       __threadfence_block();
