@@ -424,56 +424,69 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(KDS_THREADS, KDS_CTA
 
 // Next-token cross entropy over the full vocabulary with ignore index (label < 0):
 // loss[row] = lse(s) - s[label];  ds = grad_scale * (softmax(s) - onehot(label)).  Same
-// single-pass online max/sum-exp + L2-resident second pass as the KL kernel.
-__global__ void __launch_bounds__(KD_THREADS) ce_loss_kernel(const __nv_bfloat16* sl, const int32_t* __restrict__ labels,
+// single-pass online max/sum-exp + L2-resident second pass as the streaming KL kernel: four
+// vectors in flight per thread, the max over the raw logits scaled once, MUFU exp2.
+template <int THREADS, int UNROLL>
+__global__ void __launch_bounds__(THREADS, 4) ce_loss_kernel(const __nv_bfloat16* sl, const int32_t* __restrict__ labels,
                                                              __nv_bfloat16* ds, float* __restrict__ loss, int T, int V,
                                                              int lds, int ldd, float grad_scale) {
-  __shared__ float red_m[KD_THREADS / 32], red_s[KD_THREADS / 32];
+  __shared__ float red_m[THREADS / 32], red_s[THREADS / 32];
   __shared__ float fin_m, fin_s;
   const int nvec = V / 8;
+  auto combine = [](float& m, float& ss, float om, float os) {
+    const float mx = fmaxf(m, om);
+    ss = (m == -INFINITY ? 0.f : ss * ex2a(m - mx)) + (om == -INFINITY ? 0.f : os * ex2a(om - mx));
+    m = mx;
+  };
   for (int row = blockIdx.x; row < T; row += gridDim.x) {
     const int lab = labels[row];
     const uint4* s4 = reinterpret_cast<const uint4*>(sl + (size_t)row * lds);
     uint4* d4 = reinterpret_cast<uint4*>(ds + (size_t)row * ldd);
     if (lab < 0) {  // ignored position: zero loss and gradient
-      for (int v = threadIdx.x; v < nvec; v += KD_THREADS) d4[v] = make_uint4(0, 0, 0, 0);
+      for (int v = threadIdx.x; v < nvec; v += THREADS) d4[v] = make_uint4(0, 0, 0, 0);
       if (threadIdx.x == 0) loss[row] = 0.f;
       continue;
     }
     float m = -INFINITY, ss = 0.f;
-    for (int v = threadIdx.x; v < nvec; v += KD_THREADS) {
-      float f[8];
-      unpack8(s4[v], f);
-      float mx = m;
+    for (int v0 = threadIdx.x; v0 < nvec; v0 += UNROLL * THREADS) {
+      uint4 rv[UNROLL];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) mx = fmaxf(mx, f[j] * LOG2E);
-      ss *= exp2f(m - mx);
+      for (int u = 0; u < UNROLL; ++u)
+        if (v0 + u * THREADS < nvec) rv[u] = s4[v0 + u * THREADS];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) ss += exp2f(f[j] * LOG2E - mx);
-      m = mx;
+      for (int u = 0; u < UNROLL; ++u) {
+        if (v0 + u * THREADS >= nvec) break;
+        float f[8];
+        unpack8(rv[u], f);
+        float r = f[0];
+#pragma unroll
+        for (int j = 1; j < 8; ++j) r = fmaxf(r, f[j]);
+        const float mx = fmaxf(m, r * LOG2E);
+        if (mx > m) {
+          ss *= m == -INFINITY ? 0.f : ex2a(m - mx);
+          m = mx;
+        }
+        float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int j = 0; j < 8; j += 2) {
+          const float2 x = __ffma2_rn(make_float2(f[j], f[j + 1]), make_float2(LOG2E, LOG2E), make_float2(-m, -m));
+          acc = __fadd2_rn(acc, make_float2(ex2a(x.x), ex2a(x.y)));
+        }
+        ss += acc.x + acc.y;
+      }
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const float om = __shfl_xor_sync(kFull, m, o), os = __shfl_xor_sync(kFull, ss, o);
-      const float mx = fmaxf(m, om);
-      ss = (m == -INFINITY ? 0.f : ss * exp2f(m - mx)) + (om == -INFINITY ? 0.f : os * exp2f(om - mx));
-      m = mx;
-    }
+    for (int o = 16; o > 0; o >>= 1) combine(m, ss, __shfl_xor_sync(kFull, m, o), __shfl_xor_sync(kFull, ss, o));
     if ((threadIdx.x & 31) == 0) {
       red_m[threadIdx.x >> 5] = m;
       red_s[threadIdx.x >> 5] = ss;
     }
     __syncthreads();
     if (threadIdx.x < 32) {
-      m = threadIdx.x < KD_THREADS / 32 ? red_m[threadIdx.x] : -INFINITY;
-      ss = threadIdx.x < KD_THREADS / 32 ? red_s[threadIdx.x] : 0.f;
+      m = threadIdx.x < THREADS / 32 ? red_m[threadIdx.x] : -INFINITY;
+      ss = threadIdx.x < THREADS / 32 ? red_s[threadIdx.x] : 0.f;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const float om = __shfl_xor_sync(kFull, m, o), os = __shfl_xor_sync(kFull, ss, o);
-        const float mx = fmaxf(m, om);
-        ss = (m == -INFINITY ? 0.f : ss * exp2f(m - mx)) + (om == -INFINITY ? 0.f : os * exp2f(om - mx));
-        m = mx;
-      }
+      for (int o = 16; o > 0; o >>= 1) combine(m, ss, __shfl_xor_sync(kFull, m, o), __shfl_xor_sync(kFull, ss, o));
       if (threadIdx.x == 0) {
         fin_m = m;
         fin_s = ss;
@@ -482,18 +495,19 @@ __global__ void __launch_bounds__(KD_THREADS) ce_loss_kernel(const __nv_bfloat16
       }
     }
     __syncthreads();
-    const float fm = fin_m, inv = 1.f / fin_s;
-    for (int v = threadIdx.x; v < nvec; v += KD_THREADS) {
+    const float fm = fin_m, g = grad_scale / fin_s;
+    for (int v = threadIdx.x; v < nvec; v += THREADS) {
       float f[8];
       unpack8(s4[v], f);
       uint4 o;
-      __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&o);
+      uint32_t* oh = reinterpret_cast<uint32_t*>(&o);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        float g0 = exp2f(f[2 * j] * LOG2E - fm) * inv, g1 = exp2f(f[2 * j + 1] * LOG2E - fm) * inv;
-        if (8 * v + 2 * j == lab) g0 -= 1.f;
-        if (8 * v + 2 * j + 1 == lab) g1 -= 1.f;
-        oh[j] = __floats2bfloat162_rn(g0 * grad_scale, g1 * grad_scale);
+        const float2 x = __ffma2_rn(make_float2(f[2 * j], f[2 * j + 1]), make_float2(LOG2E, LOG2E), make_float2(-fm, -fm));
+        float g0 = ex2a(x.x) * g, g1 = ex2a(x.y) * g;
+        if (8 * v + 2 * j == lab) g0 -= grad_scale;
+        if (8 * v + 2 * j + 1 == lab) g1 -= grad_scale;
+        oh[j] = sm100::pack_bf16(g0, g1);
       }
       d4[v] = o;
     }
@@ -613,8 +627,8 @@ MAESTRO_API int maestro_ce_loss_fwd_bwd(const void* d_s, const int32_t* d_labels
                                         void* stream) {
   if (T <= 0) return 0;
   if (V % 8 || lds % 8 || ldd % 8) return (int)cudaErrorInvalidValue;
-  const int grid = T < 148 * 4 ? T : 148 * 4;
-  ce_loss_kernel<<<grid, KD_THREADS, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)d_s, d_labels,
+  const int grid = T < num_sms() * 4 * 4 ? T : num_sms() * 4 * 4;
+  ce_loss_kernel<256, 4><<<grid, 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)d_s, d_labels,
                                                                  (__nv_bfloat16*)d_ds, d_loss, T, V, lds, ldd,
                                                                  grad_scale);
   return launch_status();

@@ -137,6 +137,27 @@ def test_kd_loss_fused(T, V):
     assert torch.equal(loss2, loss)
 
 
+@pytest.mark.parametrize("T,V", [(64, 32000), (37, 152064), (9, 64), (130, 32768)])
+def test_ce_loss_fused(T, V):
+    """Next-token CE with ignore index (label < 0) vs torch fp32 cross_entropy: loss per row and
+    ds = grad_scale * (softmax - onehot), in place over the logits."""
+    from paper_2605_10501_b200 import kernels as K
+
+    torch.manual_seed(V + T)
+    s = (3 * torch.randn(T, V, device="cuda")).bfloat16()
+    lab = torch.randint(0, V, (T,), device="cuda", dtype=torch.int32)
+    lab[::7] = -1
+    ss = s.float().clone().requires_grad_(True)
+    ref = torch.nn.functional.cross_entropy(ss, lab.long().clamp_min(0), reduction="none") * (lab >= 0)
+    (ref.sum() * 0.5).backward()
+    loss = torch.empty(T, device="cuda")
+    ds = s.clone()
+    K.ce_loss(ds, lab, ds, loss, 0.5)
+    assert rel(loss, ref) < 1e-4
+    assert rel(ds, ss.grad) < 1e-2
+    assert torch.all(ds[lab < 0] == 0) and torch.all(loss[lab < 0] == 0)
+
+
 def _tiny_model(seed=0, shape_name="test_tiny"):
     from paper_2605_10501_b200.transformer import SHAPES, FlatParams, Transformer
 
