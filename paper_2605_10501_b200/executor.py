@@ -367,10 +367,10 @@ class KDExecutor:
         else:
             self._run_student_remote(plan, host, packed, ready, clock, loss_acc, global_tokens)
         # per-section gradient sync (student DP group) + optimizer, on the student stream
+        ar = None  # (all-reduce start, end) events; none on a teacher-only rank
         if self.student is not None:
             with torch.cuda.stream(self.s_stream):
                 dist = _dist()
-                ar = None
                 if dist is not None and self.dp_s > 1:
                     ar = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                     ar[0].record(self.s_stream)

@@ -9,3 +9,4 @@ timeout 1200 bash -c "$(declare -f tr); N=$N; tr 29513 --workload kd8b --steps 3
 timeout 900 bash -c "$(declare -f tr); N=$N; tr 29514 --workload section --graph vlm7b --steps 3 --warmup 2" > gpurun_out/sc${N}_vlm7b.log 2>&1; echo "== vlm7b N=$N $?"; grep '^{' gpurun_out/sc${N}_vlm7b.log | cut -c1-300
 timeout 900 bash -c "$(declare -f tr); N=$N; tr 29515 --workload section --graph omni --steps 3 --warmup 2" > gpurun_out/sc${N}_omni.log 2>&1; echo "== omni N=$N $?"; grep '^{' gpurun_out/sc${N}_omni.log | cut -c1-300
 timeout 600 bash -c "$(declare -f tr); N=$N; tr 29516 --workload vlm --steps 20 --warmup 5" > gpurun_out/sc${N}_vlm.log 2>&1; echo "== vlm N=$N $?"; grep '^{' gpurun_out/sc${N}_vlm.log | cut -c1-300
+timeout 600 bash -c "$(declare -f tr); N=$N; tr 29517 --workload vlm --layout disjoint --steps 20 --warmup 5" > gpurun_out/sc${N}_vlm_dis.log 2>&1; echo "== vlm disjoint N=$N $?"; grep '^{' gpurun_out/sc${N}_vlm_dis.log | cut -c1-300
