@@ -18,7 +18,7 @@ import json
 import sys
 from pathlib import Path
 
-TENSOR = ("gemm", "attn_fwd_kernel", "attn_bwd_kernel")
+TENSOR = ("gemm", "attn_fwd_kernel", "attn_fwd_dec_kernel", "attn_fwd_pp_kernel", "attn_bwd_kernel")
 LATENCY = ("sample_times", "partition", "wavefront", "rank_metrics", "fanout_merge", "varlen_pack", "pack_tokens", "fp64_",
            "tiles_kernel", "positions")
 UNIT = {"nsecond": 1e-9, "ns": 1e-9, "usecond": 1e-6, "us": 1e-6, "msecond": 1e-3, "ms": 1e-3, "second": 1.0,
