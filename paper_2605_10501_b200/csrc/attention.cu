@@ -1405,6 +1405,10 @@ __global__ void __launch_bounds__(FwdPPCfg<DH>::THREADS, 1)
 //               dP^T [64,128), dV [128,256), dK [256,384), dQ^T [384,448) (M = dh, N = q: its
 //               A operand is K read as an MN-major view, B = dS^T), P^T [448,480); K/V single-
 //               buffered (smem), so the next item's K/V load waits for the item's last MMAs.
+// Backward barrier waits sleep on the barrier (suspend hint) instead of polling: +5-8 % at
+// head_dim 128, neutral at 64 (r02_attn_suspend_ab.jsonl); the forward keeps polling (-1 %).
+__device__ __forceinline__ void bwd_wait(uint64_t* bar, uint32_t parity) { mbar_wait_sleep<20000>(bar, parity); }
+
 constexpr int BWD_THREADS = 448;  // w0 TMA, w1 MMA, w2-9 softmax (2 per lane quadrant), w10-13 dQ drain
 
 template <int DH>
@@ -1552,7 +1556,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         const BwdItem itm = itm_n;
         if (snake_item(j + 1) < n_items) itm_n = bwd_item<BQB, CAUSAL>(snake_item(j + 1), Hk, G, cu, tiles);  // prefetch
         const int kb = j % KVB;
-        mbar_wait(&kv_empty[kb], ((j / KVB) & 1) ^ 1);
+        bwd_wait(&kv_empty[kb], ((j / KVB) & 1) ^ 1);
         mbar_arrive_expect_tx(&kv_full[kb], 2 * KVT);
         unsigned char* kvd = sm + C::KV + kb * 2 * KVT;
 #pragma unroll
@@ -1564,7 +1568,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
           const int g = it / itm.n_q, qt = itm.qt_first + it % itm.n_q;
           const int h = itm.hk * G + g;
           const int st = gi % QDS;
-          mbar_wait(&qd_empty[st], ((gi / QDS) & 1) ^ 1);
+          bwd_wait(&qd_empty[st], ((gi / QDS) & 1) ^ 1);
           mbar_arrive_expect_tx(&qd_full[st], 2 * QT);
           unsigned char* dst = sm + C::QD + st * 2 * QT;
 #pragma unroll
@@ -1591,9 +1595,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       };
       // S^T(gi) = K Q^T and dP^T(gi) = V dO^T of the cursor's iteration
       auto issue_s = [&](const BwdCursor<BQB, CAUSAL>& c, int gi) {
-        mbar_wait(&qd_full[gi % QDS], (gi / QDS) & 1);
-        if (c.it == 0) mbar_wait(&kv_full[c.j % KVB], (c.j / KVB) & 1);
-        if (gi >= 1) mbar_wait(s_empty, (gi - 1) & 1);  // S^T(gi-1) is in the softmax registers
+        bwd_wait(&qd_full[gi % QDS], (gi / QDS) & 1);
+        if (c.it == 0) bwd_wait(&kv_full[c.j % KVB], (c.j / KVB) & 1);
+        if (gi >= 1) bwd_wait(s_empty, (gi - 1) & 1);  // S^T(gi-1) is in the softmax registers
         tc_fence_after();
         const uint32_t kb = kv_base(c.j), qb = qd_base(gi);
         if (elect_one()) {
@@ -1631,8 +1635,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         // (head_dim 128: a new item's S also waits for its K/V, i.e. for the previous item's last MMAs)
         if (nxt.valid && (KVB == 2 || nxt.it > 0)) issue_s(nxt, gi + 1);
         // dV += P^T dO   (B = dO, MN-major: N = dh over DH/64 atoms Q_CHUNK apart, K = q rows)
-        mbar_wait(p_ready, gi & 1);
-        if (cur.it == 0) mbar_wait(dkv_empty, (cur.j & 1) ^ 1);  // previous item's epilogue read dK/dV
+        bwd_wait(p_ready, gi & 1);
+        if (cur.it == 0) bwd_wait(dkv_empty, (cur.j & 1) ^ 1);  // previous item's epilogue read dK/dV
         tc_fence_after();
         if (elect_one()) {
 #pragma unroll
@@ -1643,8 +1647,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         }
         __syncwarp();
         // dK += dS^T Q (A = dS^T from TMEM) ; dQ from the dS^T smem operand
-        mbar_wait(ds_ready, gi & 1);
-        mbar_wait(dq_empty, (gi & 1) ^ 1);
+        bwd_wait(ds_ready, gi & 1);
+        bwd_wait(dq_empty, (gi & 1) ^ 1);
         tc_fence_after();
         if (elect_one()) {
 #pragma unroll
@@ -1694,7 +1698,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       for (int it = 0; it < itm.n_it; ++it, ++gi) {
         const int g = it / itm.n_q, qt = itm.qt_first + it % itm.n_q;
         const int h = itm.hk * G + g;
-        mbar_wait(dq_full, gi & 1);
+        bwd_wait(dq_full, gi & 1);
         tc_fence_after();
         uint32_t qa[32], qb[32];
         tmem_ld_32x32b_x32(tmem + lane_base + T_DQ, qa);
@@ -1786,7 +1790,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         const bool need_mask =
             (CAUSAL && q0 < itm.kv0 + BKV - 1) || (q0 + BQB > itm.L) || (itm.kv0 + BKV > itm.L);
         // ---- P1: S^T -> P^T
-        mbar_wait(s_full, gi & 1);
+        bwd_wait(s_full, gi & 1);
         tc_fence_after();
         uint32_t sr2[QH / 32][32];
 #pragma unroll
@@ -1794,7 +1798,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         tmem_ld_wait();
         tc_fence_before();
         warp_arrive(s_empty);
-        if (gi >= 1) mbar_wait(p_free, (gi - 1) & 1);  // dV(gi-1) has read P^T
+        if (gi >= 1) bwd_wait(p_free, (gi - 1) & 1);  // dV(gi-1) has read P^T
         uint32_t pk[QH / 2];  // this row's P^T as bf16 pairs: the dV operand, and P for phase 2
         // Two instantiations so that interior tiles carry no per-element mask code (if-converted
         // compares and selects otherwise cost more issue slots than the exponentials).
@@ -1849,9 +1853,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         tc_fence_before();
         warp_arrive(p_ready);
         // ---- P2: dP^T -> dS^T
-        mbar_wait(dp_full, gi & 1);
+        bwd_wait(dp_full, gi & 1);
         tc_fence_after();
-        if (gi >= 1) mbar_wait(ds_free, (gi - 1) & 1);  // dQ(gi-1) has read the dS^T smem operand
+        if (gi >= 1) bwd_wait(ds_free, (gi - 1) & 1);  // dQ(gi-1) has read the dS^T smem operand
         uint32_t dk2[QH / 2];  // dS^T as bf16 pairs
 #pragma unroll
         for (int cc = 0; cc < QH; cc += 32) {
@@ -1888,7 +1892,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       }
       // ---- item epilogue: dK (scaled, inverse RoPE), then dV -> bf16; TMEM is released after
       // the loads so the next item's first dV MMA can start while the stores drain
-      mbar_wait(dkv_full, j & 1);
+      bwd_wait(dkv_full, j & 1);
       tc_fence_after();
       {
         const int which = half;  // half 0 drains dK, half 1 dV
