@@ -152,6 +152,15 @@ __device__ __forceinline__ uint32_t p_offset(int r, int c) {
   return (uint32_t)(chunk * 16384 + r * 128 + ((((cc >> 3) ^ (r & 7)) << 4)) + ((cc & 7) << 1));
 }
 
+#ifndef ATTN_FWD_PRODUCER_SLEEP
+#define ATTN_FWD_PRODUCER_SLEEP 0
+#endif
+// TMA / MMA warps of the forward kernels: sleep on the barrier (suspend hint) or poll
+__device__ __forceinline__ void prod_wait(uint64_t* bar, uint32_t parity) {
+  if constexpr (ATTN_FWD_PRODUCER_SLEEP) mbar_wait_sleep<20000>(bar, parity);
+  else mbar_wait(bar, parity);
+}
+
 // Persistent forward: one CTA per SM loops over work items (query tile, head) in heavy-first
 // order.  All pipeline counters run across items: K/V stream through the ring, S alternates
 // between two TMEM buffers by global tile index, Q is double-buffered by item index, so the
@@ -735,16 +744,16 @@ __global__ void __launch_bounds__(FwdDecCfg<DH>::THREADS, 1)
         const FwdItem it = it_n;
         if (snake_item(j + 1) < n_items) it_n = fwd_item<CAUSAL>(snake_item(j + 1), H, Hk, cu, tiles);
         const int qb = j & 1;
-        mbar_wait(&q_empty[qb], ((j >> 1) & 1) ^ 1);
+        prod_wait(&q_empty[qb], ((j >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(&q_full[qb], TB);
         load_tile<DH>(sm + C::Q + qb * TB, &map_q, &q_full[qb], it.h * DH, it.s0 + it.q0);
         for (int i = 0; i < it.n_kv; ++i, ++g) {
           const int st = g % KVS;
           const uint32_t ph = (g / KVS) & 1;
-          mbar_wait(&k_empty[st], ph ^ 1);
+          prod_wait(&k_empty[st], ph ^ 1);
           mbar_arrive_expect_tx(&k_full[st], TB);
           load_tile<DH>(sm + C::K + st * TB, &map_k, &k_full[st], it.hk * DH, it.s0 + i * BKV);
-          mbar_wait(&v_empty[st], ph ^ 1);
+          prod_wait(&v_empty[st], ph ^ 1);
           mbar_arrive_expect_tx(&v_full[st], TB);
           load_tile<DH>(sm + C::V + st * TB, &map_v, &v_full[st], it.hk * DH, it.s0 + i * BKV);
         }
@@ -759,9 +768,9 @@ __global__ void __launch_bounds__(FwdDecCfg<DH>::THREADS, 1)
              *oe = o_empty(mg);
     auto issue_pv = [&](int gp, int ip, int jp, int ob) {
       const int pb = gp & 1;
-      if (ip == 0) mbar_wait(&oe[ob], ((jp / NOB) & 1) ^ 1);
-      mbar_wait(&pf[pb], (gp >> 1) & 1);
-      mbar_wait(&v_full[gp % KVS], (gp / KVS) & 1);
+      if (ip == 0) prod_wait(&oe[ob], ((jp / NOB) & 1) ^ 1);
+      prod_wait(&pf[pb], (gp >> 1) & 1);
+      prod_wait(&v_full[gp % KVS], (gp / KVS) & 1);
       tc_fence_after();
       const uint32_t v_base = smem_u32(sm + C::V + (gp % KVS) * TB);
       if (elect_one()) {
@@ -793,13 +802,13 @@ __global__ void __launch_bounds__(FwdDecCfg<DH>::THREADS, 1)
       const FwdItem it = it_n;
       if (snake_item(j + 1) < n_items) it_n = fwd_item<CAUSAL>(snake_item(j + 1), H, Hk, cu, tiles);
       const int qb = j & 1, ob = j % NOB;
-      mbar_wait(&q_full[qb], (j >> 1) & 1);
+      prod_wait(&q_full[qb], (j >> 1) & 1);
       const uint32_t q_base = smem_u32(sm + C::Q + qb * TB);
       for (int i = 0; i < it.n_kv; ++i, ++g) {
         const int b = g & 1;
         const int st = g % KVS;
-        mbar_wait(&k_full[st], (g / KVS) & 1);
-        mbar_wait(&se[b], ((g >> 1) & 1) ^ 1);
+        prod_wait(&k_full[st], (g / KVS) & 1);
+        prod_wait(&se[b], ((g >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t k_base = smem_u32(sm + C::K + st * TB);
         if (elect_one()) {
@@ -1128,17 +1137,17 @@ __global__ void __launch_bounds__(FwdPPCfg<DH>::THREADS, 1)
       for (int w = snake_item(0); w < n_items; w = snake_item(++j)) {
         const PPItem it = pp_item<CAUSAL>(w, H, Hk, cu, tiles);
         const int qb = j % QB;
-        mbar_wait(&q_empty[qb], ((j / QB) & 1) ^ 1);
+        prod_wait(&q_empty[qb], ((j / QB) & 1) ^ 1);
         mbar_arrive_expect_tx(&q_full[qb], TB * (it.n[1] > 0 ? 2 : 1));
         load_tile<DH>(sm + C::Q + qb * 2 * TB, &map_q, &q_full[qb], it.h * DH, it.s0 + it.q0);
         if (it.n[1] > 0) load_tile<DH>(sm + C::Q + (qb * 2 + 1) * TB, &map_q, &q_full[qb], it.h * DH, it.s0 + it.q0 + BQ);
         for (int i = 0; i < it.nk; ++i, ++g) {
           const int st = g % KVS;
           const uint32_t ph = (g / KVS) & 1;
-          mbar_wait(&k_empty[st], ph ^ 1);
+          prod_wait(&k_empty[st], ph ^ 1);
           mbar_arrive_expect_tx(&k_full[st], TB);
           load_tile<DH>(sm + C::K + st * TB, &map_k, &k_full[st], it.hk * DH, it.s0 + i * BKV);
-          mbar_wait(&v_empty[st], ph ^ 1);
+          prod_wait(&v_empty[st], ph ^ 1);
           mbar_arrive_expect_tx(&v_full[st], TB);
           load_tile<DH>(sm + C::V + st * TB, &map_v, &v_full[st], it.hk * DH, it.s0 + i * BKV);
         }
@@ -1153,7 +1162,7 @@ __global__ void __launch_bounds__(FwdPPCfg<DH>::THREADS, 1)
     for (int w = snake_item(0); w < n_items; w = snake_item(++j)) {
       const PPItem it = pp_item<CAUSAL>(w, H, Hk, cu, tiles);
       const int qb = j % QB;
-      mbar_wait(&q_full[qb], (j / QB) & 1);
+      prod_wait(&q_full[qb], (j / QB) & 1);
       const uint32_t q_base = smem_u32(sm + C::Q + qb * 2 * TB);
       const int n_s = it.n[0] + it.n[1];
       int s_done = 0;
@@ -1174,8 +1183,8 @@ __global__ void __launch_bounds__(FwdPPCfg<DH>::THREADS, 1)
       };
       auto issue_pv = [&](int t, int i, int vst) {  // O_t += P_t V (V tile in ring stage vst)
         const int ob = nw[t] % NOB;
-        if (i == 0) mbar_wait(&o_empty[t * 2 + ob], ((nw[t] / NOB) & 1) ^ 1);
-        mbar_wait(&p_full[t], np[t] & 1);
+        if (i == 0) prod_wait(&o_empty[t * 2 + ob], ((nw[t] / NOB) & 1) ^ 1);
+        prod_wait(&p_full[t], np[t] & 1);
         ++np[t];
         tc_fence_after();
         const uint32_t v_base = smem_u32(sm + C::V + vst * TB);
@@ -1193,7 +1202,7 @@ __global__ void __launch_bounds__(FwdPPCfg<DH>::THREADS, 1)
       // prologue: S_A(0), S_B(0)
       {
         const int st = g % KVS;
-        mbar_wait(&k_full[st], (g / KVS) & 1);
+        prod_wait(&k_full[st], (g / KVS) & 1);
         tc_fence_after();
         for (int t = 0; t < 2; ++t)
           if (it.n[t] > 0) issue_s(t, st);
@@ -1202,9 +1211,9 @@ __global__ void __launch_bounds__(FwdPPCfg<DH>::THREADS, 1)
       }
       for (int i = 0; i < it.nk; ++i) {
         const int st = (g + i) % KVS, st1 = (g + i + 1) % KVS;
-        mbar_wait(&v_full[st], ((g + i) / KVS) & 1);
+        prod_wait(&v_full[st], ((g + i) / KVS) & 1);
         const bool more = i + 1 < it.nk;
-        if (more) mbar_wait(&k_full[st1], ((g + i + 1) / KVS) & 1);
+        if (more) prod_wait(&k_full[st1], ((g + i + 1) / KVS) & 1);
         for (int t = 0; t < 2; ++t) {
           if (i < it.n[t]) issue_pv(t, i, st);
           if (i + 1 < it.n[t]) {
