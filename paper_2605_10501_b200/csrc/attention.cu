@@ -650,13 +650,14 @@ __global__ void __launch_bounds__(FwdCfg<DH, CG>::THREADS, 1)
 // Warps: w0 TMA, w1 / w2 MMA for groups 0 / 1, w3..w10 softmax (group (w - 3) / 4, quadrant w & 3).
 // TMEM: S_g buffer b at g * 128 + b * 64; O_g at 256 + (ob * 2 + g) * 64 (head_dim 64, two sets by
 // item) or 256 + g * 128 (head_dim 128, one set).
-template <int DH>
+template <int DH, int NG = 2>
 struct FwdDecCfg {
-  static constexpr int SW0 = 3;
-  static constexpr int THREADS = 32 * SW0 + 256;
+  static constexpr int CW = BKV / NG;           // key columns per group
+  static constexpr int SW0 = 1 + NG;            // w0 TMA, w1..wNG MMA (one per group), then softmax
+  static constexpr int THREADS = 32 * SW0 + 128 * NG;
   static constexpr int TILE = 128 * DH * 2;
   static constexpr int KVS = DH == 64 ? 3 : 2;
-  static constexpr int NOB = DH == 64 ? 2 : 1;
+  static constexpr int NOB = (256 + 2 * NG * DH <= 512) ? 2 : 1;  // O sets (by item)
   static constexpr int Q = 0;
   static constexpr int K = Q + 2 * TILE;
   static constexpr int V = K + KVS * TILE;
@@ -664,24 +665,26 @@ struct FwdDecCfg {
   // one-tile item's S is issued before the PV that waits for the item-before-last's epilogue),
   // so three items can have an epilogue in flight
   static constexpr int XS = 4;
-  static constexpr int XMAX = V + KVS * TILE;  // [XS items][2 groups][128]
-  static constexpr int XSUM = XMAX + XS * 2 * 128 * 4;
-  static constexpr int CNT = XSUM + XS * 2 * 128 * 4;  // [XS items][4 quadrants] arrivals
+  static constexpr int XMAX = V + KVS * TILE;  // [XS items][NG groups][128]
+  static constexpr int XSUM = XMAX + XS * NG * 128 * 4;
+  static constexpr int CNT = XSUM + XS * NG * 128 * 4;  // [XS items][4 quadrants] arrivals
   static constexpr int BAR = CNT + 64;
-  static constexpr int TOTAL = BAR + 512;
+  static constexpr int TOTAL = BAR + 1024;
   static_assert(TOTAL + 1024 <= 227 * 1024, "forward smem");
-  __device__ static constexpr uint32_t o_col(int ob, int g) { return NOB == 2 ? 256 + (ob * 2 + g) * DH : 256 + g * DH; }
+  static_assert(2 * NG * CW + NOB * NG * DH <= 512, "forward TMEM");
+  __device__ static constexpr uint32_t s_col(int g, int b) { return g * 2 * CW + b * CW; }
+  __device__ static constexpr uint32_t o_col(int ob, int g) { return 256 + (ob * NG + g) * DH; }
 };
 
-template <int DH, bool CAUSAL>
-__global__ void __launch_bounds__(FwdDecCfg<DH>::THREADS, 1)
+template <int DH, bool CAUSAL, int NG = 2>
+__global__ void __launch_bounds__(FwdDecCfg<DH, NG>::THREADS, 1)
     attn_fwd_dec_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                         const __grid_constant__ CUtensorMap map_v, const int32_t* __restrict__ cu,
                         const int2* __restrict__ tiles, const int* __restrict__ n_tiles,
                         __nv_bfloat16* __restrict__ out, int ldo, float* __restrict__ lse, int T, int H, int Hk,
                         float scale2, int stagger_ns) {
-  using C = FwdDecCfg<DH>;
-  constexpr int KVS = C::KVS, NOB = C::NOB, TB = C::TILE, CW = 64;
+  using C = FwdDecCfg<DH, NG>;
+  constexpr int KVS = C::KVS, NOB = C::NOB, TB = C::TILE, CW = C::CW;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* sm = align_smem_1024(smem_raw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::BAR);
@@ -698,7 +701,7 @@ __global__ void __launch_bounds__(FwdDecCfg<DH>::THREADS, 1)
   auto p_empty = [&](int g) { return gb + 12 * g + 6; };
   auto o_full = [&](int g) { return gb + 12 * g + 8; };
   auto o_empty = [&](int g) { return gb + 12 * g + 10; };
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gb + 24);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gb + 12 * NG);
   int* cnt = reinterpret_cast<int*>(sm + C::CNT);
 
   const int n_items = *n_tiles * H;
@@ -709,15 +712,15 @@ __global__ void __launch_bounds__(FwdDecCfg<DH>::THREADS, 1)
     tma_prefetch(&map_v);
     for (int b = 0; b < 2; ++b) {
       mbar_init(&q_full[b], 1);
-      mbar_init(&q_empty[b], 2);
+      mbar_init(&q_empty[b], NG);
     }
     for (int s = 0; s < KVS; ++s) {
       mbar_init(&k_full[s], 1);
-      mbar_init(&k_empty[s], 2);
+      mbar_init(&k_empty[s], NG);
       mbar_init(&v_full[s], 1);
-      mbar_init(&v_empty[s], 2);
+      mbar_init(&v_empty[s], NG);
     }
-    for (int g = 0; g < 2; ++g)
+    for (int g = 0; g < NG; ++g)
       for (int b = 0; b < 2; ++b) {
         mbar_init(&s_full(g)[b], 1);
         mbar_init(&s_empty(g)[b], 128);
@@ -759,9 +762,9 @@ __global__ void __launch_bounds__(FwdDecCfg<DH>::THREADS, 1)
         }
       }
     }
-  } else if (warp <= 2) {
+  } else if (warp <= NG) {
     const int mg = warp - 1;  // column group served by this MMA warp
-    if (mg == 1 && stagger_ns > 0) __nanosleep(stagger_ns);
+    if (mg > 0 && stagger_ns > 0) __nanosleep(stagger_ns * mg / (NG - 1));
     constexpr uint32_t idesc_s = idesc_bf16_f32(BQ, CW, false, false);
     constexpr uint32_t idesc_o = idesc_bf16_f32(BQ, DH, false, true);
     uint64_t *sf = s_full(mg), *se = s_empty(mg), *pf = p_full(mg), *pe = p_empty(mg), *of = o_full(mg),
@@ -775,9 +778,9 @@ __global__ void __launch_bounds__(FwdDecCfg<DH>::THREADS, 1)
       const uint32_t v_base = smem_u32(sm + C::V + (gp % KVS) * TB);
       if (elect_one()) {
 #pragma unroll
-        for (int kc = 0; kc < CW / 16; ++kc)  // keys 64 mg + 16 kc (V as an MN-major operand)
-          umma_bf16_ts(tmem + C::o_col(ob, mg), tmem + mg * 128 + pb * CW + kc * 8,
-                       sdesc((v_base >> 4) + (4 * mg + kc) * 128, DH == 64 ? 8192 : 16384, 1024), idesc_o,
+        for (int kc = 0; kc < CW / 16; ++kc)  // keys CW mg + 16 kc (V as an MN-major operand)
+          umma_bf16_ts(tmem + C::o_col(ob, mg), tmem + C::s_col(mg, pb) + kc * 8,
+                       sdesc((v_base >> 4) + ((CW / 16) * mg + kc) * 128, DH == 64 ? 8192 : 16384, 1024), idesc_o,
                        (ip > 0 || kc > 0) ? 1u : 0u);
         umma_commit(&v_empty[gp % KVS]);
         umma_commit(&pe[pb]);
@@ -813,9 +816,9 @@ __global__ void __launch_bounds__(FwdDecCfg<DH>::THREADS, 1)
         const uint32_t k_base = smem_u32(sm + C::K + st * TB);
         if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < DH / 16; ++kk)  // B = keys 64 mg .. 64 mg + 63 of the tile (8 KB into each chunk)
-            umma_bf16(tmem + mg * 128 + b * CW, sdesc((q_base >> 4) + (kk >> 2) * 1024 + (kk & 3) * 2, 16, 1024),
-                      sdesc((k_base >> 4) + (kk >> 2) * 1024 + (kk & 3) * 2 + 512 * mg, 16, 1024), idesc_s,
+          for (int kk = 0; kk < DH / 16; ++kk)  // B = keys CW mg .. CW mg + CW - 1 (CW x 128 B into each chunk)
+            umma_bf16(tmem + C::s_col(mg, b), sdesc((q_base >> 4) + (kk >> 2) * 1024 + (kk & 3) * 2, 16, 1024),
+                      sdesc((k_base >> 4) + (kk >> 2) * 1024 + (kk & 3) * 2 + 8 * CW * mg, 16, 1024), idesc_s,
                       kk > 0 ? 1u : 0u);
           umma_commit(&k_empty[st]);
           umma_commit(&sf[b]);
@@ -842,47 +845,56 @@ __global__ void __launch_bounds__(FwdDecCfg<DH>::THREADS, 1)
     // Item jj is finished by whichever group's warp of this quadrant arrives second.
     auto epilogue = [&](const FwdItem& it, int jj, float m, float l) {
       const int ob = jj % NOB, par = jj % C::XS;
-      xmax[(par * 2 + grp) * 128 + r] = m;
-      xsum[(par * 2 + grp) * 128 + r] = l;
+      xmax[(par * NG + grp) * 128 + r] = m;
+      xsum[(par * NG + grp) * 128 + r] = l;
       __threadfence_block();
       __syncwarp();
       int old = 0;
       if (lane == 0) old = atomicAdd(&cnt[par * 4 + q], 1);
       old = __shfl_sync(kFull, old, 0);
-      if (old == 0) return;
+      if (old != NG - 1) return;
       __threadfence_block();
       const uint32_t ph = (jj / NOB) & 1;
-      mbar_wait(&o_full(0)[ob], ph);
-      mbar_wait(&o_full(1)[ob], ph);
+#pragma unroll
+      for (int c = 0; c < NG; ++c) mbar_wait(&o_full(c)[ob], ph);
       tc_fence_after();
-      const float m0 = xmax[(par * 2) * 128 + r], m1 = xmax[(par * 2 + 1) * 128 + r];
-      const float l0 = xsum[(par * 2) * 128 + r], l1 = xsum[(par * 2 + 1) * 128 + r];
-      const float M = fmaxf(m0, m1);
-      float f0 = m0 == -INFINITY ? 0.f : ex2(m0 - M), f1 = m1 == -INFINITY ? 0.f : ex2(m1 - M);
-      const float l_all = l0 * f0 + l1 * f1;
+      float fc[NG], M = -INFINITY, l_all = 0.f;
+#pragma unroll
+      for (int c = 0; c < NG; ++c) M = fmaxf(M, xmax[(par * NG + c) * 128 + r]);
+#pragma unroll
+      for (int c = 0; c < NG; ++c) {
+        const float mc = xmax[(par * NG + c) * 128 + r];
+        fc[c] = mc == -INFINITY ? 0.f : ex2(mc - M);
+        l_all += xsum[(par * NG + c) * 128 + r] * fc[c];
+      }
       const float rl = __frcp_rn(l_all);
-      f0 *= rl;
-      f1 *= rl;
+#pragma unroll
+      for (int c = 0; c < NG; ++c) fc[c] *= rl;
       const int qpos = it.q0 + r;
 #pragma unroll
       for (int sub = 0; sub < DH / 32; ++sub) {
-        uint32_t ra[32], rb[32];
-        tmem_ld_32x32b_x32(tmem + lane_base + C::o_col(ob, 0) + sub * 32, ra);
-        tmem_ld_32x32b_x32(tmem + lane_base + C::o_col(ob, 1) + sub * 32, rb);
-        tmem_ld_wait();
-        if (sub == DH / 32 - 1) {  // both O sets read: the slot's counter is reset before release
+        float acc[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) acc[e] = 0.f;
+#pragma unroll
+        for (int c = 0; c < NG; ++c) {
+          uint32_t ra[32];
+          tmem_ld_32x32b_x32(tmem + lane_base + C::o_col(ob, c) + sub * 32, ra);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) acc[e] = fmaf(__uint_as_float(ra[e]), fc[c], acc[e]);
+        }
+        if (sub == DH / 32 - 1) {  // every group's O read: the slot's counter is reset before release
           if (lane == 0) cnt[par * 4 + q] = 0;
           __threadfence_block();
           tc_fence_before();
-          mbar_arrive(&o_empty(0)[ob]);
-          mbar_arrive(&o_empty(1)[ob]);
+#pragma unroll
+          for (int c = 0; c < NG; ++c) mbar_arrive(&o_empty(c)[ob]);
         }
         if (qpos < it.L) {
           uint32_t o[16];
 #pragma unroll
-          for (int e = 0; e < 16; ++e)
-            o[e] = pack_bf16(__uint_as_float(ra[2 * e]) * f0 + __uint_as_float(rb[2 * e]) * f1,
-                             __uint_as_float(ra[2 * e + 1]) * f0 + __uint_as_float(rb[2 * e + 1]) * f1);
+          for (int e = 0; e < 16; ++e) o[e] = pack_bf16(acc[2 * e], acc[2 * e + 1]);
           uint4* dst = reinterpret_cast<uint4*>(out + (size_t)(it.s0 + qpos) * ldo + it.h * DH + sub * 32);
 #pragma unroll
           for (int u = 0; u < 4; ++u) dst[u] = make_uint4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);
@@ -909,15 +921,15 @@ __global__ void __launch_bounds__(FwdDecCfg<DH>::THREADS, 1)
         const int b = g & 1;
         mbar_wait(&sf[b], (g >> 1) & 1);
         tc_fence_after();
-        const uint32_t s_col = tmem + lane_base + grp * 128 + b * CW;
+        const uint32_t s_col = tmem + lane_base + C::s_col(grp, b);
         float s[CW];
         {
-          uint32_t raw[2][32];
-          tmem_ld_32x32b_x32(s_col, raw[0]);
-          tmem_ld_32x32b_x32(s_col + 32, raw[1]);
+          uint32_t raw[CW / 32][32];
+#pragma unroll
+          for (int c = 0; c < CW / 32; ++c) tmem_ld_32x32b_x32(s_col + 32 * c, raw[c]);
           tmem_ld_wait();
 #pragma unroll
-          for (int c = 0; c < 2; ++c)
+          for (int c = 0; c < CW / 32; ++c)
 #pragma unroll
             for (int jj = 0; jj < 32; ++jj) s[c * 32 + jj] = __uint_as_float(raw[c][jj]);
         }
@@ -930,7 +942,7 @@ __global__ void __launch_bounds__(FwdDecCfg<DH>::THREADS, 1)
           uint32_t zero[CW / 2];
 #pragma unroll
           for (int e = 0; e < CW / 2; ++e) zero[e] = 0u;
-          tmem_st_32x32b_x32(s_col, zero);
+          tmem_st_cols<CW / 2>(s_col, zero);
           tmem_st_wait();
           tc_fence_before();
           mbar_arrive(&pf[b]);
@@ -997,7 +1009,7 @@ __global__ void __launch_bounds__(FwdDecCfg<DH>::THREADS, 1)
           uint32_t pk[CW / 2];
 #pragma unroll
           for (int e = 0; e < CW / 2; ++e) pk[e] = pack_bf16(s[2 * e], s[2 * e + 1]);
-          tmem_st_32x32b_x32(s_col, pk);
+          tmem_st_cols<CW / 2>(s_col, pk);
         }
         tmem_st_wait();
         tc_fence_before();
@@ -2098,7 +2110,8 @@ MAESTRO_API int maestro_attn_fwd(const void* q, const void* k, const void* v, co
   static const int env_variant = [] {
     const char* e = getenv("MAESTRO_ATTN_FWD");
     if (!e) return ATTN_FWD_VARIANT;
-    return e[0] == 'p' ? 2 : (e[0] == 'd' ? 1 : (e[0] == 'b' ? 0 : ATTN_FWD_VARIANT));
+    if (e[0] == 'd') return e[3] == '4' ? 3 : 1;  // "dec" / "dec4"
+    return e[0] == 'p' ? 2 : (e[0] == 'b' ? 0 : ATTN_FWD_VARIANT);
   }();
   const int variant = env_variant >= 0 ? env_variant : (head_dim == 64 ? 1 : (causal ? 0 : 2));
   if (variant == 2) {  // 256-row items: the plan's third list, or built into the workspace
@@ -2163,19 +2176,22 @@ MAESTRO_API int maestro_attn_fwd(const void* q, const void* k, const void* v, co
     return e ? atoi(e) : 0;
   }();
   const int cg = cg_env == 2 || cg_env == 4 ? cg_env : ATTN_FWD_CG64;
-  if (variant == 1) {
-#define MB_ATTN_DEC(D, CZ)                                                                                   \
+  if (variant == 1 || (variant == 3 && head_dim == 64)) {
+#define MB_ATTN_DEC(D, CZ, NGR)                                                                              \
   {                                                                                                          \
-    const int smem = FwdDecCfg<D>::TOTAL + 1024;                                                             \
-    if (ensure_smem<attn_fwd_dec_kernel<D, CZ>>(smem)) return launch_status();                               \
-    attn_fwd_dec_kernel<D, CZ><<<grid, FwdDecCfg<D>::THREADS, smem, st>>>(mq, mk, mv, cu, tiles, count,       \
-                                                                           (__nv_bfloat16*)out, ldo, lse, T, H, \
-                                                                           Hk, scale2, dec_stagger);         \
+    using CF = FwdDecCfg<D, NGR>;                                                                            \
+    const int smem = CF::TOTAL + 1024;                                                                       \
+    if (ensure_smem<attn_fwd_dec_kernel<D, CZ, NGR>>(smem)) return launch_status();                          \
+    attn_fwd_dec_kernel<D, CZ, NGR><<<grid, CF::THREADS, smem, st>>>(mq, mk, mv, cu, tiles, count,            \
+                                                                      (__nv_bfloat16*)out, ldo, lse, T, H,     \
+                                                                      Hk, scale2, dec_stagger);              \
   }
-    if (head_dim == 64) {
-      if (causal) MB_ATTN_DEC(64, true) else MB_ATTN_DEC(64, false)
+    if (variant == 3) {  // four 32-column groups: four softmax warps per SM sub-partition
+      if (causal) MB_ATTN_DEC(64, true, 4) else MB_ATTN_DEC(64, false, 4)
+    } else if (head_dim == 64) {
+      if (causal) MB_ATTN_DEC(64, true, 2) else MB_ATTN_DEC(64, false, 2)
     } else {
-      if (causal) MB_ATTN_DEC(128, true) else MB_ATTN_DEC(128, false)
+      if (causal) MB_ATTN_DEC(128, true, 2) else MB_ATTN_DEC(128, false, 2)
     }
 #undef MB_ATTN_DEC
     return launch_status();

@@ -49,7 +49,7 @@ def _run(variant, out):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("variant", ["dec", "pp"])
+@pytest.mark.parametrize("variant", ["dec", "pp", "dec4"])
 def test_forward_variant_matches_shared_tile(variant, tmp_path):
     import torch
 
