@@ -653,7 +653,11 @@ __global__ void __launch_bounds__(FwdCfg<DH, CG>::THREADS, 1)
 template <int DH, int NG = 2>
 struct FwdDecCfg {
   static constexpr int CW = BKV / NG;           // key columns per group
-  static constexpr int SW0 = 1 + NG;            // w0 TMA, w1..wNG MMA (one per group), then softmax
+  // w0 TMA, w1..wNG MMA (one per group), then softmax; NG = 4: softmax from warp 8 so the two
+  // producer warpgroups can hand registers to the four softmax warpgroups (setmaxnreg)
+  static constexpr bool REG_SPLIT = false;  // NG == 4 with setmaxnreg: ptxas still compiles the softmax at 80 registers (spills)
+  static constexpr int SW0 = REG_SPLIT ? 8 : 1 + NG;
+  static constexpr int REG_PROD = 40, REG_SMX = 104;  // REG_SPLIT: 8 x 32 x 40 + 16 x 32 x 104 <= 64 K
   static constexpr int THREADS = 32 * SW0 + 128 * NG;
   static constexpr int TILE = 128 * DH * 2;
   static constexpr int KVS = DH == 64 ? 3 : 2;
@@ -737,6 +741,12 @@ __global__ void __launch_bounds__(FwdDecCfg<DH, NG>::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if constexpr (C::REG_SPLIT) {
+    if (warp < C::SW0)
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(C::REG_PROD));
+    else
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(C::REG_SMX));
+  }
 
   if (warp == 0) {
     if (lane == 0) {
@@ -834,7 +844,7 @@ __global__ void __launch_bounds__(FwdDecCfg<DH, NG>::THREADS, 1)
       }
     }
     flush();
-  } else {
+  } else if (warp >= C::SW0) {
     const int q = warp & 3;
     const int grp = (warp - C::SW0) >> 2;
     const int r = q * 32 + lane;
