@@ -218,17 +218,25 @@ constexpr int KDS_VC_MAX = KDS_CH * KDS_NCH;  // 16384 columns = 64 KB of (t, s)
 constexpr int KDS_THREADS = KDS_CONS + 32; // + producer warp
 constexpr int KDS_SMEM = KDS_NCH * KDS_CH * 4 + 1024;
 constexpr int KDS_CTAS_PER_SM = 3;         // three row slices in flight per SM (different phases)
+#ifndef KDS_SLEEP_NS
+#define KDS_SLEEP_NS 20000
+#endif
 
+// Cluster-scope acquire wait with a suspend-time hint: the waiting threads sleep until the phase
+// completes instead of re-polling (each poll at cluster scope also invalidates L1: CCTL).
 __device__ __forceinline__ bool mbar_try_wait_cluster(uint32_t addr, uint32_t parity) {
   uint32_t ok;
   asm volatile(
-      "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, "
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, "
       "0, p;\n}"
       : "=r"(ok)
-      : "r"(addr), "r"(parity)
+      : "r"(addr), "r"(parity), "n"(KDS_SLEEP_NS)
       : "memory");
   return ok != 0;
 }
+// chunk barriers: sleep on the barrier rather than spin (the kernel is issue-bound; spinning
+// consumer and producer warps took a third of the issue slots)
+__device__ __forceinline__ void kds_wait(uint64_t* bar, uint32_t parity) { sm100::mbar_wait_sleep<KDS_SLEEP_NS>(bar, parity); }
 __device__ __forceinline__ void st_cluster_f32(uint32_t addr, float v) {
   asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
 }
@@ -271,7 +279,7 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(KDS_THREADS, KDS_CTA
         const __nv_bfloat16* sr = sl + (size_t)row * lds + c0;
         for (int k = 0; k < nch; ++k) {
           const int w = min(KDS_CH, cols - k * KDS_CH);
-          mbar_wait(&empty[k], (it & 1) ^ 1);
+          kds_wait(&empty[k], (it & 1) ^ 1);
           mbar_arrive_expect_tx(&full[k], 4u * (uint32_t)w);
           bulk_load_1d(sm + k * (KDS_CH * 4), tr + k * KDS_CH, 2u * (uint32_t)w, &full[k]);
           bulk_load_1d(sm + k * (KDS_CH * 4) + KDS_CH * 2, sr + k * KDS_CH, 2u * (uint32_t)w, &full[k]);
@@ -290,7 +298,7 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(KDS_THREADS, KDS_CTA
       for (int k = 0; k < KDS_NCH; ++k) {
         mh_t[k] = mh_s[k] = 0.f;
         if (k >= nch) break;
-        mbar_wait(&full[k], ph);
+        kds_wait(&full[k], ph);
         const bool mine = k * KDS_CH + 8 * tid < cols;
         uint4* pt = reinterpret_cast<uint4*>(sm + k * (KDS_CH * 4)) + tid;
         uint4* ps = reinterpret_cast<uint4*>(sm + k * (KDS_CH * 4) + KDS_CH * 2) + tid;
