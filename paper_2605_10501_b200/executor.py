@@ -244,7 +244,7 @@ class KDExecutor:
     def plan(self, stream):
         """K1-K5 on device for this step; returns per-local-rank micro-batch tables (host)."""
         with torch.cuda.stream(stream):
-            self.planner.plan_tokens(self.cost, self.tokens, self.batch, stream)
+            self.planner.plan_tokens_graphed(self.cost, self.tokens, self.batch, stream)
         tab = self.graph.tables
         crit, teach = tab.critical, tab.section_ids.index("teacher")
         out = {}

@@ -172,6 +172,30 @@ class DevicePlanner:
                                          N.ptr(self.sec_off), N.ptr(self.metrics), N.ptr(self.evals),
                                          N.ptr(self.work), N.ptr(self.err), s), "build_schedule")
 
+    def plan_tokens_graphed(self, cost_table, tokens, B: int, stream=None) -> None:
+        """``plan_tokens`` replayed from a CUDA graph: the five launches (error reset, K1, K2, K3,
+        K4) are captured once per (cost table, token buffer, B) and replayed as one graph launch
+        -- the executors whose plan inputs live in fixed device buffers (KD) use it every step."""
+        torch = self.torch
+        key = (cost_table.data_ptr(), tokens.data_ptr(), int(B))
+        if getattr(self, "_graph_key", None) != key:
+            self._check_b(B)
+            cap = torch.cuda.Stream(device=self.ids.device)
+            cap.wait_stream(torch.cuda.current_stream(self.ids.device))
+            with torch.cuda.stream(cap):
+                self.plan_tokens(cost_table, tokens, B)  # warm-up: kernel attributes set outside capture
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=cap):
+                self.plan_tokens(cost_table, tokens, B)
+            torch.cuda.current_stream(self.ids.device).wait_stream(cap)
+            self._graph, self._graph_key = graph, key
+        self.B = B
+        if stream is None:
+            self._graph.replay()
+        else:
+            with torch.cuda.stream(stream):
+                self._graph.replay()
+
     # -- host readback (syncs) ----------------------------------------------------------
     def raise_errors(self, ids=None) -> None:
         N.raise_device_error(int(self.err.item()), ids, self.tables.section_ids)

@@ -80,6 +80,16 @@ def main():
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1))
         p.raise_errors()
+        tg = []
+        for _ in range(12):  # the same plan replayed from a CUDA graph (one launch)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            p.plan_tokens_graphed(cost, tokens, B)
+            e1.record()
+            torch.cuda.synchronize()
+            tg.append(e0.elapsed_time(e1))
+        p.raise_errors()
         bd = breakdown(p, cost, tokens, B)
         times = p.times[: 6 * B].view(6, B).cpu().numpy()
         act = p.act[:B].cpu().numpy().view(np.uint32)
@@ -94,7 +104,7 @@ def main():
                                              tab.neighbor, tab.merge_order)
             best = min(best, time.perf_counter() - t0)
         got = {k: list(v) for k, v in p.host_orders().items()}
-        print(json.dumps({"case": name, "device_plan_us": min(ts[2:]) * 1e3, "cpu_port_us": best * 1e6,
+        print(json.dumps({"case": name, "device_plan_us": min(ts[2:]) * 1e3, "device_plan_graph_us": min(tg[2:]) * 1e3, "cpu_port_us": best * 1e6,
                           "evals": ev, "orders_match": got == want,
                           "breakdown_us": bd}), flush=True)
 
