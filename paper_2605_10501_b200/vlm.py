@@ -181,11 +181,14 @@ class VLMExecutor:
         tok = np.zeros((len(self.bits), B), dtype=np.int32)
         tok[self.bits["llm"]] = hb["lens"]
         tok[self.bits["vit"]] = np.where(hb["has_img"], R.VIT_PATCHES, 0)
+        if not hasattr(self, "_tok_dev"):  # fixed token buffer: the plan is replayed from a CUDA graph
+            self._tok_dev = torch.empty(tok.shape, dtype=torch.int32, device=dev)
         with torch.cuda.stream(stream):
-            tokens = torch.from_numpy(tok).pin_memory().to(dev, non_blocking=True)
+            tokens = torch.from_numpy(tok).pin_memory()
+            self._tok_dev.copy_(tokens, non_blocking=True)
             ids = torch.arange(B, dtype=torch.int32).pin_memory().to(dev, non_blocking=True)
             self.planner.ids[:B].copy_(ids)
-            self.planner.plan_tokens(self.cost, tokens, B, stream)
+            self.planner.plan_tokens_graphed(self.cost, self._tok_dev, B, stream)
             self._h_orders.copy_(self.planner.orders[: self._h_orders.numel()], non_blocking=True)
             self._h_off.copy_(self.planner.sec_off, non_blocking=True)
             self._h_err.copy_(self.planner.err, non_blocking=True)  # K1-K4 error word
@@ -512,10 +515,12 @@ class VLMGroupExecutor:
             self._h_orders = torch.empty(n_sec * B, dtype=torch.int32).pin_memory()
             self._h_off = torch.empty(n_sec * (N.MAX_DP + 1), dtype=torch.int32).pin_memory()
             self._h_err = torch.empty(1, dtype=torch.int64).pin_memory()
+        if not hasattr(self, "_tok_dev"):  # fixed token buffer: the plan is replayed from a CUDA graph
+            self._tok_dev = torch.empty(tok.shape, dtype=torch.int32, device=dev)
         with torch.cuda.stream(stream):
-            tokens = _h2d(tok, dev)
+            self._tok_dev.copy_(_h2d(tok, dev))
             self.planner.ids[:B].copy_(_h2d(np.arange(B, dtype=np.int32), dev))
-            self.planner.plan_tokens(self.cost, tokens, B, stream)
+            self.planner.plan_tokens_graphed(self.cost, self._tok_dev, B, stream)
             self._h_orders.copy_(self.planner.orders[: self._h_orders.numel()], non_blocking=True)
             self._h_off.copy_(self.planner.sec_off, non_blocking=True)
             self._h_err.copy_(self.planner.err, non_blocking=True)
