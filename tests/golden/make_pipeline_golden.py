@@ -108,5 +108,128 @@ def main():
     print(f"wrote {out} ({len(cases)} specs)")
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--random" not in sys.argv:
     main()
+
+
+# --- randomised spec documents (graph shapes x clusters x pins x batch kinds) -------------------
+
+
+def _section(name, role, mode, hidden, heads, layers, vocab, seq, params, preset=None, extra=None, pin=None):
+    d = {"name": name, "role": role, "exec_mode": mode,
+         "structural": {"hidden_dim": hidden, "num_heads": heads, "num_layers": layers, "vocab_size": vocab,
+                        "max_seq_len": seq, "param_count": params}}
+    cost = {}
+    if preset:
+        cost["preset"] = preset
+    if extra:
+        cost.update(extra)
+    if cost:
+        d["cost"] = cost
+    if pin:
+        d["config"] = pin
+    return d
+
+
+def random_docs(seed=0, n=24):
+    import random
+
+    rng = random.Random(seed)
+    docs = []
+    for i in range(n):
+        kind = ["vlm", "kd", "enc_dec", "omni"][i % 4]
+        gpus = rng.choice([4, 8, 16])
+        pin_crit = rng.random() < 0.5
+        crit_pin = {"dp": rng.choice([1, 2, 4]), "tp": 1, "pp": 1, "cp": 1, "mbs": rng.choice([1, 2])} if pin_crit else None
+        secs, edges, transforms, subs_up = [], [], [], []
+        crit = _section("llm", "critical", "forward_backward", 2048, 16, 16, 32000, 4096, 1_000_000_000,
+                        preset="moe-backbone", pin=crit_pin)
+        if kind == "vlm":
+            secs = [_section("vit", "auxiliary", "forward_backward", 1024, 16, 24, 1, 8192, 300_000_000,
+                             preset="vit-encoder"), crit]
+            edges = [{"from": "vit", "to": "llm", "payload_bytes_per_sample": 4194304}]
+            subs_up = ["vit"]
+        elif kind == "kd":
+            crit = _section("student", "critical", "forward_backward", 768, 12, 12, 32000, 2048, 125_000_000,
+                            preset="moe-backbone", extra={"flops_per_token_fwd": 2.5e9}, pin=crit_pin)
+            secs = [_section("teacher", "auxiliary", "forward_only", 2048, 32, 22, 32000, 2048, 1_100_000_000,
+                             preset="frozen-teacher"), crit]
+            edges = [{"from": "teacher", "to": "student", "payload_bytes_per_sample": 2048 * 32000 * 2}]
+            transforms = [{"op": "colocate_output_layer", "teacher": "teacher", "student": "student",
+                           "hidden_dim": 2048, "vocab_size": 32000}]
+            subs_up = ["teacher"]
+        elif kind == "enc_dec":
+            secs = [_section("enc", "auxiliary", "forward_backward", 1024, 16, 12, 1, 4096, 200_000_000,
+                             preset="vit-encoder"), crit,
+                    _section("dec", "auxiliary", "forward_backward", 1024, 8, 8, 4096, 2048, 150_000_000,
+                             preset="vit-encoder", extra={"flops_per_token_fwd": 1.5e9})]
+            edges = [{"from": "enc", "to": "llm", "payload_bytes_per_sample": 2097152},
+                     {"from": "llm", "to": "dec", "payload_bytes_per_sample": 1048576}]
+            subs_up = ["enc", "dec"]
+        else:
+            secs = [_section("image_enc", "auxiliary", "forward_backward", 1024, 16, 24, 1, 8192, 300_000_000,
+                             preset="vit-encoder"),
+                    _section("audio_enc", "auxiliary", "forward_backward", 1024, 8, 16, 1, 4096, 200_000_000,
+                             preset="vit-encoder", extra={"flops_per_token_fwd": 1.2e9}), crit]
+            edges = [{"from": "image_enc", "to": "llm", "payload_bytes_per_sample": 4194304},
+                     {"from": "audio_enc", "to": "llm", "payload_bytes_per_sample": 2097152}]
+            transforms = [{"op": "colocate_exclusive_encoders", "a": "image_enc", "b": "audio_enc"}]
+            subs_up = ["image_enc", "audio_enc"]
+        doc = {"version": "maestro-spec v1", "sections": secs, "edges": edges,
+               "cluster": {"total_gpus": gpus, "mem_per_gpu": 8.0e10}}
+        if transforms:
+            doc["transforms"] = transforms
+        crit_name = crit["name"]
+        if rng.random() < 0.5:  # explicit batch of random 6-tuples
+            B = rng.randint(4, 24)
+            samples = []
+            for s in range(B):
+                row = {"id": s, "t_f_c": round(rng.uniform(0.5, 2.0), 3), "t_b_c": round(rng.uniform(1.0, 4.0), 3)}
+                if kind == "kd":
+                    row.update(t_f_bc=round(rng.uniform(0.5, 1.5), 3), activates=["teacher"])
+                elif kind == "enc_dec":
+                    if rng.random() < 0.6:
+                        row.update(t_f_bc=round(rng.uniform(0.1, 0.5), 3), t_b_ac=round(rng.uniform(0.2, 1.0), 3),
+                                   activates=["enc"])
+                    if rng.random() < 0.5:
+                        row.update(t_f_ac=round(rng.uniform(0.1, 0.4), 3), t_b_bc=round(rng.uniform(0.1, 0.6), 3),
+                                   activates=sorted(set(row.get("activates", [])) | {"dec"}))
+                elif rng.random() < 0.6:
+                    sub = rng.choice(subs_up)
+                    row.update(t_f_bc=round(rng.uniform(0.1, 0.5), 3), t_b_ac=round(rng.uniform(0.2, 1.0), 3),
+                               activates=[sub])
+                samples.append(row)
+            doc["batch"] = {"samples": samples}
+        else:  # statistical profile, batch derived from the cost model at the plan's configs
+            prof = {"global_batch_size": rng.choice([8, 16, 32])}
+            if kind != "kd":
+                live = subs_up if kind != "omni" else []
+                if live:
+                    prof["shares"] = {s: round(rng.uniform(0.2, 0.8), 2) for s in live}
+                prof["tokens"] = {crit_name: rng.choice([1024, 2048, 4096])}
+            doc["batch"] = {"profile": prof}
+        docs.append((f"random_{i}_{kind}", doc))
+    return docs
+
+
+def random_cases():
+    out = []
+    for name, doc in random_docs():
+        case = {"name": name, "doc": doc, "validate": rpl.validate_document(doc, name), "parse": parse_outcome(doc),
+                "end2end": {}}
+        if case["parse"] is None:
+            spec = parse_spec(doc, source=name)
+            for oname in ("default", "fwd_then_bwd"):
+                try:
+                    case["end2end"][oname] = rpl.canonical_json(rpl.run_end2end(spec, OPTIONS[oname]))
+                except Exception as e:  # noqa: BLE001
+                    case["end2end"][oname] = {"error": type(e).__name__, "message": str(e)}
+        out.append(case)
+    return out
+
+
+if __name__ == "__main__" and "--random" in sys.argv:
+    rc = random_cases()
+    p = Path(__file__).resolve().parent / "pipeline_random_golden.json"
+    p.write_text(json.dumps({"cases": rc}, indent=1, sort_keys=True) + "\n")
+    print(f"wrote {p}: {len(rc)} cases, {sum(1 for c in rc if c['parse'] is None)} parsed")

@@ -121,3 +121,30 @@ def test_end2end_derived_batch_matches_reference(name):
         pytest.skip("no derived-batch bundle in the golden file")
     got = P.canonical_json(P.run_end2end(parse_spec(m["doc"]), P.RunOptions()))
     assert got == want
+
+
+RANDOM = json.loads((Path(__file__).parent / "golden" / "pipeline_random_golden.json").read_text())["cases"]
+RANDOM_IDS = [c["name"] for c in RANDOM]
+
+
+@pytest.mark.parametrize("case", RANDOM, ids=RANDOM_IDS)
+def test_random_specs_parse_and_validate(case):
+    """24 generated spec documents (VLM, KD with a colocated head, encoder + decoder, omni with
+    colocated encoders; explicit batches or profiles; pinned or free configs; 4-16 GPUs)."""
+    assert P.validate_document(case["doc"], case["name"]) == case["validate"]
+    spec = parse_spec(case["doc"], source=case["name"])
+    assert spec.graph.critical is not None
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", RANDOM, ids=RANDOM_IDS)
+@pytest.mark.parametrize("opt", ["default", "fwd_then_bwd"])
+def test_random_specs_end2end_match_reference(case, opt):
+    want = case["end2end"][opt]
+    spec = parse_spec(case["doc"], source=case["name"])
+    if isinstance(want, dict):  # the reference's planner rejected the spec
+        with pytest.raises(Exception) as ei:
+            P.run_end2end(spec, OPTIONS[opt])
+        assert type(ei.value).__name__ == want["error"] and str(ei.value) == want["message"]
+        return
+    assert P.canonical_json(P.run_end2end(spec, OPTIONS[opt])) == want
