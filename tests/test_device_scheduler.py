@@ -131,7 +131,7 @@ def test_k1_sample_times_bitexact(case):
     assert per_rank == id_orders(case)
 
 
-def _random_problem(rng, B, dp, fan, quant):
+def _random_problem(rng, B, dp, fan, quant, with_dec=True, with_bac=True):
     from paper_2605_10501_b200.workload import Edge, ExecMode, Role, SectionSpec, StructuralParams, build_graph
 
     st = StructuralParams(64, 1, 1, 1, 64)
@@ -140,12 +140,12 @@ def _random_problem(rng, B, dp, fan, quant):
                      SectionSpec("dec", Role.AUXILIARY, ExecMode.FORWARD_BACKWARD, st)],
                     [Edge("enc", "llm"), Edge("llm", "dec")])
     img = rng.random(B) < 0.5
-    dec = rng.random(B) < 0.3
+    dec = (rng.random(B) < 0.3) & with_dec
     t = np.zeros((6, B))
     t[1] = rng.uniform(0.5, 3.0, B)
     t[4] = rng.uniform(0.0, 3.0, B)
     t[0] = np.where(img, rng.uniform(0.05, 2.0, B), 0.0)
-    t[5] = np.where(img, rng.uniform(0.0, 2.0, B), 0.0)
+    t[5] = np.where(img & with_bac, rng.uniform(0.0, 2.0, B), 0.0)
     t[2] = np.where(dec, rng.uniform(0.05, 1.0, B), 0.0)
     t[3] = np.where(dec, rng.uniform(0.0, 1.0, B), 0.0)
     if quant:
@@ -156,6 +156,39 @@ def _random_problem(rng, B, dp, fan, quant):
     cf = {"llm": SectionConfig(dp=dp), "enc": SectionConfig(dp=dp // fan, fanout=fan),
           "dec": SectionConfig(dp=dp)}
     return g, cf, np.ascontiguousarray(t), img, dec
+
+
+@pytest.mark.parametrize("B,dp,with_bac,quant", [
+    (1023, 1, True, True), (1023, 1, False, False), (2048, 4, True, False), (512, 2, False, True),
+    (64, 1, False, True), (64, 1, True, False)])
+def test_no_downstream_fast_path_vs_oracle(B, dp, with_bac, quant):
+    """Interleaved ranks without a downstream stage run K3's branch-free recurrence (eval_nodown):
+    orders, eval counts and metric bits == C oracle, with and without b_ac stages (the ub chain),
+    continuous and quantised (tie-heavy) times, up to the per-rank maximum."""
+    import torch
+
+    rng = np.random.default_rng(B + dp + 7 * with_bac)
+    g, cf, t, img, dec = _random_problem(rng, B, dp, 1, quant, with_dec=False, with_bac=with_bac)
+    tab = g.tables
+    masks = np.array([tab.mask_of(["enc"] if a else []) for a in img], dtype=np.uint32)
+    p = S.DevicePlanner(g, cf, "interleaved", max_batch=B)
+    p.times[: 6 * B].copy_(torch.from_numpy(t.reshape(-1)))
+    p.ids[:B].copy_(torch.arange(B, dtype=torch.int32))
+    p.act[:B].copy_(torch.from_numpy(masks.view(np.int32)))
+    p.plan_times(B)
+    p.raise_errors()
+    up, down = oracle.resolve(masks, t, tab.sub_owner, tab.side, tab.up_candidates, tab.down_candidates)
+    dps = [cf[s].dp for s in tab.section_ids]
+    fans = [cf[s].fanout for s in tab.section_ids]
+    want, ev = oracle.build_schedule(t, np.arange(B), up, down, len(dps), tab.critical, dps, fans, tab.neighbor,
+                                     tab.merge_order, "interleaved")
+    assert {k: v.tolist() for k, v in p.host_orders().items()} == want
+    assert int(p.evals.sum().item()) == ev
+    m = p.metrics.view(-1, 3).cpu().numpy()
+    for r in range(dp):
+        o = want[(tab.critical, r)]
+        assert tuple(float.hex(float(x)) for x in m[r]) == tuple(float.hex(x) for x in
+                                                                 oracle.rank_metrics(t, o, "interleaved"))
 
 
 @pytest.mark.parametrize("B,dp,fan,policy,quant", [
