@@ -124,6 +124,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // programmatic dependent launch: the prologue above overlapped the previous kernel's tail; every
+  // global access below waits for it.  The next GEMM may start its own prologue once all of this
+  // grid's CTAs are running.
+  pdl_trigger();
+  pdl_wait();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -394,9 +399,23 @@ int launch2(const CUtensorMap& ma, const CUtensorMap& mbm, const CUtensorMap& mc
     const char* e = getenv("MAESTRO_GEMM_L2HINT");
     return e ? atoi(e) : 1;
   }();
-  gemm2_kernel<BN2, A_MN, B_MN, EPI><<<2 * pairs, THREADS, SMEM, st>>>(ma, mbm, mc, mr, C, M, N, K, ldc, splits,
-                                                                        rope_pos, rope_cs, rope_cols, rope_hd, swiglu_out,
-                                                                        ld_swiglu, resid, ldr, l2hint);
+  // launched with programmatic stream serialization (MAESTRO_PDL=0 disables)
+  static const int pdl = [] {
+    const char* e = getenv("MAESTRO_PDL");
+    return e ? atoi(e) : 1;
+  }();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * pairs, 1, 1);
+  cfg.blockDim = dim3(THREADS, 1, 1);
+  cfg.dynamicSmemBytes = SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, gemm2_kernel<BN2, A_MN, B_MN, EPI>, ma, mbm, mc, mr, C, M, N, K, ldc, splits, rope_pos,
+                     rope_cs, rope_cols, rope_hd, swiglu_out, ld_swiglu, resid, ldr, l2hint);
   return launch_status();
 }
 
