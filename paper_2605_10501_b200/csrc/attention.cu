@@ -259,6 +259,8 @@ __global__ void __launch_bounds__(FwdCfg<DH, CG>::THREADS, 1)
                     const __grid_constant__ CUtensorMap map_v, const int32_t* __restrict__ cu,
                     const int2* __restrict__ tiles, const int* __restrict__ n_tiles, __nv_bfloat16* __restrict__ out,
                     int ldo, float* __restrict__ lse, int T, int H, int Hk, float scale2, int stagger_ns) {
+  pdl_wait();  // programmatic dependent launch (launch_pdl): previous kernel done
+  pdl_trigger();
   using C = FwdCfg<DH, CG>;
   constexpr int KVS = C::KVS, NOB = C::NOB, TB = C::TILE, CW = C::CW, SMX = C::SMX;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -687,6 +689,8 @@ __global__ void __launch_bounds__(FwdDecCfg<DH, NG>::THREADS, 1)
                         const int2* __restrict__ tiles, const int* __restrict__ n_tiles,
                         __nv_bfloat16* __restrict__ out, int ldo, float* __restrict__ lse, int T, int H, int Hk,
                         float scale2, int stagger_ns) {
+  pdl_wait();  // programmatic dependent launch (launch_pdl): previous kernel done
+  pdl_trigger();
   using C = FwdDecCfg<DH, NG>;
   constexpr int KVS = C::KVS, NOB = C::NOB, TB = C::TILE, CW = C::CW;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -1106,6 +1110,8 @@ __global__ void __launch_bounds__(FwdPPCfg<DH>::THREADS, 1)
                        const int2* __restrict__ tiles, const int* __restrict__ n_tiles,
                        __nv_bfloat16* __restrict__ out, int ldo, float* __restrict__ lse, int T, int H, int Hk,
                        float scale2) {
+  pdl_wait();  // programmatic dependent launch (launch_pdl): previous kernel done
+  pdl_trigger();
   using C = FwdPPCfg<DH>;
   constexpr int KVS = C::KVS, NOB = C::NOB, QB = C::QB, TB = C::TILE;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -1515,6 +1521,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
                     const float* __restrict__ lse, const float* __restrict__ Dvec,
                     __nv_bfloat16* __restrict__ dk, int lddk, __nv_bfloat16* __restrict__ dv, int lddv, int T, int H,
                     int Hk, float scale2, float scale, const float2* __restrict__ rope_cs) {
+  pdl_wait();  // programmatic dependent launch (launch_pdl): previous kernel done
+  pdl_trigger();
   using C = BwdCfg<DH>;
   constexpr int BQB = C::BQB, QH = C::QH, QDS = C::QD_STAGES, KVB = C::KVB;
   constexpr int KVT = C::KV_TILE, QT = C::Q_TILE;
@@ -1984,6 +1992,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
 template <int DH>
 __global__ void attn_bwd_pre_kernel(const __nv_bfloat16* __restrict__ o, int ldo, const __nv_bfloat16* __restrict__ dout,
                                     int lddo, float* __restrict__ Dvec, float* __restrict__ dq_acc, int T, int H) {
+  pdl_wait();  // programmatic dependent launch (launch_pdl): previous kernel done
+  pdl_trigger();
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (w >= T * H) return;
   const int t = w / H, h = w - t * H;
@@ -2008,6 +2018,8 @@ template <int DH>
 __global__ void attn_bwd_post_kernel(const float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dq, int lddq, int T,
                                      int H, float scale, const int32_t* __restrict__ pos,
                                      const float2* __restrict__ cs) {
+  pdl_wait();  // programmatic dependent launch (launch_pdl): previous kernel done
+  pdl_trigger();
   constexpr int GROUPS = DH / 16;  // groups of 8 pairs per head
   const long long n = (long long)T * H * GROUPS;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
@@ -2142,7 +2154,7 @@ MAESTRO_API int maestro_attn_fwd(const void* q, const void* k, const void* v, co
   {                                                                                                         \
     const int smem = FwdPPCfg<D>::TOTAL + 1024;                                                             \
     if (ensure_smem<attn_fwd_pp_kernel<D, CZ>>(smem)) return launch_status();                               \
-    attn_fwd_pp_kernel<D, CZ><<<grid, FwdPPCfg<D>::THREADS, smem, st>>>(mq, mk, mv, cu, t2, c2,              \
+    launch_pdl(attn_fwd_pp_kernel<D, CZ>, dim3(grid), dim3(FwdPPCfg<D>::THREADS), smem, st, mq, mk, mv, cu, t2, c2,              \
                                                                          (__nv_bfloat16*)out, ldo, lse, T, H, \
                                                                          Hk, scale2);                        \
   }
@@ -2168,7 +2180,7 @@ MAESTRO_API int maestro_attn_fwd(const void* q, const void* k, const void* v, co
     using CF = FwdCfg<D, G>;                                                                              \
     const int smem = CF::TOTAL + 1024;                                                                    \
     if (ensure_smem<attn_fwd_kernel<D, G, CZ>>(smem)) return launch_status();                             \
-    attn_fwd_kernel<D, G, CZ><<<grid, CF::THREADS, smem, st>>>(mq, mk, mv, cu, tiles, count,               \
+    launch_pdl(attn_fwd_kernel<D, G, CZ>, dim3(grid), dim3(CF::THREADS), smem, st, mq, mk, mv, cu, tiles, count,               \
                                                               (__nv_bfloat16*)out, ldo, lse, T, H, Hk, scale2,   \
                                                               stagger);                                         \
   }
@@ -2192,7 +2204,7 @@ MAESTRO_API int maestro_attn_fwd(const void* q, const void* k, const void* v, co
     using CF = FwdDecCfg<D, NGR>;                                                                            \
     const int smem = CF::TOTAL + 1024;                                                                       \
     if (ensure_smem<attn_fwd_dec_kernel<D, CZ, NGR>>(smem)) return launch_status();                          \
-    attn_fwd_dec_kernel<D, CZ, NGR><<<grid, CF::THREADS, smem, st>>>(mq, mk, mv, cu, tiles, count,            \
+    launch_pdl(attn_fwd_dec_kernel<D, CZ, NGR>, dim3(grid), dim3(CF::THREADS), smem, st, mq, mk, mv, cu, tiles, count,            \
                                                                       (__nv_bfloat16*)out, ldo, lse, T, H,     \
                                                                       Hk, scale2, dec_stagger);              \
   }
@@ -2246,10 +2258,10 @@ MAESTRO_API int maestro_attn_bwd(const void* dout, int32_t lddo, const void* q, 
   const long long warps = (long long)T * H;
   const unsigned pre_grid = (unsigned)((warps * 32 + 255) / 256);
   if (head_dim == 64)
-    attn_bwd_pre_kernel<64><<<pre_grid, 256, 0, st>>>((const __nv_bfloat16*)o, ldo, (const __nv_bfloat16*)dout, lddo,
+    launch_pdl(attn_bwd_pre_kernel<64>, dim3(pre_grid), dim3(256), 0, st, (const __nv_bfloat16*)o, ldo, (const __nv_bfloat16*)dout, lddo,
                                                      Dvec, dq_acc, T, H);
   else
-    attn_bwd_pre_kernel<128><<<pre_grid, 256, 0, st>>>((const __nv_bfloat16*)o, ldo, (const __nv_bfloat16*)dout, lddo,
+    launch_pdl(attn_bwd_pre_kernel<128>, dim3(pre_grid), dim3(256), 0, st, (const __nv_bfloat16*)o, ldo, (const __nv_bfloat16*)dout, lddo,
                                                       Dvec, dq_acc, T, H);
   const int bqb = head_dim == 64 ? 128 : 64;
   CUtensorMap mq, mk, mv, mdo, mdq;
@@ -2268,7 +2280,7 @@ MAESTRO_API int maestro_attn_bwd(const void* dout, int32_t lddo, const void* q, 
   {                                                                                                         \
     const int smem = BwdCfg<D>::TOTAL + 1024;                                                               \
     if (ensure_smem<attn_bwd_kernel<D, CZ>>(smem)) return launch_status();                                  \
-    attn_bwd_kernel<D, CZ><<<grid, BWD_THREADS, smem, st>>>(mq, mk, mv, mdo, mdq, cu, tiles, count, lse, Dvec, \
+    launch_pdl(attn_bwd_kernel<D, CZ>, dim3(grid), dim3(BWD_THREADS), smem, st, mq, mk, mv, mdo, mdq, cu, tiles, count, lse, Dvec, \
                                                            (__nv_bfloat16*)dk, lddk, (__nv_bfloat16*)dv, lddv, T, \
                                                            H, Hk, scale2, softmax_scale, (const float2*)rope_cs); \
   }
@@ -2281,10 +2293,10 @@ MAESTRO_API int maestro_attn_bwd(const void* dout, int32_t lddo, const void* q, 
   const long long ng = (long long)T * H * (head_dim / 16);
   const unsigned post_grid = (unsigned)((ng + 255) / 256 < 148 * 16 ? (ng + 255) / 256 : 148 * 16);
   if (head_dim == 64)
-    attn_bwd_post_kernel<64><<<post_grid, 256, 0, st>>>(dq_acc, (__nv_bfloat16*)dq, lddq, T, H, softmax_scale, rope_pos,
+    launch_pdl(attn_bwd_post_kernel<64>, dim3(post_grid), dim3(256), 0, st, dq_acc, (__nv_bfloat16*)dq, lddq, T, H, softmax_scale, rope_pos,
                                                        (const float2*)rope_cs);
   else
-    attn_bwd_post_kernel<128><<<post_grid, 256, 0, st>>>(dq_acc, (__nv_bfloat16*)dq, lddq, T, H, softmax_scale,
+    launch_pdl(attn_bwd_post_kernel<128>, dim3(post_grid), dim3(256), 0, st, dq_acc, (__nv_bfloat16*)dq, lddq, T, H, softmax_scale,
                                                         rope_pos, (const float2*)rope_cs);
   return launch_status();
 }

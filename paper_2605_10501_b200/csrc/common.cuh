@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "maestro_b200.h"
 
@@ -26,6 +27,39 @@ __device__ __forceinline__ void report(int64_t* err, uint32_t prio, int code, in
 }
 
 inline int launch_status() { return (int)cudaGetLastError(); }
+
+// ---- programmatic dependent launch (PDL)
+// A kernel launched with cudaLaunchAttributeProgrammaticStreamSerialization may start (and run its
+// prologue) while the previous kernel on the stream is still finishing; pdl_wait() blocks until
+// that kernel has completed and its writes are visible (a no-op for a normal launch).  pdl_trigger()
+// lets the next dependent kernel launch once every CTA of this one has executed it.  Every kernel
+// launched through launch_pdl() calls pdl_wait() before its first global-memory access.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+inline bool pdl_enabled() {  // MAESTRO_PDL=0: ordinary stream serialisation
+  static const int v = [] {
+    const char* e = getenv("MAESTRO_PDL");
+    return e ? atoi(e) : 1;
+  }();
+  return v != 0;
+}
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
 
 // Raise a kernel's dynamic shared-memory limit to `bytes` if needed (idempotent, cached
 // per kernel).  Returns nonzero on failure (the error stays queued for launch_status()).

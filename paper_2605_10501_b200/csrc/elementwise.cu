@@ -51,6 +51,8 @@ __global__ void __launch_bounds__(256) add_rmsnorm_fwd_kernel(const __nv_bfloat1
                                                               __nv_bfloat16* __restrict__ y,
                                                               const __nv_bfloat16* __restrict__ w,
                                                               float* __restrict__ rstd, int T, int d, float eps) {
+  pdl_wait();  // programmatic dependent launch (launch_pdl): previous kernel done
+  pdl_trigger();
   const int lane = threadIdx.x & 31;
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (row >= T) return;
@@ -110,6 +112,8 @@ __global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(const __nv_bfloat16* _
                                                           const float* __restrict__ rstd,
                                                           const __nv_bfloat16* dres, __nv_bfloat16* dx,
                                                           float* __restrict__ dw, int T, int d) {
+  pdl_wait();  // programmatic dependent launch (launch_pdl): previous kernel done
+  pdl_trigger();
   extern __shared__ float sdw[];
   for (int c = threadIdx.x; c < d; c += blockDim.x) sdw[c] = 0.f;
   __syncthreads();
@@ -221,6 +225,8 @@ __global__ void __launch_bounds__(256) rmsnorm_generic_fwd_kernel(const __nv_bfl
                                                               __nv_bfloat16* __restrict__ y,
                                                               const __nv_bfloat16* __restrict__ w,
                                                               float* __restrict__ rstd, int T, int d, float eps) {
+  pdl_wait();  // programmatic dependent launch (launch_pdl): previous kernel done
+  pdl_trigger();
   const int lane = threadIdx.x & 31;
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (row >= T) return;
@@ -261,6 +267,8 @@ __global__ void __launch_bounds__(256) rmsnorm_generic_bwd_kernel(const __nv_bfl
                                                           const float* __restrict__ rstd,
                                                           const __nv_bfloat16* dres, __nv_bfloat16* dx,
                                                           float* __restrict__ dw, int T, int d) {
+  pdl_wait();  // programmatic dependent launch (launch_pdl): previous kernel done
+  pdl_trigger();
   extern __shared__ float sdw[];
   for (int c = threadIdx.x; c < d; c += blockDim.x) sdw[c] = 0.f;
   __syncthreads();
@@ -309,6 +317,8 @@ __global__ void __launch_bounds__(256) rmsnorm_generic_bwd_kernel(const __nv_bfl
 // head row moves as 16-byte vectors and the position-tiled (cos, sin) table is read coalesced.
 __global__ void rope_kernel(__nv_bfloat16* __restrict__ qk, const int32_t* __restrict__ pos,
                             const float2* __restrict__ cs, int T, int n_heads, int dh, int ld, float sign) {
+  pdl_wait();  // programmatic dependent launch (launch_pdl): previous kernel done
+  pdl_trigger();
   const int half = dh / 2;
   const long long total = (long long)T * n_heads;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
@@ -348,6 +358,8 @@ __device__ __forceinline__ long long gate_col(long long f) { return (f >> 5) * 6
 
 __global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ out, int T,
                                   int F) {
+  pdl_wait();  // programmatic dependent launch (launch_pdl): previous kernel done
+  pdl_trigger();
   const long long nv = (long long)T * F / 8;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nv; i += (long long)gridDim.x * blockDim.x) {
     const long long e = i * 8;
@@ -364,6 +376,8 @@ __global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfl
 
 __global__ void swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ dout, const __nv_bfloat16* __restrict__ gu,
                                   __nv_bfloat16* __restrict__ dgu, int T, int F) {
+  pdl_wait();  // programmatic dependent launch (launch_pdl): previous kernel done
+  pdl_trigger();
   const long long nv = (long long)T * F / 8;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nv; i += (long long)gridDim.x * blockDim.x) {
     const long long e = i * 8;
@@ -387,6 +401,8 @@ __global__ void swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ dout, const 
 // ---------------------------------------------------------------- embedding
 __global__ void embed_fwd_kernel(const __nv_bfloat16* __restrict__ table, const int32_t* __restrict__ ids,
                                  __nv_bfloat16* __restrict__ out, int T, int d) {
+  pdl_wait();  // programmatic dependent launch (launch_pdl): previous kernel done
+  pdl_trigger();
   const int lane = threadIdx.x & 31;
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (row >= T || ids[row] < 0) return;  // negative id = placeholder row filled by a scatter
@@ -397,6 +413,8 @@ __global__ void embed_fwd_kernel(const __nv_bfloat16* __restrict__ table, const 
 
 __global__ void embed_bwd_kernel(const __nv_bfloat16* __restrict__ dout, const int32_t* __restrict__ ids,
                                  float* __restrict__ dtable, int T, int d) {
+  pdl_wait();  // programmatic dependent launch (launch_pdl): previous kernel done
+  pdl_trigger();
   const int lane = threadIdx.x & 31;
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (row >= T || ids[row] < 0) return;
@@ -454,7 +472,7 @@ using namespace mb;
 
 static int rmsnorm_generic_fwd(const void* x, const void* a, void* h, void* y, const void* w, float* rstd, int T,
                                int d, float eps, cudaStream_t st) {
-  rmsnorm_generic_fwd_kernel<<<(T + 7) / 8, 256, 0, st>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)a,
+  launch_pdl(rmsnorm_generic_fwd_kernel, dim3((T + 7) / 8), dim3(256), 0, st, (const __nv_bfloat16*)x, (const __nv_bfloat16*)a,
                                                           (__nv_bfloat16*)h, (__nv_bfloat16*)y,
                                                           (const __nv_bfloat16*)w, rstd, T, d, eps);
   return launch_status();
@@ -467,7 +485,7 @@ static int rmsnorm_generic_bwd(const void* dy, const void* h, const void* w, con
   // four CTAs per SM (a warp walks its rows with the full load latency per row, so rows in
   // flight per SM set the speed); 592 x d global atomics for dw at the end
   const int grid = (T + 7) / 8 < 148 * 4 ? (T + 7) / 8 : 148 * 4;
-  rmsnorm_generic_bwd_kernel<<<grid, 256, smem, st>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)h,
+  launch_pdl(rmsnorm_generic_bwd_kernel, dim3(grid), dim3(256), smem, st, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)h,
                                                       (const __nv_bfloat16*)w, rstd, (const __nv_bfloat16*)dres,
                                                       (__nv_bfloat16*)dx, dw, T, d);
   return launch_status();
@@ -476,7 +494,7 @@ static int rmsnorm_generic_bwd(const void* dy, const void* h, const void* w, con
 template <int NV>
 static int rmsnorm_fwd_launch(const void* x, const void* a, void* h, void* y, const void* w, float* rstd, int T, int d,
                               float eps, cudaStream_t st) {
-  add_rmsnorm_fwd_kernel<NV><<<(T + 7) / 8, 256, 0, st>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)a,
+  launch_pdl(add_rmsnorm_fwd_kernel<NV>, dim3((T + 7) / 8), dim3(256), 0, st, (const __nv_bfloat16*)x, (const __nv_bfloat16*)a,
                                                           (__nv_bfloat16*)h, (__nv_bfloat16*)y,
                                                           (const __nv_bfloat16*)w, rstd, T, d, eps);
   return launch_status();
@@ -488,7 +506,7 @@ static int rmsnorm_bwd_launch(const void* dy, const void* h, const void* w, cons
   const size_t smem = (size_t)d * sizeof(float);
   if (ensure_smem<rmsnorm_bwd_kernel<NV>>(smem)) return launch_status();
   const int grid = T / 8 < 148 ? (T + 7) / 8 : 148;  // one CTA per SM: 148 x d atomics for dw, ~7 rows per warp
-  rmsnorm_bwd_kernel<NV><<<grid, 256, smem, st>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)h,
+  launch_pdl(rmsnorm_bwd_kernel<NV>, dim3(grid), dim3(256), smem, st, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)h,
                                                   (const __nv_bfloat16*)w, rstd, (const __nv_bfloat16*)dres,
                                                   (__nv_bfloat16*)dx, dw, T, d);
   return launch_status();
@@ -534,7 +552,7 @@ MAESTRO_API int maestro_rope(void* qk, const int32_t* pos, const void* cos_sin, 
   if (T <= 0) return 0;
   if ((dh % 16) || (ld % 8)) return (int)cudaErrorInvalidValue;  // 16-byte row vectors
   const long long work = (long long)T * n_heads;
-  rope_kernel<<<grid_for(work, 256), 256, 0, (cudaStream_t)stream>>>(
+  launch_pdl(rope_kernel, dim3(grid_for(work, 256)), dim3(256), 0, (cudaStream_t)stream, 
       (__nv_bfloat16*)qk, pos, (const float2*)cos_sin, T, n_heads, dh, ld, backward ? -1.f : 1.f);
   return launch_status();
 }
@@ -548,7 +566,7 @@ MAESTRO_API int maestro_positions(const int32_t* cu, int32_t nseq, int32_t* pos,
 MAESTRO_API int maestro_swiglu_fwd(const void* gu, void* out, int32_t T, int32_t F, void* stream) {
   if (T <= 0) return 0;
   if (F % 32) return (int)cudaErrorInvalidValue;
-  swiglu_fwd_kernel<<<grid_for((long long)T * F / 8, 256), 256, 0, (cudaStream_t)stream>>>(
+  launch_pdl(swiglu_fwd_kernel, dim3(grid_for((long long)T * F / 8, 256)), dim3(256), 0, (cudaStream_t)stream, 
       (const __nv_bfloat16*)gu, (__nv_bfloat16*)out, T, F);
   return launch_status();
 }
@@ -556,7 +574,7 @@ MAESTRO_API int maestro_swiglu_fwd(const void* gu, void* out, int32_t T, int32_t
 MAESTRO_API int maestro_swiglu_bwd(const void* dout, const void* gu, void* dgu, int32_t T, int32_t F, void* stream) {
   if (T <= 0) return 0;
   if (F % 32) return (int)cudaErrorInvalidValue;
-  swiglu_bwd_kernel<<<grid_for((long long)T * F / 8, 256), 256, 0, (cudaStream_t)stream>>>(
+  launch_pdl(swiglu_bwd_kernel, dim3(grid_for((long long)T * F / 8, 256)), dim3(256), 0, (cudaStream_t)stream, 
       (const __nv_bfloat16*)dout, (const __nv_bfloat16*)gu, (__nv_bfloat16*)dgu, T, F);
   return launch_status();
 }
@@ -564,7 +582,7 @@ MAESTRO_API int maestro_swiglu_bwd(const void* dout, const void* gu, void* dgu, 
 MAESTRO_API int maestro_embed_fwd(const void* table, const int32_t* ids, void* out, int32_t T, int32_t d,
                                   void* stream) {
   if (T <= 0) return 0;
-  embed_fwd_kernel<<<(T + 7) / 8, 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)table, ids,
+  launch_pdl(embed_fwd_kernel, dim3((T + 7) / 8), dim3(256), 0, (cudaStream_t)stream, (const __nv_bfloat16*)table, ids,
                                                                   (__nv_bfloat16*)out, T, d);
   return launch_status();
 }
@@ -572,7 +590,7 @@ MAESTRO_API int maestro_embed_fwd(const void* table, const int32_t* ids, void* o
 MAESTRO_API int maestro_embed_bwd(const void* dout, const int32_t* ids, float* dtable, int32_t T, int32_t d,
                                   void* stream) {
   if (T <= 0) return 0;
-  embed_bwd_kernel<<<(T + 7) / 8, 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)dout, ids, dtable, T, d);
+  launch_pdl(embed_bwd_kernel, dim3((T + 7) / 8), dim3(256), 0, (cudaStream_t)stream, (const __nv_bfloat16*)dout, ids, dtable, T, d);
   return launch_status();
 }
 

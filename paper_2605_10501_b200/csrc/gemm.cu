@@ -400,22 +400,8 @@ int launch2(const CUtensorMap& ma, const CUtensorMap& mbm, const CUtensorMap& mc
     return e ? atoi(e) : 1;
   }();
   // launched with programmatic stream serialization (MAESTRO_PDL=0 disables)
-  static const int pdl = [] {
-    const char* e = getenv("MAESTRO_PDL");
-    return e ? atoi(e) : 1;
-  }();
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(2 * pairs, 1, 1);
-  cfg.blockDim = dim3(THREADS, 1, 1);
-  cfg.dynamicSmemBytes = SMEM;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, gemm2_kernel<BN2, A_MN, B_MN, EPI>, ma, mbm, mc, mr, C, M, N, K, ldc, splits, rope_pos,
-                     rope_cs, rope_cols, rope_hd, swiglu_out, ld_swiglu, resid, ldr, l2hint);
+  launch_pdl(gemm2_kernel<BN2, A_MN, B_MN, EPI>, dim3(2 * pairs), dim3(THREADS), SMEM, st, ma, mbm, mc, mr, C, M, N, K,
+             ldc, splits, rope_pos, rope_cs, rope_cols, rope_hd, swiglu_out, ld_swiglu, resid, ldr, l2hint);
   return launch_status();
 }
 

@@ -79,6 +79,8 @@ __global__ void __launch_bounds__(THREADS, MIN_BLOCKS) kd_loss_kernel(const __nv
                                                              float* __restrict__ loss,
                                                              int T, int V, int ldt, int lds, int ldd, float scale2,
                                                              float grad_scale, float inv_tau) {
+  pdl_wait();  // programmatic dependent launch (launch_pdl): previous kernel done
+  pdl_trigger();
   __shared__ Stat red[THREADS / 32];
   __shared__ Stat fin;
   const int nvec = V / 8;
@@ -246,6 +248,8 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(KDS_THREADS, KDS_CTA
     kd_loss_smem_kernel(const __nv_bfloat16* __restrict__ tl, const __nv_bfloat16* sl, __nv_bfloat16* ds,
                         float* __restrict__ loss, int T, int V, int VC, int ldt, int lds, int ldd, float scale2,
                         float grad_scale, float inv_tau) {
+  pdl_wait();  // programmatic dependent launch (launch_pdl): previous kernel done
+  pdl_trigger();
   using namespace sm100;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* sm = align_smem_1024(smem_raw);
@@ -438,6 +442,8 @@ template <int THREADS, int UNROLL>
 __global__ void __launch_bounds__(THREADS, 4) ce_loss_kernel(const __nv_bfloat16* sl, const int32_t* __restrict__ labels,
                                                              __nv_bfloat16* ds, float* __restrict__ loss, int T, int V,
                                                              int lds, int ldd, float grad_scale) {
+  pdl_wait();  // programmatic dependent launch (launch_pdl): previous kernel done
+  pdl_trigger();
   __shared__ float red_m[THREADS / 32], red_s[THREADS / 32];
   __shared__ float fin_m, fin_s;
   const int nvec = V / 8;
@@ -594,7 +600,7 @@ MAESTRO_API int maestro_kd_loss_fwd_bwd(const void* d_t, const void* d_s, void* 
     if (ensure_smem<kd_loss_smem_kernel<CC>>(KDS_SMEM)) return launch_status();                                \
     static const int max_cl = max_clusters(kd_loss_smem_kernel<CC>, CC, KDS_THREADS, KDS_SMEM);                \
     const int n_cl = T < max_cl ? T : max_cl;                                                                   \
-    kd_loss_smem_kernel<CC><<<n_cl * CC, KDS_THREADS, KDS_SMEM, (cudaStream_t)stream>>>(                        \
+    launch_pdl(kd_loss_smem_kernel<CC>, dim3(n_cl * CC), dim3(KDS_THREADS), KDS_SMEM, (cudaStream_t)stream,                         \
         (const __nv_bfloat16*)d_t, (const __nv_bfloat16*)d_s, (__nv_bfloat16*)d_ds, d_loss, T, V, VC, ldt, lds, \
         ldd, inv_tau * LOG2E, grad_scale, inv_tau);                                                             \
     return launch_status();                                                                                     \
@@ -617,13 +623,13 @@ MAESTRO_API int maestro_kd_loss_fwd_bwd(const void* d_t, const void* d_s, void* 
   const bool big = rows_env == 1;
   if (big) {
     const int grid = T < num_sms() ? T : num_sms();
-    kd_loss_kernel<512, 1, 8><<<grid, 512, 0, (cudaStream_t)stream>>>(
+    launch_pdl(kd_loss_kernel<512, 1, 8>, dim3(grid), dim3(512), 0, (cudaStream_t)stream, 
         (const __nv_bfloat16*)d_t, (const __nv_bfloat16*)d_s, (__nv_bfloat16*)d_ds, d_loss, T, V, ldt, lds, ldd,
         inv_tau * LOG2E, grad_scale, inv_tau);
     return launch_status();
   }
   const int grid = T < 148 * MB * 4 ? T : 148 * MB * 4;
-  kd_loss_kernel<TH, MB, UN><<<grid, TH, 0, (cudaStream_t)stream>>>(
+  launch_pdl(kd_loss_kernel<TH, MB, UN>, dim3(grid), dim3(TH), 0, (cudaStream_t)stream, 
       (const __nv_bfloat16*)d_t, (const __nv_bfloat16*)d_s, (__nv_bfloat16*)d_ds, d_loss, T, V, ldt, lds, ldd,
       inv_tau * LOG2E, grad_scale, inv_tau);
   return launch_status();
@@ -636,7 +642,7 @@ MAESTRO_API int maestro_ce_loss_fwd_bwd(const void* d_s, const int32_t* d_labels
   if (T <= 0) return 0;
   if (V % 8 || lds % 8 || ldd % 8) return (int)cudaErrorInvalidValue;
   const int grid = T < num_sms() * 4 * 4 ? T : num_sms() * 4 * 4;
-  ce_loss_kernel<256, 4><<<grid, 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)d_s, d_labels,
+  launch_pdl(ce_loss_kernel<256, 4>, dim3(grid), dim3(256), 0, (cudaStream_t)stream, (const __nv_bfloat16*)d_s, d_labels,
                                                                  (__nv_bfloat16*)d_ds, d_loss, T, V, lds, ldd,
                                                                  grad_scale);
   return launch_status();

@@ -76,14 +76,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
-// ---------------------------------------------------------------- programmatic dependent launch
-// A kernel launched with cudaLaunchAttributeProgrammaticStreamSerialization may start (and run its
-// prologue) while the previous kernel on the stream is still finishing; pdl_wait() blocks until
-// that kernel has completed and its writes are visible (a no-op for a normal launch).  pdl_trigger()
-// lets the next dependent kernel launch as soon as every CTA of this one has executed it.
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-
 // ---------------------------------------------------------------- clusters
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;

@@ -1,13 +1,17 @@
 #!/bin/bash
 # programmatic dependent launch for the GEMM: parity, then A/B (same box, interleaved)
-timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pdl_tests.log 2>&1; echo "rc=$?" >> gpurun_out/pdl_tests.log
-if grep -q "rc=0" gpurun_out/pdl_tests.log; then
+timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pdl2_tests.log 2>&1; echo "rc=$?" >> gpurun_out/pdl2_tests.log
+if grep -q "rc=0" gpurun_out/pdl2_tests.log; then
 for rep in 1 2; do
   for v in 1 0; do
-    echo "{\"pdl\": $v, \"rep\": $rep}" >> gpurun_out/pdl.jsonl
-    MAESTRO_PDL=$v timeout 400 python bench.py --steps 10 --warmup 3 --no-cpu-baseline 2>/dev/null | tail -1 | cut -c1-300 >> gpurun_out/pdl.jsonl
-    MAESTRO_PDL=$v timeout 400 python bench.py --workload vlm --steps 20 --warmup 5 --no-cpu-baseline 2>/dev/null | tail -1 | cut -c1-300 >> gpurun_out/pdl.jsonl
+    echo "{\"pdl\": $v, \"rep\": $rep}" >> gpurun_out/pdl2.jsonl
+    MAESTRO_PDL=$v timeout 400 python bench.py --steps 10 --warmup 3 --no-cpu-baseline 2>/dev/null | tail -1 | cut -c1-300 >> gpurun_out/pdl2.jsonl
+    MAESTRO_PDL=$v timeout 400 python bench.py --workload vlm --steps 20 --warmup 5 --no-cpu-baseline 2>/dev/null | tail -1 | cut -c1-300 >> gpurun_out/pdl2.jsonl
   done
 done
 fi
 echo done
+for v in 1 0; do
+  echo "{\"pdl\": $v, \"w\": \"kd8b\"}" >> gpurun_out/pdl2.jsonl
+  MAESTRO_PDL=$v timeout 900 python bench.py --workload kd8b --steps 3 --warmup 2 --no-cpu-baseline 2>/dev/null | tail -1 | cut -c1-300 >> gpurun_out/pdl2.jsonl
+done
