@@ -42,6 +42,8 @@ constexpr float LN2_F = 0.6931471805599453f;
 template <int QT = BQ>
 __global__ void attn_tiles_kernel(const int32_t* __restrict__ cu, int nseq, int2* __restrict__ tiles,
                                   int* __restrict__ count) {
+  pdl_wait();  // programmatic dependent launch (launch_pdl): previous kernel done
+  pdl_trigger();
   __shared__ int s_max, s_n;
   if (threadIdx.x == 0) {
     s_max = 0;
@@ -2062,6 +2064,8 @@ __global__ void attn_bwd_post_kernel(const float* __restrict__ dq_acc, __nv_bflo
 // a KV tile shrinks with kv0, so ascending kv0 puts the heaviest tiles first.
 __global__ void attn_kv_tiles_kernel(const int32_t* __restrict__ cu, int nseq, int2* __restrict__ tiles,
                                      int* __restrict__ count) {
+  pdl_wait();  // programmatic dependent launch (launch_pdl): previous kernel done
+  pdl_trigger();
   __shared__ int s_max, s_n;
   if (threadIdx.x == 0) {
     s_max = 0;
@@ -2107,10 +2111,10 @@ MAESTRO_API int maestro_attn_plan(const int32_t* cu, int32_t nseq, int32_t T, vo
   const int max_tiles = (T + BQ - 1) / BQ + nseq;
   int2* fw = reinterpret_cast<int2*>(plan);
   int2* bw = reinterpret_cast<int2*>(reinterpret_cast<unsigned char*>(plan) + maestro_attn_workspace(T, nseq));
-  attn_tiles_kernel<<<1, 1024, 0, st>>>(cu, nseq, fw, reinterpret_cast<int*>(fw + max_tiles));
-  attn_kv_tiles_kernel<<<1, 1024, 0, st>>>(cu, nseq, bw, reinterpret_cast<int*>(bw + max_tiles));
+  launch_pdl(attn_tiles_kernel<>, dim3(1), dim3(1024), 0, st, cu, nseq, fw, reinterpret_cast<int*>(fw + max_tiles));
+  launch_pdl(attn_kv_tiles_kernel, dim3(1), dim3(1024), 0, st, cu, nseq, bw, reinterpret_cast<int*>(bw + max_tiles));
   int2* pw = reinterpret_cast<int2*>(reinterpret_cast<unsigned char*>(plan) + 2 * maestro_attn_workspace(T, nseq));
-  attn_tiles_kernel<2 * BQ><<<1, 1024, 0, st>>>(cu, nseq, pw, reinterpret_cast<int*>(pw + max_tiles));
+  launch_pdl(attn_tiles_kernel<2 * BQ>, dim3(1), dim3(1024), 0, st, cu, nseq, pw, reinterpret_cast<int*>(pw + max_tiles));
   return launch_status();
 }
 
@@ -2141,7 +2145,7 @@ MAESTRO_API int maestro_attn_fwd(const void* q, const void* k, const void* v, co
                                                          2 * maestro_attn_workspace(T, nseq))
                                : reinterpret_cast<int2*>(workspace);
     int* c2 = reinterpret_cast<int*>(t2 + max_tiles);
-    if (plan == nullptr) attn_tiles_kernel<2 * BQ><<<1, 1024, 0, st>>>(cu, nseq, t2, c2);
+    if (plan == nullptr) launch_pdl(attn_tiles_kernel<2 * BQ>, dim3(1), dim3(1024), 0, st, cu, nseq, t2, c2);
     CUtensorMap mq, mk, mv;
     bool ok = make_map_2d(&mq, q, (uint64_t)H * head_dim, T, ldq, 64, 128);
     ok = ok && make_map_2d(&mk, k, (uint64_t)Hk * head_dim, T, ldk, 64, 128);
@@ -2166,7 +2170,7 @@ MAESTRO_API int maestro_attn_fwd(const void* q, const void* k, const void* v, co
 #undef MB_ATTN_PP
     return launch_status();
   }
-  if (plan == nullptr) attn_tiles_kernel<<<1, 1024, 0, st>>>(cu, nseq, tiles, count);
+  if (plan == nullptr) launch_pdl(attn_tiles_kernel<>, dim3(1), dim3(1024), 0, st, cu, nseq, tiles, count);
   CUtensorMap mq, mk, mv;
   bool ok = make_map_2d(&mq, q, (uint64_t)H * head_dim, T, ldq, 64, 128);
   ok = ok && make_map_2d(&mk, k, (uint64_t)Hk * head_dim, T, ldk, 64, 128);
@@ -2254,7 +2258,7 @@ MAESTRO_API int maestro_attn_bwd(const void* dout, int32_t lddo, const void* q, 
   float* Dvec = reinterpret_cast<float*>(w + off_d);
   const size_t off_acc = (off_d + (size_t)4 * H * T + 255) / 256 * 256;
   float* dq_acc = reinterpret_cast<float*>(w + off_acc);
-  if (plan == nullptr) attn_kv_tiles_kernel<<<1, 1024, 0, st>>>(cu, nseq, tiles, count);
+  if (plan == nullptr) launch_pdl(attn_kv_tiles_kernel, dim3(1), dim3(1024), 0, st, cu, nseq, tiles, count);
   const long long warps = (long long)T * H;
   const unsigned pre_grid = (unsigned)((warps * 32 + 255) / 256);
   if (head_dim == 64)

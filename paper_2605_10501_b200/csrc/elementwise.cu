@@ -345,6 +345,8 @@ __global__ void rope_kernel(__nv_bfloat16* __restrict__ qk, const int32_t* __res
 
 // positions inside each packed sequence: pos[t] = t - cu[j] for cu[j] <= t < cu[j+1]
 __global__ void positions_kernel(const int32_t* __restrict__ cu, int nseq, int32_t* __restrict__ pos) {
+  pdl_wait();  // programmatic dependent launch (launch_pdl): previous kernel done
+  pdl_trigger();
   const int j = blockIdx.x;
   if (j >= nseq) return;
   const int a = cu[j], b = cu[j + 1];
@@ -432,6 +434,8 @@ __global__ void embed_bwd_kernel(const __nv_bfloat16* __restrict__ dout, const i
 __global__ void adamw_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
                              float* __restrict__ v, __nv_bfloat16* __restrict__ pb, long long n, float lr, float b1,
                              float b2, float eps, float wd, float bc1, float bc2, float gscale) {
+  pdl_wait();  // programmatic dependent launch (launch_pdl): previous kernel done
+  pdl_trigger();
   const long long n4 = n / 4;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
     float4 pp = reinterpret_cast<float4*>(p)[i];
@@ -559,7 +563,7 @@ MAESTRO_API int maestro_rope(void* qk, const int32_t* pos, const void* cos_sin, 
 
 MAESTRO_API int maestro_positions(const int32_t* cu, int32_t nseq, int32_t* pos, void* stream) {
   if (nseq <= 0) return 0;
-  positions_kernel<<<nseq, 256, 0, (cudaStream_t)stream>>>(cu, nseq, pos);
+  launch_pdl(positions_kernel, dim3(nseq), dim3(256), 0, (cudaStream_t)stream, cu, nseq, pos);
   return launch_status();
 }
 
@@ -618,6 +622,8 @@ __device__ __forceinline__ void transpose_tile(const __nv_bfloat16* __restrict__
 
 __global__ void transpose_bf16_kernel(const __nv_bfloat16* __restrict__ src, __nv_bfloat16* __restrict__ dst,
                                       int rows, int cols, int ld_src, int ld_dst) {
+  pdl_wait();  // programmatic dependent launch (launch_pdl): previous kernel done
+  pdl_trigger();
   __shared__ __nv_bfloat16 tile[64][64 + 8];
   transpose_tile(src, dst, rows, cols, ld_src, ld_dst, blockIdx.y * 64, blockIdx.x * 64, tile);
 }
@@ -626,6 +632,8 @@ __global__ void transpose_bf16_kernel(const __nv_bfloat16* __restrict__ src, __n
 // ~60 small matrices per section, launch-bound one by one).  desc[i] = {src, dst, rows, cols,
 // ld_src, ld_dst, first tile, tiles along cols}; block b handles tile b of the concatenation.
 __global__ void transpose_bf16_batched_kernel(const int64_t* __restrict__ desc, int n) {
+  pdl_wait();  // programmatic dependent launch (launch_pdl): previous kernel done
+  pdl_trigger();
   __shared__ __nv_bfloat16 tile[64][64 + 8];
   __shared__ int s_i;
   const int b = blockIdx.x;
@@ -649,14 +657,14 @@ MAESTRO_API int maestro_transpose_bf16(const void* src, void* dst, int32_t rows,
   if (rows <= 0 || cols <= 0) return 0;
   if ((rows % 8) || (cols % 8) || (ld_src % 8) || (ld_dst % 8)) return (int)cudaErrorInvalidValue;
   dim3 grid((cols + 63) / 64, (rows + 63) / 64);
-  transpose_bf16_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)src, (__nv_bfloat16*)dst, rows,
+  launch_pdl(transpose_bf16_kernel, dim3(grid), dim3(256), 0, (cudaStream_t)stream, (const __nv_bfloat16*)src, (__nv_bfloat16*)dst, rows,
                                                                  cols, ld_src, ld_dst);
   return launch_status();
 }
 
 MAESTRO_API int maestro_transpose_bf16_batched(const int64_t* desc, int32_t n, int32_t total_tiles, void* stream) {
   if (n <= 0 || total_tiles <= 0) return 0;
-  transpose_bf16_batched_kernel<<<total_tiles, 256, 0, (cudaStream_t)stream>>>(desc, n);
+  launch_pdl(transpose_bf16_batched_kernel, dim3(total_tiles), dim3(256), 0, (cudaStream_t)stream, desc, n);
   return launch_status();
 }
 
@@ -665,7 +673,7 @@ MAESTRO_API int maestro_adamw(float* p, const float* g, float* m, float* v, void
   if (n <= 0) return 0;
   if (n % 4) return (int)cudaErrorInvalidValue;
   const float bc1 = 1.f - powf(b1, (float)step), bc2 = 1.f - powf(b2, (float)step);
-  adamw_kernel<<<grid_for(n / 4, 256), 256, 0, (cudaStream_t)stream>>>(p, g, m, v, (__nv_bfloat16*)pb, n, lr, b1, b2,
+  launch_pdl(adamw_kernel, dim3(grid_for(n / 4, 256)), dim3(256), 0, (cudaStream_t)stream, p, g, m, v, (__nv_bfloat16*)pb, n, lr, b1, b2,
                                                                         eps, wd, bc1, bc2, gscale);
   return launch_status();
 }

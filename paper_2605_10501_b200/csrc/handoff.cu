@@ -59,6 +59,8 @@ __global__ void __launch_bounds__(1024) handoff_scan_kernel(const int32_t* __res
                                                             const int32_t* __restrict__ rows, int B,
                                                             int32_t* __restrict__ up_off, int32_t* __restrict__ pos,
                                                             int64_t* __restrict__ err) {
+  pdl_wait();  // programmatic dependent launch (launch_pdl): previous kernel done
+  pdl_trigger();
   __shared__ int ws[33];
   for (int i = threadIdx.x; i < B; i += blockDim.x) up_off[i] = -1;
   __syncthreads();
@@ -94,6 +96,8 @@ __global__ void handoff_fill_kernel(const int32_t* __restrict__ crit, int n, con
                                     int mbs, const int32_t* __restrict__ rows, const int32_t* __restrict__ dst_off,
                                     const int32_t* __restrict__ up_off, const int32_t* __restrict__ pos,
                                     int32_t* __restrict__ src_rows, int32_t* __restrict__ dst_rows) {
+  pdl_wait();  // programmatic dependent launch (launch_pdl): previous kernel done
+  pdl_trigger();
   for (int k = blockIdx.x; k < n; k += gridDim.x) {
     const int i = crit[k];
     const int nr = rows[i];
@@ -119,9 +123,9 @@ MAESTRO_API int maestro_handoff_index(const int32_t* d_up_order, int32_t nu, con
                                       int32_t* d_src_rows, int32_t* d_dst_rows, int64_t* d_err, void* stream) {
   if (n < 0 || nu < 0 || B <= 0 || mbs <= 0) return (int)cudaErrorInvalidValue;
   cudaStream_t st = (cudaStream_t)stream;
-  handoff_scan_kernel<<<1, 1024, 0, st>>>(d_up_order, nu, d_crit_order, n, d_rows, B, d_scratch, d_pos, d_err);
+  launch_pdl(handoff_scan_kernel, dim3(1), dim3(1024), 0, st, d_up_order, nu, d_crit_order, n, d_rows, B, d_scratch, d_pos, d_err);
   if (n > 0)
-    handoff_fill_kernel<<<n < 1024 ? n : 1024, 128, 0, st>>>(d_crit_order, n, d_tok_off, mbs, d_rows, d_dst_off,
+    launch_pdl(handoff_fill_kernel, dim3(n < 1024 ? n : 1024), dim3(128), 0, st, d_crit_order, n, d_tok_off, mbs, d_rows, d_dst_off,
                                                              d_scratch, d_pos, d_src_rows, d_dst_rows);
   return launch_status();
 }

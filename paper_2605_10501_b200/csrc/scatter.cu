@@ -20,6 +20,8 @@ __global__ void __launch_bounds__(256) scatter_rows_kernel(const uint4* __restri
                                                            const int32_t* __restrict__ dst_row, int n_rows,
                                                            int vec_per_row, const int32_t* __restrict__ pos, int k0,
                                                            int k1) {
+  pdl_wait();  // programmatic dependent launch (launch_pdl): previous kernel done
+  pdl_trigger();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   int lo = 0, hi = n_rows;
@@ -70,6 +72,8 @@ __global__ void __launch_bounds__(256) gather_rows_bwd_kernel(const __nv_bfloat1
                                                               const int32_t* __restrict__ seg,
                                                               const int32_t* __restrict__ seg_dst, int n_src,
                                                               int d) {
+  pdl_wait();  // programmatic dependent launch (launch_pdl): previous kernel done
+  pdl_trigger();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= n_src) return;
@@ -119,7 +123,7 @@ MAESTRO_API int maestro_scatter_rows_fwd(const void* d_src, void* d_dst, const i
   if (d % 8) return (int)cudaErrorInvalidValue;
   const int warps = (n_rows + kRowsPerWarp - 1) / kRowsPerWarp;
   const int blocks = (warps * 32 + 255) / 256;
-  scatter_rows_kernel<false><<<blocks, 256, 0, (cudaStream_t)stream>>>((const uint4*)d_src, (uint4*)d_dst, d_src_row,
+  launch_pdl(scatter_rows_kernel<false>, dim3(blocks), dim3(256), 0, (cudaStream_t)stream, (const uint4*)d_src, (uint4*)d_dst, d_src_row,
                                                                        d_dst_row, n_rows, d / 8, nullptr, 0, 0);
   return launch_status();
 }
@@ -135,10 +139,10 @@ MAESTRO_API int maestro_scatter_rows_range(const void* d_src, void* d_dst, const
   const int warps = (max_rows + kRowsPerWarp - 1) / kRowsPerWarp;
   const int blocks = (warps * 32 + 255) / 256;
   if (accumulate)
-    scatter_rows_kernel<true><<<blocks, 256, 0, (cudaStream_t)stream>>>(
+    launch_pdl(scatter_rows_kernel<true>, dim3(blocks), dim3(256), 0, (cudaStream_t)stream, 
         (const uint4*)d_src, (uint4*)d_dst, d_src_row, d_dst_row, max_rows, d / 8, d_pos, k0, k1);
   else
-    scatter_rows_kernel<false><<<blocks, 256, 0, (cudaStream_t)stream>>>(
+    launch_pdl(scatter_rows_kernel<false>, dim3(blocks), dim3(256), 0, (cudaStream_t)stream, 
         (const uint4*)d_src, (uint4*)d_dst, d_src_row, d_dst_row, max_rows, d / 8, d_pos, k0, k1);
   return launch_status();
 }
@@ -148,7 +152,7 @@ MAESTRO_API int maestro_gather_rows_bwd(const void* d_ddst, void* d_dsrc, const 
   if (n_src_rows <= 0) return 0;
   if (d % 8) return (int)cudaErrorInvalidValue;
   const int blocks = (n_src_rows * 32 + 255) / 256;
-  gather_rows_bwd_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+  launch_pdl(gather_rows_bwd_kernel, dim3(blocks), dim3(256), 0, (cudaStream_t)stream, 
       (const __nv_bfloat16*)d_ddst, (__nv_bfloat16*)d_dsrc, d_seg, d_seg_dst, n_src_rows, d);
   return launch_status();
 }
