@@ -225,6 +225,10 @@ int maestro_fp64_probe(double* out, int32_t mode, int32_t iters, int32_t blocks,
  * that a static persistent tile schedule never waits on a CTA that cannot become resident. */
 int maestro_set_sm_budget(int32_t n_sms);
 
+/* Programmatic dependent launch of the step kernels (GEMM, attention, losses, norms, ...): 1 on
+ * (default; MAESTRO_PDL=0 starts it off), 0 off.  Returns the previous setting. */
+int maestro_set_pdl(int32_t on);
+
 /* One-sided NVLink handoff (mq.PeerTransport): receiver-owned slot ring + per-slot flags exported
  * by CUDA IPC; sends are copy-engine copies into the peer slot followed by a stream memory write of
  * the slot flag, receives are stream waits on the flag -- no kernel spins on another GPU. */

@@ -98,6 +98,13 @@ def extra_symbols(names):
     return L
 
 
+def set_pdl(on: bool) -> bool:
+    """Programmatic dependent launch of the step kernels on/off (maestro_set_pdl); returns the
+    previous setting."""
+    L = extra_symbols({"maestro_set_pdl": ([ctypes.c_int32], ctypes.c_int)})
+    return bool(L.maestro_set_pdl(1 if on else 0))
+
+
 def reserve_sms_for_comm(default: int = 16) -> int:
     """Cap the persistent kernels' grids below the SM count so NCCL point-to-point kernels that
     spin while waiting on another GPU never hold an SM a persistent CTA needs

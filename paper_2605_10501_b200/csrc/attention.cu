@@ -261,8 +261,6 @@ __global__ void __launch_bounds__(FwdCfg<DH, CG>::THREADS, 1)
                     const __grid_constant__ CUtensorMap map_v, const int32_t* __restrict__ cu,
                     const int2* __restrict__ tiles, const int* __restrict__ n_tiles, __nv_bfloat16* __restrict__ out,
                     int ldo, float* __restrict__ lse, int T, int H, int Hk, float scale2, int stagger_ns) {
-  pdl_wait();  // programmatic dependent launch (launch_pdl): previous kernel done
-  pdl_trigger();
   using C = FwdCfg<DH, CG>;
   constexpr int KVS = C::KVS, NOB = C::NOB, TB = C::TILE, CW = C::CW, SMX = C::SMX;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -283,7 +281,6 @@ __global__ void __launch_bounds__(FwdCfg<DH, CG>::THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
   const Bars BR{bar, smem_u32(bar)};
 
-  const int n_items = *n_tiles * H;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
     tma_prefetch(&map_q);
@@ -312,6 +309,11 @@ __global__ void __launch_bounds__(FwdCfg<DH, CG>::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // programmatic dependent launch: the prologue above (barriers, TMEM, tensor-map prefetch)
+  // overlapped the previous kernel; global memory (the tile list included) only from here
+  pdl_trigger();
+  pdl_wait();
+  const int n_items = *n_tiles * H;
   if constexpr (CG == 4 && ATTN_SETMAXNREG) {  // registers from the TMA/MMA warpgroup to the 16 softmax warps
     if (warp < 4)
       asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(C::REG_LO));
@@ -691,8 +693,6 @@ __global__ void __launch_bounds__(FwdDecCfg<DH, NG>::THREADS, 1)
                         const int2* __restrict__ tiles, const int* __restrict__ n_tiles,
                         __nv_bfloat16* __restrict__ out, int ldo, float* __restrict__ lse, int T, int H, int Hk,
                         float scale2, int stagger_ns) {
-  pdl_wait();  // programmatic dependent launch (launch_pdl): previous kernel done
-  pdl_trigger();
   using C = FwdDecCfg<DH, NG>;
   constexpr int KVS = C::KVS, NOB = C::NOB, TB = C::TILE, CW = C::CW;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -714,7 +714,6 @@ __global__ void __launch_bounds__(FwdDecCfg<DH, NG>::THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gb + 12 * NG);
   int* cnt = reinterpret_cast<int*>(sm + C::CNT);
 
-  const int n_items = *n_tiles * H;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
     tma_prefetch(&map_q);
@@ -747,6 +746,11 @@ __global__ void __launch_bounds__(FwdDecCfg<DH, NG>::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // programmatic dependent launch: the prologue above (barriers, TMEM, tensor-map prefetch)
+  // overlapped the previous kernel; global memory (the tile list included) only from here
+  pdl_trigger();
+  pdl_wait();
+  const int n_items = *n_tiles * H;
   if constexpr (C::REG_SPLIT) {
     if (warp < C::SW0)
       asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(C::REG_PROD));
@@ -1112,8 +1116,6 @@ __global__ void __launch_bounds__(FwdPPCfg<DH>::THREADS, 1)
                        const int2* __restrict__ tiles, const int* __restrict__ n_tiles,
                        __nv_bfloat16* __restrict__ out, int ldo, float* __restrict__ lse, int T, int H, int Hk,
                        float scale2) {
-  pdl_wait();  // programmatic dependent launch (launch_pdl): previous kernel done
-  pdl_trigger();
   using C = FwdPPCfg<DH>;
   constexpr int KVS = C::KVS, NOB = C::NOB, QB = C::QB, TB = C::TILE;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -1131,7 +1133,6 @@ __global__ void __launch_bounds__(FwdPPCfg<DH>::THREADS, 1)
   uint64_t* o_empty = o_full + 4;    // [2 tiles][2 sets]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 4);
 
-  const int n_items = *n_tiles * H;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
     tma_prefetch(&map_q);
@@ -1160,6 +1161,11 @@ __global__ void __launch_bounds__(FwdPPCfg<DH>::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // programmatic dependent launch: the prologue above (barriers, TMEM, tensor-map prefetch)
+  // overlapped the previous kernel; global memory (the tile list included) only from here
+  pdl_trigger();
+  pdl_wait();
+  const int n_items = *n_tiles * H;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -1523,8 +1529,6 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
                     const float* __restrict__ lse, const float* __restrict__ Dvec,
                     __nv_bfloat16* __restrict__ dk, int lddk, __nv_bfloat16* __restrict__ dv, int lddv, int T, int H,
                     int Hk, float scale2, float scale, const float2* __restrict__ rope_cs) {
-  pdl_wait();  // programmatic dependent launch (launch_pdl): previous kernel done
-  pdl_trigger();
   using C = BwdCfg<DH>;
   constexpr int BQB = C::BQB, QH = C::QH, QDS = C::QD_STAGES, KVB = C::KVB;
   constexpr int KVT = C::KV_TILE, QT = C::Q_TILE;
@@ -1553,7 +1557,6 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   float* s_D = reinterpret_cast<float*>(sm + C::DD);
 
   const int G = H / Hk;
-  const int n_items = *n_tiles * Hk;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
@@ -1587,6 +1590,11 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // programmatic dependent launch: the prologue above (barriers, TMEM, tensor-map prefetch)
+  // overlapped the previous kernel; global memory (the tile list included) only from here
+  pdl_trigger();
+  pdl_wait();
+  const int n_items = *n_tiles * Hk;
 
   if (warp == 0) {
     if (lane == 0) {

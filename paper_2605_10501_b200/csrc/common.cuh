@@ -37,13 +37,14 @@ inline int launch_status() { return (int)cudaGetLastError(); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-inline bool pdl_enabled() {  // MAESTRO_PDL=0: ordinary stream serialisation
-  static const int v = [] {
+inline int& pdl_flag() {  // MAESTRO_PDL=0 or maestro_set_pdl(0): ordinary stream serialisation
+  static int v = [] {
     const char* e = getenv("MAESTRO_PDL");
     return e ? atoi(e) : 1;
   }();
-  return v != 0;
+  return v;
 }
+inline bool pdl_enabled() { return pdl_flag() != 0; }
 
 template <typename... KArgs, typename... Args>
 inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,

@@ -112,3 +112,12 @@ MAESTRO_API int maestro_set_sm_budget(int32_t n_sms) {
   sm_budget() = n_sms;
   return 0;
 }
+
+// Programmatic dependent launch of the step kernels on (1) or off (0); returns the previous
+// setting.  Executors that run several sections' streams concurrently turn it off: a dependent
+// kernel's early CTAs hold SMs the other streams could use (cfg 3/4: -1 % with it on).
+MAESTRO_API int maestro_set_pdl(int32_t on) {
+  const int prev = pdl_flag();
+  pdl_flag() = on ? 1 : 0;
+  return prev;
+}

@@ -280,6 +280,16 @@ class SectionGraphExecutor:
 
     # ---------------------------------------------------------------- one step
     def step(self, gb: GraphBatch, want_loss: bool = True) -> StepStats:
+        """One iteration; programmatic dependent launch is off while it enqueues (the sections'
+        streams run concurrently and early dependent CTAs would hold SMs the other streams use:
+        cfg 3/4 measured -1 % with it, r02_pdl_section_ab.jsonl)."""
+        prev = N.set_pdl(False)
+        try:
+            return self._step(gb, want_loss)
+        finally:
+            N.set_pdl(prev)
+
+    def _step(self, gb: GraphBatch, want_loss: bool = True) -> StepStats:
         dev, B = self.device, gb.B
         main = torch.cuda.current_stream(dev)
         t0 = torch.cuda.Event(enable_timing=True)
