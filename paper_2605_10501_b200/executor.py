@@ -147,6 +147,13 @@ def handoff_mode() -> str:
     return mode
 
 
+def _prio_section() -> str:
+    """MAESTRO_STREAM_PRIORITY=teacher|student|none: which co-resident section's stream gets the
+    higher CUDA scheduling priority (its CTAs dispatched first when both have work).  Measured on
+    cfg 2: student first -3 %, teacher first -0.7 % (r02_stream_priority_ab.jsonl); default none."""
+    return os.environ.get("MAESTRO_STREAM_PRIORITY", "none")
+
+
 def _dist():
     import torch.distributed as dist
 
@@ -196,14 +203,14 @@ class KDExecutor:
         if self.t_rank is not None:
             tp = FlatParams(self.tshape.param_shapes(), dev, trainable=False, seed=seed + 1)
             self.teacher = Transformer(self.tshape, tp, dev, max_pos=seq)
-            self.t_stream = torch.cuda.Stream(device=dev)
+            self.t_stream = torch.cuda.Stream(device=dev, priority=-1 if _prio_section() == "teacher" else 0)
         if self.s_rank is not None:
             sp = FlatParams(self.sshape.param_shapes(), dev, trainable=True, seed=seed + 2)
             self.student = Transformer(self.sshape, sp, dev, max_pos=seq)
             # colocated teacher output layer (workload.colocate_output_layer): frozen, lives here
             g = torch.Generator(device=dev).manual_seed(seed + 3)
             self.t_head = (torch.randn(self.tshape.vocab, self.tshape.d, device=dev, generator=g) * 0.02).bfloat16()
-            self.s_stream = torch.cuda.Stream(device=dev)
+            self.s_stream = torch.cuda.Stream(device=dev, priority=-1 if _prio_section() == "student" else 0)
         self.lr = lr
         # --- device planner (every rank computes the same deterministic schedule)
         self.planner = DevicePlanner(self.graph, cfg, policy, max_batch=self.batch, device=dev)
