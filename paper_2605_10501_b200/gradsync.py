@@ -15,11 +15,29 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 
 import torch
 
 from . import _native as N
 from .transformer import _align
+
+
+def _subtract(ranges, holes):
+    """[a, b) ranges minus the hole ranges (each hole inside one range)."""
+    out = list(ranges)
+    for h0, h1 in holes:
+        nxt = []
+        for a, b in out:
+            if h1 <= a or h0 >= b:
+                nxt.append((a, b))
+                continue
+            if a < h0:
+                nxt.append((a, h0))
+            if h1 < b:
+                nxt.append((h1, b))
+        out = nxt
+    return out
 
 
 def _dist():
@@ -38,7 +56,15 @@ class GradSync:
             o, shp = idx[f"l{i}.wd"]
             self.layers.append((a, o + _align(math.prod(shp))))
         lo, hi = (self.layers[0][0], self.layers[-1][1]) if self.layers else (0, 0)
-        self.rest = [(a, b) for a, b in ((0, lo), (hi, params.numel)) if b > a]
+        rest = [(a, b) for a, b in ((0, lo), (hi, params.numel)) if b > a]
+        # the untied output head and the final norm are final right after their (first) backward
+        # step: reduced at layer_done(-1), not with the embedding at the end (MAESTRO_C2_EARLY_HEAD)
+        self.early = []
+        if "head" in idx and os.environ.get("MAESTRO_C2_EARLY_HEAD", "1") != "0":
+            for name in ("head", "lnf"):
+                o, shp = idx[name]
+                self.early.append((o, o + _align(math.prod(shp))))
+        self.rest = _subtract(rest, self.early)
         self.group = group
         self.comm = torch.cuda.Stream(device=device)
         self.reserve = reserve
@@ -52,7 +78,7 @@ class GradSync:
 
     def begin(self) -> None:
         """Before the last micro-batch's backward: every layer is pending; compute grids shrink."""
-        self.pending = set(range(len(self.layers)))
+        self.pending = set(range(len(self.layers))) | ({-1} if self.early else set())
         if self.reserve > 0:
             self._budget(self._sms - self.reserve)
             self._budget_set = True
@@ -61,7 +87,8 @@ class GradSync:
         _dist().all_reduce(self.p.grad[a:b], group=self.group)
 
     def layer_done(self, i: int) -> None:
-        """Layer hook: layer i's gradient is final on the current stream -> reduce it on comm."""
+        """Layer hook: layer i's gradient is final on the current stream -> reduce it on comm
+        (i = -1: the output head and final norm, before the layers)."""
         if i not in self.pending:
             return
         self.pending.discard(i)
@@ -69,7 +96,8 @@ class GradSync:
         ev.record(torch.cuda.current_stream())
         self.comm.wait_event(ev)
         with torch.cuda.stream(self.comm):
-            self._reduce(*self.layers[i])
+            for a, b in (self.early if i == -1 else [self.layers[i]]):
+                self._reduce(a, b)
 
     def finish(self, stream) -> None:
         """After the backward: reduce what is left and make ``stream`` wait for every bucket."""
@@ -81,7 +109,8 @@ class GradSync:
         self.comm.wait_event(ev)
         with torch.cuda.stream(self.comm):
             for i in sorted(self.pending):
-                self._reduce(*self.layers[i])
+                for a, b in (self.early if i == -1 else [self.layers[i]]):
+                    self._reduce(a, b)
             for a, b in self.rest:
                 self._reduce(a, b)
         self.pending = set()

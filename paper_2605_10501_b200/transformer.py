@@ -321,6 +321,8 @@ class Transformer:
             dyf_hook(dyf)
         dh_ = torch.empty(T, s.d, device=dev, dtype=bf)
         K.rmsnorm_bwd(dyf, hf, p["lnf"], rf, None, dh_, p.g("lnf"))
+        if layer_hook is not None:
+            layer_hook(-1)  # the output head (untied) and the final norm are final from here
         for i in reversed(range(s.layers)):
             h1, r1, y1, qkv, o, lse, h2, r2, y2, gu, sw = ctx["layers"][i]
             # MLP
