@@ -213,13 +213,19 @@ __global__ void __launch_bounds__(THREADS, MIN_BLOCKS) kd_loss_kernel(const __nv
 // HBM traffic is the algorithmic 2 x V x 2 B read + V x 2 B written per row.  fp16 storage of
 // the exponentials (all <= 1) adds a relative error <= 2^-12 per probability to ds (which is then
 // rounded to bf16, 2^-9); the loss uses the fp32 exponentials.
-constexpr int KDS_CONS = 256;              // consumer threads: one 8-column vector per chunk each
+#ifndef KDS_CONS_T
+#define KDS_CONS_T 256
+#endif
+#ifndef KDS_CTAS
+#define KDS_CTAS 3
+#endif
+constexpr int KDS_CONS = KDS_CONS_T;       // consumer threads: one 8-column vector per chunk each
 constexpr int KDS_CH = 8 * KDS_CONS;       // columns per chunk
 constexpr int KDS_NCH = 8;                 // chunks per CTA slice
 constexpr int KDS_VC_MAX = KDS_CH * KDS_NCH;  // 16384 columns = 64 KB of (t, s) per CTA
 constexpr int KDS_THREADS = KDS_CONS + 32; // + producer warp
 constexpr int KDS_SMEM = KDS_NCH * KDS_CH * 4 + 1024;
-constexpr int KDS_CTAS_PER_SM = 3;         // three row slices in flight per SM (different phases)
+constexpr int KDS_CTAS_PER_SM = KDS_CTAS;  // row slices in flight per SM (different phases)
 #ifndef KDS_SLEEP_NS
 #define KDS_SLEEP_NS 20000
 #endif
