@@ -2147,7 +2147,10 @@ MAESTRO_API int maestro_attn_fwd(const void* q, const void* k, const void* v, co
     if (e[0] == 'd') return e[3] == '4' ? 3 : 1;  // "dec" / "dec4"
     return e[0] == 'p' ? 2 : (e[0] == 'b' ? 0 : ATTN_FWD_VARIANT);
   }();
-  const int variant = env_variant >= 0 ? env_variant : (head_dim == 64 ? 1 : (causal ? 0 : 2));
+  // causal head_dim 128: ping-pong for long sequences (cfg 5 teacher, 8k: +2 %), shared tile below
+  // (cfg 3 backbone, 4k: ping-pong -5 %)
+  const bool long_seq = nseq > 0 && T / nseq >= 6144;
+  const int variant = env_variant >= 0 ? env_variant : (head_dim == 64 ? 1 : ((causal && !long_seq) ? 0 : 2));
   if (variant == 2) {  // 256-row items: the plan's third list, or built into the workspace
     int2* t2 = plan != nullptr ? reinterpret_cast<int2*>(reinterpret_cast<unsigned char*>(const_cast<void*>(plan)) +
                                                          2 * maestro_attn_workspace(T, nseq))
